@@ -1,0 +1,142 @@
+"""Write plan JSON files for the BASELINE.json configs (seeded, synthetic).
+
+Plan JSON (the input of ``tn_plan_load``, include/tn.h):
+  {"version": 1,
+   "tensors": [{"labels": [int...], "data": [re0, im0, re1, im1, ...]}, ...],  # row-major, dims 2
+   "open": [labels...],        # output legs, in output order (slowest first)
+   "tree": [[u, v], ...],      # SSA pairs; ids < n_tensors are leaves
+   "sliced": [labels...],      # bit j of a slice id fixes sliced[j] (C-A20)
+   "stem": [node ids...],      # leaf->root stem path (C-A18)
+   "circuit": {...}, "bits": [...], "open_qubits": [...], "meta": {...}}   # ignored by the library
+
+Usage:  python -m workload.make_plans [c1 c2 c3 ...]
+"""
+from __future__ import annotations
+
+import json
+import os
+import sys
+import time
+
+from . import circuit as C
+from . import network as NW
+from . import planner as PL
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+PLAN_DIR = os.path.join(os.path.dirname(HERE), "plans")
+
+# name -> (rows, cols, drop_corner, cycles, n_open, max_log2, trials)
+CONFIGS = {
+    # C1: 12-qubit depth-8, all legs open (full state), unsliced (BJ configs[0])
+    "c1": dict(rows=3, cols=4, drop=False, cycles=8, n_open=12, max_log2=None, trials=8),
+    # C2: 30-qubit 14-cycle, stem <= 2^28, 10 open legs (BJ configs[1])
+    "c2": dict(rows=5, cols=6, drop=False, cycles=14, n_open=10, max_log2=30, trials=4),
+    # C3: 53-qubit (6x9 minus a corner) 20-cycle, stem <= 2^32, 6 open legs (BJ configs[2])
+    "c3": dict(rows=6, cols=9, drop=True, cycles=20, n_open=6, max_log2=35, trials=2),
+}
+
+
+def open_qubit_choice(n, n_open):
+    """Open the last n_open qubits (a contiguous block at the grid edge)."""
+    return list(range(n - n_open, n))
+
+
+def sweep_orders(circ, net):
+    """Leaf orders that sweep the grid column by column (and row by row), time-forward inside a
+    column: the stem then carries the bonds across one cut of the 2-D grid."""
+    sites = circ["sites"]
+    info = []
+    for ls, _ in net.tensors:
+        qs = [net.label_pos[l][0] for l in ls]
+        ts = [net.label_pos[l][1] for l in ls]
+        rows = [sites[q][0] for q in qs]
+        cols = [sites[q][1] for q in qs]
+        if not ls:  # scalar factor (a qubit without two-qubit gates, fully closed)
+            rows, cols, ts = [0], [0], [0]
+        info.append((rows, cols, sum(ts) / len(ts)))
+    idx = range(len(info))
+    orders = []
+    orders.append(sorted(idx, key=lambda i: (max(info[i][1]), info[i][2], min(info[i][0]))))
+    orders.append(sorted(idx, key=lambda i: (max(info[i][1]), min(info[i][0]), info[i][2])))
+    orders.append(sorted(idx, key=lambda i: (max(info[i][0]), info[i][2], min(info[i][1]))))
+    orders.append(sorted(idx, key=lambda i: (min(info[i][1]), info[i][2], min(info[i][0]))))
+    return orders
+
+
+def build_plan(rows, cols, drop, cycles, n_open, max_log2, trials, seed=0, group=True,
+               max_branch_log2=20):
+    circ = C.make_circuit(rows, cols, cycles, seed=seed, drop_corner=drop)
+    n = circ["n_qubits"]
+    bits = C.random_bits(n, seed + 1000)
+    oq = open_qubit_choice(n, n_open)
+    net = NW.simplify(NW.build_network(circ, bits=bits, open_qubits=oq))
+    leaf_masks = []
+    for ls, _ in net.tensors:
+        m = 0
+        for l in ls:
+            m |= 1 << l
+        leaf_masks.append(m)
+    open_mask = 0
+    for l in net.open:
+        open_mask |= 1 << l
+    if max_log2 is None:
+        max_log2 = 10 ** 6
+    res = PL.plan_network(leaf_masks, open_mask, max_log2, trials=trials, seed=seed, group=group,
+                          max_branch_log2=max_branch_log2, sweeps=sweep_orders(circ, net))
+    tree, sliced, stem = res["tree"], res["sliced"], res["stem"]
+    tensors = []
+    for ls, d in net.tensors:
+        flat = d.reshape(-1)
+        data = []
+        for z in flat:
+            data.append(float(z.real))
+            data.append(float(z.imag))
+        tensors.append({"labels": list(ls), "data": data})
+    geo = PL.stem_report(tree, sliced, stem)
+    meta = {
+        "n_qubits": n, "cycles": cycles, "seed": seed,
+        "n_tensors": len(tensors), "n_sliced": PL.popcount(sliced),
+        "slice_cost_cmacs": tree.total_cost(sliced),
+        "max_log2": tree.max_log2(sliced),
+        "stem_steps_mkn_log2": geo,
+        "est_time_s": res["est_time"],
+    }
+    return {
+        "version": 1,
+        "tensors": tensors,
+        "open": list(net.open),
+        "tree": [list(p) for p in tree.pairs],
+        "sliced": PL.bits_of(sliced),
+        "stem": stem,
+        "circuit": circ,
+        "bits": bits,
+        "open_qubits": oq,
+        "meta": meta,
+    }
+
+
+def write_plan(name, plan):
+    os.makedirs(PLAN_DIR, exist_ok=True)
+    path = os.path.join(PLAN_DIR, f"{name}.json")
+    with open(path, "w") as f:
+        json.dump(plan, f, separators=(",", ":"))
+    return path
+
+
+def main(argv):
+    names = argv or list(CONFIGS)
+    for name in names:
+        cfg = CONFIGS[name]
+        t0 = time.time()
+        plan = build_plan(cfg["rows"], cfg["cols"], cfg["drop"], cfg["cycles"], cfg["n_open"],
+                          cfg["max_log2"], cfg["trials"])
+        p = write_plan(name, plan)
+        m = plan["meta"]
+        print(f"{name}: {p} tensors={m['n_tensors']} sliced={m['n_sliced']} "
+              f"max_log2={m['max_log2']} slice_cmacs={m['slice_cost_cmacs']:.3e} "
+              f"stem_steps={len(m['stem_steps_mkn_log2'])} est={m['est_time_s']} "
+              f"({time.time() - t0:.1f}s)")
+
+
+if __name__ == "__main__":
+    main(sys.argv[1:])
