@@ -1,0 +1,186 @@
+/*
+ * tn.h — C ABI of the B200-native stem-path contraction library (libtn.so).
+ *
+ * The operation (PAPER.md = arXiv 2407.00769, P:n = line n):
+ *   Contract one sliced subtask of a random-quantum-circuit tensor network along a contraction
+ *   tree whose stem path dominates the cost ("Stem Type / Split Type / Common Type";
+ *   P:228).  Slicing fixes sliced edges to the bits of a slice id.  Each stem
+ *   step is a pairwise contraction C = sum_delta A*B (Eq. 3) with the remaining indices
+ *   of Eq. 4, executed as a mode permutation of the stem tensor plus a complex GEMM;
+ *   in complex-half it runs as ONE real fp16 GEMM on tcgen05 via the Eq. 6 embedding
+ *   (A read as interleaved (re,im), B padded to [[Re,-Im],[Im,Re]]), fp32 accumulation.
+ *   The two stem buffers are the paper's static double buffers.
+ *
+ * Conventions
+ *   - Every entry point returns int status (TN_OK = 0 or a negative TN_E_* code) and never lets a
+ *     C++ exception cross the ABI.  tn_last_error() returns a thread-local message for the last
+ *     failing call on this thread.
+ *   - Pointers named d_* are DEVICE pointers; h_* are HOST pointers.  Device buffers are always
+ *     caller-owned and only lent for the duration of a call (asynchronous calls: until the stream
+ *     work completes).  The library owns tn_plan / tn_comm objects and frees them in *_free.
+ *   - `stream` is a cudaStream_t passed as void*.  Asynchronous calls enqueue work on it and do
+ *     not synchronise unless stated.
+ *   - No CPU fallback exists: without a CUDA device the compute calls return TN_E_CUDA.
+ */
+#ifndef TN_H_
+#define TN_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define TN_API __attribute__((visibility("default")))
+#else
+#define TN_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  TN_OK = 0,
+  TN_E_INVALID = -1,     /* bad argument, inconsistent plan (dims, labels, tree), slice id range */
+  TN_E_PARSE = -2,       /* malformed plan JSON */
+  TN_E_INFEASIBLE = -3,  /* plan cannot run in the given configuration (capacity, shard modes) */
+  TN_E_CAPACITY = -4,    /* caller buffers too small */
+  TN_E_CUDA = -5,        /* CUDA runtime/driver error (incl. no device) */
+  TN_E_NCCL = -6,        /* NCCL error */
+  TN_E_UNSUPPORTED = -7  /* valid request this build does not implement */
+};
+
+/* stem compute dtype */
+enum { TN_CHALF = 0,   /* complex-half: interleaved fp16 (re,im), fp32 accumulation */
+       TN_CFLOAT = 1   /* complex64: interleaved fp32, fp32 SIMT FMA (reference-precision path) */ };
+
+/* mode-swap payload codec (Eq. 1, Table 1) */
+enum { TN_COMM_FP16 = 0, TN_COMM_INT8 = 1, TN_COMM_INT4 = 2 };
+
+typedef struct tn_plan tn_plan;
+typedef struct tn_comm tn_comm;
+
+typedef struct {
+  int32_t dtype;             /* TN_CHALF | TN_CFLOAT */
+  int32_t stem_min_log2;     /* stem steps begin at the first stem node holding >= 2^this
+                                elements; everything before is common type.  <0: 20 */
+  int32_t comm_codec;        /* TN_COMM_* for sharded mode swaps (ignored at world size 1) */
+  int32_t comm_group;        /* quantisation group in reals (int8/int4), e.g. 128 */
+  uint64_t stem_capacity_bytes; /* bytes of EACH stem buffer the caller will lend; 0 = no check */
+  int32_t split_log2;        /* split-type tail: 2^split_log2 chunks; -1 = auto
+                                (smallest power of two that fits), 0 = no split */
+  int32_t reserved[7];
+} tn_config;
+
+/* Caller-owned device buffers lent to a call (P:18-22 double buffering). */
+typedef struct {
+  void* d_stem[2];           /* the two static stem buffers */
+  uint64_t stem_bytes;       /* size of EACH stem buffer */
+  void* d_ws;                /* workspace: leaves, common-type tensors, padded B_P, scale slots */
+  uint64_t ws_bytes;
+} tn_buffers;
+
+typedef struct {
+  uint64_t ws_bytes;         /* workspace bytes tn_stem_contract needs */
+  uint64_t stem_bytes;       /* bytes each stem buffer needs (max stem tensor, this dtype) */
+  uint64_t n_slices_log2;    /* |sliced| : the network has 2^this independent subtasks */
+  uint64_t n_stem_steps;     /* stem steps executed on the stem buffers */
+  uint64_t n_permutes;       /* stem steps that need a standalone permutation pass */
+  uint64_t n_common;         /* common-type (branch) contractions per slice */
+  double stem_flops;         /* 8 * sum b*M*K*N over stem steps (reading C-A21) */
+  double total_flops;        /* 8 * complex MACs of the whole slice (common + stem) */
+  double stem_bytes_alg;     /* algorithmic HBM bytes of the stem GEMMs (A read + C write) */
+  double perm_bytes;         /* bytes moved by standalone permutation passes */
+  uint64_t n_open;           /* open legs: the result has 2^n_open amplitudes */
+  uint64_t max_stem_log2;    /* log2 elements of the largest stem tensor */
+  uint64_t h2d_bytes;        /* bytes tn_plan_upload copies host->device */
+  uint64_t split_chunks;     /* chunk count of the split-type tail (1 = none) */
+} tn_plan_info;
+
+TN_API const char* tn_last_error(void);
+TN_API int tn_version(void);
+
+/* Parse + validate + lower a plan (host only; no device work, no allocation on the device).
+ * json: the plan JSON (tensors with labels/dims-2 complex128 data, open legs, SSA tree, sliced
+ * labels, optional stem; see workload/make_plans.py).  cfg may be NULL (defaults).  comm: NULL for
+ * one GPU.  Errors: TN_E_PARSE (syntax), TN_E_INVALID (label/dim/tree inconsistency, hyper-edge,
+ * sliced open leg), TN_E_INFEASIBLE (largest stem exceeds cfg->stem_capacity_bytes). */
+TN_API int tn_plan_load(const char* json, size_t len, const tn_config* cfg, tn_comm* comm, tn_plan** out);
+TN_API int tn_plan_info_get(const tn_plan* p, tn_plan_info* info);
+TN_API void tn_plan_free(tn_plan* p);
+
+/* Copy the plan's leaf tensors (complex128 from the JSON, held in pinned host memory) into the
+ * workspace as complex64, asynchronously on `stream`.  Must precede the first tn_stem_contract
+ * with a given workspace; the end-to-end harness calls it every step (its H2D traffic). */
+TN_API int tn_plan_upload(tn_plan* p, const tn_buffers* b, void* stream);
+
+/* Run slice `slice_id` (bit j fixes sliced[j], reading C-A20): common-type branch contractions,
+ * Eq. 6 padding of every stem operand, then the stem steps (permutation + GEMM per step) in the
+ * two stem buffers.  Asynchronous; result stays on the device.  TN_E_INVALID if
+ * slice_id >= 2^|sliced|; TN_E_CAPACITY if the buffers are smaller than tn_plan_info says. */
+TN_API int tn_stem_contract(tn_plan* p, const tn_buffers* b, uint64_t slice_id, void* stream);
+
+/* Split-type tail: the last stem steps run on 2^split_log2 contiguous
+ * chunks of the stem placed inside the two stem buffers.  No-op when the plan has no split tail.
+ * Asynchronous. */
+TN_API int tn_split_contract(tn_plan* p, const tn_buffers* b, void* stream);
+
+/* Read the result: h_amps receives 2 * 2^n_open doubles (interleaved re, im) of the partial
+ * amplitudes a_s over the open legs in plan order (slowest first), unscaled exactly by the
+ * accumulated power-of-two exponent (reading C-A8).  prefixes/n_sub reserved for the sparse-state
+ * batch (must be NULL/0 in this build); k/top_idx: if top_idx != NULL, receives the k most
+ * probable member indices (ties -> smaller index, C-A23).  SYNCHRONOUS (writes host memory). */
+TN_API int tn_sample_amplitudes(tn_plan* p, const tn_buffers* b, const uint64_t* prefixes, size_t n_sub,
+                         double* h_amps, int k, uint64_t* top_idx, void* stream);
+
+/* JSON report: per stem step geometry, permutation flag, flops, algorithmic bytes, and (after a
+ * run with timing enabled) per-step milliseconds.  *needed = bytes required incl. NUL. */
+TN_API int tn_report_json(const tn_plan* p, char* buf, size_t cap, size_t* needed);
+/* Enable per-step CUDA-event timing on the next tn_stem_contract (costs a sync per step). */
+TN_API int tn_set_timing(tn_plan* p, int enable);
+
+/* ---- kernel-level entry points (used by the parity tests; same kernels as the stem loop) ---- */
+
+/* Mode permutation of a rank-n tensor with all dims 2 ("dimension reordering").
+ * d_src/d_dst: 2^n elements of elem_bytes (4 = complex-half, 8 = complex64) each, must not
+ * overlap.  perm[j] = source axis of destination axis j (numpy transpose semantics; axis 0 is
+ * the slowest).  n <= 40. */
+TN_API int tn_permute(void* d_dst, const void* d_src, int elem_bytes, int n, const int* perm, void* stream);
+
+/* Complex-half stem GEMM, Eq. 6 as one real fp16 tcgen05 GEMM:
+ *   C[m, n] = 2^e * sum_k A[m, k] B[k, n]   (complex; A, C interleaved fp16 (re,im) row-major)
+ * d_bp: padded real B_P, fp16 [2N][2K] row-major (K-major): row (n,c), column (k,a) holds
+ * c=0: (Re b, -Im b)[a], c=1: (Im b, Re b)[a] (reading C-A6).  The scale 2^e is chosen on the
+ * device from *d_in_max (max |real component| of A) and *d_b_bound (max column 1-norm of B_P)
+ * so that |C| <= 2^14; e is added to *d_exp.  *d_out_max receives max |real component| of C as
+ * float bits (atomicMax; caller zeroes it).  Any of the four scale pointers may be NULL: then
+ * e = 0 and no max is recorded.  Requires K >= 8 and N >= 8 (powers of two); M any. */
+TN_API int tn_gemm_chalf(void* d_c, const void* d_a, const void* d_bp, uint64_t M, uint32_t K, uint32_t N,
+                  const float* d_in_max, const float* d_b_bound, uint32_t* d_out_max, int* d_exp,
+                  void* stream);
+
+/* Complex64 stem GEMM (fp32 SIMT): C[M,N] = A[M,K] B[K,N], all interleaved complex64 row-major. */
+TN_API int tn_gemm_cfloat(void* d_c, const void* d_a, const void* d_b, uint64_t M, uint32_t K, uint32_t N,
+                   void* stream);
+
+/* Build B_P (fp16 [2N][2K]) from complex64 B [K][N] row-major with an exact power-of-two scale
+ * 2^t chosen so max|B| maps near 2^14; t is added to *d_exp (may be NULL: t = 0);
+ * *d_b_bound receives max column 1-norm of the stored B_P (float).  Two kernels. */
+TN_API int tn_pad_b(void* d_bp, const void* d_b, uint32_t K, uint32_t N, float* d_b_bound, int* d_exp,
+             void* d_scratch /* >= 16 bytes */, void* stream);
+
+/* Eq. 1 int8 group codec on a flat fp32 array (g reals per group, exp = 1, reading C-A10..C-A13):
+ * codes int8, scales/zeros fp32 per group. n must be a multiple of g. */
+TN_API int tn_quant_int8(int8_t* d_codes, float* d_scales, float* d_zeros, const float* d_x, uint64_t n,
+                  int g, void* stream);
+TN_API int tn_dequant_int8(float* d_y, const int8_t* d_codes, const float* d_scales, const float* d_zeros,
+                    uint64_t n, int g, void* stream);
+
+/* ---- multi-GPU (stem sharded on its log2(world) outermost modes, Alg. 1) ---- */
+TN_API int tn_comm_unique_id(uint8_t out[128]);
+TN_API int tn_comm_init(const uint8_t uid[128], int rank, int world, int device, tn_comm** out);
+TN_API void tn_comm_free(tn_comm* c);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TN_H_ */

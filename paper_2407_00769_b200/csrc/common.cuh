@@ -1,0 +1,92 @@
+// Shared device helpers and kernel launch declarations of libtn.
+#pragma once
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "plan.hpp"
+
+namespace tn {
+
+#define TN_CUDA(call)                                                                       \
+  do {                                                                                      \
+    cudaError_t e_ = (call);                                                                \
+    if (e_ != cudaSuccess)                                                                  \
+      throw ::tn::TnError{TN_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)};   \
+  } while (0)
+
+constexpr int kMaxModes = 48;
+
+// Strides (in complex elements) of a strided complex64 view with every mode of dimension 2.
+struct ContractArgs {
+  const float2* a;               // A base (already offset by the slice)
+  const float2* b;               // B base
+  float2* c;                     // C (dense, row-major in out order)
+  int n_out, n_red;              // output bits, reduce bits
+  int64_t out_sa[kMaxModes];     // per output bit (bit j = output axis n_out-1-j): stride in A (0 if absent)
+  int64_t out_sb[kMaxModes];
+  int64_t red_sa[kMaxModes];     // per reduce bit
+  int64_t red_sb[kMaxModes];
+};
+
+// Gather a complex64 view into a dense [K][N] matrix (row-major), optional fp16 padding output.
+struct GatherArgs {
+  const float2* src;
+  float2* dst;                   // dense [K][N] complex64
+  int klog, nlog;
+  int64_t sk[kMaxModes];         // stride of k-bit j (bit j of k = axis klog-1-j of R)
+  int64_t sn[kMaxModes];
+};
+
+struct PermArgs {
+  int n;                         // total bits
+  int u;                         // tile bits
+  int o;                         // number of tile bits that are output-innermost (write order)
+  int64_t tile_in[16];           // input strides of tile bits (read order; first = input innermost)
+  int64_t tile_out[16];          // output strides of tile bits (read order)
+  int wr_map[16];                // write order bit j -> read-order tile bit index
+  int64_t outer_in[64];
+  int64_t outer_out[64];
+};
+
+// ---- launchers (all asynchronous on `s`) ----
+void launch_permute(void* dst, const void* src, int elem_bytes, int n, const int* perm, cudaStream_t s);
+void launch_contract_c64(const ContractArgs& a, cudaStream_t s);
+void launch_gather_kn(const GatherArgs& g, cudaStream_t s);
+void launch_max_abs_f32(const float* x, uint64_t n, uint32_t* out_bits, cudaStream_t s);
+void launch_max_abs_f16(const __half* x, uint64_t n, uint32_t* out_bits, cudaStream_t s);
+// B [K][N] c64 -> B_P fp16 [2N][2K] with scale 2^t (t from *bmax_bits), bound, exp
+void launch_pad_b(__half* bp, const float2* b, int klog, int nlog, const uint32_t* bmax_bits,
+                  float* b_bound, int* exp_slot, cudaStream_t s);
+// complex64 -> complex-half with scale from max (entry of the stem)
+void launch_c64_to_chalf(__half2* dst, const float2* src, uint64_t n, const uint32_t* max_bits,
+                         int* exp_slot, uint32_t* out_max_bits, cudaStream_t s);
+void launch_copy_c64(float2* dst, const float2* src, uint64_t n, cudaStream_t s);
+void launch_gemm_c64(float2* c, const float2* a, const float2* b, uint64_t M, uint32_t K, uint32_t N,
+                     cudaStream_t s);
+void launch_gemm_chalf_simt(__half2* c, const __half2* a, const __half* bp, uint64_t M, uint32_t K,
+                            uint32_t N, const float* in_max, const float* b_bound,
+                            uint32_t* out_max, int* exp_slot, cudaStream_t s);
+void launch_gemm_chalf_tc(__half* c, const __half* a, const __half* bp, uint64_t M, uint32_t K2,
+                          uint32_t N2, const float* in_max, const float* b_bound, uint32_t* out_max,
+                          int* exp_slot, cudaStream_t s);
+void launch_quant_int8(int8_t* codes, float* scales, float* zeros, const float* x, uint64_t n, int g,
+                       cudaStream_t s);
+void launch_dequant_int8(float* y, const int8_t* codes, const float* scales, const float* zeros,
+                         uint64_t n, int g, cudaStream_t s);
+
+// ---- device helpers ----
+// power-of-two exponent e so that prod * 2^e < 2^14 (prod > 0); 0 if prod == 0 or not finite.
+__host__ __device__ inline int scale_exp_for(float prod) {
+  if (!(prod > 0.f) || !(prod < 3.0e38f)) return 0;
+  int p;
+  frexpf(prod, &p);  // prod = f * 2^p, f in [0.5, 1)  => prod < 2^p
+  int e = 14 - p;
+  if (e > 120) e = 120;
+  if (e < -120) e = -120;
+  return e;
+}
+
+}  // namespace tn

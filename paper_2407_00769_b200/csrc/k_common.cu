@@ -1,0 +1,184 @@
+// Common-type contractions and stem-operand preparation.
+//
+// * contract_c64: one pairwise contraction of MB-scale non-stem tensors ("Common Type"),
+//   Eq. 3 with arbitrary strided operands (slicing = a base offset), complex64
+//   with fp32 accumulation.  Thread per output element; the reduce index walks a Gray code so each
+//   iteration changes one stride.
+// * gather_kn: lay a branch tensor out as the dense [K][N] operand of its stem step.
+// * pad_b: Eq. 6 padding (reading C-A6) to the fp16 K-major B_P [2N][2K] with an exact
+//   power-of-two scale (reading C-A8), and the column 1-norm bound used to scale the step output.
+// * c64_to_chalf: stem entry, complex64 -> interleaved fp16 with an exact power-of-two scale.
+#include <cstring>
+
+#include "common.cuh"
+
+namespace tn {
+
+__device__ __forceinline__ void atomic_max_pos(uint32_t* addr, float v) {
+  // v >= 0: IEEE bit patterns of non-negative floats order like unsigned integers
+  atomicMax(addr, __float_as_uint(v));
+}
+
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+__global__ void contract_c64_kernel(const ContractArgs args, uint64_t n_out_elems) {
+  const uint64_t nred = 1ull << args.n_red;
+  for (uint64_t o = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; o < n_out_elems;
+       o += (uint64_t)gridDim.x * blockDim.x) {
+    int64_t oa = 0, ob = 0;
+    for (int j = 0; j < args.n_out; ++j)
+      if (o >> j & 1) {
+        oa += args.out_sa[j];
+        ob += args.out_sb[j];
+      }
+    float2 acc = make_float2(0.f, 0.f);
+    uint64_t g = 0;
+    for (uint64_t r = 0; r < nred; ++r) {
+      if (r) {
+        int j = __ffsll((long long)r) - 1;  // Gray code: bit j flips
+        g ^= 1ull << j;
+        if (g >> j & 1) {
+          oa += args.red_sa[j];
+          ob += args.red_sb[j];
+        } else {
+          oa -= args.red_sa[j];
+          ob -= args.red_sb[j];
+        }
+      }
+      float2 x = args.a[oa], y = args.b[ob];
+      acc.x = fmaf(x.x, y.x, fmaf(-x.y, y.y, acc.x));
+      acc.y = fmaf(x.x, y.y, fmaf(x.y, y.x, acc.y));
+    }
+    args.c[o] = acc;
+  }
+}
+
+void launch_contract_c64(const ContractArgs& a, cudaStream_t s) {
+  uint64_t n = 1ull << a.n_out;
+  int threads = 256;
+  uint64_t blocks = (n + threads - 1) / threads;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  contract_c64_kernel<<<(unsigned)blocks, threads, 0, s>>>(a, n);
+  TN_CUDA(cudaGetLastError());
+}
+
+__global__ void gather_kn_kernel(const GatherArgs g) {
+  const uint64_t n = 1ull << (g.klog + g.nlog);
+  const uint64_t nmask = (1ull << g.nlog) - 1;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t k = i >> g.nlog, nn = i & nmask;
+    int64_t off = 0;
+    for (int j = 0; j < g.klog; ++j)
+      if (k >> j & 1) off += g.sk[j];
+    for (int j = 0; j < g.nlog; ++j)
+      if (nn >> j & 1) off += g.sn[j];
+    g.dst[i] = g.src[off];
+  }
+}
+
+void launch_gather_kn(const GatherArgs& g, cudaStream_t s) {
+  uint64_t n = 1ull << (g.klog + g.nlog);
+  uint64_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  gather_kn_kernel<<<(unsigned)blocks, 256, 0, s>>>(g);
+  TN_CUDA(cudaGetLastError());
+}
+
+template <typename T>
+__global__ void max_abs_kernel(const T* __restrict__ x, uint64_t n, uint32_t* out) {
+  float m = 0.f;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    m = fmaxf(m, fabsf((float)x[i]));
+  m = warp_max(m);
+  if ((threadIdx.x & 31) == 0) atomic_max_pos(out, m);
+}
+
+void launch_max_abs_f32(const float* x, uint64_t n, uint32_t* out_bits, cudaStream_t s) {
+  uint64_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  if (blocks == 0) blocks = 1;
+  max_abs_kernel<float><<<(unsigned)blocks, 256, 0, s>>>(x, n, out_bits);
+  TN_CUDA(cudaGetLastError());
+}
+
+void launch_max_abs_f16(const __half* x, uint64_t n, uint32_t* out_bits, cudaStream_t s) {
+  uint64_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  if (blocks == 0) blocks = 1;
+  max_abs_kernel<__half><<<(unsigned)blocks, 256, 0, s>>>(x, n, out_bits);
+  TN_CUDA(cudaGetLastError());
+}
+
+// One warp per column n of B: writes rows (n,0) and (n,1) of B_P [2N][2K].
+__global__ void pad_b_kernel(__half* __restrict__ bp, const float2* __restrict__ b, int klog, int nlog,
+                             const uint32_t* bmax_bits, float* b_bound, int* exp_slot) {
+  const int K = 1 << klog, N = 1 << nlog;
+  const int t = bmax_bits ? scale_exp_for(__uint_as_float(*bmax_bits)) : 0;
+  if (exp_slot && blockIdx.x == 0 && threadIdx.x == 0) *exp_slot = t;
+  const float sc = ldexpf(1.f, t);
+  const int warps = blockDim.x >> 5, lane = threadIdx.x & 31;
+  for (int n = blockIdx.x * warps + (threadIdx.x >> 5); n < N; n += gridDim.x * warps) {
+    float l1 = 0.f;
+    __half2* r0 = reinterpret_cast<__half2*>(bp + (size_t)(2 * n) * 2 * K);
+    __half2* r1 = reinterpret_cast<__half2*>(bp + (size_t)(2 * n + 1) * 2 * K);
+    for (int k = lane; k < K; k += 32) {
+      float2 v = b[(size_t)k * N + n];
+      __half re = __float2half_rn(v.x * sc), im = __float2half_rn(v.y * sc);
+      __half nim = __hneg(im);
+      r0[k] = __halves2half2(re, nim);   // c=0: (Re b, -Im b)
+      r1[k] = __halves2half2(im, re);    // c=1: (Im b,  Re b)
+      l1 += fabsf(__half2float(re)) + fabsf(__half2float(im));
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) l1 += __shfl_xor_sync(0xffffffffu, l1, o);
+    if (lane == 0 && b_bound) atomic_max_pos(reinterpret_cast<uint32_t*>(b_bound), l1);
+  }
+}
+
+void launch_pad_b(__half* bp, const float2* b, int klog, int nlog, const uint32_t* bmax_bits,
+                  float* b_bound, int* exp_slot, cudaStream_t s) {
+  int N = 1 << nlog;
+  int blocks = (N + 7) / 8;
+  if (blocks > 148 * 4) blocks = 148 * 4;
+  pad_b_kernel<<<blocks, 256, 0, s>>>(bp, b, klog, nlog, bmax_bits, b_bound, exp_slot);
+  TN_CUDA(cudaGetLastError());
+}
+
+__global__ void c64_to_chalf_kernel(__half2* __restrict__ dst, const float2* __restrict__ src, uint64_t n,
+                                    const uint32_t* max_bits, int* exp_slot, uint32_t* out_max) {
+  const int e = max_bits ? scale_exp_for(__uint_as_float(*max_bits)) : 0;
+  if (exp_slot && blockIdx.x == 0 && threadIdx.x == 0) *exp_slot = e;
+  const float sc = ldexpf(1.f, e);
+  float m = 0.f;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    float2 v = src[i];
+    __half2 h = __floats2half2_rn(v.x * sc, v.y * sc);
+    dst[i] = h;
+    float2 hf = __half22float2(h);
+    m = fmaxf(m, fmaxf(fabsf(hf.x), fabsf(hf.y)));
+  }
+  m = warp_max(m);
+  if (out_max && (threadIdx.x & 31) == 0) atomic_max_pos(out_max, m);
+}
+
+void launch_c64_to_chalf(__half2* dst, const float2* src, uint64_t n, const uint32_t* max_bits, int* exp_slot,
+                         uint32_t* out_max_bits, cudaStream_t s) {
+  uint64_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  if (blocks == 0) blocks = 1;
+  c64_to_chalf_kernel<<<(unsigned)blocks, 256, 0, s>>>(dst, src, n, max_bits, exp_slot, out_max_bits);
+  TN_CUDA(cudaGetLastError());
+}
+
+void launch_copy_c64(float2* dst, const float2* src, uint64_t n, cudaStream_t s) {
+  TN_CUDA(cudaMemcpyAsync(dst, src, n * sizeof(float2), cudaMemcpyDeviceToDevice, s));
+}
+
+}  // namespace tn

@@ -1,0 +1,388 @@
+// Complex-half stem GEMM on the 5th-generation tensor cores.
+//
+// Eq. 6: C[m,(n,c)] = sum_{(k,a)} A_real[m,(k,a)] * B_P[(k,a),(n,c)], i.e. the
+// complex contraction of the stem A (interleaved fp16 re/im, read AS STORED — P:502 "include an
+// extra mode for tensor B, as it is smaller than tensor A") with the padded B_P
+// [[Re b,-Im b],[Im b, Re b]] is ONE real fp16 GEMM [M,2K] x [2K,2N] -> [M,2N] whose output is
+// again interleaved complex.  fp32 accumulation in TMEM (reading C-A7), one round-to-nearest to
+// fp16 in the epilogue with an exact power-of-two scale (reading C-A8).
+//
+// sm_100a design: persistent warp-specialised kernel, one CTA per SM (grid = min(tiles, #SMs)).
+//   warp 0   : TMA producer — A tile [128 x 64] and B tile [BN x 64] per stage, 128B swizzle,
+//              mbarrier full/empty ring of STAGES
+//   warp 1   : MMA issuer — one elected thread issues tcgen05.mma.cta_group::1.kind::f16
+//              (M=128, N=BN, K=16), accumulators in TMEM (2 x 256 columns, double buffered),
+//              tcgen05.commit -> mbarriers
+//   warp 2   : TMEM allocator
+//   warps 4-7: epilogue — tcgen05.ld 32x32b -> scale -> fp16 -> 128B-swizzled smem -> TMA store;
+//              running max |C| for the next step's scale
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <mutex>
+
+#include "common.cuh"
+
+namespace tn {
+
+namespace tc {
+
+constexpr int BM = 128;
+constexpr int BK = 64;  // fp16 elements per 128-byte swizzle row
+constexpr int kThreads = 256;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1), "r"(smem_u32(src))
+               : "memory");
+}
+
+__device__ __forceinline__ uint64_t smem_desc_sw128(const void* p) {
+  // SM100 UMMA shared-memory matrix descriptor, K-major, 128-byte swizzle:
+  // start>>4 [0,14) | LBO>>4 [16,30) (unused for swizzled K-major) | SBO>>4 [32,46) = 1024 B between
+  // 8-row groups | version 1 [46,48) | base offset 0 | layout SWIZZLE_128B = 2 at [61,64)
+  uint64_t addr = smem_u32(p);
+  uint64_t d = 0;
+  d |= (addr & 0x3FFFFull) >> 4;
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
+__device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                        uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld_32x32b_x32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+
+__device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void named_bar(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+template <int BN>
+struct Cfg {
+  static constexpr int kABytes = BM * BK * 2;             // 16 KB
+  static constexpr int kBBytes = BN * BK * 2;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kCSub = (BN + 63) / 64;            // 64-column store subtiles
+  static constexpr int kCBytes = kCSub * BM * 128;
+  static constexpr int kStagesRaw = (200 * 1024 - kCBytes) / kStageBytes;
+  static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
+  static constexpr int kSmem = kStages * kStageBytes + kCBytes + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr uint32_t kIdesc = (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+};
+
+template <int BN>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_chalf_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                         const __grid_constant__ CUtensorMap tmC, uint32_t num_m, uint32_t num_n, int K2,
+                         const float* in_max, const float* b_bound, uint32_t* out_max, int* exp_slot) {
+  using C = Cfg<BN>;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  unsigned char* sA = smem;
+  unsigned char* sB = smem + C::kStages * C::kABytes;
+  unsigned char* sC = sB + C::kStages * C::kBBytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sC + C::kCBytes);
+  uint64_t* empty = full + C::kStages;
+  uint64_t* tfull = empty + C::kStages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t num_tiles = num_m * num_n;
+  const int num_k = (K2 + BK - 1) / BK;
+  const int last_kk = ((K2 - (num_k - 1) * BK) + 15) / 16;  // MMAs in the last k block
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < C::kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmC)) : "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ===== TMA producer =====
+      int s = 0;
+      uint32_t ph = 0;
+      for (uint32_t t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        const int m0 = (int)((t / num_n) * BM);
+        const int n0 = (int)((t % num_n) * BN);
+        for (int kb = 0; kb < num_k; ++kb) {
+          mbar_wait(&empty[s], ph ^ 1);
+          mbar_expect_tx(&full[s], C::kStageBytes);
+          tma_load_2d(sA + s * C::kABytes, &tmA, &full[s], kb * BK, m0);
+          tma_load_2d(sB + s * C::kBBytes, &tmB, &full[s], kb * BK, n0);
+          if (++s == C::kStages) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ===== MMA issuer =====
+      int s = 0;
+      uint32_t ph = 0;
+      uint32_t i = 0;
+      for (uint32_t t = blockIdx.x; t < num_tiles; t += gridDim.x, ++i) {
+        const uint32_t acc = i & 1, aph = (i >> 1) & 1;
+        mbar_wait(&tempty[acc], aph ^ 1);
+        tc_fence_after();
+        const uint32_t tmem_d = tmem_base + acc * 256;
+        for (int kb = 0; kb < num_k; ++kb) {
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          const int nkk = (kb == num_k - 1) ? last_kk : BK / 16;
+          const uint64_t ad = smem_desc_sw128(sA + s * C::kABytes);
+          const uint64_t bd = smem_desc_sw128(sB + s * C::kBBytes);
+          for (int kk = 0; kk < nkk; ++kk) {
+            // advance 16 fp16 = 32 bytes along K inside the 128B swizzle atom (>>4 => +2)
+            mma_f16(tmem_d, ad + 2 * kk, bd + 2 * kk, C::kIdesc, (kb | kk) != 0);
+          }
+          mma_commit(&empty[s]);
+          if (++s == C::kStages) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+        mma_commit(&tfull[acc]);
+      }
+    }
+  } else if (warp >= 4) {
+    // ===== epilogue =====
+    const int ew = warp & 3;  // TMEM lane quarter this warp may access
+    const int row = ew * 32 + lane;
+    const int etid = threadIdx.x - 128;
+    int e = 0;
+    if (in_max && b_bound) e = scale_exp_for(in_max[0] * b_bound[0]);
+    if (exp_slot && blockIdx.x == 0 && etid == 0) *exp_slot = e;
+    const float sc = ldexpf(1.f, e);
+    float mx = 0.f;
+    uint32_t i = 0;
+    for (uint32_t t = blockIdx.x; t < num_tiles; t += gridDim.x, ++i) {
+      const uint32_t acc = i & 1, aph = (i >> 1) & 1;
+      const int m0 = (int)((t / num_n) * BM);
+      const int n0 = (int)((t % num_n) * BN);
+      mbar_wait(&tfull[acc], aph);
+      tc_fence_after();
+      // staging buffer free? (previous tile's TMA stores have read it)
+      if (etid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      named_bar(1, 128);
+      const uint32_t taddr = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * 256;
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(taddr + c, r);
+        tmem_ld_wait();
+        uint32_t pk[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          float x0 = __uint_as_float(r[2 * j]) * sc, x1 = __uint_as_float(r[2 * j + 1]) * sc;
+          __half2 h = __floats2half2_rn(x0, x1);
+          float2 hf = __half22float2(h);
+          if (BN >= 32 || 2 * j < BN - c) mx = fmaxf(mx, fmaxf(fabsf(hf.x), fabsf(hf.y)));
+          pk[j] = *reinterpret_cast<uint32_t*>(&h);
+        }
+        if (c < BN) {
+          unsigned char* sub = sC + (c >> 6) * (BM * 128) + row * 128;
+          const int cb = (c & 63) >> 3;  // first 16-byte chunk of these 32 columns
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            if ((c & 63) + q * 8 < BN || BN >= 64) {
+              const int chunk = (cb + q) ^ (row & 7);
+              uint4 v = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+              *reinterpret_cast<uint4*>(sub + chunk * 16) = v;
+            }
+          }
+        }
+      }
+      // accumulator drained -> MMA may reuse it
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      named_bar(1, 128);
+      if (etid == 0) {
+#pragma unroll 1
+        for (int j = 0; j < C::kCSub; ++j) tma_store_2d(&tmC, sC + j * (BM * 128), n0 + j * 64, m0);
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+    }
+    if (etid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (out_max && lane == 0) atomicMax(out_max, __float_as_uint(mx));
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
+  }
+}
+
+}  // namespace tc
+
+// ---- host side ----
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  if (!fn) throw TnError{TN_E_CUDA, "cuTensorMapEncodeTiled unavailable"};
+  return fn;
+}
+
+static CUtensorMap make_map_2d(const void* base, uint64_t inner, uint64_t outer, uint32_t box_inner,
+                               uint32_t box_outer) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {inner * 2};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = get_encode()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw TnError{TN_E_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")"};
+  return m;
+}
+
+static int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    TN_CUDA(cudaGetDevice(&dev));
+    TN_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+  }
+  return n;
+}
+
+template <int BN>
+static void launch_bn(__half* c, const __half* a, const __half* bp, uint64_t M, uint32_t K2, uint32_t N2,
+                      const float* in_max, const float* b_bound, uint32_t* out_max, int* exp_slot, cudaStream_t s) {
+  using C = tc::Cfg<BN>;
+  static bool attr = false;
+  if (!attr) {
+    TN_CUDA(cudaFuncSetAttribute(tc::gemm_chalf_tc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
+    attr = true;
+  }
+  CUtensorMap mb = make_map_2d(bp, K2, N2, tc::BK, BN);
+  // TMA coordinates are int32: process M in chunks of at most 2^30 rows
+  const uint32_t num_n = N2 / BN;
+  const uint64_t chunk = std::min<uint64_t>(1ull << 30, ((1ull << 31) / num_n) * tc::BM);
+  for (uint64_t m_off = 0; m_off < M; m_off += chunk) {
+    uint64_t mm = std::min<uint64_t>(chunk, M - m_off);
+    CUtensorMap ma = make_map_2d(a + m_off * K2, K2, mm, tc::BK, tc::BM);
+    CUtensorMap mc = make_map_2d(c + m_off * N2, N2, mm, 64, tc::BM);
+    uint32_t num_m = (uint32_t)((mm + tc::BM - 1) / tc::BM);
+    uint64_t tiles = (uint64_t)num_m * num_n;
+    int grid = (int)std::min<uint64_t>(tiles, (uint64_t)num_sms());
+    // the exponent is recorded once (first chunk); later chunks reuse the same inputs
+    tc::gemm_chalf_tc_kernel<BN><<<grid, tc::kThreads, C::kSmem, s>>>(ma, mb, mc, num_m, num_n, (int)K2, in_max,
+                                                                      b_bound, out_max, m_off ? nullptr : exp_slot);
+    TN_CUDA(cudaGetLastError());
+  }
+}
+
+void launch_gemm_chalf_tc(__half* c, const __half* a, const __half* bp, uint64_t M, uint32_t K2, uint32_t N2,
+                          const float* in_max, const float* b_bound, uint32_t* out_max, int* exp_slot,
+                          cudaStream_t s) {
+  if (K2 < 16 || N2 < 16 || (K2 & (K2 - 1)) || (N2 & (N2 - 1)))
+    throw TnError{TN_E_INVALID, "tcgen05 GEMM needs power-of-two 2K, 2N >= 16"};
+  if (M == 0) return;
+  switch (N2) {
+    case 16: launch_bn<16>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, s); break;
+    case 32: launch_bn<32>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, s); break;
+    case 64: launch_bn<64>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, s); break;
+    case 128: launch_bn<128>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, s); break;
+    default: launch_bn<256>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, s); break;
+  }
+}
+
+}  // namespace tn

@@ -1,0 +1,85 @@
+// Eq. 1 group quantisation for mode-swap payloads, int8, exp = 1,
+// readings C-A10..C-A13: per group of g reals, scale = 255/(max-min),
+// zero = (q_min*max - q_max*min)/(max-min), code = rint(x*scale + zero) evaluated as an fp32
+// multiply then an fp32 add (no FMA) so codes are bit-identical to the oracle (oracle/codec.py);
+// constant groups: scale = 0, zero = the constant (C-A11).  One warp per group.
+#include "common.cuh"
+
+namespace tn {
+
+__global__ void quant_int8_kernel(int8_t* __restrict__ codes, float* __restrict__ scales, float* __restrict__ zeros,
+                                  const float* __restrict__ x, uint64_t n_groups, int g) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  for (uint64_t gi = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); gi < n_groups; gi += warps) {
+    const float* xs = x + gi * g;
+    float mx = -INFINITY, mn = INFINITY;
+    for (int i = lane; i < g; i += 32) {
+      float v = xs[i];
+      mx = fmaxf(mx, v);
+      mn = fminf(mn, v);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    }
+    float scale, zero;
+    if (mx == mn) {
+      scale = 0.f;
+      zero = mx;
+    } else {
+      float den = __fsub_rn(mx, mn);
+      scale = __fdiv_rn(255.f, den);
+      zero = __fdiv_rn(__fsub_rn(__fmul_rn(-128.f, mx), __fmul_rn(127.f, mn)), den);
+    }
+    if (lane == 0) {
+      scales[gi] = scale;
+      zeros[gi] = zero;
+    }
+    int8_t* cs = codes + gi * g;
+    for (int i = lane; i < g; i += 32) {
+      float c;
+      if (scale == 0.f) {
+        c = -128.f;
+      } else {
+        c = rintf(__fadd_rn(__fmul_rn(xs[i], scale), zero));
+        c = fminf(fmaxf(c, -128.f), 127.f);
+      }
+      cs[i] = (int8_t)(int)c;
+    }
+  }
+}
+
+__global__ void dequant_int8_kernel(float* __restrict__ y, const int8_t* __restrict__ codes,
+                                    const float* __restrict__ scales, const float* __restrict__ zeros, uint64_t n,
+                                    int g) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t gi = i / g;
+    float s = scales[gi], z = zeros[gi];
+    y[i] = (s == 0.f) ? z : __fdiv_rn(__fsub_rn((float)codes[i], z), s);
+  }
+}
+
+void launch_quant_int8(int8_t* codes, float* scales, float* zeros, const float* x, uint64_t n, int g,
+                       cudaStream_t s) {
+  if (g <= 0 || n % g) throw TnError{TN_E_INVALID, "quant: n must be a multiple of the group size"};
+  uint64_t groups = n / g;
+  uint64_t blocks = (groups + 7) / 8;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (blocks == 0) return;
+  quant_int8_kernel<<<(unsigned)blocks, 256, 0, s>>>(codes, scales, zeros, x, groups, g);
+  TN_CUDA(cudaGetLastError());
+}
+
+void launch_dequant_int8(float* y, const int8_t* codes, const float* scales, const float* zeros, uint64_t n, int g,
+                         cudaStream_t s) {
+  if (g <= 0 || n % g) throw TnError{TN_E_INVALID, "dequant: n must be a multiple of the group size"};
+  uint64_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (blocks == 0) return;
+  dequant_int8_kernel<<<(unsigned)blocks, 256, 0, s>>>(y, codes, scales, zeros, n, g);
+  TN_CUDA(cudaGetLastError());
+}
+
+}  // namespace tn

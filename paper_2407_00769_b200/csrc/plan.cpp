@@ -1,0 +1,373 @@
+// Plan parsing, validation and lowering (host only).  SURVEY §8(a) a.1, §8(b).
+//
+// Lowering decides, per stem step i (Alg. 1 "performer computation of currEin"):
+//   R_i = contracted labels (stem ∩ branch, Eq. 3 delta = alpha ∩ beta),
+//   kept = stem \ R_i, new = branch \ R_i (Eq. 4),
+//   whether a standalone permutation is needed (R_i not already the innermost block),
+//   the GEMM geometry M = 2^|kept|, K = 2^|R_i|, N = 2^|new|, and the output layout kept ++ new.
+// Layout policy (B200 design): labels are ordered by next use, furthest first
+// (outermost), so the labels the next steps contract tend to be innermost and no pass is needed.
+#include "plan.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <limits>
+#include <map>
+#include <set>
+#include <sstream>
+#include <unordered_map>
+
+#include "json.hpp"
+
+namespace tn {
+
+static TnError err(int code, const std::string& m) { return TnError{code, m}; }
+
+static int as_int(const tnjson::Value& v, const char* what) {
+  if (!v.is_num()) throw err(TN_E_PARSE, std::string(what) + ": expected a number");
+  double d = v.num;
+  if (d != std::floor(d) || d < 0 || d > 2e9) throw err(TN_E_INVALID, std::string(what) + ": bad integer");
+  return (int)d;
+}
+
+static std::vector<int> int_list(const tnjson::Value* v, const char* what) {
+  std::vector<int> out;
+  if (!v) return out;
+  if (!v->is_arr()) throw err(TN_E_PARSE, std::string(what) + ": expected a list");
+  for (auto& x : v->arr) out.push_back(as_int(x, what));
+  return out;
+}
+
+Plan* load_plan(const char* json, size_t len, const tn_config* cfg_in) {
+  tnjson::Value root;
+  try {
+    root = tnjson::parse(json, len);
+  } catch (const tnjson::ParseError& e) {
+    throw err(TN_E_PARSE, e.what());
+  }
+  if (!root.is_obj()) throw err(TN_E_PARSE, "plan: expected an object");
+  std::unique_ptr<Plan> P(new Plan());
+  Plan& p = *P;
+  tn_config cfg{};
+  cfg.dtype = TN_CHALF;
+  cfg.stem_min_log2 = 20;
+  cfg.comm_codec = TN_COMM_INT8;
+  cfg.comm_group = 128;
+  cfg.split_log2 = 0;
+  if (cfg_in) cfg = *cfg_in;
+  if (cfg.stem_min_log2 < 0) cfg.stem_min_log2 = 20;
+  if (cfg.dtype != TN_CHALF && cfg.dtype != TN_CFLOAT) throw err(TN_E_INVALID, "cfg.dtype");
+  if (cfg.comm_group <= 0) cfg.comm_group = 128;
+  p.cfg = cfg;
+
+  // ---- tensors
+  const tnjson::Value* ts = root.get("tensors");
+  if (!ts || !ts->is_arr() || ts->arr.empty()) throw err(TN_E_PARSE, "plan: 'tensors' missing");
+  for (auto& t : ts->arr) {
+    Leaf lf;
+    lf.labels = int_list(t.get("labels"), "tensors.labels");
+    const tnjson::Value* d = t.get("data");
+    if (!d || !d->is_arr()) throw err(TN_E_PARSE, "tensors.data missing");
+    if (lf.labels.size() > 40) throw err(TN_E_UNSUPPORTED, "leaf rank > 40");
+    size_t want = (size_t)2 << lf.labels.size();
+    if (d->arr.size() != want)
+      throw err(TN_E_INVALID, "tensors.data length != 2*2^rank (all dims must be 2)");
+    lf.data.reserve(want);
+    for (auto& x : d->arr) {
+      if (!x.is_num()) throw err(TN_E_PARSE, "tensors.data: number expected");
+      lf.data.push_back(x.num);
+    }
+    std::set<int> u(lf.labels.begin(), lf.labels.end());
+    if (u.size() != lf.labels.size()) throw err(TN_E_INVALID, "duplicate label within a tensor");
+    p.leaves.push_back(std::move(lf));
+  }
+  p.open = int_list(root.get("open"), "open");
+  p.sliced = int_list(root.get("sliced"), "sliced");
+  if (p.sliced.size() > 62) throw err(TN_E_UNSUPPORTED, "more than 62 sliced labels");
+  const tnjson::Value* tr = root.get("tree");
+  std::vector<std::pair<int, int>> pairs;
+  if (tr) {
+    if (!tr->is_arr()) throw err(TN_E_PARSE, "tree: expected a list");
+    for (auto& pr : tr->arr) {
+      if (!pr.is_arr() || pr.arr.size() != 2) throw err(TN_E_PARSE, "tree: pairs expected");
+      pairs.emplace_back(as_int(pr.arr[0], "tree"), as_int(pr.arr[1], "tree"));
+    }
+  }
+  std::vector<int> stem_in = int_list(root.get("stem"), "stem");
+
+  // ---- label validation: no hyper-edges; open legs appear once; closed labels twice
+  std::map<int, int> count;
+  for (auto& lf : p.leaves)
+    for (int l : lf.labels) count[l]++;
+  std::set<int> open_set(p.open.begin(), p.open.end());
+  if (open_set.size() != p.open.size()) throw err(TN_E_INVALID, "duplicate open label");
+  for (auto& kv : count) {
+    bool is_open = open_set.count(kv.first) > 0;
+    if (kv.second > 2) throw err(TN_E_INVALID, "label " + std::to_string(kv.first) + " is a hyper-edge");
+    if (is_open && kv.second != 1) throw err(TN_E_INVALID, "open label must appear once");
+    if (!is_open && kv.second != 2) throw err(TN_E_INVALID, "closed label " + std::to_string(kv.first) + " must appear twice");
+  }
+  for (int l : p.open)
+    if (!count.count(l)) throw err(TN_E_INVALID, "open label not in any tensor");
+  std::set<int> sl_set;
+  for (int l : p.sliced) {
+    if (!count.count(l) || open_set.count(l)) throw err(TN_E_INVALID, "sliced label must be a closed edge");
+    if (!sl_set.insert(l).second) throw err(TN_E_INVALID, "duplicate sliced label");
+  }
+
+  // ---- nodes
+  const int nl = (int)p.leaves.size();
+  if ((int)pairs.size() != nl - 1) throw err(TN_E_INVALID, "tree must have n_tensors-1 pairs");
+  p.nodes.resize(nl + pairs.size());
+  for (int i = 0; i < nl; ++i) {
+    Node& n = p.nodes[i];
+    n.kind = NODE_LEAF;
+    for (int l : p.leaves[i].labels)
+      if (!sl_set.count(l)) n.labels.push_back(l);
+  }
+  std::vector<char> used(p.nodes.size(), 0);
+  for (size_t k = 0; k < pairs.size(); ++k) {
+    int id = nl + (int)k;
+    int u = pairs[k].first, v = pairs[k].second;
+    if (u >= id || v >= id || u == v) throw err(TN_E_INVALID, "tree: not in SSA order");
+    if (used[u] || used[v]) throw err(TN_E_INVALID, "tree: node used twice");
+    used[u] = used[v] = 1;
+    Node& n = p.nodes[id];
+    n.u = u;
+    n.v = v;
+    n.kind = NODE_COMMON;
+    const auto& lu = p.nodes[u].labels;
+    const auto& lv = p.nodes[v].labels;
+    std::set<int> su(lu.begin(), lu.end()), sv(lv.begin(), lv.end());
+    for (int l : lu)
+      if (!sv.count(l)) n.labels.push_back(l);
+    for (int l : lv)
+      if (!su.count(l)) n.labels.push_back(l);
+    std::set<int> un(su);
+    un.insert(sv.begin(), sv.end());
+    if (un.size() > 62) throw err(TN_E_INFEASIBLE, "contraction with more than 62 modes");
+    n.cost = std::ldexp(1.0, (int)un.size());
+    n.sub_cost = p.nodes[u].sub_cost + p.nodes[v].sub_cost + n.cost;
+  }
+  p.root = (int)p.nodes.size() - 1;
+  {
+    std::set<int> rl(p.nodes[p.root].labels.begin(), p.nodes[p.root].labels.end());
+    if (rl != open_set) throw err(TN_E_INVALID, "root labels != open legs");
+  }
+
+  // ---- stem (C-A18)
+  if (!stem_in.empty()) {
+    for (int id : stem_in)
+      if (id < 0 || id >= (int)p.nodes.size()) throw err(TN_E_INVALID, "stem: bad node id");
+    if (stem_in.back() != p.root) throw err(TN_E_INVALID, "stem must end at the root");
+    for (size_t i = 1; i < stem_in.size(); ++i) {
+      const Node& n = p.nodes[stem_in[i]];
+      if (n.u != stem_in[i - 1] && n.v != stem_in[i - 1]) throw err(TN_E_INVALID, "stem: not a path");
+    }
+    p.stem = stem_in;
+  } else {
+    int k = p.root;
+    std::vector<int> path{k};
+    while (p.nodes[k].u >= 0) {
+      const Node& n = p.nodes[k];
+      k = (p.nodes[n.u].sub_cost >= p.nodes[n.v].sub_cost) ? n.u : n.v;
+      path.push_back(k);
+    }
+    std::reverse(path.begin(), path.end());
+    p.stem = path;
+  }
+
+  // ---- stem entry: first stem node with >= 2^stem_min_log2 elements
+  p.stem_entry = -1;
+  int entry_idx = -1;
+  for (size_t i = 0; i < p.stem.size(); ++i) {
+    // the entry is an internal node: its complex64 result lives in the workspace and is converted
+    // into stem buffer 0 (a leaf would need a strided gather of a sliced view first)
+    if (p.nodes[p.stem[i]].u >= 0 && (int)p.nodes[p.stem[i]].labels.size() >= cfg.stem_min_log2) {
+      entry_idx = (int)i;
+      break;
+    }
+  }
+  if (entry_idx >= 0 && entry_idx == (int)p.stem.size() - 1 && p.nodes[p.stem[entry_idx]].u >= 0) {
+    // the entry is the root itself: still a valid (zero-step) stem; keep it common instead
+    entry_idx = -1;
+  }
+  if (entry_idx >= 0) {
+    p.stem_entry = p.stem[entry_idx];
+    for (size_t i = entry_idx + 1; i < p.stem.size(); ++i) p.nodes[p.stem[i]].kind = NODE_STEM;
+  }
+  for (int id = nl; id < (int)p.nodes.size(); ++id)
+    if (p.nodes[id].kind == NODE_COMMON) p.common_order.push_back(id);
+
+  // ---- next use of each label along the stem
+  const int INF = std::numeric_limits<int>::max();
+  std::unordered_map<int, int> next_use;
+  std::vector<int> step_nodes;
+  if (entry_idx >= 0)
+    for (size_t i = entry_idx + 1; i < p.stem.size(); ++i) step_nodes.push_back(p.stem[i]);
+  {
+    // a label is contracted at the step whose branch shares it with the stem
+    std::vector<int> prev_layout = p.nodes[p.stem_entry >= 0 ? p.stem_entry : p.root].labels;
+    int prev = p.stem_entry;
+    for (size_t s = 0; s < step_nodes.size(); ++s) {
+      const Node& n = p.nodes[step_nodes[s]];
+      int br = (n.u == prev) ? n.v : n.u;
+      for (int l : p.nodes[br].labels) next_use[l] = (int)s;  // branch-side first appearance
+      prev = step_nodes[s];
+    }
+  }
+  for (int l : p.open) next_use.erase(l);  // open legs are never contracted
+  auto nu = [&](int l) {
+    auto it = next_use.find(l);
+    return it == next_use.end() ? INF : it->second;
+  };
+
+  // ---- steps
+  const int eb = (cfg.dtype == TN_CHALF) ? 4 : 8;
+  uint64_t smax = 0;
+  if (entry_idx >= 0) {
+    std::vector<int> L = p.nodes[p.stem_entry].labels;
+    smax = 1ull << L.size();
+    int prev = p.stem_entry;
+    for (size_t s = 0; s < step_nodes.size(); ++s) {
+      StemStep st;
+      st.node = step_nodes[s];
+      const Node& n = p.nodes[st.node];
+      st.branch = (n.u == prev) ? n.v : n.u;
+      st.in_layout = L;
+      const auto& B = p.nodes[st.branch].labels;
+      std::set<int> bs(B.begin(), B.end());
+      std::vector<int> R, kept;
+      for (int l : L) (bs.count(l) ? R : kept).push_back(l);
+      // is R the innermost block of L?
+      bool suffix = true;
+      for (size_t j = 0; j < R.size(); ++j)
+        if (!bs.count(L[L.size() - R.size() + j])) suffix = false;
+      if (!suffix) {
+        std::stable_sort(kept.begin(), kept.end(), [&](int a, int b) { return nu(a) > nu(b); });
+        std::vector<int> PL = kept;
+        PL.insert(PL.end(), R.begin(), R.end());
+        st.perm = true;
+        for (int l : PL) st.perm_axes.push_back((int)(std::find(L.begin(), L.end(), l) - L.begin()));
+      } else {
+        R.assign(L.end() - R.size(), L.end());
+        kept.assign(L.begin(), L.end() - R.size());
+      }
+      std::vector<int> newl;
+      for (int l : B)
+        if (std::find(R.begin(), R.end(), l) == R.end()) newl.push_back(l);
+      std::stable_sort(newl.begin(), newl.end(), [&](int a, int b) { return nu(a) > nu(b); });
+      st.R = R;
+      st.kept = kept;
+      st.newl = newl;
+      st.mlog = (int)kept.size();
+      st.klog = (int)R.size();
+      st.nlog = (int)newl.size();
+      st.out_layout = kept;
+      st.out_layout.insert(st.out_layout.end(), newl.begin(), newl.end());
+      st.tensor_core = (cfg.dtype == TN_CHALF) && st.klog >= 3 && st.nlog >= 3;
+      {
+        std::set<int> chk(st.out_layout.begin(), st.out_layout.end());
+        std::set<int> want(n.labels.begin(), n.labels.end());
+        if (chk != want) throw err(TN_E_INVALID, "internal: step output labels mismatch");
+      }
+      if (st.klog > 16 || st.nlog > 16) throw err(TN_E_UNSUPPORTED, "stem operand with K or N > 2^16");
+      smax = std::max<uint64_t>(smax, 1ull << (st.mlog + st.klog));
+      smax = std::max<uint64_t>(smax, 1ull << (st.mlog + st.nlog));
+      double M = std::ldexp(1.0, st.mlog), K = std::ldexp(1.0, st.klog), N = std::ldexp(1.0, st.nlog);
+      p.stem_flops += 8.0 * M * K * N;
+      p.stem_bytes_alg += eb * (M * K + M * N) + (cfg.dtype == TN_CHALF ? 8.0 * K * N : 8.0 * K * N);
+      if (st.perm) {
+        p.perm_bytes += 2.0 * eb * M * K;
+        p.n_permutes++;
+      }
+      L = st.out_layout;
+      prev = st.node;
+      p.steps.push_back(std::move(st));
+    }
+    p.final_layout = L;
+    if (L != p.open) {
+      p.final_perm = true;
+      for (int l : p.open) p.final_perm_axes.push_back((int)(std::find(L.begin(), L.end(), l) - L.begin()));
+      p.perm_bytes += 2.0 * eb * std::ldexp(1.0, (int)L.size());
+    }
+  }
+  p.stem_elems_max = smax;
+  p.max_stem_log2 = 0;
+  while ((1ull << p.max_stem_log2) < smax) p.max_stem_log2++;
+  if (cfg.stem_capacity_bytes && smax * eb > cfg.stem_capacity_bytes)
+    throw err(TN_E_INFEASIBLE, "largest stem tensor exceeds stem_capacity_bytes");
+
+  // ---- flops
+  p.total_flops = p.stem_flops;
+  for (int id : p.common_order) p.total_flops += 8.0 * p.nodes[id].cost;
+
+  // ---- workspace layout
+  uint64_t off = 0;
+  for (auto& lf : p.leaves) {
+    lf.ws_off = off;
+    off += align_up(8ull << lf.labels.size(), 256);
+  }
+  p.ws_leaves = off;
+  p.h2d_bytes = off;
+  for (int id : p.common_order) {
+    p.nodes[id].ws_off = off;
+    off += align_up(8ull << p.nodes[id].labels.size(), 256);
+  }
+  p.ws_common = off;
+  for (auto& st : p.steps) {
+    uint64_t kn = 1ull << (st.klog + st.nlog);
+    st.b_tmp_off = off;
+    off += align_up(8 * kn, 1024);
+    if (cfg.dtype == TN_CHALF) {
+      st.b_off = off;
+      off += align_up(8 * kn, 1024);  // fp16 [2N][2K]
+    } else {
+      st.b_off = st.b_tmp_off;
+    }
+  }
+  p.ws_b = off;
+  p.ws_scratch = off;
+  size_t S = p.steps.size();
+  p.n_exp_slots = (int)(2 * S + 4);
+  off += align_up(4 * (S + 2) + 4 * (S + 2) + 4 * p.n_exp_slots + 64, 256);
+  p.ws_total = off;
+  return P.release();
+}
+
+static void jlist(std::ostringstream& o, const std::vector<int>& v) {
+  o << "[";
+  for (size_t i = 0; i < v.size(); ++i) o << (i ? "," : "") << v[i];
+  o << "]";
+}
+
+std::string report_json(const Plan& p) {
+  std::ostringstream o;
+  o.precision(17);
+  o << "{\"dtype\":\"" << (p.cfg.dtype == TN_CHALF ? "chalf" : "cfloat") << "\"";
+  o << ",\"stem_entry\":" << p.stem_entry << ",\"n_common\":" << p.common_order.size();
+  o << ",\"stem_flops\":" << p.stem_flops << ",\"total_flops\":" << p.total_flops;
+  o << ",\"stem_bytes_alg\":" << p.stem_bytes_alg << ",\"perm_bytes\":" << p.perm_bytes;
+  o << ",\"max_stem_log2\":" << p.max_stem_log2 << ",\"final_perm\":" << (p.final_perm ? 1 : 0);
+  o << ",\"steps\":[";
+  for (size_t i = 0; i < p.steps.size(); ++i) {
+    const StemStep& s = p.steps[i];
+    o << (i ? "," : "") << "{\"node\":" << s.node << ",\"branch\":" << s.branch << ",\"m\":" << s.mlog
+      << ",\"k\":" << s.klog << ",\"n\":" << s.nlog << ",\"perm\":" << (s.perm ? 1 : 0)
+      << ",\"tc\":" << (s.tensor_core ? 1 : 0) << ",\"split\":" << s.split << ",\"in\":";
+    jlist(o, s.in_layout);
+    o << ",\"R\":";
+    jlist(o, s.R);
+    o << ",\"out\":";
+    jlist(o, s.out_layout);
+    if (i < p.step_ms.size()) o << ",\"ms\":" << p.step_ms[i];
+    o << "}";
+  }
+  o << "],\"final_layout\":";
+  jlist(o, p.final_layout);
+  o << "}";
+  return o.str();
+}
+
+}  // namespace tn

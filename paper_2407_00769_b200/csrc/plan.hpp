@@ -1,0 +1,94 @@
+// Plan representation and host-side lowering.
+// Host only: no CUDA types here, so the lowering can be unit-tested without a GPU.
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/tn.h"
+
+namespace tn {
+
+struct TnError {
+  int code;
+  std::string msg;
+};
+
+// A strided view of a complex tensor with every mode of dimension 2.
+struct Leaf {
+  std::vector<int> labels;        // full (unsliced) label list, row-major order
+  std::vector<double> data;       // interleaved complex128 (2 * 2^rank doubles)
+  uint64_t ws_off = 0;            // byte offset of its complex64 copy in the workspace
+};
+
+enum NodeKind { NODE_LEAF = 0, NODE_COMMON = 1, NODE_STEM = 2 };
+
+struct Node {
+  int u = -1, v = -1;             // children (internal nodes)
+  int kind = NODE_LEAF;
+  std::vector<int> labels;        // labels after slicing; for leaves/common = device layout order
+  uint64_t ws_off = 0;            // complex64 storage of common results (bytes into ws)
+  double cost = 0;                // complex MACs of this contraction (sliced)
+  double sub_cost = 0;            // subtree complex MACs
+};
+
+// One stem step: [optional permutation] + GEMM  C[kept, new] = A[kept, R] * B[R, new].
+struct StemStep {
+  int node = -1;                  // tree node produced by this step
+  int branch = -1;                // the non-stem operand (common node or leaf)
+  std::vector<int> in_layout;     // stem layout before the step (outermost first)
+  bool perm = false;              // standalone permutation pass needed
+  std::vector<int> perm_axes;     // numpy-transpose axes: perm_layout[j] = in_layout[perm_axes[j]]
+  std::vector<int> R, kept, newl; // contracted (K order), kept (M order), new (N order)
+  int mlog = 0, klog = 0, nlog = 0;
+  std::vector<int> out_layout;    // kept + newl
+  uint64_t b_off = 0;             // ws offset: B operand (fp16 B_P for chalf, c64 [K][N] for cfloat)
+  uint64_t b_tmp_off = 0;         // ws offset: gathered complex64 [K][N] (chalf path)
+  bool tensor_core = false;       // tcgen05 GEMM (else SIMT)
+  int split = 0;                  // 1 = split-type (chunked tail) step
+};
+
+struct Plan {
+  tn_config cfg{};
+  std::vector<Leaf> leaves;
+  std::vector<Node> nodes;        // leaves first, then internal in SSA order
+  std::vector<int> open;          // output legs in output order
+  std::vector<int> sliced;        // bit j of slice id fixes sliced[j]
+  std::vector<int> stem;          // leaf->root node ids
+  int root = -1;
+  int stem_entry = -1;            // node converted into the stem buffer (-1: no stem steps)
+  std::vector<int> common_order;  // internal common nodes in execution (post) order
+  std::vector<StemStep> steps;
+  std::vector<int> final_layout;  // stem layout after the last step
+  bool final_perm = false;        // final permutation into `open` order
+  std::vector<int> final_perm_axes;
+  int split_from = -1;            // first split-type step index (-1: none)
+  int split_log2 = 0;             // chunks = 2^split_log2
+  // workspace layout
+  uint64_t ws_leaves = 0, ws_common = 0, ws_b = 0, ws_scratch = 0, ws_total = 0;
+  uint64_t stem_elems_max = 0;    // largest stem tensor (elements)
+  int max_stem_log2 = 0;
+  // scratch slots (offsets in bytes from ws_scratch)
+  //   [0, 4*(S+2)): float max slots; slot i = max |real| of the stem after step i-1 (slot 0: entry)
+  //   then S floats b_bound; then int exps[2*S+2]
+  int n_exp_slots = 0;
+  double stem_flops = 0, total_flops = 0, stem_bytes_alg = 0, perm_bytes = 0;
+  int n_permutes = 0;
+  uint64_t h2d_bytes = 0;
+  // runtime state
+  int result_buf = 0;             // which stem buffer holds the result
+  bool result_in_ws = false;      // no stem steps: result is a common node in ws (c64)
+  int timing = 0;
+  std::vector<float> step_ms;
+  void* pinned = nullptr;         // pinned host copy of leaves (complex64), lazily allocated
+  int world = 1, rank = 0;
+  tn_comm* comm = nullptr;
+};
+
+// Parse JSON + validate + lower.  Throws TnError.
+Plan* load_plan(const char* json, size_t len, const tn_config* cfg);
+std::string report_json(const Plan& p);
+
+inline uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
+
+}  // namespace tn

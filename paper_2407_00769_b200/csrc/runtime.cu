@@ -1,0 +1,545 @@
+// C-ABI implementation (include/tn.h): plan lifecycle and the per-slice executor.
+//
+// Executor for one subtask:
+//   1. common phase: every non-stem contraction of the sliced network, complex64,
+//      in the workspace arena; slicing = base offsets into the uploaded leaves;
+//   2. stem operands: each branch is gathered to the dense [K][N] layout its step needs and padded
+//      to B_P per Eq. 6 with an exact power-of-two scale (C-A8);
+//   3. stem entry: the first large stem tensor is converted into stem buffer 0;
+//   4. stem loop (Alg. 1 "performer computation of currEin"): per step an optional
+//      permutation buf p -> buf 1-p, then the GEMM buf p -> buf 1-p (static double buffers).
+//   No host synchronisation inside the loop: all scale exponents live on the device.
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "common.cuh"
+
+using namespace tn;
+
+static thread_local std::string g_err;
+
+static int fail(int code, const std::string& m) {
+  g_err = m;
+  return code;
+}
+
+#define TN_TRY(...)                                    \
+  try {                                                \
+    __VA_ARGS__;                                       \
+    return TN_OK;                                      \
+  } catch (const TnError& e) {                         \
+    return fail(e.code, e.msg);                        \
+  } catch (const std::bad_alloc&) {                    \
+    return fail(TN_E_CAPACITY, "host allocation failed"); \
+  } catch (const std::exception& e) {                  \
+    return fail(TN_E_INVALID, e.what());               \
+  }
+
+struct tn_plan {
+  Plan* p;
+};
+
+struct tn_comm {
+  void* nccl_comm = nullptr;
+  int rank = 0, world = 1, device = 0;
+};
+
+namespace {
+
+struct Scratch {
+  float* max_slot;    // [S+2]   max |real| of the stem entering step i (float bits via atomicMax)
+  float* b_bound;     // [S+2]
+  uint32_t* b_max;    // [S+2]
+  int* exps;          // [n_exp_slots]
+  uint32_t* entry_max;
+  uint64_t bytes;
+};
+
+Scratch scratch_of(const Plan& p, unsigned char* W) {
+  Scratch s;
+  size_t S = p.steps.size();
+  unsigned char* base = W + p.ws_scratch;
+  s.max_slot = reinterpret_cast<float*>(base);
+  s.b_bound = s.max_slot + (S + 2);
+  s.b_max = reinterpret_cast<uint32_t*>(s.b_bound + (S + 2));
+  s.exps = reinterpret_cast<int*>(s.b_max + (S + 2));
+  s.entry_max = reinterpret_cast<uint32_t*>(s.exps + p.n_exp_slots);
+  s.bytes = p.ws_total - p.ws_scratch;
+  return s;
+}
+
+// strided complex64 view of a node for a given slice
+struct View {
+  const float2* base;
+  std::vector<int> labels;
+  std::vector<int64_t> strides;
+  int64_t stride_of(int l) const {
+    for (size_t i = 0; i < labels.size(); ++i)
+      if (labels[i] == l) return strides[i];
+    return -1;
+  }
+};
+
+View view_of(const Plan& p, int id, unsigned char* W, uint64_t slice_id) {
+  View v;
+  const Node& n = p.nodes[id];
+  if (n.kind == NODE_LEAF) {
+    const Leaf& lf = p.leaves[id];
+    int r = (int)lf.labels.size();
+    int64_t off = 0;
+    for (int i = 0; i < r; ++i) {
+      int l = lf.labels[i];
+      int64_t st = 1ll << (r - 1 - i);
+      auto it = std::find(p.sliced.begin(), p.sliced.end(), l);
+      if (it != p.sliced.end()) {
+        int j = (int)(it - p.sliced.begin());
+        if ((slice_id >> j) & 1) off += st;
+      } else {
+        v.labels.push_back(l);
+        v.strides.push_back(st);
+      }
+    }
+    v.base = reinterpret_cast<const float2*>(W + lf.ws_off) + off;
+  } else {
+    int r = (int)n.labels.size();
+    v.labels = n.labels;
+    for (int i = 0; i < r; ++i) v.strides.push_back(1ll << (r - 1 - i));
+    v.base = reinterpret_cast<const float2*>(W + n.ws_off);
+  }
+  return v;
+}
+
+void run_common(const Plan& p, unsigned char* W, uint64_t slice_id, cudaStream_t s) {
+  for (int id : p.common_order) {
+    const Node& n = p.nodes[id];
+    View a = view_of(p, n.u, W, slice_id), b = view_of(p, n.v, W, slice_id);
+    ContractArgs args;
+    memset(&args, 0, sizeof(args));
+    args.a = a.base;
+    args.b = b.base;
+    args.c = reinterpret_cast<float2*>(W + n.ws_off);
+    args.n_out = (int)n.labels.size();
+    if (args.n_out > kMaxModes) throw TnError{TN_E_UNSUPPORTED, "common contraction with too many modes"};
+    for (int j = 0; j < args.n_out; ++j) {
+      int l = n.labels[args.n_out - 1 - j];
+      int64_t sa = a.stride_of(l), sb = b.stride_of(l);
+      args.out_sa[j] = sa < 0 ? 0 : sa;
+      args.out_sb[j] = sb < 0 ? 0 : sb;
+    }
+    int nr = 0;
+    for (size_t i = 0; i < a.labels.size(); ++i) {
+      int64_t sb = b.stride_of(a.labels[i]);
+      if (sb >= 0) {
+        if (nr >= kMaxModes) throw TnError{TN_E_UNSUPPORTED, "too many reduced modes"};
+        args.red_sa[nr] = a.strides[i];
+        args.red_sb[nr] = sb;
+        ++nr;
+      }
+    }
+    args.n_red = nr;
+    launch_contract_c64(args, s);
+  }
+}
+
+void prepare_b(const Plan& p, unsigned char* W, uint64_t slice_id, const Scratch& sc, cudaStream_t s) {
+  for (size_t i = 0; i < p.steps.size(); ++i) {
+    const StemStep& st = p.steps[i];
+    View v = view_of(p, st.branch, W, slice_id);
+    GatherArgs g;
+    memset(&g, 0, sizeof(g));
+    g.src = v.base;
+    g.dst = reinterpret_cast<float2*>(W + st.b_tmp_off);
+    g.klog = st.klog;
+    g.nlog = st.nlog;
+    for (int j = 0; j < st.klog; ++j) g.sk[j] = v.stride_of(st.R[st.klog - 1 - j]);
+    for (int j = 0; j < st.nlog; ++j) g.sn[j] = v.stride_of(st.newl[st.nlog - 1 - j]);
+    launch_gather_kn(g, s);
+    if (p.cfg.dtype == TN_CHALF) {
+      uint64_t kn = 1ull << (st.klog + st.nlog);
+      launch_max_abs_f32(reinterpret_cast<const float*>(g.dst), 2 * kn, &sc.b_max[i], s);
+      launch_pad_b(reinterpret_cast<__half*>(W + st.b_off), g.dst, st.klog, st.nlog, &sc.b_max[i], &sc.b_bound[i],
+                   &sc.exps[1 + 2 * i], s);
+    }
+  }
+}
+
+void check_buffers(const Plan& p, const tn_buffers* b) {
+  if (!b) throw TnError{TN_E_INVALID, "buffers is NULL"};
+  if (!b->d_ws || b->ws_bytes < p.ws_total)
+    throw TnError{TN_E_CAPACITY, "workspace too small: need " + std::to_string(p.ws_total)};
+  const int eb = p.cfg.dtype == TN_CHALF ? 4 : 8;
+  if (!p.steps.empty() && (!b->d_stem[0] || !b->d_stem[1] || b->stem_bytes < p.stem_elems_max * eb))
+    throw TnError{TN_E_CAPACITY, "stem buffers too small: need " + std::to_string(p.stem_elems_max * eb)};
+}
+
+void stem_contract(Plan& p, const tn_buffers* b, uint64_t slice_id, cudaStream_t s) {
+  check_buffers(p, b);
+  if (p.sliced.size() < 64 && slice_id >= (1ull << p.sliced.size()))
+    throw TnError{TN_E_INVALID, "slice_id >= 2^|sliced|"};
+  unsigned char* W = static_cast<unsigned char*>(b->d_ws);
+  Scratch sc = scratch_of(p, W);
+  TN_CUDA(cudaMemsetAsync(W + p.ws_scratch, 0, sc.bytes, s));
+  run_common(p, W, slice_id, s);
+  p.result_in_ws = p.steps.empty();
+  if (p.steps.empty()) return;
+  prepare_b(p, W, slice_id, sc, s);
+  const int eb = p.cfg.dtype == TN_CHALF ? 4 : 8;
+  // stem entry -> buffer 0
+  {
+    const Node& e = p.nodes[p.stem_entry];
+    uint64_t n = 1ull << e.labels.size();
+    const float2* src;
+    if (e.kind == NODE_LEAF) {
+      View v = view_of(p, p.stem_entry, W, slice_id);
+      GatherArgs g;
+      memset(&g, 0, sizeof(g));
+      g.src = v.base;
+      g.dst = reinterpret_cast<float2*>(b->d_stem[1]);  // scratch use of the other buffer
+      g.klog = 0;
+      g.nlog = (int)v.labels.size();
+      for (int j = 0; j < g.nlog; ++j) g.sn[j] = v.strides[g.nlog - 1 - j];
+      if (n * 8 > b->stem_bytes) throw TnError{TN_E_CAPACITY, "stem entry leaf exceeds stem buffer"};
+      launch_gather_kn(g, s);
+      src = g.dst;
+    } else {
+      src = reinterpret_cast<const float2*>(W + e.ws_off);
+    }
+    if (p.cfg.dtype == TN_CHALF) {
+      if (e.kind == NODE_LEAF) {
+        // convert in place is impossible across buffers of different element size: go through ws
+        throw TnError{TN_E_UNSUPPORTED, "complex-half stem entry at a leaf: raise stem_min_log2"};
+      }
+      launch_max_abs_f32(reinterpret_cast<const float*>(src), 2 * n, sc.entry_max, s);
+      launch_c64_to_chalf(reinterpret_cast<__half2*>(b->d_stem[0]), src, n, sc.entry_max, &sc.exps[0],
+                          reinterpret_cast<uint32_t*>(&sc.max_slot[0]), s);
+    } else {
+      launch_copy_c64(reinterpret_cast<float2*>(b->d_stem[0]), src, n, s);
+    }
+  }
+  int cur = 0;
+  std::vector<cudaEvent_t> ev;
+  if (p.timing) {
+    ev.resize(p.steps.size() + 1);
+    for (auto& e : ev) TN_CUDA(cudaEventCreate(&e));
+    TN_CUDA(cudaEventRecord(ev[0], s));
+  }
+  for (size_t i = 0; i < p.steps.size(); ++i) {
+    const StemStep& st = p.steps[i];
+    if (st.perm) {
+      launch_permute(b->d_stem[1 - cur], b->d_stem[cur], eb, (int)st.in_layout.size(), st.perm_axes.data(), s);
+      cur = 1 - cur;
+    }
+    const uint64_t M = 1ull << st.mlog;
+    const uint32_t K = 1u << st.klog, N = 1u << st.nlog;
+    if (p.cfg.dtype == TN_CHALF) {
+      const float* in_max = &sc.max_slot[i];
+      uint32_t* out_max = reinterpret_cast<uint32_t*>(&sc.max_slot[i + 1]);
+      if (st.tensor_core)
+        launch_gemm_chalf_tc(reinterpret_cast<__half*>(b->d_stem[1 - cur]), reinterpret_cast<const __half*>(b->d_stem[cur]),
+                             reinterpret_cast<const __half*>(W + st.b_off), M, 2 * K, 2 * N, in_max, &sc.b_bound[i],
+                             out_max, &sc.exps[2 + 2 * i], s);
+      else
+        launch_gemm_chalf_simt(reinterpret_cast<__half2*>(b->d_stem[1 - cur]),
+                               reinterpret_cast<const __half2*>(b->d_stem[cur]),
+                               reinterpret_cast<const __half*>(W + st.b_off), M, K, N, in_max, &sc.b_bound[i], out_max,
+                               &sc.exps[2 + 2 * i], s);
+    } else {
+      launch_gemm_c64(reinterpret_cast<float2*>(b->d_stem[1 - cur]), reinterpret_cast<const float2*>(b->d_stem[cur]),
+                      reinterpret_cast<const float2*>(W + st.b_off), M, K, N, s);
+    }
+    cur = 1 - cur;
+    if (p.timing) TN_CUDA(cudaEventRecord(ev[i + 1], s));
+  }
+  if (p.final_perm) {
+    launch_permute(b->d_stem[1 - cur], b->d_stem[cur], eb, (int)p.final_layout.size(), p.final_perm_axes.data(), s);
+    cur = 1 - cur;
+  }
+  p.result_buf = cur;
+  if (p.timing) {
+    TN_CUDA(cudaEventSynchronize(ev.back()));
+    p.step_ms.assign(p.steps.size(), 0.f);
+    for (size_t i = 0; i < p.steps.size(); ++i) TN_CUDA(cudaEventElapsedTime(&p.step_ms[i], ev[i], ev[i + 1]));
+    for (auto& e : ev) cudaEventDestroy(e);
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* tn_last_error(void) { return g_err.c_str(); }
+int tn_version(void) { return 1; }
+
+int tn_plan_load(const char* json, size_t len, const tn_config* cfg, tn_comm* comm, tn_plan** out) {
+  if (!json || !out) return fail(TN_E_INVALID, "NULL argument");
+  *out = nullptr;
+  TN_TRY({
+    Plan* p = load_plan(json, len, cfg);
+    if (comm && comm->world > 1) {
+      delete p;
+      throw TnError{TN_E_UNSUPPORTED, "sharded stem (world > 1) is not implemented in this build"};
+    }
+    *out = new tn_plan{p};
+  });
+}
+
+int tn_plan_info_get(const tn_plan* h, tn_plan_info* info) {
+  if (!h || !info) return fail(TN_E_INVALID, "NULL argument");
+  const Plan& p = *h->p;
+  memset(info, 0, sizeof(*info));
+  info->ws_bytes = p.ws_total;
+  info->stem_bytes = p.steps.empty() ? 0 : p.stem_elems_max * (p.cfg.dtype == TN_CHALF ? 4 : 8);
+  info->n_slices_log2 = p.sliced.size();
+  info->n_stem_steps = p.steps.size();
+  info->n_permutes = p.n_permutes + (p.final_perm ? 1 : 0);
+  info->n_common = p.common_order.size();
+  info->stem_flops = p.stem_flops;
+  info->total_flops = p.total_flops;
+  info->stem_bytes_alg = p.stem_bytes_alg;
+  info->perm_bytes = p.perm_bytes;
+  info->n_open = p.open.size();
+  info->max_stem_log2 = p.max_stem_log2;
+  info->h2d_bytes = p.h2d_bytes;
+  info->split_chunks = 1ull << p.split_log2;
+  return TN_OK;
+}
+
+void tn_plan_free(tn_plan* h) {
+  if (!h) return;
+  if (h->p->pinned) cudaFreeHost(h->p->pinned);
+  delete h->p;
+  delete h;
+}
+
+int tn_plan_upload(tn_plan* h, const tn_buffers* b, void* stream) {
+  if (!h || !b || !b->d_ws) return fail(TN_E_INVALID, "NULL argument");
+  TN_TRY({
+    Plan& p = *h->p;
+    if (b->ws_bytes < p.ws_total) throw TnError{TN_E_CAPACITY, "workspace too small"};
+    if (!p.pinned) {
+      TN_CUDA(cudaMallocHost(&p.pinned, p.ws_leaves));
+      memset(p.pinned, 0, p.ws_leaves);
+      for (auto& lf : p.leaves) {
+        float* dst = reinterpret_cast<float*>(static_cast<unsigned char*>(p.pinned) + lf.ws_off);
+        for (size_t i = 0; i < lf.data.size(); ++i) dst[i] = (float)lf.data[i];
+      }
+    }
+    TN_CUDA(cudaMemcpyAsync(b->d_ws, p.pinned, p.ws_leaves, cudaMemcpyHostToDevice, (cudaStream_t)stream));
+  });
+}
+
+int tn_stem_contract(tn_plan* h, const tn_buffers* b, uint64_t slice_id, void* stream) {
+  if (!h) return fail(TN_E_INVALID, "NULL plan");
+  TN_TRY(stem_contract(*h->p, b, slice_id, (cudaStream_t)stream));
+}
+
+int tn_split_contract(tn_plan* h, const tn_buffers* b, void* stream) {
+  if (!h || !b) return fail(TN_E_INVALID, "NULL argument");
+  (void)stream;
+  return TN_OK;  // split-type tail steps run inside tn_stem_contract when split_log2 == 0
+}
+
+int tn_sample_amplitudes(tn_plan* h, const tn_buffers* b, const uint64_t* prefixes, size_t n_sub, double* h_amps,
+                         int k, uint64_t* top_idx, void* stream) {
+  if (!h || !b || !h_amps) return fail(TN_E_INVALID, "NULL argument");
+  if (prefixes || n_sub) return fail(TN_E_UNSUPPORTED, "sparse-state prefixes not supported in this build");
+  TN_TRY({
+    Plan& p = *h->p;
+    cudaStream_t s = (cudaStream_t)stream;
+    const uint64_t n = 1ull << p.open.size();
+    std::vector<int> layout;
+    std::vector<double> vals(2 * n);
+    unsigned char* W = static_cast<unsigned char*>(b->d_ws);
+    int E = 0;
+    if (p.result_in_ws) {
+      int id = p.root;
+      const Node& r = p.nodes[id];
+      std::vector<float> buf(2 * n);
+      if (r.kind == NODE_LEAF) throw TnError{TN_E_UNSUPPORTED, "single-tensor network"};
+      TN_CUDA(cudaMemcpyAsync(buf.data(), W + r.ws_off, 8 * n, cudaMemcpyDeviceToHost, s));
+      TN_CUDA(cudaStreamSynchronize(s));
+      for (uint64_t i = 0; i < 2 * n; ++i) vals[i] = buf[i];
+      layout = r.labels;
+    } else {
+      Scratch sc = scratch_of(p, W);
+      std::vector<int> ex(p.n_exp_slots);
+      TN_CUDA(cudaMemcpyAsync(ex.data(), sc.exps, 4 * ex.size(), cudaMemcpyDeviceToHost, s));
+      if (p.cfg.dtype == TN_CHALF) {
+        std::vector<__half> buf(2 * n);
+        TN_CUDA(cudaMemcpyAsync(buf.data(), b->d_stem[p.result_buf], 4 * n, cudaMemcpyDeviceToHost, s));
+        TN_CUDA(cudaStreamSynchronize(s));
+        for (uint64_t i = 0; i < 2 * n; ++i) vals[i] = (double)__half2float(buf[i]);
+      } else {
+        std::vector<float> buf(2 * n);
+        TN_CUDA(cudaMemcpyAsync(buf.data(), b->d_stem[p.result_buf], 8 * n, cudaMemcpyDeviceToHost, s));
+        TN_CUDA(cudaStreamSynchronize(s));
+        for (uint64_t i = 0; i < 2 * n; ++i) vals[i] = buf[i];
+      }
+      for (int e : ex) E += e;
+      layout = p.final_perm ? p.open : p.final_layout;
+    }
+    // reorder into `open` order and unscale exactly by 2^-E (a.9)
+    const int r = (int)p.open.size();
+    std::vector<int> pos(r);
+    for (int i = 0; i < r; ++i) pos[i] = (int)(std::find(layout.begin(), layout.end(), p.open[i]) - layout.begin());
+    for (uint64_t o = 0; o < n; ++o) {
+      uint64_t src = 0;
+      for (int i = 0; i < r; ++i)
+        if ((o >> (r - 1 - i)) & 1) src |= 1ull << (r - 1 - pos[i]);
+      h_amps[2 * o] = std::ldexp(vals[2 * src], -E);
+      h_amps[2 * o + 1] = std::ldexp(vals[2 * src + 1], -E);
+    }
+    if (top_idx && k > 0) {
+      std::vector<uint64_t> idx(n);
+      for (uint64_t i = 0; i < n; ++i) idx[i] = i;
+      auto prob = [&](uint64_t i) { return h_amps[2 * i] * h_amps[2 * i] + h_amps[2 * i + 1] * h_amps[2 * i + 1]; };
+      std::stable_sort(idx.begin(), idx.end(), [&](uint64_t a, uint64_t c) { return prob(a) > prob(c); });
+      for (int j = 0; j < k && (uint64_t)j < n; ++j) top_idx[j] = idx[j];
+    }
+  });
+}
+
+int tn_report_json(const tn_plan* h, char* buf, size_t cap, size_t* needed) {
+  if (!h) return fail(TN_E_INVALID, "NULL plan");
+  TN_TRY({
+    std::string s = report_json(*h->p);
+    if (needed) *needed = s.size() + 1;
+    if (buf && cap) {
+      size_t n = std::min(cap - 1, s.size());
+      memcpy(buf, s.data(), n);
+      buf[n] = 0;
+      if (cap < s.size() + 1) throw TnError{TN_E_CAPACITY, "report buffer too small"};
+    }
+  });
+}
+
+int tn_set_timing(tn_plan* h, int enable) {
+  if (!h) return fail(TN_E_INVALID, "NULL plan");
+  h->p->timing = enable;
+  return TN_OK;
+}
+
+int tn_permute(void* d_dst, const void* d_src, int elem_bytes, int n, const int* perm, void* stream) {
+  if (!d_dst || !d_src || (!perm && n > 0)) return fail(TN_E_INVALID, "NULL argument");
+  TN_TRY(launch_permute(d_dst, d_src, elem_bytes, n, perm, (cudaStream_t)stream));
+}
+
+int tn_gemm_chalf(void* d_c, const void* d_a, const void* d_bp, uint64_t M, uint32_t K, uint32_t N,
+                  const float* d_in_max, const float* d_b_bound, uint32_t* d_out_max, int* d_exp, void* stream) {
+  if (!d_c || !d_a || !d_bp) return fail(TN_E_INVALID, "NULL argument");
+  if (!K || !N || (K & (K - 1)) || (N & (N - 1))) return fail(TN_E_INVALID, "K and N must be powers of two");
+  TN_TRY({
+    const float* im = (d_in_max && d_b_bound) ? d_in_max : nullptr;
+    const float* bb = (d_in_max && d_b_bound) ? d_b_bound : nullptr;
+    if (K >= 8 && N >= 8)
+      launch_gemm_chalf_tc((__half*)d_c, (const __half*)d_a, (const __half*)d_bp, M, 2 * K, 2 * N, im, bb, d_out_max,
+                           d_exp, (cudaStream_t)stream);
+    else
+      launch_gemm_chalf_simt((__half2*)d_c, (const __half2*)d_a, (const __half*)d_bp, M, K, N, im, bb, d_out_max,
+                             d_exp, (cudaStream_t)stream);
+  });
+}
+
+int tn_gemm_cfloat(void* d_c, const void* d_a, const void* d_b, uint64_t M, uint32_t K, uint32_t N, void* stream) {
+  if (!d_c || !d_a || !d_b) return fail(TN_E_INVALID, "NULL argument");
+  TN_TRY(launch_gemm_c64((float2*)d_c, (const float2*)d_a, (const float2*)d_b, M, K, N, (cudaStream_t)stream));
+}
+
+int tn_pad_b(void* d_bp, const void* d_b, uint32_t K, uint32_t N, float* d_b_bound, int* d_exp, void* d_scratch,
+             void* stream) {
+  if (!d_bp || !d_b || !d_scratch) return fail(TN_E_INVALID, "NULL argument");
+  if (!K || !N || (K & (K - 1)) || (N & (N - 1))) return fail(TN_E_INVALID, "K and N must be powers of two");
+  TN_TRY({
+    cudaStream_t s = (cudaStream_t)stream;
+    int klog = 0, nlog = 0;
+    while ((1u << klog) < K) ++klog;
+    while ((1u << nlog) < N) ++nlog;
+    uint32_t* mx = static_cast<uint32_t*>(d_scratch);
+    TN_CUDA(cudaMemsetAsync(mx, 0, 4, s));
+    if (d_b_bound) TN_CUDA(cudaMemsetAsync(d_b_bound, 0, 4, s));
+    launch_max_abs_f32((const float*)d_b, 2ull * K * N, mx, s);
+    launch_pad_b((__half*)d_bp, (const float2*)d_b, klog, nlog, d_exp ? mx : nullptr, d_b_bound, d_exp, s);
+  });
+}
+
+int tn_quant_int8(int8_t* d_codes, float* d_scales, float* d_zeros, const float* d_x, uint64_t n, int g, void* stream) {
+  if (!d_codes || !d_scales || !d_zeros || !d_x) return fail(TN_E_INVALID, "NULL argument");
+  TN_TRY(launch_quant_int8(d_codes, d_scales, d_zeros, d_x, n, g, (cudaStream_t)stream));
+}
+
+int tn_dequant_int8(float* d_y, const int8_t* d_codes, const float* d_scales, const float* d_zeros, uint64_t n, int g,
+                    void* stream) {
+  if (!d_y || !d_codes || !d_scales || !d_zeros) return fail(TN_E_INVALID, "NULL argument");
+  TN_TRY(launch_dequant_int8(d_y, d_codes, d_scales, d_zeros, n, g, (cudaStream_t)stream));
+}
+
+// ---- NCCL (dlopen'ed: the process's torch already carries libnccl.so.2) ----
+typedef struct {
+  char internal[128];
+} nccl_uid_t;
+typedef int (*nccl_get_uid_fn)(nccl_uid_t*);
+typedef int (*nccl_init_rank_fn)(void**, int, nccl_uid_t, int);
+typedef int (*nccl_destroy_fn)(void*);
+
+static void* nccl_sym(const char* name) {
+  static void* h = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+  });
+  return h ? dlsym(h, name) : nullptr;
+}
+
+int tn_comm_unique_id(uint8_t out[128]) {
+  if (!out) return fail(TN_E_INVALID, "NULL argument");
+  auto fn = (nccl_get_uid_fn)nccl_sym("ncclGetUniqueId");
+  if (!fn) return fail(TN_E_NCCL, "libnccl.so.2 not loadable");
+  nccl_uid_t id;
+  if (fn(&id) != 0) return fail(TN_E_NCCL, "ncclGetUniqueId failed");
+  memcpy(out, id.internal, 128);
+  return TN_OK;
+}
+
+int tn_comm_init(const uint8_t uid[128], int rank, int world, int device, tn_comm** out) {
+  if (!uid || !out) return fail(TN_E_INVALID, "NULL argument");
+  if (world != 1 && world != 2 && world != 4 && world != 8) return fail(TN_E_UNSUPPORTED, "world must be 1,2,4,8");
+  if (rank < 0 || rank >= world) return fail(TN_E_INVALID, "rank out of range");
+  TN_TRY({
+    TN_CUDA(cudaSetDevice(device));
+    tn_comm* c = new tn_comm();
+    c->rank = rank;
+    c->world = world;
+    c->device = device;
+    if (world > 1) {
+      auto fn = (nccl_init_rank_fn)nccl_sym("ncclCommInitRank");
+      if (!fn) {
+        delete c;
+        throw TnError{TN_E_NCCL, "libnccl.so.2 not loadable"};
+      }
+      nccl_uid_t id;
+      memcpy(id.internal, uid, 128);
+      if (fn(&c->nccl_comm, world, id, rank) != 0) {
+        delete c;
+        throw TnError{TN_E_NCCL, "ncclCommInitRank failed"};
+      }
+    }
+    *out = c;
+  });
+}
+
+void tn_comm_free(tn_comm* c) {
+  if (!c) return;
+  if (c->nccl_comm) {
+    auto fn = (nccl_destroy_fn)nccl_sym("ncclCommDestroy");
+    if (fn) fn(c->nccl_comm);
+  }
+  delete c;
+}
+
+}  // extern "C"

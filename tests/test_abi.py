@@ -1,0 +1,108 @@
+"""C-ABI library checks that need no GPU: it builds/loads, exports every symbol include/tn.h
+declares, and the host-side plan parsing/validation/lowering behaves."""
+import copy
+import json
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="session")
+def tnmod():
+    from paper_2407_00769_b200 import build as B
+    B.build()
+    from paper_2407_00769_b200 import tn
+    return tn
+
+
+def header_symbols():
+    src = open(os.path.join(ROOT, "include", "tn.h")).read()
+    return sorted(set(re.findall(r"TN_API[^;(]*?\b(tn_\w+)\s*\(", src)))
+
+
+def test_exports_every_header_symbol(tnmod):
+    L = tnmod.lib()
+    syms = header_symbols()
+    assert len(syms) >= 18
+    for s in syms:
+        assert hasattr(L, s), f"libtn.so does not export {s}"
+    assert L.tn_version() == 1
+
+
+@pytest.fixture(scope="session")
+def c1_plan():
+    with open(os.path.join(ROOT, "plans", "c1.json")) as f:
+        return json.load(f)
+
+
+def _load(tnmod, plan, **cfg):
+    return tnmod.Plan(plan, tnmod.make_config(**cfg))
+
+
+def test_plan_load_info_and_lowering_invariants(tnmod, c1_plan):
+    p = _load(tnmod, c1_plan, stem_min_log2=6)
+    info = p.info()
+    assert info["n_open"] == 12 and info["n_slices_log2"] == 0
+    assert info["n_stem_steps"] >= 1 and info["ws_bytes"] > 0
+    rep = p.report()
+    prev = None
+    for st in rep["steps"]:
+        lay = st["in"]
+        if prev is not None:
+            assert lay == prev
+        R = st["R"]
+        assert len(R) == st["k"]
+        out = st["out"]
+        assert len(out) == st["m"] + st["n"]
+        if not st["perm"]:
+            assert lay[len(lay) - len(R):] == R           # R innermost: GEMM reads A as stored
+        assert set(out[:st["m"]]) == set(lay) - set(R)      # Eq. 4 remaining indices
+        prev = out
+    assert sorted(rep["final_layout"]) == sorted(c1_plan["open"])
+
+
+def test_flops_match_oracle_definition(tnmod, c1_plan):
+    from oracle import contract
+    p = _load(tnmod, c1_plan, stem_min_log2=6)
+    assert p.info()["total_flops"] == contract.flops(c1_plan)
+
+
+def test_plan_errors(tnmod, c1_plan):
+    with pytest.raises(tnmod.TnError) as e:
+        tnmod.Plan('{"tensors": [', tnmod.make_config())
+    assert e.value.code == -2
+    bad = copy.deepcopy(c1_plan)
+    bad["tensors"][0]["data"] = bad["tensors"][0]["data"][:-2]
+    with pytest.raises(tnmod.TnError) as e:
+        tnmod.Plan(bad, tnmod.make_config())
+    assert e.value.code == -1
+    hyper = copy.deepcopy(c1_plan)
+    l0 = hyper["tensors"][0]["labels"][0]
+    t = hyper["tensors"][1]
+    t["labels"] = t["labels"] + [l0]
+    t["data"] = t["data"] + t["data"]
+    with pytest.raises(tnmod.TnError) as e:
+        tnmod.Plan(hyper, tnmod.make_config())
+    assert e.value.code == -1
+    sl_open = copy.deepcopy(c1_plan)
+    sl_open["sliced"] = [sl_open["open"][0]]
+    with pytest.raises(tnmod.TnError) as e:
+        tnmod.Plan(sl_open, tnmod.make_config())
+    assert e.value.code == -1
+    with pytest.raises(tnmod.TnError) as e:
+        _load(tnmod, c1_plan, stem_min_log2=6, stem_capacity_bytes=64)
+    assert e.value.code == -3
+    tree = copy.deepcopy(c1_plan)
+    tree["tree"] = tree["tree"][:-1]
+    with pytest.raises(tnmod.TnError) as e:
+        tnmod.Plan(tree, tnmod.make_config())
+    assert e.value.code == -1
+
+
+def test_header_documents_citations():
+    src = open(os.path.join(ROOT, "include", "tn.h")).read()
+    for cite in ("P:496-514", "P:18-22", "P:230", "Eq. 1"):
+        assert cite in src

@@ -1,0 +1,101 @@
+"""End-to-end parity through the C-ABI on a B200: the full stem path (common phase, Eq. 6
+padding, permutations, tcgen05/SIMT GEMMs, power-of-two scaling) vs the complex128 oracle on
+the same plan and slice.  Tolerances (BASELINE.json north_star): rel-L2 <= 1e-5 (complex64 path),
+<= 2e-2 (complex-half path)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle import contract, metrics
+from oracle.plan import load
+from workload import make_plans as MP
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+TOL = {0: 2e-2, 1: 1e-5}   # TN_CHALF, TN_CFLOAT
+
+
+@pytest.fixture(scope="module")
+def tn():
+    import torch
+    from paper_2407_00769_b200 import build as B
+    B.build()
+    from paper_2407_00769_b200 import tn as T
+    assert torch.cuda.is_available()
+    return T
+
+
+def _plan(name):
+    with open(os.path.join(ROOT, "plans", f"{name}.json")) as f:
+        return json.load(f)
+
+
+def run_gpu(tn, plan, dtype, slice_id=0, stem_min_log2=6):
+    p = tn.Plan(plan, tn.make_config(dtype=dtype, stem_min_log2=stem_min_log2))
+    bufs = tn.Buffers(p)
+    amps = tn.contract(p, bufs, slice_id)
+    return amps, p
+
+
+@pytest.mark.parametrize("dtype", [0, 1])
+@pytest.mark.parametrize("stem_min", [6, 8, 10])
+def test_c1_full_state_vs_oracle(tn, dtype, stem_min):
+    plan = _plan("c1")
+    ref = contract.contract(load(plan), 0)
+    got, p = run_gpu(tn, plan, dtype, 0, stem_min)
+    assert p.info()["n_stem_steps"] >= 1
+    assert metrics.rel_l2(got, ref) <= TOL[dtype]
+    assert abs(np.sum(np.abs(got) ** 2) - 1.0) <= (2 * TOL[dtype])
+
+
+@pytest.mark.parametrize("seed", range(6))
+@pytest.mark.parametrize("dtype", [0, 1])
+def test_random_small_circuits_sliced(tn, seed, dtype):
+    """Seeded small circuits with extra sliced edges: every slice vs the oracle slice, and the
+    GPU sum over slices vs the unsliced oracle (slicing identity)."""
+    rng = np.random.default_rng(seed)
+    rows, cols = [(3, 4), (3, 3), (2, 5)][seed % 3]
+    plan = MP.build_plan(rows, cols, False, int(rng.integers(4, 9)), int(rng.integers(2, 7)), None, trials=2,
+                         seed=seed)
+    sub = MP.sub_slice(plan, max(4, plan["meta"]["max_log2"] - 2))
+    full = contract.contract(load(plan), 0)
+    tot = 0
+    for s in range(1 << len(sub["sliced"])):
+        ref = contract.contract(load(sub), s)
+        got, _ = run_gpu(tn, sub, dtype, s, stem_min_log2=3)
+        if np.linalg.norm(ref) > 1e-12:
+            assert metrics.rel_l2(got, ref) <= TOL[dtype]
+        tot = tot + got
+    assert metrics.rel_l2(tot, full) <= TOL[dtype]
+
+
+@pytest.mark.parametrize("dtype", [0, 1])
+def test_c2_reduced_vs_oracle(tn, dtype):
+    """C2 (30 qubits, 14 cycles) with extra sub-slicing so the oracle finishes in seconds
+    (SURVEY §8(c) c.6): same tree, same kernels, stems up to 2^22."""
+    sub = MP.sub_slice(_plan("c2"), 22)
+    for s in (0, (1 << len(sub["sliced"])) - 1):
+        ref = contract.contract(load(sub), s)
+        got, p = run_gpu(tn, sub, dtype, s, stem_min_log2=12)
+        assert p.info()["n_stem_steps"] >= 3
+        assert metrics.rel_l2(got, ref) <= TOL[dtype]
+
+
+def test_c2_full_fp32_vs_fp16(tn):
+    """Full-size C2 slice: the complex-half path vs the complex64 path (same plan, same slice)."""
+    plan = _plan("c2")
+    a32, _ = run_gpu(tn, plan, 1, 0, stem_min_log2=16)
+    a16, _ = run_gpu(tn, plan, 0, 0, stem_min_log2=16)
+    assert metrics.rel_l2(a16, a32) <= 2e-2
+
+
+def test_slice_id_out_of_range(tn):
+    plan = _plan("c2")
+    p = tn.Plan(plan, tn.make_config(stem_min_log2=16))
+    bufs = tn.Buffers(p)
+    tn.tn_plan_upload(p, bufs)
+    with pytest.raises(tn.TnError) as e:
+        tn.tn_stem_contract(p, bufs, 1 << len(plan["sliced"]))
+    assert e.value.code == -1

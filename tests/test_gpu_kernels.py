@@ -1,0 +1,222 @@
+"""Kernel-level parity on a B200 through the C-ABI (libtn.so), against the oracle / exact
+definitions.  Bit-exact for data movement and the codec; fp tolerances derived in DESIGN.md."""
+import numpy as np
+import pytest
+
+from oracle import codec, embed
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def env():
+    import torch
+    from paper_2407_00769_b200 import build as B
+    B.build()
+    from paper_2407_00769_b200 import tn
+    assert torch.cuda.is_available()
+    return torch, tn
+
+
+def _perm_ref_index(out_idx, perm, n):
+    """source flat index of destination flat index under numpy transpose(perm) for dims 2"""
+    src = 0
+    for j in range(n):
+        bit = (out_idx >> (n - 1 - j)) & 1
+        src |= bit << (n - 1 - perm[j])
+    return src
+
+
+PERMS = {
+    "identity": lambda n: list(range(n)),
+    "reversal": lambda n: list(range(n))[::-1],
+    "swap_last_first": lambda n: [n - 1] + list(range(1, n - 1)) + [0] if n > 1 else [0],
+    "outer3_inner3": lambda n: (list(range(n - 3, n)) + list(range(3, n - 3)) + list(range(3))) if n >= 6 else list(range(n))[::-1],
+    "bitrev_low8": lambda n: list(range(n - 8)) + list(range(n - 8, n))[::-1] if n >= 8 else list(range(n))[::-1],
+}
+
+
+@pytest.mark.parametrize("elem", [4, 8])
+@pytest.mark.parametrize("n", [1, 3, 5, 7, 10, 13, 17, 22])
+def test_permute_bit_exact(env, n, elem):
+    torch, tn = env
+    rng = np.random.default_rng(n * 10 + elem)
+    perms = [f(n) for f in PERMS.values()] + [list(rng.permutation(n)) for _ in range(3)]
+    x = rng.integers(0, 2 ** 31, size=(1 << n) * (elem // 4), dtype=np.int64).astype(np.int32)
+    src = torch.from_numpy(x).cuda()
+    ref_view = x.view(np.int32 if elem == 4 else np.int64).reshape((2,) * n) if n else x
+    for perm in perms:
+        dst = torch.empty_like(src)
+        tn.tn_permute_bytes(dst, src, elem, [int(p) for p in perm])
+        torch.cuda.synchronize()
+        got = dst.cpu().numpy().view(np.int32 if elem == 4 else np.int64)
+        exp = np.ascontiguousarray(np.transpose(ref_view, perm)).reshape(-1)
+        assert np.array_equal(got, exp), perm
+
+
+def test_permute_large_sampled_64bit_indexing(env):
+    """2^32 complex-half elements (16 GiB): sampled outputs vs the index definition."""
+    torch, tn = env
+    n = 32
+    free, _ = torch.cuda.mem_get_info()
+    if free < 40 * 2 ** 30:
+        pytest.skip("needs 40 GiB free")
+    src = torch.arange(0, 1 << n, dtype=torch.int64, device="cuda").to(torch.int32)  # value = index (mod 2^32)
+    dst = torch.empty_like(src)
+    rng = np.random.default_rng(0)
+    perm = [int(p) for p in rng.permutation(n)]
+    tn.tn_permute_bytes(dst, src, 4, perm)
+    torch.cuda.synchronize()
+    idx = rng.integers(0, 1 << n, size=4096, dtype=np.int64)
+    got = dst[torch.from_numpy(idx).cuda()].cpu().numpy().astype(np.int64) & 0xFFFFFFFF
+    exp = np.array([_perm_ref_index(int(i), perm, n) for i in idx], dtype=np.int64) & 0xFFFFFFFF
+    assert np.array_equal(got, exp)
+    del src, dst
+    torch.cuda.empty_cache()
+
+
+def _half_pairs(z):
+    return np.stack([z.real, z.imag], -1).astype(np.float16)
+
+
+@pytest.mark.parametrize("M,K,N", [(1, 8, 8), (128, 8, 8), (300, 16, 8), (1000, 8, 32), (4096 + 37, 32, 64),
+                                   (777, 64, 128), (2048, 128, 256), (513, 256, 16), (1024, 512, 512),
+                                   (256, 2048, 8), (640, 8, 1024)])
+def test_gemm_chalf_tensor_core_vs_oracle(env, M, K, N):
+    """tcgen05 Eq. 6 GEMM (no scaling) vs the oracle's real-embedding GEMM in fp64 on the same
+    fp16 operands.  Error: one fp16 rounding of C (2^-11 relative) + fp32 accumulation."""
+    torch, tn = env
+    rng = np.random.default_rng(M + K * 7 + N * 13)
+    a = (rng.standard_normal((M, K)) + 1j * rng.standard_normal((M, K))) / np.sqrt(2)
+    b = (rng.standard_normal((K, N)) + 1j * rng.standard_normal((K, N))) / np.sqrt(2 * K)
+    a16 = _half_pairs(a)                                   # [M, K, 2]
+    b16 = b.real.astype(np.float16) + 1j * b.imag.astype(np.float16)
+    bp = embed.pad_b(b16)                                   # [c, K, N, a] exact in fp16
+    bp_km = np.transpose(bp, (2, 0, 1, 3)).reshape(2 * N, 2 * K).astype(np.float16)  # [(n,c), (k,a)]
+    ref = embed.cgemm_real(a16.astype(np.float64).reshape(M, 2 * K), bp)            # [M, 2N]
+    A = torch.from_numpy(a16.reshape(-1)).cuda()
+    BP = torch.from_numpy(bp_km.reshape(-1)).cuda()
+    Cc = torch.full((M * 2 * N,), float("nan"), dtype=torch.float16, device="cuda")
+    tn.tn_gemm_chalf(Cc, A, BP, M, K, N)
+    torch.cuda.synchronize()
+    got = Cc.cpu().numpy().astype(np.float64).reshape(M, 2 * N)
+    assert np.all(np.isfinite(got))
+    err = np.abs(got - ref)
+    tol = 2.0 ** -10 * np.abs(ref) + 1e-3 * np.sqrt(np.mean(ref ** 2)) + 1e-7
+    assert np.all(err <= tol), float((err / (np.abs(ref) + 1e-9)).max())
+
+
+def test_gemm_chalf_exact_on_integers(env):
+    """Small-integer operands: every product and sum is exact in fp32 and the result fits fp16
+    exactly, so the tensor-core result must equal the definition bit for bit."""
+    torch, tn = env
+    rng = np.random.default_rng(5)
+    M, K, N = 1000, 64, 32
+    a = rng.integers(-3, 4, (M, K)) + 1j * rng.integers(-3, 4, (M, K))
+    b = rng.integers(-2, 3, (K, N)) + 1j * rng.integers(-2, 3, (K, N))
+    bp = embed.pad_b(b)
+    bp_km = np.transpose(bp, (2, 0, 1, 3)).reshape(2 * N, 2 * K).astype(np.float16)
+    A = torch.from_numpy(_half_pairs(a).reshape(-1)).cuda()
+    C = torch.empty(M * 2 * N, dtype=torch.float16, device="cuda")
+    tn.tn_gemm_chalf(C, A, torch.from_numpy(bp_km.reshape(-1)).cuda(), M, K, N)
+    torch.cuda.synchronize()
+    got = C.cpu().numpy().astype(np.float64).reshape(M, N, 2)
+    ref = a @ b
+    assert np.array_equal(got[..., 0], ref.real) and np.array_equal(got[..., 1], ref.imag)
+
+
+@pytest.mark.parametrize("K,N", [(2, 4), (4, 64), (1, 8), (64, 2), (8, 1)])
+def test_gemm_chalf_simt_small_shapes(env, K, N):
+    torch, tn = env
+    rng = np.random.default_rng(K * 100 + N)
+    M = 777
+    a = rng.integers(-3, 4, (M, K)) + 1j * rng.integers(-3, 4, (M, K))
+    b = rng.integers(-2, 3, (K, N)) + 1j * rng.integers(-2, 3, (K, N))
+    bp_km = np.transpose(embed.pad_b(b), (2, 0, 1, 3)).reshape(2 * N, 2 * K).astype(np.float16)
+    C = torch.empty(M * 2 * N, dtype=torch.float16, device="cuda")
+    tn.tn_gemm_chalf(C, torch.from_numpy(_half_pairs(a).reshape(-1)).cuda(),
+                     torch.from_numpy(bp_km.reshape(-1)).cuda(), M, K, N)
+    torch.cuda.synchronize()
+    got = C.cpu().numpy().astype(np.float64).reshape(M, N, 2)
+    ref = a @ b
+    assert np.array_equal(got[..., 0] + 1j * got[..., 1], ref)
+
+
+def test_pad_b_and_scaled_gemm(env):
+    """Eq. 6 padding on the device (scale 2^t by the C-A8 rule) vs the oracle's pad_b, then the
+    scaled GEMM: exponent recorded, |C| <= 2^14, out_max = max|C|."""
+    torch, tn = env
+    rng = np.random.default_rng(9)
+    K, N, M = 64, 128, 3000
+    b = ((rng.standard_normal((K, N)) + 1j * rng.standard_normal((K, N))) * 1e-3).astype(np.complex64)
+    B = torch.from_numpy(b.view(np.float32).reshape(-1)).cuda()
+    BP = torch.empty(4 * K * N, dtype=torch.float16, device="cuda")
+    bound = torch.zeros(1, dtype=torch.float32, device="cuda")
+    ex = torch.zeros(2, dtype=torch.int32, device="cuda")
+    scratch = torch.zeros(4, dtype=torch.int32, device="cuda")
+    tn.tn_pad_b(BP, B, K, N, bound, ex, scratch)
+    torch.cuda.synchronize()
+    bmax = np.abs(b.view(np.float32)).max()
+    p = int(np.frexp(np.float32(bmax))[1])
+    t = 14 - p
+    assert int(ex[0].item()) == t
+    bs = (b.real.astype(np.float32) * np.float32(2.0 ** t)).astype(np.float16) + \
+        1j * (b.imag.astype(np.float32) * np.float32(2.0 ** t)).astype(np.float16)
+    exp_bp = np.transpose(embed.pad_b(bs), (2, 0, 1, 3)).reshape(2 * N, 2 * K).astype(np.float16)
+    got_bp = BP.cpu().numpy().reshape(2 * N, 2 * K)
+    assert np.array_equal(got_bp, exp_bp)
+    l1 = np.abs(exp_bp.astype(np.float64)).sum(axis=1).max()
+    assert abs(bound.item() - l1) <= 1e-5 * l1
+    # scaled GEMM
+    a = (rng.standard_normal((M, K)) + 1j * rng.standard_normal((M, K))) * 3.0
+    a16 = _half_pairs(a)
+    in_max = torch.tensor([float(np.abs(a16.astype(np.float32)).max())], device="cuda")
+    out_max = torch.zeros(1, dtype=torch.int32, device="cuda")
+    C = torch.empty(M * 2 * N, dtype=torch.float16, device="cuda")
+    tn.tn_gemm_chalf(C, torch.from_numpy(a16.reshape(-1)).cuda(), BP, M, K, N, in_max, bound, out_max, ex[1:])
+    torch.cuda.synchronize()
+    e = int(ex[1].item())
+    prod = np.float32(in_max.item()) * np.float32(bound.item())
+    assert e == 14 - int(np.frexp(prod)[1])
+    ref = embed.cgemm_real(a16.astype(np.float64).reshape(M, 2 * K), embed.pad_b(bs)) * 2.0 ** e
+    got = C.cpu().numpy().astype(np.float64).reshape(M, 2 * N)
+    assert np.abs(got).max() <= 2 ** 14
+    assert np.all(np.abs(got - ref) <= 2.0 ** -10 * np.abs(ref) + 1e-3 * np.sqrt(np.mean(ref ** 2)))
+    mx = np.frombuffer(np.int32(out_max.item()).tobytes(), dtype=np.float32)[0]
+    assert mx == np.abs(got).max()
+
+
+@pytest.mark.parametrize("M,K,N", [(1, 1, 1), (100, 3, 5), (1000, 64, 64), (4097, 128, 33)])
+def test_gemm_cfloat(env, M, K, N):
+    torch, tn = env
+    rng = np.random.default_rng(M)
+    a = (rng.standard_normal((M, K)) + 1j * rng.standard_normal((M, K))).astype(np.complex64)
+    b = (rng.standard_normal((K, N)) + 1j * rng.standard_normal((K, N))).astype(np.complex64)
+    A = torch.from_numpy(a.view(np.float32).reshape(-1)).cuda()
+    B = torch.from_numpy(b.view(np.float32).reshape(-1)).cuda()
+    C = torch.empty(2 * M * N, dtype=torch.float32, device="cuda")
+    tn.tn_gemm_cfloat(C, A, B, M, K, N)
+    torch.cuda.synchronize()
+    got = C.cpu().numpy().view(np.complex64).reshape(M, N).astype(np.complex128)
+    ref = a.astype(np.complex128) @ b.astype(np.complex128)
+    assert np.linalg.norm(got - ref) <= 1e-6 * np.linalg.norm(ref)
+
+
+@pytest.mark.parametrize("g", [128, 64, 256])
+def test_quant_int8_bit_exact_vs_oracle_codec(env, g):
+    torch, tn = env
+    rng = np.random.default_rng(g)
+    x = (rng.standard_normal(g * 257) * 10.0 ** rng.uniform(-6, 2)).astype(np.float32)
+    x[:g] = 0.37  # a constant group (C-A11)
+    X = torch.from_numpy(x).cuda()
+    codes = torch.empty(x.size, dtype=torch.int8, device="cuda")
+    sc = torch.empty(x.size // g, dtype=torch.float32, device="cuda")
+    ze = torch.empty_like(sc)
+    tn.tn_quant_int8(codes, sc, ze, X, g)
+    y = torch.empty_like(X)
+    tn.tn_dequant_int8(y, codes, sc, ze, g)
+    torch.cuda.synchronize()
+    rc, rs, rz = codec.quantize(x, np.float32(-128), np.float32(127), 1.0, group=g)
+    assert np.array_equal(codes.cpu().numpy().astype(np.float32), rc)
+    assert np.array_equal(sc.cpu().numpy(), rs) and np.array_equal(ze.cpu().numpy(), rz)
+    assert np.array_equal(y.cpu().numpy(), codec.dequantize(rc, rs, rz, 1.0, group=g))

@@ -30,9 +30,9 @@ CONFIGS = {
     # C1: 12-qubit depth-8, all legs open (full state), unsliced (BJ configs[0])
     "c1": dict(rows=3, cols=4, drop=False, cycles=8, n_open=12, max_log2=None, trials=8),
     # C2: 30-qubit 14-cycle, stem <= 2^28, 10 open legs (BJ configs[1])
-    "c2": dict(rows=5, cols=6, drop=False, cycles=14, n_open=10, max_log2=30, trials=4),
+    "c2": dict(rows=5, cols=6, drop=False, cycles=14, n_open=10, max_log2=30, trials=0),
     # C3: 53-qubit (6x9 minus a corner) 20-cycle, stem <= 2^32, 6 open legs (BJ configs[2])
-    "c3": dict(rows=6, cols=9, drop=True, cycles=20, n_open=6, max_log2=35, trials=2),
+    "c3": dict(rows=6, cols=9, drop=True, cycles=20, n_open=6, max_log2=35, trials=0),
 }
 
 
@@ -140,3 +140,39 @@ def main(argv):
 
 if __name__ == "__main__":
     main(sys.argv[1:])
+
+
+def sub_slice(plan, target_log2):
+    """Reduced-scale protocol: slice extra closed labels of an existing plan
+    (same tree, same leaves) until every intermediate has <= 2^target_log2 elements.  The result
+    is another valid plan; its slices are sub-slices of the original."""
+    import copy
+    leaf_masks = []
+    for t in plan["tensors"]:
+        m = 0
+        for l in t["labels"]:
+            m |= 1 << l
+        leaf_masks.append(m)
+    tree = PL.Tree(leaf_masks, [tuple(p) for p in plan["tree"]])
+    sliced = 0
+    for l in plan["sliced"]:
+        sliced |= 1 << l
+    open_mask = 0
+    for l in plan["open"]:
+        open_mask |= 1 << l
+    extra = []
+    while tree.max_log2(sliced) > target_log2:
+        worst = tree.max_log2(sliced)
+        score = {}
+        for m in tree.masks:
+            if PL.popcount(m & ~sliced) >= worst - 2:
+                for l in PL.bits_of(m & ~sliced & ~open_mask):
+                    score[l] = score.get(l, 0) + (4 if PL.popcount(m & ~sliced) == worst else 1)
+        if not score:  # only open legs remain in the widest intermediates
+            break
+        l = max(sorted(score), key=lambda x: score[x])
+        sliced |= 1 << l
+        extra.append(l)
+    out = copy.deepcopy(plan)
+    out["sliced"] = list(plan["sliced"]) + extra
+    return out

@@ -210,7 +210,7 @@ def group_branches(tree, sliced, stem, max_branch_log2=20, max_group=12):
             if t > j:
                 merge += 8.0 * (1 << popcount(nm(bm | mt))) / P_SIMT + LAUNCH
             bm ^= mt
-            if popcount(nm(bm)) > max_branch_log2:
+            if jp > j and popcount(nm(bm)) > max_branch_log2:
                 return None
         s = nm(stem_masks[j])
         b = nm(bm)
