@@ -1,0 +1,293 @@
+#!/usr/bin/env python
+"""Benchmark: stem-path contraction of one sliced subtask of the C3 workload (53-qubit, 20-cycle
+Sycamore-style RQC network, largest stem 2^33 complex-half) on B200 — BASELINE.json metric
+"stem-contraction effective TFLOPS/GPU and subtask time-to-solution".
+
+A step = one subtask: tn_stem_contract (common phase + Eq. 6 padding + all stem steps) +
+tn_split_contract, inputs (leaves) resident in HBM.  value = aggregate effective TFLOPS over all
+ranks (8 flops per complex MAC of the stem GEMMs, reading C-A21) / max-over-ranks device time.
+Multi-GPU: replicas over independent slices (weak scaling, no data-path collective).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--plan c3]
+"""
+import os
+
+_CORES = len(os.sched_getaffinity(0))
+for _v in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS"):
+    os.environ.setdefault(_v, str(_CORES))
+
+import argparse  # noqa: E402
+import json  # noqa: E402
+import statistics  # noqa: E402
+import subprocess  # noqa: E402
+import sys  # noqa: E402
+import tempfile  # noqa: E402
+import time  # noqa: E402
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "stem-contraction effective TFLOPS/GPU and subtask time-to-solution at 1/2/4/8 B200"
+WORKLOADS = {
+    "c3": "C3: 53-qubit (6x9 grid minus a corner) 20-cycle Sycamore-style RQC network, one sliced subtask, "
+          "6 open legs, largest stem 2^33 complex-half, stem buffers 2 x 32 GiB",
+    "c2": "C2: 30-qubit (5x6) 14-cycle RQC, one sliced subtask, 10 open legs",
+}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), float(d["bf16_tflops"]), float(d.get("bf16_tflops_sustained", d["bf16_tflops"])), "measured"
+    except Exception:
+        return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index):
+        self.f = tempfile.NamedTemporaryFile("w+", delete=False, suffix=".csv")
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(index), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                       "-lms", "200"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.f.flush()
+        rows = []
+        with open(self.f.name) as f:
+            for line in f:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) >= 9:
+                    rows.append(parts)
+        os.unlink(self.f.name)
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            for n, v in zip(names, r[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": float(rows[0][2]) if rows[0][2].replace(".", "").isdigit() else None,
+                "power_w_max": max(float(r[3]) for r in rows if r[3].replace(".", "").isdigit()) if rows else None,
+                "samples": len(rows), "reasons": sorted(reasons)}
+
+
+def oracle_sample(plan, target_log2):
+    from workload import make_plans as MP
+    return MP.sub_slice(plan, target_log2)
+
+
+def run_oracle(sub, steps, warmup):
+    from oracle import contract
+    from oracle.plan import load
+    p = load(sub)
+    fl = contract.flops(sub)
+    for _ in range(warmup):
+        contract.contract(p, 0)
+    ts = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        contract.contract(p, 0)
+        ts.append(time.perf_counter() - t0)
+    t = statistics.median(ts)
+    return fl, t
+
+
+def cpu_baseline(plan, target_log2, steps=1, warmup=0):
+    sub = oracle_sample(plan, target_log2)
+    fl, t = run_oracle(sub, steps, warmup)
+    return {"value": fl / t / 1e12, "unit": "TFLOPS", "cores": _CORES, "kind": "oracle",
+            "seconds": t, "sample": f"oracle (numpy complex128, np.tensordot) on slice 0 of the same plan "
+                                   f"sub-sliced by {len(sub['sliced']) - len(plan['sliced'])} extra edges "
+                                   f"(every intermediate <= 2^{target_log2}); {fl:.3e} flops in {t:.2f} s"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--plan", default="c3")
+    ap.add_argument("--oracle-log2", type=int, default=24)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    with open(os.path.join(ROOT, "plans", f"{args.plan}.json")) as f:
+        plan_json = json.load(f)
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        sub = oracle_sample(plan_json, args.oracle_log2)
+        fl, t = run_oracle(sub, args.steps, args.warmup)
+        line = {"metric": METRIC, "value": fl / t / 1e12, "unit": "TFLOPS", "n_gpus": args.gpus, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "c128", "data": "synthetic", "impl": "reference",
+                "config": {"workload": WORKLOADS.get(args.plan, args.plan), "plan": f"plans/{args.plan}.json",
+                           "sample": f"sub-sliced to 2^{args.oracle_log2}"},
+                "cpu_baseline": {"value": fl / t / 1e12, "unit": "TFLOPS", "cores": _CORES, "kind": "oracle",
+                                 "sample": f"slice 0 of plans/{args.plan}.json sub-sliced so every intermediate "
+                                           f"<= 2^{args.oracle_log2}; {fl:.3e} flops"},
+                "e2e": {"value": fl / t / 1e12, "unit": "TFLOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    import torch
+    import torch.distributed as dist
+    from paper_2407_00769_b200 import build as B
+    B.build()
+    from paper_2407_00769_b200 import tn
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev_stream = torch.cuda.current_stream()
+
+    p = tn.Plan(plan_json, tn.make_config(dtype=tn.TN_CHALF, stem_min_log2=20))
+    info = p.info()
+    bufs = tn.Buffers(p)
+    n_sl = min(info["n_slices_log2"], 63)
+    slice_id = rank % (1 << n_sl) if n_sl else 0
+    tn.tn_plan_upload(p, bufs)
+
+    def step():
+        tn.tn_stem_contract(p, bufs, slice_id)
+        tn.tn_split_contract(p, bufs)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    p.set_timing(True)
+    clk = Clocks(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(dev_stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(dev_stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = clk.stop()
+    t_ms = e0.elapsed_time(e1) / args.steps
+    rep = p.report()
+    launches = p.info()["n_launches"] * args.steps
+    p.set_timing(False)
+    if world > 1:
+        tt = torch.tensor([t_ms], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_ms = float(tt.item())
+
+    # ---- end to end through the public API with host buffers (H2D leaves, D2H amplitudes)
+    for _ in range(2):
+        tn.contract(p, bufs, slice_id)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        tn.contract(p, bufs, slice_id)
+    torch.cuda.synchronize()
+    te_ms = (time.perf_counter() - t0) * 1e3 / args.steps
+    if world > 1:
+        tt = torch.tensor([te_ms], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        te_ms = float(tt.item())
+
+    flops = info["stem_flops"]
+    value = world * flops / (t_ms * 1e-3) / 1e12
+    hbm, tc_burst, tc_sus, src = peaks()
+
+    # ---- roofline of the dominant kernel (from the timed region's CUDA events)
+    ms = rep.get("ms", [])
+    steps = rep["steps"]
+    gemm_ms = perm_ms = 0.0
+    gemm_bytes = gemm_flops = t_roof_gemm = perm_bytes = 0.0
+    eb = 4
+    for i, st in enumerate(steps):
+        M, K, N = 2.0 ** st["m"], 2.0 ** st["k"], 2.0 ** st["n"]
+        pm, gm = ms[1 + 2 * i], ms[2 + 2 * i]
+        perm_ms += pm
+        gemm_ms += gm
+        by = eb * (M * K + M * N) + 8 * K * N
+        fl = 8 * M * K * N
+        gemm_bytes += by
+        gemm_flops += fl
+        t_roof_gemm += max(by / (hbm * 1e9), fl / (tc_burst * 1e12)) * 1e3
+        if st["perm"]:
+            perm_bytes += 2 * eb * M * K
+    final_ms = ms[-1] if ms else 0.0
+    if rep.get("final_layout") and final_ms > 0:
+        perm_ms += final_ms
+        perm_bytes += 2 * eb * 2.0 ** len(rep["final_layout"])
+    common_ms = ms[0] if ms else 0.0
+    if gemm_ms >= perm_ms:
+        bytes_bound = gemm_bytes / (hbm * 1e9) >= gemm_flops / (tc_burst * 1e12)
+        if bytes_bound:
+            ach = gemm_bytes / (gemm_ms * 1e-3) / 1e9
+            roof = {"kernel": "gemm_chalf_tc (+simt small-K/N steps)", "bound": "hbm", "achieved": ach, "peak": hbm,
+                    "unit": "GB/s", "frac": ach / hbm}
+        else:
+            ach = gemm_flops / (gemm_ms * 1e-3) / 1e12
+            roof = {"kernel": "gemm_chalf_tc", "bound": "tensor", "achieved": ach, "peak": tc_burst,
+                    "unit": "TFLOP/s", "frac": ach / tc_burst}
+        roof["roofline_time_frac"] = t_roof_gemm / gemm_ms if gemm_ms else None
+        roof["launches_per_step"] = len(steps)
+    else:
+        ach = perm_bytes / (perm_ms * 1e-3) / 1e9
+        roof = {"kernel": "permute", "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm}
+    roof["peak_source"] = src
+    roof["traffic"] = None
+    roof["share_of_step"] = {"gemm": gemm_ms / t_ms, "permute": perm_ms / t_ms, "common+prep": common_ms / t_ms}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "TFLOPS", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": t_ms, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f16", "data": "synthetic",
+                "config": {"workload": WORKLOADS.get(args.plan, args.plan), "plan": f"plans/{args.plan}.json",
+                           "slice": "rank r runs slice r (replicas over independent subtasks)",
+                           "stem_steps": info["n_stem_steps"], "permutes": info["n_permutes"],
+                           "max_stem_log2": info["max_stem_log2"], "stem_flops": flops,
+                           "l2": "inputs larger than L2 (stem tensors up to 32 GiB >> 126 MB)"},
+                "tflops_per_gpu": value / world, "subtask_ms": t_ms,
+                "breakdown_ms": {"common+prep": common_ms, "permute": perm_ms, "gemm": gemm_ms},
+                "roofline": roof,
+                "e2e": {"value": world * flops / (te_ms * 1e-3) / 1e12, "unit": "TFLOPS",
+                        "ms_per_step": te_ms, "h2d_bytes_per_step": info["h2d_bytes"],
+                        "d2h_bytes_per_step": (4 << info["n_open"]) + 4 * (2 * info["n_stem_steps"] + 4)},
+                "gpu_launches": launches, "clocks": clocks}
+        if world == 1 and not args.no_cpu:
+            try:
+                line["cpu_baseline"] = cpu_baseline(plan_json, args.oracle_log2)
+            except Exception as e:  # the oracle must not take the GPU number down with it
+                line["cpu_baseline"] = {"error": str(e)}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

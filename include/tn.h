@@ -94,6 +94,7 @@ typedef struct {
   uint64_t max_stem_log2;    /* log2 elements of the largest stem tensor */
   uint64_t h2d_bytes;        /* bytes tn_plan_upload copies host->device */
   uint64_t split_chunks;     /* chunk count of the split-type tail (1 = none) */
+  uint64_t n_launches;       /* kernels the last tn_stem_contract launched (0 before the first) */
 } tn_plan_info;
 
 TN_API const char* tn_last_error(void);
@@ -113,7 +114,9 @@ TN_API void tn_plan_free(tn_plan* p);
  * with a given workspace; the end-to-end harness calls it every step (its H2D traffic). */
 TN_API int tn_plan_upload(tn_plan* p, const tn_buffers* b, void* stream);
 
-/* Run slice `slice_id` (bit j fixes sliced[j], reading C-A20): common-type branch contractions,
+/* Run slice `slice_id` (bit j fixes sliced[j], reading C-A20; sliced labels beyond the 64th are
+ * fixed to 0, so a plan with more than 64 sliced labels exposes its first 2^64 subtasks here):
+ * common-type branch contractions,
  * Eq. 6 padding of every stem operand, then the stem steps (permutation + GEMM per step) in the
  * two stem buffers.  Asynchronous; result stays on the device.  TN_E_INVALID if
  * slice_id >= 2^|sliced|; TN_E_CAPACITY if the buffers are smaller than tn_plan_info says. */
@@ -133,9 +136,11 @@ TN_API int tn_sample_amplitudes(tn_plan* p, const tn_buffers* b, const uint64_t*
                          double* h_amps, int k, uint64_t* top_idx, void* stream);
 
 /* JSON report: per stem step geometry, permutation flag, flops, algorithmic bytes, and (after a
- * run with timing enabled) per-step milliseconds.  *needed = bytes required incl. NUL. */
+ * run with timing enabled) "ms": [common phase, (permutation, GEMM) per step..., final perm],
+ * measured with CUDA events on the call's stream (synchronises on the last event).
+ * *needed = bytes required incl. NUL. */
 TN_API int tn_report_json(const tn_plan* p, char* buf, size_t cap, size_t* needed);
-/* Enable per-step CUDA-event timing on the next tn_stem_contract (costs a sync per step). */
+/* Enable CUDA-event timing of the phases of tn_stem_contract (events only, no host sync). */
 TN_API int tn_set_timing(tn_plan* p, int enable);
 
 /* ---- kernel-level entry points (used by the parity tests; same kernels as the stem loop) ---- */

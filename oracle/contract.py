@@ -20,7 +20,7 @@ from .plan import Plan, load
 
 def slice_leaves(plan: Plan, slice_id: int):
     """Leaves with every sliced label fixed to its bit of ``slice_id`` (mode dropped)."""
-    if slice_id < 0 or slice_id >= (1 << len(plan.sliced)):
+    if slice_id < 0 or slice_id >= (1 << min(len(plan.sliced), 64)):
         raise ValueError("slice id out of range")
     val = {l: (slice_id >> j) & 1 for j, l in enumerate(plan.sliced)}
     out = []

@@ -84,7 +84,7 @@ Plan* load_plan(const char* json, size_t len, const tn_config* cfg_in) {
   }
   p.open = int_list(root.get("open"), "open");
   p.sliced = int_list(root.get("sliced"), "sliced");
-  if (p.sliced.size() > 62) throw err(TN_E_UNSUPPORTED, "more than 62 sliced labels");
+  if (p.sliced.size() > 4096) throw err(TN_E_UNSUPPORTED, "more than 4096 sliced labels");
   const tnjson::Value* tr = root.get("tree");
   std::vector<std::pair<int, int>> pairs;
   if (tr) {
@@ -342,7 +342,7 @@ static void jlist(std::ostringstream& o, const std::vector<int>& v) {
   o << "]";
 }
 
-std::string report_json(const Plan& p) {
+std::string report_json(const Plan& p, const std::vector<float>& ms) {
   std::ostringstream o;
   o.precision(17);
   o << "{\"dtype\":\"" << (p.cfg.dtype == TN_CHALF ? "chalf" : "cfloat") << "\"";
@@ -361,11 +361,16 @@ std::string report_json(const Plan& p) {
     jlist(o, s.R);
     o << ",\"out\":";
     jlist(o, s.out_layout);
-    if (i < p.step_ms.size()) o << ",\"ms\":" << p.step_ms[i];
     o << "}";
   }
   o << "],\"final_layout\":";
   jlist(o, p.final_layout);
+  o << ",\"launches\":" << p.launches;
+  if (!ms.empty()) {  // [common_ms, (perm_ms, gemm_ms) per step..., final_ms]
+    o << ",\"ms\":[";
+    for (size_t i = 0; i < ms.size(); ++i) o << (i ? "," : "") << ms[i];
+    o << "]";
+  }
   o << "}";
   return o.str();
 }

@@ -79,7 +79,11 @@ struct Plan {
   int result_buf = 0;             // which stem buffer holds the result
   bool result_in_ws = false;      // no stem steps: result is a common node in ws (c64)
   int timing = 0;
-  std::vector<float> step_ms;
+  // timing events (cudaEvent_t as void*): [0] start, [1] stem entry ready, then per step i
+  // [2+2i] after the permutation, [3+2i] after the GEMM; [2+2S] after the final permutation.
+  std::vector<void*> ev;
+  bool ev_valid = false;
+  uint64_t launches = 0;          // kernels launched by the last tn_stem_contract
   void* pinned = nullptr;         // pinned host copy of leaves (complex64), lazily allocated
   int world = 1, rank = 0;
   tn_comm* comm = nullptr;
@@ -87,7 +91,7 @@ struct Plan {
 
 // Parse JSON + validate + lower.  Throws TnError.
 Plan* load_plan(const char* json, size_t len, const tn_config* cfg);
-std::string report_json(const Plan& p);
+std::string report_json(const Plan& p, const std::vector<float>& ms);
 
 inline uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
 

@@ -98,7 +98,7 @@ View view_of(const Plan& p, int id, unsigned char* W, uint64_t slice_id) {
       auto it = std::find(p.sliced.begin(), p.sliced.end(), l);
       if (it != p.sliced.end()) {
         int j = (int)(it - p.sliced.begin());
-        if ((slice_id >> j) & 1) off += st;
+        if (j < 64 && ((slice_id >> j) & 1)) off += st;  // bits >= 64 of a slice id are 0
       } else {
         v.labels.push_back(l);
         v.strides.push_back(st);
@@ -160,6 +160,7 @@ void prepare_b(const Plan& p, unsigned char* W, uint64_t slice_id, const Scratch
     for (int j = 0; j < st.nlog; ++j) g.sn[j] = v.stride_of(st.newl[st.nlog - 1 - j]);
     launch_gather_kn(g, s);
     if (p.cfg.dtype == TN_CHALF) {
+      const_cast<Plan&>(p).launches += 2;
       uint64_t kn = 1ull << (st.klog + st.nlog);
       launch_max_abs_f32(reinterpret_cast<const float*>(g.dst), 2 * kn, &sc.b_max[i], s);
       launch_pad_b(reinterpret_cast<__half*>(W + st.b_off), g.dst, st.klog, st.nlog, &sc.b_max[i], &sc.b_bound[i],
@@ -183,11 +184,24 @@ void stem_contract(Plan& p, const tn_buffers* b, uint64_t slice_id, cudaStream_t
     throw TnError{TN_E_INVALID, "slice_id >= 2^|sliced|"};
   unsigned char* W = static_cast<unsigned char*>(b->d_ws);
   Scratch sc = scratch_of(p, W);
+  p.launches = 0;
+  p.ev_valid = false;
+  if (p.timing && p.ev.empty()) {
+    p.ev.resize(3 + 2 * p.steps.size());
+    for (auto& e : p.ev) {
+      cudaEvent_t ce;
+      TN_CUDA(cudaEventCreate(&ce));
+      e = (void*)ce;
+    }
+  }
+  if (p.timing) TN_CUDA(cudaEventRecord((cudaEvent_t)p.ev[0], s));
   TN_CUDA(cudaMemsetAsync(W + p.ws_scratch, 0, sc.bytes, s));
   run_common(p, W, slice_id, s);
+  p.launches += p.common_order.size();
   p.result_in_ws = p.steps.empty();
   if (p.steps.empty()) return;
   prepare_b(p, W, slice_id, sc, s);
+  p.launches += p.steps.size() + 2;  // gathers + entry conversion (max + convert)
   const int eb = p.cfg.dtype == TN_CHALF ? 4 : 8;
   // stem entry -> buffer 0
   {
@@ -222,18 +236,18 @@ void stem_contract(Plan& p, const tn_buffers* b, uint64_t slice_id, cudaStream_t
     }
   }
   int cur = 0;
-  std::vector<cudaEvent_t> ev;
-  if (p.timing) {
-    ev.resize(p.steps.size() + 1);
-    for (auto& e : ev) TN_CUDA(cudaEventCreate(&e));
-    TN_CUDA(cudaEventRecord(ev[0], s));
-  }
+  auto rec = [&](size_t k) {
+    if (p.timing) TN_CUDA(cudaEventRecord((cudaEvent_t)p.ev[k], s));
+  };
+  rec(1);
   for (size_t i = 0; i < p.steps.size(); ++i) {
     const StemStep& st = p.steps[i];
     if (st.perm) {
       launch_permute(b->d_stem[1 - cur], b->d_stem[cur], eb, (int)st.in_layout.size(), st.perm_axes.data(), s);
+      ++p.launches;
       cur = 1 - cur;
     }
+    rec(2 + 2 * i);
     const uint64_t M = 1ull << st.mlog;
     const uint32_t K = 1u << st.klog, N = 1u << st.nlog;
     if (p.cfg.dtype == TN_CHALF) {
@@ -252,20 +266,18 @@ void stem_contract(Plan& p, const tn_buffers* b, uint64_t slice_id, cudaStream_t
       launch_gemm_c64(reinterpret_cast<float2*>(b->d_stem[1 - cur]), reinterpret_cast<const float2*>(b->d_stem[cur]),
                       reinterpret_cast<const float2*>(W + st.b_off), M, K, N, s);
     }
+    ++p.launches;
     cur = 1 - cur;
-    if (p.timing) TN_CUDA(cudaEventRecord(ev[i + 1], s));
+    rec(3 + 2 * i);
   }
   if (p.final_perm) {
     launch_permute(b->d_stem[1 - cur], b->d_stem[cur], eb, (int)p.final_layout.size(), p.final_perm_axes.data(), s);
+    ++p.launches;
     cur = 1 - cur;
   }
+  rec(2 + 2 * p.steps.size());
+  p.ev_valid = p.timing != 0;
   p.result_buf = cur;
-  if (p.timing) {
-    TN_CUDA(cudaEventSynchronize(ev.back()));
-    p.step_ms.assign(p.steps.size(), 0.f);
-    for (size_t i = 0; i < p.steps.size(); ++i) TN_CUDA(cudaEventElapsedTime(&p.step_ms[i], ev[i], ev[i + 1]));
-    for (auto& e : ev) cudaEventDestroy(e);
-  }
 }
 
 }  // namespace
@@ -306,12 +318,14 @@ int tn_plan_info_get(const tn_plan* h, tn_plan_info* info) {
   info->max_stem_log2 = p.max_stem_log2;
   info->h2d_bytes = p.h2d_bytes;
   info->split_chunks = 1ull << p.split_log2;
+  info->n_launches = p.launches;
   return TN_OK;
 }
 
 void tn_plan_free(tn_plan* h) {
   if (!h) return;
   if (h->p->pinned) cudaFreeHost(h->p->pinned);
+  for (void* e : h->p->ev) cudaEventDestroy((cudaEvent_t)e);
   delete h->p;
   delete h;
 }
@@ -407,7 +421,15 @@ int tn_sample_amplitudes(tn_plan* h, const tn_buffers* b, const uint64_t* prefix
 int tn_report_json(const tn_plan* h, char* buf, size_t cap, size_t* needed) {
   if (!h) return fail(TN_E_INVALID, "NULL plan");
   TN_TRY({
-    std::string s = report_json(*h->p);
+    const Plan& p = *h->p;
+    std::vector<float> ms;
+    if (p.ev_valid) {
+      TN_CUDA(cudaEventSynchronize((cudaEvent_t)p.ev.back()));
+      ms.resize(p.ev.size() - 1);
+      for (size_t i = 0; i + 1 < p.ev.size(); ++i)
+        TN_CUDA(cudaEventElapsedTime(&ms[i], (cudaEvent_t)p.ev[i], (cudaEvent_t)p.ev[i + 1]));
+    }
+    std::string s = report_json(p, ms);
     if (needed) *needed = s.size() + 1;
     if (buf && cap) {
       size_t n = std::min(cap - 1, s.size());

@@ -40,7 +40,7 @@ class tn_plan_info(C.Structure):
                 ("n_stem_steps", C.c_uint64), ("n_permutes", C.c_uint64), ("n_common", C.c_uint64),
                 ("stem_flops", C.c_double), ("total_flops", C.c_double), ("stem_bytes_alg", C.c_double),
                 ("perm_bytes", C.c_double), ("n_open", C.c_uint64), ("max_stem_log2", C.c_uint64),
-                ("h2d_bytes", C.c_uint64), ("split_chunks", C.c_uint64)]
+                ("h2d_bytes", C.c_uint64), ("split_chunks", C.c_uint64), ("n_launches", C.c_uint64)]
 
 
 _lib = None
