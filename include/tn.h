@@ -68,7 +68,12 @@ typedef struct {
   uint64_t stem_capacity_bytes; /* bytes of EACH stem buffer the caller will lend; 0 = no check */
   int32_t split_log2;        /* split-type tail: 2^split_log2 chunks; -1 = auto
                                 (smallest power of two that fits), 0 = no split */
-  int32_t reserved[7];
+  int32_t layout_policy;     /* 2: each GEMM writes its output with the next step's contracted
+                                modes innermost (scatter epilogue, no permutation passes);
+                                1: output = kept ++ new plus a permutation pass when needed;
+                                0 (default): scatter when its stores are >= 64 B contiguous,
+                                otherwise as 1 */
+  int32_t reserved[6];
 } tn_config;
 
 /* Caller-owned device buffers lent to a call (P:18-22 double buffering). */
@@ -158,7 +163,8 @@ TN_API int tn_permute(void* d_dst, const void* d_src, int elem_bytes, int n, con
  * device from *d_in_max (max |real component| of A) and *d_b_bound (max column 1-norm of B_P)
  * so that |C| <= 2^14; e is added to *d_exp.  *d_out_max receives max |real component| of C as
  * float bits (atomicMax; caller zeroes it).  Any of the four scale pointers may be NULL: then
- * e = 0 and no max is recorded.  Requires K >= 8 and N >= 8 (powers of two); M any. */
+ * e = 0 and no max is recorded.  K, N powers of two, M any.  K >= 4 runs on tcgen05 (for N < 8,
+ * d_bp must hold 16 rows with rows 2N..15 zero); K < 4 runs on the SIMT kernel. */
 TN_API int tn_gemm_chalf(void* d_c, const void* d_a, const void* d_bp, uint64_t M, uint32_t K, uint32_t N,
                   const float* d_in_max, const float* d_b_bound, uint32_t* d_out_max, int* d_exp,
                   void* stream);

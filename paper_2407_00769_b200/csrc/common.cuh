@@ -40,6 +40,15 @@ struct GatherArgs {
   int64_t sn[kMaxModes];
 };
 
+// Output address map of a stem GEMM: C[m, n] lives at
+//   sum_j bit_j(m) * ms[j] + sum_j bit_j(n) * ns[j]   (complex elements)
+// identity != 0 means plain row-major [M][N] (ms[j] = N << j, ns[j] = 1 << j).
+struct OutMap {
+  int mbits, nbits, identity;
+  int64_t ms[kMaxModes];
+  int64_t ns[24];
+};
+
 struct PermArgs {
   int n;                         // total bits
   int u;                         // tile bits
@@ -65,19 +74,32 @@ void launch_c64_to_chalf(__half2* dst, const float2* src, uint64_t n, const uint
                          int* exp_slot, uint32_t* out_max_bits, cudaStream_t s);
 void launch_copy_c64(float2* dst, const float2* src, uint64_t n, cudaStream_t s);
 void launch_gemm_c64(float2* c, const float2* a, const float2* b, uint64_t M, uint32_t K, uint32_t N,
-                     cudaStream_t s);
+                     const OutMap* om, cudaStream_t s);
 void launch_gemm_chalf_simt(__half2* c, const __half2* a, const __half* bp, uint64_t M, uint32_t K,
                             uint32_t N, const float* in_max, const float* b_bound,
-                            uint32_t* out_max, int* exp_slot, cudaStream_t s);
+                            uint32_t* out_max, int* exp_slot, const OutMap* om, cudaStream_t s);
 void launch_gemm_chalf_tc(__half* c, const __half* a, const __half* bp, uint64_t M, uint32_t K2,
                           uint32_t N2, const float* in_max, const float* b_bound, uint32_t* out_max,
-                          int* exp_slot, cudaStream_t s);
+                          int* exp_slot, const OutMap* om, cudaStream_t s);
+OutMap identity_map(uint64_t M, uint32_t N);
 void launch_quant_int8(int8_t* codes, float* scales, float* zeros, const float* x, uint64_t n, int g,
                        cudaStream_t s);
 void launch_dequant_int8(float* y, const int8_t* codes, const float* scales, const float* zeros,
                          uint64_t n, int g, cudaStream_t s);
 
 // ---- device helpers ----
+__host__ __device__ inline int64_t outmap_m(const OutMap& o, uint64_t m) {
+  int64_t a = 0;
+  for (int j = 0; j < o.mbits; ++j)
+    if ((m >> j) & 1) a += o.ms[j];
+  return a;
+}
+__host__ __device__ inline int64_t outmap_n(const OutMap& o, uint64_t n) {
+  int64_t a = 0;
+  for (int j = 0; j < o.nbits; ++j)
+    if ((n >> j) & 1) a += o.ns[j];
+  return a;
+}
 // power-of-two exponent e so that prod * 2^e < 2^14 (prod > 0); 0 if prod == 0 or not finite.
 __host__ __device__ inline int scale_exp_for(float prod) {
   if (!(prod > 0.f) || !(prod < 3.0e38f)) return 0;

@@ -5,6 +5,8 @@
 // * gemm_chalf_simt: complex-half stem steps whose K or N is below the tcgen05 minimum
 //   (2K or 2N < 16): memory-bound, thread per output element, fp32 accumulation, B read from the
 //   same Eq. 6 padded B_P the tensor-core path uses, same power-of-two output scaling (C-A8).
+#include <cstring>
+
 #include "common.cuh"
 
 namespace tn {
@@ -12,7 +14,8 @@ namespace tn {
 constexpr int TM = 64, TN_ = 64, TK = 8;
 
 __global__ void __launch_bounds__(256) gemm_c64_kernel(float2* __restrict__ C, const float2* __restrict__ A,
-                                                       const float2* __restrict__ B, uint64_t M, int K, int N) {
+                                                       const float2* __restrict__ B, uint64_t M, int K, int N,
+                                                       const OutMap om, uint64_t m_base) {
   __shared__ float2 As[TK][TM + 1];
   __shared__ float2 Bs[TK][TN_];
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
@@ -57,16 +60,23 @@ __global__ void __launch_bounds__(256) gemm_c64_kernel(float2* __restrict__ C, c
   for (int i = 0; i < 4; ++i) {
     uint64_t gm = m0 + ty * 4 + i;
     if (gm >= M) continue;
+    const int64_t mo = om.identity ? 0 : outmap_m(om, m_base + gm);
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       int gn = n0 + tx + 16 * j;
-      if (gn < N) C[gm * N + gn] = acc[i][j];
+      if (gn < N) {
+        if (om.identity)
+          C[gm * N + gn] = acc[i][j];
+        else
+          C[mo + outmap_n(om, gn)] = acc[i][j];
+      }
     }
   }
 }
 
 void launch_gemm_c64(float2* c, const float2* a, const float2* b, uint64_t M, uint32_t K, uint32_t N,
-                     cudaStream_t s) {
+                     const OutMap* om_in, cudaStream_t s) {
+  OutMap om = om_in ? *om_in : identity_map(M, N);
   uint64_t gy = (M + TM - 1) / TM;
   if (gy > 65535ull * 1024) throw TnError{TN_E_UNSUPPORTED, "gemm_c64: M too large"};
   dim3 grid((N + TN_ - 1) / TN_, 1, 1);
@@ -76,57 +86,268 @@ void launch_gemm_c64(float2* c, const float2* a, const float2* b, uint64_t M, ui
     uint64_t ny = std::min<uint64_t>(maxy, gy - y0);
     grid.y = (unsigned)ny;
     uint64_t moff = y0 * TM;
-    gemm_c64_kernel<<<grid, 256, 0, s>>>(c + moff * N, a + moff * K, b, M - moff, (int)K, (int)N);
+    gemm_c64_kernel<<<grid, 256, 0, s>>>(om.identity ? c + moff * N : c, a + moff * K, b, M - moff, (int)K, (int)N, om,
+                                         moff);
   }
   TN_CUDA(cudaGetLastError());
 }
 
+OutMap identity_map(uint64_t M, uint32_t N) {
+  OutMap o;
+  memset(&o, 0, sizeof(o));
+  o.identity = 1;
+  int mb = 0, nb = 0;
+  while ((1ull << mb) < M) ++mb;
+  while ((1u << nb) < N) ++nb;
+  o.mbits = mb;
+  o.nbits = nb;
+  for (int j = 0; j < mb && j < kMaxModes; ++j) o.ms[j] = (int64_t)N << j;
+  for (int j = 0; j < nb && j < 24; ++j) o.ns[j] = (int64_t)1 << j;
+  return o;
+}
+
 __device__ __forceinline__ void atomic_max_pos2(uint32_t* addr, float v) { atomicMax(addr, __float_as_uint(v)); }
+
+// Memory-bound complex-half stem steps with small K*N (K <= 8 and N <= 4, or K <= 4): a CTA
+// streams a contiguous tile of T rows of A (16-byte vector loads) into shared memory, computes the
+// T x N outputs with B (complex fp32, from the Eq. 6 padded B_P) in shared memory, and writes them
+// in output order: consecutive threads -> consecutive outputs (coalesced; vector stores when the
+// output layout keeps the lowest n bits contiguous).
+constexpr int kTileCplx = 4096;   // complex elements of A per CTA tile
 
 __global__ void __launch_bounds__(256) gemm_chalf_simt_kernel(__half2* __restrict__ C, const __half2* __restrict__ A,
                                                               const __half* __restrict__ BP, uint64_t M, int K, int N,
-                                                              const float* in_max, const float* b_bound,
-                                                              uint32_t* out_max, int* exp_slot) {
+                                                              int rows_log, int run, const float* in_max,
+                                                              const float* b_bound, uint32_t* out_max, int* exp_slot,
+                                                              const OutMap om) {
+  __shared__ __align__(16) __half2 sA[kTileCplx];
+  __shared__ float2 sB[2048];
+  const bool smem_b = K * N <= 2048;
   int e = 0;
   if (in_max && b_bound) e = scale_exp_for(in_max[0] * b_bound[0]);
   if (exp_slot && blockIdx.x == 0 && threadIdx.x == 0) *exp_slot = e;
   const float sc = ldexpf(1.f, e);
-  const uint64_t total = M * (uint64_t)N;
   const int K2 = 2 * K;
+  for (int i = threadIdx.x; smem_b && i < K * N; i += blockDim.x) {
+    int k = i / N, n = i - k * N;
+    // B_P row (n,0) holds (Re b, -Im b); row (n,1) holds (Im b, Re b)
+    sB[i] = make_float2(__half2float(BP[(size_t)(2 * n) * K2 + 2 * k]), __half2float(BP[(size_t)(2 * n + 1) * K2 + 2 * k]));
+  }
+  const int T = 1 << rows_log;  // rows per tile
+  int nlog = 0;
+  while ((1 << nlog) < N) ++nlog;
+  const int vlog = run < 2 ? run : 2;  // vector of 2^vlog outputs when contiguous
+  const int V = 1 << vlog;
+  const uint64_t tiles = (M + T - 1) >> rows_log;
   float mx = 0.f;
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
-       i += (uint64_t)gridDim.x * blockDim.x) {
-    uint64_t m = i / N;
-    int n = (int)(i - m * N);
-    const __half2* a = A + m * K;
-    const __half* b0 = BP + (size_t)(2 * n) * K2;      // (Re b, -Im b) pairs
-    const __half* b1 = BP + (size_t)(2 * n + 1) * K2;  // (Im b,  Re b) pairs
-    float cr = 0.f, ci = 0.f;
-    for (int k = 0; k < K; ++k) {
-      float2 av = __half22float2(a[k]);
-      float br = __half2float(b0[2 * k]), bi = __half2float(b1[2 * k]);
-      cr = fmaf(av.x, br, fmaf(-av.y, bi, cr));
-      ci = fmaf(av.x, bi, fmaf(av.y, br, ci));
+  for (uint64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    const uint64_t m0 = tile << rows_log;
+    const int rows = (int)((M - m0) < (uint64_t)T ? (M - m0) : (uint64_t)T);
+    __syncthreads();  // sB ready / previous tile consumed
+    const int cnt = rows * K;
+    const uint4* src = reinterpret_cast<const uint4*>(A + m0 * K);
+    if ((cnt & 3) == 0) {
+      for (int i = threadIdx.x; i < (cnt >> 2); i += blockDim.x) reinterpret_cast<uint4*>(sA)[i] = src[i];
+    } else {
+      for (int i = threadIdx.x; i < cnt; i += blockDim.x) sA[i] = A[m0 * K + i];
     }
-    __half2 h = __floats2half2_rn(cr * sc, ci * sc);
-    C[i] = h;
-    float2 hf = __half22float2(h);
-    mx = fmaxf(mx, fmaxf(fabsf(hf.x), fabsf(hf.y)));
+    __syncthreads();
+    const int outs = rows * N;
+    for (int g = threadIdx.x; g < (outs >> vlog); g += blockDim.x) {
+      const int o0 = g << vlog;
+      const int r = o0 >> nlog, n0 = o0 & (N - 1);
+      uint32_t pk[4];
+      for (int v = 0; v < V; ++v) {
+        float cr = 0.f, ci = 0.f;
+        for (int k = 0; k < K; ++k) {
+          float2 a = __half22float2(sA[r * K + k]);
+          float2 b = smem_b ? sB[k * N + n0 + v]
+                            : make_float2(__half2float(BP[(size_t)(2 * (n0 + v)) * K2 + 2 * k]),
+                                          __half2float(BP[(size_t)(2 * (n0 + v) + 1) * K2 + 2 * k]));
+          cr = fmaf(a.x, b.x, fmaf(-a.y, b.y, cr));
+          ci = fmaf(a.x, b.y, fmaf(a.y, b.x, ci));
+        }
+        __half2 h = __floats2half2_rn(cr * sc, ci * sc);
+        float2 hf = __half22float2(h);
+        mx = fmaxf(mx, fmaxf(fabsf(hf.x), fabsf(hf.y)));
+        pk[v] = *reinterpret_cast<uint32_t*>(&h);
+      }
+      const uint64_t m = m0 + r;
+      int64_t base;
+      if (om.identity) {
+        base = (int64_t)(m * N + n0);
+      } else {
+        base = 0;
+        uint64_t mm = m;
+        while (mm) {
+          int j = __ffsll((long long)mm) - 1;
+          base += om.ms[j];
+          mm &= mm - 1;
+        }
+        for (int j = vlog; j < om.nbits; ++j)
+          if ((n0 >> j) & 1) base += om.ns[j];
+      }
+      uint32_t* dst = reinterpret_cast<uint32_t*>(C) + base;
+      if (V == 4)
+        *reinterpret_cast<uint4*>(dst) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+      else if (V == 2)
+        *reinterpret_cast<uint2*>(dst) = make_uint2(pk[0], pk[1]);
+      else
+        dst[0] = pk[0];
+    }
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
   if (out_max && (threadIdx.x & 31) == 0) atomic_max_pos2(out_max, mx);
 }
 
+// Row-streaming variant for K <= 8 and N <= 16: one thread per row of A (K complex-half = up to
+// 32 contiguous bytes, vector loads), N outputs in registers, stored as one contiguous run when the
+// output layout keeps the row's outputs contiguous.  No shared-memory round trip for A, no
+// barriers: consecutive threads read consecutive rows (fully coalesced) and the grid-stride loop
+// keeps many rows in flight.
+template <int K, int N>
+__global__ void __launch_bounds__(256) gemm_chalf_rows_kernel(uint32_t* __restrict__ C, const __half2* __restrict__ A,
+                                                              const __half* __restrict__ BP, uint64_t M, int contiguous,
+                                                              const float* in_max, const float* b_bound,
+                                                              uint32_t* out_max, int* exp_slot, const OutMap om) {
+  __shared__ float2 sB[K * N];
+  int e = 0;
+  if (in_max && b_bound) e = scale_exp_for(in_max[0] * b_bound[0]);
+  if (exp_slot && blockIdx.x == 0 && threadIdx.x == 0) *exp_slot = e;
+  const float sc = ldexpf(1.f, e);
+  for (int i = threadIdx.x; i < K * N; i += blockDim.x) {
+    int k = i / N, n = i - k * N;
+    sB[i] = make_float2(__half2float(BP[(size_t)(2 * n) * 2 * K + 2 * k]), __half2float(BP[(size_t)(2 * n + 1) * 2 * K + 2 * k]));
+  }
+  __syncthreads();
+  float mx = 0.f;
+  for (uint64_t m = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; m < M; m += (uint64_t)gridDim.x * blockDim.x) {
+    float2 a[K];
+    const __half2* ar = A + m * K;
+    if constexpr (K >= 4) {
+#pragma unroll
+      for (int q = 0; q < K / 4; ++q) {
+        uint4 v = __ldg(reinterpret_cast<const uint4*>(ar) + q);
+        a[4 * q] = __half22float2(*reinterpret_cast<__half2*>(&v.x));
+        a[4 * q + 1] = __half22float2(*reinterpret_cast<__half2*>(&v.y));
+        a[4 * q + 2] = __half22float2(*reinterpret_cast<__half2*>(&v.z));
+        a[4 * q + 3] = __half22float2(*reinterpret_cast<__half2*>(&v.w));
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < K; ++k) a[k] = __half22float2(ar[k]);
+    }
+    uint32_t out[N];
+#pragma unroll
+    for (int n = 0; n < N; ++n) {
+      float cr = 0.f, ci = 0.f;
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        float2 b = sB[k * N + n];
+        cr = fmaf(a[k].x, b.x, fmaf(-a[k].y, b.y, cr));
+        ci = fmaf(a[k].x, b.y, fmaf(a[k].y, b.x, ci));
+      }
+      __half2 h = __floats2half2_rn(cr * sc, ci * sc);
+      float2 hf = __half22float2(h);
+      mx = fmaxf(mx, fmaxf(fabsf(hf.x), fabsf(hf.y)));
+      out[n] = *reinterpret_cast<uint32_t*>(&h);
+    }
+    int64_t base;
+    if (om.identity) {
+      base = (int64_t)(m * N);
+    } else {
+      base = 0;
+      uint64_t mm = m;
+      while (mm) {
+        int j = __ffsll((long long)mm) - 1;
+        base += om.ms[j];
+        mm &= mm - 1;
+      }
+    }
+    uint32_t* dst = C + base;
+    if (contiguous) {
+      if constexpr (N >= 4) {
+#pragma unroll
+        for (int q = 0; q < N / 4; ++q)
+          reinterpret_cast<uint4*>(dst)[q] = make_uint4(out[4 * q], out[4 * q + 1], out[4 * q + 2], out[4 * q + 3]);
+      } else if constexpr (N == 2) {
+        *reinterpret_cast<uint2*>(dst) = make_uint2(out[0], out[1]);
+      } else {
+        dst[0] = out[0];
+      }
+    } else {
+#pragma unroll
+      for (int n = 0; n < N; ++n) {
+        int64_t o = 0;
+        for (int j = 0; j < om.nbits; ++j)
+          if ((n >> j) & 1) o += om.ns[j];
+        dst[o] = out[n];
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if (out_max && (threadIdx.x & 31) == 0) atomic_max_pos2(out_max, mx);
+}
+
+template <int K, int N>
+static void launch_rows(__half2* c, const __half2* a, const __half* bp, uint64_t M, int contiguous, const float* in_max,
+                        const float* b_bound, uint32_t* out_max, int* exp_slot, const OutMap& om, cudaStream_t s) {
+  uint64_t blocks = std::min<uint64_t>((M + 255) / 256, 148ull * 16);
+  if (blocks == 0) blocks = 1;
+  gemm_chalf_rows_kernel<K, N><<<(unsigned)blocks, 256, 0, s>>>(reinterpret_cast<uint32_t*>(c), a, bp, M, contiguous,
+                                                                in_max, b_bound, out_max, exp_slot, om);
+}
+
+template <int K>
+static bool dispatch_rows_n(uint32_t N, __half2* c, const __half2* a, const __half* bp, uint64_t M, int contiguous,
+                            const float* in_max, const float* b_bound, uint32_t* out_max, int* exp_slot,
+                            const OutMap& om, cudaStream_t s) {
+  switch (N) {
+    case 1: launch_rows<K, 1>(c, a, bp, M, contiguous, in_max, b_bound, out_max, exp_slot, om, s); return true;
+    case 2: launch_rows<K, 2>(c, a, bp, M, contiguous, in_max, b_bound, out_max, exp_slot, om, s); return true;
+    case 4: launch_rows<K, 4>(c, a, bp, M, contiguous, in_max, b_bound, out_max, exp_slot, om, s); return true;
+    case 8: launch_rows<K, 8>(c, a, bp, M, contiguous, in_max, b_bound, out_max, exp_slot, om, s); return true;
+    case 16: launch_rows<K, 16>(c, a, bp, M, contiguous, in_max, b_bound, out_max, exp_slot, om, s); return true;
+  }
+  return false;
+}
+
 void launch_gemm_chalf_simt(__half2* c, const __half2* a, const __half* bp, uint64_t M, uint32_t K, uint32_t N,
                             const float* in_max, const float* b_bound, uint32_t* out_max, int* exp_slot,
-                            cudaStream_t s) {
-  uint64_t total = M * (uint64_t)N;
-  uint64_t blocks = (total + 255) / 256;
-  if (blocks > 148 * 16) blocks = 148 * 16;
+                            const OutMap* om_in, cudaStream_t s) {
+  if (K > (uint32_t)kTileCplx) throw TnError{TN_E_UNSUPPORTED, "SIMT complex-half GEMM: K > 4096"};
+  OutMap om = om_in ? *om_in : identity_map(M, N);
+  int nlog = 0;
+  while ((1u << nlog) < N) ++nlog;
+  int run = 0;
+  if (om.identity)
+    run = nlog;
+  else
+    while (run < om.nbits && om.ns[run] == ((int64_t)1 << run)) ++run;
+  if (K <= 8 && N <= 16) {
+    const int contiguous = run >= nlog;
+    bool ok = false;
+    switch (K) {
+      case 1: ok = dispatch_rows_n<1>(N, c, a, bp, M, contiguous, in_max, b_bound, out_max, exp_slot, om, s); break;
+      case 2: ok = dispatch_rows_n<2>(N, c, a, bp, M, contiguous, in_max, b_bound, out_max, exp_slot, om, s); break;
+      case 4: ok = dispatch_rows_n<4>(N, c, a, bp, M, contiguous, in_max, b_bound, out_max, exp_slot, om, s); break;
+      case 8: ok = dispatch_rows_n<8>(N, c, a, bp, M, contiguous, in_max, b_bound, out_max, exp_slot, om, s); break;
+    }
+    if (ok) {
+      TN_CUDA(cudaGetLastError());
+      return;
+    }
+  }
+  // rows per tile: A tile of <= kTileCplx complex, at least one row
+  int rows_log = 0;
+  while ((2ull << rows_log) * K <= (uint64_t)kTileCplx && (2ull << rows_log) <= 1024) ++rows_log;
+  uint64_t tiles = (M + (1ull << rows_log) - 1) >> rows_log;
+  uint64_t blocks = std::min<uint64_t>(tiles, 148ull * 8);
   if (blocks == 0) blocks = 1;
-  gemm_chalf_simt_kernel<<<(unsigned)blocks, 256, 0, s>>>(c, a, bp, M, (int)K, (int)N, in_max, b_bound, out_max,
-                                                           exp_slot);
+  gemm_chalf_simt_kernel<<<(unsigned)blocks, 256, 0, s>>>(c, a, bp, M, (int)K, (int)N, rows_log, run, in_max, b_bound,
+                                                           out_max, exp_slot, om);
   TN_CUDA(cudaGetLastError());
 }
 

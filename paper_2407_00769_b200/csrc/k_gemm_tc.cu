@@ -128,18 +128,61 @@ struct Cfg {
   static constexpr int kBBytes = BN * BK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kCSub = (BN + 63) / 64;            // 64-column store subtiles
-  static constexpr int kCBytes = kCSub * BM * 128;
+  static constexpr int kCTma = kCSub * BM * 128;          // 128B-swizzled staging for TMA stores
+  static constexpr int kCBytes = kCTma;
   static constexpr int kStagesRaw = (200 * 1024 - kCBytes) / kStageBytes;
   static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
   static constexpr int kSmem = kStages * kStageBytes + kCBytes + 1024 /*align*/ + 256 /*barriers*/;
   static constexpr uint32_t kIdesc = (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
 };
 
+}  // namespace tc
+
+// Scatter epilogue description (output layout = any bit placement of m and n, see OutMap):
+// C[m, n] goes to sum_j bit_j(m) ms[j] + sum_j bit_j(n) ns[j] (complex elements).  Each epilogue
+// thread owns one row of the tile and stores its values straight from registers in contiguous
+// vectors along the lowest n bits whose strides are 1, 2, 4, ... (no shared-memory staging).
+// Tile rasterisation for scatter layouts: tile index bit b sets bit vbit_idx[b] of the m-block
+// (vbit_is_m[b] = 1) or of the n-block; bits are ordered by output stride so tiles that fill the
+// same output lines run concurrently on neighbouring CTAs and their partial sectors merge in L2.
+struct ScatterArgs {
+  int on;
+  int mbits, nbits;
+  int nv;
+  int8_t vbit_is_m[64];
+  int8_t vbit_idx[64];
+  int64_t ms[kMaxModes];
+  int64_t ns[24];
+};
+
+__device__ __forceinline__ void tile_coords(const ScatterArgs& sa, uint32_t t, uint32_t num_n, int BMv, int BNv,
+                                            int& m0, int& n0) {
+  if (sa.on) {
+    uint32_t mb = 0, nb = 0;
+    for (int b = 0; b < sa.nv; ++b)
+      if ((t >> b) & 1) {
+        if (sa.vbit_is_m[b])
+          mb |= 1u << sa.vbit_idx[b];
+        else
+          nb |= 1u << sa.vbit_idx[b];
+      }
+    m0 = (int)(mb * BMv);
+    n0 = (int)(nb * BNv);
+  } else {
+    m0 = (int)((t / num_n) * BMv);
+    n0 = (int)((t % num_n) * BNv);
+  }
+}
+
+namespace tc {
+
 template <int BN>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_chalf_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                          const __grid_constant__ CUtensorMap tmC, uint32_t num_m, uint32_t num_n, int K2,
-                         const float* in_max, const float* b_bound, uint32_t* out_max, int* exp_slot) {
+                         const float* in_max, const float* b_bound, uint32_t* out_max, int* exp_slot,
+                         const __grid_constant__ ScatterArgs sc_args, uint32_t* out_scatter, uint64_t rows,
+                         uint32_t n_cols) {
   using C = Cfg<BN>;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
@@ -186,8 +229,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       int s = 0;
       uint32_t ph = 0;
       for (uint32_t t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-        const int m0 = (int)((t / num_n) * BM);
-        const int n0 = (int)((t % num_n) * BN);
+        int m0, n0;
+        tile_coords(sc_args, t, num_n, BM, BN, m0, n0);
         for (int kb = 0; kb < num_k; ++kb) {
           mbar_wait(&empty[s], ph ^ 1);
           mbar_expect_tx(&full[s], C::kStageBytes);
@@ -240,32 +283,70 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (exp_slot && blockIdx.x == 0 && etid == 0) *exp_slot = e;
     const float sc = ldexpf(1.f, e);
     float mx = 0.f;
+    const bool scat = sc_args.on != 0;
+    // scatter mode: run = number of lowest n bits whose output strides are 1, 2, 4, ...: each
+    // thread stores its row's values in contiguous vectors of 2^run complex (<= 16)
+    int run = 0;
+    if (scat)
+      while (run < 4 && run < sc_args.nbits && sc_args.ns[run] == ((int64_t)1 << run)) ++run;
     uint32_t i = 0;
     for (uint32_t t = blockIdx.x; t < num_tiles; t += gridDim.x, ++i) {
       const uint32_t acc = i & 1, aph = (i >> 1) & 1;
-      const int m0 = (int)((t / num_n) * BM);
-      const int n0 = (int)((t % num_n) * BN);
+      int m0, n0;
+      tile_coords(sc_args, t, num_n, BM, BN, m0, n0);
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
-      // staging buffer free? (previous tile's TMA stores have read it)
+      // staging buffer free? (previous tile's TMA stores / scatter reads have finished)
       if (etid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
       named_bar(1, 128);
       const uint32_t taddr = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * 256;
+      int64_t row_off = 0;
+      const bool row_ok = (uint64_t)(m0 + row) < rows;
+      if (scat) {
+        const uint64_t mg = (uint64_t)(m0 + row);
+        for (int j = 0; j < sc_args.mbits; ++j)
+          if ((mg >> j) & 1) row_off += sc_args.ms[j];
+      }
 #pragma unroll 1
       for (int c = 0; c < BN; c += 32) {
         uint32_t r[32];
         tmem_ld_32x32b_x32(taddr + c, r);
         tmem_ld_wait();
         uint32_t pk[16];
+        // complex values of this 32-column chunk that exist (N < 8 pads B_P with zero rows)
+        const int nleft = (int)n_cols - ((n0 + c) >> 1);
+        const int nvalid = nleft < 16 ? (nleft > 0 ? nleft : 0) : 16;
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
           float x0 = __uint_as_float(r[2 * j]) * sc, x1 = __uint_as_float(r[2 * j + 1]) * sc;
           __half2 h = __floats2half2_rn(x0, x1);
           float2 hf = __half22float2(h);
-          if (BN >= 32 || 2 * j < BN - c) mx = fmaxf(mx, fmaxf(fabsf(hf.x), fabsf(hf.y)));
+          if (j < nvalid) mx = fmaxf(mx, fmaxf(fabsf(hf.x), fabsf(hf.y)));
           pk[j] = *reinterpret_cast<uint32_t*>(&h);
         }
-        if (c < BN) {
+        if (scat) {
+          if (row_ok) {
+            const uint64_t nb = (uint64_t)((n0 + c) >> 1);
+            const int V = 1 << run;
+#pragma unroll 1
+            for (int q = 0; q < nvalid; q += V) {
+              int64_t off = row_off;
+              const uint64_t ng = nb + q;
+              for (int j = run; j < sc_args.nbits; ++j)
+                if ((ng >> j) & 1) off += sc_args.ns[j];
+              uint32_t* dst = out_scatter + off;
+              if (V >= 4) {
+#pragma unroll
+                for (int v = 0; v < 16; v += 4)
+                  if (v < V) *reinterpret_cast<uint4*>(dst + v) = make_uint4(pk[q + v], pk[q + v + 1], pk[q + v + 2], pk[q + v + 3]);
+              } else if (V == 2) {
+                *reinterpret_cast<uint2*>(dst) = make_uint2(pk[q], pk[q + 1]);
+              } else {
+                *dst = pk[q];
+              }
+            }
+          }
+        } else {
           unsigned char* sub = sC + (c >> 6) * (BM * 128) + row * 128;
           const int cb = (c & 63) >> 3;  // first 16-byte chunk of these 32 columns
 #pragma unroll
@@ -281,12 +362,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       // accumulator drained -> MMA may reuse it
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      named_bar(1, 128);
-      if (etid == 0) {
+      if (!scat) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        named_bar(1, 128);
+        if (etid == 0) {
 #pragma unroll 1
-        for (int j = 0; j < C::kCSub; ++j) tma_store_2d(&tmC, sC + j * (BM * 128), n0 + j * 64, m0);
-        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          for (int j = 0; j < C::kCSub; ++j) tma_store_2d(&tmC, sC + j * (BM * 128), n0 + j * 64, m0);
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
       }
     }
     if (etid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
@@ -344,15 +427,56 @@ static int num_sms() {
 }
 
 template <int BN>
-static void launch_bn(__half* c, const __half* a, const __half* bp, uint64_t M, uint32_t K2, uint32_t N2,
-                      const float* in_max, const float* b_bound, uint32_t* out_max, int* exp_slot, cudaStream_t s) {
+static void launch_bn(__half* c, const __half* a, const __half* bp, uint64_t M, uint32_t K2, uint32_t N2_real,
+                      const float* in_max, const float* b_bound, uint32_t* out_max, int* exp_slot, const OutMap* om,
+                      cudaStream_t s) {
+  const uint32_t N2 = std::max<uint32_t>(N2_real, 16);  // B_P has at least 16 (zero-padded) rows
   using C = tc::Cfg<BN>;
   static bool attr = false;
   if (!attr) {
     TN_CUDA(cudaFuncSetAttribute(tc::gemm_chalf_tc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
     attr = true;
   }
-  CUtensorMap mb = make_map_2d(bp, K2, N2, tc::BK, BN);
+  ScatterArgs sa;
+  memset(&sa, 0, sizeof(sa));
+  const uint32_t n_cols = N2_real / 2;
+  OutMap ident;
+  if (N2_real < 16 && (!om || om->identity)) {  // TMA stores need 16-byte rows: store directly
+    ident = identity_map(M, N2_real / 2);
+    om = &ident;
+    ident.identity = 0;
+  }
+  if (om && !om->identity) {
+    sa.on = 1;
+    sa.mbits = om->mbits;
+    sa.nbits = om->nbits;
+    {
+      // m-block bits (m bits >= 7) and n-block bits (complex n bits >= log2(BN/2)), by output stride
+      int cb = 0;
+      while ((1 << cb) < BN / 2) ++cb;
+      struct VB {
+        int64_t stride;
+        int is_m, idx;
+      };
+      std::vector<VB> vb;
+      // only the m bits inside one launch chunk (chunks cover 2^30 rows or fewer, see below)
+      const uint64_t chunk_rows = std::min<uint64_t>(1ull << 30, ((1ull << 31) / (N2 / BN)) * tc::BM);
+      int cl2 = 0;
+      while ((1ull << cl2) < chunk_rows) ++cl2;
+      for (int j = 7; j < std::min(om->mbits, cl2); ++j) vb.push_back({om->ms[j], 1, j - 7});
+      for (int j = cb; j < om->nbits; ++j) vb.push_back({om->ns[j], 0, j - cb});
+      std::stable_sort(vb.begin(), vb.end(), [](const VB& x, const VB& y) { return x.stride < y.stride; });
+      sa.nv = (int)vb.size();
+      if (sa.nv > 31) throw TnError{TN_E_UNSUPPORTED, "too many tile bits"};
+      for (int b = 0; b < sa.nv; ++b) {
+        sa.vbit_is_m[b] = (int8_t)vb[b].is_m;
+        sa.vbit_idx[b] = (int8_t)vb[b].idx;
+      }
+    }
+    for (int j = 0; j < kMaxModes; ++j) sa.ms[j] = om->ms[j];
+    for (int j = 0; j < 24; ++j) sa.ns[j] = om->ns[j];
+  }
+  CUtensorMap mb = make_map_2d(bp, K2, N2_real, tc::BK, BN);  // rows >= 2N: TMA zero fill
   // TMA coordinates are int32: process M in chunks of at most 2^30 rows
   const uint32_t num_n = N2 / BN;
   const uint64_t chunk = std::min<uint64_t>(1ull << 30, ((1ull << 31) / num_n) * tc::BM);
@@ -360,28 +484,30 @@ static void launch_bn(__half* c, const __half* a, const __half* bp, uint64_t M, 
     uint64_t mm = std::min<uint64_t>(chunk, M - m_off);
     CUtensorMap ma = make_map_2d(a + m_off * K2, K2, mm, tc::BK, tc::BM);
     CUtensorMap mc = make_map_2d(c + m_off * N2, N2, mm, 64, tc::BM);
+    uint32_t* out_sc = reinterpret_cast<uint32_t*>(c) + (sa.on ? outmap_m(*om, m_off) : 0);
     uint32_t num_m = (uint32_t)((mm + tc::BM - 1) / tc::BM);
     uint64_t tiles = (uint64_t)num_m * num_n;
     int grid = (int)std::min<uint64_t>(tiles, (uint64_t)num_sms());
     // the exponent is recorded once (first chunk); later chunks reuse the same inputs
-    tc::gemm_chalf_tc_kernel<BN><<<grid, tc::kThreads, C::kSmem, s>>>(ma, mb, mc, num_m, num_n, (int)K2, in_max,
-                                                                      b_bound, out_max, m_off ? nullptr : exp_slot);
+    tc::gemm_chalf_tc_kernel<BN><<<grid, tc::kThreads, C::kSmem, s>>>(
+        ma, mb, mc, num_m, num_n, (int)K2, in_max, b_bound, out_max, m_off ? nullptr : exp_slot, sa, out_sc, mm,
+        n_cols);
     TN_CUDA(cudaGetLastError());
   }
 }
 
 void launch_gemm_chalf_tc(__half* c, const __half* a, const __half* bp, uint64_t M, uint32_t K2, uint32_t N2,
                           const float* in_max, const float* b_bound, uint32_t* out_max, int* exp_slot,
-                          cudaStream_t s) {
-  if (K2 < 16 || N2 < 16 || (K2 & (K2 - 1)) || (N2 & (N2 - 1)))
-    throw TnError{TN_E_INVALID, "tcgen05 GEMM needs power-of-two 2K, 2N >= 16"};
+                          const OutMap* om, cudaStream_t s) {
+  if (K2 < 8 || N2 < 2 || (K2 & (K2 - 1)) || (N2 & (N2 - 1)))
+    throw TnError{TN_E_INVALID, "tcgen05 GEMM needs power-of-two 2K >= 8, 2N >= 2"};
   if (M == 0) return;
-  switch (N2) {
-    case 16: launch_bn<16>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, s); break;
-    case 32: launch_bn<32>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, s); break;
-    case 64: launch_bn<64>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, s); break;
-    case 128: launch_bn<128>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, s); break;
-    default: launch_bn<256>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, s); break;
+  switch (N2 < 16 ? 16 : N2) {
+    case 16: launch_bn<16>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s); break;
+    case 32: launch_bn<32>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s); break;
+    case 64: launch_bn<64>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s); break;
+    case 128: launch_bn<128>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s); break;
+    default: launch_bn<256>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s); break;
   }
 }
 

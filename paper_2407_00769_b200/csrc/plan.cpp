@@ -224,9 +224,44 @@ Plan* load_plan(const char* json, size_t len, const tn_config* cfg_in) {
   };
 
   // ---- steps
+  // Layout policy.  layout_policy 0 (default): every GEMM writes its output with
+  // the modes the NEXT step contracts as the innermost block (scatter epilogue), so each stem
+  // operand is read as stored (K-major) and no standalone permutation pass is needed; the other
+  // modes are ordered by next use, furthest first.  layout_policy 1: output = kept ++ new and a
+  // permutation pass whenever R_i is not innermost (the classic "reorder then GEMM").
+  const int policy = cfg.layout_policy;
   const int eb = (cfg.dtype == TN_CHALF) ? 4 : 8;
   uint64_t smax = 0;
   if (entry_idx >= 0) {
+    // branch label sets and contracted sets R_s (stem ∩ branch) along the stem
+    std::vector<std::set<int>> Rsets(step_nodes.size());
+    {
+      std::set<int> cur(p.nodes[p.stem_entry].labels.begin(), p.nodes[p.stem_entry].labels.end());
+      int prev = p.stem_entry;
+      for (size_t s = 0; s < step_nodes.size(); ++s) {
+        const Node& n = p.nodes[step_nodes[s]];
+        int br = (n.u == prev) ? n.v : n.u;
+        for (int l : p.nodes[br].labels) (cur.count(l) ? Rsets[s] : cur).insert(l);
+        for (int l : Rsets[s]) cur.erase(l);
+        prev = step_nodes[s];
+      }
+    }
+    auto by_next_use = [&](std::vector<int>& v) {
+      std::stable_sort(v.begin(), v.end(), [&](int a, int b) { return nu(a) > nu(b); });
+    };
+    // order a set of labels as [others by next use desc] ++ [those in `inner`]
+    auto order_with_inner = [&](const std::vector<int>& all, const std::set<int>& inner) {
+      std::vector<int> outer, in;
+      for (int l : all) (inner.count(l) ? in : outer).push_back(l);
+      by_next_use(outer);
+      outer.insert(outer.end(), in.begin(), in.end());
+      return outer;
+    };
+    if ((policy == 0 || policy == 2) && !step_nodes.empty()) {
+      // the entry is a common node whose device layout we choose: R_1 innermost
+      Node& e = p.nodes[p.stem_entry];
+      e.labels = order_with_inner(e.labels, Rsets[0]);
+    }
     std::vector<int> L = p.nodes[p.stem_entry].labels;
     smax = 1ull << L.size();
     int prev = p.stem_entry;
@@ -245,7 +280,7 @@ Plan* load_plan(const char* json, size_t len, const tn_config* cfg_in) {
       for (size_t j = 0; j < R.size(); ++j)
         if (!bs.count(L[L.size() - R.size() + j])) suffix = false;
       if (!suffix) {
-        std::stable_sort(kept.begin(), kept.end(), [&](int a, int b) { return nu(a) > nu(b); });
+        by_next_use(kept);
         std::vector<int> PL = kept;
         PL.insert(PL.end(), R.begin(), R.end());
         st.perm = true;
@@ -257,27 +292,84 @@ Plan* load_plan(const char* json, size_t len, const tn_config* cfg_in) {
       std::vector<int> newl;
       for (int l : B)
         if (std::find(R.begin(), R.end(), l) == R.end()) newl.push_back(l);
-      std::stable_sort(newl.begin(), newl.end(), [&](int a, int b) { return nu(a) > nu(b); });
+      std::vector<int> out;
+      bool scatter = false;
+      if (policy == 0 || policy == 2) {
+        if (s + 1 == step_nodes.size()) {
+          out = p.open;  // the last step writes the result directly in output order
+          scatter = true;
+        } else {
+          // [rest by next use] ++ [kept ∩ R_next] ++ [new ∩ R_next]  (new innermost)
+          const std::set<int>& Rn = Rsets[s + 1];
+          std::vector<int> rest, kl, nlo, nhi;
+          for (int l : kept) (Rn.count(l) ? kl : rest).push_back(l);
+          for (int l : newl) (Rn.count(l) ? nlo : nhi).push_back(l);
+          // the scatter epilogue stores contiguous runs along the innermost new modes: worth it
+          // only when a thread's 16 consecutive outputs are contiguous (>= 4 new modes innermost)
+          // or no permutation would be needed anyway
+          if (policy == 2 || nlo.size() >= 4 || kl.empty() || nhi.empty()) {
+            rest.insert(rest.end(), nhi.begin(), nhi.end());
+            by_next_use(rest);
+            out = rest;
+            out.insert(out.end(), kl.begin(), kl.end());
+            out.insert(out.end(), nlo.begin(), nlo.end());
+            scatter = true;
+          } else {
+            // identity output (TMA store): kept ++ [new by next use, new ∩ R_next innermost]
+            by_next_use(nhi);
+            out = kept;
+            out.insert(out.end(), nhi.begin(), nhi.end());
+            out.insert(out.end(), nlo.begin(), nlo.end());
+          }
+        }
+        (void)scatter;
+        // B's N order follows the output order of the new labels (outer -> inner)
+        std::vector<int> nord;
+        for (int l : out)
+          if (std::find(newl.begin(), newl.end(), l) != newl.end()) nord.push_back(l);
+        newl = nord;
+      } else {
+        by_next_use(newl);
+        out = kept;
+        out.insert(out.end(), newl.begin(), newl.end());
+      }
       st.R = R;
       st.kept = kept;
       st.newl = newl;
       st.mlog = (int)kept.size();
       st.klog = (int)R.size();
       st.nlog = (int)newl.size();
-      st.out_layout = kept;
-      st.out_layout.insert(st.out_layout.end(), newl.begin(), newl.end());
-      st.tensor_core = (cfg.dtype == TN_CHALF) && st.klog >= 3 && st.nlog >= 3;
+      st.out_layout = out;
+      // tcgen05 when the tile carries enough work; small K*N steps go to the tiled SIMT kernel
+      st.tensor_core = (cfg.dtype == TN_CHALF) && st.klog >= 2 &&
+                       ((st.klog >= 3 && st.nlog >= 3) || st.klog >= 4 || st.klog + st.nlog > 11);
       {
         std::set<int> chk(st.out_layout.begin(), st.out_layout.end());
         std::set<int> want(n.labels.begin(), n.labels.end());
-        if (chk != want) throw err(TN_E_INVALID, "internal: step output labels mismatch");
+        if (chk != want || chk.size() != st.out_layout.size())
+          throw err(TN_E_INVALID, "internal: step output labels mismatch");
+      }
+      // output address map: bit j of m (kept[mlog-1-j]) and of n (newl[nlog-1-j])
+      {
+        const int r = (int)out.size();
+        auto stride_of = [&](int l) {
+          int q = (int)(std::find(out.begin(), out.end(), l) - out.begin());
+          return (int64_t)1 << (r - 1 - q);
+        };
+        st.m_stride.resize(st.mlog);
+        st.n_stride.resize(st.nlog);
+        for (int j = 0; j < st.mlog; ++j) st.m_stride[j] = stride_of(kept[st.mlog - 1 - j]);
+        for (int j = 0; j < st.nlog; ++j) st.n_stride[j] = stride_of(newl[st.nlog - 1 - j]);
+        std::vector<int> ident = kept;
+        ident.insert(ident.end(), newl.begin(), newl.end());
+        st.out_identity = (ident == out);
       }
       if (st.klog > 16 || st.nlog > 16) throw err(TN_E_UNSUPPORTED, "stem operand with K or N > 2^16");
       smax = std::max<uint64_t>(smax, 1ull << (st.mlog + st.klog));
       smax = std::max<uint64_t>(smax, 1ull << (st.mlog + st.nlog));
       double M = std::ldexp(1.0, st.mlog), K = std::ldexp(1.0, st.klog), N = std::ldexp(1.0, st.nlog);
       p.stem_flops += 8.0 * M * K * N;
-      p.stem_bytes_alg += eb * (M * K + M * N) + (cfg.dtype == TN_CHALF ? 8.0 * K * N : 8.0 * K * N);
+      p.stem_bytes_alg += eb * (M * K + M * N) + 8.0 * K * N;
       if (st.perm) {
         p.perm_bytes += 2.0 * eb * M * K;
         p.n_permutes++;
@@ -322,7 +414,8 @@ Plan* load_plan(const char* json, size_t len, const tn_config* cfg_in) {
     off += align_up(8 * kn, 1024);
     if (cfg.dtype == TN_CHALF) {
       st.b_off = off;
-      off += align_up(8 * kn, 1024);  // fp16 [2N][2K]
+      // fp16 [max(2N, 16)][2K]: rows beyond 2N are zero (tcgen05 N >= 16)
+      off += align_up(std::max<uint64_t>(8 * kn, 64ull << st.klog), 1024);
     } else {
       st.b_off = st.b_tmp_off;
     }

@@ -162,6 +162,8 @@ void prepare_b(const Plan& p, unsigned char* W, uint64_t slice_id, const Scratch
     if (p.cfg.dtype == TN_CHALF) {
       const_cast<Plan&>(p).launches += 2;
       uint64_t kn = 1ull << (st.klog + st.nlog);
+      if (st.nlog < 3)  // zero the padding rows of B_P (tcgen05 needs N >= 16 real columns)
+        TN_CUDA(cudaMemsetAsync(W + st.b_off, 0, 64ull << st.klog, s));
       launch_max_abs_f32(reinterpret_cast<const float*>(g.dst), 2 * kn, &sc.b_max[i], s);
       launch_pad_b(reinterpret_cast<__half*>(W + st.b_off), g.dst, st.klog, st.nlog, &sc.b_max[i], &sc.b_bound[i],
                    &sc.exps[1 + 2 * i], s);
@@ -250,21 +252,28 @@ void stem_contract(Plan& p, const tn_buffers* b, uint64_t slice_id, cudaStream_t
     rec(2 + 2 * i);
     const uint64_t M = 1ull << st.mlog;
     const uint32_t K = 1u << st.klog, N = 1u << st.nlog;
+    OutMap om;
+    memset(&om, 0, sizeof(om));
+    om.identity = st.out_identity ? 1 : 0;
+    om.mbits = st.mlog;
+    om.nbits = st.nlog;
+    for (int j = 0; j < st.mlog; ++j) om.ms[j] = st.m_stride[j];
+    for (int j = 0; j < st.nlog; ++j) om.ns[j] = st.n_stride[j];
     if (p.cfg.dtype == TN_CHALF) {
       const float* in_max = &sc.max_slot[i];
       uint32_t* out_max = reinterpret_cast<uint32_t*>(&sc.max_slot[i + 1]);
       if (st.tensor_core)
         launch_gemm_chalf_tc(reinterpret_cast<__half*>(b->d_stem[1 - cur]), reinterpret_cast<const __half*>(b->d_stem[cur]),
                              reinterpret_cast<const __half*>(W + st.b_off), M, 2 * K, 2 * N, in_max, &sc.b_bound[i],
-                             out_max, &sc.exps[2 + 2 * i], s);
+                             out_max, &sc.exps[2 + 2 * i], &om, s);
       else
         launch_gemm_chalf_simt(reinterpret_cast<__half2*>(b->d_stem[1 - cur]),
                                reinterpret_cast<const __half2*>(b->d_stem[cur]),
                                reinterpret_cast<const __half*>(W + st.b_off), M, K, N, in_max, &sc.b_bound[i], out_max,
-                               &sc.exps[2 + 2 * i], s);
+                               &sc.exps[2 + 2 * i], &om, s);
     } else {
       launch_gemm_c64(reinterpret_cast<float2*>(b->d_stem[1 - cur]), reinterpret_cast<const float2*>(b->d_stem[cur]),
-                      reinterpret_cast<const float2*>(W + st.b_off), M, K, N, s);
+                      reinterpret_cast<const float2*>(W + st.b_off), M, K, N, &om, s);
     }
     ++p.launches;
     cur = 1 - cur;
@@ -458,18 +467,18 @@ int tn_gemm_chalf(void* d_c, const void* d_a, const void* d_bp, uint64_t M, uint
   TN_TRY({
     const float* im = (d_in_max && d_b_bound) ? d_in_max : nullptr;
     const float* bb = (d_in_max && d_b_bound) ? d_b_bound : nullptr;
-    if (K >= 8 && N >= 8)
+    if (K >= 4)
       launch_gemm_chalf_tc((__half*)d_c, (const __half*)d_a, (const __half*)d_bp, M, 2 * K, 2 * N, im, bb, d_out_max,
-                           d_exp, (cudaStream_t)stream);
+                           d_exp, nullptr, (cudaStream_t)stream);
     else
       launch_gemm_chalf_simt((__half2*)d_c, (const __half2*)d_a, (const __half*)d_bp, M, K, N, im, bb, d_out_max,
-                             d_exp, (cudaStream_t)stream);
+                             d_exp, nullptr, (cudaStream_t)stream);
   });
 }
 
 int tn_gemm_cfloat(void* d_c, const void* d_a, const void* d_b, uint64_t M, uint32_t K, uint32_t N, void* stream) {
   if (!d_c || !d_a || !d_b) return fail(TN_E_INVALID, "NULL argument");
-  TN_TRY(launch_gemm_c64((float2*)d_c, (const float2*)d_a, (const float2*)d_b, M, K, N, (cudaStream_t)stream));
+  TN_TRY(launch_gemm_c64((float2*)d_c, (const float2*)d_a, (const float2*)d_b, M, K, N, nullptr, (cudaStream_t)stream));
 }
 
 int tn_pad_b(void* d_bp, const void* d_b, uint32_t K, uint32_t N, float* d_b_bound, int* d_exp, void* d_scratch,

@@ -27,7 +27,7 @@ class TnError(RuntimeError):
 class tn_config(C.Structure):
     _fields_ = [("dtype", C.c_int32), ("stem_min_log2", C.c_int32), ("comm_codec", C.c_int32),
                 ("comm_group", C.c_int32), ("stem_capacity_bytes", C.c_uint64), ("split_log2", C.c_int32),
-                ("reserved", C.c_int32 * 7)]
+                ("layout_policy", C.c_int32), ("reserved", C.c_int32 * 6)]
 
 
 class tn_buffers(C.Structure):
@@ -94,8 +94,9 @@ def _stream(stream):
 
 
 def make_config(dtype=TN_CHALF, stem_min_log2=20, comm_codec=TN_COMM_INT8, comm_group=128,
-                stem_capacity_bytes=0, split_log2=0):
+                stem_capacity_bytes=0, split_log2=0, layout_policy=0):
     c = tn_config()
+    c.layout_policy = layout_policy
     c.dtype, c.stem_min_log2, c.comm_codec, c.comm_group = dtype, stem_min_log2, comm_codec, comm_group
     c.stem_capacity_bytes, c.split_log2 = stem_capacity_bytes, split_log2
     return c

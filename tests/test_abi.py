@@ -59,9 +59,24 @@ def test_plan_load_info_and_lowering_invariants(tnmod, c1_plan):
         assert len(out) == st["m"] + st["n"]
         if not st["perm"]:
             assert lay[len(lay) - len(R):] == R           # R innermost: GEMM reads A as stored
-        assert set(out[:st["m"]]) == set(lay) - set(R)      # Eq. 4 remaining indices
+        assert (set(lay) - set(R)) <= set(out)              # Eq. 4: kept modes remain
+        assert not (set(out) & set(R))                       # contracted modes are gone
         prev = out
     assert sorted(rep["final_layout"]) == sorted(c1_plan["open"])
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3"])
+def test_scatter_layout_policy_needs_no_permutation(tnmod, name):
+    """Layout policy 2: each GEMM writes the next step's contracted modes innermost, so every stem
+    operand is read as stored and the result lands in output order."""
+    with open(os.path.join(ROOT, "plans", f"{name}.json")) as f:
+        plan = json.load(f)
+    p = _load(tnmod, plan, stem_min_log2=6 if name == "c1" else 16, layout_policy=2)
+    rep = p.report()
+    assert p.info()["n_permutes"] == 0 and rep["final_perm"] == 0
+    for a, b in zip(rep["steps"], rep["steps"][1:]):
+        assert b["in"][len(b["in"]) - len(b["R"]):] == b["R"]
+    assert rep["final_layout"] == plan["open"]
 
 
 def test_flops_match_oracle_definition(tnmod, c1_plan):

@@ -32,19 +32,21 @@ def _plan(name):
         return json.load(f)
 
 
-def run_gpu(tn, plan, dtype, slice_id=0, stem_min_log2=6):
-    p = tn.Plan(plan, tn.make_config(dtype=dtype, stem_min_log2=stem_min_log2))
+def run_gpu(tn, plan, dtype, slice_id=0, stem_min_log2=6, policy=0):
+    p = tn.Plan(plan, tn.make_config(dtype=dtype, stem_min_log2=stem_min_log2, layout_policy=policy))
     bufs = tn.Buffers(p)
     amps = tn.contract(p, bufs, slice_id)
     return amps, p
 
 
+@pytest.mark.parametrize("policy", [0, 1, 2])
 @pytest.mark.parametrize("dtype", [0, 1])
 @pytest.mark.parametrize("stem_min", [6, 8, 10])
-def test_c1_full_state_vs_oracle(tn, dtype, stem_min):
+def test_c1_full_state_vs_oracle(tn, dtype, stem_min, policy):
+    """policy 0: scatter-epilogue layouts (no permutation passes); 1: permutation passes."""
     plan = _plan("c1")
     ref = contract.contract(load(plan), 0)
-    got, p = run_gpu(tn, plan, dtype, 0, stem_min)
+    got, p = run_gpu(tn, plan, dtype, 0, stem_min, policy)
     assert p.info()["n_stem_steps"] >= 1
     assert metrics.rel_l2(got, ref) <= TOL[dtype]
     assert abs(np.sum(np.abs(got) ** 2) - 1.0) <= (2 * TOL[dtype])
@@ -52,7 +54,8 @@ def test_c1_full_state_vs_oracle(tn, dtype, stem_min):
 
 @pytest.mark.parametrize("seed", range(6))
 @pytest.mark.parametrize("dtype", [0, 1])
-def test_random_small_circuits_sliced(tn, seed, dtype):
+@pytest.mark.parametrize("policy", [0, 1, 2])
+def test_random_small_circuits_sliced(tn, seed, dtype, policy):
     """Seeded small circuits with extra sliced edges: every slice vs the oracle slice, and the
     GPU sum over slices vs the unsliced oracle (slicing identity)."""
     rng = np.random.default_rng(seed)
@@ -64,7 +67,7 @@ def test_random_small_circuits_sliced(tn, seed, dtype):
     tot = 0
     for s in range(1 << len(sub["sliced"])):
         ref = contract.contract(load(sub), s)
-        got, _ = run_gpu(tn, sub, dtype, s, stem_min_log2=3)
+        got, _ = run_gpu(tn, sub, dtype, s, stem_min_log2=3, policy=policy)
         if np.linalg.norm(ref) > 1e-12:
             assert metrics.rel_l2(got, ref) <= TOL[dtype]
         tot = tot + got
@@ -72,13 +75,14 @@ def test_random_small_circuits_sliced(tn, seed, dtype):
 
 
 @pytest.mark.parametrize("dtype", [0, 1])
-def test_c2_reduced_vs_oracle(tn, dtype):
+@pytest.mark.parametrize("policy", [0, 1, 2])
+def test_c2_reduced_vs_oracle(tn, dtype, policy):
     """C2 (30 qubits, 14 cycles) with extra sub-slicing so the oracle finishes in seconds
     (SURVEY §8(c) c.6): same tree, same kernels, stems up to 2^22."""
     sub = MP.sub_slice(_plan("c2"), 22)
     for s in (0, (1 << len(sub["sliced"])) - 1):
         ref = contract.contract(load(sub), s)
-        got, p = run_gpu(tn, sub, dtype, s, stem_min_log2=12)
+        got, p = run_gpu(tn, sub, dtype, s, stem_min_log2=12, policy=policy)
         assert p.info()["n_stem_steps"] >= 3
         assert metrics.rel_l2(got, ref) <= TOL[dtype]
 

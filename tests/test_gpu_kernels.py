@@ -125,7 +125,7 @@ def test_gemm_chalf_exact_on_integers(env):
     assert np.array_equal(got[..., 0], ref.real) and np.array_equal(got[..., 1], ref.imag)
 
 
-@pytest.mark.parametrize("K,N", [(2, 4), (4, 64), (1, 8), (64, 2), (8, 1)])
+@pytest.mark.parametrize("K,N", [(2, 4), (4, 64), (1, 8), (64, 2), (8, 1), (4, 1), (4, 4), (2, 64), (16, 4), (8, 16), (1, 1), (2, 32)])
 def test_gemm_chalf_simt_small_shapes(env, K, N):
     torch, tn = env
     rng = np.random.default_rng(K * 100 + N)
