@@ -68,11 +68,11 @@ typedef struct {
   uint64_t stem_capacity_bytes; /* bytes of EACH stem buffer the caller will lend; 0 = no check */
   int32_t split_log2;        /* split-type tail: 2^split_log2 chunks; -1 = auto
                                 (smallest power of two that fits), 0 = no split */
-  int32_t layout_policy;     /* 2: each GEMM writes its output with the next step's contracted
+  int32_t layout_policy;     /* 0 (default): output = kept ++ new (TMA-store epilogue) plus a
+                                permutation pass when the next step's modes are not innermost;
+                                2: each GEMM writes its output with the next step's contracted
                                 modes innermost (scatter epilogue, no permutation passes);
-                                1: output = kept ++ new plus a permutation pass when needed;
-                                0 (default): scatter when its stores are >= 64 B contiguous,
-                                otherwise as 1 */
+                                1: scatter when its stores are >= 64 B contiguous, else as 0 */
   int32_t reserved[6];
 } tn_config;
 

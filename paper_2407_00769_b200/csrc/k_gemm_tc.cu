@@ -20,6 +20,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 
 #include "common.cuh"
@@ -128,7 +129,8 @@ struct Cfg {
   static constexpr int kBBytes = BN * BK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kCSub = (BN + 63) / 64;            // 64-column store subtiles
-  static constexpr int kCTma = kCSub * BM * 128;          // 128B-swizzled staging for TMA stores
+  static constexpr int kNBuf = kCSub >= 2 ? kCSub : 2;    // staging ring of 64-column subtiles
+  static constexpr int kCTma = kNBuf * BM * 128;          // 128B-swizzled staging for TMA stores
   static constexpr int kCBytes = kCTma;
   static constexpr int kStagesRaw = (200 * 1024 - kCBytes) / kStageBytes;
   static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
@@ -290,15 +292,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (scat)
       while (run < 4 && run < sc_args.nbits && sc_args.ns[run] == ((int64_t)1 << run)) ++run;
     uint32_t i = 0;
+    uint32_t gsub = 0;  // staging subtiles used so far (ring position)
     for (uint32_t t = blockIdx.x; t < num_tiles; t += gridDim.x, ++i) {
       const uint32_t acc = i & 1, aph = (i >> 1) & 1;
       int m0, n0;
       tile_coords(sc_args, t, num_n, BM, BN, m0, n0);
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
-      // staging buffer free? (previous tile's TMA stores / scatter reads have finished)
-      if (etid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-      named_bar(1, 128);
       const uint32_t taddr = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * 256;
       int64_t row_off = 0;
       const bool row_ok = (uint64_t)(m0 + row) < rows;
@@ -308,7 +308,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           if ((mg >> j) & 1) row_off += sc_args.ms[j];
       }
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
+      for (int sub = 0; sub < BN; sub += 64, ++gsub) {
+      unsigned char* sbuf = sC + (gsub % C::kNBuf) * (BM * 128);
+      if (!scat) {
+        // ring slot free? (the TMA store that used it kNBuf subtiles ago has read it)
+        if (etid == 0) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(C::kNBuf - 1) : "memory");
+        named_bar(1, 128);
+      }
+#pragma unroll 1
+      for (int c = sub; c < BN && c < sub + 64; c += 32) {
         uint32_t r[32];
         tmem_ld_32x32b_x32(taddr + c, r);
         tmem_ld_wait();
@@ -335,10 +343,17 @@ __global__ void __launch_bounds__(kThreads, 1)
               for (int j = run; j < sc_args.nbits; ++j)
                 if ((ng >> j) & 1) off += sc_args.ns[j];
               uint32_t* dst = out_scatter + off;
-              if (V >= 4) {
+              if (V >= 8) {
+                // 256-bit stores (STG.256): one full 32-byte sector per instruction and thread
 #pragma unroll
-                for (int v = 0; v < 16; v += 4)
-                  if (v < V) *reinterpret_cast<uint4*>(dst + v) = make_uint4(pk[q + v], pk[q + v + 1], pk[q + v + 2], pk[q + v + 3]);
+                for (int v = 0; v < 16; v += 8)
+                  if (v < V)
+                    asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(dst + v), "r"(pk[q + v]),
+                                 "r"(pk[q + v + 1]), "r"(pk[q + v + 2]), "r"(pk[q + v + 3]), "r"(pk[q + v + 4]),
+                                 "r"(pk[q + v + 5]), "r"(pk[q + v + 6]), "r"(pk[q + v + 7])
+                                 : "memory");
+              } else if (V == 4) {
+                *reinterpret_cast<uint4*>(dst) = make_uint4(pk[q], pk[q + 1], pk[q + 2], pk[q + 3]);
               } else if (V == 2) {
                 *reinterpret_cast<uint2*>(dst) = make_uint2(pk[q], pk[q + 1]);
               } else {
@@ -347,29 +362,31 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
         } else {
-          unsigned char* sub = sC + (c >> 6) * (BM * 128) + row * 128;
+          unsigned char* srow = sbuf + row * 128;
           const int cb = (c & 63) >> 3;  // first 16-byte chunk of these 32 columns
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             if ((c & 63) + q * 8 < BN || BN >= 64) {
               const int chunk = (cb + q) ^ (row & 7);
               uint4 v = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
-              *reinterpret_cast<uint4*>(sub + chunk * 16) = v;
+              *reinterpret_cast<uint4*>(srow + chunk * 16) = v;
             }
           }
         }
       }
-      // accumulator drained -> MMA may reuse it
-      tc_fence_before();
-      mbar_arrive(&tempty[acc]);
+      if (sub + 64 >= BN) {
+        // accumulator drained -> MMA may reuse it (before the last store is issued)
+        tc_fence_before();
+        mbar_arrive(&tempty[acc]);
+      }
       if (!scat) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         named_bar(1, 128);
         if (etid == 0) {
-#pragma unroll 1
-          for (int j = 0; j < C::kCSub; ++j) tma_store_2d(&tmC, sC + j * (BM * 128), n0 + j * 64, m0);
+          tma_store_2d(&tmC, sbuf, n0 + sub, m0);
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
+      }
       }
     }
     if (etid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
@@ -441,7 +458,8 @@ static void launch_bn(__half* c, const __half* a, const __half* bp, uint64_t M, 
   memset(&sa, 0, sizeof(sa));
   const uint32_t n_cols = N2_real / 2;
   OutMap ident;
-  if (N2_real < 16 && (!om || om->identity)) {  // TMA stores need 16-byte rows: store directly
+  static const bool direct_env = getenv("TN_DIRECT_EPI") != nullptr;  // experiment knob
+  if ((N2_real < 16 || direct_env) && (!om || om->identity)) {  // TMA stores need 16-byte rows
     ident = identity_map(M, N2_real / 2);
     om = &ident;
     ident.identity = 0;

@@ -229,7 +229,8 @@ Plan* load_plan(const char* json, size_t len, const tn_config* cfg_in) {
   // operand is read as stored (K-major) and no standalone permutation pass is needed; the other
   // modes are ordered by next use, furthest first.  layout_policy 1: output = kept ++ new and a
   // permutation pass whenever R_i is not innermost (the classic "reorder then GEMM").
-  const int policy = cfg.layout_policy;
+  // public numbering: 0 = permutation passes (default, fastest measured), 1 = hybrid, 2 = scatter
+  const int policy = cfg.layout_policy == 0 ? 1 : (cfg.layout_policy == 1 ? 0 : cfg.layout_policy);
   const int eb = (cfg.dtype == TN_CHALF) ? 4 : 8;
   uint64_t smax = 0;
   if (entry_idx >= 0) {
