@@ -73,7 +73,12 @@ typedef struct {
                                 2: each GEMM writes its output with the next step's contracted
                                 modes innermost (scatter epilogue, no permutation passes);
                                 1: scatter when its stores are >= 64 B contiguous, else as 0 */
-  int32_t reserved[6];
+  int32_t quant_from_pct;    /* int8/int4 swaps only at stem steps >= this percentage of the path
+                                ("quantify in the later stages"); earlier swaps send
+                                fp16.  Negative: 50 */
+  int32_t virtual_world;     /* > 1 with comm == NULL: lower the plan for that many ranks
+                                (host-only inspection of the shard/swap schedule) */
+  int32_t reserved[4];
 } tn_config;
 
 /* Caller-owned device buffers lent to a call (P:18-22 double buffering). */
@@ -185,6 +190,12 @@ TN_API int tn_quant_int8(int8_t* d_codes, float* d_scales, float* d_zeros, const
                   int g, void* stream);
 TN_API int tn_dequant_int8(float* d_y, const int8_t* d_codes, const float* d_scales, const float* d_zeros,
                     uint64_t n, int g, void* stream);
+/* Same codec on fp16 reals (the complex-half mode-swap payload): the codec's input is the exact
+ * float32 value of each fp16; dequantised values are rounded to fp16 (round to nearest even). */
+TN_API int tn_quant_int8_f16(int8_t* d_codes, float* d_scales, float* d_zeros, const void* d_x, uint64_t n,
+                             int g, void* stream);
+TN_API int tn_dequant_int8_f16(void* d_y, const int8_t* d_codes, const float* d_scales, const float* d_zeros,
+                               uint64_t n, int g, void* stream);
 
 /* ---- multi-GPU (stem sharded on its log2(world) outermost modes, Alg. 1) ---- */
 TN_API int tn_comm_unique_id(uint8_t out[128]);

@@ -86,6 +86,10 @@ void launch_quant_int8(int8_t* codes, float* scales, float* zeros, const float* 
                        cudaStream_t s);
 void launch_dequant_int8(float* y, const int8_t* codes, const float* scales, const float* zeros,
                          uint64_t n, int g, cudaStream_t s);
+void launch_quant_int8_half(int8_t* codes, float* scales, float* zeros, const __half* x, uint64_t n, int g,
+                            cudaStream_t s);
+void launch_dequant_int8_half(__half* y, const int8_t* codes, const float* scales, const float* zeros, uint64_t n,
+                              int g, cudaStream_t s);
 
 // ---- device helpers ----
 __host__ __device__ inline int64_t outmap_m(const OutMap& o, uint64_t m) {

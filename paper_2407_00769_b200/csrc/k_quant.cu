@@ -3,19 +3,27 @@
 // zero = (q_min*max - q_max*min)/(max-min), code = rint(x*scale + zero) evaluated as an fp32
 // multiply then an fp32 add (no FMA) so codes are bit-identical to the oracle (oracle/codec.py);
 // constant groups: scale = 0, zero = the constant (C-A11).  One warp per group.
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace tn {
 
+__device__ __forceinline__ float to_f32(float v) { return v; }
+__device__ __forceinline__ float to_f32(__half v) { return __half2float(v); }
+__device__ __forceinline__ void from_f32(float& d, float v) { d = v; }
+__device__ __forceinline__ void from_f32(__half& d, float v) { d = __float2half_rn(v); }
+
+template <typename T>
 __global__ void quant_int8_kernel(int8_t* __restrict__ codes, float* __restrict__ scales, float* __restrict__ zeros,
-                                  const float* __restrict__ x, uint64_t n_groups, int g) {
+                                  const T* __restrict__ x, uint64_t n_groups, int g) {
   const int lane = threadIdx.x & 31;
   const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
   for (uint64_t gi = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); gi < n_groups; gi += warps) {
-    const float* xs = x + gi * g;
+    const T* xs = x + gi * g;
     float mx = -INFINITY, mn = INFINITY;
     for (int i = lane; i < g; i += 32) {
-      float v = xs[i];
+      float v = to_f32(xs[i]);
       mx = fmaxf(mx, v);
       mn = fminf(mn, v);
     }
@@ -43,7 +51,7 @@ __global__ void quant_int8_kernel(int8_t* __restrict__ codes, float* __restrict_
       if (scale == 0.f) {
         c = -128.f;
       } else {
-        c = rintf(__fadd_rn(__fmul_rn(xs[i], scale), zero));
+        c = rintf(__fadd_rn(__fmul_rn(to_f32(xs[i]), scale), zero));
         c = fminf(fmaxf(c, -128.f), 127.f);
       }
       cs[i] = (int8_t)(int)c;
@@ -51,13 +59,14 @@ __global__ void quant_int8_kernel(int8_t* __restrict__ codes, float* __restrict_
   }
 }
 
-__global__ void dequant_int8_kernel(float* __restrict__ y, const int8_t* __restrict__ codes,
+template <typename T>
+__global__ void dequant_int8_kernel(T* __restrict__ y, const int8_t* __restrict__ codes,
                                     const float* __restrict__ scales, const float* __restrict__ zeros, uint64_t n,
                                     int g) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
     uint64_t gi = i / g;
     float s = scales[gi], z = zeros[gi];
-    y[i] = (s == 0.f) ? z : __fdiv_rn(__fsub_rn((float)codes[i], z), s);
+    from_f32(y[i], (s == 0.f) ? z : __fdiv_rn(__fsub_rn((float)codes[i], z), s));
   }
 }
 
@@ -68,7 +77,7 @@ void launch_quant_int8(int8_t* codes, float* scales, float* zeros, const float* 
   uint64_t blocks = (groups + 7) / 8;
   if (blocks > 148 * 16) blocks = 148 * 16;
   if (blocks == 0) return;
-  quant_int8_kernel<<<(unsigned)blocks, 256, 0, s>>>(codes, scales, zeros, x, groups, g);
+  quant_int8_kernel<float><<<(unsigned)blocks, 256, 0, s>>>(codes, scales, zeros, x, groups, g);
   TN_CUDA(cudaGetLastError());
 }
 
@@ -78,7 +87,28 @@ void launch_dequant_int8(float* y, const int8_t* codes, const float* scales, con
   uint64_t blocks = (n + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
   if (blocks == 0) return;
-  dequant_int8_kernel<<<(unsigned)blocks, 256, 0, s>>>(y, codes, scales, zeros, n, g);
+  dequant_int8_kernel<float><<<(unsigned)blocks, 256, 0, s>>>(y, codes, scales, zeros, n, g);
+  TN_CUDA(cudaGetLastError());
+}
+
+// complex-half payload of a mode swap: the interleaved fp16 reals are the codec's input (their exact
+// float32 values), and the dequantised values are rounded back to fp16
+void launch_quant_int8_half(int8_t* codes, float* scales, float* zeros, const __half* x, uint64_t n, int g,
+                            cudaStream_t s) {
+  if (g <= 0 || n % g) throw TnError{TN_E_INVALID, "quant: n must be a multiple of the group size"};
+  uint64_t groups = n / g;
+  uint64_t blocks = std::min<uint64_t>((groups + 7) / 8, 148ull * 16);
+  if (blocks == 0) return;
+  quant_int8_kernel<__half><<<(unsigned)blocks, 256, 0, s>>>(codes, scales, zeros, x, groups, g);
+  TN_CUDA(cudaGetLastError());
+}
+
+void launch_dequant_int8_half(__half* y, const int8_t* codes, const float* scales, const float* zeros, uint64_t n,
+                              int g, cudaStream_t s) {
+  if (g <= 0 || n % g) throw TnError{TN_E_INVALID, "dequant: n must be a multiple of the group size"};
+  uint64_t blocks = std::min<uint64_t>((n + 255) / 256, 148ull * 16);
+  if (blocks == 0) return;
+  dequant_int8_kernel<__half><<<(unsigned)blocks, 256, 0, s>>>(y, codes, scales, zeros, n, g);
   TN_CUDA(cudaGetLastError());
 }
 

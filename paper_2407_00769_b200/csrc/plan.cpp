@@ -39,7 +39,7 @@ static std::vector<int> int_list(const tnjson::Value* v, const char* what) {
   return out;
 }
 
-Plan* load_plan(const char* json, size_t len, const tn_config* cfg_in) {
+Plan* load_plan(const char* json, size_t len, const tn_config* cfg_in, int world) {
   tnjson::Value root;
   try {
     root = tnjson::parse(json, len);
@@ -60,6 +60,9 @@ Plan* load_plan(const char* json, size_t len, const tn_config* cfg_in) {
   if (cfg.dtype != TN_CHALF && cfg.dtype != TN_CFLOAT) throw err(TN_E_INVALID, "cfg.dtype");
   if (cfg.comm_group <= 0) cfg.comm_group = 128;
   p.cfg = cfg;
+  if (world != 1 && world != 2 && world != 4 && world != 8) throw err(TN_E_UNSUPPORTED, "world must be 1, 2, 4 or 8");
+  p.world = world;
+  while ((1 << p.shard_log2) < world) p.shard_log2++;
 
   // ---- tensors
   const tnjson::Value* ts = root.get("tensors");
@@ -263,7 +266,23 @@ Plan* load_plan(const char* json, size_t len, const tn_config* cfg_in) {
       Node& e = p.nodes[p.stem_entry];
       e.labels = order_with_inner(e.labels, Rsets[0]);
     }
+    // ---- sharding: the stem's log2(world) outermost modes index the GPU.  Shard
+    // modes are the entry labels used furthest in the future (never-contracted open legs first).
+    std::vector<int> shard;
+    if (p.shard_log2 > 0) {
+      Node& e = p.nodes[p.stem_entry];
+      std::vector<int> cand = e.labels;
+      std::stable_sort(cand.begin(), cand.end(), [&](int a, int b) { return nu(a) > nu(b); });
+      if ((int)cand.size() <= p.shard_log2) throw err(TN_E_INFEASIBLE, "stem entry has too few modes to shard");
+      shard.assign(cand.begin(), cand.begin() + p.shard_log2);
+      std::vector<int> lay = shard;
+      for (int l : e.labels)
+        if (std::find(shard.begin(), shard.end(), l) == shard.end()) lay.push_back(l);
+      e.labels = lay;
+      p.shard0 = shard;
+    }
     std::vector<int> L = p.nodes[p.stem_entry].labels;
+    L.erase(L.begin(), L.begin() + shard.size());  // local layout (shard modes are rank bits)
     smax = 1ull << L.size();
     int prev = p.stem_entry;
     for (size_t s = 0; s < step_nodes.size(); ++s) {
@@ -271,9 +290,55 @@ Plan* load_plan(const char* json, size_t len, const tn_config* cfg_in) {
       st.node = step_nodes[s];
       const Node& n = p.nodes[st.node];
       st.branch = (n.u == prev) ? n.v : n.u;
-      st.in_layout = L;
       const auto& B = p.nodes[st.branch].labels;
       std::set<int> bs(B.begin(), B.end());
+      if (!shard.empty()) {
+        // Alg. 1: a contracted shard mode forces an all-to-all mode swap first.
+        st.shard_before = shard;
+        std::vector<int> out_pos;
+        for (size_t j = 0; j < shard.size(); ++j)
+          if (bs.count(shard[j])) out_pos.push_back((int)j);
+        if (!out_pos.empty()) {
+          // swap in the local modes used furthest in the future (reading C-A17: furthest next use;
+          // only the contracted shard modes are swapped)
+          std::vector<int> cand;
+          for (int l : L)
+            if (!bs.count(l)) cand.push_back(l);
+          std::stable_sort(cand.begin(), cand.end(), [&](int a, int b) { return nu(a) > nu(b); });
+          if (cand.size() < out_pos.size()) throw err(TN_E_INFEASIBLE, "partition modes run out (swap)");
+          st.swap = true;
+          // quantise only in the later stages of the path (earlier errors accumulate)
+          {
+            const int pct = cfg.quant_from_pct < 0 ? 50 : cfg.quant_from_pct;
+            st.quant = cfg.dtype == TN_CHALF && cfg.comm_codec == TN_COMM_INT8 &&
+                       100.0 * (double)s >= pct * (double)step_nodes.size();
+          }
+          st.swap_out_pos = out_pos;
+          st.swap_in.assign(cand.begin(), cand.begin() + out_pos.size());
+          // sender layout: swap_in outermost (chunk v of the outer bits goes to member v)
+          std::vector<int> snd = st.swap_in;
+          for (int l : L)
+            if (std::find(st.swap_in.begin(), st.swap_in.end(), l) == st.swap_in.end()) snd.push_back(l);
+          st.send_layout = snd;
+          if (snd != L) {
+            st.send_perm = true;
+            for (int l : snd) st.send_perm_axes.push_back((int)(std::find(L.begin(), L.end(), l) - L.begin()));
+          }
+          // after the exchange: the swapped-out shard modes become the outermost local modes
+          std::vector<int> lay;
+          for (int j : out_pos) lay.push_back(shard[j]);
+          lay.insert(lay.end(), snd.begin() + out_pos.size(), snd.end());
+          for (size_t t = 0; t < out_pos.size(); ++t) shard[out_pos[t]] = st.swap_in[t];
+          L = lay;
+          p.n_swaps++;
+          const double n_local = std::ldexp(1.0, (int)L.size());
+          const double frac = 1.0 - std::ldexp(1.0, -(int)out_pos.size());
+          const double per = !st.quant ? (cfg.dtype == TN_CHALF ? 4.0 : 8.0) : (2.0 + 16.0 / cfg.comm_group);
+          p.swap_bytes += frac * n_local * per;
+        }
+        st.shard_after = shard;
+      }
+      st.in_layout = L;
       std::vector<int> R, kept;
       for (int l : L) (bs.count(l) ? R : kept).push_back(l);
       // is R the innermost block of L?
@@ -297,7 +362,9 @@ Plan* load_plan(const char* json, size_t len, const tn_config* cfg_in) {
       bool scatter = false;
       if (policy == 0 || policy == 2) {
         if (s + 1 == step_nodes.size()) {
-          out = p.open;  // the last step writes the result directly in output order
+          // the last step writes the result directly in output order (local modes only)
+          for (int l : p.open)
+            if (std::find(shard.begin(), shard.end(), l) == shard.end()) out.push_back(l);
           scatter = true;
         } else {
           // [rest by next use] ++ [kept ∩ R_next] ++ [new ∩ R_next]  (new innermost)
@@ -346,8 +413,9 @@ Plan* load_plan(const char* json, size_t len, const tn_config* cfg_in) {
                        ((st.klog >= 3 && st.nlog >= 3) || st.klog >= 4 || st.klog + st.nlog > 11);
       {
         std::set<int> chk(st.out_layout.begin(), st.out_layout.end());
+        chk.insert(shard.begin(), shard.end());
         std::set<int> want(n.labels.begin(), n.labels.end());
-        if (chk != want || chk.size() != st.out_layout.size())
+        if (chk != want || chk.size() != st.out_layout.size() + shard.size())
           throw err(TN_E_INVALID, "internal: step output labels mismatch");
       }
       // output address map: bit j of m (kept[mlog-1-j]) and of n (newl[nlog-1-j])
@@ -380,7 +448,8 @@ Plan* load_plan(const char* json, size_t len, const tn_config* cfg_in) {
       p.steps.push_back(std::move(st));
     }
     p.final_layout = L;
-    if (L != p.open) {
+    p.final_shard = shard;
+    if (shard.empty() && L != p.open) {
       p.final_perm = true;
       for (int l : p.open) p.final_perm_axes.push_back((int)(std::find(L.begin(), L.end(), l) - L.begin()));
       p.perm_bytes += 2.0 * eb * std::ldexp(1.0, (int)L.size());
@@ -425,7 +494,8 @@ Plan* load_plan(const char* json, size_t len, const tn_config* cfg_in) {
   p.ws_scratch = off;
   size_t S = p.steps.size();
   p.n_exp_slots = (int)(2 * S + 4);
-  off += align_up(4 * (S + 2) + 4 * (S + 2) + 4 * p.n_exp_slots + 64, 256);
+  // max_slot[S+2], b_bound[S+2], b_max[S+2], exps[n_exp_slots], entry_max (runtime.cu scratch_of)
+  off += align_up(4 * 3 * (S + 2) + 4 * p.n_exp_slots + 4 + 64, 256);
   p.ws_total = off;
   return P.release();
 }
@@ -449,17 +519,37 @@ std::string report_json(const Plan& p, const std::vector<float>& ms) {
     const StemStep& s = p.steps[i];
     o << (i ? "," : "") << "{\"node\":" << s.node << ",\"branch\":" << s.branch << ",\"m\":" << s.mlog
       << ",\"k\":" << s.klog << ",\"n\":" << s.nlog << ",\"perm\":" << (s.perm ? 1 : 0)
-      << ",\"tc\":" << (s.tensor_core ? 1 : 0) << ",\"split\":" << s.split << ",\"in\":";
+      << ",\"tc\":" << (s.tensor_core ? 1 : 0) << ",\"split\":" << s.split << ",\"swap\":" << (s.swap ? 1 : 0)
+      << ",\"quant\":" << (s.quant ? 1 : 0)
+      << ",\"in\":";
     jlist(o, s.in_layout);
     o << ",\"R\":";
     jlist(o, s.R);
     o << ",\"out\":";
     jlist(o, s.out_layout);
+    if (s.swap) {
+      o << ",\"shard_before\":";
+      jlist(o, s.shard_before);
+      o << ",\"shard_after\":";
+      jlist(o, s.shard_after);
+      o << ",\"swap_out_pos\":";
+      jlist(o, s.swap_out_pos);
+      o << ",\"swap_in\":";
+      jlist(o, s.swap_in);
+      o << ",\"send_layout\":";
+      jlist(o, s.send_layout);
+    }
     o << "}";
   }
-  o << "],\"final_layout\":";
+  o << "],\"entry_layout\":";
+  jlist(o, p.stem_entry >= 0 ? p.nodes[p.stem_entry].labels : std::vector<int>());
+  o << ",\"shard0\":";
+  jlist(o, p.shard0);
+  o << ",\"final_layout\":";
   jlist(o, p.final_layout);
-  o << ",\"launches\":" << p.launches;
+  o << ",\"launches\":" << p.launches << ",\"world\":" << p.world << ",\"n_swaps\":" << p.n_swaps
+    << ",\"swap_bytes\":" << p.swap_bytes << ",\"final_shard\":";
+  jlist(o, p.final_shard);
   if (!ms.empty()) {  // [common_ms, (perm_ms, gemm_ms) per step..., final_ms]
     o << ",\"ms\":[";
     for (size_t i = 0; i < ms.size(); ++i) o << (i ? "," : "") << ms[i];

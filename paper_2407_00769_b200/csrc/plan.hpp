@@ -49,6 +49,15 @@ struct StemStep {
   std::vector<int64_t> m_stride, n_stride;
   bool out_identity = true;       // out_layout == kept ++ newl (plain row-major [M][N])
   int split = 0;                  // 1 = split-type (chunked tail) step
+  // sharded stem (world > 1), Alg. 1: mode swap before this step when R ∩ shard != ∅
+  bool swap = false;
+  std::vector<int> shard_before, shard_after;  // shard labels, rank bit order (MSB first)
+  std::vector<int> swap_out_pos;  // positions (in shard_before) of the contracted shard modes
+  std::vector<int> swap_in;       // local labels that become shard modes (same positions)
+  bool send_perm = false;         // local permutation putting swap_in outermost before sending
+  bool quant = false;             // this swap's payload is group-quantised (else fp16)
+  std::vector<int> send_perm_axes;
+  std::vector<int> send_layout;   // local layout being sent (swap_in outermost)
 };
 
 struct Plan {
@@ -72,8 +81,8 @@ struct Plan {
   uint64_t stem_elems_max = 0;    // largest stem tensor (elements)
   int max_stem_log2 = 0;
   // scratch slots (offsets in bytes from ws_scratch)
-  //   [0, 4*(S+2)): float max slots; slot i = max |real| of the stem after step i-1 (slot 0: entry)
-  //   then S floats b_bound; then int exps[2*S+2]
+  //   float max_slot[S+2] (slot i = max |real| of the stem entering step i), float b_bound[S+2],
+  //   uint b_max[S+2], int exps[n_exp_slots], uint entry_max  (runtime.cu scratch_of)
   int n_exp_slots = 0;
   double stem_flops = 0, total_flops = 0, stem_bytes_alg = 0, perm_bytes = 0;
   int n_permutes = 0;
@@ -89,11 +98,16 @@ struct Plan {
   uint64_t launches = 0;          // kernels launched by the last tn_stem_contract
   void* pinned = nullptr;         // pinned host copy of leaves (complex64), lazily allocated
   int world = 1, rank = 0;
+  int shard_log2 = 0;             // log2(world): the stem is sharded on this many modes
+  std::vector<int> shard0;        // initial shard labels (outermost of the entry layout)
+  std::vector<int> final_shard;   // shard labels after the last step (the result's rank bits)
+  int n_swaps = 0;
+  double swap_bytes = 0;          // payload bytes each rank sends per slice (codec applied)
   tn_comm* comm = nullptr;
 };
 
 // Parse JSON + validate + lower.  Throws TnError.
-Plan* load_plan(const char* json, size_t len, const tn_config* cfg);
+Plan* load_plan(const char* json, size_t len, const tn_config* cfg, int world = 1);
 std::string report_json(const Plan& p, const std::vector<float>& ms);
 
 inline uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }

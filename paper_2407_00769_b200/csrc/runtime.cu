@@ -49,6 +49,50 @@ struct tn_comm {
   int rank = 0, world = 1, device = 0;
 };
 
+// ---- NCCL (dlopen'ed: the process's torch already carries libnccl.so.2) ----
+namespace {
+enum { NCCL_INT8 = 0, NCCL_FLOAT16 = 6, NCCL_FLOAT32 = 7, NCCL_MAX = 2 };
+void* nccl_sym(const char* name) {
+  static void* h = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+  });
+  void* f = h ? dlsym(h, name) : nullptr;
+  if (!f) throw TnError{TN_E_NCCL, std::string("NCCL symbol unavailable: ") + name};
+  return f;
+}
+void nccl_check(int r, const char* what) {
+  if (r != 0) throw TnError{TN_E_NCCL, std::string(what) + " failed (" + std::to_string(r) + ")"};
+}
+void nccl_group(bool start) {
+  typedef int (*fn_t)();
+  static fn_t gs = (fn_t)nccl_sym("ncclGroupStart"), ge = (fn_t)nccl_sym("ncclGroupEnd");
+  nccl_check(start ? gs() : ge(), start ? "ncclGroupStart" : "ncclGroupEnd");
+}
+void nccl_send(const void* buf, size_t count, int type, int peer, void* comm, cudaStream_t s) {
+  typedef int (*fn_t)(const void*, size_t, int, int, void*, cudaStream_t);
+  static fn_t f = (fn_t)nccl_sym("ncclSend");
+  nccl_check(f(buf, count, type, peer, comm, s), "ncclSend");
+}
+void nccl_recv(void* buf, size_t count, int type, int peer, void* comm, cudaStream_t s) {
+  typedef int (*fn_t)(void*, size_t, int, int, void*, cudaStream_t);
+  static fn_t f = (fn_t)nccl_sym("ncclRecv");
+  nccl_check(f(buf, count, type, peer, comm, s), "ncclRecv");
+}
+void nccl_allreduce_max(float* buf, size_t count, void* comm, cudaStream_t s) {
+  typedef int (*fn_t)(const void*, void*, size_t, int, int, void*, cudaStream_t);
+  static fn_t f = (fn_t)nccl_sym("ncclAllReduce");
+  nccl_check(f(buf, buf, count, NCCL_FLOAT32, NCCL_MAX, comm, s), "ncclAllReduce");
+}
+void nccl_allgather(const void* send, void* recv, size_t count, int type, void* comm, cudaStream_t s) {
+  typedef int (*fn_t)(const void*, void*, size_t, int, void*, cudaStream_t);
+  static fn_t f = (fn_t)nccl_sym("ncclAllGather");
+  nccl_check(f(send, recv, count, type, comm, s), "ncclAllGather");
+}
+}  // namespace
+
 namespace {
 
 struct Scratch {
@@ -180,8 +224,90 @@ void check_buffers(const Plan& p, const tn_buffers* b) {
     throw TnError{TN_E_CAPACITY, "stem buffers too small: need " + std::to_string(p.stem_elems_max * eb)};
 }
 
+// Sharded mode swap before step `st` (Alg. 1 "intra-node communication"; group
+// quantisation Eq. 1).  The contracted shard modes (positions swap_out_pos of the shard
+// set) trade places with the local modes swap_in: the sender's layout has swap_in outermost, so
+// chunk v (the v-th block of those bits) belongs to the group member whose swapped-out bits are v.
+// The receiver stores the chunk from member v at slot v, so after the exchange the swapped-out shard
+// modes are the outermost local modes.  Only members that differ in the swapped bits talk (partial
+// swap, reading C-A17).  int8: each chunk is quantised in groups of comm_group reals (groups never
+// straddle chunks), sent as codes + fp32 scale/zero, and dequantised straight into complex-half.
+void mode_swap(Plan& p, const StemStep& st, const tn_buffers* b, int& cur, cudaStream_t s) {
+  if (!p.comm || !p.comm->nccl_comm) throw TnError{TN_E_NCCL, "sharded plan without an NCCL communicator"};
+  const int eb = p.cfg.dtype == TN_CHALF ? 4 : 8;
+  if (st.send_perm) {
+    launch_permute(b->d_stem[1 - cur], b->d_stem[cur], eb, (int)st.send_layout.size(), st.send_perm_axes.data(), s);
+    ++p.launches;
+    cur = 1 - cur;
+  }
+  const int sx = (int)st.swap_out_pos.size();
+  const int S = (int)st.shard_before.size();
+  const uint64_t n_local = 1ull << st.send_layout.size();
+  const uint64_t chunk = n_local >> sx;  // complex elements per chunk
+  // member index of this rank: its bits at the swapped shard positions (position 0 = rank MSB)
+  auto bit_of = [&](int r, int pos) { return (r >> (S - 1 - pos)) & 1; };
+  int me = 0;
+  for (int t = 0; t < sx; ++t) me = (me << 1) | bit_of(p.rank, st.swap_out_pos[t]);
+  auto peer_of = [&](int v) {
+    int r = p.rank;
+    for (int t = 0; t < sx; ++t) {
+      int pos = st.swap_out_pos[t], bit = (v >> (sx - 1 - t)) & 1;
+      int shift = S - 1 - pos;
+      r = (r & ~(1 << shift)) | (bit << shift);
+    }
+    return r;
+  };
+  void* comm = p.comm->nccl_comm;
+  unsigned char* X = static_cast<unsigned char*>(b->d_stem[cur]);
+  unsigned char* Y = static_cast<unsigned char*>(b->d_stem[1 - cur]);
+  const bool int8 = st.quant;  // lowering: int8 codec, complex-half, late enough in the path
+  if (int8) {
+    const int g = p.cfg.comm_group;
+    const uint64_t reals = 2 * n_local, creals = 2 * chunk;
+    if (creals % g) throw TnError{TN_E_INFEASIBLE, "swap chunk is not a multiple of the quantisation group"};
+    const uint64_t ng = reals / g, cng = creals / g;
+    const uint64_t codes_bytes = align_up(reals, 256);
+    auto codes = [&](unsigned char* base) { return reinterpret_cast<int8_t*>(base); };
+    auto scales = [&](unsigned char* base) { return reinterpret_cast<float*>(base + codes_bytes); };
+    auto zeros = [&](unsigned char* base) { return reinterpret_cast<float*>(base + codes_bytes + align_up(4 * ng, 256)); };
+    launch_quant_int8_half(codes(Y), scales(Y), zeros(Y), reinterpret_cast<const __half*>(X), reals, g, s);
+    nccl_group(true);
+    for (int v = 0; v < (1 << sx); ++v) {
+      if (v == me) continue;
+      int peer = peer_of(v);
+      nccl_send(codes(Y) + v * creals, creals, NCCL_INT8, peer, comm, s);
+      nccl_send(scales(Y) + v * cng, cng, NCCL_FLOAT32, peer, comm, s);
+      nccl_send(zeros(Y) + v * cng, cng, NCCL_FLOAT32, peer, comm, s);
+      nccl_recv(codes(X) + v * creals, creals, NCCL_INT8, peer, comm, s);
+      nccl_recv(scales(X) + v * cng, cng, NCCL_FLOAT32, peer, comm, s);
+      nccl_recv(zeros(X) + v * cng, cng, NCCL_FLOAT32, peer, comm, s);
+    }
+    nccl_group(false);
+    TN_CUDA(cudaMemcpyAsync(codes(X) + me * creals, codes(Y) + me * creals, creals, cudaMemcpyDeviceToDevice, s));
+    TN_CUDA(cudaMemcpyAsync(scales(X) + me * cng, scales(Y) + me * cng, 4 * cng, cudaMemcpyDeviceToDevice, s));
+    TN_CUDA(cudaMemcpyAsync(zeros(X) + me * cng, zeros(Y) + me * cng, 4 * cng, cudaMemcpyDeviceToDevice, s));
+    launch_dequant_int8_half(reinterpret_cast<__half*>(Y), codes(X), scales(X), zeros(X), reals, g, s);
+    p.launches += 2;
+  } else {
+    const int type = eb == 4 ? NCCL_FLOAT16 : NCCL_FLOAT32;
+    const size_t cnt = 2 * chunk;  // reals per chunk
+    nccl_group(true);
+    for (int v = 0; v < (1 << sx); ++v) {
+      if (v == me) continue;
+      int peer = peer_of(v);
+      nccl_send(X + (uint64_t)v * chunk * eb, cnt, type, peer, comm, s);
+      nccl_recv(Y + (uint64_t)v * chunk * eb, cnt, type, peer, comm, s);
+    }
+    nccl_group(false);
+    TN_CUDA(cudaMemcpyAsync(Y + (uint64_t)me * chunk * eb, X + (uint64_t)me * chunk * eb, chunk * eb,
+                            cudaMemcpyDeviceToDevice, s));
+  }
+  cur = 1 - cur;
+}
+
 void stem_contract(Plan& p, const tn_buffers* b, uint64_t slice_id, cudaStream_t s) {
   check_buffers(p, b);
+  if (p.world > 1 && !p.comm) throw TnError{TN_E_INVALID, "plan lowered for several ranks without a communicator"};
   if (p.sliced.size() < 64 && slice_id >= (1ull << p.sliced.size()))
     throw TnError{TN_E_INVALID, "slice_id >= 2^|sliced|"};
   unsigned char* W = static_cast<unsigned char*>(b->d_ws);
@@ -209,6 +335,7 @@ void stem_contract(Plan& p, const tn_buffers* b, uint64_t slice_id, cudaStream_t
   {
     const Node& e = p.nodes[p.stem_entry];
     uint64_t n = 1ull << e.labels.size();
+    const uint64_t n_local = n >> p.shard_log2;  // this rank's shard: shard modes are outermost
     const float2* src;
     if (e.kind == NODE_LEAF) {
       View v = view_of(p, p.stem_entry, W, slice_id);
@@ -230,11 +357,13 @@ void stem_contract(Plan& p, const tn_buffers* b, uint64_t slice_id, cudaStream_t
         // convert in place is impossible across buffers of different element size: go through ws
         throw TnError{TN_E_UNSUPPORTED, "complex-half stem entry at a leaf: raise stem_min_log2"};
       }
+      // the exponent comes from the whole entry tensor (identical on every rank)
       launch_max_abs_f32(reinterpret_cast<const float*>(src), 2 * n, sc.entry_max, s);
-      launch_c64_to_chalf(reinterpret_cast<__half2*>(b->d_stem[0]), src, n, sc.entry_max, &sc.exps[0],
-                          reinterpret_cast<uint32_t*>(&sc.max_slot[0]), s);
+      launch_c64_to_chalf(reinterpret_cast<__half2*>(b->d_stem[0]), src + (uint64_t)p.rank * n_local, n_local,
+                          sc.entry_max, &sc.exps[0], reinterpret_cast<uint32_t*>(&sc.max_slot[0]), s);
+      if (p.world > 1) nccl_allreduce_max(&sc.max_slot[0], 1, p.comm->nccl_comm, s);
     } else {
-      launch_copy_c64(reinterpret_cast<float2*>(b->d_stem[0]), src, n, s);
+      launch_copy_c64(reinterpret_cast<float2*>(b->d_stem[0]), src + (uint64_t)p.rank * n_local, n_local, s);
     }
   }
   int cur = 0;
@@ -244,6 +373,9 @@ void stem_contract(Plan& p, const tn_buffers* b, uint64_t slice_id, cudaStream_t
   rec(1);
   for (size_t i = 0; i < p.steps.size(); ++i) {
     const StemStep& st = p.steps[i];
+    if (st.swap) {
+      mode_swap(p, st, b, cur, s);
+    }
     if (st.perm) {
       launch_permute(b->d_stem[1 - cur], b->d_stem[cur], eb, (int)st.in_layout.size(), st.perm_axes.data(), s);
       ++p.launches;
@@ -271,6 +403,8 @@ void stem_contract(Plan& p, const tn_buffers* b, uint64_t slice_id, cudaStream_t
                                reinterpret_cast<const __half2*>(b->d_stem[cur]),
                                reinterpret_cast<const __half*>(W + st.b_off), M, K, N, in_max, &sc.b_bound[i], out_max,
                                &sc.exps[2 + 2 * i], &om, s);
+      // every rank must scale the next step by the same power of two
+      if (p.world > 1) nccl_allreduce_max(&sc.max_slot[i + 1], 1, p.comm->nccl_comm, s);
     } else {
       launch_gemm_c64(reinterpret_cast<float2*>(b->d_stem[1 - cur]), reinterpret_cast<const float2*>(b->d_stem[cur]),
                       reinterpret_cast<const float2*>(W + st.b_off), M, K, N, &om, s);
@@ -300,10 +434,13 @@ int tn_plan_load(const char* json, size_t len, const tn_config* cfg, tn_comm* co
   if (!json || !out) return fail(TN_E_INVALID, "NULL argument");
   *out = nullptr;
   TN_TRY({
-    Plan* p = load_plan(json, len, cfg);
-    if (comm && comm->world > 1) {
-      delete p;
-      throw TnError{TN_E_UNSUPPORTED, "sharded stem (world > 1) is not implemented in this build"};
+    // virtual_world > 1 without a communicator: lower for that many ranks (host-only inspection
+    // of the sharded schedule; such a plan cannot be executed)
+    const int vworld = (!comm && cfg && cfg->virtual_world > 1) ? cfg->virtual_world : 1;
+    Plan* p = load_plan(json, len, cfg, comm ? comm->world : vworld);
+    if (comm) {
+      p->comm = comm;
+      p->rank = comm->rank;
     }
     *out = new tn_plan{p};
   });
@@ -392,19 +529,32 @@ int tn_sample_amplitudes(tn_plan* h, const tn_buffers* b, const uint64_t* prefix
       Scratch sc = scratch_of(p, W);
       std::vector<int> ex(p.n_exp_slots);
       TN_CUDA(cudaMemcpyAsync(ex.data(), sc.exps, 4 * ex.size(), cudaMemcpyDeviceToHost, s));
+      const void* res = b->d_stem[p.result_buf];
+      if (p.world > 1) {
+        // the result is sharded on final_shard: gather every rank's block (rank order)
+        const int eb = p.cfg.dtype == TN_CHALF ? 4 : 8;
+        const uint64_t n_local = n >> p.shard_log2;
+        nccl_allgather(res, b->d_stem[1 - p.result_buf], n_local * eb, NCCL_INT8, p.comm->nccl_comm, s);
+        res = b->d_stem[1 - p.result_buf];
+      }
       if (p.cfg.dtype == TN_CHALF) {
         std::vector<__half> buf(2 * n);
-        TN_CUDA(cudaMemcpyAsync(buf.data(), b->d_stem[p.result_buf], 4 * n, cudaMemcpyDeviceToHost, s));
+        TN_CUDA(cudaMemcpyAsync(buf.data(), res, 4 * n, cudaMemcpyDeviceToHost, s));
         TN_CUDA(cudaStreamSynchronize(s));
         for (uint64_t i = 0; i < 2 * n; ++i) vals[i] = (double)__half2float(buf[i]);
       } else {
         std::vector<float> buf(2 * n);
-        TN_CUDA(cudaMemcpyAsync(buf.data(), b->d_stem[p.result_buf], 8 * n, cudaMemcpyDeviceToHost, s));
+        TN_CUDA(cudaMemcpyAsync(buf.data(), res, 8 * n, cudaMemcpyDeviceToHost, s));
         TN_CUDA(cudaStreamSynchronize(s));
         for (uint64_t i = 0; i < 2 * n; ++i) vals[i] = buf[i];
       }
       for (int e : ex) E += e;
-      layout = p.final_perm ? p.open : p.final_layout;
+      if (p.final_perm) {
+        layout = p.open;
+      } else {
+        layout = p.final_shard;
+        layout.insert(layout.end(), p.final_layout.begin(), p.final_layout.end());
+      }
     }
     // reorder into `open` order and unscale exactly by 2^-E (a.9)
     const int r = (int)p.open.size();
@@ -509,6 +659,18 @@ int tn_dequant_int8(float* d_y, const int8_t* d_codes, const float* d_scales, co
   TN_TRY(launch_dequant_int8(d_y, d_codes, d_scales, d_zeros, n, g, (cudaStream_t)stream));
 }
 
+int tn_quant_int8_f16(int8_t* d_codes, float* d_scales, float* d_zeros, const void* d_x, uint64_t n, int g,
+                      void* stream) {
+  if (!d_codes || !d_scales || !d_zeros || !d_x) return fail(TN_E_INVALID, "NULL argument");
+  TN_TRY(launch_quant_int8_half(d_codes, d_scales, d_zeros, (const __half*)d_x, n, g, (cudaStream_t)stream));
+}
+
+int tn_dequant_int8_f16(void* d_y, const int8_t* d_codes, const float* d_scales, const float* d_zeros, uint64_t n,
+                        int g, void* stream) {
+  if (!d_y || !d_codes || !d_scales || !d_zeros) return fail(TN_E_INVALID, "NULL argument");
+  TN_TRY(launch_dequant_int8_half((__half*)d_y, d_codes, d_scales, d_zeros, n, g, (cudaStream_t)stream));
+}
+
 // ---- NCCL (dlopen'ed: the process's torch already carries libnccl.so.2) ----
 typedef struct {
   char internal[128];
@@ -517,24 +679,14 @@ typedef int (*nccl_get_uid_fn)(nccl_uid_t*);
 typedef int (*nccl_init_rank_fn)(void**, int, nccl_uid_t, int);
 typedef int (*nccl_destroy_fn)(void*);
 
-static void* nccl_sym(const char* name) {
-  static void* h = nullptr;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
-    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
-  });
-  return h ? dlsym(h, name) : nullptr;
-}
-
 int tn_comm_unique_id(uint8_t out[128]) {
   if (!out) return fail(TN_E_INVALID, "NULL argument");
-  auto fn = (nccl_get_uid_fn)nccl_sym("ncclGetUniqueId");
-  if (!fn) return fail(TN_E_NCCL, "libnccl.so.2 not loadable");
-  nccl_uid_t id;
-  if (fn(&id) != 0) return fail(TN_E_NCCL, "ncclGetUniqueId failed");
-  memcpy(out, id.internal, 128);
-  return TN_OK;
+  TN_TRY({
+    auto fn = (nccl_get_uid_fn)nccl_sym("ncclGetUniqueId");
+    nccl_uid_t id;
+    if (fn(&id) != 0) throw TnError{TN_E_NCCL, "ncclGetUniqueId failed"};
+    memcpy(out, id.internal, 128);
+  });
 }
 
 int tn_comm_init(const uint8_t uid[128], int rank, int world, int device, tn_comm** out) {
@@ -548,10 +700,12 @@ int tn_comm_init(const uint8_t uid[128], int rank, int world, int device, tn_com
     c->world = world;
     c->device = device;
     if (world > 1) {
-      auto fn = (nccl_init_rank_fn)nccl_sym("ncclCommInitRank");
-      if (!fn) {
+      nccl_init_rank_fn fn = nullptr;
+      try {
+        fn = (nccl_init_rank_fn)nccl_sym("ncclCommInitRank");
+      } catch (...) {
         delete c;
-        throw TnError{TN_E_NCCL, "libnccl.so.2 not loadable"};
+        throw;
       }
       nccl_uid_t id;
       memcpy(id.internal, uid, 128);
@@ -567,8 +721,11 @@ int tn_comm_init(const uint8_t uid[128], int rank, int world, int device, tn_com
 void tn_comm_free(tn_comm* c) {
   if (!c) return;
   if (c->nccl_comm) {
-    auto fn = (nccl_destroy_fn)nccl_sym("ncclCommDestroy");
-    if (fn) fn(c->nccl_comm);
+    try {
+      auto fn = (nccl_destroy_fn)nccl_sym("ncclCommDestroy");
+      fn(c->nccl_comm);
+    } catch (...) {
+    }
   }
   delete c;
 }

@@ -27,7 +27,8 @@ class TnError(RuntimeError):
 class tn_config(C.Structure):
     _fields_ = [("dtype", C.c_int32), ("stem_min_log2", C.c_int32), ("comm_codec", C.c_int32),
                 ("comm_group", C.c_int32), ("stem_capacity_bytes", C.c_uint64), ("split_log2", C.c_int32),
-                ("layout_policy", C.c_int32), ("reserved", C.c_int32 * 6)]
+                ("layout_policy", C.c_int32), ("quant_from_pct", C.c_int32), ("virtual_world", C.c_int32),
+                ("reserved", C.c_int32 * 4)]
 
 
 class tn_buffers(C.Structure):
@@ -70,6 +71,8 @@ def lib():
         L.tn_pad_b.argtypes = [vp, vp, C.c_uint32, C.c_uint32, vp, vp, vp, vp]
         L.tn_quant_int8.argtypes = [vp, vp, vp, vp, u64, i32, vp]
         L.tn_dequant_int8.argtypes = [vp, vp, vp, vp, u64, i32, vp]
+        L.tn_quant_int8_f16.argtypes = [vp, vp, vp, vp, u64, i32, vp]
+        L.tn_dequant_int8_f16.argtypes = [vp, vp, vp, vp, u64, i32, vp]
         L.tn_comm_unique_id.argtypes = [vp]
         L.tn_comm_init.argtypes = [vp, i32, i32, i32, C.POINTER(vp)]
         L.tn_comm_free.argtypes = [vp]
@@ -94,9 +97,11 @@ def _stream(stream):
 
 
 def make_config(dtype=TN_CHALF, stem_min_log2=20, comm_codec=TN_COMM_INT8, comm_group=128,
-                stem_capacity_bytes=0, split_log2=0, layout_policy=0):
+                stem_capacity_bytes=0, split_log2=0, layout_policy=0, virtual_world=1, quant_from_pct=-1):
     c = tn_config()
     c.layout_policy = layout_policy
+    c.virtual_world = virtual_world  # host-only lowering for several ranks (no communicator)
+    c.quant_from_pct = quant_from_pct
     c.dtype, c.stem_min_log2, c.comm_codec, c.comm_group = dtype, stem_min_log2, comm_codec, comm_group
     c.stem_capacity_bytes, c.split_log2 = stem_capacity_bytes, split_log2
     return c
@@ -114,7 +119,9 @@ class Plan:
         data = plan.encode() if isinstance(plan, str) else plan
         self._h = C.c_void_p()
         self.cfg = cfg or make_config()
-        _check(lib().tn_plan_load(data, len(data), C.byref(self.cfg), comm, C.byref(self._h)))
+        self.comm = comm  # keep the communicator alive as long as the plan
+        _check(lib().tn_plan_load(data, len(data), C.byref(self.cfg), comm.handle if comm is not None else None,
+                                  C.byref(self._h)))
 
     def __del__(self):
         if getattr(self, "_h", None) and _lib is not None:
@@ -220,5 +227,42 @@ def tn_quant_int8(codes, scales, zeros, x, g, stream=None):
     _check(lib().tn_quant_int8(_ptr(codes), _ptr(scales), _ptr(zeros), _ptr(x), x.numel(), g, _stream(stream)))
 
 
+def tn_quant_int8_f16(codes, scales, zeros, x, g, stream=None):
+    _check(lib().tn_quant_int8_f16(_ptr(codes), _ptr(scales), _ptr(zeros), _ptr(x), x.numel(), g, _stream(stream)))
+
+
+def tn_dequant_int8_f16(y, codes, scales, zeros, g, stream=None):
+    _check(lib().tn_dequant_int8_f16(_ptr(y), _ptr(codes), _ptr(scales), _ptr(zeros), y.numel(), g, _stream(stream)))
+
+
 def tn_dequant_int8(y, codes, scales, zeros, g, stream=None):
     _check(lib().tn_dequant_int8(_ptr(y), _ptr(codes), _ptr(scales), _ptr(zeros), y.numel(), g, _stream(stream)))
+
+
+class Comm:
+    """tn_comm_unique_id / tn_comm_init / tn_comm_free.  The library owns its NCCL communicator;
+    torch.distributed (already initialised) only broadcasts the unique id."""
+
+    def __init__(self, rank, world, device):
+        import torch.distributed as dist
+        L = lib()
+        uid = (C.c_uint8 * 128)()
+        obj = [None]
+        if rank == 0:
+            _check(L.tn_comm_unique_id(uid))
+            obj = [bytes(uid)]
+        if world > 1:
+            dist.broadcast_object_list(obj, src=0)
+        uid = (C.c_uint8 * 128)(*obj[0])
+        self._h = C.c_void_p()
+        _check(L.tn_comm_init(uid, rank, world, device, C.byref(self._h)))
+        self.rank, self.world = rank, world
+
+    @property
+    def handle(self):
+        return self._h
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.tn_comm_free(self._h)
+            self._h = None

@@ -220,3 +220,27 @@ def test_quant_int8_bit_exact_vs_oracle_codec(env, g):
     assert np.array_equal(codes.cpu().numpy().astype(np.float32), rc)
     assert np.array_equal(sc.cpu().numpy(), rs) and np.array_equal(ze.cpu().numpy(), rz)
     assert np.array_equal(y.cpu().numpy(), codec.dequantize(rc, rs, rz, 1.0, group=g))
+
+
+def test_quant_int8_f16_payload_bit_exact(env):
+    """The mode-swap codec on complex-half payloads (fp16 reals): codes/scales/zeros bit-exact vs
+    the oracle codec on the same float32 values; dequantised fp16 = oracle dequant rounded to fp16."""
+    torch, tn = env
+    rng = np.random.default_rng(3)
+    g = 128
+    x = (rng.standard_normal(g * 300) * 2000).astype(np.float16)
+    x[g:2 * g] = 0                           # all-zero group
+    x[2 * g:3 * g:2] = 0                     # half zeros (interleaved imaginary parts)
+    X = torch.from_numpy(x).cuda()
+    codes = torch.empty(x.size, dtype=torch.int8, device="cuda")
+    sc = torch.empty(x.size // g, dtype=torch.float32, device="cuda")
+    ze = torch.empty_like(sc)
+    tn.tn_quant_int8_f16(codes, sc, ze, X, g)
+    y = torch.empty_like(X)
+    tn.tn_dequant_int8_f16(y, codes, sc, ze, g)
+    torch.cuda.synchronize()
+    rc, rs, rz = codec.quantize(x.astype(np.float32), np.float32(-128), np.float32(127), 1.0, group=g)
+    assert np.array_equal(codes.cpu().numpy().astype(np.float32), rc)
+    assert np.array_equal(sc.cpu().numpy(), rs) and np.array_equal(ze.cpu().numpy(), rz)
+    assert np.array_equal(y.cpu().numpy(), codec.dequantize(rc, rs, rz, 1.0, group=g).astype(np.float16))
+    assert np.linalg.norm(y.cpu().numpy().astype(np.float64) - x) <= 0.01 * np.linalg.norm(x.astype(np.float64))
