@@ -4,9 +4,11 @@ Sycamore-style RQC network, largest stem 2^33 complex-half) on B200 — BASELINE
 "stem-contraction effective TFLOPS/GPU and subtask time-to-solution".
 
 A step = one subtask: tn_stem_contract (common phase + Eq. 6 padding + all stem steps) +
-tn_split_contract, inputs (leaves) resident in HBM.  value = aggregate effective TFLOPS over all
-ranks (8 flops per complex MAC of the stem GEMMs, reading C-A21) / max-over-ranks device time.
-Multi-GPU: replicas over independent slices (weak scaling, no data-path collective).
+tn_split_contract, inputs (leaves) resident in HBM.  value = effective TFLOPS of the job (8 flops
+per complex MAC of the stem GEMMs, reading C-A21) / max-over-ranks device time.
+Multi-GPU (C4): ONE subtask sharded across the N GPUs on its log2 N outermost modes, with
+int8-quantised (late-stage) or fp16 NCCL mode swaps (Alg. 1) — strong scaling.
+--replicas runs independent slices per GPU instead (weak scaling, no collective).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--plan c3]
 """
@@ -128,6 +130,8 @@ def main():
     ap.add_argument("--plan", default="c3")
     ap.add_argument("--oracle-log2", type=int, default=24)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--replicas", action="store_true", help="N>1: independent slices per GPU (weak scaling)")
+    ap.add_argument("--comm", default="int8", choices=["int8", "fp16"])
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -164,11 +168,14 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev_stream = torch.cuda.current_stream()
 
-    p = tn.Plan(plan_json, tn.make_config(dtype=tn.TN_CHALF, stem_min_log2=20))
+    sharded = world > 1 and not args.replicas
+    comm = tn.Comm(rank, world, local) if sharded else None
+    codec = tn.TN_COMM_INT8 if args.comm == "int8" else tn.TN_COMM_FP16
+    p = tn.Plan(plan_json, tn.make_config(dtype=tn.TN_CHALF, stem_min_log2=20, comm_codec=codec), comm=comm)
     info = p.info()
     bufs = tn.Buffers(p)
     n_sl = min(info["n_slices_log2"], 63)
-    slice_id = rank % (1 << n_sl) if n_sl else 0
+    slice_id = 0 if sharded else (rank % (1 << n_sl) if n_sl else 0)
     tn.tn_plan_upload(p, bufs)
 
     def step():
@@ -217,8 +224,10 @@ def main():
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         te_ms = float(tt.item())
 
-    flops = info["stem_flops"]
-    value = world * flops / (t_ms * 1e-3) / 1e12
+    # job flops: stem_flops is per rank (a shard does 1/N of the subtask's stem work when sharded;
+    # a replica does a whole subtask)
+    flops = info["stem_flops"] * world
+    value = flops / (t_ms * 1e-3) / 1e12
     hbm, tc_burst, tc_sus, src = peaks()
 
     # ---- roofline of the dominant kernel (from the timed region's CUDA events)
@@ -265,17 +274,20 @@ def main():
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "TFLOPS", "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": t_ms, "higher_is_better": True, "scaling": "weak",
+                "warmup": args.warmup, "ms_per_step": t_ms, "higher_is_better": True,
+                "scaling": "strong" if (sharded or world == 1) else "weak",
                 "vs_baseline": None, "dtype": "f16", "data": "synthetic",
                 "config": {"workload": WORKLOADS.get(args.plan, args.plan), "plan": f"plans/{args.plan}.json",
-                           "slice": "rank r runs slice r (replicas over independent subtasks)",
+                           "slice": ("slice 0 sharded over all ranks (C4), swaps: " + args.comm) if sharded else
+                                    "rank r runs slice r (replicas over independent subtasks)",
+                           "mode_swaps": rep.get("n_swaps", 0), "swap_bytes_per_rank": rep.get("swap_bytes", 0),
                            "stem_steps": info["n_stem_steps"], "permutes": info["n_permutes"],
                            "max_stem_log2": info["max_stem_log2"], "stem_flops": flops,
                            "l2": "inputs larger than L2 (stem tensors up to 32 GiB >> 126 MB)"},
                 "tflops_per_gpu": value / world, "subtask_ms": t_ms,
                 "breakdown_ms": {"common+prep": common_ms, "permute": perm_ms, "gemm": gemm_ms},
                 "roofline": roof,
-                "e2e": {"value": world * flops / (te_ms * 1e-3) / 1e12, "unit": "TFLOPS",
+                "e2e": {"value": flops / (te_ms * 1e-3) / 1e12, "unit": "TFLOPS",
                         "ms_per_step": te_ms, "h2d_bytes_per_step": info["h2d_bytes"],
                         "d2h_bytes_per_step": (4 << info["n_open"]) + 4 * (2 * info["n_stem_steps"] + 4)},
                 "gpu_launches": launches, "clocks": clocks}

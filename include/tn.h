@@ -109,6 +109,9 @@ typedef struct {
 
 TN_API const char* tn_last_error(void);
 TN_API int tn_version(void);
+/* Select the CUDA device for this thread's subsequent calls (libtn links its own CUDA runtime, so
+ * the caller's framework-level device selection is not implied). */
+TN_API int tn_set_device(int device);
 
 /* Parse + validate + lower a plan (host only; no device work, no allocation on the device).
  * json: the plan JSON (tensors with labels/dims-2 complex128 data, open legs, SSA tree, sliced

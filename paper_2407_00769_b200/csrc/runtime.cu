@@ -430,6 +430,10 @@ extern "C" {
 const char* tn_last_error(void) { return g_err.c_str(); }
 int tn_version(void) { return 1; }
 
+int tn_set_device(int device) {
+  TN_TRY(TN_CUDA(cudaSetDevice(device)));
+}
+
 int tn_plan_load(const char* json, size_t len, const tn_config* cfg, tn_comm* comm, tn_plan** out) {
   if (!json || !out) return fail(TN_E_INVALID, "NULL argument");
   *out = nullptr;

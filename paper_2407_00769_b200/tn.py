@@ -55,6 +55,7 @@ def lib():
         L = C.CDLL(LIB_PATH)
         vp, u64, i32 = C.c_void_p, C.c_uint64, C.c_int
         L.tn_last_error.restype = C.c_char_p
+        L.tn_set_device.argtypes = [C.c_int]
         L.tn_plan_load.argtypes = [C.c_char_p, C.c_size_t, C.POINTER(tn_config), vp, C.POINTER(vp)]
         L.tn_plan_info_get.argtypes = [vp, C.POINTER(tn_plan_info)]
         L.tn_plan_free.argtypes = [vp]
@@ -79,6 +80,19 @@ def lib():
         L.tn_comm_free.restype = None
         _lib = L
     return _lib
+
+
+def set_device(device=None):
+    """Make libtn's CUDA runtime use torch's current device (or `device`)."""
+    try:
+        import torch
+        if device is None:
+            if not torch.cuda.is_available():
+                return
+            device = torch.cuda.current_device()
+    except ImportError:
+        return
+    _check(lib().tn_set_device(int(device)))
 
 
 def _check(code):
@@ -120,6 +134,7 @@ class Plan:
         self._h = C.c_void_p()
         self.cfg = cfg or make_config()
         self.comm = comm  # keep the communicator alive as long as the plan
+        set_device()
         _check(lib().tn_plan_load(data, len(data), C.byref(self.cfg), comm.handle if comm is not None else None,
                                   C.byref(self._h)))
 
