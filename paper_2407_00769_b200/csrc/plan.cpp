@@ -221,9 +221,38 @@ Plan* load_plan(const char* json, size_t len, const tn_config* cfg_in, int world
     }
   }
   for (int l : p.open) next_use.erase(l);  // open legs are never contracted
+  // ---- split-type tail: 2^j chunks fix j open legs.  The chosen legs are
+  // the open legs that enter the stem earliest (longest tail); they sort outermost in every layout.
+  std::set<int> split_set;
+  if (cfg.split_log2 > 0 && entry_idx >= 0) {
+    if (world > 1) throw err(TN_E_UNSUPPORTED, "split-type tail with a sharded stem");
+    std::map<int, int> first_app;  // open leg -> first stem step whose INPUT holds it
+    for (int l : p.nodes[p.stem_entry].labels) first_app[l] = 0;
+    {
+      int prev = p.stem_entry;
+      for (size_t s = 0; s < step_nodes.size(); ++s) {
+        const Node& n = p.nodes[step_nodes[s]];
+        int br = (n.u == prev) ? n.v : n.u;
+        for (int l : p.nodes[br].labels)
+          if (!first_app.count(l)) first_app[l] = (int)s + 1;
+        prev = step_nodes[s];
+      }
+    }
+    std::vector<int> cand(p.open.begin(), p.open.end());
+    std::stable_sort(cand.begin(), cand.end(), [&](int a, int b) { return first_app[a] < first_app[b]; });
+    if ((int)cand.size() < cfg.split_log2) throw err(TN_E_INFEASIBLE, "split: fewer open legs than split modes");
+    for (int t = 0; t < cfg.split_log2; ++t) {
+      split_set.insert(cand[t]);
+      p.split_modes.push_back(cand[t]);
+      p.split_from = std::max(p.split_from, first_app[cand[t]]);
+    }
+    p.split_log2 = cfg.split_log2;
+    if (p.split_from >= (int)step_nodes.size()) throw err(TN_E_INFEASIBLE, "split: no tail step holds the split modes");
+  }
   auto nu = [&](int l) {
+    if (split_set.count(l)) return INF;  // split modes outermost, then the other open legs
     auto it = next_use.find(l);
-    return it == next_use.end() ? INF : it->second;
+    return it == next_use.end() ? INF - 1 : it->second;
   };
 
   // ---- steps
@@ -345,6 +374,12 @@ Plan* load_plan(const char* json, size_t len, const tn_config* cfg_in, int world
       bool suffix = true;
       for (size_t j = 0; j < R.size(); ++j)
         if (!bs.count(L[L.size() - R.size() + j])) suffix = false;
+      if ((int)s == p.split_from && !split_set.empty()) {
+        // entering the split tail: the split modes must be the outermost block (one permutation
+        // pass if they are not; kept modes sort by next use with the split modes first)
+        std::set<int> pre(L.begin(), L.begin() + std::min(L.size(), split_set.size()));
+        if (pre != split_set) suffix = false;
+      }
       if (!suffix) {
         by_next_use(kept);
         std::vector<int> PL = kept;
@@ -363,8 +398,10 @@ Plan* load_plan(const char* json, size_t len, const tn_config* cfg_in, int world
       if (policy == 0 || policy == 2) {
         if (s + 1 == step_nodes.size()) {
           // the last step writes the result directly in output order (local modes only)
+          for (int l : L)  // split tail: the split modes stay the outermost block
+            if (split_set.count(l)) out.push_back(l);
           for (int l : p.open)
-            if (std::find(shard.begin(), shard.end(), l) == shard.end()) out.push_back(l);
+            if (std::find(shard.begin(), shard.end(), l) == shard.end() && !split_set.count(l)) out.push_back(l);
           scatter = true;
         } else {
           // [rest by next use] ++ [kept ∩ R_next] ++ [new ∩ R_next]  (new innermost)
@@ -452,7 +489,46 @@ Plan* load_plan(const char* json, size_t len, const tn_config* cfg_in, int world
     }
     p.final_layout = L;
     p.final_shard = shard;
-    if (shard.empty() && L != p.open) {
+    if (!p.split_modes.empty()) {
+      // every tail step must keep the split modes as the outermost block of its input, of its
+      // permuted input and of its output, so chunk v is the contiguous slab v everywhere
+      const int j = (int)p.split_modes.size();
+      auto prefix_ok = [&](const std::vector<int>& lay) {
+        if ((int)lay.size() < j) return false;
+        std::set<int> pre(lay.begin(), lay.begin() + j);
+        return pre == split_set;
+      };
+      uint64_t cmax = 0;
+      for (size_t s = p.split_from; s < p.steps.size(); ++s) {
+        StemStep& st = p.steps[s];
+        std::vector<int> permuted;
+        for (int a : st.perm_axes) permuted.push_back(st.in_layout[a]);
+        // the first tail step's permutation runs on the whole stem before chunking
+        const bool in_ok = ((int)s == p.split_from && st.perm) ? true : prefix_ok(st.in_layout);
+        if (!in_ok || !prefix_ok(st.out_layout) || (st.perm && !prefix_ok(permuted)) || st.mlog < j)
+          throw err(TN_E_INFEASIBLE, "split: the split modes do not stay outermost in the tail (step " +
+                                         std::to_string(s) + ", from " + std::to_string(p.split_from) + ", in " +
+                                         std::to_string(prefix_ok(st.in_layout)) + " out " +
+                                         std::to_string(prefix_ok(st.out_layout)) + ")");
+        st.split = 1;
+        cmax = std::max<uint64_t>(cmax, 1ull << (st.in_layout.size() - j));
+        cmax = std::max<uint64_t>(cmax, 1ull << (st.out_layout.size() - j));
+      }
+      p.split_chunk_max = cmax;
+      p.final_perm = false;  // the host reorders the chunked result (each chunk has its own scale)
+      // the free buffer holds two chunk regions plus the assembled result
+      smax = std::max<uint64_t>(smax, 2 * cmax + (1ull << L.size()));
+      // the full-size tensors of the tail are never materialised: the stem buffers only need the
+      // tail's input (the stem entering the split point)
+      uint64_t need = 2 * cmax + (1ull << L.size());
+      for (int s = 0; s <= p.split_from && s < (int)p.steps.size(); ++s) {
+        const StemStep& st = p.steps[s];
+        need = std::max<uint64_t>(need, 1ull << st.in_layout.size());
+        if (s < p.split_from) need = std::max<uint64_t>(need, 1ull << st.out_layout.size());
+      }
+      smax = need;
+    }
+    if (shard.empty() && p.split_modes.empty() && L != p.open) {
       p.final_perm = true;
       for (int l : p.open) p.final_perm_axes.push_back((int)(std::find(L.begin(), L.end(), l) - L.begin()));
       p.perm_bytes += 2.0 * eb * std::ldexp(1.0, (int)L.size());
@@ -499,6 +575,11 @@ Plan* load_plan(const char* json, size_t len, const tn_config* cfg_in, int world
   p.n_exp_slots = (int)(2 * S + 4);
   // max_slot[S+2], b_bound[S+2], b_max[S+2], exps[n_exp_slots], entry_max (runtime.cu scratch_of)
   off += align_up(4 * 3 * (S + 2) + 4 * p.n_exp_slots + 4 + 64, 256);
+  if (!p.split_modes.empty()) {
+    // per chunk: max slots [T+1] and step exponents [T] of the tail (each chunk has its own scale)
+    const uint64_t T = p.steps.size() - p.split_from, c = 1ull << p.split_log2;
+    off += align_up(4 * c * (2 * T + 1) + 64, 256);
+  }
   p.ws_total = off;
   return P.release();
 }

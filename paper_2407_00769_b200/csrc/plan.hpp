@@ -76,6 +76,10 @@ struct Plan {
   std::vector<int> final_perm_axes;
   int split_from = -1;            // first split-type step index (-1: none)
   int split_log2 = 0;             // chunks = 2^split_log2
+  std::vector<int> split_modes;   // open legs fixed per chunk (outermost in every tail layout)
+  uint64_t split_chunk_max = 0;   // largest per-chunk stem tensor of the tail (elements)
+  int stem_cur = 0;               // buffer holding the stem after tn_stem_contract (split mode)
+  uint64_t result_off = 0;        // element offset of the result inside its buffer
   // workspace layout
   uint64_t ws_leaves = 0, ws_common = 0, ws_b = 0, ws_scratch = 0, ws_total = 0;
   uint64_t stem_elems_max = 0;    // largest stem tensor (elements)

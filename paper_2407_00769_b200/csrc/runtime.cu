@@ -305,6 +305,40 @@ void mode_swap(Plan& p, const StemStep& st, const tn_buffers* b, int& cur, cudaS
   cur = 1 - cur;
 }
 
+void rec_event(Plan& p, size_t k, cudaStream_t s) {
+  if (p.timing) TN_CUDA(cudaEventRecord((cudaEvent_t)p.ev[k], s));
+}
+
+// One stem GEMM (Eq. 6 on tcgen05, SIMT for small K*N, complex64 SIMT for the fp32 path) from
+// `src` to `dst`; mshift > 0 runs it on one chunk of the split tail (the top mshift m bits fixed).
+void run_gemm(Plan& p, const StemStep& st, size_t i, const void* src, void* dst, int mshift, const float* in_max,
+              uint32_t* out_max, int* exp_slot, unsigned char* W, const Scratch& sc, cudaStream_t s) {
+  const int mlog = st.mlog - mshift;
+  const uint64_t M = 1ull << mlog;
+  const uint32_t K = 1u << st.klog, N = 1u << st.nlog;
+  OutMap om;
+  memset(&om, 0, sizeof(om));
+  om.identity = st.out_identity ? 1 : 0;
+  om.mbits = mlog;
+  om.nbits = st.nlog;
+  for (int j = 0; j < mlog; ++j) om.ms[j] = st.m_stride[j];
+  for (int j = 0; j < st.nlog; ++j) om.ns[j] = st.n_stride[j];
+  if (p.cfg.dtype == TN_CHALF) {
+    if (st.tensor_core)
+      launch_gemm_chalf_tc(reinterpret_cast<__half*>(dst), reinterpret_cast<const __half*>(src),
+                           reinterpret_cast<const __half*>(W + st.b_off), M, 2 * K, 2 * N, in_max, &sc.b_bound[i],
+                           out_max, exp_slot, &om, s);
+    else
+      launch_gemm_chalf_simt(reinterpret_cast<__half2*>(dst), reinterpret_cast<const __half2*>(src),
+                             reinterpret_cast<const __half*>(W + st.b_off), M, K, N, in_max, &sc.b_bound[i], out_max,
+                             exp_slot, &om, s);
+  } else {
+    launch_gemm_c64(reinterpret_cast<float2*>(dst), reinterpret_cast<const float2*>(src),
+                    reinterpret_cast<const float2*>(W + st.b_off), M, K, N, &om, s);
+  }
+  ++p.launches;
+}
+
 void stem_contract(Plan& p, const tn_buffers* b, uint64_t slice_id, cudaStream_t s) {
   check_buffers(p, b);
   if (p.world > 1 && !p.comm) throw TnError{TN_E_INVALID, "plan lowered for several ranks without a communicator"};
@@ -367,11 +401,9 @@ void stem_contract(Plan& p, const tn_buffers* b, uint64_t slice_id, cudaStream_t
     }
   }
   int cur = 0;
-  auto rec = [&](size_t k) {
-    if (p.timing) TN_CUDA(cudaEventRecord((cudaEvent_t)p.ev[k], s));
-  };
-  rec(1);
-  for (size_t i = 0; i < p.steps.size(); ++i) {
+  rec_event(p, 1, s);
+  const size_t n_main = p.split_modes.empty() ? p.steps.size() : (size_t)p.split_from;
+  for (size_t i = 0; i < n_main; ++i) {
     const StemStep& st = p.steps[i];
     if (st.swap) {
       mode_swap(p, st, b, cur, s);
@@ -381,46 +413,91 @@ void stem_contract(Plan& p, const tn_buffers* b, uint64_t slice_id, cudaStream_t
       ++p.launches;
       cur = 1 - cur;
     }
-    rec(2 + 2 * i);
-    const uint64_t M = 1ull << st.mlog;
-    const uint32_t K = 1u << st.klog, N = 1u << st.nlog;
-    OutMap om;
-    memset(&om, 0, sizeof(om));
-    om.identity = st.out_identity ? 1 : 0;
-    om.mbits = st.mlog;
-    om.nbits = st.nlog;
-    for (int j = 0; j < st.mlog; ++j) om.ms[j] = st.m_stride[j];
-    for (int j = 0; j < st.nlog; ++j) om.ns[j] = st.n_stride[j];
-    if (p.cfg.dtype == TN_CHALF) {
-      const float* in_max = &sc.max_slot[i];
-      uint32_t* out_max = reinterpret_cast<uint32_t*>(&sc.max_slot[i + 1]);
-      if (st.tensor_core)
-        launch_gemm_chalf_tc(reinterpret_cast<__half*>(b->d_stem[1 - cur]), reinterpret_cast<const __half*>(b->d_stem[cur]),
-                             reinterpret_cast<const __half*>(W + st.b_off), M, 2 * K, 2 * N, in_max, &sc.b_bound[i],
-                             out_max, &sc.exps[2 + 2 * i], &om, s);
-      else
-        launch_gemm_chalf_simt(reinterpret_cast<__half2*>(b->d_stem[1 - cur]),
-                               reinterpret_cast<const __half2*>(b->d_stem[cur]),
-                               reinterpret_cast<const __half*>(W + st.b_off), M, K, N, in_max, &sc.b_bound[i], out_max,
-                               &sc.exps[2 + 2 * i], &om, s);
-      // every rank must scale the next step by the same power of two
-      if (p.world > 1) nccl_allreduce_max(&sc.max_slot[i + 1], 1, p.comm->nccl_comm, s);
-    } else {
-      launch_gemm_c64(reinterpret_cast<float2*>(b->d_stem[1 - cur]), reinterpret_cast<const float2*>(b->d_stem[cur]),
-                      reinterpret_cast<const float2*>(W + st.b_off), M, K, N, &om, s);
-    }
-    ++p.launches;
+    rec_event(p, 2 + 2 * i, s);
+    run_gemm(p, st, i, b->d_stem[cur], b->d_stem[1 - cur], 0, &sc.max_slot[i],
+             reinterpret_cast<uint32_t*>(&sc.max_slot[i + 1]), &sc.exps[2 + 2 * i], W, sc, s);
+    // every rank must scale the next step by the same power of two
+    if (p.world > 1 && p.cfg.dtype == TN_CHALF) nccl_allreduce_max(&sc.max_slot[i + 1], 1, p.comm->nccl_comm, s);
     cur = 1 - cur;
-    rec(3 + 2 * i);
+    rec_event(p, 3 + 2 * i, s);
   }
+  if (!p.split_modes.empty()) {
+    // entering the split tail: its first permutation (split modes outermost) runs on the whole stem
+    const StemStep& st = p.steps[p.split_from];
+    if (st.perm) {
+      launch_permute(b->d_stem[1 - cur], b->d_stem[cur], eb, (int)st.in_layout.size(), st.perm_axes.data(), s);
+      ++p.launches;
+      cur = 1 - cur;
+    }
+    p.stem_cur = cur;
+    return;  // the chunked tail runs in tn_split_contract
+  }
+  p.stem_cur = cur;
   if (p.final_perm) {
     launch_permute(b->d_stem[1 - cur], b->d_stem[cur], eb, (int)p.final_layout.size(), p.final_perm_axes.data(), s);
     ++p.launches;
     cur = 1 - cur;
   }
-  rec(2 + 2 * p.steps.size());
+  rec_event(p, 2 + 2 * p.steps.size(), s);
   p.ev_valid = p.timing != 0;
   p.result_buf = cur;
+  p.result_off = 0;
+}
+
+// Split-type tail ("dividing the stem tensor into smaller chunks", P:22 chunks inside the
+// double buffers, P:526 chunk count from capacity).  The split modes are the outermost modes of
+// every tail layout, so chunk v is the contiguous slab v of each tail tensor: chunk v's input is
+// read in place from the stem buffer, its intermediates ping-pong between two chunk regions at the
+// start of the other buffer, and its result lands in slot v of a result region behind them.  Each
+// chunk keeps its own max/exponent chain (the first tail step starts from the global bound).
+void split_contract(Plan& p, const tn_buffers* b, cudaStream_t s) {
+  if (p.split_modes.empty()) return;
+  check_buffers(p, b);
+  unsigned char* W = static_cast<unsigned char*>(b->d_ws);
+  Scratch sc = scratch_of(p, W);
+  const int eb = p.cfg.dtype == TN_CHALF ? 4 : 8;
+  const int j = (int)p.split_modes.size();
+  const uint64_t chunks = 1ull << j, T = p.steps.size() - p.split_from, cmax = p.split_chunk_max;
+  const uint64_t chunk_in = 1ull << (p.steps[p.split_from].in_layout.size() - j);
+  const uint64_t chunk_out = 1ull << (p.final_layout.size() - j);
+  if ((2 * cmax + chunks * chunk_out) * eb > b->stem_bytes)
+    throw TnError{TN_E_CAPACITY, "split tail: chunk regions do not fit the free stem buffer"};
+  unsigned char* X = static_cast<unsigned char*>(b->d_stem[p.stem_cur]);
+  unsigned char* Y = static_cast<unsigned char*>(b->d_stem[1 - p.stem_cur]);
+  unsigned char* RA = Y;
+  unsigned char* RB = Y + cmax * eb;
+  unsigned char* RES = Y + 2 * cmax * eb;
+  float* cmaxs = reinterpret_cast<float*>(sc.entry_max + 1);   // [chunks][T+1]
+  int* cexps = reinterpret_cast<int*>(cmaxs + chunks * (T + 1));  // [chunks][T]
+  // timing: the whole chunked tail is attributed to the final interval of the report
+  for (uint64_t t = 0; t < T; ++t) {
+    rec_event(p, 2 + 2 * (p.split_from + t), s);
+    rec_event(p, 3 + 2 * (p.split_from + t), s);
+  }
+  for (uint64_t v = 0; v < chunks; ++v) {
+    unsigned char* current = X + v * chunk_in * eb;
+    for (uint64_t t = 0; t < T; ++t) {
+      const size_t i = p.split_from + t;
+      const StemStep& st = p.steps[i];
+      if (st.perm && t > 0) {  // (the first tail step's permutation ran on the whole stem)
+        unsigned char* dst = (current == RA) ? RB : RA;
+        std::vector<int> axes;
+        for (size_t a = j; a < st.perm_axes.size(); ++a) axes.push_back(st.perm_axes[a] - j);
+        launch_permute(dst, current, eb, (int)st.in_layout.size() - j, axes.data(), s);
+        ++p.launches;
+        current = dst;
+      }
+      unsigned char* dst = (t + 1 == T) ? RES + v * chunk_out * eb : ((current == RA) ? RB : RA);
+      const float* in_max = t == 0 ? &sc.max_slot[i] : &cmaxs[v * (T + 1) + t];
+      run_gemm(p, st, i, current, dst, j, in_max, reinterpret_cast<uint32_t*>(&cmaxs[v * (T + 1) + t + 1]),
+               &cexps[v * T + t], W, sc, s);
+      current = dst;
+    }
+  }
+  rec_event(p, 2 + 2 * p.steps.size(), s);
+  p.ev_valid = p.timing != 0;
+  p.result_buf = 1 - p.stem_cur;
+  p.result_off = 2 * cmax;
 }
 
 }  // namespace
@@ -504,8 +581,7 @@ int tn_stem_contract(tn_plan* h, const tn_buffers* b, uint64_t slice_id, void* s
 
 int tn_split_contract(tn_plan* h, const tn_buffers* b, void* stream) {
   if (!h || !b) return fail(TN_E_INVALID, "NULL argument");
-  (void)stream;
-  return TN_OK;  // split-type tail steps run inside tn_stem_contract when split_log2 == 0
+  TN_TRY(split_contract(*h->p, b, (cudaStream_t)stream));  // no-op without a split tail
 }
 
 int tn_sample_amplitudes(tn_plan* h, const tn_buffers* b, const uint64_t* prefixes, size_t n_sub, double* h_amps,
@@ -533,7 +609,19 @@ int tn_sample_amplitudes(tn_plan* h, const tn_buffers* b, const uint64_t* prefix
       Scratch sc = scratch_of(p, W);
       std::vector<int> ex(p.n_exp_slots);
       TN_CUDA(cudaMemcpyAsync(ex.data(), sc.exps, 4 * ex.size(), cudaMemcpyDeviceToHost, s));
-      const void* res = b->d_stem[p.result_buf];
+      const int ebr = p.cfg.dtype == TN_CHALF ? 4 : 8;
+      const void* res = static_cast<const unsigned char*>(b->d_stem[p.result_buf]) + p.result_off * ebr;
+      std::vector<int> chunk_e;  // split tail: each chunk's own exponent sum
+      if (!p.split_modes.empty()) {
+        const uint64_t chunks = 1ull << p.split_modes.size(), T = p.steps.size() - p.split_from;
+        std::vector<int> ce(chunks * T);
+        const float* cmaxs = reinterpret_cast<const float*>(sc.entry_max + 1);
+        TN_CUDA(cudaMemcpyAsync(ce.data(), cmaxs + chunks * (T + 1), 4 * ce.size(), cudaMemcpyDeviceToHost, s));
+        TN_CUDA(cudaStreamSynchronize(s));
+        chunk_e.assign(chunks, 0);
+        for (uint64_t v = 0; v < chunks; ++v)
+          for (uint64_t t = 0; t < T; ++t) chunk_e[v] += ce[v * T + t];
+      }
       if (p.world > 1) {
         // the result is sharded on final_shard: gather every rank's block (rank order)
         const int eb = p.cfg.dtype == TN_CHALF ? 4 : 8;
@@ -558,6 +646,15 @@ int tn_sample_amplitudes(tn_plan* h, const tn_buffers* b, const uint64_t* prefix
       } else {
         layout = p.final_shard;
         layout.insert(layout.end(), p.final_layout.begin(), p.final_layout.end());
+      }
+      if (!chunk_e.empty()) {
+        // chunk v = top j bits of the result index (split modes outermost): apply its exponent
+        const int j = (int)p.split_modes.size(), r = (int)layout.size();
+        for (uint64_t i = 0; i < n; ++i) {
+          const int sh = -chunk_e[i >> (r - j)];
+          vals[2 * i] = std::ldexp(vals[2 * i], sh);
+          vals[2 * i + 1] = std::ldexp(vals[2 * i + 1], sh);
+        }
       }
     }
     // reorder into `open` order and unscale exactly by 2^-E (a.9)

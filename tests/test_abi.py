@@ -121,3 +121,21 @@ def test_header_documents_citations():
     src = open(os.path.join(ROOT, "include", "tn.h")).read()
     for cite in ("P:496-514", "P:18-22", "P:230", "Eq. 1"):
         assert cite in src
+
+
+@pytest.mark.parametrize("j", [1, 2, 3])
+def test_split_tail_lowering(tnmod, j):
+    """Split modes are open legs, stay the outermost block through the tail, and are never
+    contracted there (chunks of the stem contract with chunked non-stem inputs)."""
+    with open(os.path.join(ROOT, "plans", "c3.json")) as f:
+        plan = json.load(f)
+    for policy in (0, 2):
+        p = _load(tnmod, plan, stem_min_log2=20, split_log2=j, layout_policy=policy)
+        rep = p.report()
+        assert p.info()["split_chunks"] == 2 ** j
+        tail = [s for s in rep["steps"] if s["split"]]
+        assert tail and tail[-1] is rep["steps"][-1]
+        first = tail[0]["out"][:j]
+        assert set(first) <= set(plan["open"])
+        for s in tail:
+            assert s["out"][:j] == first and not (set(s["R"]) & set(first))

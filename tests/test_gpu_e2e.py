@@ -103,3 +103,23 @@ def test_slice_id_out_of_range(tn):
     with pytest.raises(tn.TnError) as e:
         tn.tn_stem_contract(p, bufs, 1 << len(plan["sliced"]))
     assert e.value.code == -1
+
+
+@pytest.mark.parametrize("policy", [0, 2])
+@pytest.mark.parametrize("split", [1, 2, 3])
+@pytest.mark.parametrize("dtype", [0, 1])
+def test_split_tail_vs_oracle(tn, split, policy, dtype):
+    """Split-type tail: the last stem steps run on 2^j chunks inside the
+    stem buffers.  Same amplitudes as the oracle; the complex64 path is bit-identical to the
+    unsplit run (chunking does not change any per-element sum)."""
+    sub = MP.sub_slice(_plan("c2"), 20)
+    ref = contract.contract(load(sub), 0)
+    p = tn.Plan(sub, tn.make_config(dtype=dtype, stem_min_log2=12, split_log2=split, layout_policy=policy))
+    assert p.info()["split_chunks"] == 2 ** split
+    rep = p.report()
+    assert sum(s["split"] for s in rep["steps"]) >= 1
+    got = tn.contract(p, tn.Buffers(p), 0)
+    assert metrics.rel_l2(got, ref) <= TOL[dtype]
+    if dtype == 1:
+        p0 = tn.Plan(sub, tn.make_config(dtype=dtype, stem_min_log2=12, layout_policy=policy))
+        assert np.array_equal(tn.contract(p0, tn.Buffers(p0), 0), got)
