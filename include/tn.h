@@ -140,11 +140,16 @@ TN_API int tn_stem_contract(tn_plan* p, const tn_buffers* b, uint64_t slice_id, 
  * Asynchronous. */
 TN_API int tn_split_contract(tn_plan* p, const tn_buffers* b, void* stream);
 
-/* Read the result: h_amps receives 2 * 2^n_open doubles (interleaved re, im) of the partial
- * amplitudes a_s over the open legs in plan order (slowest first), unscaled exactly by the
- * accumulated power-of-two exponent (reading C-A8).  prefixes/n_sub reserved for the sparse-state
- * batch (must be NULL/0 in this build); k/top_idx: if top_idx != NULL, receives the k most
- * probable member indices (ties -> smaller index, C-A23).  SYNCHRONOUS (writes host memory). */
+/* Read the result, SYNCHRONOUS (writes host memory).
+ * Dense (prefixes == NULL, n_sub == 0): h_amps receives 2 * 2^n_open doubles (interleaved re, im)
+ * of the partial amplitudes a_s over the open legs in plan order (slowest first), unscaled exactly
+ * by the accumulated power-of-two exponents (reading C-A8); top_idx (if not NULL) receives the k
+ * most probable indices (ties -> smaller index, C-A23).
+ * Sparse-state batch (Fig. 5; needs cfg.split_log2 = j > 0): prefixes[i] < 2^j selects a
+ * correlated subspace = one value of the j split legs (bit j-1-t of the prefix <-> the t-th entry of
+ * "split_modes" in tn_report_json); only those chunks of the tail are contracted.  h_amps receives
+ * n_sub blocks of 2^(n_open-j) amplitudes (members = the other open legs in plan order); top_idx
+ * receives n_sub*k member indices, k = 1 computed on the device (post-selection). */
 TN_API int tn_sample_amplitudes(tn_plan* p, const tn_buffers* b, const uint64_t* prefixes, size_t n_sub,
                          double* h_amps, int k, uint64_t* top_idx, void* stream);
 

@@ -82,6 +82,7 @@ void launch_gemm_chalf_tc(__half* c, const __half* a, const __half* bp, uint64_t
                           uint32_t N2, const float* in_max, const float* b_bound, uint32_t* out_max,
                           int* exp_slot, const OutMap* om, cudaStream_t s);
 OutMap identity_map(uint64_t M, uint32_t N);
+void launch_top1_chalf(const __half2* amps, uint64_t n_sub, uint64_t members, uint64_t* top, cudaStream_t s);
 void launch_quant_int8(int8_t* codes, float* scales, float* zeros, const float* x, uint64_t n, int g,
                        cudaStream_t s);
 void launch_dequant_int8(float* y, const int8_t* codes, const float* scales, const float* zeros,

@@ -515,6 +515,16 @@ Plan* load_plan(const char* json, size_t len, const tn_config* cfg_in, int world
         cmax = std::max<uint64_t>(cmax, 1ull << (st.out_layout.size() - j));
       }
       p.split_chunk_max = cmax;
+      // chunk v = value v of the split legs in the order of the first tail step's (permuted) input
+      {
+        const StemStep& f = p.steps[p.split_from];
+        std::vector<int> lay0;
+        if (f.perm)
+          for (int a : f.perm_axes) lay0.push_back(f.in_layout[a]);
+        else
+          lay0 = f.in_layout;
+        p.split_modes.assign(lay0.begin(), lay0.begin() + j);
+      }
       p.final_perm = false;  // the host reorders the chunked result (each chunk has its own scale)
       // the free buffer holds two chunk regions plus the assembled result
       smax = std::max<uint64_t>(smax, 2 * cmax + (1ull << L.size()));
@@ -578,7 +588,8 @@ Plan* load_plan(const char* json, size_t len, const tn_config* cfg_in, int world
   if (!p.split_modes.empty()) {
     // per chunk: max slots [T+1] and step exponents [T] of the tail (each chunk has its own scale)
     const uint64_t T = p.steps.size() - p.split_from, c = 1ull << p.split_log2;
-    off += align_up(4 * c * (2 * T + 1) + 64, 256);
+    // + the post-selected member of each subspace (uint64 per chunk)
+    off += align_up(4 * c * (2 * T + 1) + 8 * c + 64, 256);
   }
   p.ws_total = off;
   return P.release();
@@ -627,6 +638,9 @@ std::string report_json(const Plan& p, const std::vector<float>& ms) {
   }
   o << "],\"entry_layout\":";
   jlist(o, p.stem_entry >= 0 ? p.nodes[p.stem_entry].labels : std::vector<int>());
+  o << ",\"split_modes\":";
+  jlist(o, p.split_modes);
+  o << ",\"split_from\":" << p.split_from;
   o << ",\"shard0\":";
   jlist(o, p.shard0);
   o << ",\"final_layout\":";

@@ -80,6 +80,7 @@ struct Plan {
   uint64_t split_chunk_max = 0;   // largest per-chunk stem tensor of the tail (elements)
   int stem_cur = 0;               // buffer holding the stem after tn_stem_contract (split mode)
   uint64_t result_off = 0;        // element offset of the result inside its buffer
+  std::vector<uint64_t> tail_slots;  // chunk id held by each result slot of the last tail run
   // workspace layout
   uint64_t ws_leaves = 0, ws_common = 0, ws_b = 0, ws_scratch = 0, ws_total = 0;
   uint64_t stem_elems_max = 0;    // largest stem tensor (elements)

@@ -450,7 +450,9 @@ void stem_contract(Plan& p, const tn_buffers* b, uint64_t slice_id, cudaStream_t
 // read in place from the stem buffer, its intermediates ping-pong between two chunk regions at the
 // start of the other buffer, and its result lands in slot v of a result region behind them.  Each
 // chunk keeps its own max/exponent chain (the first tail step starts from the global bound).
-void split_contract(Plan& p, const tn_buffers* b, cudaStream_t s) {
+// ids == nullptr: every chunk, result slot v = chunk v.  Otherwise only the listed chunks (the
+// sparse-state batch of P:525-537: only the requested prefixes are contracted), slot i = ids[i].
+void split_contract(Plan& p, const tn_buffers* b, cudaStream_t s, const std::vector<uint64_t>* ids = nullptr) {
   if (p.split_modes.empty()) return;
   check_buffers(p, b);
   unsigned char* W = static_cast<unsigned char*>(b->d_ws);
@@ -458,6 +460,13 @@ void split_contract(Plan& p, const tn_buffers* b, cudaStream_t s) {
   const int eb = p.cfg.dtype == TN_CHALF ? 4 : 8;
   const int j = (int)p.split_modes.size();
   const uint64_t chunks = 1ull << j, T = p.steps.size() - p.split_from, cmax = p.split_chunk_max;
+  const uint64_t nsel = ids ? ids->size() : chunks;
+  if (nsel > chunks) throw TnError{TN_E_INVALID, "more prefixes than chunks"};
+  if (ids)
+    for (uint64_t v : *ids)
+      if (v >= chunks) throw TnError{TN_E_INVALID, "prefix out of range"};
+  p.tail_slots.assign(nsel, 0);
+  for (uint64_t i = 0; i < nsel; ++i) p.tail_slots[i] = ids ? (*ids)[i] : i;
   const uint64_t chunk_in = 1ull << (p.steps[p.split_from].in_layout.size() - j);
   const uint64_t chunk_out = 1ull << (p.final_layout.size() - j);
   if ((2 * cmax + chunks * chunk_out) * eb > b->stem_bytes)
@@ -474,7 +483,10 @@ void split_contract(Plan& p, const tn_buffers* b, cudaStream_t s) {
     rec_event(p, 2 + 2 * (p.split_from + t), s);
     rec_event(p, 3 + 2 * (p.split_from + t), s);
   }
-  for (uint64_t v = 0; v < chunks; ++v) {
+  // fresh per-slot scale chains (the tail may run again for a sparse-state batch)
+  TN_CUDA(cudaMemsetAsync(cmaxs, 0, 4 * chunks * (2 * T + 1), s));
+  for (uint64_t sl = 0; sl < nsel; ++sl) {
+    const uint64_t v = p.tail_slots[sl];  // chunk id; `sl` indexes the result slot and scratch
     unsigned char* current = X + v * chunk_in * eb;
     for (uint64_t t = 0; t < T; ++t) {
       const size_t i = p.split_from + t;
@@ -487,10 +499,10 @@ void split_contract(Plan& p, const tn_buffers* b, cudaStream_t s) {
         ++p.launches;
         current = dst;
       }
-      unsigned char* dst = (t + 1 == T) ? RES + v * chunk_out * eb : ((current == RA) ? RB : RA);
-      const float* in_max = t == 0 ? &sc.max_slot[i] : &cmaxs[v * (T + 1) + t];
-      run_gemm(p, st, i, current, dst, j, in_max, reinterpret_cast<uint32_t*>(&cmaxs[v * (T + 1) + t + 1]),
-               &cexps[v * T + t], W, sc, s);
+      unsigned char* dst = (t + 1 == T) ? RES + sl * chunk_out * eb : ((current == RA) ? RB : RA);
+      const float* in_max = t == 0 ? &sc.max_slot[i] : &cmaxs[sl * (T + 1) + t];
+      run_gemm(p, st, i, current, dst, j, in_max, reinterpret_cast<uint32_t*>(&cmaxs[sl * (T + 1) + t + 1]),
+               &cexps[sl * T + t], W, sc, s);
       current = dst;
     }
   }
@@ -498,6 +510,93 @@ void split_contract(Plan& p, const tn_buffers* b, cudaStream_t s) {
   p.ev_valid = p.timing != 0;
   p.result_buf = 1 - p.stem_cur;
   p.result_off = 2 * cmax;
+}
+
+// Sparse-state batch (Fig. 5): the requested correlated subspaces are the prefix values
+// of the split legs; only those chunks of the tail are contracted (a gather on the stem operand,
+// the branches do not depend on the prefix).  Writes n_sub blocks of 2^(n_open - j) amplitudes
+// (members in `open` order without the split legs), unscaled exactly (a.9), and the post-selected
+// member of each subspace (device top-1, ties -> smaller index, C-A23).
+void sample_sparse(Plan& p, const tn_buffers* b, const uint64_t* prefixes, size_t n_sub, double* h_amps, int k,
+                   uint64_t* top_idx, cudaStream_t s) {
+  if (p.split_modes.empty())
+    throw TnError{TN_E_UNSUPPORTED, "sparse-state batch needs a split plan (cfg.split_log2 = prefix legs)"};
+  if (p.world > 1) throw TnError{TN_E_UNSUPPORTED, "sparse-state batch with a sharded stem"};
+  std::vector<uint64_t> ids(prefixes, prefixes + n_sub);
+  split_contract(p, b, s, &ids);
+  unsigned char* W = static_cast<unsigned char*>(b->d_ws);
+  Scratch sc = scratch_of(p, W);
+  const int eb = p.cfg.dtype == TN_CHALF ? 4 : 8;
+  const int j = (int)p.split_modes.size();
+  const uint64_t chunks = 1ull << j, T = p.steps.size() - p.split_from;
+  const std::vector<int> lay(p.final_layout.begin() + j, p.final_layout.end());
+  const uint64_t members = 1ull << lay.size();
+  const unsigned char* res = static_cast<const unsigned char*>(b->d_stem[p.result_buf]) + p.result_off * eb;
+  std::vector<uint64_t> top_dev;
+  if (top_idx && k == 1 && p.cfg.dtype == TN_CHALF) {
+    // behind the per-chunk scale chains in the split scratch (the stem must stay intact: a later
+    // dense readout re-runs the tail from it)
+    const float* cm = reinterpret_cast<const float*>(sc.entry_max + 1);
+    uintptr_t top_addr = reinterpret_cast<uintptr_t>(cm + chunks * (2 * T + 1));
+    uint64_t* d_top = reinterpret_cast<uint64_t*>((top_addr + 7) & ~(uintptr_t)7);
+    launch_top1_chalf(reinterpret_cast<const __half2*>(res), n_sub, members, d_top, s);
+    top_dev.resize(n_sub);
+    TN_CUDA(cudaMemcpyAsync(top_dev.data(), d_top, 8 * n_sub, cudaMemcpyDeviceToHost, s));
+  }
+  std::vector<int> ex(p.n_exp_slots), ce(chunks * T);
+  TN_CUDA(cudaMemcpyAsync(ex.data(), sc.exps, 4 * ex.size(), cudaMemcpyDeviceToHost, s));
+  const float* cmaxs = reinterpret_cast<const float*>(sc.entry_max + 1);
+  TN_CUDA(cudaMemcpyAsync(ce.data(), cmaxs + chunks * (T + 1), 4 * ce.size(), cudaMemcpyDeviceToHost, s));
+  std::vector<double> vals(2 * n_sub * members);
+  if (p.cfg.dtype == TN_CHALF) {
+    std::vector<__half> buf(2 * n_sub * members);
+    TN_CUDA(cudaMemcpyAsync(buf.data(), res, 4 * n_sub * members, cudaMemcpyDeviceToHost, s));
+    TN_CUDA(cudaStreamSynchronize(s));
+    for (size_t i = 0; i < buf.size(); ++i) vals[i] = (double)__half2float(buf[i]);
+  } else {
+    std::vector<float> buf(2 * n_sub * members);
+    TN_CUDA(cudaMemcpyAsync(buf.data(), res, 8 * n_sub * members, cudaMemcpyDeviceToHost, s));
+    TN_CUDA(cudaStreamSynchronize(s));
+    for (size_t i = 0; i < buf.size(); ++i) vals[i] = buf[i];
+  }
+  int E = 0;
+  for (int e : ex) E += e;
+  // member order: the open legs without the split legs, in `open` order
+  std::vector<int> mord;
+  for (int l : p.open)
+    if (std::find(p.split_modes.begin(), p.split_modes.end(), l) == p.split_modes.end()) mord.push_back(l);
+  const int r = (int)lay.size();
+  std::vector<int> pos(r);
+  for (int i = 0; i < r; ++i) pos[i] = (int)(std::find(lay.begin(), lay.end(), mord[i]) - lay.begin());
+  auto lay_index = [&](uint64_t o) {  // member index in `mord` order -> index in layout order
+    uint64_t src = 0;
+    for (int i = 0; i < r; ++i)
+      if ((o >> (r - 1 - i)) & 1) src |= 1ull << (r - 1 - pos[i]);
+    return src;
+  };
+  std::vector<uint64_t> inv(members);
+  for (uint64_t o = 0; o < members; ++o) inv[lay_index(o)] = o;
+  for (size_t sl = 0; sl < n_sub; ++sl) {
+    int Ev = E;
+    for (uint64_t t = 0; t < T; ++t) Ev += ce[sl * T + t];
+    for (uint64_t o = 0; o < members; ++o) {
+      const uint64_t src = sl * members + lay_index(o);
+      h_amps[2 * (sl * members + o)] = std::ldexp(vals[2 * src], -Ev);
+      h_amps[2 * (sl * members + o) + 1] = std::ldexp(vals[2 * src + 1], -Ev);
+    }
+    if (top_idx && k > 0) {
+      if (!top_dev.empty()) {
+        top_idx[sl] = inv[top_dev[sl]];
+      } else {
+        std::vector<uint64_t> idx(members);
+        for (uint64_t i = 0; i < members; ++i) idx[i] = i;
+        const double* a = h_amps + 2 * sl * members;
+        auto prob = [&](uint64_t i) { return a[2 * i] * a[2 * i] + a[2 * i + 1] * a[2 * i + 1]; };
+        std::stable_sort(idx.begin(), idx.end(), [&](uint64_t x, uint64_t y) { return prob(x) > prob(y); });
+        for (int q = 0; q < k && (uint64_t)q < members; ++q) top_idx[sl * k + q] = idx[q];
+      }
+    }
+  }
 }
 
 }  // namespace
@@ -587,7 +686,10 @@ int tn_split_contract(tn_plan* h, const tn_buffers* b, void* stream) {
 int tn_sample_amplitudes(tn_plan* h, const tn_buffers* b, const uint64_t* prefixes, size_t n_sub, double* h_amps,
                          int k, uint64_t* top_idx, void* stream) {
   if (!h || !b || !h_amps) return fail(TN_E_INVALID, "NULL argument");
-  if (prefixes || n_sub) return fail(TN_E_UNSUPPORTED, "sparse-state prefixes not supported in this build");
+  if ((prefixes == nullptr) != (n_sub == 0)) return fail(TN_E_INVALID, "prefixes and n_sub must come together");
+  if (prefixes) {
+    TN_TRY(sample_sparse(*h->p, b, prefixes, n_sub, h_amps, k, top_idx, (cudaStream_t)stream));
+  }
   TN_TRY({
     Plan& p = *h->p;
     cudaStream_t s = (cudaStream_t)stream;
@@ -610,6 +712,12 @@ int tn_sample_amplitudes(tn_plan* h, const tn_buffers* b, const uint64_t* prefix
       std::vector<int> ex(p.n_exp_slots);
       TN_CUDA(cudaMemcpyAsync(ex.data(), sc.exps, 4 * ex.size(), cudaMemcpyDeviceToHost, s));
       const int ebr = p.cfg.dtype == TN_CHALF ? 4 : 8;
+      if (!p.split_modes.empty()) {
+        // dense readout needs every chunk in its own slot (a sparse batch may have run last)
+        bool all = p.tail_slots.size() == (1ull << p.split_modes.size());
+        for (size_t i = 0; all && i < p.tail_slots.size(); ++i) all = p.tail_slots[i] == i;
+        if (!all) split_contract(p, b, s);
+      }
       const void* res = static_cast<const unsigned char*>(b->d_stem[p.result_buf]) + p.result_off * ebr;
       std::vector<int> chunk_e;  // split tail: each chunk's own exponent sum
       if (!p.split_modes.empty()) {
@@ -645,7 +753,12 @@ int tn_sample_amplitudes(tn_plan* h, const tn_buffers* b, const uint64_t* prefix
         layout = p.open;
       } else {
         layout = p.final_shard;
-        layout.insert(layout.end(), p.final_layout.begin(), p.final_layout.end());
+        if (!p.split_modes.empty()) {  // slot v = chunk v: split legs in chunk order, then the rest
+          layout.insert(layout.end(), p.split_modes.begin(), p.split_modes.end());
+          layout.insert(layout.end(), p.final_layout.begin() + p.split_modes.size(), p.final_layout.end());
+        } else {
+          layout.insert(layout.end(), p.final_layout.begin(), p.final_layout.end());
+        }
       }
       if (!chunk_e.empty()) {
         // chunk v = top j bits of the result index (split modes outermost): apply its exponent

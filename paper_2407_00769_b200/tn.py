@@ -200,6 +200,22 @@ def tn_sample_amplitudes(plan, bufs, k=0, stream=None):
     return amps, (top[:k].copy() if k > 0 else None)
 
 
+def tn_sample_sparse(plan, bufs, prefixes, k=1, stream=None):
+    """Sparse-state batch: amplitudes of the correlated subspaces `prefixes` (values of the split
+    legs) and the post-selected member of each.  Returns (complex128 [n_sub, members], top [n_sub, k])."""
+    import numpy as np
+    info = plan.info()
+    j = int(np.log2(info["split_chunks"]))
+    members = 1 << (info["n_open"] - j)
+    pre = np.ascontiguousarray(np.asarray(prefixes, dtype=np.uint64))
+    out = np.empty(2 * len(pre) * members, dtype=np.float64)
+    top = np.empty(max(1, len(pre) * max(k, 1)), dtype=np.uint64)
+    _check(lib().tn_sample_amplitudes(plan._h, C.byref(bufs.c), pre.ctypes.data, len(pre), out.ctypes.data, k,
+                                      top.ctypes.data if k > 0 else None, _stream(stream)))
+    amps = (out[0::2] + 1j * out[1::2]).reshape(len(pre), members)
+    return amps, (top[:len(pre) * k].reshape(len(pre), k) if k > 0 else None)
+
+
 def contract(plan, bufs, slice_id=0, stream=None, upload=True):
     """Public one-call API: upload leaves, contract one slice, read the amplitudes."""
     if upload:
