@@ -62,7 +62,9 @@ typedef struct tn_comm tn_comm;
 typedef struct {
   int32_t dtype;             /* TN_CHALF | TN_CFLOAT */
   int32_t stem_min_log2;     /* stem steps begin at the first stem node holding >= 2^this
-                                elements; everything before is common type.  <0: 20 */
+                                elements; everything before is common type.  <0: 20.
+                                If that node holds > 2^(this+2), the entry moves back along the
+                                stem (to internal nodes >= 2^(this-8)) until it does not. */
   int32_t comm_codec;        /* TN_COMM_* for sharded mode swaps (ignored at world size 1) */
   int32_t comm_group;        /* quantisation group in reals (int8/int4), e.g. 128 */
   uint64_t stem_capacity_bytes; /* bytes of EACH stem buffer the caller will lend; 0 = no check */
@@ -132,7 +134,11 @@ TN_API int tn_plan_upload(tn_plan* p, const tn_buffers* b, void* stream);
  * common-type branch contractions,
  * Eq. 6 padding of every stem operand, then the stem steps (permutation + GEMM per step) in the
  * two stem buffers.  Asynchronous; result stays on the device.  TN_E_INVALID if
- * slice_id >= 2^|sliced|; TN_E_CAPACITY if the buffers are smaller than tn_plan_info says. */
+ * slice_id >= 2^|sliced|; TN_E_CAPACITY if the buffers are smaller than tn_plan_info says.
+ * Single-rank plans: the slice id is written to the workspace by one kernel and the rest of the
+ * call is a replay of a CUDA graph captured (on a library-owned stream) at the first call with a
+ * given buffer set / timing flag; the graph is re-captured when either changes.  Buffers must
+ * therefore stay allocated while the plan may replay them (free the plan first). */
 TN_API int tn_stem_contract(tn_plan* p, const tn_buffers* b, uint64_t slice_id, void* stream);
 
 /* Split-type tail: the last stem steps run on 2^split_log2 contiguous
@@ -160,6 +166,9 @@ TN_API int tn_sample_amplitudes(tn_plan* p, const tn_buffers* b, const uint64_t*
 TN_API int tn_report_json(const tn_plan* p, char* buf, size_t cap, size_t* needed);
 /* Enable CUDA-event timing of the phases of tn_stem_contract (events only, no host sync). */
 TN_API int tn_set_timing(tn_plan* p, int enable);
+/* Enable (default) or disable the CUDA-graph replay of tn_stem_contract (disabled: every launch
+ * is issued eagerly on the caller's stream; also forced by the environment variable TN_NO_GRAPH). */
+TN_API int tn_set_graph(tn_plan* p, int enable);
 
 /* ---- kernel-level entry points (used by the parity tests; same kernels as the stem loop) ---- */
 

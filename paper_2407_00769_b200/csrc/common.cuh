@@ -19,10 +19,34 @@ namespace tn {
 
 constexpr int kMaxModes = 48;
 
+// Offset of a sliced leaf view, computed on the device from the slice id (C-A20): every
+// sliced label of the leaf contributes bit `bit[t]` of the slice id times its stride.  Reading the
+// slice id from device memory lets one captured CUDA graph serve every slice.
+struct SliceOff {
+  const uint64_t* slice;         // device slot holding the slice id (nullptr: no sliced labels)
+  int n;
+  int bit[8];
+  int64_t stride[8];
+};
+
+__host__ __device__ inline int64_t slice_offset(const SliceOff& so) {
+#ifdef __CUDA_ARCH__
+  if (!so.slice || so.n == 0) return 0;
+  const uint64_t id = *so.slice;
+  int64_t off = 0;
+  for (int t = 0; t < so.n; ++t)
+    if ((id >> so.bit[t]) & 1) off += so.stride[t];
+  return off;
+#else
+  return 0;
+#endif
+}
+
 // Strides (in complex elements) of a strided complex64 view with every mode of dimension 2.
 struct ContractArgs {
-  const float2* a;               // A base (already offset by the slice)
+  const float2* a;               // A base (the slice offset is added on the device)
   const float2* b;               // B base
+  SliceOff sa, sb;
   float2* c;                     // C (dense, row-major in out order)
   int n_out, n_red;              // output bits, reduce bits
   int64_t out_sa[kMaxModes];     // per output bit (bit j = output axis n_out-1-j): stride in A (0 if absent)
@@ -34,6 +58,7 @@ struct ContractArgs {
 // Gather a complex64 view into a dense [K][N] matrix (row-major), optional fp16 padding output.
 struct GatherArgs {
   const float2* src;
+  SliceOff ss;
   float2* dst;                   // dense [K][N] complex64
   int klog, nlog;
   int64_t sk[kMaxModes];         // stride of k-bit j (bit j of k = axis klog-1-j of R)
@@ -72,6 +97,7 @@ void launch_pad_b(__half* bp, const float2* b, int klog, int nlog, const uint32_
 // complex64 -> complex-half with scale from max (entry of the stem)
 void launch_c64_to_chalf(__half2* dst, const float2* src, uint64_t n, const uint32_t* max_bits,
                          int* exp_slot, uint32_t* out_max_bits, cudaStream_t s);
+void launch_set_u64(uint64_t* p, uint64_t v, cudaStream_t s);
 void launch_copy_c64(float2* dst, const float2* src, uint64_t n, cudaStream_t s);
 void launch_gemm_c64(float2* c, const float2* a, const float2* b, uint64_t M, uint32_t K, uint32_t N,
                      const OutMap* om, cudaStream_t s);

@@ -27,6 +27,8 @@ __device__ __forceinline__ float warp_max(float v) {
 
 __global__ void contract_c64_kernel(const ContractArgs args, uint64_t n_out_elems) {
   const uint64_t nred = 1ull << args.n_red;
+  const float2* A = args.a + slice_offset(args.sa);
+  const float2* B = args.b + slice_offset(args.sb);
   for (uint64_t o = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; o < n_out_elems;
        o += (uint64_t)gridDim.x * blockDim.x) {
     int64_t oa = 0, ob = 0;
@@ -49,7 +51,7 @@ __global__ void contract_c64_kernel(const ContractArgs args, uint64_t n_out_elem
           ob -= args.red_sb[j];
         }
       }
-      float2 x = args.a[oa], y = args.b[ob];
+      float2 x = A[oa], y = B[ob];
       acc.x = fmaf(x.x, y.x, fmaf(-x.y, y.y, acc.x));
       acc.y = fmaf(x.x, y.y, fmaf(x.y, y.x, acc.y));
     }
@@ -68,6 +70,7 @@ void launch_contract_c64(const ContractArgs& a, cudaStream_t s) {
 
 __global__ void gather_kn_kernel(const GatherArgs g) {
   const uint64_t n = 1ull << (g.klog + g.nlog);
+  const float2* src = g.src + slice_offset(g.ss);
   const uint64_t nmask = (1ull << g.nlog) - 1;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x) {
@@ -77,7 +80,7 @@ __global__ void gather_kn_kernel(const GatherArgs g) {
       if (k >> j & 1) off += g.sk[j];
     for (int j = 0; j < g.nlog; ++j)
       if (nn >> j & 1) off += g.sn[j];
-    g.dst[i] = g.src[off];
+    g.dst[i] = src[off];
   }
 }
 
@@ -174,6 +177,13 @@ void launch_c64_to_chalf(__half2* dst, const float2* src, uint64_t n, const uint
   if (blocks > 148 * 8) blocks = 148 * 8;
   if (blocks == 0) blocks = 1;
   c64_to_chalf_kernel<<<(unsigned)blocks, 256, 0, s>>>(dst, src, n, max_bits, exp_slot, out_max_bits);
+  TN_CUDA(cudaGetLastError());
+}
+
+__global__ void set_u64_kernel(uint64_t* p, uint64_t v) { *p = v; }
+
+void launch_set_u64(uint64_t* p, uint64_t v, cudaStream_t s) {
+  set_u64_kernel<<<1, 1, 0, s>>>(p, v);
   TN_CUDA(cudaGetLastError());
 }
 

@@ -196,6 +196,14 @@ Plan* load_plan(const char* json, size_t len, const tn_config* cfg_in, int world
     // the entry is the root itself: still a valid (zero-step) stem; keep it common instead
     entry_idx = -1;
   }
+  // A huge entry would itself be a common-type (complex64 SIMT) contraction: enter one node earlier
+  // instead, so that contraction becomes the first stem GEMM (C3: a 2^28 entry built from a 2^16 stem
+  // node and a 2^20 branch costs ~12 ms as a common contraction, 0.4 ms as a tcgen05 step).
+  while (entry_idx > 0 && (int)p.nodes[p.stem[entry_idx]].labels.size() > cfg.stem_min_log2 + 2) {
+    const Node& prev = p.nodes[p.stem[entry_idx - 1]];
+    if (prev.u < 0 || (int)prev.labels.size() < std::max(cfg.stem_min_log2 - 8, 1)) break;
+    --entry_idx;
+  }
   if (entry_idx >= 0) {
     p.stem_entry = p.stem[entry_idx];
     for (size_t i = entry_idx + 1; i < p.stem.size(); ++i) p.nodes[p.stem[i]].kind = NODE_STEM;
@@ -580,6 +588,8 @@ Plan* load_plan(const char* json, size_t len, const tn_config* cfg_in, int world
     }
   }
   p.ws_b = off;
+  p.ws_slice = off;
+  off += 256;
   p.ws_scratch = off;
   size_t S = p.steps.size();
   p.n_exp_slots = (int)(2 * S + 4);
@@ -635,6 +645,18 @@ std::string report_json(const Plan& p, const std::vector<float>& ms) {
       jlist(o, s.send_layout);
     }
     o << "}";
+  }
+  o << "],\"common\":[";  // per common contraction: [out rank, unsliced rank of u, of v, reduced modes]
+  for (size_t i = 0; i < p.common_order.size(); ++i) {
+    const Node& n = p.nodes[p.common_order[i]];
+    auto urank = [&](int id) {
+      int r = 0;
+      for (int l : p.nodes[id].labels)
+        if (std::find(p.sliced.begin(), p.sliced.end(), l) == p.sliced.end()) ++r;
+      return r;
+    };
+    const int ru = urank(n.u), rv = urank(n.v), ro = (int)n.labels.size();
+    o << (i ? "," : "") << "[" << ro << "," << ru << "," << rv << "," << (ru + rv - ro) / 2 << "]";
   }
   o << "],\"entry_layout\":";
   jlist(o, p.stem_entry >= 0 ? p.nodes[p.stem_entry].labels : std::vector<int>());

@@ -83,6 +83,7 @@ struct Plan {
   std::vector<uint64_t> tail_slots;  // chunk id held by each result slot of the last tail run
   // workspace layout
   uint64_t ws_leaves = 0, ws_common = 0, ws_b = 0, ws_scratch = 0, ws_total = 0;
+  uint64_t ws_slice = 0;          // uint64 slice id, read by the kernels (one CUDA graph serves every slice)
   uint64_t stem_elems_max = 0;    // largest stem tensor (elements)
   int max_stem_log2 = 0;
   // scratch slots (offsets in bytes from ws_scratch)
@@ -109,6 +110,15 @@ struct Plan {
   int n_swaps = 0;
   double swap_bytes = 0;          // payload bytes each rank sends per slice (codec applied)
   tn_comm* comm = nullptr;
+  // CUDA graph of the whole tn_stem_contract body (world == 1): captured once per buffer set on a
+  // library stream, replayed on the caller's stream.  Opaque CUDA handles as void*.
+  void* graph_exec = nullptr;
+  void* cap_stream = nullptr;
+  const void* graph_key[4] = {nullptr, nullptr, nullptr, nullptr};
+  uint64_t graph_stem_bytes = 0;
+  uint64_t graph_launches = 0;
+  int graph_stem_cur = 0, graph_result_buf = 0, graph_timing = 0;
+  bool graph_off = false;         // tn_set_graph(p, 0)
 };
 
 // Parse JSON + validate + lower.  Throws TnError.

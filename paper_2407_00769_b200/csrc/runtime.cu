@@ -120,6 +120,7 @@ Scratch scratch_of(const Plan& p, unsigned char* W) {
 // strided complex64 view of a node for a given slice
 struct View {
   const float2* base;
+  SliceOff so{};                  // sliced-leaf offset, resolved on the device from the slice id
   std::vector<int> labels;
   std::vector<int64_t> strides;
   int64_t stride_of(int l) const {
@@ -129,26 +130,33 @@ struct View {
   }
 };
 
-View view_of(const Plan& p, int id, unsigned char* W, uint64_t slice_id) {
+// A node's tensor as strides over its labels.  A sliced leaf's offset (slicing fixes the
+// sliced labels) is resolved on the device from the slice id in the workspace (SliceOff).
+View view_of(const Plan& p, int id, unsigned char* W) {
   View v;
   const Node& n = p.nodes[id];
   if (n.kind == NODE_LEAF) {
     const Leaf& lf = p.leaves[id];
     int r = (int)lf.labels.size();
-    int64_t off = 0;
+    v.so.slice = reinterpret_cast<const uint64_t*>(W + p.ws_slice);
     for (int i = 0; i < r; ++i) {
       int l = lf.labels[i];
       int64_t st = 1ll << (r - 1 - i);
       auto it = std::find(p.sliced.begin(), p.sliced.end(), l);
       if (it != p.sliced.end()) {
         int j = (int)(it - p.sliced.begin());
-        if (j < 64 && ((slice_id >> j) & 1)) off += st;  // bits >= 64 of a slice id are 0
+        if (j < 64) {  // bits >= 64 of a slice id are 0 (C-A27)
+          if (v.so.n >= 8) throw TnError{TN_E_UNSUPPORTED, "leaf with more than 8 sliced labels"};
+          v.so.bit[v.so.n] = j;
+          v.so.stride[v.so.n] = st;
+          v.so.n++;
+        }
       } else {
         v.labels.push_back(l);
         v.strides.push_back(st);
       }
     }
-    v.base = reinterpret_cast<const float2*>(W + lf.ws_off) + off;
+    v.base = reinterpret_cast<const float2*>(W + lf.ws_off);
   } else {
     int r = (int)n.labels.size();
     v.labels = n.labels;
@@ -158,14 +166,16 @@ View view_of(const Plan& p, int id, unsigned char* W, uint64_t slice_id) {
   return v;
 }
 
-void run_common(const Plan& p, unsigned char* W, uint64_t slice_id, cudaStream_t s) {
+void run_common(const Plan& p, unsigned char* W, cudaStream_t s) {
   for (int id : p.common_order) {
     const Node& n = p.nodes[id];
-    View a = view_of(p, n.u, W, slice_id), b = view_of(p, n.v, W, slice_id);
+    View a = view_of(p, n.u, W), b = view_of(p, n.v, W);
     ContractArgs args;
     memset(&args, 0, sizeof(args));
     args.a = a.base;
     args.b = b.base;
+    args.sa = a.so;
+    args.sb = b.so;
     args.c = reinterpret_cast<float2*>(W + n.ws_off);
     args.n_out = (int)n.labels.size();
     if (args.n_out > kMaxModes) throw TnError{TN_E_UNSUPPORTED, "common contraction with too many modes"};
@@ -190,13 +200,14 @@ void run_common(const Plan& p, unsigned char* W, uint64_t slice_id, cudaStream_t
   }
 }
 
-void prepare_b(const Plan& p, unsigned char* W, uint64_t slice_id, const Scratch& sc, cudaStream_t s) {
+void prepare_b(const Plan& p, unsigned char* W, const Scratch& sc, cudaStream_t s) {
   for (size_t i = 0; i < p.steps.size(); ++i) {
     const StemStep& st = p.steps[i];
-    View v = view_of(p, st.branch, W, slice_id);
+    View v = view_of(p, st.branch, W);
     GatherArgs g;
     memset(&g, 0, sizeof(g));
     g.src = v.base;
+    g.ss = v.so;
     g.dst = reinterpret_cast<float2*>(W + st.b_tmp_off);
     g.klog = st.klog;
     g.nlog = st.nlog;
@@ -306,7 +317,14 @@ void mode_swap(Plan& p, const StemStep& st, const tn_buffers* b, int& cur, cudaS
 }
 
 void rec_event(Plan& p, size_t k, cudaStream_t s) {
-  if (p.timing) TN_CUDA(cudaEventRecord((cudaEvent_t)p.ev[k], s));
+  if (!p.timing) return;
+  // under stream capture an External record becomes an event-record node (every replay records it)
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  TN_CUDA(cudaStreamIsCapturing(s, &cs));
+  if (cs == cudaStreamCaptureStatusActive)
+    TN_CUDA(cudaEventRecordWithFlags((cudaEvent_t)p.ev[k], s, cudaEventRecordExternal));
+  else
+    TN_CUDA(cudaEventRecord((cudaEvent_t)p.ev[k], s));
 }
 
 // One stem GEMM (Eq. 6 on tcgen05, SIMT for small K*N, complex64 SIMT for the fp32 path) from
@@ -339,30 +357,18 @@ void run_gemm(Plan& p, const StemStep& st, size_t i, const void* src, void* dst,
   ++p.launches;
 }
 
-void stem_contract(Plan& p, const tn_buffers* b, uint64_t slice_id, cudaStream_t s) {
-  check_buffers(p, b);
-  if (p.world > 1 && !p.comm) throw TnError{TN_E_INVALID, "plan lowered for several ranks without a communicator"};
-  if (p.sliced.size() < 64 && slice_id >= (1ull << p.sliced.size()))
-    throw TnError{TN_E_INVALID, "slice_id >= 2^|sliced|"};
+// The subtask body: every launch after the slice id is in the workspace.  Nothing here depends on
+// the slice id on the host, so one capture of it serves every slice (stem_contract).
+void stem_body(Plan& p, const tn_buffers* b, cudaStream_t s) {
   unsigned char* W = static_cast<unsigned char*>(b->d_ws);
   Scratch sc = scratch_of(p, W);
-  p.launches = 0;
-  p.ev_valid = false;
-  if (p.timing && p.ev.empty()) {
-    p.ev.resize(3 + 2 * p.steps.size());
-    for (auto& e : p.ev) {
-      cudaEvent_t ce;
-      TN_CUDA(cudaEventCreate(&ce));
-      e = (void*)ce;
-    }
-  }
-  if (p.timing) TN_CUDA(cudaEventRecord((cudaEvent_t)p.ev[0], s));
+  rec_event(p, 0, s);
   TN_CUDA(cudaMemsetAsync(W + p.ws_scratch, 0, sc.bytes, s));
-  run_common(p, W, slice_id, s);
+  run_common(p, W, s);
   p.launches += p.common_order.size();
   p.result_in_ws = p.steps.empty();
   if (p.steps.empty()) return;
-  prepare_b(p, W, slice_id, sc, s);
+  prepare_b(p, W, sc, s);
   p.launches += p.steps.size() + 2;  // gathers + entry conversion (max + convert)
   const int eb = p.cfg.dtype == TN_CHALF ? 4 : 8;
   // stem entry -> buffer 0
@@ -372,10 +378,11 @@ void stem_contract(Plan& p, const tn_buffers* b, uint64_t slice_id, cudaStream_t
     const uint64_t n_local = n >> p.shard_log2;  // this rank's shard: shard modes are outermost
     const float2* src;
     if (e.kind == NODE_LEAF) {
-      View v = view_of(p, p.stem_entry, W, slice_id);
+      View v = view_of(p, p.stem_entry, W);
       GatherArgs g;
       memset(&g, 0, sizeof(g));
       g.src = v.base;
+      g.ss = v.so;
       g.dst = reinterpret_cast<float2*>(b->d_stem[1]);  // scratch use of the other buffer
       g.klog = 0;
       g.nlog = (int)v.labels.size();
@@ -442,6 +449,87 @@ void stem_contract(Plan& p, const tn_buffers* b, uint64_t slice_id, cudaStream_t
   p.ev_valid = p.timing != 0;
   p.result_buf = cur;
   p.result_off = 0;
+}
+
+bool graph_wanted(const Plan& p) {
+  static const bool env_off = getenv("TN_NO_GRAPH") != nullptr;
+  return !env_off && !p.graph_off && p.world == 1;
+}
+
+// Capture stem_body on the library stream and instantiate it (once per buffer set).
+void capture_stem(Plan& p, const tn_buffers* b) {
+  if (!p.cap_stream) {
+    cudaStream_t cs;
+    TN_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    p.cap_stream = (void*)cs;
+  }
+  if (p.graph_exec) {
+    cudaGraphExecDestroy((cudaGraphExec_t)p.graph_exec);
+    p.graph_exec = nullptr;
+  }
+  cudaStream_t cs = (cudaStream_t)p.cap_stream;
+  p.launches = 0;
+  TN_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+  try {
+    stem_body(p, b, cs);
+  } catch (...) {
+    cudaGraph_t junk = nullptr;
+    cudaStreamEndCapture(cs, &junk);
+    if (junk) cudaGraphDestroy(junk);
+    throw;
+  }
+  cudaGraph_t g = nullptr;
+  TN_CUDA(cudaStreamEndCapture(cs, &g));
+  cudaGraphExec_t ex = nullptr;
+  cudaError_t e = cudaGraphInstantiate(&ex, g, 0);
+  cudaGraphDestroy(g);
+  TN_CUDA(e);
+  p.graph_exec = (void*)ex;
+  p.graph_key[0] = b->d_ws;
+  p.graph_key[1] = b->d_stem[0];
+  p.graph_key[2] = b->d_stem[1];
+  p.graph_stem_bytes = b->stem_bytes;
+  p.graph_timing = p.timing;
+  p.graph_launches = p.launches;
+  p.graph_stem_cur = p.stem_cur;
+  p.graph_result_buf = p.result_buf;
+}
+
+// One sliced subtask (P:318 slicing; P:8-22 the stem path).  The slice id goes to the device first
+// (one tiny kernel), then the body runs eagerly or as a replay of its CUDA graph: the common phase
+// alone is hundreds of small launches whose CPU cost would otherwise not shrink with more GPUs.
+void stem_contract(Plan& p, const tn_buffers* b, uint64_t slice_id, cudaStream_t s) {
+  check_buffers(p, b);
+  if (p.world > 1 && !p.comm) throw TnError{TN_E_INVALID, "plan lowered for several ranks without a communicator"};
+  if (p.sliced.size() < 64 && slice_id >= (1ull << p.sliced.size()))
+    throw TnError{TN_E_INVALID, "slice_id >= 2^|sliced|"};
+  unsigned char* W = static_cast<unsigned char*>(b->d_ws);
+  p.ev_valid = false;
+  if (p.timing && p.ev.empty()) {
+    p.ev.resize(3 + 2 * p.steps.size());
+    for (auto& e : p.ev) {
+      cudaEvent_t ce;
+      TN_CUDA(cudaEventCreate(&ce));
+      e = (void*)ce;
+    }
+  }
+  launch_set_u64(reinterpret_cast<uint64_t*>(W + p.ws_slice), slice_id, s);
+  if (graph_wanted(p)) {
+    const bool same = p.graph_exec && p.graph_key[0] == b->d_ws && p.graph_key[1] == b->d_stem[0] &&
+                      p.graph_key[2] == b->d_stem[1] && p.graph_stem_bytes == b->stem_bytes && p.graph_timing == p.timing;
+    if (!same) capture_stem(p, b);
+    TN_CUDA(cudaGraphLaunch((cudaGraphExec_t)p.graph_exec, s));
+    p.launches = p.graph_launches + 1;
+    p.stem_cur = p.graph_stem_cur;
+    p.result_buf = p.graph_result_buf;
+    p.result_off = 0;
+    p.result_in_ws = p.steps.empty();
+    p.ev_valid = p.timing != 0 && p.split_modes.empty();  // the graph records the same events
+    return;
+  }
+  p.launches = 0;
+  stem_body(p, b, s);
+  p.launches += 1;
 }
 
 // Split-type tail ("dividing the stem tensor into smaller chunks", P:22 chunks inside the
@@ -651,6 +739,8 @@ int tn_plan_info_get(const tn_plan* h, tn_plan_info* info) {
 void tn_plan_free(tn_plan* h) {
   if (!h) return;
   if (h->p->pinned) cudaFreeHost(h->p->pinned);
+  if (h->p->graph_exec) cudaGraphExecDestroy((cudaGraphExec_t)h->p->graph_exec);
+  if (h->p->cap_stream) cudaStreamDestroy((cudaStream_t)h->p->cap_stream);
   for (void* e : h->p->ev) cudaEventDestroy((cudaEvent_t)e);
   delete h->p;
   delete h;
@@ -816,6 +906,12 @@ int tn_report_json(const tn_plan* h, char* buf, size_t cap, size_t* needed) {
 int tn_set_timing(tn_plan* h, int enable) {
   if (!h) return fail(TN_E_INVALID, "NULL plan");
   h->p->timing = enable;
+  return TN_OK;
+}
+
+int tn_set_graph(tn_plan* h, int enable) {
+  if (!h) return fail(TN_E_INVALID, "NULL plan");
+  h->p->graph_off = !enable;
   return TN_OK;
 }
 

@@ -66,6 +66,7 @@ def lib():
         L.tn_sample_amplitudes.argtypes = [vp, C.POINTER(tn_buffers), vp, C.c_size_t, vp, i32, vp, vp]
         L.tn_report_json.argtypes = [vp, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]
         L.tn_set_timing.argtypes = [vp, i32]
+        L.tn_set_graph.argtypes = [vp, i32]
         L.tn_permute.argtypes = [vp, vp, i32, i32, C.POINTER(C.c_int), vp]
         L.tn_gemm_chalf.argtypes = [vp, vp, vp, u64, C.c_uint32, C.c_uint32, vp, vp, vp, vp, vp]
         L.tn_gemm_cfloat.argtypes = [vp, vp, vp, u64, C.c_uint32, C.c_uint32, vp]
@@ -157,6 +158,9 @@ class Plan:
 
     def set_timing(self, on=True):
         _check(lib().tn_set_timing(self._h, 1 if on else 0))
+
+    def set_graph(self, on=True):
+        _check(lib().tn_set_graph(self._h, 1 if on else 0))
 
 
 class Buffers:

@@ -12,7 +12,8 @@ def main():
     name = sys.argv[1] if len(sys.argv) > 1 else "c3"
     pol = int(sys.argv[2]) if len(sys.argv) > 2 else 0
     plan = json.load(open(f"plans/{name}.json"))
-    p = tn.Plan(plan, tn.make_config(stem_min_log2=20, layout_policy=pol))
+    sm = int(sys.argv[3]) if len(sys.argv) > 3 else 20
+    p = tn.Plan(plan, tn.make_config(stem_min_log2=sm, layout_policy=pol))
     print(p.info()["n_permutes"], "permutes")
     b = tn.Buffers(p)
     tn.tn_plan_upload(p, b)
