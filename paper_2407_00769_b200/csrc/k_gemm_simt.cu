@@ -201,8 +201,8 @@ __global__ void __launch_bounds__(256) gemm_chalf_simt_kernel(__half2* __restric
   if (out_max && (threadIdx.x & 31) == 0) atomic_max_pos2(out_max, mx);
 }
 
-// Row-streaming variant for K <= 8 and N <= 16: one thread per row of A (K complex-half = up to
-// 32 contiguous bytes, vector loads), N outputs in registers, stored as one contiguous run when the
+// Row-streaming variant for K*N <= 128 (K <= 16, N <= 32; see rows_ok): one thread per row of A
+// (K complex-half = up to 64 contiguous bytes, vector loads), N outputs in registers, stored as one contiguous run when the
 // output layout keeps the row's outputs contiguous.  No shared-memory round trip for A, no
 // barriers: consecutive threads read consecutive rows (fully coalesced) and the grid-stride loop
 // keeps many rows in flight.
@@ -309,10 +309,24 @@ static bool dispatch_rows_n(uint32_t N, __half2* c, const __half2* a, const __ha
     case 2: launch_rows<K, 2>(c, a, bp, M, contiguous, in_max, b_bound, out_max, exp_slot, om, s); return true;
     case 4: launch_rows<K, 4>(c, a, bp, M, contiguous, in_max, b_bound, out_max, exp_slot, om, s); return true;
     case 8: launch_rows<K, 8>(c, a, bp, M, contiguous, in_max, b_bound, out_max, exp_slot, om, s); return true;
-    case 16: launch_rows<K, 16>(c, a, bp, M, contiguous, in_max, b_bound, out_max, exp_slot, om, s); return true;
+  }
+  if constexpr (K <= 8) {
+    if (N == 16) {
+      launch_rows<K, 16>(c, a, bp, M, contiguous, in_max, b_bound, out_max, exp_slot, om, s);
+      return true;
+    }
+  }
+  if constexpr (K <= 4) {
+    if (N == 32) {
+      launch_rows<K, 32>(c, a, bp, M, contiguous, in_max, b_bound, out_max, exp_slot, om, s);
+      return true;
+    }
   }
   return false;
 }
+
+// Shapes the row-streaming kernel covers (the lowering's tensor-core rule mirrors this, plan.cpp).
+static bool rows_ok(uint32_t K, uint32_t N) { return K <= 16 && N <= 32 && K * N <= 128; }
 
 void launch_gemm_chalf_simt(__half2* c, const __half2* a, const __half* bp, uint64_t M, uint32_t K, uint32_t N,
                             const float* in_max, const float* b_bound, uint32_t* out_max, int* exp_slot,
@@ -326,10 +340,11 @@ void launch_gemm_chalf_simt(__half2* c, const __half2* a, const __half* bp, uint
     run = nlog;
   else
     while (run < om.nbits && om.ns[run] == ((int64_t)1 << run)) ++run;
-  if (K <= 8 && N <= 16) {
+  if (rows_ok(K, N)) {
     const int contiguous = run >= nlog;
     bool ok = false;
     switch (K) {
+      case 16: ok = dispatch_rows_n<16>(N, c, a, bp, M, contiguous, in_max, b_bound, out_max, exp_slot, om, s); break;
       case 1: ok = dispatch_rows_n<1>(N, c, a, bp, M, contiguous, in_max, b_bound, out_max, exp_slot, om, s); break;
       case 2: ok = dispatch_rows_n<2>(N, c, a, bp, M, contiguous, in_max, b_bound, out_max, exp_slot, om, s); break;
       case 4: ok = dispatch_rows_n<4>(N, c, a, bp, M, contiguous, in_max, b_bound, out_max, exp_slot, om, s); break;

@@ -11,11 +11,13 @@
 //   warp 0   : TMA producer — A tile [128 x 64] and B tile [BN x 64] per stage, 128B swizzle,
 //              mbarrier full/empty ring of STAGES
 //   warp 1   : MMA issuer — one elected thread issues tcgen05.mma.cta_group::1.kind::f16
-//              (M=128, N=BN, K=16), accumulators in TMEM (2 x 256 columns, double buffered),
+//              (M=128, N=BN, K=16), accumulators in TMEM (512 columns: 2 x 256 ... 16 x 32),
 //              tcgen05.commit -> mbarriers
 //   warp 2   : TMEM allocator
-//   warps 4-7: epilogue — tcgen05.ld 32x32b -> scale -> fp16 -> 128B-swizzled smem -> TMA store;
-//              running max |C| for the next step's scale
+//   warps 4-11: epilogue, two warpgroups; group g drains every other tile —
+//              tcgen05.ld 32x32b -> scale -> fp16 -> 128B-swizzled smem ring -> TMA store; running
+//              max |C| for the next step's scale.  Two groups keep two warps per SM sub-partition
+//              converting, which output-heavy shapes (small K, large N) need to reach HBM write speed
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -30,8 +32,7 @@ namespace tn {
 namespace tc {
 
 constexpr int BM = 128;
-constexpr int BK = 64;  // fp16 elements per 128-byte swizzle row
-constexpr int kThreads = 256;
+constexpr int kThreads = 384;  // 4 role warps + 2 epilogue warpgroups
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -76,17 +77,21 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void*
                : "memory");
 }
 
-__device__ __forceinline__ uint64_t smem_desc_sw128(const void* p) {
-  // SM100 UMMA shared-memory matrix descriptor, K-major, 128-byte swizzle:
-  // start>>4 [0,14) | LBO>>4 [16,30) (unused for swizzled K-major) | SBO>>4 [32,46) = 1024 B between
-  // 8-row groups | version 1 [46,48) | base offset 0 | layout SWIZZLE_128B = 2 at [61,64)
+// SM100 UMMA shared-memory matrix descriptor, K-major, rows of KB fp16 = 2*KB bytes swizzled at that
+// width: start>>4 [0,14) | LBO>>4 [16,30) (unused for swizzled K-major) | SBO>>4 [32,46) = 8 rows
+// between 8-row groups | version 1 [46,48) | base offset 0 | layout [61,64): SWIZZLE_128B = 2,
+// SWIZZLE_64B = 4, SWIZZLE_32B = 6.
+template <int KB>
+__device__ __forceinline__ uint64_t smem_desc_sw(const void* p) {
+  constexpr uint64_t kRow = 2 * KB;
+  constexpr uint64_t kLayout = KB == 64 ? 2 : (KB == 32 ? 4 : 6);
   uint64_t addr = smem_u32(p);
   uint64_t d = 0;
   d |= (addr & 0x3FFFFull) >> 4;
   d |= (uint64_t)1 << 16;
-  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)((8 * kRow) >> 4) << 32;
   d |= (uint64_t)1 << 46;
-  d |= (uint64_t)2 << 61;
+  d |= kLayout << 61;
   return d;
 }
 
@@ -123,18 +128,26 @@ __device__ __forceinline__ void named_bar(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
-template <int BN>
+// KB: fp16 elements of K per stage (the TMA box and swizzle width): 64, or 2K when 2K < 64 so that
+// small-K steps neither stage nor zero-fill 3/4 empty boxes and keep more tiles in flight.
+template <int BN, int KB>
 struct Cfg {
-  static constexpr int kABytes = BM * BK * 2;             // 16 KB
-  static constexpr int kBBytes = BN * BK * 2;
+  static constexpr int kABytes = BM * KB * 2;
+  static constexpr int kBBytes = BN * KB * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kCSub = (BN + 63) / 64;            // 64-column store subtiles
-  static constexpr int kNBuf = kCSub >= 2 ? kCSub : 2;    // staging ring of 64-column subtiles
-  static constexpr int kCTma = kNBuf * BM * 128;          // 128B-swizzled staging for TMA stores
+  // staging ring (64-column subtiles) per epilogue group: 4 deep (more TMA stores in flight) when
+  // that still leaves >= 4 pipeline stages, else 2
+  static constexpr int kNBuf = ((220 * 1024 - 2 * 4 * BM * 128) / kStageBytes >= 4) ? 4 : 2;
+  static constexpr int kCTma = 2 * kNBuf * BM * 128;      // 128B-swizzled staging for TMA stores, 2 groups
   static constexpr int kCBytes = kCTma;
-  static constexpr int kStagesRaw = (200 * 1024 - kCBytes) / kStageBytes;
-  static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
-  static constexpr int kSmem = kStages * kStageBytes + kCBytes + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int kStagesRaw = (220 * 1024 - kCBytes) / kStageBytes;
+  static constexpr int kStages = kStagesRaw > 24 ? 24 : kStagesRaw;
+  static constexpr int kSmem = kStages * kStageBytes + kCBytes + 1024 /*align*/ + 1024 /*barriers*/;
+  // TMEM accumulators: as many as fit in 512 columns (<= 16), so the MMA runs ahead of the
+  // epilogue by several tiles when a tile is small (small K, small N)
+  static constexpr int kAccStride = BN < 32 ? 32 : BN;
+  static constexpr int kNAcc = (512 / kAccStride) > 16 ? 16 : (512 / kAccStride);
   static constexpr uint32_t kIdesc = (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
 };
 
@@ -178,14 +191,14 @@ __device__ __forceinline__ void tile_coords(const ScatterArgs& sa, uint32_t t, u
 
 namespace tc {
 
-template <int BN>
+template <int BN, int KB>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_chalf_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                          const __grid_constant__ CUtensorMap tmC, uint32_t num_m, uint32_t num_n, int K2,
                          const float* in_max, const float* b_bound, uint32_t* out_max, int* exp_slot,
                          const __grid_constant__ ScatterArgs sc_args, uint32_t* out_scatter, uint64_t rows,
                          uint32_t n_cols) {
-  using C = Cfg<BN>;
+  using C = Cfg<BN, KB>;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   unsigned char* sA = smem;
@@ -194,20 +207,20 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(sC + C::kCBytes);
   uint64_t* empty = full + C::kStages;
   uint64_t* tfull = empty + C::kStages;
-  uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* tempty = tfull + C::kNAcc;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + C::kNAcc);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t num_tiles = num_m * num_n;
-  const int num_k = (K2 + BK - 1) / BK;
-  const int last_kk = ((K2 - (num_k - 1) * BK) + 15) / 16;  // MMAs in the last k block
+  const int num_k = (K2 + KB - 1) / KB;
+  const int last_kk = ((K2 - (num_k - 1) * KB) + 15) / 16;  // MMAs in the last k block
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < C::kStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    for (int a = 0; a < 2; ++a) {
+    for (int a = 0; a < C::kNAcc; ++a) {
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 128);
     }
@@ -230,14 +243,23 @@ __global__ void __launch_bounds__(kThreads, 1)
       // ===== TMA producer =====
       int s = 0;
       uint32_t ph = 0;
+      const uint32_t reuse_dist = (uint32_t)C::kStages * gridDim.x;  // tile that last filled this slot
       for (uint32_t t = blockIdx.x; t < num_tiles; t += gridDim.x) {
         int m0, n0;
         tile_coords(sc_args, t, num_n, BM, BN, m0, n0);
+        // single k-block: the slot still holds B of the tile kStages iterations ago; skip the B
+        // load when that tile had the same n-block (always when N fits one tile)
+        bool b_resident = false;
+        if (num_k == 1 && t >= blockIdx.x + reuse_dist) {
+          int pm, pn;
+          tile_coords(sc_args, t - reuse_dist, num_n, BM, BN, pm, pn);
+          b_resident = pn == n0;
+        }
         for (int kb = 0; kb < num_k; ++kb) {
           mbar_wait(&empty[s], ph ^ 1);
-          mbar_expect_tx(&full[s], C::kStageBytes);
-          tma_load_2d(sA + s * C::kABytes, &tmA, &full[s], kb * BK, m0);
-          tma_load_2d(sB + s * C::kBBytes, &tmB, &full[s], kb * BK, n0);
+          mbar_expect_tx(&full[s], b_resident ? C::kABytes : C::kStageBytes);
+          tma_load_2d(sA + s * C::kABytes, &tmA, &full[s], kb * KB, m0);
+          if (!b_resident) tma_load_2d(sB + s * C::kBBytes, &tmB, &full[s], kb * KB, n0);
           if (++s == C::kStages) {
             s = 0;
             ph ^= 1;
@@ -252,18 +274,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t ph = 0;
       uint32_t i = 0;
       for (uint32_t t = blockIdx.x; t < num_tiles; t += gridDim.x, ++i) {
-        const uint32_t acc = i & 1, aph = (i >> 1) & 1;
+        const uint32_t acc = i % C::kNAcc, aph = (i / C::kNAcc) & 1;
         mbar_wait(&tempty[acc], aph ^ 1);
         tc_fence_after();
-        const uint32_t tmem_d = tmem_base + acc * 256;
+        const uint32_t tmem_d = tmem_base + acc * C::kAccStride;
         for (int kb = 0; kb < num_k; ++kb) {
           mbar_wait(&full[s], ph);
           tc_fence_after();
-          const int nkk = (kb == num_k - 1) ? last_kk : BK / 16;
-          const uint64_t ad = smem_desc_sw128(sA + s * C::kABytes);
-          const uint64_t bd = smem_desc_sw128(sB + s * C::kBBytes);
+          const int nkk = (kb == num_k - 1) ? last_kk : KB / 16;
+          const uint64_t ad = smem_desc_sw<KB>(sA + s * C::kABytes);
+          const uint64_t bd = smem_desc_sw<KB>(sB + s * C::kBBytes);
           for (int kk = 0; kk < nkk; ++kk) {
-            // advance 16 fp16 = 32 bytes along K inside the 128B swizzle atom (>>4 => +2)
+            // advance 16 fp16 = 32 bytes along K inside the swizzle atom (>>4 => +2)
             mma_f16(tmem_d, ad + 2 * kk, bd + 2 * kk, C::kIdesc, (kb | kk) != 0);
           }
           mma_commit(&empty[s]);
@@ -276,13 +298,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp >= 4) {
-    // ===== epilogue =====
+    // ===== epilogue: two independent warpgroups, group g drains the tiles i = g mod 2
+    const int grp = (warp - 4) >> 2;
     const int ew = warp & 3;  // TMEM lane quarter this warp may access
     const int row = ew * 32 + lane;
-    const int etid = threadIdx.x - 128;
+    const int etid = threadIdx.x - 128 - 128 * grp;
+    unsigned char* sCg = sC + grp * (C::kNBuf * BM * 128);
     int e = 0;
     if (in_max && b_bound) e = scale_exp_for(in_max[0] * b_bound[0]);
-    if (exp_slot && blockIdx.x == 0 && etid == 0) *exp_slot = e;
+    if (exp_slot && blockIdx.x == 0 && grp == 0 && etid == 0) *exp_slot = e;
     const float sc = ldexpf(1.f, e);
     float mx = 0.f;
     const bool scat = sc_args.on != 0;
@@ -291,15 +315,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     int run = 0;
     if (scat)
       while (run < 4 && run < sc_args.nbits && sc_args.ns[run] == ((int64_t)1 << run)) ++run;
-    uint32_t i = 0;
     uint32_t gsub = 0;  // staging subtiles used so far (ring position)
-    for (uint32_t t = blockIdx.x; t < num_tiles; t += gridDim.x, ++i) {
-      const uint32_t acc = i & 1, aph = (i >> 1) & 1;
+    for (uint32_t t = blockIdx.x + grp * gridDim.x, i = grp; t < num_tiles; t += 2 * gridDim.x, i += 2) {
+      const uint32_t acc = i % C::kNAcc, aph = (i / C::kNAcc) & 1;
       int m0, n0;
       tile_coords(sc_args, t, num_n, BM, BN, m0, n0);
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
-      const uint32_t taddr = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * 256;
+      const uint32_t taddr = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * C::kAccStride;
       int64_t row_off = 0;
       const bool row_ok = (uint64_t)(m0 + row) < rows;
       if (scat) {
@@ -309,84 +332,90 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
 #pragma unroll 1
       for (int sub = 0; sub < BN; sub += 64, ++gsub) {
-      unsigned char* sbuf = sC + (gsub % C::kNBuf) * (BM * 128);
-      if (!scat) {
-        // ring slot free? (the TMA store that used it kNBuf subtiles ago has read it)
-        if (etid == 0) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(C::kNBuf - 1) : "memory");
-        named_bar(1, 128);
-      }
-#pragma unroll 1
-      for (int c = sub; c < BN && c < sub + 64; c += 32) {
-        uint32_t r[32];
-        tmem_ld_32x32b_x32(taddr + c, r);
-        tmem_ld_wait();
-        uint32_t pk[16];
-        // complex values of this 32-column chunk that exist (N < 8 pads B_P with zero rows)
-        const int nleft = (int)n_cols - ((n0 + c) >> 1);
-        const int nvalid = nleft < 16 ? (nleft > 0 ? nleft : 0) : 16;
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          float x0 = __uint_as_float(r[2 * j]) * sc, x1 = __uint_as_float(r[2 * j + 1]) * sc;
-          __half2 h = __floats2half2_rn(x0, x1);
-          float2 hf = __half22float2(h);
-          if (j < nvalid) mx = fmaxf(mx, fmaxf(fabsf(hf.x), fabsf(hf.y)));
-          pk[j] = *reinterpret_cast<uint32_t*>(&h);
+        unsigned char* sbuf = sCg + (gsub % C::kNBuf) * (BM * 128);
+        if (!scat) {
+          // ring slot free? (the TMA store that used it kNBuf subtiles ago has read it)
+          if (etid == 0) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(C::kNBuf - 1) : "memory");
+          named_bar(1 + grp, 128);
         }
-        if (scat) {
-          if (row_ok) {
-            const uint64_t nb = (uint64_t)((n0 + c) >> 1);
-            const int V = 1 << run;
-#pragma unroll 1
-            for (int q = 0; q < nvalid; q += V) {
-              int64_t off = row_off;
-              const uint64_t ng = nb + q;
-              for (int j = run; j < sc_args.nbits; ++j)
-                if ((ng >> j) & 1) off += sc_args.ns[j];
-              uint32_t* dst = out_scatter + off;
-              if (V >= 8) {
-                // 256-bit stores (STG.256): one full 32-byte sector per instruction and thread
+        // both 32-column halves of the subtile in flight before one wait
+        uint32_t r[2][32];
+        tmem_ld_32x32b_x32(taddr + sub, r[0]);
+        if (sub + 32 < BN) tmem_ld_32x32b_x32(taddr + sub + 32, r[1]);
+        tmem_ld_wait();
+        if (sub + 64 >= BN) {
+          // accumulator drained -> MMA may reuse it (before the stores are issued)
+          tc_fence_before();
+          mbar_arrive(&tempty[acc]);
+        }
 #pragma unroll
-                for (int v = 0; v < 16; v += 8)
-                  if (v < V)
-                    asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(dst + v), "r"(pk[q + v]),
-                                 "r"(pk[q + v + 1]), "r"(pk[q + v + 2]), "r"(pk[q + v + 3]), "r"(pk[q + v + 4]),
-                                 "r"(pk[q + v + 5]), "r"(pk[q + v + 6]), "r"(pk[q + v + 7])
-                                 : "memory");
-              } else if (V == 4) {
-                *reinterpret_cast<uint4*>(dst) = make_uint4(pk[q], pk[q + 1], pk[q + 2], pk[q + 3]);
-              } else if (V == 2) {
-                *reinterpret_cast<uint2*>(dst) = make_uint2(pk[q], pk[q + 1]);
-              } else {
-                *dst = pk[q];
+        for (int h = 0; h < 2; ++h) {
+          const int c = sub + 32 * h;
+          if (c >= BN) break;
+          uint32_t pk[16];
+          // complex values of this 32-column chunk that exist (N < 8 pads B_P with zero rows)
+          const int nleft = (int)n_cols - ((n0 + c) >> 1);
+          const int nvalid = nleft < 16 ? (nleft > 0 ? nleft : 0) : 16;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            float x0 = __uint_as_float(r[h][2 * j]) * sc, x1 = __uint_as_float(r[h][2 * j + 1]) * sc;
+            __half2 hv = __floats2half2_rn(x0, x1);
+            float2 hf = __half22float2(hv);
+            if (j < nvalid) mx = fmaxf(mx, fmaxf(fabsf(hf.x), fabsf(hf.y)));
+            pk[j] = *reinterpret_cast<uint32_t*>(&hv);
+          }
+          if (scat) {
+            if (row_ok) {
+              const uint64_t nb = (uint64_t)((n0 + c) >> 1);
+              const int V = 1 << run;
+              // q and v are compile-time (full unroll) so pk stays in registers
+#pragma unroll
+              for (int q = 0; q < 16; ++q) {
+                if ((q & (V - 1)) || q >= nvalid) continue;
+                int64_t off = row_off;
+                const uint64_t ng = nb + q;
+                for (int j = run; j < sc_args.nbits; ++j)
+                  if ((ng >> j) & 1) off += sc_args.ns[j];
+                uint32_t* dst = out_scatter + off;
+                if (V >= 8) {
+                  // 256-bit stores (STG.256): one full 32-byte sector per instruction and thread
+#pragma unroll
+                  for (int v = 0; v < 16; v += 8)
+                    if (v < V && q + v + 7 < 16)
+                      asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(dst + v), "r"(pk[q + v]),
+                                   "r"(pk[q + v + 1]), "r"(pk[q + v + 2]), "r"(pk[q + v + 3]), "r"(pk[q + v + 4]),
+                                   "r"(pk[q + v + 5]), "r"(pk[q + v + 6]), "r"(pk[q + v + 7])
+                                   : "memory");
+                } else if (V == 4) {
+                  if (q + 3 < 16) *reinterpret_cast<uint4*>(dst) = make_uint4(pk[q], pk[q + 1], pk[q + 2], pk[q + 3]);
+                } else if (V == 2) {
+                  if (q + 1 < 16) *reinterpret_cast<uint2*>(dst) = make_uint2(pk[q], pk[q + 1]);
+                } else {
+                  *dst = pk[q];
+                }
+              }
+            }
+          } else {
+            unsigned char* srow = sbuf + row * 128;
+            const int cb = (c & 63) >> 3;  // first 16-byte chunk of these 32 columns
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              if ((c & 63) + q * 8 < BN || BN >= 64) {
+                const int chunk = (cb + q) ^ (row & 7);
+                uint4 v = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+                *reinterpret_cast<uint4*>(srow + chunk * 16) = v;
               }
             }
           }
-        } else {
-          unsigned char* srow = sbuf + row * 128;
-          const int cb = (c & 63) >> 3;  // first 16-byte chunk of these 32 columns
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            if ((c & 63) + q * 8 < BN || BN >= 64) {
-              const int chunk = (cb + q) ^ (row & 7);
-              uint4 v = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
-              *reinterpret_cast<uint4*>(srow + chunk * 16) = v;
-            }
+        }
+        if (!scat) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          named_bar(1 + grp, 128);
+          if (etid == 0) {
+            tma_store_2d(&tmC, sbuf, n0 + sub, m0);
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
           }
         }
-      }
-      if (sub + 64 >= BN) {
-        // accumulator drained -> MMA may reuse it (before the last store is issued)
-        tc_fence_before();
-        mbar_arrive(&tempty[acc]);
-      }
-      if (!scat) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        named_bar(1, 128);
-        if (etid == 0) {
-          tma_store_2d(&tmC, sbuf, n0 + sub, m0);
-          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-        }
-      }
       }
     }
     if (etid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
@@ -421,13 +450,16 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 
 static CUtensorMap make_map_2d(const void* base, uint64_t inner, uint64_t outer, uint32_t box_inner,
                                uint32_t box_outer) {
+  // swizzle width = the box row (64 fp16 = 128 B, 32 = 64 B, 16 = 32 B), matching smem_desc_sw
+  const CUtensorMapSwizzle sw = box_inner >= 64 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                : (box_inner == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B);
   CUtensorMap m;
   cuuint64_t dims[2] = {inner, outer};
   cuuint64_t strides[1] = {inner * 2};
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = get_encode()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
-                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw TnError{TN_E_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")"};
   return m;
@@ -443,15 +475,15 @@ static int num_sms() {
   return n;
 }
 
-template <int BN>
+template <int BN, int KB>
 static void launch_bn(__half* c, const __half* a, const __half* bp, uint64_t M, uint32_t K2, uint32_t N2_real,
                       const float* in_max, const float* b_bound, uint32_t* out_max, int* exp_slot, const OutMap* om,
                       cudaStream_t s) {
   const uint32_t N2 = std::max<uint32_t>(N2_real, 16);  // B_P has at least 16 (zero-padded) rows
-  using C = tc::Cfg<BN>;
+  using C = tc::Cfg<BN, KB>;
   static bool attr = false;
   if (!attr) {
-    TN_CUDA(cudaFuncSetAttribute(tc::gemm_chalf_tc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
+    TN_CUDA(cudaFuncSetAttribute(tc::gemm_chalf_tc_kernel<BN, KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
     attr = true;
   }
   ScatterArgs sa;
@@ -494,23 +526,36 @@ static void launch_bn(__half* c, const __half* a, const __half* bp, uint64_t M, 
     for (int j = 0; j < kMaxModes; ++j) sa.ms[j] = om->ms[j];
     for (int j = 0; j < 24; ++j) sa.ns[j] = om->ns[j];
   }
-  CUtensorMap mb = make_map_2d(bp, K2, N2_real, tc::BK, BN);  // rows >= 2N: TMA zero fill
+  CUtensorMap mb = make_map_2d(bp, K2, N2_real, KB, BN);  // rows >= 2N: TMA zero fill
   // TMA coordinates are int32: process M in chunks of at most 2^30 rows
   const uint32_t num_n = N2 / BN;
   const uint64_t chunk = std::min<uint64_t>(1ull << 30, ((1ull << 31) / num_n) * tc::BM);
   for (uint64_t m_off = 0; m_off < M; m_off += chunk) {
     uint64_t mm = std::min<uint64_t>(chunk, M - m_off);
-    CUtensorMap ma = make_map_2d(a + m_off * K2, K2, mm, tc::BK, tc::BM);
+    CUtensorMap ma = make_map_2d(a + m_off * K2, K2, mm, KB, tc::BM);
     CUtensorMap mc = make_map_2d(c + m_off * N2, N2, mm, 64, tc::BM);
     uint32_t* out_sc = reinterpret_cast<uint32_t*>(c) + (sa.on ? outmap_m(*om, m_off) : 0);
     uint32_t num_m = (uint32_t)((mm + tc::BM - 1) / tc::BM);
     uint64_t tiles = (uint64_t)num_m * num_n;
     int grid = (int)std::min<uint64_t>(tiles, (uint64_t)num_sms());
     // the exponent is recorded once (first chunk); later chunks reuse the same inputs
-    tc::gemm_chalf_tc_kernel<BN><<<grid, tc::kThreads, C::kSmem, s>>>(
+    tc::gemm_chalf_tc_kernel<BN, KB><<<grid, tc::kThreads, C::kSmem, s>>>(
         ma, mb, mc, num_m, num_n, (int)K2, in_max, b_bound, out_max, m_off ? nullptr : exp_slot, sa, out_sc, mm,
         n_cols);
     TN_CUDA(cudaGetLastError());
+  }
+}
+
+template <int KB>
+static void launch_k(__half* c, const __half* a, const __half* bp, uint64_t M, uint32_t K2, uint32_t N2,
+                     const float* in_max, const float* b_bound, uint32_t* out_max, int* exp_slot, const OutMap* om,
+                     cudaStream_t s) {
+  switch (N2 < 16 ? 16 : N2) {
+    case 16: launch_bn<16, KB>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s); break;
+    case 32: launch_bn<32, KB>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s); break;
+    case 64: launch_bn<64, KB>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s); break;
+    case 128: launch_bn<128, KB>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s); break;
+    default: launch_bn<256, KB>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s); break;
   }
 }
 
@@ -520,12 +565,10 @@ void launch_gemm_chalf_tc(__half* c, const __half* a, const __half* bp, uint64_t
   if (K2 < 8 || N2 < 2 || (K2 & (K2 - 1)) || (N2 & (N2 - 1)))
     throw TnError{TN_E_INVALID, "tcgen05 GEMM needs power-of-two 2K >= 8, 2N >= 2"};
   if (M == 0) return;
-  switch (N2 < 16 ? 16 : N2) {
-    case 16: launch_bn<16>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s); break;
-    case 32: launch_bn<32>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s); break;
-    case 64: launch_bn<64>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s); break;
-    case 128: launch_bn<128>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s); break;
-    default: launch_bn<256>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s); break;
+  switch (K2 >= 64 ? 64 : (K2 >= 32 ? 32 : 16)) {
+    case 64: launch_k<64>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s); break;
+    case 32: launch_k<32>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s); break;
+    default: launch_k<16>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s); break;
   }
 }
 

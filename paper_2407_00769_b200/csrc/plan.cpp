@@ -453,10 +453,10 @@ Plan* load_plan(const char* json, size_t len, const tn_config* cfg_in, int world
       st.klog = (int)R.size();
       st.nlog = (int)newl.size();
       st.out_layout = out;
-      // tcgen05 when the tile carries enough work; small K*N steps go to the tiled SIMT kernel
-      // (K <= 8, N <= 16: the SIMT row kernel streams at HBM speed; ncu showed 128x16 tcgen05
-      //  tiles at 16 % of DRAM peak, profiles/r01_ncu_summary.md)
-      const bool rows_kernel = st.klog <= 3 && st.nlog <= 4;
+      // tcgen05 when the tile carries enough work; small K*N steps go to the SIMT row-streaming
+      // kernel (K <= 16, N <= 32, K*N <= 128: streams at HBM speed, k_gemm_simt.cu rows_ok; ncu
+      // showed 128x16 tcgen05 tiles at 16 % of DRAM peak, profiles/r01_ncu_summary.md)
+      const bool rows_kernel = st.klog <= 4 && st.nlog <= 5 && st.klog + st.nlog <= 7;
       st.tensor_core = (cfg.dtype == TN_CHALF) && st.klog >= 2 && !rows_kernel &&
                        ((st.klog >= 3 && st.nlog >= 3) || st.klog >= 4 || st.klog + st.nlog > 11);
       {

@@ -81,7 +81,8 @@ def _half_pairs(z):
 
 @pytest.mark.parametrize("M,K,N", [(1, 8, 8), (128, 8, 8), (300, 16, 8), (1000, 8, 32), (4096 + 37, 32, 64),
                                    (777, 64, 128), (2048, 128, 256), (513, 256, 16), (1024, 512, 512),
-                                   (256, 2048, 8), (640, 8, 1024)])
+                                   (256, 2048, 8), (640, 8, 1024), (1000, 4, 64), (5000, 16, 4),
+                                   (3000, 8, 2), (129, 4, 256), (4100, 16, 256)])
 def test_gemm_chalf_tensor_core_vs_oracle(env, M, K, N):
     """tcgen05 Eq. 6 GEMM (no scaling) vs the oracle's real-embedding GEMM in fp64 on the same
     fp16 operands.  Error: one fp16 rounding of C (2^-11 relative) + fp32 accumulation."""
