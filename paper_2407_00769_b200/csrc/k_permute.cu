@@ -6,12 +6,15 @@
 // B200 design: HBM-bound (algorithmic bytes = 2 * elem_bytes * 2^n per pass).
 //  * leading modes that stay innermost in the same order are folded into a wider element
 //    (up to 16 bytes), so pure block moves become 16-byte copies;
-//  * each CTA moves tiles of 2^u elements (16 KB) spanning the innermost INPUT bits and the
-//    innermost OUTPUT bits (extended alternately until the tile reaches 16 KB, so overlapping
+//  * each CTA moves tiles of 2^u elements (32 KB) spanning the innermost INPUT bits and the
+//    innermost OUTPUT bits (extended alternately until the tile reaches 32 KB, so overlapping
 //    inner modes never shrink the tile), staged through shared memory: HBM reads are 16-byte
 //    vectors along the input's innermost bits, HBM writes 16-byte vectors along the output's;
-//  * tile index tables are built once per CTA; grid-stride over tiles, grid = 148 x CTAs/SM.
+//  * stem-sized tensors (permute_pipe_kernel): per-thread offsets in registers, a 3-deep cp.async
+//    ring of XOR-swizzled tiles, grid = 148 x 2 persistent CTAs (measured best of 16/32/64 KB
+//    tiles x 1-8 CTAs/SM on C3: 32 KB x 2);  tiny tensors: permute_kernel (smem index tables).
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -94,6 +97,132 @@ __global__ void __launch_bounds__(256) permute_kernel(T* __restrict__ dst, const
   }
 }
 
+// Pipelined variant for full 16-byte vectors (the stem-sized case): the tile structure is the same
+// for every tile, so each thread keeps its NV read offsets, write offsets and gather indices in
+// registers (no smem tables), and tiles stream through a ring of kPermStages shared-memory buffers
+// filled by cp.async (LDGSTS, 16 B): kPermStages-1 tiles of reads are in flight while one is written.
+constexpr int kPermStages = 3;
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)),
+               "l"(gmem)
+               : "memory");
+}
+
+// 16-byte slots of a tile are XOR-swizzled (slot bits 0-2 ^= the XOR of bit triples 3-5, 6-8, 9-11)
+// so the write-side gathers, which step through the tile at power-of-two strides, spread over the
+// banks whichever tile bits vary across a warp.  Bits >= 3 are unchanged: a bijection.
+__device__ __forceinline__ int perm_swz(int v) { return v ^ (((v >> 3) ^ (v >> 6) ^ (v >> 9)) & 7); }
+
+template <typename T, int NV>
+__global__ void __launch_bounds__(256) permute_pipe_kernel(T* __restrict__ dst, const T* __restrict__ src,
+                                                           const PermArgs2 args, uint64_t n_tiles) {
+  extern __shared__ __align__(16) uint4 ring[];
+  constexpr int V = 16 / sizeof(T);
+  const int u = args.u, vb = args.vb;
+  const int nvec = (1 << u) >> vb;
+  int64_t in_off[NV], out_off[NV];
+  uint16_t gi[NV][V];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int v = threadIdx.x + 256 * i;
+    const int e = v << vb;
+    int64_t io = 0, oo = 0;
+    for (int j = vb; j < u; ++j)
+      if ((e >> j) & 1) {
+        io += args.tile_in[j];
+        oo += args.tile_out[args.wr_map[j]];
+      }
+    in_off[i] = io;
+    out_off[i] = oo;
+#pragma unroll
+    for (int q = 0; q < V; ++q) {
+      const int w = e + q;
+      int r = 0;
+      for (int j = 0; j < u; ++j)
+        if ((w >> j) & 1) r |= 1 << args.wr_map[j];
+      gi[i][q] = (uint16_t)((perm_swz(r >> vb) << vb) | (r & ((1 << vb) - 1)));
+    }
+  }
+  const int n_outer = args.n - u;
+  auto base_of = [&](uint64_t t, int64_t& bi, int64_t& bo) {
+    bi = 0;
+    bo = 0;
+    for (int j = 0; j < n_outer; ++j)
+      if ((t >> j) & 1) {
+        bi += args.outer_in[j];
+        bo += args.outer_out[j];
+      }
+  };
+  auto issue = [&](uint64_t t, int slot) {
+    int64_t bi, bo;
+    base_of(t, bi, bo);
+    uint4* buf = ring + (size_t)slot * nvec;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int v = threadIdx.x + 256 * i;
+      if (v < nvec) cp_async16(buf + perm_swz(v), src + bi + in_off[i]);
+    }
+  };
+#pragma unroll
+  for (int st = 0; st < kPermStages - 1; ++st) {
+    const uint64_t t = blockIdx.x + (uint64_t)st * gridDim.x;
+    if (t < n_tiles) issue(t, st);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  int slot = 0;
+  for (uint64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+    const uint64_t t2 = t + (uint64_t)(kPermStages - 1) * gridDim.x;
+    if (t2 < n_tiles) issue(t2, (slot + kPermStages - 1) % kPermStages);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_group %0;" ::"n"(kPermStages - 1) : "memory");
+    __syncthreads();
+    int64_t bi, bo;
+    base_of(t, bi, bo);
+    const T* tile = reinterpret_cast<const T*>(ring + (size_t)slot * nvec);
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int v = threadIdx.x + 256 * i;
+      if (v < nvec) {
+        uint4 x;
+        T* xp = reinterpret_cast<T*>(&x);
+#pragma unroll
+        for (int q = 0; q < V; ++q) xp[q] = tile[gi[i][q]];
+        *reinterpret_cast<uint4*>(dst + bo + out_off[i]) = x;
+      }
+    }
+    __syncthreads();
+    slot = (slot + 1) % kPermStages;
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
+
+template <typename T>
+static void launch_pipe(void* dst, const void* src, const PermArgs2& args, uint64_t n_tiles, int nvec, cudaStream_t s) {
+  const size_t smem = (size_t)kPermStages * nvec * 16;
+  static bool attr = false;
+  if (!attr) {
+    TN_CUDA(cudaFuncSetAttribute(permute_pipe_kernel<T, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    TN_CUDA(cudaFuncSetAttribute(permute_pipe_kernel<T, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024));
+    TN_CUDA(cudaFuncSetAttribute(permute_pipe_kernel<T, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+    TN_CUDA(cudaFuncSetAttribute(permute_pipe_kernel<T, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+    TN_CUDA(cudaFuncSetAttribute(permute_pipe_kernel<T, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+    attr = true;
+  }
+  static const int ctas = getenv("TN_PERM_CTAS") ? atoi(getenv("TN_PERM_CTAS")) : 2;  // tuning knob
+  const int blocks = (int)std::min<uint64_t>(n_tiles, 148ull * ctas);
+  if (nvec > 2048)
+    permute_pipe_kernel<T, 16><<<blocks, 256, smem, s>>>((T*)dst, (const T*)src, args, n_tiles);
+  else if (nvec > 1024)
+    permute_pipe_kernel<T, 8><<<blocks, 256, smem, s>>>((T*)dst, (const T*)src, args, n_tiles);
+  else if (nvec > 512)
+    permute_pipe_kernel<T, 4><<<blocks, 256, smem, s>>>((T*)dst, (const T*)src, args, n_tiles);
+  else if (nvec > 256)
+    permute_pipe_kernel<T, 2><<<blocks, 256, smem, s>>>((T*)dst, (const T*)src, args, n_tiles);
+  else
+    permute_pipe_kernel<T, 1><<<blocks, 256, smem, s>>>((T*)dst, (const T*)src, args, n_tiles);
+}
+
 void launch_permute(void* dst, const void* src, int elem_bytes, int n, const int* perm, cudaStream_t s) {
   if (n < 0 || n > 46) throw TnError{TN_E_INVALID, "permute: rank out of range"};
   if (elem_bytes != 4 && elem_bytes != 8 && elem_bytes != 16)
@@ -127,7 +256,8 @@ void launch_permute(void* dst, const void* src, int elem_bytes, int n, const int
   const int vb_full = eb == 4 ? 2 : (eb == 8 ? 1 : 0);  // 16-byte vectors
   const int vb = (nn >= vb_full) ? vb_full : 0;  // tiny tensors: scalar elements
   // tile: input bits 0..a-1 and output bits 0..b-1, extended until 16 KB (or the whole tensor)
-  const int u_target = std::min(nn, (eb == 4 ? 12 : (eb == 8 ? 11 : 10)));
+  static const int ux = getenv("TN_PERM_UX") ? atoi(getenv("TN_PERM_UX")) : 1;  // tuning knob: tile bits
+  const int u_target = std::min(nn, (eb == 4 ? 12 : (eb == 8 ? 11 : 10)) + ux);
   std::vector<char> in_tile(nn, 0);
   std::vector<int> tile_bits;
   int a = 0, b = 0;
@@ -186,6 +316,16 @@ void launch_permute(void* dst, const void* src, int elem_bytes, int n, const int
     }
   const uint64_t n_tiles = 1ull << (nn - args.u);
   const int tsz = 1 << args.u, nvec = tsz >> vb;
+  static const bool legacy = getenv("TN_PERM_LEGACY") != nullptr;  // A/B knob for the old kernel
+  if (vb == vb_full && nvec <= 4096 && !legacy) {
+    switch (eb) {
+      case 4: launch_pipe<uint32_t>(dst, src, args, n_tiles, nvec, s); break;
+      case 8: launch_pipe<uint2>(dst, src, args, n_tiles, nvec, s); break;
+      default: launch_pipe<uint4>(dst, src, args, n_tiles, nvec, s); break;
+    }
+    TN_CUDA(cudaGetLastError());
+    return;
+  }
   size_t smem = (size_t)nvec * 16 + (((size_t)tsz * 2 + 15) & ~(size_t)15) + (size_t)tsz * eb;
   int blocks = (int)std::min<uint64_t>(n_tiles, 148ull * 8);
   static bool attr_set[3] = {false, false, false};
