@@ -269,7 +269,16 @@ def main():
         ach = perm_bytes / (perm_ms * 1e-3) / 1e9
         roof = {"kernel": "permute", "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm}
     roof["peak_source"] = src
+    # traffic: DRAM bytes (dram__bytes_read + dram__bytes_write) of the same kernel family per
+    # subtask, from the committed ncu launch list of this command (profiles/, C3 single GPU only)
     roof["traffic"] = None
+    roof["algorithmic_bytes"] = gemm_bytes
+    summ = os.path.join(ROOT, "profiles", "r01_launches_summary.json")
+    if roof["kernel"].startswith("gemm") and args.plan == "c3" and world == 1 and os.path.exists(summ):
+        with open(summ) as fh:
+            ps = json.load(fh)["per_subtask"]
+        roof["traffic"] = sum(ps[f]["dram_bytes"] for f in ("gemm_tc", "gemm_simt") if f in ps)
+        roof["traffic_source"] = "profiles/r01_launches_summary.json (ncu, bytes per subtask, all GEMM launches)"
     roof["share_of_step"] = {"gemm": gemm_ms / t_ms, "permute": perm_ms / t_ms, "common+prep": common_ms / t_ms}
 
     if rank == 0:
