@@ -80,7 +80,10 @@ typedef struct {
                                 fp16.  Negative: 50 */
   int32_t virtual_world;     /* > 1 with comm == NULL: lower the plan for that many ranks
                                 (host-only inspection of the shard/swap schedule) */
-  int32_t reserved[4];
+  int32_t no_gather;         /* 0 (default): a permutation before a tensor-core step whose two
+                                innermost modes are contracted is fused into the GEMM's A load
+                                (gathered cp.async, no permutation pass); 1: always a pass */
+  int32_t reserved[3];
 } tn_config;
 
 /* Caller-owned device buffers lent to a call (P:18-22 double buffering). */
@@ -190,6 +193,16 @@ TN_API int tn_permute(void* d_dst, const void* d_src, int elem_bytes, int n, con
 TN_API int tn_gemm_chalf(void* d_c, const void* d_a, const void* d_bp, uint64_t M, uint32_t K, uint32_t N,
                   const float* d_in_max, const float* d_b_bound, uint32_t* d_out_max, int* d_exp,
                   void* stream);
+
+/* tn_gemm_chalf with a strided (gathered) A: A[m, k] is the complex-half element at
+ * d_a + sum_j bit_j(m) m_stride[j] + sum_j bit_j(k) k_stride[j] (complex elements; j = 0 is the
+ * lowest bit).  This is the stem permutation fused into the GEMM load ("dimension
+ * reordering").  M = 2^mlog >= 128, K = 2^klog >= 8 with k_stride[0] = 1, k_stride[1] = 2 (every
+ * 16-byte piece of a row contiguous), N a power of two; C row-major [M][N].  Scale pointers as
+ * tn_gemm_chalf.  TN_E_INVALID otherwise. */
+TN_API int tn_gemm_chalf_gather(void* d_c, const void* d_a, const void* d_bp, int mlog, int klog, uint32_t N,
+                                const int64_t* m_stride, const int64_t* k_stride, const float* d_in_max,
+                                const float* d_b_bound, uint32_t* d_out_max, int* d_exp, void* stream);
 
 /* Complex64 stem GEMM (fp32 SIMT): C[M,N] = A[M,K] B[K,N], all interleaved complex64 row-major. */
 TN_API int tn_gemm_cfloat(void* d_c, const void* d_a, const void* d_b, uint64_t M, uint32_t K, uint32_t N,

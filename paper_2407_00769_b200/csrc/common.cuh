@@ -104,9 +104,16 @@ void launch_gemm_c64(float2* c, const float2* a, const float2* b, uint64_t M, ui
 void launch_gemm_chalf_simt(__half2* c, const __half2* a, const __half* bp, uint64_t M, uint32_t K,
                             uint32_t N, const float* in_max, const float* b_bound,
                             uint32_t* out_max, int* exp_slot, const OutMap* om, cudaStream_t s);
+// Strided A operand of a tcgen05 GEMM (the stem permutation fused into the load): A[m, k] at
+// a + sum_j bit_j(m) ms[j] + sum_j bit_j(k) ks[j] complex elements; requires ks[0] = 1, ks[1] = 2.
+struct AGather {
+  int mlog, klog;
+  int64_t ms[kMaxModes];
+  int64_t ks[24];
+};
 void launch_gemm_chalf_tc(__half* c, const __half* a, const __half* bp, uint64_t M, uint32_t K2,
                           uint32_t N2, const float* in_max, const float* b_bound, uint32_t* out_max,
-                          int* exp_slot, const OutMap* om, cudaStream_t s);
+                          int* exp_slot, const OutMap* om, cudaStream_t s, const AGather* ag = nullptr);
 OutMap identity_map(uint64_t M, uint32_t N);
 void launch_top1_chalf(const __half2* amps, uint64_t n_sub, uint64_t members, uint64_t* top, cudaStream_t s);
 void launch_quant_int8(int8_t* codes, float* scales, float* zeros, const float* x, uint64_t n, int g,

@@ -32,7 +32,9 @@ namespace tn {
 namespace tc {
 
 constexpr int BM = 128;
-constexpr int kThreads = 384;  // 4 role warps + 2 epilogue warpgroups
+constexpr int kThreads = 384;        // 4 role warps + 2 epilogue warpgroups
+constexpr int kThreadsGather = 512;  // + 4 warps gathering A (fused permutation)
+constexpr int kGatherWarps = 4;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -143,7 +145,7 @@ struct Cfg {
   static constexpr int kCBytes = kCTma;
   static constexpr int kStagesRaw = (220 * 1024 - kCBytes) / kStageBytes;
   static constexpr int kStages = kStagesRaw > 24 ? 24 : kStagesRaw;
-  static constexpr int kSmem = kStages * kStageBytes + kCBytes + 1024 /*align*/ + 1024 /*barriers*/;
+  static constexpr int kSmem = kStages * kStageBytes + kCBytes + 1024 /*align*/ + 2048 /*barriers, gather table*/;
   // TMEM accumulators: as many as fit in 512 columns (<= 16), so the MMA runs ahead of the
   // epilogue by several tiles when a tile is small (small K, small N)
   static constexpr int kAccStride = BN < 32 ? 32 : BN;
@@ -189,15 +191,36 @@ __device__ __forceinline__ void tile_coords(const ScatterArgs& sa, uint32_t t, u
   }
 }
 
+// Gathered A operand (the stem permutation fused into the GEMM load): A[m, k] (complex-half) sits at
+// a + sum_j bit_j(m) ms[j] + sum_j bit_j(k) ks[j] (complex elements) with ks[0] = 1, ks[1] = 2, so
+// every 16-byte piece of a K-major smem row is 4 contiguous complex values.  A stage (128 rows x
+// KB fp16) is nvb = 7 + log2(KB/8) "vector bits" (row bits and 16-byte chunk bits); they are sorted
+// by source stride on the host so the 32 lanes of a warp read the lowest-stride (most contiguous)
+// combinations.
+struct AGatherArgs {
+  const uint32_t* a;
+  uint64_t m_base;  // row offset of this launch chunk
+  int mlog, klog, nvb;
+  int fence;           // consumer-side proxy fence (TN_GATHER_FENCE; off: CUTLASS's cp.async->UMMA pipelines use none)
+  int8_t vb_is_k[16];  // vector bit b: 16-byte chunk bit (k bit 2 + idx) or row bit (m bit idx)
+  int8_t vb_idx[16];
+  int64_t ms[kMaxModes];
+  int64_t ks[24];
+};
+
 namespace tc {
 
-template <int BN, int KB>
-__global__ void __launch_bounds__(kThreads, 1)
+__device__ __forceinline__ void cp_async16(uint32_t smem_addr, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr), "l"(gmem) : "memory");
+}
+
+template <int BN, int KB, bool kGather>
+__global__ void __launch_bounds__(kGather ? kThreadsGather : kThreads, 1)
     gemm_chalf_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                          const __grid_constant__ CUtensorMap tmC, uint32_t num_m, uint32_t num_n, int K2,
                          const float* in_max, const float* b_bound, uint32_t* out_max, int* exp_slot,
                          const __grid_constant__ ScatterArgs sc_args, uint32_t* out_scatter, uint64_t rows,
-                         uint32_t n_cols) {
+                         uint32_t n_cols, const __grid_constant__ AGatherArgs ga) {
   using C = Cfg<BN, KB>;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
@@ -209,6 +232,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tfull = empty + C::kStages;
   uint64_t* tempty = tfull + C::kNAcc;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + C::kNAcc);
+  struct GTab {
+    int64_t off;
+    int rc;
+    int pad;
+  };
+  GTab* gtab = reinterpret_cast<GTab*>(reinterpret_cast<unsigned char*>(full) + 1024);  // gather table
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t num_tiles = num_m * num_n;
@@ -217,7 +246,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < C::kStages; ++s) {
-      mbar_init(&full[s], 1);
+      mbar_init(&full[s], kGather ? 2 : 1);  // gather: the TMA (B) arrive + the gather warp's arrive
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < C::kNAcc; ++a) {
@@ -257,9 +286,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int kb = 0; kb < num_k; ++kb) {
           mbar_wait(&empty[s], ph ^ 1);
-          mbar_expect_tx(&full[s], b_resident ? C::kABytes : C::kStageBytes);
-          tma_load_2d(sA + s * C::kABytes, &tmA, &full[s], kb * KB, m0);
-          if (!b_resident) tma_load_2d(sB + s * C::kBBytes, &tmB, &full[s], kb * KB, n0);
+          if (kGather) {  // A comes from the gather warps
+            if (b_resident) {
+              mbar_arrive(&full[s]);
+            } else {
+              mbar_expect_tx(&full[s], C::kBBytes);
+              tma_load_2d(sB + s * C::kBBytes, &tmB, &full[s], kb * KB, n0);
+            }
+          } else {
+            mbar_expect_tx(&full[s], b_resident ? C::kABytes : C::kStageBytes);
+            tma_load_2d(sA + s * C::kABytes, &tmA, &full[s], kb * KB, m0);
+            if (!b_resident) tma_load_2d(sB + s * C::kBBytes, &tmB, &full[s], kb * KB, n0);
+          }
           if (++s == C::kStages) {
             s = 0;
             ph ^= 1;
@@ -281,6 +319,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kb = 0; kb < num_k; ++kb) {
           mbar_wait(&full[s], ph);
           tc_fence_after();
+          if (kGather && ga.fence) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // experiment knob
           const int nkk = (kb == num_k - 1) ? last_kk : KB / 16;
           const uint64_t ad = smem_desc_sw<KB>(sA + s * C::kABytes);
           const uint64_t bd = smem_desc_sw<KB>(sB + s * C::kBBytes);
@@ -297,6 +336,102 @@ __global__ void __launch_bounds__(kThreads, 1)
         mma_commit(&tfull[acc]);
       }
     }
+  } else if (kGather && warp >= 12) {
+    // ===== A gather (fused stem permutation): warp g fills the ring slots s = g mod 4 with
+    // cp.async 16-byte pieces at arbitrary source strides, up to 4 stages in flight per warp
+    // (commit groups); a stage is published by wait_group + proxy fence + mbarrier arrive
+    const int g = warp - 12;
+    constexpr int kCB = KB / 8;                 // 16-byte chunks per row
+    constexpr int kLogCB = kCB == 8 ? 3 : (kCB == 4 ? 2 : 1);
+    constexpr int kIters = BM * kCB / 32;       // pieces per lane per stage (32, 16 or 8)
+    // piece v = it * 32 + lane; vector bits 0..4 come from the lane, 5.. from it.  Offsets and
+    // (row, chunk) of both parts are tile-independent: lane part in registers, it part in a
+    // 32-entry smem table (one broadcast load per piece)
+    int64_t off_lane = 0;
+    int r_lane = 0, c_lane = 0;
+    int64_t off_it = 0;
+    int r_it = 0, c_it = 0;
+    for (int b = 0; b < ga.nvb; ++b) {
+      const bool on = b < 5 ? ((lane >> b) & 1) : ((lane >> (b - 5)) & 1);
+      if (!on) continue;
+      const int64_t st = ga.vb_is_k[b] ? ga.ks[2 + ga.vb_idx[b]] : ga.ms[ga.vb_idx[b]];
+      const int rb = ga.vb_is_k[b] ? 0 : (1 << ga.vb_idx[b]);
+      const int cb = ga.vb_is_k[b] ? (1 << ga.vb_idx[b]) : 0;
+      if (b < 5) {
+        off_lane += st;
+        r_lane |= rb;
+        c_lane |= cb;
+      } else {
+        off_it += st;
+        r_it |= rb;
+        c_it |= cb;
+      }
+    }
+    if (lane < kIters) {
+      gtab[lane].off = off_it;
+      gtab[lane].rc = (r_it << 8) | c_it;
+    }
+    __syncwarp();
+    const uint32_t sA_u32 = smem_u32(sA);
+    // this warp owns ring slots g, g+4, ...; it keeps up to `depth` of them in flight (cp.async
+    // groups), completing the oldest (wait_group + proxy fence + arrive) before reusing a slot
+    const int owned = C::kStages > g ? (C::kStages - 1 - g) / kGatherWarps + 1 : 0;
+    const int depth = owned < 4 ? owned : 4;
+    uint32_t pend = 0;  // ring of pending slots, 8 bits each, oldest in the low byte
+    int npend = 0;
+    auto complete_oldest = [&]() {
+      switch (npend - 1) {  // wait until only the npend-1 youngest groups are outstanding
+        case 0: asm volatile("cp.async.wait_group 0;" ::: "memory"); break;
+        case 1: asm volatile("cp.async.wait_group 1;" ::: "memory"); break;
+        case 2: asm volatile("cp.async.wait_group 2;" ::: "memory"); break;
+        default: asm volatile("cp.async.wait_group 3;" ::: "memory"); break;
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic (cp.async) -> async proxy (UMMA)
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&full[pend & 0xff]);
+      pend >>= 8;
+      --npend;
+    };
+    uint32_t q = 0;
+    int64_t mbase = 0;
+    for (uint32_t t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      int m0, n0;
+      tile_coords(sc_args, t, num_n, BM, BN, m0, n0);
+      bool have_m = false;
+      for (int kb = 0; kb < num_k; ++kb, ++q) {
+        // each ring slot always belongs to the same gather warp, so its phases are waited in order
+        const int s = (int)(q % C::kStages);
+        if (s % kGatherWarps != g) continue;
+        const uint32_t ph = (q / C::kStages) & 1;
+        if (!have_m) {  // m bits >= 7 of the tile's first row
+          mbase = 0;
+          const uint64_t mrow = ga.m_base + (uint64_t)m0;
+          for (int j = 7; j < ga.mlog; ++j)
+            if ((mrow >> j) & 1) mbase += ga.ms[j];
+          have_m = true;
+        }
+        int64_t base = mbase + off_lane;
+        const uint32_t kc = (uint32_t)kb * (KB / 2);  // complex k index of the box start
+        for (int j = 2 + kLogCB; j < ga.klog; ++j)
+          if ((kc >> j) & 1) base += ga.ks[j];
+        if (npend == depth) complete_oldest();
+        mbar_wait(&empty[s], ph ^ 1);
+        const uint32_t stage = sA_u32 + s * C::kABytes;
+        const uint32_t* src = ga.a + base;
+#pragma unroll
+        for (int it = 0; it < kIters; ++it) {
+          const GTab e = gtab[it];
+          const int r = r_lane | (e.rc >> 8), c = c_lane | (e.rc & 0xff);
+          // swizzled K-major row (SW128 / SW64 / SW32 as the TMA box would have written it)
+          const int sw = KB == 64 ? (r & 7) : (KB == 32 ? ((r >> 1) & 3) : ((r >> 2) & 1));
+          cp_async16(stage + r * (2 * KB) + ((c ^ sw) << 4), src + e.off);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        pend |= (uint32_t)s << (8 * npend);
+        ++npend;
+      }
+    }
+    while (npend > 0) complete_oldest();
   } else if (warp >= 4) {
     // ===== epilogue: two independent warpgroups, group g drains the tiles i = g mod 2
     const int grp = (warp - 4) >> 2;
@@ -475,16 +610,44 @@ static int num_sms() {
   return n;
 }
 
-template <int BN, int KB>
+template <int BN, int KB, bool G>
 static void launch_bn(__half* c, const __half* a, const __half* bp, uint64_t M, uint32_t K2, uint32_t N2_real,
                       const float* in_max, const float* b_bound, uint32_t* out_max, int* exp_slot, const OutMap* om,
-                      cudaStream_t s) {
+                      cudaStream_t s, const AGather* ag) {
   const uint32_t N2 = std::max<uint32_t>(N2_real, 16);  // B_P has at least 16 (zero-padded) rows
   using C = tc::Cfg<BN, KB>;
   static bool attr = false;
   if (!attr) {
-    TN_CUDA(cudaFuncSetAttribute(tc::gemm_chalf_tc_kernel<BN, KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
+    TN_CUDA(cudaFuncSetAttribute(tc::gemm_chalf_tc_kernel<BN, KB, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 C::kSmem));
     attr = true;
+  }
+  AGatherArgs gargs;
+  memset(&gargs, 0, sizeof(gargs));
+  if (G) {
+    // vector bits of a stage: 7 row bits + log2(KB/8) chunk bits, by source stride (lanes take the
+    // 5 smallest: the most contiguous reads)
+    gargs.a = reinterpret_cast<const uint32_t*>(a);
+    static const bool fence_env = getenv("TN_GATHER_FENCE") != nullptr;
+    gargs.fence = fence_env ? 1 : 0;
+    gargs.mlog = ag->mlog;
+    gargs.klog = ag->klog;
+    for (int j = 0; j < kMaxModes; ++j) gargs.ms[j] = ag->ms[j];
+    for (int j = 0; j < 24; ++j) gargs.ks[j] = ag->ks[j];
+    struct VB {
+      int64_t stride;
+      int is_k, idx;
+    };
+    std::vector<VB> vb;
+    for (int j = 0; j < 7; ++j) vb.push_back({ag->ms[j], 0, j});
+    const int cb = KB == 64 ? 3 : (KB == 32 ? 2 : 1);
+    for (int j = 0; j < cb; ++j) vb.push_back({ag->ks[2 + j], 1, j});
+    std::stable_sort(vb.begin(), vb.end(), [](const VB& x, const VB& y) { return x.stride < y.stride; });
+    gargs.nvb = (int)vb.size();
+    for (int b = 0; b < gargs.nvb; ++b) {
+      gargs.vb_is_k[b] = (int8_t)vb[b].is_k;
+      gargs.vb_idx[b] = (int8_t)vb[b].idx;
+    }
   }
   ScatterArgs sa;
   memset(&sa, 0, sizeof(sa));
@@ -532,43 +695,58 @@ static void launch_bn(__half* c, const __half* a, const __half* bp, uint64_t M, 
   const uint64_t chunk = std::min<uint64_t>(1ull << 30, ((1ull << 31) / num_n) * tc::BM);
   for (uint64_t m_off = 0; m_off < M; m_off += chunk) {
     uint64_t mm = std::min<uint64_t>(chunk, M - m_off);
-    CUtensorMap ma = make_map_2d(a + m_off * K2, K2, mm, KB, tc::BM);
+    // (gather: the A map is unused; any valid map will do)
+    CUtensorMap ma = make_map_2d(G ? a : a + m_off * K2, K2, G ? tc::BM : mm, KB, tc::BM);
+    gargs.m_base = m_off;
     CUtensorMap mc = make_map_2d(c + m_off * N2, N2, mm, 64, tc::BM);
     uint32_t* out_sc = reinterpret_cast<uint32_t*>(c) + (sa.on ? outmap_m(*om, m_off) : 0);
     uint32_t num_m = (uint32_t)((mm + tc::BM - 1) / tc::BM);
     uint64_t tiles = (uint64_t)num_m * num_n;
     int grid = (int)std::min<uint64_t>(tiles, (uint64_t)num_sms());
     // the exponent is recorded once (first chunk); later chunks reuse the same inputs
-    tc::gemm_chalf_tc_kernel<BN, KB><<<grid, tc::kThreads, C::kSmem, s>>>(
+    tc::gemm_chalf_tc_kernel<BN, KB, G><<<grid, G ? tc::kThreadsGather : tc::kThreads, C::kSmem, s>>>(
         ma, mb, mc, num_m, num_n, (int)K2, in_max, b_bound, out_max, m_off ? nullptr : exp_slot, sa, out_sc, mm,
-        n_cols);
+        n_cols, gargs);
     TN_CUDA(cudaGetLastError());
   }
 }
 
-template <int KB>
+template <int KB, bool G>
 static void launch_k(__half* c, const __half* a, const __half* bp, uint64_t M, uint32_t K2, uint32_t N2,
                      const float* in_max, const float* b_bound, uint32_t* out_max, int* exp_slot, const OutMap* om,
-                     cudaStream_t s) {
+                     cudaStream_t s, const AGather* ag) {
   switch (N2 < 16 ? 16 : N2) {
-    case 16: launch_bn<16, KB>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s); break;
-    case 32: launch_bn<32, KB>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s); break;
-    case 64: launch_bn<64, KB>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s); break;
-    case 128: launch_bn<128, KB>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s); break;
-    default: launch_bn<256, KB>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s); break;
+    case 16: launch_bn<16, KB, G>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, ag); break;
+    case 32: launch_bn<32, KB, G>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, ag); break;
+    case 64: launch_bn<64, KB, G>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, ag); break;
+    case 128: launch_bn<128, KB, G>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, ag); break;
+    default: launch_bn<256, KB, G>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, ag); break;
   }
 }
 
 void launch_gemm_chalf_tc(__half* c, const __half* a, const __half* bp, uint64_t M, uint32_t K2, uint32_t N2,
                           const float* in_max, const float* b_bound, uint32_t* out_max, int* exp_slot,
-                          const OutMap* om, cudaStream_t s) {
+                          const OutMap* om, cudaStream_t s, const AGather* ag) {
   if (K2 < 8 || N2 < 2 || (K2 & (K2 - 1)) || (N2 & (N2 - 1)))
     throw TnError{TN_E_INVALID, "tcgen05 GEMM needs power-of-two 2K >= 8, 2N >= 2"};
   if (M == 0) return;
+  if (ag) {
+    // the gathered load needs whole 128-row tiles, 16-byte pieces (k bits 0, 1 contiguous) and
+    // K-boxes of at least 16 fp16
+    if (M % tc::BM || K2 < 16 || ag->ks[0] != 1 || ag->ks[1] != 2 || (uint64_t)1 << ag->mlog != M ||
+        (2u << ag->klog) != K2)
+      throw TnError{TN_E_INVALID, "gathered-A GEMM: unsupported operand geometry"};
+    switch (K2 >= 64 ? 64 : (K2 >= 32 ? 32 : 16)) {
+      case 64: launch_k<64, true>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, ag); break;
+      case 32: launch_k<32, true>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, ag); break;
+      default: launch_k<16, true>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, ag); break;
+    }
+    return;
+  }
   switch (K2 >= 64 ? 64 : (K2 >= 32 ? 32 : 16)) {
-    case 64: launch_k<64>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s); break;
-    case 32: launch_k<32>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s); break;
-    default: launch_k<16>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s); break;
+    case 64: launch_k<64, false>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, nullptr); break;
+    case 32: launch_k<32, false>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, nullptr); break;
+    default: launch_k<16, false>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, nullptr); break;
   }
 }
 

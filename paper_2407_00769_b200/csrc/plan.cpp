@@ -546,6 +546,33 @@ Plan* load_plan(const char* json, size_t len, const tn_config* cfg_in, int world
       }
       smax = need;
     }
+    // ---- fused permutations (gathered-A tcgen05 GEMM): a permutation before a tensor-core step is
+    // folded into the GEMM's A load when the two innermost input modes are contracted (16-byte
+    // pieces stay contiguous), the step is not chunked (split tail) and M >= 128.  K order = R in
+    // input order, M order = kept as the permutation would have placed them, so B_P and the output
+    // layout are unchanged.
+    if (!cfg.no_gather && cfg.dtype == TN_CHALF) {
+      for (auto& st : p.steps) {
+        if (!st.perm || !st.tensor_core || st.split || st.mlog < 7 || st.klog < 3) continue;
+        const std::vector<int>& IL = st.in_layout;
+        const int r = (int)IL.size();
+        std::set<int> Rs(st.R.begin(), st.R.end());
+        if (r < 2 || !Rs.count(IL[r - 1]) || !Rs.count(IL[r - 2])) continue;
+        auto src_stride = [&](int l) {
+          return (int64_t)1 << (r - 1 - (int)(std::find(IL.begin(), IL.end(), l) - IL.begin()));
+        };
+        st.a_m_stride.resize(st.mlog);
+        st.a_k_stride.resize(st.klog);
+        for (int j = 0; j < st.mlog; ++j) st.a_m_stride[j] = src_stride(st.kept[st.mlog - 1 - j]);
+        for (int j = 0; j < st.klog; ++j) st.a_k_stride[j] = src_stride(st.R[st.klog - 1 - j]);
+        if (st.a_k_stride[0] != 1 || st.a_k_stride[1] != 2) continue;
+        st.gather_a = true;
+        st.perm = false;
+        st.perm_axes.clear();
+        p.perm_bytes -= 2.0 * eb * std::ldexp(1.0, st.mlog + st.klog);
+        p.n_permutes--;
+      }
+    }
     if (shard.empty() && p.split_modes.empty() && L != p.open) {
       p.final_perm = true;
       for (int l : p.open) p.final_perm_axes.push_back((int)(std::find(L.begin(), L.end(), l) - L.begin()));
@@ -624,7 +651,7 @@ std::string report_json(const Plan& p, const std::vector<float>& ms) {
     const StemStep& s = p.steps[i];
     o << (i ? "," : "") << "{\"node\":" << s.node << ",\"branch\":" << s.branch << ",\"m\":" << s.mlog
       << ",\"k\":" << s.klog << ",\"n\":" << s.nlog << ",\"perm\":" << (s.perm ? 1 : 0)
-      << ",\"tc\":" << (s.tensor_core ? 1 : 0) << ",\"split\":" << s.split << ",\"swap\":" << (s.swap ? 1 : 0)
+      << ",\"tc\":" << (s.tensor_core ? 1 : 0) << ",\"ga\":" << (s.gather_a ? 1 : 0) << ",\"split\":" << s.split << ",\"swap\":" << (s.swap ? 1 : 0)
       << ",\"quant\":" << (s.quant ? 1 : 0)
       << ",\"in\":";
     jlist(o, s.in_layout);

@@ -45,6 +45,10 @@ struct StemStep {
   uint64_t b_off = 0;             // ws offset: B operand (fp16 B_P for chalf, c64 [K][N] for cfloat)
   uint64_t b_tmp_off = 0;         // ws offset: gathered complex64 [K][N] (chalf path)
   bool tensor_core = false;       // tcgen05 GEMM (else SIMT)
+  // permutation fused into the GEMM's A load: A[m, k] at sum bit_j(m) a_m_stride[j] +
+  // sum bit_j(k) a_k_stride[j] of the UNPERMUTED in_layout (perm == false then)
+  bool gather_a = false;
+  std::vector<int64_t> a_m_stride, a_k_stride;
   // output address of C[m, n] = sum_j bit_j(m) m_stride[j] + sum_j bit_j(n) n_stride[j] (elements)
   std::vector<int64_t> m_stride, n_stride;
   bool out_identity = true;       // out_layout == kept ++ newl (plain row-major [M][N])

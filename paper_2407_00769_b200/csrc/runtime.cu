@@ -342,10 +342,18 @@ void run_gemm(Plan& p, const StemStep& st, size_t i, const void* src, void* dst,
   for (int j = 0; j < mlog; ++j) om.ms[j] = st.m_stride[j];
   for (int j = 0; j < st.nlog; ++j) om.ns[j] = st.n_stride[j];
   if (p.cfg.dtype == TN_CHALF) {
+    AGather ag;
+    if (st.gather_a) {  // the step's permutation, fused into the A load (mshift == 0: not a split step)
+      memset(&ag, 0, sizeof(ag));
+      ag.mlog = st.mlog;
+      ag.klog = st.klog;
+      for (int j = 0; j < st.mlog; ++j) ag.ms[j] = st.a_m_stride[j];
+      for (int j = 0; j < st.klog; ++j) ag.ks[j] = st.a_k_stride[j];
+    }
     if (st.tensor_core)
       launch_gemm_chalf_tc(reinterpret_cast<__half*>(dst), reinterpret_cast<const __half*>(src),
                            reinterpret_cast<const __half*>(W + st.b_off), M, 2 * K, 2 * N, in_max, &sc.b_bound[i],
-                           out_max, exp_slot, &om, s);
+                           out_max, exp_slot, &om, s, st.gather_a ? &ag : nullptr);
     else
       launch_gemm_chalf_simt(reinterpret_cast<__half2*>(dst), reinterpret_cast<const __half2*>(src),
                              reinterpret_cast<const __half*>(W + st.b_off), M, K, N, in_max, &sc.b_bound[i], out_max,
@@ -933,6 +941,26 @@ int tn_gemm_chalf(void* d_c, const void* d_a, const void* d_bp, uint64_t M, uint
     else
       launch_gemm_chalf_simt((__half2*)d_c, (const __half2*)d_a, (const __half*)d_bp, M, K, N, im, bb, d_out_max,
                              d_exp, nullptr, (cudaStream_t)stream);
+  });
+}
+
+int tn_gemm_chalf_gather(void* d_c, const void* d_a, const void* d_bp, int mlog, int klog, uint32_t N,
+                         const int64_t* m_stride, const int64_t* k_stride, const float* d_in_max,
+                         const float* d_b_bound, uint32_t* d_out_max, int* d_exp, void* stream) {
+  if (!d_c || !d_a || !d_bp || !m_stride || !k_stride) return fail(TN_E_INVALID, "NULL argument");
+  if (mlog < 7 || mlog >= kMaxModes || klog < 3 || klog > 16 || !N || (N & (N - 1)))
+    return fail(TN_E_INVALID, "gathered GEMM: need mlog in [7, 48), klog in [3, 16], N a power of two");
+  TN_TRY({
+    AGather ag;
+    memset(&ag, 0, sizeof(ag));
+    ag.mlog = mlog;
+    ag.klog = klog;
+    for (int j = 0; j < mlog; ++j) ag.ms[j] = m_stride[j];
+    for (int j = 0; j < klog; ++j) ag.ks[j] = k_stride[j];
+    const float* im = (d_in_max && d_b_bound) ? d_in_max : nullptr;
+    const float* bb = (d_in_max && d_b_bound) ? d_b_bound : nullptr;
+    launch_gemm_chalf_tc((__half*)d_c, (const __half*)d_a, (const __half*)d_bp, 1ull << mlog, 2u << klog, 2 * N, im,
+                         bb, d_out_max, d_exp, nullptr, (cudaStream_t)stream, &ag);
   });
 }
 

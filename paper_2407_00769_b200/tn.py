@@ -28,7 +28,7 @@ class tn_config(C.Structure):
     _fields_ = [("dtype", C.c_int32), ("stem_min_log2", C.c_int32), ("comm_codec", C.c_int32),
                 ("comm_group", C.c_int32), ("stem_capacity_bytes", C.c_uint64), ("split_log2", C.c_int32),
                 ("layout_policy", C.c_int32), ("quant_from_pct", C.c_int32), ("virtual_world", C.c_int32),
-                ("reserved", C.c_int32 * 4)]
+                ("no_gather", C.c_int32), ("reserved", C.c_int32 * 3)]
 
 
 class tn_buffers(C.Structure):
@@ -69,6 +69,8 @@ def lib():
         L.tn_set_graph.argtypes = [vp, i32]
         L.tn_permute.argtypes = [vp, vp, i32, i32, C.POINTER(C.c_int), vp]
         L.tn_gemm_chalf.argtypes = [vp, vp, vp, u64, C.c_uint32, C.c_uint32, vp, vp, vp, vp, vp]
+        L.tn_gemm_chalf_gather.argtypes = [vp, vp, vp, i32, i32, C.c_uint32, C.POINTER(C.c_int64),
+                                           C.POINTER(C.c_int64), vp, vp, vp, vp, vp]
         L.tn_gemm_cfloat.argtypes = [vp, vp, vp, u64, C.c_uint32, C.c_uint32, vp]
         L.tn_pad_b.argtypes = [vp, vp, C.c_uint32, C.c_uint32, vp, vp, vp, vp]
         L.tn_quant_int8.argtypes = [vp, vp, vp, vp, u64, i32, vp]
@@ -112,8 +114,10 @@ def _stream(stream):
 
 
 def make_config(dtype=TN_CHALF, stem_min_log2=20, comm_codec=TN_COMM_INT8, comm_group=128,
-                stem_capacity_bytes=0, split_log2=0, layout_policy=0, virtual_world=1, quant_from_pct=-1):
+                stem_capacity_bytes=0, split_log2=0, layout_policy=0, virtual_world=1, quant_from_pct=-1,
+                no_gather=0):
     c = tn_config()
+    c.no_gather = no_gather
     c.layout_policy = layout_policy
     c.virtual_world = virtual_world  # host-only lowering for several ranks (no communicator)
     c.quant_from_pct = quant_from_pct
@@ -248,6 +252,14 @@ def tn_permute_bytes(dst, src, elem_bytes, perm, stream=None):
 def tn_gemm_chalf(c, a, bp, M, K, N, in_max=None, b_bound=None, out_max=None, exp=None, stream=None):
     _check(lib().tn_gemm_chalf(_ptr(c), _ptr(a), _ptr(bp), M, K, N, _ptr(in_max), _ptr(b_bound),
                                _ptr(out_max), _ptr(exp), _stream(stream)))
+
+
+def tn_gemm_chalf_gather(c, a, bp, mlog, klog, N, m_stride, k_stride, in_max=None, b_bound=None, out_max=None,
+                         exp=None, stream=None):
+    ms = (C.c_int64 * max(len(m_stride), 1))(*m_stride)
+    ks = (C.c_int64 * max(len(k_stride), 1))(*k_stride)
+    _check(lib().tn_gemm_chalf_gather(_ptr(c), _ptr(a), _ptr(bp), mlog, klog, N, ms, ks, _ptr(in_max),
+                                      _ptr(b_bound), _ptr(out_max), _ptr(exp), _stream(stream)))
 
 
 def tn_gemm_cfloat(c, a, b, M, K, N, stream=None):

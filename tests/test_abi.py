@@ -57,7 +57,10 @@ def test_plan_load_info_and_lowering_invariants(tnmod, c1_plan):
         assert len(R) == st["k"]
         out = st["out"]
         assert len(out) == st["m"] + st["n"]
-        if not st["perm"]:
+        if st["ga"]:
+            # permutation fused into the GEMM load: the two innermost stored modes are contracted
+            assert not st["perm"] and st["tc"] and set(lay[-2:]) <= set(R) and st["m"] >= 7
+        elif not st["perm"]:
             assert lay[len(lay) - len(R):] == R           # R innermost: GEMM reads A as stored
         assert (set(lay) - set(R)) <= set(out)              # Eq. 4: kept modes remain
         assert not (set(out) & set(R))                       # contracted modes are gone

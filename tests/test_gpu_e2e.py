@@ -150,3 +150,19 @@ def test_graph_replay_across_slices(tn, dtype):
     tn.tn_stem_contract(p, bufs, picks[-1])
     ms = p.report()["ms"]
     assert len(ms) == 2 + 2 * p.info()["n_stem_steps"] and all(m >= 0 for m in ms) and sum(ms) > 0
+
+
+@pytest.mark.parametrize("dtype", [0])
+def test_fused_permutation_matches_permute_pass(tn, dtype):
+    """Gathered-A GEMMs (permutation fused into the load) vs explicit permutation passes on the
+    same plan: same operands, same K order, same accumulation -> bit-identical amplitudes; and the
+    oracle within tolerance."""
+    sub = MP.sub_slice(_plan("c2"), 22)
+    out = {}
+    for ng in (0, 1):
+        p = tn.Plan(sub, tn.make_config(dtype=dtype, stem_min_log2=12, no_gather=ng))
+        rep = p.report()
+        out[ng] = (tn.contract(p, tn.Buffers(p), 0), sum(s["ga"] for s in rep["steps"]), p.info()["n_permutes"])
+    assert out[0][1] >= 1 and out[1][1] == 0 and out[0][2] < out[1][2]
+    assert np.array_equal(out[0][0], out[1][0])
+    assert metrics.rel_l2(out[0][0], contract.contract(load(sub), 0)) <= TOL[dtype]

@@ -245,3 +245,48 @@ def test_quant_int8_f16_payload_bit_exact(env):
     assert np.array_equal(sc.cpu().numpy(), rs) and np.array_equal(ze.cpu().numpy(), rz)
     assert np.array_equal(y.cpu().numpy(), codec.dequantize(rc, rs, rz, 1.0, group=g).astype(np.float16))
     assert np.linalg.norm(y.cpu().numpy().astype(np.float64) - x) <= 0.01 * np.linalg.norm(x.astype(np.float64))
+
+
+@pytest.mark.parametrize("mlog,klog,N,seed", [(7, 3, 8, 0), (9, 4, 16, 1), (10, 5, 64, 2), (8, 7, 32, 3),
+                                              (12, 6, 256, 4), (11, 8, 4, 5), (13, 5, 2, 6), (10, 9, 128, 7)])
+def test_gemm_chalf_gathered_a_exact(env, mlog, klog, N, seed):
+    """The stem permutation fused into the GEMM load: A[m, k] read at arbitrary per-bit strides of
+    the unpermuted stem (k bits 0, 1 fixed contiguous).  Integer operands in [-1, 1] keep every
+    product, sum and the fp16 result exact, so the gathered tcgen05 GEMM must equal (transpose,
+    then multiply) bit for bit."""
+    torch, tn = env
+    rng = np.random.default_rng(seed)
+    n = mlog + klog
+    pos = [int(x) for x in rng.permutation(np.arange(2, n))]
+    kpos = [0, 1] + pos[:klog - 2]
+    mpos = pos[klog - 2:]
+    ms = [1 << p for p in mpos]
+    ks = [1 << p for p in kpos]
+    x = rng.integers(-1, 2, 1 << n) + 1j * rng.integers(-1, 2, 1 << n)
+    mi = np.arange(1 << mlog)
+    ki = np.arange(1 << klog)
+    moff = sum(((mi >> j) & 1) * ms[j] for j in range(mlog))
+    koff = sum(((ki >> j) & 1) * ks[j] for j in range(klog))
+    a = x[moff[:, None] + koff[None, :]]                       # [M, K] = the permuted stem
+    K = 1 << klog
+    b = rng.integers(-1, 2, (K, N)) + 1j * rng.integers(-1, 2, (K, N))
+    bp = embed.pad_b(b)
+    rows = max(2 * N, 16)
+    bp_km = np.zeros((rows, 2 * K), np.float16)
+    bp_km[:2 * N] = np.transpose(bp, (2, 0, 1, 3)).reshape(2 * N, 2 * K)
+    X = torch.from_numpy(_half_pairs(x.reshape(1, -1)).reshape(-1)).cuda()
+    C = torch.full(((1 << mlog) * 2 * N,), float("nan"), dtype=torch.float16, device="cuda")
+    tn.tn_gemm_chalf_gather(C, X, torch.from_numpy(bp_km.reshape(-1)).cuda(), mlog, klog, N, ms, ks)
+    torch.cuda.synchronize()
+    got = C.cpu().numpy().astype(np.float64).reshape(1 << mlog, N, 2)
+    ref = a @ b
+    assert np.array_equal(got[..., 0], ref.real) and np.array_equal(got[..., 1], ref.imag)
+
+
+def test_gemm_chalf_gathered_rejects_bad_geometry(env):
+    torch, tn = env
+    t = torch.zeros(1 << 12, dtype=torch.float16, device="cuda")
+    with pytest.raises(tn.TnError):   # k bit 1 not contiguous
+        tn.tn_gemm_chalf_gather(t, t, t, 7, 3, 8, [1 << j for j in range(3, 10)], [1, 4, 2])
+    with pytest.raises(tn.TnError):   # M < 128
+        tn.tn_gemm_chalf_gather(t, t, t, 6, 3, 8, [1 << j for j in range(3, 9)], [1, 2, 4])
