@@ -72,6 +72,24 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 
+// N-dimensional TMA tile load (3..5 dims; coordinates innermost first)
+__device__ __forceinline__ void tma_load_nd(void* dst, const CUtensorMap* map, uint64_t* bar, int nd, const int* c) {
+  const uint32_t d = smem_u32(dst), b = smem_u32(bar);
+  const uint64_t m = reinterpret_cast<uint64_t>(map);
+  if (nd == 3)
+    asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+                 ::"r"(d), "l"(m), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(b) : "memory");
+  else if (nd == 4)
+    asm volatile("cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];"
+                 ::"r"(d), "l"(m), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(b) : "memory");
+  else if (nd == 5)
+    asm volatile("cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, %6}], [%7];"
+                 ::"r"(d), "l"(m), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(b) : "memory");
+  else
+    asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+                 ::"r"(d), "l"(m), "r"(c[0]), "r"(c[1]), "r"(b) : "memory");
+}
+
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
                    reinterpret_cast<uint64_t>(map)),
@@ -94,6 +112,18 @@ __device__ __forceinline__ uint64_t smem_desc_sw(const void* p) {
   d |= (uint64_t)((8 * kRow) >> 4) << 32;
   d |= (uint64_t)1 << 46;
   d |= kLayout << 61;
+  return d;
+}
+
+// K-major, no swizzle ("interleaved" core matrices of 8 rows x 16 B): rows 16 B apart, 8-row groups
+// SBO = 128 B apart, 16-byte K pieces LBO = 128 rows x 16 B = 2048 B apart (layout type 0)
+__device__ __forceinline__ uint64_t smem_desc_interleaved(const void* p) {
+  uint64_t addr = smem_u32(p);
+  uint64_t d = 0;
+  d |= (addr & 0x3FFFFull) >> 4;
+  d |= (uint64_t)(2048 >> 4) << 16;
+  d |= (uint64_t)(128 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
   return d;
 }
 
@@ -208,19 +238,31 @@ struct AGatherArgs {
   int64_t ks[24];
 };
 
+// Gathered A through one N-dimensional TMA box (the fused stem permutation when the source's bit
+// runs allow, <= 5 dims): dim d's coordinate = bits [j0, j0 + nb) of the tile's start row
+// (kind 0), of its start k index (kind 1), or 0 (kind 2: box-only dim).  nd == 0: plain 2-D A map.
+struct NdArgs {
+  int nd;
+  int8_t kind[5], j0[5], nb[5];
+};
+
 namespace tc {
 
 __device__ __forceinline__ void cp_async16(uint32_t smem_addr, const void* gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr), "l"(gmem) : "memory");
 }
 
-template <int BN, int KB, bool kGather>
-__global__ void __launch_bounds__(kGather ? kThreadsGather : kThreads, 1)
+// kAMode: 0 = A by TMA (2-D map, or N-d box when nda.nd > 0; swizzled rows), 1 = A gathered by
+// cp.async producer warps, 2 = A by N-d TMA box into the no-swizzle (interleaved) K-major layout
+template <int BN, int KB, int kAMode>
+__global__ void __launch_bounds__(kAMode == 1 ? kThreadsGather : kThreads, 1)
     gemm_chalf_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                          const __grid_constant__ CUtensorMap tmC, uint32_t num_m, uint32_t num_n, int K2,
                          const float* in_max, const float* b_bound, uint32_t* out_max, int* exp_slot,
                          const __grid_constant__ ScatterArgs sc_args, uint32_t* out_scatter, uint64_t rows,
-                         uint32_t n_cols, const __grid_constant__ AGatherArgs ga) {
+                         uint32_t n_cols, const __grid_constant__ AGatherArgs ga,
+                         const __grid_constant__ NdArgs nda) {
+  constexpr bool kGather = kAMode == 1;
   using C = Cfg<BN, KB>;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
@@ -295,7 +337,19 @@ __global__ void __launch_bounds__(kGather ? kThreadsGather : kThreads, 1)
             }
           } else {
             mbar_expect_tx(&full[s], b_resident ? C::kABytes : C::kStageBytes);
-            tma_load_2d(sA + s * C::kABytes, &tmA, &full[s], kb * KB, m0);
+            if (nda.nd > 0) {
+              const uint64_t mst = ga.m_base + (uint64_t)m0;
+              const uint64_t kst = (uint64_t)kb * (KB / 2);
+              int cc[5];
+#pragma unroll
+              for (int d = 0; d < 5; ++d) {
+                const uint64_t v = nda.kind[d] == 0 ? mst : (nda.kind[d] == 1 ? kst : 0);
+                cc[d] = (int)((v >> nda.j0[d]) & ((1ull << nda.nb[d]) - 1));
+              }
+              tma_load_nd(sA + s * C::kABytes, &tmA, &full[s], nda.nd, cc);
+            } else {
+              tma_load_2d(sA + s * C::kABytes, &tmA, &full[s], kb * KB, m0);
+            }
             if (!b_resident) tma_load_2d(sB + s * C::kBBytes, &tmB, &full[s], kb * KB, n0);
           }
           if (++s == C::kStages) {
@@ -321,11 +375,13 @@ __global__ void __launch_bounds__(kGather ? kThreadsGather : kThreads, 1)
           tc_fence_after();
           if (kGather && ga.fence) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // experiment knob
           const int nkk = (kb == num_k - 1) ? last_kk : KB / 16;
-          const uint64_t ad = smem_desc_sw<KB>(sA + s * C::kABytes);
+          const uint64_t ad = kAMode == 2 ? smem_desc_interleaved(sA + s * C::kABytes)
+                                           : smem_desc_sw<KB>(sA + s * C::kABytes);
           const uint64_t bd = smem_desc_sw<KB>(sB + s * C::kBBytes);
           for (int kk = 0; kk < nkk; ++kk) {
-            // advance 16 fp16 = 32 bytes along K inside the swizzle atom (>>4 => +2)
-            mma_f16(tmem_d, ad + 2 * kk, bd + 2 * kk, C::kIdesc, (kb | kk) != 0);
+            // advance 16 fp16 along K: 32 bytes inside a swizzle atom (>>4 => +2), or two
+            // 2048-byte core-matrix columns in the interleaved layout (>>4 => +256)
+            mma_f16(tmem_d, ad + (kAMode == 2 ? 256 : 2) * kk, bd + 2 * kk, C::kIdesc, (kb | kk) != 0);
           }
           mma_commit(&empty[s]);
           if (++s == C::kStages) {
@@ -610,10 +666,147 @@ static int num_sms() {
   return n;
 }
 
-template <int BN, int KB, bool G>
+// Gathered A as one N-dimensional TMA box (<= 5 dims).  Logical bits of a stage: complex k bits
+// and m (row) bits with source positions log2(stride).  w = number of k bits sitting at source bits
+// 0..w-1.  w >= 3: rows of 2^min(w,5) complex (32/64/128 B, swizzled like the 2-D path), box =
+// [row][m0..m6].  w == 2: no-swizzle core matrices, box = [k0 k1 m0..m6 | k2..k(1+cb)] so the smem
+// image is [k piece][row][16 B].  Each tensor dim is a maximal run of logical successors at
+// consecutive source bits (box bits first, <= 8 per dim); more than 5 dims -> not representable.
+struct NdPlan {
+  int interleaved = 0, KB = 0, nd = 0;
+  uint64_t dim[5], stride[5];
+  uint32_t box[5];
+  NdArgs args;
+};
+
+static bool build_nd(const AGather& ag, NdPlan& out) {
+  int pm[kMaxModes], pk[24];
+  auto lg = [](int64_t v) {
+    int r = 0;
+    while ((1ll << r) < v) ++r;
+    return ((1ll << r) == v) ? r : -1;
+  };
+  for (int j = 0; j < ag.mlog; ++j)
+    if ((pm[j] = lg(ag.ms[j])) < 0) return false;
+  for (int j = 0; j < ag.klog; ++j)
+    if ((pk[j] = lg(ag.ks[j])) < 0) return false;
+  if (ag.klog < 3 || pk[0] != 0 || pk[1] != 1 || ag.mlog < 7) return false;
+  int w = 0;
+  while (w < ag.klog && pk[w] == w) ++w;
+  const bool inter = w < 3;
+  const int W = inter ? 2 : std::min(w, 5);
+  const int cb = inter ? std::min(3, ag.klog - 2) : 0;
+  out.interleaved = inter ? 1 : 0;
+  out.KB = inter ? (8 << cb) : (2 << W);
+  auto src = [&](int kind, int j) { return kind == 0 ? pm[j] : pk[j]; };
+  auto inbox = [&](int kind, int j) { return kind == 0 ? j < 7 : (inter ? j < 2 + cb : j < W); };
+  auto succ = [&](int kind, int j, int& nk, int& nj) {
+    if (inter && kind == 1 && j == 1) {  // k1 -> m0 (the 16-byte piece, then the rows)
+      nk = 0;
+      nj = 0;
+      return true;
+    }
+    nk = kind;
+    nj = j + 1;
+    return nj < (kind == 0 ? ag.mlog : ag.klog);
+  };
+  std::vector<std::pair<int, int>> boxseq;
+  if (inter) {
+    boxseq = {{1, 0}, {1, 1}};
+    for (int j = 0; j < 7; ++j) boxseq.push_back({0, j});
+    for (int j = 2; j < 2 + cb; ++j) boxseq.push_back({1, j});
+  } else {
+    for (int j = 0; j < W; ++j) boxseq.push_back({1, j});
+    for (int j = 0; j < 7; ++j) boxseq.push_back({0, j});
+  }
+  std::vector<char> used_m(ag.mlog, 0), used_k(ag.klog, 0);
+  auto used = [&](int kind, int j) -> char& { return kind == 0 ? used_m[j] : used_k[j]; };
+  std::vector<std::vector<std::pair<int, int>>> dims;
+  auto grow = [&](int kind, int j) {
+    std::vector<std::pair<int, int>> d{{kind, j}};
+    used(kind, j) = 1;
+    int nb = inbox(kind, j) ? 1 : 0;
+    int ck = kind, cj = j, nk, nj;
+    while (succ(ck, cj, nk, nj) && !used(nk, nj) && src(nk, nj) == src(ck, cj) + 1) {
+      if (inbox(nk, nj)) {
+        if (nb == 8 || !inbox(ck, cj)) break;
+        ++nb;
+      }
+      d.push_back({nk, nj});
+      used(nk, nj) = 1;
+      ck = nk;
+      cj = nj;
+    }
+    dims.push_back(d);
+  };
+  for (auto& b : boxseq)
+    if (!used(b.first, b.second)) grow(b.first, b.second);
+  for (int j = 0; j < ag.mlog; ++j)
+    if (!used_m[j]) grow(0, j);
+  for (int j = 0; j < ag.klog; ++j)
+    if (!used_k[j]) grow(1, j);
+  if (dims.size() > 5) return false;
+  // box dims must tile the box sequence in order (each a contiguous segment)
+  size_t pos = 0;
+  for (auto& d : dims) {
+    for (auto& b : d) {
+      if (!inbox(b.first, b.second)) break;
+      if (pos >= boxseq.size() || boxseq[pos] != b) return false;
+      ++pos;
+    }
+  }
+  if (pos != boxseq.size()) return false;
+  out.nd = (int)dims.size();
+  memset(&out.args, 0, sizeof(out.args));
+  out.args.nd = out.nd;
+  for (int d = 0; d < out.nd; ++d) {
+    const auto& v = dims[d];
+    int nbox = 0;
+    bool mixed = false;
+    for (auto& b : v) {
+      nbox += inbox(b.first, b.second) ? 1 : 0;
+      mixed |= b.first != v[0].first;
+    }
+    if (v.size() > 32) return false;
+    out.dim[d] = 1ull << v.size();
+    out.stride[d] = 4ull << src(v[0].first, v[0].second);
+    out.box[d] = 1u << nbox;
+    if (mixed && nbox != (int)v.size()) return false;  // a mixed dim must lie inside the box
+    out.args.kind[d] = (int8_t)((nbox == (int)v.size()) ? 2 : v[0].first);
+    out.args.j0[d] = (int8_t)v[0].second;
+    out.args.nb[d] = (int8_t)v.size();
+  }
+  if (out.stride[0] != 4) return false;
+  for (int d = 1; d < out.nd; ++d)
+    if (out.stride[d] % 16) return false;
+  return true;
+}
+
+static CUtensorMap make_map_nd(const void* base, const NdPlan& np) {
+  CUtensorMap m;
+  cuuint64_t dims[5], strides[4];
+  cuuint32_t box[5], estr[5];
+  for (int d = 0; d < np.nd; ++d) {
+    dims[d] = np.dim[d];
+    box[d] = np.box[d];
+    estr[d] = 1;
+    if (d) strides[d - 1] = np.stride[d];
+  }
+  const int row_bytes = (int)np.box[0] * 4;
+  const CUtensorMapSwizzle sw = np.interleaved ? CU_TENSOR_MAP_SWIZZLE_NONE
+                                : (row_bytes >= 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                   : (row_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B));
+  CUresult r = get_encode()(&m, CU_TENSOR_MAP_DATA_TYPE_UINT32, np.nd, const_cast<void*>(base), dims, strides, box,
+                            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw TnError{TN_E_CUDA, "cuTensorMapEncodeTiled (N-d gather) failed (" + std::to_string((int)r) + ")"};
+  return m;
+}
+
+template <int BN, int KB, int G>
 static void launch_bn(__half* c, const __half* a, const __half* bp, uint64_t M, uint32_t K2, uint32_t N2_real,
                       const float* in_max, const float* b_bound, uint32_t* out_max, int* exp_slot, const OutMap* om,
-                      cudaStream_t s, const AGather* ag) {
+                      cudaStream_t s, const AGather* ag, const NdPlan* np) {
   const uint32_t N2 = std::max<uint32_t>(N2_real, 16);  // B_P has at least 16 (zero-padded) rows
   using C = tc::Cfg<BN, KB>;
   static bool attr = false;
@@ -624,7 +817,10 @@ static void launch_bn(__half* c, const __half* a, const __half* bp, uint64_t M, 
   }
   AGatherArgs gargs;
   memset(&gargs, 0, sizeof(gargs));
-  if (G) {
+  NdArgs nda;
+  memset(&nda, 0, sizeof(nda));
+  if (np) nda = np->args;
+  if (G == 1) {
     // vector bits of a stage: 7 row bits + log2(KB/8) chunk bits, by source stride (lanes take the
     // 5 smallest: the most contiguous reads)
     gargs.a = reinterpret_cast<const uint32_t*>(a);
@@ -695,8 +891,8 @@ static void launch_bn(__half* c, const __half* a, const __half* bp, uint64_t M, 
   const uint64_t chunk = std::min<uint64_t>(1ull << 30, ((1ull << 31) / num_n) * tc::BM);
   for (uint64_t m_off = 0; m_off < M; m_off += chunk) {
     uint64_t mm = std::min<uint64_t>(chunk, M - m_off);
-    // (gather: the A map is unused; any valid map will do)
-    CUtensorMap ma = make_map_2d(G ? a : a + m_off * K2, K2, G ? tc::BM : mm, KB, tc::BM);
+    // (cp.async gather: the A map is unused; N-d: the whole stem, coordinates from the global row)
+    CUtensorMap ma = np ? make_map_nd(a, *np) : make_map_2d(G ? a : a + m_off * K2, K2, G ? tc::BM : mm, KB, tc::BM);
     gargs.m_base = m_off;
     CUtensorMap mc = make_map_2d(c + m_off * N2, N2, mm, 64, tc::BM);
     uint32_t* out_sc = reinterpret_cast<uint32_t*>(c) + (sa.on ? outmap_m(*om, m_off) : 0);
@@ -704,23 +900,34 @@ static void launch_bn(__half* c, const __half* a, const __half* bp, uint64_t M, 
     uint64_t tiles = (uint64_t)num_m * num_n;
     int grid = (int)std::min<uint64_t>(tiles, (uint64_t)num_sms());
     // the exponent is recorded once (first chunk); later chunks reuse the same inputs
-    tc::gemm_chalf_tc_kernel<BN, KB, G><<<grid, G ? tc::kThreadsGather : tc::kThreads, C::kSmem, s>>>(
+    tc::gemm_chalf_tc_kernel<BN, KB, G><<<grid, G == 1 ? tc::kThreadsGather : tc::kThreads, C::kSmem, s>>>(
         ma, mb, mc, num_m, num_n, (int)K2, in_max, b_bound, out_max, m_off ? nullptr : exp_slot, sa, out_sc, mm,
-        n_cols, gargs);
+        n_cols, gargs, nda);
     TN_CUDA(cudaGetLastError());
   }
 }
 
-template <int KB, bool G>
+template <int KB, int G>
 static void launch_k(__half* c, const __half* a, const __half* bp, uint64_t M, uint32_t K2, uint32_t N2,
                      const float* in_max, const float* b_bound, uint32_t* out_max, int* exp_slot, const OutMap* om,
-                     cudaStream_t s, const AGather* ag) {
+                     cudaStream_t s, const AGather* ag, const NdPlan* np) {
   switch (N2 < 16 ? 16 : N2) {
-    case 16: launch_bn<16, KB, G>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, ag); break;
-    case 32: launch_bn<32, KB, G>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, ag); break;
-    case 64: launch_bn<64, KB, G>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, ag); break;
-    case 128: launch_bn<128, KB, G>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, ag); break;
-    default: launch_bn<256, KB, G>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, ag); break;
+    case 16: launch_bn<16, KB, G>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, ag, np); break;
+    case 32: launch_bn<32, KB, G>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, ag, np); break;
+    case 64: launch_bn<64, KB, G>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, ag, np); break;
+    case 128: launch_bn<128, KB, G>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, ag, np); break;
+    default: launch_bn<256, KB, G>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, ag, np); break;
+  }
+}
+
+template <int G>
+static void launch_kb(int KB, __half* c, const __half* a, const __half* bp, uint64_t M, uint32_t K2, uint32_t N2,
+                      const float* in_max, const float* b_bound, uint32_t* out_max, int* exp_slot, const OutMap* om,
+                      cudaStream_t s, const AGather* ag, const NdPlan* np) {
+  switch (KB) {
+    case 64: launch_k<64, G>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, ag, np); break;
+    case 32: launch_k<32, G>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, ag, np); break;
+    default: launch_k<16, G>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, ag, np); break;
   }
 }
 
@@ -730,24 +937,27 @@ void launch_gemm_chalf_tc(__half* c, const __half* a, const __half* bp, uint64_t
   if (K2 < 8 || N2 < 2 || (K2 & (K2 - 1)) || (N2 & (N2 - 1)))
     throw TnError{TN_E_INVALID, "tcgen05 GEMM needs power-of-two 2K >= 8, 2N >= 2"};
   if (M == 0) return;
+  const int kb_plain = K2 >= 64 ? 64 : (K2 >= 32 ? 32 : 16);
   if (ag) {
     // the gathered load needs whole 128-row tiles, 16-byte pieces (k bits 0, 1 contiguous) and
     // K-boxes of at least 16 fp16
     if (M % tc::BM || K2 < 16 || ag->ks[0] != 1 || ag->ks[1] != 2 || (uint64_t)1 << ag->mlog != M ||
         (2u << ag->klog) != K2)
       throw TnError{TN_E_INVALID, "gathered-A GEMM: unsupported operand geometry"};
-    switch (K2 >= 64 ? 64 : (K2 >= 32 ? 32 : 16)) {
-      case 64: launch_k<64, true>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, ag); break;
-      case 32: launch_k<32, true>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, ag); break;
-      default: launch_k<16, true>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, ag); break;
+    static const bool force_cpasync = getenv("TN_GATHER_CPASYNC") != nullptr;  // A/B knob
+    NdPlan np;
+    if (!force_cpasync && build_nd(*ag, np)) {
+      // one N-d TMA box per stage (M is never chunked: coordinates are per dim)
+      if (np.interleaved)
+        launch_kb<2>(np.KB, c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, ag, &np);
+      else
+        launch_kb<0>(np.KB, c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, ag, &np);
+      return;
     }
+    launch_kb<1>(kb_plain, c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, ag, nullptr);
     return;
   }
-  switch (K2 >= 64 ? 64 : (K2 >= 32 ? 32 : 16)) {
-    case 64: launch_k<64, false>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, nullptr); break;
-    case 32: launch_k<32, false>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, nullptr); break;
-    default: launch_k<16, false>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, nullptr); break;
-  }
+  launch_kb<0>(kb_plain, c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, nullptr, nullptr);
 }
 
 }  // namespace tn

@@ -389,7 +389,17 @@ Plan* load_plan(const char* json, size_t len, const tn_config* cfg_in, int world
         if (pre != split_set) suffix = false;
       }
       if (!suffix) {
-        by_next_use(kept);
+        // a permutation the GEMM's A load will absorb (gathered-A tcgen05 step, see the fused-
+        // permutation pass below) keeps the kept modes in stored order: the m bits then form long
+        // source runs, so the gather is a few-dimensional TMA box with 1 KB rows
+        const int kl = (int)R.size(), nl = (int)(B.size() - R.size());
+        const bool rows_k = kl <= 4 && nl <= 5 && kl + nl <= 7;
+        const bool tc_k = cfg.dtype == TN_CHALF && kl >= 2 && !rows_k &&
+                          ((kl >= 3 && nl >= 3) || kl >= 4 || kl + nl > 11);
+        const bool fusable = !cfg.no_gather && tc_k && kl >= 3 && kept.size() >= 7 && L.size() >= 2 &&
+                             bs.count(L[L.size() - 1]) && bs.count(L[L.size() - 2]) &&
+                             (split_set.empty() || (int)s < p.split_from);
+        if (!fusable) by_next_use(kept);
         std::vector<int> PL = kept;
         PL.insert(PL.end(), R.begin(), R.end());
         st.perm = true;
