@@ -1,0 +1,907 @@
+// Shared implementation of the tcgen05 complex-half GEMM (included by k_gemm_tc*.cu; each
+// k_gemm_tc_m<G>.cu instantiates one A-operand mode so the variants compile in parallel).
+#pragma once
+// Complex-half stem GEMM on the 5th-generation tensor cores.
+//
+// Eq. 6: C[m,(n,c)] = sum_{(k,a)} A_real[m,(k,a)] * B_P[(k,a),(n,c)], i.e. the
+// complex contraction of the stem A (interleaved fp16 re/im, read AS STORED — P:502 "include an
+// extra mode for tensor B, as it is smaller than tensor A") with the padded B_P
+// [[Re b,-Im b],[Im b, Re b]] is ONE real fp16 GEMM [M,2K] x [2K,2N] -> [M,2N] whose output is
+// again interleaved complex.  fp32 accumulation in TMEM (reading C-A7), one round-to-nearest to
+// fp16 in the epilogue with an exact power-of-two scale (reading C-A8).
+//
+// sm_100a design: persistent warp-specialised kernel, one CTA per SM (grid = min(tiles, #SMs)).
+//   warp 0   : TMA producer — A tile [128 x 64] and B tile [BN x 64] per stage, 128B swizzle,
+//              mbarrier full/empty ring of STAGES
+//   warp 1   : MMA issuer — one elected thread issues tcgen05.mma.cta_group::1.kind::f16
+//              (M=128, N=BN, K=16), accumulators in TMEM (512 columns: 2 x 256 ... 16 x 32),
+//              tcgen05.commit -> mbarriers
+//   warp 2   : TMEM allocator
+//   warps 4-11: epilogue, two warpgroups; group g drains every other tile —
+//              tcgen05.ld 32x32b -> scale -> fp16 -> 128B-swizzled smem ring -> TMA store; running
+//              max |C| for the next step's scale.  Two groups keep two warps per SM sub-partition
+//              converting, which output-heavy shapes (small K, large N) need to reach HBM write speed
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <mutex>
+
+#include "common.cuh"
+
+namespace tn {
+
+namespace tc {
+
+constexpr int BM = 128;
+constexpr int kThreads = 384;        // 4 role warps + 2 epilogue warpgroups
+constexpr int kThreadsGather = 512;  // + 4 warps gathering A (fused permutation)
+constexpr int kGatherWarps = 4;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// N-dimensional TMA tile load (3..5 dims; coordinates innermost first)
+__device__ __forceinline__ void tma_load_nd(void* dst, const CUtensorMap* map, uint64_t* bar, int nd, const int* c) {
+  const uint32_t d = smem_u32(dst), b = smem_u32(bar);
+  const uint64_t m = reinterpret_cast<uint64_t>(map);
+  if (nd == 3)
+    asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+                 ::"r"(d), "l"(m), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(b) : "memory");
+  else if (nd == 4)
+    asm volatile("cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];"
+                 ::"r"(d), "l"(m), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(b) : "memory");
+  else if (nd == 5)
+    asm volatile("cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, %6}], [%7];"
+                 ::"r"(d), "l"(m), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(b) : "memory");
+  else
+    asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+                 ::"r"(d), "l"(m), "r"(c[0]), "r"(c[1]), "r"(b) : "memory");
+}
+
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1), "r"(smem_u32(src))
+               : "memory");
+}
+
+// SM100 UMMA shared-memory matrix descriptor, K-major, rows of KB fp16 = 2*KB bytes swizzled at that
+// width: start>>4 [0,14) | LBO>>4 [16,30) (unused for swizzled K-major) | SBO>>4 [32,46) = 8 rows
+// between 8-row groups | version 1 [46,48) | base offset 0 | layout [61,64): SWIZZLE_128B = 2,
+// SWIZZLE_64B = 4, SWIZZLE_32B = 6.
+template <int KB>
+__device__ __forceinline__ uint64_t smem_desc_sw(const void* p) {
+  constexpr uint64_t kRow = 2 * KB;
+  constexpr uint64_t kLayout = KB == 64 ? 2 : (KB == 32 ? 4 : 6);
+  uint64_t addr = smem_u32(p);
+  uint64_t d = 0;
+  d |= (addr & 0x3FFFFull) >> 4;
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)((8 * kRow) >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= kLayout << 61;
+  return d;
+}
+
+// K-major, no swizzle ("interleaved" core matrices of 8 rows x 16 B): rows 16 B apart, 8-row groups
+// SBO = 128 B apart, 16-byte K pieces LBO = 128 rows x 16 B = 2048 B apart (layout type 0)
+__device__ __forceinline__ uint64_t smem_desc_interleaved(const void* p) {
+  uint64_t addr = smem_u32(p);
+  uint64_t d = 0;
+  d |= (addr & 0x3FFFFull) >> 4;
+  d |= (uint64_t)(2048 >> 4) << 16;
+  d |= (uint64_t)(128 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  return d;
+}
+
+__device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                        uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld_32x32b_x32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+
+__device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void named_bar(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+// KB: fp16 elements of K per stage (the TMA box and swizzle width): 64, or 2K when 2K < 64 so that
+// small-K steps neither stage nor zero-fill 3/4 empty boxes and keep more tiles in flight.
+template <int BN, int KB, int RAW = 0>
+struct Cfg {
+  static constexpr int kABytes = BM * KB * 2;
+  static constexpr int kBBytes = BN * KB * 2;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kCSub = (BN + 63) / 64;            // 64-column store subtiles
+  // staging ring (64-column subtiles) per epilogue group: 4 deep (more TMA stores in flight) when
+  // that still leaves >= 4 pipeline stages, else 2
+  static constexpr int kNBuf = ((220 * 1024 - 2 * 4 * BM * 128) / kStageBytes >= 4) ? 4 : 2;
+  static constexpr int kCTma = 2 * kNBuf * BM * 128;      // 128B-swizzled staging for TMA stores, 2 groups
+  static constexpr int kCBytes = kCTma;
+  static constexpr int kRawBytes = RAW * kABytes;  // raw TMA landing slots (A mode 3)
+  static constexpr int kStagesRaw = (220 * 1024 - kCBytes - kRawBytes) / kStageBytes;
+  static constexpr int kStages = kStagesRaw > 24 ? 24 : kStagesRaw;
+  static constexpr int kSmem =
+      kStages * kStageBytes + kCBytes + kRawBytes + 1024 /*align*/ + 2048 /*barriers, gather table*/;
+  // TMEM accumulators: as many as fit in 512 columns (<= 16), so the MMA runs ahead of the
+  // epilogue by several tiles when a tile is small (small K, small N)
+  static constexpr int kAccStride = BN < 32 ? 32 : BN;
+  static constexpr int kNAcc = (512 / kAccStride) > 16 ? 16 : (512 / kAccStride);
+  static constexpr uint32_t kIdesc = (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+};
+
+}  // namespace tc
+
+// Scatter epilogue description (output layout = any bit placement of m and n, see OutMap):
+// C[m, n] goes to sum_j bit_j(m) ms[j] + sum_j bit_j(n) ns[j] (complex elements).  Each epilogue
+// thread owns one row of the tile and stores its values straight from registers in contiguous
+// vectors along the lowest n bits whose strides are 1, 2, 4, ... (no shared-memory staging).
+// Tile rasterisation for scatter layouts: tile index bit b sets bit vbit_idx[b] of the m-block
+// (vbit_is_m[b] = 1) or of the n-block; bits are ordered by output stride so tiles that fill the
+// same output lines run concurrently on neighbouring CTAs and their partial sectors merge in L2.
+struct ScatterArgs {
+  int on;
+  int mbits, nbits;
+  int nv;
+  int8_t vbit_is_m[64];
+  int8_t vbit_idx[64];
+  int64_t ms[kMaxModes];
+  int64_t ns[24];
+};
+
+__device__ __forceinline__ void tile_coords(const ScatterArgs& sa, uint32_t t, uint32_t num_n, int BMv, int BNv,
+                                            int& m0, int& n0) {
+  if (sa.on) {
+    uint32_t mb = 0, nb = 0;
+    for (int b = 0; b < sa.nv; ++b)
+      if ((t >> b) & 1) {
+        if (sa.vbit_is_m[b])
+          mb |= 1u << sa.vbit_idx[b];
+        else
+          nb |= 1u << sa.vbit_idx[b];
+      }
+    m0 = (int)(mb * BMv);
+    n0 = (int)(nb * BNv);
+  } else {
+    m0 = (int)((t / num_n) * BMv);
+    n0 = (int)((t % num_n) * BNv);
+  }
+}
+
+// Gathered A operand (the stem permutation fused into the GEMM load): A[m, k] (complex-half) sits at
+// a + sum_j bit_j(m) ms[j] + sum_j bit_j(k) ks[j] (complex elements) with ks[0] = 1, ks[1] = 2, so
+// every 16-byte piece of a K-major smem row is 4 contiguous complex values.  A stage (128 rows x
+// KB fp16) is nvb = 7 + log2(KB/8) "vector bits" (row bits and 16-byte chunk bits); they are sorted
+// by source stride on the host so the 32 lanes of a warp read the lowest-stride (most contiguous)
+// combinations.
+struct AGatherArgs {
+  const uint32_t* a;
+  uint64_t m_base;  // row offset of this launch chunk
+  int mlog, klog, nvb;
+  int fence;           // consumer-side proxy fence (TN_GATHER_FENCE; off: CUTLASS's cp.async->UMMA pipelines use none)
+  int8_t vb_is_k[16];  // vector bit b: 16-byte chunk bit (k bit 2 + idx) or row bit (m bit idx)
+  int8_t vb_idx[16];
+  int64_t ms[kMaxModes];
+  int64_t ks[24];
+};
+
+// Gathered A through one N-dimensional TMA box (the fused stem permutation when the source's bit
+// runs allow, <= 5 dims): dim d's coordinate = bits [j0, j0 + nb) of the tile's start row
+// (kind 0), of its start k index (kind 1), or 0 (kind 2: box-only dim).  nd == 0: plain 2-D A map.
+struct NdArgs {
+  int nd;
+  // dim d's coordinate = ((row >> mj0) & mmask) << msh | ((k >> kj0) & kmask) << ksh  (row, k =
+  // the tile's start row and start k index; a zero mask drops that part)
+  int8_t mj0[5], msh[5], kj0[5], ksh[5];
+  uint32_t mmask[5], kmask[5];
+  // mode 3 (raw box + reshuffle): byte offset in the interleaved stage of each 16-byte piece bit
+  int npb;
+  uint32_t piece_dst[12];
+};
+
+namespace tc {
+
+__device__ __forceinline__ void cp_async16(uint32_t smem_addr, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr), "l"(gmem) : "memory");
+}
+
+// Row / k parts of the N-d box coordinates: the TMA thread evaluates the row part once per tile
+// and the k part once per stage (a handful of shifts, so the single issuing thread keeps up).
+__device__ __forceinline__ void nd_coords_rows(const NdArgs& nda, uint64_t row, int (&cm)[5]) {
+#pragma unroll
+  for (int d = 0; d < 5; ++d) cm[d] = (int)(((uint32_t)(row >> nda.mj0[d]) & nda.mmask[d]) << nda.msh[d]);
+}
+__device__ __forceinline__ void nd_coords_k(const NdArgs& nda, uint32_t k, const int (&cm)[5], int (&cc)[5]) {
+#pragma unroll
+  for (int d = 0; d < 5; ++d) cc[d] = cm[d] | (int)(((k >> nda.kj0[d]) & nda.kmask[d]) << nda.ksh[d]);
+}
+
+// kAMode: 0 = A by TMA (2-D map, or N-d box when nda.nd > 0; swizzled rows), 1 = A gathered by
+// cp.async producer warps, 2 = A by N-d TMA box into the no-swizzle (interleaved) K-major layout,
+// 3 = A by an N-d TMA box in source order into a raw slot, reshuffled by warp 3 (16-byte pieces)
+// into the interleaved layout
+template <int BN, int KB, int kAMode>
+__global__ void __launch_bounds__(kAMode == 1 ? kThreadsGather : kThreads, 1)
+    gemm_chalf_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                         const __grid_constant__ CUtensorMap tmC, uint32_t num_m, uint32_t num_n, int K2,
+                         const float* in_max, const float* b_bound, uint32_t* out_max, int* exp_slot,
+                         const __grid_constant__ ScatterArgs sc_args, uint32_t* out_scatter, uint64_t rows,
+                         uint32_t n_cols, const __grid_constant__ AGatherArgs ga,
+                         const __grid_constant__ NdArgs nda) {
+  constexpr bool kGather = kAMode == 1;
+  constexpr bool kInter = kAMode == 2 || kAMode == 3;
+  using C = Cfg<BN, KB, kAMode == 3 ? 2 : 0>;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  unsigned char* sA = smem;
+  unsigned char* sB = smem + C::kStages * C::kABytes;
+  unsigned char* sC = sB + C::kStages * C::kBBytes;
+  unsigned char* sRaw = sC + C::kCBytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sRaw + C::kRawBytes);
+  uint64_t* empty = full + C::kStages;
+  uint64_t* tfull = empty + C::kStages;
+  uint64_t* tempty = tfull + C::kNAcc;
+  uint64_t* raw_full = tempty + C::kNAcc;
+  uint64_t* raw_empty = raw_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(raw_empty + 2);
+  struct GTab {
+    int64_t off;
+    int rc;
+    int pad;
+  };
+  GTab* gtab = reinterpret_cast<GTab*>(reinterpret_cast<unsigned char*>(full) + 1024);  // gather table
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t num_tiles = num_m * num_n;
+  const int num_k = (K2 + KB - 1) / KB;
+  const int last_kk = ((K2 - (num_k - 1) * KB) + 15) / 16;  // MMAs in the last k block
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < C::kStages; ++s) {
+      // gather / reshuffle: the TMA (B) arrive + the A producer warp's arrive
+      mbar_init(&full[s], (kGather || kAMode == 3) ? 2 : 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int r = 0; r < 2; ++r) {
+      mbar_init(&raw_full[r], 1);
+      mbar_init(&raw_empty[r], 1);
+    }
+    for (int a = 0; a < C::kNAcc; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmC)) : "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ===== TMA producer =====
+      int s = 0;
+      uint32_t ph = 0;
+      const uint32_t reuse_dist = (uint32_t)C::kStages * gridDim.x;  // tile that last filled this slot
+      uint32_t qa = 0;  // stage counter (raw A slots)
+      for (uint32_t t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        int m0, n0;
+        tile_coords(sc_args, t, num_n, BM, BN, m0, n0);
+        int cm[5] = {0, 0, 0, 0, 0};  // row part of the N-d box coordinates (once per tile)
+        if (nda.nd > 0) nd_coords_rows(nda, ga.m_base + (uint64_t)m0, cm);
+        // single k-block: the slot still holds B of the tile kStages iterations ago; skip the B
+        // load when that tile had the same n-block (always when N fits one tile)
+        bool b_resident = false;
+        if (num_k == 1 && t >= blockIdx.x + reuse_dist) {
+          int pm, pn;
+          tile_coords(sc_args, t - reuse_dist, num_n, BM, BN, pm, pn);
+          b_resident = pn == n0;
+        }
+        for (int kb = 0; kb < num_k; ++kb, ++qa) {
+          if (kAMode == 3) {
+            // A: the raw box (source order) into raw slot qa & 1, for warp 3 to reshuffle
+            const int r = (int)(qa & 1);
+            mbar_wait(&raw_empty[r], ((qa >> 1) & 1) ^ 1);
+            mbar_expect_tx(&raw_full[r], C::kABytes);
+            int cc[5];
+            nd_coords_k(nda, (uint32_t)kb * (KB / 2), cm, cc);
+            tma_load_nd(sRaw + r * C::kABytes, &tmA, &raw_full[r], nda.nd, cc);
+          }
+          mbar_wait(&empty[s], ph ^ 1);
+          if (kGather || kAMode == 3) {  // A comes from the gather / reshuffle warps
+            if (b_resident) {
+              mbar_arrive(&full[s]);
+            } else {
+              mbar_expect_tx(&full[s], C::kBBytes);
+              tma_load_2d(sB + s * C::kBBytes, &tmB, &full[s], kb * KB, n0);
+            }
+          } else {
+            mbar_expect_tx(&full[s], b_resident ? C::kABytes : C::kStageBytes);
+            if (nda.nd > 0) {
+              int cc[5];
+              nd_coords_k(nda, (uint32_t)kb * (KB / 2), cm, cc);
+              tma_load_nd(sA + s * C::kABytes, &tmA, &full[s], nda.nd, cc);
+            } else {
+              tma_load_2d(sA + s * C::kABytes, &tmA, &full[s], kb * KB, m0);
+            }
+            if (!b_resident) tma_load_2d(sB + s * C::kBBytes, &tmB, &full[s], kb * KB, n0);
+          }
+          if (++s == C::kStages) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ===== MMA issuer =====
+      int s = 0;
+      uint32_t ph = 0;
+      uint32_t i = 0;
+      for (uint32_t t = blockIdx.x; t < num_tiles; t += gridDim.x, ++i) {
+        const uint32_t acc = i % C::kNAcc, aph = (i / C::kNAcc) & 1;
+        mbar_wait(&tempty[acc], aph ^ 1);
+        tc_fence_after();
+        const uint32_t tmem_d = tmem_base + acc * C::kAccStride;
+        for (int kb = 0; kb < num_k; ++kb) {
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          if (kGather && ga.fence) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // experiment knob
+          const int nkk = (kb == num_k - 1) ? last_kk : KB / 16;
+          const uint64_t ad = kInter ? smem_desc_interleaved(sA + s * C::kABytes)
+                                     : smem_desc_sw<KB>(sA + s * C::kABytes);
+          const uint64_t bd = smem_desc_sw<KB>(sB + s * C::kBBytes);
+          for (int kk = 0; kk < nkk; ++kk) {
+            // advance 16 fp16 along K: 32 bytes inside a swizzle atom (>>4 => +2), or two
+            // 2048-byte core-matrix columns in the interleaved layout (>>4 => +256)
+            mma_f16(tmem_d, ad + (kInter ? 256 : 2) * kk, bd + 2 * kk, C::kIdesc, (kb | kk) != 0);
+          }
+          mma_commit(&empty[s]);
+          if (++s == C::kStages) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+        mma_commit(&tfull[acc]);
+      }
+    }
+  } else if (kAMode == 3 && warp == 3) {
+    // ===== A reshuffle: raw slot (source order) -> interleaved K-major stage, 16-byte pieces.
+    // piece p of the raw box goes to sum_b bit_b(p) piece_dst[b]; lanes take piece bits 0..4
+    uint32_t dst_lane = 0;
+    for (int b = 0; b < 5 && b < nda.npb; ++b)
+      if ((lane >> b) & 1) dst_lane += nda.piece_dst[b];
+    const int n_it = 1 << (nda.npb - 5);
+    uint32_t* itab = reinterpret_cast<uint32_t*>(gtab);
+    if (lane < n_it) {
+      uint32_t d = 0;
+      for (int b = 5; b < nda.npb; ++b)
+        if ((lane >> (b - 5)) & 1) d += nda.piece_dst[b];
+      itab[lane] = d;
+    }
+    __syncwarp();
+    uint32_t q = 0;
+    for (uint32_t t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      for (int kb = 0; kb < num_k; ++kb, ++q) {
+        const int r = (int)(q & 1);
+        const int s = (int)(q % C::kStages);
+        mbar_wait(&raw_full[r], (q >> 1) & 1);
+        mbar_wait(&empty[s], ((q / C::kStages) & 1) ^ 1);
+        const uint4* src = reinterpret_cast<const uint4*>(sRaw + r * C::kABytes);
+        unsigned char* dst = sA + s * C::kABytes + dst_lane;
+#pragma unroll 8
+        for (int it = 0; it < n_it; ++it) {
+          const uint4 v = src[it * 32 + lane];
+          *reinterpret_cast<uint4*>(dst + itab[it]) = v;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> UMMA reads
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&full[s]);
+          mbar_arrive(&raw_empty[r]);
+        }
+      }
+    }
+  } else if (kGather && warp >= 12) {
+    // ===== A gather (fused stem permutation): warp g fills the ring slots s = g mod 4 with
+    // cp.async 16-byte pieces at arbitrary source strides, up to 4 stages in flight per warp
+    // (commit groups); a stage is published by wait_group + proxy fence + mbarrier arrive
+    const int g = warp - 12;
+    constexpr int kCB = KB / 8;                 // 16-byte chunks per row
+    constexpr int kLogCB = kCB == 8 ? 3 : (kCB == 4 ? 2 : 1);
+    constexpr int kIters = BM * kCB / 32;       // pieces per lane per stage (32, 16 or 8)
+    // piece v = it * 32 + lane; vector bits 0..4 come from the lane, 5.. from it.  Offsets and
+    // (row, chunk) of both parts are tile-independent: lane part in registers, it part in a
+    // 32-entry smem table (one broadcast load per piece)
+    int64_t off_lane = 0;
+    int r_lane = 0, c_lane = 0;
+    int64_t off_it = 0;
+    int r_it = 0, c_it = 0;
+    for (int b = 0; b < ga.nvb; ++b) {
+      const bool on = b < 5 ? ((lane >> b) & 1) : ((lane >> (b - 5)) & 1);
+      if (!on) continue;
+      const int64_t st = ga.vb_is_k[b] ? ga.ks[2 + ga.vb_idx[b]] : ga.ms[ga.vb_idx[b]];
+      const int rb = ga.vb_is_k[b] ? 0 : (1 << ga.vb_idx[b]);
+      const int cb = ga.vb_is_k[b] ? (1 << ga.vb_idx[b]) : 0;
+      if (b < 5) {
+        off_lane += st;
+        r_lane |= rb;
+        c_lane |= cb;
+      } else {
+        off_it += st;
+        r_it |= rb;
+        c_it |= cb;
+      }
+    }
+    if (lane < kIters) {
+      gtab[lane].off = off_it;
+      gtab[lane].rc = (r_it << 8) | c_it;
+    }
+    __syncwarp();
+    const uint32_t sA_u32 = smem_u32(sA);
+    // this warp owns ring slots g, g+4, ...; it keeps up to `depth` of them in flight (cp.async
+    // groups), completing the oldest (wait_group + proxy fence + arrive) before reusing a slot
+    const int owned = C::kStages > g ? (C::kStages - 1 - g) / kGatherWarps + 1 : 0;
+    const int depth = owned < 4 ? owned : 4;
+    uint32_t pend = 0;  // ring of pending slots, 8 bits each, oldest in the low byte
+    int npend = 0;
+    auto complete_oldest = [&]() {
+      switch (npend - 1) {  // wait until only the npend-1 youngest groups are outstanding
+        case 0: asm volatile("cp.async.wait_group 0;" ::: "memory"); break;
+        case 1: asm volatile("cp.async.wait_group 1;" ::: "memory"); break;
+        case 2: asm volatile("cp.async.wait_group 2;" ::: "memory"); break;
+        default: asm volatile("cp.async.wait_group 3;" ::: "memory"); break;
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic (cp.async) -> async proxy (UMMA)
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&full[pend & 0xff]);
+      pend >>= 8;
+      --npend;
+    };
+    uint32_t q = 0;
+    int64_t mbase = 0;
+    for (uint32_t t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      int m0, n0;
+      tile_coords(sc_args, t, num_n, BM, BN, m0, n0);
+      bool have_m = false;
+      for (int kb = 0; kb < num_k; ++kb, ++q) {
+        // each ring slot always belongs to the same gather warp, so its phases are waited in order
+        const int s = (int)(q % C::kStages);
+        if (s % kGatherWarps != g) continue;
+        const uint32_t ph = (q / C::kStages) & 1;
+        if (!have_m) {  // m bits >= 7 of the tile's first row
+          mbase = 0;
+          const uint64_t mrow = ga.m_base + (uint64_t)m0;
+          for (int j = 7; j < ga.mlog; ++j)
+            if ((mrow >> j) & 1) mbase += ga.ms[j];
+          have_m = true;
+        }
+        int64_t base = mbase + off_lane;
+        const uint32_t kc = (uint32_t)kb * (KB / 2);  // complex k index of the box start
+        for (int j = 2 + kLogCB; j < ga.klog; ++j)
+          if ((kc >> j) & 1) base += ga.ks[j];
+        if (npend == depth) complete_oldest();
+        mbar_wait(&empty[s], ph ^ 1);
+        const uint32_t stage = sA_u32 + s * C::kABytes;
+        const uint32_t* src = ga.a + base;
+#pragma unroll
+        for (int it = 0; it < kIters; ++it) {
+          const GTab e = gtab[it];
+          const int r = r_lane | (e.rc >> 8), c = c_lane | (e.rc & 0xff);
+          // swizzled K-major row (SW128 / SW64 / SW32 as the TMA box would have written it)
+          const int sw = KB == 64 ? (r & 7) : (KB == 32 ? ((r >> 1) & 3) : ((r >> 2) & 1));
+          cp_async16(stage + r * (2 * KB) + ((c ^ sw) << 4), src + e.off);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        pend |= (uint32_t)s << (8 * npend);
+        ++npend;
+      }
+    }
+    while (npend > 0) complete_oldest();
+  } else if (warp >= 4) {
+    // ===== epilogue: two independent warpgroups, group g drains the tiles i = g mod 2
+    const int grp = (warp - 4) >> 2;
+    const int ew = warp & 3;  // TMEM lane quarter this warp may access
+    const int row = ew * 32 + lane;
+    const int etid = threadIdx.x - 128 - 128 * grp;
+    unsigned char* sCg = sC + grp * (C::kNBuf * BM * 128);
+    int e = 0;
+    if (in_max && b_bound) e = scale_exp_for(in_max[0] * b_bound[0]);
+    if (exp_slot && blockIdx.x == 0 && grp == 0 && etid == 0) *exp_slot = e;
+    const float sc = ldexpf(1.f, e);
+    float mx = 0.f;
+    const bool scat = sc_args.on != 0;
+    // scatter mode: run = number of lowest n bits whose output strides are 1, 2, 4, ...: each
+    // thread stores its row's values in contiguous vectors of 2^run complex (<= 16)
+    int run = 0;
+    if (scat)
+      while (run < 4 && run < sc_args.nbits && sc_args.ns[run] == ((int64_t)1 << run)) ++run;
+    uint32_t gsub = 0;  // staging subtiles used so far (ring position)
+    for (uint32_t t = blockIdx.x + grp * gridDim.x, i = grp; t < num_tiles; t += 2 * gridDim.x, i += 2) {
+      const uint32_t acc = i % C::kNAcc, aph = (i / C::kNAcc) & 1;
+      int m0, n0;
+      tile_coords(sc_args, t, num_n, BM, BN, m0, n0);
+      mbar_wait(&tfull[acc], aph);
+      tc_fence_after();
+      const uint32_t taddr = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * C::kAccStride;
+      int64_t row_off = 0;
+      const bool row_ok = (uint64_t)(m0 + row) < rows;
+      if (scat) {
+        const uint64_t mg = (uint64_t)(m0 + row);
+        for (int j = 0; j < sc_args.mbits; ++j)
+          if ((mg >> j) & 1) row_off += sc_args.ms[j];
+      }
+#pragma unroll 1
+      for (int sub = 0; sub < BN; sub += 64, ++gsub) {
+        unsigned char* sbuf = sCg + (gsub % C::kNBuf) * (BM * 128);
+        if (!scat) {
+          // ring slot free? (the TMA store that used it kNBuf subtiles ago has read it)
+          if (etid == 0) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(C::kNBuf - 1) : "memory");
+          named_bar(1 + grp, 128);
+        }
+        // both 32-column halves of the subtile in flight before one wait
+        uint32_t r[2][32];
+        tmem_ld_32x32b_x32(taddr + sub, r[0]);
+        if (sub + 32 < BN) tmem_ld_32x32b_x32(taddr + sub + 32, r[1]);
+        tmem_ld_wait();
+        if (sub + 64 >= BN) {
+          // accumulator drained -> MMA may reuse it (before the stores are issued)
+          tc_fence_before();
+          mbar_arrive(&tempty[acc]);
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int c = sub + 32 * h;
+          if (c >= BN) break;
+          uint32_t pk[16];
+          // complex values of this 32-column chunk that exist (N < 8 pads B_P with zero rows)
+          const int nleft = (int)n_cols - ((n0 + c) >> 1);
+          const int nvalid = nleft < 16 ? (nleft > 0 ? nleft : 0) : 16;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            float x0 = __uint_as_float(r[h][2 * j]) * sc, x1 = __uint_as_float(r[h][2 * j + 1]) * sc;
+            __half2 hv = __floats2half2_rn(x0, x1);
+            float2 hf = __half22float2(hv);
+            if (j < nvalid) mx = fmaxf(mx, fmaxf(fabsf(hf.x), fabsf(hf.y)));
+            pk[j] = *reinterpret_cast<uint32_t*>(&hv);
+          }
+          if (scat) {
+            if (row_ok) {
+              const uint64_t nb = (uint64_t)((n0 + c) >> 1);
+              const int V = 1 << run;
+              // q and v are compile-time (full unroll) so pk stays in registers
+#pragma unroll
+              for (int q = 0; q < 16; ++q) {
+                if ((q & (V - 1)) || q >= nvalid) continue;
+                int64_t off = row_off;
+                const uint64_t ng = nb + q;
+                for (int j = run; j < sc_args.nbits; ++j)
+                  if ((ng >> j) & 1) off += sc_args.ns[j];
+                uint32_t* dst = out_scatter + off;
+                if (V >= 8) {
+                  // 256-bit stores (STG.256): one full 32-byte sector per instruction and thread
+#pragma unroll
+                  for (int v = 0; v < 16; v += 8)
+                    if (v < V && q + v + 7 < 16)
+                      asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(dst + v), "r"(pk[q + v]),
+                                   "r"(pk[q + v + 1]), "r"(pk[q + v + 2]), "r"(pk[q + v + 3]), "r"(pk[q + v + 4]),
+                                   "r"(pk[q + v + 5]), "r"(pk[q + v + 6]), "r"(pk[q + v + 7])
+                                   : "memory");
+                } else if (V == 4) {
+                  if (q + 3 < 16) *reinterpret_cast<uint4*>(dst) = make_uint4(pk[q], pk[q + 1], pk[q + 2], pk[q + 3]);
+                } else if (V == 2) {
+                  if (q + 1 < 16) *reinterpret_cast<uint2*>(dst) = make_uint2(pk[q], pk[q + 1]);
+                } else {
+                  *dst = pk[q];
+                }
+              }
+            }
+          } else {
+            unsigned char* srow = sbuf + row * 128;
+            const int cb = (c & 63) >> 3;  // first 16-byte chunk of these 32 columns
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              if ((c & 63) + q * 8 < BN || BN >= 64) {
+                const int chunk = (cb + q) ^ (row & 7);
+                uint4 v = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+                *reinterpret_cast<uint4*>(srow + chunk * 16) = v;
+              }
+            }
+          }
+        }
+        if (!scat) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          named_bar(1 + grp, 128);
+          if (etid == 0) {
+            tma_store_2d(&tmC, sbuf, n0 + sub, m0);
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          }
+        }
+      }
+    }
+    if (etid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (out_max && lane == 0) atomicMax(out_max, __float_as_uint(mx));
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
+  }
+}
+
+}  // namespace tc
+
+// ---- host side ----
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  if (!fn) throw TnError{TN_E_CUDA, "cuTensorMapEncodeTiled unavailable"};
+  return fn;
+}
+
+static CUtensorMap make_map_2d(const void* base, uint64_t inner, uint64_t outer, uint32_t box_inner,
+                               uint32_t box_outer) {
+  // swizzle width = the box row (64 fp16 = 128 B, 32 = 64 B, 16 = 32 B), matching smem_desc_sw
+  const CUtensorMapSwizzle sw = box_inner >= 64 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                : (box_inner == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B);
+  CUtensorMap m;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {inner * 2};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = get_encode()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw TnError{TN_E_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")"};
+  return m;
+}
+
+static int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    TN_CUDA(cudaGetDevice(&dev));
+    TN_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+  }
+  return n;
+}
+
+// Gathered A as one N-dimensional TMA box (<= 5 dims).  Logical bits of a stage: complex k bits
+// and m (row) bits with source positions log2(stride).  w = number of k bits sitting at source bits
+// 0..w-1.  w >= 3: rows of 2^min(w,5) complex (32/64/128 B, swizzled like the 2-D path), box =
+// [row][m0..m6].  w == 2: no-swizzle core matrices, box = [k0 k1 m0..m6 | k2..k(1+cb)] so the smem
+// image is [k piece][row][16 B].  Each tensor dim is a maximal run of logical successors at
+// consecutive source bits (box bits first, <= 8 per dim); more than 5 dims -> not representable.
+struct NdPlan {
+  int interleaved = 0, KB = 0, nd = 0;
+  uint64_t dim[5], stride[5];
+  uint32_t box[5];
+  NdArgs args;
+};
+
+static CUtensorMap make_map_nd(const void* base, const NdPlan& np) {
+  CUtensorMap m;
+  cuuint64_t dims[5], strides[4];
+  cuuint32_t box[5], estr[5];
+  for (int d = 0; d < np.nd; ++d) {
+    dims[d] = np.dim[d];
+    box[d] = np.box[d];
+    estr[d] = 1;
+    if (d) strides[d - 1] = np.stride[d];
+  }
+  const int row_bytes = (int)np.box[0] * 4;
+  const CUtensorMapSwizzle sw = np.interleaved ? CU_TENSOR_MAP_SWIZZLE_NONE
+                                : (row_bytes >= 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                   : (row_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B));
+  CUresult r = get_encode()(&m, CU_TENSOR_MAP_DATA_TYPE_UINT32, np.nd, const_cast<void*>(base), dims, strides, box,
+                            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw TnError{TN_E_CUDA, "cuTensorMapEncodeTiled (N-d gather) failed (" + std::to_string((int)r) + ")"};
+  return m;
+}
+
+template <int BN, int KB, int G>
+static void launch_bn(__half* c, const __half* a, const __half* bp, uint64_t M, uint32_t K2, uint32_t N2_real,
+                      const float* in_max, const float* b_bound, uint32_t* out_max, int* exp_slot, const OutMap* om,
+                      cudaStream_t s, const AGather* ag, const NdPlan* np) {
+  const uint32_t N2 = std::max<uint32_t>(N2_real, 16);  // B_P has at least 16 (zero-padded) rows
+  using C = tc::Cfg<BN, KB, G == 3 ? 2 : 0>;
+  static bool attr = false;
+  if (!attr) {
+    TN_CUDA(cudaFuncSetAttribute(tc::gemm_chalf_tc_kernel<BN, KB, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 C::kSmem));
+    attr = true;
+  }
+  AGatherArgs gargs;
+  memset(&gargs, 0, sizeof(gargs));
+  NdArgs nda;
+  memset(&nda, 0, sizeof(nda));
+  if (np) nda = np->args;
+  if (G == 1) {
+    // vector bits of a stage: 7 row bits + log2(KB/8) chunk bits, by source stride (lanes take the
+    // 5 smallest: the most contiguous reads)
+    gargs.a = reinterpret_cast<const uint32_t*>(a);
+    static const bool fence_env = getenv("TN_GATHER_FENCE") != nullptr;
+    gargs.fence = fence_env ? 1 : 0;
+    gargs.mlog = ag->mlog;
+    gargs.klog = ag->klog;
+    for (int j = 0; j < kMaxModes; ++j) gargs.ms[j] = ag->ms[j];
+    for (int j = 0; j < 24; ++j) gargs.ks[j] = ag->ks[j];
+    struct VB {
+      int64_t stride;
+      int is_k, idx;
+    };
+    std::vector<VB> vb;
+    for (int j = 0; j < 7; ++j) vb.push_back({ag->ms[j], 0, j});
+    const int cb = KB == 64 ? 3 : (KB == 32 ? 2 : 1);
+    for (int j = 0; j < cb; ++j) vb.push_back({ag->ks[2 + j], 1, j});
+    std::stable_sort(vb.begin(), vb.end(), [](const VB& x, const VB& y) { return x.stride < y.stride; });
+    gargs.nvb = (int)vb.size();
+    for (int b = 0; b < gargs.nvb; ++b) {
+      gargs.vb_is_k[b] = (int8_t)vb[b].is_k;
+      gargs.vb_idx[b] = (int8_t)vb[b].idx;
+    }
+  }
+  ScatterArgs sa;
+  memset(&sa, 0, sizeof(sa));
+  const uint32_t n_cols = N2_real / 2;
+  OutMap ident;
+  static const bool direct_env = getenv("TN_DIRECT_EPI") != nullptr;  // experiment knob
+  if ((N2_real < 16 || direct_env) && (!om || om->identity)) {  // TMA stores need 16-byte rows
+    ident = identity_map(M, N2_real / 2);
+    om = &ident;
+    ident.identity = 0;
+  }
+  if (om && !om->identity) {
+    sa.on = 1;
+    sa.mbits = om->mbits;
+    sa.nbits = om->nbits;
+    {
+      // m-block bits (m bits >= 7) and n-block bits (complex n bits >= log2(BN/2)), by output stride
+      int cb = 0;
+      while ((1 << cb) < BN / 2) ++cb;
+      struct VB {
+        int64_t stride;
+        int is_m, idx;
+      };
+      std::vector<VB> vb;
+      // only the m bits inside one launch chunk (chunks cover 2^30 rows or fewer, see below)
+      const uint64_t chunk_rows = std::min<uint64_t>(1ull << 30, ((1ull << 31) / (N2 / BN)) * tc::BM);
+      int cl2 = 0;
+      while ((1ull << cl2) < chunk_rows) ++cl2;
+      for (int j = 7; j < std::min(om->mbits, cl2); ++j) vb.push_back({om->ms[j], 1, j - 7});
+      for (int j = cb; j < om->nbits; ++j) vb.push_back({om->ns[j], 0, j - cb});
+      std::stable_sort(vb.begin(), vb.end(), [](const VB& x, const VB& y) { return x.stride < y.stride; });
+      sa.nv = (int)vb.size();
+      if (sa.nv > 31) throw TnError{TN_E_UNSUPPORTED, "too many tile bits"};
+      for (int b = 0; b < sa.nv; ++b) {
+        sa.vbit_is_m[b] = (int8_t)vb[b].is_m;
+        sa.vbit_idx[b] = (int8_t)vb[b].idx;
+      }
+    }
+    for (int j = 0; j < kMaxModes; ++j) sa.ms[j] = om->ms[j];
+    for (int j = 0; j < 24; ++j) sa.ns[j] = om->ns[j];
+  }
+  CUtensorMap mb = make_map_2d(bp, K2, N2_real, KB, BN);  // rows >= 2N: TMA zero fill
+  // TMA coordinates are int32: process M in chunks of at most 2^30 rows
+  const uint32_t num_n = N2 / BN;
+  const uint64_t chunk = std::min<uint64_t>(1ull << 30, ((1ull << 31) / num_n) * tc::BM);
+  for (uint64_t m_off = 0; m_off < M; m_off += chunk) {
+    uint64_t mm = std::min<uint64_t>(chunk, M - m_off);
+    // (cp.async gather: the A map is unused; N-d: the whole stem, coordinates from the global row)
+    CUtensorMap ma = np ? make_map_nd(a, *np) : make_map_2d(G ? a : a + m_off * K2, K2, G ? tc::BM : mm, KB, tc::BM);
+    gargs.m_base = m_off;
+    CUtensorMap mc = make_map_2d(c + m_off * N2, N2, mm, 64, tc::BM);
+    uint32_t* out_sc = reinterpret_cast<uint32_t*>(c) + (sa.on ? outmap_m(*om, m_off) : 0);
+    uint32_t num_m = (uint32_t)((mm + tc::BM - 1) / tc::BM);
+    uint64_t tiles = (uint64_t)num_m * num_n;
+    int grid = (int)std::min<uint64_t>(tiles, (uint64_t)num_sms());
+    // the exponent is recorded once (first chunk); later chunks reuse the same inputs
+    tc::gemm_chalf_tc_kernel<BN, KB, G><<<grid, G == 1 ? tc::kThreadsGather : tc::kThreads, C::kSmem, s>>>(
+        ma, mb, mc, num_m, num_n, (int)K2, in_max, b_bound, out_max, m_off ? nullptr : exp_slot, sa, out_sc, mm,
+        n_cols, gargs, nda);
+    TN_CUDA(cudaGetLastError());
+  }
+}
+
+template <int KB, int G>
+static void launch_k(__half* c, const __half* a, const __half* bp, uint64_t M, uint32_t K2, uint32_t N2,
+                     const float* in_max, const float* b_bound, uint32_t* out_max, int* exp_slot, const OutMap* om,
+                     cudaStream_t s, const AGather* ag, const NdPlan* np) {
+  switch (N2 < 16 ? 16 : N2) {
+    case 16: launch_bn<16, KB, G>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, ag, np); break;
+    case 32: launch_bn<32, KB, G>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, ag, np); break;
+    case 64: launch_bn<64, KB, G>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, ag, np); break;
+    case 128: launch_bn<128, KB, G>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, ag, np); break;
+    default: launch_bn<256, KB, G>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, ag, np); break;
+  }
+}
+
+template <int G>
+void launch_kb(int KB, __half* c, const __half* a, const __half* bp, uint64_t M, uint32_t K2, uint32_t N2,
+                      const float* in_max, const float* b_bound, uint32_t* out_max, int* exp_slot, const OutMap* om,
+                      cudaStream_t s, const AGather* ag, const NdPlan* np) {
+  switch (KB) {
+    case 64: launch_k<64, G>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, ag, np); break;
+    case 32: launch_k<32, G>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, ag, np); break;
+    default: launch_k<16, G>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, ag, np); break;
+  }
+}
+
+}  // namespace tn
