@@ -165,7 +165,7 @@ __device__ __forceinline__ void named_bar(int id, int n) {
 
 // KB: fp16 elements of K per stage (the TMA box and swizzle width): 64, or 2K when 2K < 64 so that
 // small-K steps neither stage nor zero-fill 3/4 empty boxes and keep more tiles in flight.
-template <int BN, int KB, int RAW = 0>
+template <int BN, int KB, int MODE3 = 0>
 struct Cfg {
   static constexpr int kABytes = BM * KB * 2;
   static constexpr int kBBytes = BN * KB * 2;
@@ -176,7 +176,9 @@ struct Cfg {
   static constexpr int kNBuf = ((220 * 1024 - 2 * 4 * BM * 128) / kStageBytes >= 4) ? 4 : 2;
   static constexpr int kCTma = 2 * kNBuf * BM * 128;      // 128B-swizzled staging for TMA stores, 2 groups
   static constexpr int kCBytes = kCTma;
-  static constexpr int kRawBytes = RAW * kABytes;  // raw TMA landing slots (A mode 3)
+  // raw TMA landing slots (A mode 3): 4 when that leaves >= 2 pipeline stages, else 2
+  static constexpr int kRaw = !MODE3 ? 0 : (((220 * 1024 - kCBytes - 4 * kABytes) / kStageBytes >= 2) ? 4 : 2);
+  static constexpr int kRawBytes = kRaw * kABytes;
   static constexpr int kStagesRaw = (220 * 1024 - kCBytes - kRawBytes) / kStageBytes;
   static constexpr int kStages = kStagesRaw > 24 ? 24 : kStagesRaw;
   static constexpr int kSmem =
@@ -252,9 +254,15 @@ struct NdArgs {
   // the tile's start row and start k index; a zero mask drops that part)
   int8_t mj0[5], msh[5], kj0[5], ksh[5];
   uint32_t mmask[5], kmask[5];
-  // mode 3 (raw box + reshuffle): byte offset in the interleaved stage of each 16-byte piece bit
+  // mode 3 (raw box + reshuffle): the raw box's 16-byte pieces are enumerated as
+  // p = XOR of lane_pat[b] over the lane's bits b, XOR it_pat[i] over the iteration's bits i (a
+  // basis of GF(2)^npb chosen on the host so that every 8-lane phase touches 8 distinct 16-byte bank
+  // slots on both the raw read and the stage write).  Piece p sits at raw byte 16 p and goes to
+  // byte dst(p) of the interleaved stage; dst is GF(2)-linear (each piece bit owns one address
+  // bit), so it is carried as lane_dst / it_dst the same way.
   int npb;
-  uint32_t piece_dst[12];
+  uint16_t lane_pat[5], it_pat[8];
+  uint32_t lane_dst[5], it_dst[8];
 };
 
 namespace tc {
@@ -288,7 +296,7 @@ __global__ void __launch_bounds__(kAMode == 1 ? kThreadsGather : kThreads, 1)
                          const __grid_constant__ NdArgs nda) {
   constexpr bool kGather = kAMode == 1;
   constexpr bool kInter = kAMode == 2 || kAMode == 3;
-  using C = Cfg<BN, KB, kAMode == 3 ? 2 : 0>;
+  using C = Cfg<BN, KB, kAMode == 3 ? 1 : 0>;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   unsigned char* sA = smem;
@@ -300,8 +308,8 @@ __global__ void __launch_bounds__(kAMode == 1 ? kThreadsGather : kThreads, 1)
   uint64_t* tfull = empty + C::kStages;
   uint64_t* tempty = tfull + C::kNAcc;
   uint64_t* raw_full = tempty + C::kNAcc;
-  uint64_t* raw_empty = raw_full + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(raw_empty + 2);
+  uint64_t* raw_empty = raw_full + 4;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(raw_empty + 4);
   struct GTab {
     int64_t off;
     int rc;
@@ -317,12 +325,12 @@ __global__ void __launch_bounds__(kAMode == 1 ? kThreadsGather : kThreads, 1)
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < C::kStages; ++s) {
       // gather / reshuffle: the TMA (B) arrive + the A producer warp's arrive
-      mbar_init(&full[s], (kGather || kAMode == 3) ? 2 : 1);
+      mbar_init(&full[s], kGather ? 2 : (kAMode == 3 ? 3 : 1));
       mbar_init(&empty[s], 1);
     }
-    for (int r = 0; r < 2; ++r) {
+    for (int r = 0; r < 4; ++r) {
       mbar_init(&raw_full[r], 1);
-      mbar_init(&raw_empty[r], 1);
+      mbar_init(&raw_empty[r], 2);  // both reshuffle warps
     }
     for (int a = 0; a < C::kNAcc; ++a) {
       mbar_init(&tfull[a], 1);
@@ -364,9 +372,9 @@ __global__ void __launch_bounds__(kAMode == 1 ? kThreadsGather : kThreads, 1)
         }
         for (int kb = 0; kb < num_k; ++kb, ++qa) {
           if (kAMode == 3) {
-            // A: the raw box (source order) into raw slot qa & 1, for warp 3 to reshuffle
-            const int r = (int)(qa & 1);
-            mbar_wait(&raw_empty[r], ((qa >> 1) & 1) ^ 1);
+            // A: the raw box (source order) into raw slot qa % kRaw, for warps 2-3 to reshuffle
+            const int r = (int)(qa % C::kRaw);
+            mbar_wait(&raw_empty[r], ((qa / C::kRaw) & 1) ^ 1);
             mbar_expect_tx(&raw_full[r], C::kABytes);
             int cc[5];
             nd_coords_k(nda, (uint32_t)kb * (KB / 2), cm, cc);
@@ -431,34 +439,48 @@ __global__ void __launch_bounds__(kAMode == 1 ? kThreadsGather : kThreads, 1)
         mma_commit(&tfull[acc]);
       }
     }
-  } else if (kAMode == 3 && warp == 3) {
-    // ===== A reshuffle: raw slot (source order) -> interleaved K-major stage, 16-byte pieces.
-    // piece p of the raw box goes to sum_b bit_b(p) piece_dst[b]; lanes take piece bits 0..4
-    uint32_t dst_lane = 0;
-    for (int b = 0; b < 5 && b < nda.npb; ++b)
-      if ((lane >> b) & 1) dst_lane += nda.piece_dst[b];
+  } else if (kAMode == 3 && (warp == 2 || warp == 3)) {
+    // ===== A reshuffle (warps 2 and 3, alternate iterations): raw slot (source order) ->
+    // interleaved K-major stage, 16-byte pieces, bank-conflict-free enumeration (NdArgs)
+    const int h = warp - 2;
+    uint32_t raw_lane = 0, dst_lane = 0;
+#pragma unroll
+    for (int b = 0; b < 5; ++b)
+      if ((lane >> b) & 1) {
+        raw_lane ^= (uint32_t)nda.lane_pat[b] << 4;
+        dst_lane ^= nda.lane_dst[b];
+      }
     const int n_it = 1 << (nda.npb - 5);
-    uint32_t* itab = reinterpret_cast<uint32_t*>(gtab);
-    if (lane < n_it) {
-      uint32_t d = 0;
-      for (int b = 5; b < nda.npb; ++b)
-        if ((lane >> (b - 5)) & 1) d += nda.piece_dst[b];
-      itab[lane] = d;
+    uint2* itab = reinterpret_cast<uint2*>(gtab);  // (raw byte, stage byte) per iteration
+    if (h == 0 && lane < n_it) {
+      uint32_t rr = 0, dd = 0;
+      for (int b = 0; b < nda.npb - 5; ++b)
+        if ((lane >> b) & 1) {
+          rr ^= (uint32_t)nda.it_pat[b] << 4;
+          dd ^= nda.it_dst[b];
+        }
+      itab[lane] = make_uint2(rr, dd);
     }
-    __syncwarp();
+    asm volatile("bar.sync 3, 64;" ::: "memory");  // both reshuffle warps see the table
+    const uint32_t raw_u32 = smem_u32(sRaw), a_u32 = smem_u32(sA);
     uint32_t q = 0;
     for (uint32_t t = blockIdx.x; t < num_tiles; t += gridDim.x) {
       for (int kb = 0; kb < num_k; ++kb, ++q) {
-        const int r = (int)(q & 1);
+        const int r = (int)(q % C::kRaw);
         const int s = (int)(q % C::kStages);
-        mbar_wait(&raw_full[r], (q >> 1) & 1);
+        mbar_wait(&raw_full[r], (q / C::kRaw) & 1);
         mbar_wait(&empty[s], ((q / C::kStages) & 1) ^ 1);
-        const uint4* src = reinterpret_cast<const uint4*>(sRaw + r * C::kABytes);
-        unsigned char* dst = sA + s * C::kABytes + dst_lane;
-#pragma unroll 8
-        for (int it = 0; it < n_it; ++it) {
-          const uint4 v = src[it * 32 + lane];
-          *reinterpret_cast<uint4*>(dst + itab[it]) = v;
+        const uint32_t src = raw_u32 + r * C::kABytes, dst = a_u32 + s * C::kABytes;
+#pragma unroll 4
+        for (int it = h; it < n_it; it += 2) {
+          const uint2 e = itab[it];
+          uint4 v;
+          asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
+                       : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                       : "r"(src + (raw_lane ^ e.x)));
+          asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(dst + (dst_lane ^ e.y)), "r"(v.x), "r"(v.y),
+                       "r"(v.z), "r"(v.w)
+                       : "memory");
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> UMMA reads
         __syncwarp();
@@ -781,7 +803,7 @@ static void launch_bn(__half* c, const __half* a, const __half* bp, uint64_t M, 
                       const float* in_max, const float* b_bound, uint32_t* out_max, int* exp_slot, const OutMap* om,
                       cudaStream_t s, const AGather* ag, const NdPlan* np) {
   const uint32_t N2 = std::max<uint32_t>(N2_real, 16);  // B_P has at least 16 (zero-padded) rows
-  using C = tc::Cfg<BN, KB, G == 3 ? 2 : 0>;
+  using C = tc::Cfg<BN, KB, G == 3 ? 1 : 0>;
   static bool attr = false;
   if (!attr) {
     TN_CUDA(cudaFuncSetAttribute(tc::gemm_chalf_tc_kernel<BN, KB, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -156,6 +156,7 @@ static bool build_raw(const AGather& ag, NdPlan& out) {
   }
   if (kind[0] != 1 || jj[0] != 0 || kind[1] != 1 || jj[1] != 1) return false;
   const int cb = std::min(3, ag.klog - 2);
+  uint32_t pdst[16];
   auto inbox = [&](int p) { return kind[p] == 0 ? jj[p] < 7 : jj[p] < 2 + cb; };
   std::vector<std::vector<int>> dims;  // source positions
   for (int p = 0; p < n; ++p) {
@@ -186,12 +187,12 @@ static bool build_raw(const AGather& ag, NdPlan& out) {
     out.dim[d] = 1ull << v.size();
     out.stride[d] = 4ull << v[0];
     out.box[d] = 1u << nbox;
-    // piece bits = box bits except k0, k1 (the 16-byte piece itself)
+    // piece bits = box bits except k0, k1 (the 16-byte piece itself); each owns one stage byte bit
     for (int t = 0; t < nbox; ++t) {
       const int x = v[t];
       if (kind[x] == 1 && jj[x] < 2) continue;
       if (npb >= 12) return false;
-      out.args.piece_dst[npb++] = kind[x] == 0 ? (16u << jj[x]) : (2048u << (jj[x] - 2));
+      pdst[npb++] = kind[x] == 0 ? (16u << jj[x]) : (2048u << (jj[x] - 2));
     }
     // coordinate: the outer bits form at most one run of rows and one run of k (consecutive j)
     bool has_m = false, has_k = false;
@@ -215,7 +216,66 @@ static bool build_raw(const AGather& ag, NdPlan& out) {
     }
   }
   out.args.npb = npb;
-  if (npb != 7 + cb || npb < 5) return false;
+  if (npb != 7 + cb || npb < 5 || npb > 13) return false;
+  // Enumeration basis over GF(2)^npb (piece-bit masks).  Lanes 0-2 each flip one raw slot bit
+  // (raw bytes 16/32/64) and one stage slot bit (stage bytes 16/32/64 = rows m0..m2), so in every
+  // 8-lane phase both the reads and the writes hit 8 distinct 16-byte bank slots.
+  auto dst_of = [&](uint32_t mask) {
+    uint32_t d = 0;
+    for (int i = 0; i < npb; ++i)
+      if ((mask >> i) & 1) d ^= pdst[i];
+    return d;
+  };
+  int dm[3] = {-1, -1, -1};
+  for (int i = 0; i < npb; ++i)
+    for (int t = 0; t < 3; ++t)
+      if (pdst[i] == (16u << t)) dm[t] = i;
+  std::vector<uint32_t> basis;  // reduced copies for the rank test
+  auto add_if_indep = [&](uint32_t m) {
+    uint32_t r = m;
+    for (uint32_t b : basis)
+      if ((r ^ b) < r) r ^= b;
+    if (!r) return false;
+    basis.push_back(r);
+    std::sort(basis.begin(), basis.end(), [](uint32_t x, uint32_t y) { return x > y; });
+    return true;
+  };
+  uint32_t lane[5], its[8];
+  int nl = 0;
+  bool diag = dm[0] >= 0 && dm[1] >= 0 && dm[2] >= 0;
+  if (diag) {
+    // raw-slot and stage-slot projections of the three lane patterns must both be invertible
+    uint32_t rawp[3], dstp[3];
+    for (int t = 0; t < 3; ++t) {
+      lane[t] = (1u << t) | (1u << dm[t]);
+      rawp[t] = lane[t] & 7u;
+      dstp[t] = (dst_of(lane[t]) >> 4) & 7u;
+    }
+    auto inv3 = [](const uint32_t* v) {
+      uint32_t a = v[0], b = v[1], c = v[2];
+      return a && b && c && a != b && a != c && b != c && (a ^ b) != c;
+    };
+    diag = inv3(rawp) && inv3(dstp);
+  }
+  if (diag) {
+    for (int t = 0; t < 3; ++t)
+      if (!add_if_indep(lane[t])) return false;
+    nl = 3;
+  }
+  for (int i = 0; nl < 5 && i < npb; ++i)
+    if (add_if_indep(1u << i)) lane[nl++] = 1u << i;
+  int ni = 0;
+  for (int i = 0; i < npb; ++i)
+    if (add_if_indep(1u << i)) its[ni++] = 1u << i;
+  if (nl != 5 || nl + ni != npb) return false;
+  for (int b = 0; b < 5; ++b) {
+    out.args.lane_pat[b] = (uint16_t)lane[b];
+    out.args.lane_dst[b] = dst_of(lane[b]);
+  }
+  for (int b = 0; b < ni; ++b) {
+    out.args.it_pat[b] = (uint16_t)its[b];
+    out.args.it_dst[b] = dst_of(its[b]);
+  }
   for (int d = 1; d < out.nd; ++d)
     if (out.stride[d] % 16) return false;
   return true;
@@ -240,9 +300,12 @@ void launch_gemm_chalf_tc(__half* c, const __half* a, const __half* bp, uint64_t
     NdPlan np, rp;
     const bool direct = force != 1 && force != 3 && build_nd(*ag, np);
     const bool raw = force != 1 && force != 2 && build_raw(*ag, rp);
-    // a direct box whenever one exists (measured: faster than the raw box + reshuffle even with 32 B
-    // rows, profiles/r01_ncu_summary.md); the raw box when no direct one does (<= 5 dims); else cp.async
-    const bool direct_wide = direct;
+    // A direct box unless its TMA rows are only 32 B with few k blocks: there the raw box (rows as long
+    // as the source runs allow) plus the smem reshuffle wins (C3 step 50, m28 k5 n5: 22.5 -> 16-17 ms);
+    // with many k blocks (K >= 128) the reshuffle's extra smem traffic loses (C3 steps 18, 32).
+    // Raw box when no direct one exists (<= 5 dims); else cp.async.
+    static const int raw_below = getenv("TN_RAW_BELOW") ? atoi(getenv("TN_RAW_BELOW")) : 64;  // tuning knob
+    const bool direct_wide = direct && ((int)(np.box[0] * 4) >= raw_below || ag->klog > 6);
     static const bool dbg = getenv("TN_GATHER_DEBUG") != nullptr;
     if (dbg) {
       fprintf(stderr, "gather mlog %d klog %d: direct %d (inter %d KB %d nd %d box0 %u) raw %d (KB %d nd %d box0 %u)\n",
