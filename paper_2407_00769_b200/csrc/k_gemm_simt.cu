@@ -201,16 +201,25 @@ __global__ void __launch_bounds__(256) gemm_chalf_simt_kernel(__half2* __restric
   if (out_max && (threadIdx.x & 31) == 0) atomic_max_pos2(out_max, mx);
 }
 
-// Row-streaming variant for K*N <= 128 (K <= 16, N <= 32; see rows_ok): one thread per row of A
-// (K complex-half = up to 64 contiguous bytes, vector loads), N outputs in registers, stored as one contiguous run when the
-// output layout keeps the row's outputs contiguous.  No shared-memory round trip for A, no
-// barriers: consecutive threads read consecutive rows (fully coalesced) and the grid-stride loop
-// keeps many rows in flight.
+// Row-streaming variant for K*N <= 128 (K <= 16, N <= 32; see rows_ok): each thread owns RPT
+// consecutive rows of A (RPT*K complex-half contiguous, 16-byte vector loads), keeps the RPT*N
+// outputs in registers and, for a row-major output, stores them as one contiguous run with 256-bit
+// stores (one full 32-byte sector per instruction and lane; RPT is chosen so a thread writes >= 32
+// B when registers allow).  No shared memory for A, no barriers; the grid-stride loop keeps many
+// rows in flight.
+template <int K, int N>
+struct RowsCfg {
+  static constexpr int kRptWant = N >= 8 ? 1 : 8 / N;
+  static constexpr int kRptRegs = 16 / K >= 1 ? 16 / K : 1;
+  static constexpr int kRpt = kRptWant < kRptRegs ? kRptWant : kRptRegs;
+};
+
 template <int K, int N>
 __global__ void __launch_bounds__(256) gemm_chalf_rows_kernel(uint32_t* __restrict__ C, const __half2* __restrict__ A,
                                                               const __half* __restrict__ BP, uint64_t M, int contiguous,
                                                               const float* in_max, const float* b_bound,
                                                               uint32_t* out_max, int* exp_slot, const OutMap om) {
+  constexpr int R = RowsCfg<K, N>::kRpt;
   __shared__ float2 sB[K * N];
   int e = 0;
   if (in_max && b_bound) e = scale_exp_for(in_max[0] * b_bound[0]);
@@ -222,67 +231,102 @@ __global__ void __launch_bounds__(256) gemm_chalf_rows_kernel(uint32_t* __restri
   }
   __syncthreads();
   float mx = 0.f;
-  for (uint64_t m = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; m < M; m += (uint64_t)gridDim.x * blockDim.x) {
-    float2 a[K];
-    const __half2* ar = A + m * K;
-    if constexpr (K >= 4) {
+  const uint64_t groups = (M + R - 1) / R;
+  for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < groups; g += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t m0 = g * R;
+    const bool full = m0 + R <= M;
+    float2 a[R * K];
+    const __half2* ar = A + m0 * K;
+    if constexpr ((R * K) % 4 == 0) {
+      if (full) {
 #pragma unroll
-      for (int q = 0; q < K / 4; ++q) {
-        uint4 v = __ldg(reinterpret_cast<const uint4*>(ar) + q);
-        a[4 * q] = __half22float2(*reinterpret_cast<__half2*>(&v.x));
-        a[4 * q + 1] = __half22float2(*reinterpret_cast<__half2*>(&v.y));
-        a[4 * q + 2] = __half22float2(*reinterpret_cast<__half2*>(&v.z));
-        a[4 * q + 3] = __half22float2(*reinterpret_cast<__half2*>(&v.w));
+        for (int q = 0; q < R * K / 4; ++q) {
+          uint4 v = __ldg(reinterpret_cast<const uint4*>(ar) + q);
+          a[4 * q] = __half22float2(*reinterpret_cast<__half2*>(&v.x));
+          a[4 * q + 1] = __half22float2(*reinterpret_cast<__half2*>(&v.y));
+          a[4 * q + 2] = __half22float2(*reinterpret_cast<__half2*>(&v.z));
+          a[4 * q + 3] = __half22float2(*reinterpret_cast<__half2*>(&v.w));
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < R * K; ++k) a[k] = (m0 + k / K < M) ? __half22float2(ar[k]) : make_float2(0.f, 0.f);
       }
     } else {
 #pragma unroll
-      for (int k = 0; k < K; ++k) a[k] = __half22float2(ar[k]);
+      for (int k = 0; k < R * K; ++k) a[k] = (m0 + k / K < M) ? __half22float2(ar[k]) : make_float2(0.f, 0.f);
     }
-    uint32_t out[N];
+    uint32_t out[R * N];
 #pragma unroll
-    for (int n = 0; n < N; ++n) {
-      float cr = 0.f, ci = 0.f;
+    for (int r = 0; r < R; ++r)
 #pragma unroll
-      for (int k = 0; k < K; ++k) {
-        float2 b = sB[k * N + n];
-        cr = fmaf(a[k].x, b.x, fmaf(-a[k].y, b.y, cr));
-        ci = fmaf(a[k].x, b.y, fmaf(a[k].y, b.x, ci));
+      for (int n = 0; n < N; ++n) {
+        float cr = 0.f, ci = 0.f;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          float2 b = sB[k * N + n];
+          cr = fmaf(a[r * K + k].x, b.x, fmaf(-a[r * K + k].y, b.y, cr));
+          ci = fmaf(a[r * K + k].x, b.y, fmaf(a[r * K + k].y, b.x, ci));
+        }
+        __half2 h = __floats2half2_rn(cr * sc, ci * sc);
+        float2 hf = __half22float2(h);
+        if (r == 0 || m0 + r < M) mx = fmaxf(mx, fmaxf(fabsf(hf.x), fabsf(hf.y)));
+        out[r * N + n] = *reinterpret_cast<uint32_t*>(&h);
       }
-      __half2 h = __floats2half2_rn(cr * sc, ci * sc);
-      float2 hf = __half22float2(h);
-      mx = fmaxf(mx, fmaxf(fabsf(hf.x), fabsf(hf.y)));
-      out[n] = *reinterpret_cast<uint32_t*>(&h);
-    }
-    int64_t base;
-    if (om.identity) {
-      base = (int64_t)(m * N);
-    } else {
-      base = 0;
-      uint64_t mm = m;
-      while (mm) {
-        int j = __ffsll((long long)mm) - 1;
-        base += om.ms[j];
-        mm &= mm - 1;
-      }
-    }
-    uint32_t* dst = C + base;
-    if (contiguous) {
-      if constexpr (N >= 4) {
+    if (om.identity && full) {
+      // the thread's R*N outputs are one contiguous run
+      uint32_t* dst = C + m0 * N;
+      if constexpr (R * N >= 8) {
 #pragma unroll
-        for (int q = 0; q < N / 4; ++q)
-          reinterpret_cast<uint4*>(dst)[q] = make_uint4(out[4 * q], out[4 * q + 1], out[4 * q + 2], out[4 * q + 3]);
-      } else if constexpr (N == 2) {
+        for (int q = 0; q < R * N; q += 8)
+          asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(dst + q), "r"(out[q]), "r"(out[q + 1]),
+                       "r"(out[q + 2]), "r"(out[q + 3]), "r"(out[q + 4]), "r"(out[q + 5]), "r"(out[q + 6]),
+                       "r"(out[q + 7])
+                       : "memory");
+      } else if constexpr (R * N == 4) {
+        *reinterpret_cast<uint4*>(dst) = make_uint4(out[0], out[1], out[2], out[3]);
+      } else if constexpr (R * N == 2) {
         *reinterpret_cast<uint2*>(dst) = make_uint2(out[0], out[1]);
       } else {
         dst[0] = out[0];
       }
-    } else {
+      continue;
+    }
 #pragma unroll
-      for (int n = 0; n < N; ++n) {
-        int64_t o = 0;
-        for (int j = 0; j < om.nbits; ++j)
-          if ((n >> j) & 1) o += om.ns[j];
-        dst[o] = out[n];
+    for (int r = 0; r < R; ++r) {
+      const uint64_t m = m0 + r;
+      if (m >= M) break;
+      int64_t base;
+      if (om.identity) {
+        base = (int64_t)(m * N);
+      } else {
+        base = 0;
+        uint64_t mm = m;
+        while (mm) {
+          int j = __ffsll((long long)mm) - 1;
+          base += om.ms[j];
+          mm &= mm - 1;
+        }
+      }
+      uint32_t* dst = C + base;
+      if (contiguous) {
+        if constexpr (N >= 4) {
+#pragma unroll
+          for (int q = 0; q < N / 4; ++q)
+            reinterpret_cast<uint4*>(dst)[q] =
+                make_uint4(out[r * N + 4 * q], out[r * N + 4 * q + 1], out[r * N + 4 * q + 2], out[r * N + 4 * q + 3]);
+        } else if constexpr (N == 2) {
+          *reinterpret_cast<uint2*>(dst) = make_uint2(out[r * N], out[r * N + 1]);
+        } else {
+          dst[0] = out[r * N];
+        }
+      } else {
+#pragma unroll
+        for (int n = 0; n < N; ++n) {
+          int64_t o = 0;
+          for (int j = 0; j < om.nbits; ++j)
+            if ((n >> j) & 1) o += om.ns[j];
+          dst[o] = out[r * N + n];
+        }
       }
     }
   }
@@ -294,7 +338,8 @@ __global__ void __launch_bounds__(256) gemm_chalf_rows_kernel(uint32_t* __restri
 template <int K, int N>
 static void launch_rows(__half2* c, const __half2* a, const __half* bp, uint64_t M, int contiguous, const float* in_max,
                         const float* b_bound, uint32_t* out_max, int* exp_slot, const OutMap& om, cudaStream_t s) {
-  uint64_t blocks = std::min<uint64_t>((M + 255) / 256, 148ull * 16);
+  constexpr int R = RowsCfg<K, N>::kRpt;
+  uint64_t blocks = std::min<uint64_t>(((M + R - 1) / R + 255) / 256, 148ull * 16);
   if (blocks == 0) blocks = 1;
   gemm_chalf_rows_kernel<K, N><<<(unsigned)blocks, 256, 0, s>>>(reinterpret_cast<uint32_t*>(c), a, bp, M, contiguous,
                                                                 in_max, b_bound, out_max, exp_slot, om);
