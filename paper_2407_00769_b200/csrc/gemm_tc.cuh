@@ -30,6 +30,9 @@
 
 #include "common.cuh"
 
+#ifndef TN_RAW_CAP
+#define TN_RAW_CAP 8
+#endif
 namespace tn {
 
 namespace tc {
@@ -176,13 +179,17 @@ struct Cfg {
   static constexpr int kNBuf = ((220 * 1024 - 2 * 4 * BM * 128) / kStageBytes >= 4) ? 4 : 2;
   static constexpr int kCTma = 2 * kNBuf * BM * 128;      // 128B-swizzled staging for TMA stores, 2 groups
   static constexpr int kCBytes = kCTma;
-  // raw TMA landing slots (A mode 3): 4 when that leaves >= 2 pipeline stages, else 2
-  static constexpr int kRaw = !MODE3 ? 0 : (((220 * 1024 - kCBytes - 4 * kABytes) / kStageBytes >= 2) ? 4 : 2);
+  // raw TMA landing slots (A mode 3): they are the A bytes in flight from HBM, so as many as fit
+  // (<= 8) next to 2 pipeline stages
+  static constexpr int kRawFit = (220 * 1024 - kCBytes - 2 * kStageBytes) / kABytes;
+  static constexpr int kRaw = !MODE3 ? 0 : (kRawFit > TN_RAW_CAP ? TN_RAW_CAP : (kRawFit < 2 ? 2 : kRawFit));
   static constexpr int kRawBytes = kRaw * kABytes;
   static constexpr int kStagesRaw = (220 * 1024 - kCBytes - kRawBytes) / kStageBytes;
   static constexpr int kStages = kStagesRaw > 24 ? 24 : kStagesRaw;
+  // the TMA-store staging (128B swizzle) must start 1024-aligned: pad the stage area
+  static constexpr int kStageArea = (kStages * kStageBytes + 1023) / 1024 * 1024;
   static constexpr int kSmem =
-      kStages * kStageBytes + kCBytes + kRawBytes + 1024 /*align*/ + 2048 /*barriers, gather table*/;
+      kStageArea + kCBytes + kRawBytes + 1024 /*align*/ + 2048 /*barriers, gather table*/;
   // TMEM accumulators: as many as fit in 512 columns (<= 16), so the MMA runs ahead of the
   // epilogue by several tiles when a tile is small (small K, small N)
   static constexpr int kAccStride = BN < 32 ? 32 : BN;
@@ -301,15 +308,15 @@ __global__ void __launch_bounds__(kAMode == 1 ? kThreadsGather : kThreads, 1)
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   unsigned char* sA = smem;
   unsigned char* sB = smem + C::kStages * C::kABytes;
-  unsigned char* sC = sB + C::kStages * C::kBBytes;
+  unsigned char* sC = smem + C::kStageArea;  // 1024-aligned (SW128 staging)
   unsigned char* sRaw = sC + C::kCBytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(sRaw + C::kRawBytes);
   uint64_t* empty = full + C::kStages;
   uint64_t* tfull = empty + C::kStages;
   uint64_t* tempty = tfull + C::kNAcc;
   uint64_t* raw_full = tempty + C::kNAcc;
-  uint64_t* raw_empty = raw_full + 4;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(raw_empty + 4);
+  uint64_t* raw_empty = raw_full + 8;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(raw_empty + 8);
   struct GTab {
     int64_t off;
     int rc;
@@ -328,7 +335,7 @@ __global__ void __launch_bounds__(kAMode == 1 ? kThreadsGather : kThreads, 1)
       mbar_init(&full[s], kGather ? 2 : (kAMode == 3 ? 3 : 1));
       mbar_init(&empty[s], 1);
     }
-    for (int r = 0; r < 4; ++r) {
+    for (int r = 0; r < 8; ++r) {
       mbar_init(&raw_full[r], 1);
       mbar_init(&raw_empty[r], 2);  // both reshuffle warps
     }
@@ -906,7 +913,9 @@ template <int KB, int G>
 static void launch_k(__half* c, const __half* a, const __half* bp, uint64_t M, uint32_t K2, uint32_t N2,
                      const float* in_max, const float* b_bound, uint32_t* out_max, int* exp_slot, const OutMap* om,
                      cudaStream_t s, const AGather* ag, const NdPlan* np) {
-  switch (N2 < 16 ? 16 : N2) {
+  static const uint32_t bn_cap = getenv("TN_MAX_BN") ? (uint32_t)atoi(getenv("TN_MAX_BN")) : 256;  // tuning knob
+  const uint32_t nsel = std::min<uint32_t>(N2 < 16 ? 16 : N2, bn_cap);
+  switch (nsel) {
     case 16: launch_bn<16, KB, G>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, ag, np); break;
     case 32: launch_bn<32, KB, G>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, ag, np); break;
     case 64: launch_bn<64, KB, G>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, ag, np); break;
