@@ -367,18 +367,23 @@ void run_gemm(Plan& p, const StemStep& st, size_t i, const void* src, void* dst,
 
 // The subtask body: every launch after the slice id is in the workspace.  Nothing here depends on
 // the slice id on the host, so one capture of it serves every slice (stem_contract).
-void stem_body(Plan& p, const tn_buffers* b, cudaStream_t s) {
+// head = everything before the first collective (scratch reset, common phase, operand prep, the
+// rank-local stem entry conversion); tail = the rest.  Sharded plans capture only the head.
+void stem_body(Plan& p, const tn_buffers* b, cudaStream_t s, bool head = true, bool tail = true) {
   unsigned char* W = static_cast<unsigned char*>(b->d_ws);
   Scratch sc = scratch_of(p, W);
-  rec_event(p, 0, s);
-  TN_CUDA(cudaMemsetAsync(W + p.ws_scratch, 0, sc.bytes, s));
-  run_common(p, W, s);
-  p.launches += p.common_order.size();
+  if (head) {
+    rec_event(p, 0, s);
+    TN_CUDA(cudaMemsetAsync(W + p.ws_scratch, 0, sc.bytes, s));
+    run_common(p, W, s);
+    p.launches += p.common_order.size();
+  }
   p.result_in_ws = p.steps.empty();
   if (p.steps.empty()) return;
+  const int eb = p.cfg.dtype == TN_CHALF ? 4 : 8;
+  if (head) {
   prepare_b(p, W, sc, s);
   p.launches += p.steps.size() + 2;  // gathers + entry conversion (max + convert)
-  const int eb = p.cfg.dtype == TN_CHALF ? 4 : 8;
   // stem entry -> buffer 0
   {
     const Node& e = p.nodes[p.stem_entry];
@@ -410,11 +415,14 @@ void stem_body(Plan& p, const tn_buffers* b, cudaStream_t s) {
       launch_max_abs_f32(reinterpret_cast<const float*>(src), 2 * n, sc.entry_max, s);
       launch_c64_to_chalf(reinterpret_cast<__half2*>(b->d_stem[0]), src + (uint64_t)p.rank * n_local, n_local,
                           sc.entry_max, &sc.exps[0], reinterpret_cast<uint32_t*>(&sc.max_slot[0]), s);
-      if (p.world > 1) nccl_allreduce_max(&sc.max_slot[0], 1, p.comm->nccl_comm, s);
     } else {
       launch_copy_c64(reinterpret_cast<float2*>(b->d_stem[0]), src + (uint64_t)p.rank * n_local, n_local, s);
     }
   }
+  }
+  if (!tail) return;
+  // every rank scales the first step by the same power of two
+  if (p.world > 1 && p.cfg.dtype == TN_CHALF) nccl_allreduce_max(&sc.max_slot[0], 1, p.comm->nccl_comm, s);
   int cur = 0;
   rec_event(p, 1, s);
   const size_t n_main = p.split_modes.empty() ? p.steps.size() : (size_t)p.split_from;
@@ -461,7 +469,7 @@ void stem_body(Plan& p, const tn_buffers* b, cudaStream_t s) {
 
 bool graph_wanted(const Plan& p) {
   static const bool env_off = getenv("TN_NO_GRAPH") != nullptr;
-  return !env_off && !p.graph_off && p.world == 1;
+  return !env_off && !p.graph_off;
 }
 
 // Capture stem_body on the library stream and instantiate it (once per buffer set).
@@ -479,7 +487,7 @@ void capture_stem(Plan& p, const tn_buffers* b) {
   p.launches = 0;
   TN_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
   try {
-    stem_body(p, b, cs);
+    stem_body(p, b, cs, true, p.world == 1);  // sharded: the collective-free head only
   } catch (...) {
     cudaGraph_t junk = nullptr;
     cudaStreamEndCapture(cs, &junk);
@@ -528,6 +536,10 @@ void stem_contract(Plan& p, const tn_buffers* b, uint64_t slice_id, cudaStream_t
     if (!same) capture_stem(p, b);
     TN_CUDA(cudaGraphLaunch((cudaGraphExec_t)p.graph_exec, s));
     p.launches = p.graph_launches + 1;
+    if (p.world > 1) {  // the tail (swaps, GEMMs) eagerly on the caller's stream
+      stem_body(p, b, s, false, true);
+      return;
+    }
     p.stem_cur = p.graph_stem_cur;
     p.result_buf = p.graph_result_buf;
     p.result_off = 0;
