@@ -142,3 +142,28 @@ def test_split_tail_lowering(tnmod, j):
         assert set(first) <= set(plan["open"])
         for s in tail:
             assert s["out"][:j] == first and not (set(s["R"]) & set(first))
+
+
+@pytest.mark.parametrize("name", ["c2", "c3"])
+def test_fused_permutation_lowering(tnmod, name):
+    """Gathered-A steps (the permutation folded into the GEMM load): only tensor-core steps with
+    M >= 128 and the two innermost stored modes contracted; their kept modes stay in stored order;
+    the output layout is kept ++ new exactly as after a permutation pass; fusing only removes
+    passes (same GEMM geometry and flops)."""
+    with open(os.path.join(ROOT, "plans", f"{name}.json")) as f:
+        plan = json.load(f)
+    fused = _load(tnmod, plan, stem_min_log2=16)
+    plain = _load(tnmod, plan, stem_min_log2=16, no_gather=1)
+    rf, rp = fused.report(), plain.report()
+    assert sum(s["ga"] for s in rf["steps"]) >= 1 and sum(s["ga"] for s in rp["steps"]) == 0
+    assert fused.info()["n_permutes"] < plain.info()["n_permutes"]
+    assert fused.info()["perm_bytes"] < plain.info()["perm_bytes"]
+    assert fused.info()["stem_flops"] == plain.info()["stem_flops"]
+    for s in rf["steps"]:
+        if not s["ga"]:
+            continue
+        lay, R = s["in"], set(s["R"])
+        assert s["tc"] and not s["perm"] and s["m"] >= 7 and s["k"] >= 3
+        assert lay[-1] in R and lay[-2] in R
+        kept = [l for l in lay if l not in R]
+        assert s["out"][:len(kept)] == kept              # kept modes in stored order, then new modes
