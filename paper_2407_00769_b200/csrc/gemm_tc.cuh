@@ -300,7 +300,7 @@ __global__ void __launch_bounds__(kAMode == 1 ? kThreadsGather : kThreads, 1)
                          const float* in_max, const float* b_bound, uint32_t* out_max, int* exp_slot,
                          const __grid_constant__ ScatterArgs sc_args, uint32_t* out_scatter, uint64_t rows,
                          uint32_t n_cols, const __grid_constant__ AGatherArgs ga,
-                         const __grid_constant__ NdArgs nda) {
+                         const __grid_constant__ NdArgs nda, int epi_stg) {
   constexpr bool kGather = kAMode == 1;
   constexpr bool kInter = kAMode == 2 || kAMode == 3;
   using C = Cfg<BN, KB, kAMode == 3 ? 1 : 0>;
@@ -629,7 +629,7 @@ __global__ void __launch_bounds__(kAMode == 1 ? kThreadsGather : kThreads, 1)
 #pragma unroll 1
       for (int sub = 0; sub < BN; sub += 64, ++gsub) {
         unsigned char* sbuf = sCg + (gsub % C::kNBuf) * (BM * 128);
-        if (!scat) {
+        if (!scat && !epi_stg) {
           // ring slot free? (the TMA store that used it kNBuf subtiles ago has read it)
           if (etid == 0) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(C::kNBuf - 1) : "memory");
           named_bar(1 + grp, 128);
@@ -704,7 +704,25 @@ __global__ void __launch_bounds__(kAMode == 1 ? kThreadsGather : kThreads, 1)
             }
           }
         }
-        if (!scat) {
+        if (!scat && epi_stg) {
+          // coalesced stores from the staged subtile: 8 threads per 128-byte row segment, each warp
+          // instruction writes 4 full lines (LSU path instead of the TMA store engine)
+          named_bar(1 + grp, 128);
+          const uint32_t pitch = num_n * BN;  // halfs per output row
+          const int ncol = (int)(2 * n_cols);
+#pragma unroll 4
+          for (int it = 0; it < 8; ++it) {
+            const int id = it * 128 + etid;
+            const int rr = id >> 3, cc = id & 7;
+            const int col = n0 + sub + cc * 8;
+            if ((uint64_t)(m0 + rr) < rows && col < ncol && (BN >= 64 || sub + cc * 8 < BN)) {
+              const uint4 v = *reinterpret_cast<const uint4*>(sbuf + rr * 128 + ((cc ^ (rr & 7)) << 4));
+              __half* gp = reinterpret_cast<__half*>(out_scatter) + (uint64_t)(m0 + rr) * pitch + col;
+              *reinterpret_cast<uint4*>(gp) = v;
+            }
+          }
+          named_bar(1 + grp, 128);  // the ring slot may be rewritten
+        } else if (!scat) {
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           named_bar(1 + grp, 128);
           if (etid == 0) {
@@ -888,6 +906,8 @@ static void launch_bn(__half* c, const __half* a, const __half* bp, uint64_t M, 
     for (int j = 0; j < 24; ++j) sa.ns[j] = om->ns[j];
   }
   CUtensorMap mb = make_map_2d(bp, K2, N2_real, KB, BN);  // rows >= 2N: TMA zero fill
+  static const int stg_env = getenv("TN_STG_EPI") ? atoi(getenv("TN_STG_EPI")) : 0;  // experiment knob
+  const int epi_stg = stg_env;
   // TMA coordinates are int32: process M in chunks of at most 2^30 rows
   const uint32_t num_n = N2 / BN;
   const uint64_t chunk = std::min<uint64_t>(1ull << 30, ((1ull << 31) / num_n) * tc::BM);
@@ -897,14 +917,15 @@ static void launch_bn(__half* c, const __half* a, const __half* bp, uint64_t M, 
     CUtensorMap ma = np ? make_map_nd(a, *np) : make_map_2d(G ? a : a + m_off * K2, K2, G ? tc::BM : mm, KB, tc::BM);
     gargs.m_base = m_off;
     CUtensorMap mc = make_map_2d(c + m_off * N2, N2, mm, 64, tc::BM);
-    uint32_t* out_sc = reinterpret_cast<uint32_t*>(c) + (sa.on ? outmap_m(*om, m_off) : 0);
+    // scatter: base of this chunk's rows in the OutMap; row-major: the chunk's first row (STG epilogue)
+    uint32_t* out_sc = reinterpret_cast<uint32_t*>(c) + (sa.on ? outmap_m(*om, m_off) : m_off * (N2 / 2));
     uint32_t num_m = (uint32_t)((mm + tc::BM - 1) / tc::BM);
     uint64_t tiles = (uint64_t)num_m * num_n;
     int grid = (int)std::min<uint64_t>(tiles, (uint64_t)num_sms());
     // the exponent is recorded once (first chunk); later chunks reuse the same inputs
     tc::gemm_chalf_tc_kernel<BN, KB, G><<<grid, G == 1 ? tc::kThreadsGather : tc::kThreads, C::kSmem, s>>>(
         ma, mb, mc, num_m, num_n, (int)K2, in_max, b_bound, out_max, m_off ? nullptr : exp_slot, sa, out_sc, mm,
-        n_cols, gargs, nda);
+        n_cols, gargs, nda, epi_stg);
     TN_CUDA(cudaGetLastError());
   }
 }
