@@ -131,7 +131,7 @@ def main():
     ap.add_argument("--oracle-log2", type=int, default=24)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--replicas", action="store_true", help="N>1: independent slices per GPU (weak scaling)")
-    ap.add_argument("--comm", default="int8", choices=["int8", "fp16"])
+    ap.add_argument("--comm", default="int8", choices=["int8", "int4", "fp16"])
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -170,7 +170,7 @@ def main():
 
     sharded = world > 1 and not args.replicas
     comm = tn.Comm(rank, world, local) if sharded else None
-    codec = tn.TN_COMM_INT8 if args.comm == "int8" else tn.TN_COMM_FP16
+    codec = {"int8": tn.TN_COMM_INT8, "int4": tn.TN_COMM_INT4}.get(args.comm, tn.TN_COMM_FP16)
     p = tn.Plan(plan_json, tn.make_config(dtype=tn.TN_CHALF, stem_min_log2=20, comm_codec=codec), comm=comm)
     info = p.info()
     bufs = tn.Buffers(p)

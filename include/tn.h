@@ -226,6 +226,14 @@ TN_API int tn_quant_int8_f16(int8_t* d_codes, float* d_scales, float* d_zeros, c
                              int g, void* stream);
 TN_API int tn_dequant_int8_f16(void* d_y, const int8_t* d_codes, const float* d_scales, const float* d_zeros,
                                uint64_t n, int g, void* stream);
+/* int4 preset (Table 1: q in [0, 15], exp 1, groups of g reals) on fp16
+ * reals: n/2 packed bytes, two codes per byte with the low nibble = even index (reading C-A14);
+ * scale = 15/(max-min), zero = -15*min/(max-min) per group (fp32, multiply then add, no FMA;
+ * constant groups: scale 0, zero = the constant, codes 0).  g even, n a multiple of g. */
+TN_API int tn_quant_int4_f16(uint8_t* d_packed, float* d_scales, float* d_zeros, const void* d_x, uint64_t n,
+                             int g, void* stream);
+TN_API int tn_dequant_int4_f16(void* d_y, const uint8_t* d_packed, const float* d_scales, const float* d_zeros,
+                               uint64_t n, int g, void* stream);
 
 /* ---- multi-GPU (stem sharded on its log2(world) outermost modes, Alg. 1) ---- */
 TN_API int tn_comm_unique_id(uint8_t out[128]);

@@ -97,6 +97,10 @@ void launch_pad_b(__half* bp, const float2* b, int klog, int nlog, const uint32_
 // complex64 -> complex-half with scale from max (entry of the stem)
 void launch_c64_to_chalf(__half2* dst, const float2* src, uint64_t n, const uint32_t* max_bits,
                          int* exp_slot, uint32_t* out_max_bits, cudaStream_t s);
+void launch_quant_int4_half(uint8_t* packed, float* scales, float* zeros, const __half* x, uint64_t n, int g,
+                            cudaStream_t s);
+void launch_dequant_int4_half(__half* y, const uint8_t* packed, const float* scales, const float* zeros, uint64_t n,
+                              int g, cudaStream_t s);
 void launch_set_u64(uint64_t* p, uint64_t v, cudaStream_t s);
 void launch_copy_c64(float2* dst, const float2* src, uint64_t n, cudaStream_t s);
 void launch_gemm_c64(float2* c, const float2* a, const float2* b, uint64_t M, uint32_t K, uint32_t N,

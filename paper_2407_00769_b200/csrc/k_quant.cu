@@ -112,4 +112,88 @@ void launch_dequant_int8_half(__half* y, const int8_t* codes, const float* scale
   TN_CUDA(cudaGetLastError());
 }
 
+// int4 preset of Table 1: q in [0, 15], exp = 1, groups of g reals (reading C-A14: two
+// codes per byte, low nibble = even index).  scale = 15/(max-min), zero = (0*max - 15*min)/(max-min)
+// in the same fp32 operation order as the int8 codec; degenerate groups: scale 0, zero = the
+// constant, codes 0 (q_min).  One warp per group, each lane packs pairs of reals.
+__global__ void quant_int4_half_kernel(uint8_t* __restrict__ packed, float* __restrict__ scales,
+                                       float* __restrict__ zeros, const __half* __restrict__ x, uint64_t n_groups,
+                                       int g) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  for (uint64_t gi = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); gi < n_groups; gi += warps) {
+    const __half* xs = x + gi * g;
+    float mx = -INFINITY, mn = INFINITY;
+    for (int i = lane; i < g; i += 32) {
+      float v = __half2float(xs[i]);
+      mx = fmaxf(mx, v);
+      mn = fminf(mn, v);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    }
+    float scale, zero;
+    if (mx == mn) {
+      scale = 0.f;
+      zero = mx;
+    } else {
+      float den = __fsub_rn(mx, mn);
+      scale = __fdiv_rn(15.f, den);
+      zero = __fdiv_rn(__fsub_rn(__fmul_rn(0.f, mx), __fmul_rn(15.f, mn)), den);
+    }
+    if (lane == 0) {
+      scales[gi] = scale;
+      zeros[gi] = zero;
+    }
+    uint8_t* ps = packed + gi * (g / 2);
+    for (int i = lane; i < g / 2; i += 32) {
+      uint32_t q[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        float c = 0.f;
+        if (scale != 0.f) {
+          c = rintf(__fadd_rn(__fmul_rn(__half2float(xs[2 * i + h]), scale), zero));
+          c = fminf(fmaxf(c, 0.f), 15.f);
+        }
+        q[h] = (uint32_t)c;
+      }
+      ps[i] = (uint8_t)(q[0] | (q[1] << 4));
+    }
+  }
+}
+
+__global__ void dequant_int4_half_kernel(__half* __restrict__ y, const uint8_t* __restrict__ packed,
+                                         const float* __restrict__ scales, const float* __restrict__ zeros,
+                                         uint64_t n, int g) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; 2 * i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint8_t b = packed[i];
+    const uint64_t gi = (2 * i) / g;
+    const float s = scales[gi], z = zeros[gi];
+    const float c0 = (float)(b & 0xF), c1 = (float)(b >> 4);
+    y[2 * i] = __float2half_rn((s == 0.f) ? z : __fdiv_rn(__fsub_rn(c0, z), s));
+    y[2 * i + 1] = __float2half_rn((s == 0.f) ? z : __fdiv_rn(__fsub_rn(c1, z), s));
+  }
+}
+
+void launch_quant_int4_half(uint8_t* packed, float* scales, float* zeros, const __half* x, uint64_t n, int g,
+                            cudaStream_t s) {
+  if (g <= 0 || (g & 1) || n % g) throw TnError{TN_E_INVALID, "int4 quant: n must be a multiple of an even group size"};
+  uint64_t groups = n / g;
+  uint64_t blocks = std::min<uint64_t>((groups + 7) / 8, 148ull * 16);
+  if (blocks == 0) return;
+  quant_int4_half_kernel<<<(unsigned)blocks, 256, 0, s>>>(packed, scales, zeros, x, groups, g);
+  TN_CUDA(cudaGetLastError());
+}
+
+void launch_dequant_int4_half(__half* y, const uint8_t* packed, const float* scales, const float* zeros, uint64_t n,
+                              int g, cudaStream_t s) {
+  if (g <= 0 || (g & 1) || n % g) throw TnError{TN_E_INVALID, "int4 dequant: n must be a multiple of an even group size"};
+  uint64_t blocks = std::min<uint64_t>((n / 2 + 255) / 256, 148ull * 16);
+  if (blocks == 0) return;
+  dequant_int4_half_kernel<<<(unsigned)blocks, 256, 0, s>>>(y, packed, scales, zeros, n, g);
+  TN_CUDA(cudaGetLastError());
+}
+
 }  // namespace tn

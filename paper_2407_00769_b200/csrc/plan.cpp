@@ -347,7 +347,7 @@ Plan* load_plan(const char* json, size_t len, const tn_config* cfg_in, int world
           // quantise only in the later stages of the path (earlier errors accumulate)
           {
             const int pct = cfg.quant_from_pct < 0 ? 50 : cfg.quant_from_pct;
-            st.quant = cfg.dtype == TN_CHALF && cfg.comm_codec == TN_COMM_INT8 &&
+            st.quant = cfg.dtype == TN_CHALF && (cfg.comm_codec == TN_COMM_INT8 || cfg.comm_codec == TN_COMM_INT4) &&
                        100.0 * (double)s >= pct * (double)step_nodes.size();
           }
           st.swap_out_pos = out_pos;
@@ -370,7 +370,8 @@ Plan* load_plan(const char* json, size_t len, const tn_config* cfg_in, int world
           p.n_swaps++;
           const double n_local = std::ldexp(1.0, (int)L.size());
           const double frac = 1.0 - std::ldexp(1.0, -(int)out_pos.size());
-          const double per = !st.quant ? (cfg.dtype == TN_CHALF ? 4.0 : 8.0) : (2.0 + 16.0 / cfg.comm_group);
+          const double per = !st.quant ? (cfg.dtype == TN_CHALF ? 4.0 : 8.0)
+                                        : ((cfg.comm_codec == TN_COMM_INT4 ? 1.0 : 2.0) + 16.0 / cfg.comm_group);
           p.swap_bytes += frac * n_local * per;
         }
         st.shard_after = shard;

@@ -271,33 +271,43 @@ void mode_swap(Plan& p, const StemStep& st, const tn_buffers* b, int& cur, cudaS
   void* comm = p.comm->nccl_comm;
   unsigned char* X = static_cast<unsigned char*>(b->d_stem[cur]);
   unsigned char* Y = static_cast<unsigned char*>(b->d_stem[1 - cur]);
-  const bool int8 = st.quant;  // lowering: int8 codec, complex-half, late enough in the path
-  if (int8) {
+  const bool quant = st.quant;  // lowering: int8/int4 codec, complex-half, late enough in the path
+  if (quant) {
     const int g = p.cfg.comm_group;
+    const bool int4 = p.cfg.comm_codec == TN_COMM_INT4;
     const uint64_t reals = 2 * n_local, creals = 2 * chunk;
     if (creals % g) throw TnError{TN_E_INFEASIBLE, "swap chunk is not a multiple of the quantisation group"};
     const uint64_t ng = reals / g, cng = creals / g;
-    const uint64_t codes_bytes = align_up(reals, 256);
+    const uint64_t cbytes = int4 ? creals / 2 : creals;  // code bytes per chunk
+    const uint64_t codes_bytes = align_up(int4 ? reals / 2 : reals, 256);
     auto codes = [&](unsigned char* base) { return reinterpret_cast<int8_t*>(base); };
     auto scales = [&](unsigned char* base) { return reinterpret_cast<float*>(base + codes_bytes); };
     auto zeros = [&](unsigned char* base) { return reinterpret_cast<float*>(base + codes_bytes + align_up(4 * ng, 256)); };
-    launch_quant_int8_half(codes(Y), scales(Y), zeros(Y), reinterpret_cast<const __half*>(X), reals, g, s);
+    if (int4)
+      launch_quant_int4_half(reinterpret_cast<uint8_t*>(codes(Y)), scales(Y), zeros(Y), reinterpret_cast<const __half*>(X),
+                             reals, g, s);
+    else
+      launch_quant_int8_half(codes(Y), scales(Y), zeros(Y), reinterpret_cast<const __half*>(X), reals, g, s);
     nccl_group(true);
     for (int v = 0; v < (1 << sx); ++v) {
       if (v == me) continue;
       int peer = peer_of(v);
-      nccl_send(codes(Y) + v * creals, creals, NCCL_INT8, peer, comm, s);
+      nccl_send(codes(Y) + v * cbytes, cbytes, NCCL_INT8, peer, comm, s);
       nccl_send(scales(Y) + v * cng, cng, NCCL_FLOAT32, peer, comm, s);
       nccl_send(zeros(Y) + v * cng, cng, NCCL_FLOAT32, peer, comm, s);
-      nccl_recv(codes(X) + v * creals, creals, NCCL_INT8, peer, comm, s);
+      nccl_recv(codes(X) + v * cbytes, cbytes, NCCL_INT8, peer, comm, s);
       nccl_recv(scales(X) + v * cng, cng, NCCL_FLOAT32, peer, comm, s);
       nccl_recv(zeros(X) + v * cng, cng, NCCL_FLOAT32, peer, comm, s);
     }
     nccl_group(false);
-    TN_CUDA(cudaMemcpyAsync(codes(X) + me * creals, codes(Y) + me * creals, creals, cudaMemcpyDeviceToDevice, s));
+    TN_CUDA(cudaMemcpyAsync(codes(X) + me * cbytes, codes(Y) + me * cbytes, cbytes, cudaMemcpyDeviceToDevice, s));
     TN_CUDA(cudaMemcpyAsync(scales(X) + me * cng, scales(Y) + me * cng, 4 * cng, cudaMemcpyDeviceToDevice, s));
     TN_CUDA(cudaMemcpyAsync(zeros(X) + me * cng, zeros(Y) + me * cng, 4 * cng, cudaMemcpyDeviceToDevice, s));
-    launch_dequant_int8_half(reinterpret_cast<__half*>(Y), codes(X), scales(X), zeros(X), reals, g, s);
+    if (int4)
+      launch_dequant_int4_half(reinterpret_cast<__half*>(Y), reinterpret_cast<const uint8_t*>(codes(X)), scales(X),
+                               zeros(X), reals, g, s);
+    else
+      launch_dequant_int8_half(reinterpret_cast<__half*>(Y), codes(X), scales(X), zeros(X), reals, g, s);
     p.launches += 2;
   } else {
     const int type = eb == 4 ? NCCL_FLOAT16 : NCCL_FLOAT32;
@@ -1013,6 +1023,18 @@ int tn_quant_int8_f16(int8_t* d_codes, float* d_scales, float* d_zeros, const vo
                       void* stream) {
   if (!d_codes || !d_scales || !d_zeros || !d_x) return fail(TN_E_INVALID, "NULL argument");
   TN_TRY(launch_quant_int8_half(d_codes, d_scales, d_zeros, (const __half*)d_x, n, g, (cudaStream_t)stream));
+}
+
+int tn_quant_int4_f16(uint8_t* d_packed, float* d_scales, float* d_zeros, const void* d_x, uint64_t n, int g,
+                      void* stream) {
+  if (!d_packed || !d_scales || !d_zeros || !d_x) return fail(TN_E_INVALID, "NULL argument");
+  TN_TRY(launch_quant_int4_half(d_packed, d_scales, d_zeros, (const __half*)d_x, n, g, (cudaStream_t)stream));
+}
+
+int tn_dequant_int4_f16(void* d_y, const uint8_t* d_packed, const float* d_scales, const float* d_zeros, uint64_t n,
+                        int g, void* stream) {
+  if (!d_y || !d_packed || !d_scales || !d_zeros) return fail(TN_E_INVALID, "NULL argument");
+  TN_TRY(launch_dequant_int4_half((__half*)d_y, d_packed, d_scales, d_zeros, n, g, (cudaStream_t)stream));
 }
 
 int tn_dequant_int8_f16(void* d_y, const int8_t* d_codes, const float* d_scales, const float* d_zeros, uint64_t n,

@@ -77,6 +77,8 @@ def lib():
         L.tn_dequant_int8.argtypes = [vp, vp, vp, vp, u64, i32, vp]
         L.tn_quant_int8_f16.argtypes = [vp, vp, vp, vp, u64, i32, vp]
         L.tn_dequant_int8_f16.argtypes = [vp, vp, vp, vp, u64, i32, vp]
+        L.tn_quant_int4_f16.argtypes = [vp, vp, vp, vp, u64, i32, vp]
+        L.tn_dequant_int4_f16.argtypes = [vp, vp, vp, vp, u64, i32, vp]
         L.tn_comm_unique_id.argtypes = [vp]
         L.tn_comm_init.argtypes = [vp, i32, i32, i32, C.POINTER(vp)]
         L.tn_comm_free.argtypes = [vp]
@@ -280,6 +282,14 @@ def tn_quant_int8_f16(codes, scales, zeros, x, g, stream=None):
 
 def tn_dequant_int8_f16(y, codes, scales, zeros, g, stream=None):
     _check(lib().tn_dequant_int8_f16(_ptr(y), _ptr(codes), _ptr(scales), _ptr(zeros), y.numel(), g, _stream(stream)))
+
+
+def tn_quant_int4_f16(packed, scales, zeros, x, g, stream=None):
+    _check(lib().tn_quant_int4_f16(_ptr(packed), _ptr(scales), _ptr(zeros), _ptr(x), x.numel(), g, _stream(stream)))
+
+
+def tn_dequant_int4_f16(y, packed, scales, zeros, g, stream=None):
+    _check(lib().tn_dequant_int4_f16(_ptr(y), _ptr(packed), _ptr(scales), _ptr(zeros), y.numel(), g, _stream(stream)))
 
 
 def tn_dequant_int8(y, codes, scales, zeros, g, stream=None):

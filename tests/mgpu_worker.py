@@ -41,7 +41,9 @@ def main():
     with open(os.path.join(ROOT, "plans", "c2.json")) as f:
         c2 = MP.sub_slice(json.load(f), 20)
     for codec, name, plan, pct, sm in ((tn.TN_COMM_FP16, "fp16", sub, -1, 14), (tn.TN_COMM_INT8, "int8", sub, -1, 14),
-                                       (tn.TN_COMM_INT8, "int8_all_c2", c2, 0, 12)):
+                                       (tn.TN_COMM_INT8, "int8_all_c2", c2, 0, 12),
+                                       (tn.TN_COMM_INT4, "int4", sub, -1, 14),
+                                       (tn.TN_COMM_INT4, "int4_late", sub, 30, 14)):
         p = tn.Plan(plan, tn.make_config(stem_min_log2=sm, comm_codec=codec, quant_from_pct=pct), comm=comm)
         b = tn.Buffers(p)
         amps = tn.contract(p, b, 0)
@@ -61,6 +63,10 @@ def main():
                    "int8_swaps_c3": sum(1 for s in results["int8"][1]["steps"] if s.get("quant")),
                    "rel_fp16_oracle": metrics.rel_l2(results["fp16"][0], ref),
                    "rel_int8_oracle": metrics.rel_l2(results["int8"][0], ref),
+                   "rel_int4_oracle": metrics.rel_l2(results["int4"][0], ref),
+                   "int4_swaps_c3": sum(1 for s in results["int4"][1]["steps"] if s.get("quant")),
+                   "rel_int4_late_oracle": metrics.rel_l2(results["int4_late"][0], ref),
+                   "int4_swaps_late": sum(1 for s in results["int4_late"][1]["steps"] if s.get("quant")),
                    "rel_fp16_vs_1gpu": metrics.rel_l2(results["fp16"][0], one),
                    "rel_1gpu_oracle": metrics.rel_l2(one, ref),
                    "swaps": sum(1 for s in results["int8"][1]["steps"] if s.get("swap")),

@@ -329,3 +329,32 @@ def test_gemm_chalf_gathered_runs_exact(env, runs, N):
     got = C.cpu().numpy().astype(np.float64).reshape(1 << mlog, N, 2)
     ref = a @ bm
     assert np.array_equal(got[..., 0], ref.real) and np.array_equal(got[..., 1], ref.imag)
+
+
+def test_quant_int4_f16_payload_bit_exact(env):
+    """int4 preset (Table 1; reading C-A14 packing) on fp16 payloads: packed codes,
+    scales and zeros bit-exact vs the oracle codec; dequantised fp16 = oracle dequant rounded."""
+    torch, tn = env
+    rng = np.random.default_rng(4)
+    g = 128
+    x = (rng.standard_normal(g * 300) * 2000).astype(np.float16)
+    x[g:2 * g] = 0                           # constant group (C-A11)
+    x[2 * g:3 * g:2] = 0
+    X = torch.from_numpy(x).cuda()
+    packed = torch.empty(x.size // 2, dtype=torch.uint8, device="cuda")
+    sc = torch.empty(x.size // g, dtype=torch.float32, device="cuda")
+    ze = torch.empty_like(sc)
+    tn.tn_quant_int4_f16(packed, sc, ze, X, g)
+    y = torch.empty_like(X)
+    tn.tn_dequant_int4_f16(y, packed, sc, ze, g)
+    torch.cuda.synchronize()
+    rc, rs, rz = codec.quantize(x.astype(np.float32), np.float32(0), np.float32(15), 1.0, group=g)
+    assert np.array_equal(packed.cpu().numpy(), codec.pack_int4(rc))
+    assert np.array_equal(sc.cpu().numpy(), rs) and np.array_equal(ze.cpu().numpy(), rz)
+    assert np.array_equal(y.cpu().numpy(), codec.dequantize(rc, rs, rz, 1.0, group=g).astype(np.float16))
+    # half a quantisation step per element, plus the fp16 rounding of the dequantised value:
+    # |err| <= (max - min) / 30 + ulp_fp16(|x|) per group
+    xg = x.astype(np.float64).reshape(-1, g)
+    err = np.abs(y.cpu().numpy().astype(np.float64).reshape(-1, g) - xg)
+    span = np.ptp(xg, axis=1)
+    assert np.all(err.max(axis=1) <= span / 30 * (1 + 1e-5) + np.abs(xg).max(axis=1) * 2.0 ** -10)
