@@ -46,6 +46,32 @@ def peaks():
         return 6650.0, 1590.0, 1400.0, "fallback"
 
 
+class Energy:
+    """Board energy over the timed region from NVML's cumulative counter (mJ since driver load;
+    SURVEY §8(f) #4, context beside the paper's Wh per subtask)."""
+
+    def __init__(self, index):
+        self.h = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.e0 = pynvml.nvmlDeviceGetTotalEnergyConsumption(self.h)
+            self.t0 = time.perf_counter()
+        except Exception:
+            self.h = None
+
+    def stop(self):
+        if self.h is None:
+            return None
+        try:
+            j = (self.nv.nvmlDeviceGetTotalEnergyConsumption(self.h) - self.e0) / 1000.0  # J
+            return j / (time.perf_counter() - self.t0)  # mean board power over the interval, W
+        except Exception:
+            return None
+
+
 class Clocks:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
 
@@ -190,15 +216,21 @@ def main():
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    nrg = Energy(local)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(dev_stream)
     for _ in range(args.steps):
         step()
     e1.record(dev_stream)
     torch.cuda.synchronize()
+    watts = nrg.stop()
     if world > 1:
         dist.barrier()
     clocks = clk.stop()
+    if world > 1 and watts is not None:  # whole-job power: sum over ranks
+        wt = torch.tensor([watts], device="cuda", dtype=torch.float64)
+        dist.all_reduce(wt, op=dist.ReduceOp.SUM)
+        watts = float(wt.item())
     t_ms = e0.elapsed_time(e1) / args.steps
     rep = p.report()
     launches = p.info()["n_launches"] * args.steps
@@ -299,7 +331,13 @@ def main():
                 "e2e": {"value": flops / (te_ms * 1e-3) / 1e12, "unit": "TFLOPS",
                         "ms_per_step": te_ms, "h2d_bytes_per_step": info["h2d_bytes"],
                         "d2h_bytes_per_step": (4 << info["n_open"]) + 4 * (2 * info["n_stem_steps"] + 4)},
-                "gpu_launches": launches, "clocks": clocks}
+                "gpu_launches": launches, "clocks": clocks,
+                "energy": None if watts is None else
+                {"joules_per_step": watts * t_ms * 1e-3, "wh_per_step": watts * t_ms * 1e-3 / 3600.0,
+                 "mean_board_w_per_gpu": watts / world,
+                 "source": "nvmlDeviceGetTotalEnergyConsumption delta / wall time over the timed region "
+                           "(summed over ranks) x device ms_per_step",
+                 "note": "context only (SURVEY 8(f) #4); a step = one subtask (sharded) or one per rank"}}
         if world == 1 and not args.no_cpu:
             try:
                 line["cpu_baseline"] = cpu_baseline(plan_json, args.oracle_log2)
