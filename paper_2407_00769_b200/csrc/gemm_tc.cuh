@@ -478,16 +478,28 @@ __global__ void __launch_bounds__(kAMode == 1 ? kThreadsGather : kThreads, 1)
         mbar_wait(&raw_full[r], (q / C::kRaw) & 1);
         mbar_wait(&empty[s], ((q / C::kStages) & 1) ^ 1);
         const uint32_t src = raw_u32 + r * C::kABytes, dst = a_u32 + s * C::kABytes;
-#pragma unroll 4
-        for (int it = h; it < n_it; it += 2) {
-          const uint2 e = itab[it];
-          uint4 v;
-          asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
-                       : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-                       : "r"(src + (raw_lane ^ e.x)));
-          asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(dst + (dst_lane ^ e.y)), "r"(v.x), "r"(v.y),
-                       "r"(v.z), "r"(v.w)
-                       : "memory");
+        // batches of 8 pieces: all 8 loads in flight before the 8 stores (the LDS->STS latency,
+        // not bandwidth, bounded the single-piece loop)
+        for (int it0 = h; it0 < n_it; it0 += 16) {
+          uint4 v[8];
+          uint32_t dd[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int it = it0 + 2 * u;
+            if (it < n_it) {
+              const uint2 e = itab[it];
+              dd[u] = dst + (dst_lane ^ e.y);
+              asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
+                           : "=r"(v[u].x), "=r"(v[u].y), "=r"(v[u].z), "=r"(v[u].w)
+                           : "r"(src + (raw_lane ^ e.x)));
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (it0 + 2 * u < n_it)
+              asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(dd[u]), "r"(v[u].x), "r"(v[u].y), "r"(v[u].z),
+                           "r"(v[u].w)
+                           : "memory");
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> UMMA reads
         __syncwarp();

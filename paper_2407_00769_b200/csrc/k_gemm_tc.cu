@@ -300,12 +300,12 @@ void launch_gemm_chalf_tc(__half* c, const __half* a, const __half* bp, uint64_t
     NdPlan np, rp;
     const bool direct = force != 1 && force != 3 && build_nd(*ag, np);
     const bool raw = force != 1 && force != 2 && build_raw(*ag, rp);
-    // A direct box unless its TMA rows are only 32 B with few k blocks: there the raw box (rows as long
-    // as the source runs allow) plus the smem reshuffle wins (C3 step 50, m28 k5 n5: 22.5 -> 16-17 ms);
-    // with many k blocks (K >= 128) the reshuffle's extra smem traffic loses (C3 steps 18, 32).
+    // A direct box unless its TMA rows are only 32 B: there the raw box (rows as long as the source
+    // runs allow) plus the smem reshuffle wins (C3 step 50, m28 k5 n5: 22.5 -> 13.5 ms; m21 k9 n6:
+    // 1.63 -> 1.18 ms); at 64-byte rows the two tie, at 128 B the direct box is faster.
     // Raw box when no direct one exists (<= 5 dims); else cp.async.
     static const int raw_below = getenv("TN_RAW_BELOW") ? atoi(getenv("TN_RAW_BELOW")) : 64;  // tuning knob
-    const bool direct_wide = direct && ((int)(np.box[0] * 4) >= raw_below || ag->klog > 6);
+    const bool direct_wide = direct && (int)(np.box[0] * 4) >= raw_below;
     static const bool dbg = getenv("TN_GATHER_DEBUG") != nullptr;
     if (dbg) {
       fprintf(stderr, "gather mlog %d klog %d: direct %d (inter %d KB %d nd %d box0 %u) raw %d (KB %d nd %d box0 %u)\n",
