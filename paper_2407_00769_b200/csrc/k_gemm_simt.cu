@@ -209,8 +209,10 @@ __global__ void __launch_bounds__(256) gemm_chalf_simt_kernel(__half2* __restric
 // rows in flight.
 template <int K, int N>
 struct RowsCfg {
-  static constexpr int kRptWant = N >= 8 ? 1 : 8 / N;
-  static constexpr int kRptRegs = 16 / K >= 1 ? 16 / K : 1;
+  // K <= 2 (outer-product-like, write-bound): >= 64 output bytes per thread; larger K: >= 32 bytes
+  // with <= 16 complex of A in registers (measured on C3: more rows per thread slowed K >= 4)
+  static constexpr int kRptWant = K <= 2 ? (N >= 16 ? 1 : 16 / N) : (N >= 8 ? 1 : 8 / N);
+  static constexpr int kRptRegs = K <= 2 ? 32 / K : (16 / K >= 1 ? 16 / K : 1);
   static constexpr int kRpt = kRptWant < kRptRegs ? kRptWant : kRptRegs;
 };
 
