@@ -96,6 +96,14 @@ __device__ __forceinline__ void tma_load_nd(void* dst, const CUtensorMap* map, u
                  ::"r"(d), "l"(m), "r"(c[0]), "r"(c[1]), "r"(b) : "memory");
 }
 
+__device__ __forceinline__ void tma_store_2d_hint(const CUtensorMap* map, const void* src, int c0, int c1,
+                                                  uint64_t policy) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%1, %2}], [%3], %4;" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1), "r"(smem_u32(src)), "l"(policy)
+               : "memory");
+}
+
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
                    reinterpret_cast<uint64_t>(map)),
@@ -641,7 +649,7 @@ __global__ void __launch_bounds__(kAMode == 1 ? kThreadsGather : kThreads, 1)
 #pragma unroll 1
       for (int sub = 0; sub < BN; sub += 64, ++gsub) {
         unsigned char* sbuf = sCg + (gsub % C::kNBuf) * (BM * 128);
-        if (!scat && !epi_stg) {
+        if (!scat && epi_stg != 1) {
           // ring slot free? (the TMA store that used it kNBuf subtiles ago has read it)
           if (etid == 0) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(C::kNBuf - 1) : "memory");
           named_bar(1 + grp, 128);
@@ -716,7 +724,7 @@ __global__ void __launch_bounds__(kAMode == 1 ? kThreadsGather : kThreads, 1)
             }
           }
         }
-        if (!scat && epi_stg) {
+        if (!scat && epi_stg == 1) {
           // coalesced stores from the staged subtile: 8 threads per 128-byte row segment, each warp
           // instruction writes 4 full lines (LSU path instead of the TMA store engine)
           named_bar(1 + grp, 128);
@@ -738,7 +746,13 @@ __global__ void __launch_bounds__(kAMode == 1 ? kThreadsGather : kThreads, 1)
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           named_bar(1 + grp, 128);
           if (etid == 0) {
-            tma_store_2d(&tmC, sbuf, n0 + sub, m0);
+            if (epi_stg == 2) {  // experiment: streaming output, evict-first in L2
+              uint64_t pol;
+              asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+              tma_store_2d_hint(&tmC, sbuf, n0 + sub, m0, pol);
+            } else {
+              tma_store_2d(&tmC, sbuf, n0 + sub, m0);
+            }
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
           }
         }
