@@ -649,7 +649,11 @@ __global__ void __launch_bounds__(kAMode == 1 ? kThreadsGather : kThreads, 1)
 #pragma unroll 1
       for (int sub = 0; sub < BN; sub += 64, ++gsub) {
         unsigned char* sbuf = sCg + (gsub % C::kNBuf) * (BM * 128);
-        if (!scat && epi_stg != 1) {
+        if (!scat && epi_stg == 3) {
+          // per-warp stores: this warp's 32 rows of the slot are free once its own store has read them
+          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(C::kNBuf - 1) : "memory");
+          __syncwarp();
+        } else if (!scat && epi_stg != 1) {
           // ring slot free? (the TMA store that used it kNBuf subtiles ago has read it)
           if (etid == 0) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(C::kNBuf - 1) : "memory");
           named_bar(1 + grp, 128);
@@ -742,6 +746,14 @@ __global__ void __launch_bounds__(kAMode == 1 ? kThreadsGather : kThreads, 1)
             }
           }
           named_bar(1 + grp, 128);  // the ring slot may be rewritten
+        } else if (!scat && epi_stg == 3) {
+          // experiment: each warp stores its own 32 x 64 box (no group barrier per subtile)
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&tmC, sbuf + ew * 32 * 128, n0 + sub, m0 + ew * 32);
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          }
         } else if (!scat) {
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           named_bar(1 + grp, 128);
@@ -758,7 +770,7 @@ __global__ void __launch_bounds__(kAMode == 1 ? kThreadsGather : kThreads, 1)
         }
       }
     }
-    if (etid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 #pragma unroll
     for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     if (out_max && lane == 0) atomicMax(out_max, __float_as_uint(mx));
@@ -932,7 +944,11 @@ static void launch_bn(__half* c, const __half* a, const __half* bp, uint64_t M, 
     for (int j = 0; j < 24; ++j) sa.ns[j] = om->ns[j];
   }
   CUtensorMap mb = make_map_2d(bp, K2, N2_real, KB, BN);  // rows >= 2N: TMA zero fill
-  static const int stg_env = getenv("TN_STG_EPI") ? atoi(getenv("TN_STG_EPI")) : 0;  // experiment knob
+  // output store mode: 0 = one 128-row TMA store per subtile after a group barrier.  Experiments
+  // (TN_STG_EPI): 1 = LSU stores from the staged subtile (slower); 2 = evict-first L2 hint (mixed);
+  // 3 = each warp stores its own 32 rows with no group barrier (3-4 % faster on standalone
+  // output-heavy GEMMs, but no net change over the C3 plan's N >= 2^8 steps: 23.84 -> 23.71 ms)
+  static const int stg_env = getenv("TN_STG_EPI") ? atoi(getenv("TN_STG_EPI")) : 0;
   const int epi_stg = stg_env;
   // TMA coordinates are int32: process M in chunks of at most 2^30 rows
   const uint32_t num_n = N2 / BN;
@@ -942,7 +958,7 @@ static void launch_bn(__half* c, const __half* a, const __half* bp, uint64_t M, 
     // (cp.async gather: the A map is unused; N-d: the whole stem, coordinates from the global row)
     CUtensorMap ma = np ? make_map_nd(a, *np) : make_map_2d(G ? a : a + m_off * K2, K2, G ? tc::BM : mm, KB, tc::BM);
     gargs.m_base = m_off;
-    CUtensorMap mc = make_map_2d(c + m_off * N2, N2, mm, 64, tc::BM);
+    CUtensorMap mc = make_map_2d(c + m_off * N2, N2, mm, 64, epi_stg == 3 ? 32 : tc::BM);
     // scatter: base of this chunk's rows in the OutMap; row-major: the chunk's first row (STG epilogue)
     uint32_t* out_sc = reinterpret_cast<uint32_t*>(c) + (sa.on ? outmap_m(*om, m_off) : m_off * (N2 / 2));
     uint32_t num_m = (uint32_t)((mm + tc::BM - 1) / tc::BM);

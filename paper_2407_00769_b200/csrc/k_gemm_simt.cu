@@ -239,7 +239,23 @@ __global__ void __launch_bounds__(256) gemm_chalf_rows_kernel(uint32_t* __restri
     const bool full = m0 + R <= M;
     float2 a[R * K];
     const __half2* ar = A + m0 * K;
-    if constexpr ((R * K) % 4 == 0) {
+    if constexpr ((R * K) % 8 == 0) {
+      if (full) {
+        // 256-bit loads: a lane's 32-byte piece is one full sector per instruction
+#pragma unroll
+        for (int q = 0; q < R * K / 8; ++q) {
+          uint32_t w[8];
+          asm volatile("ld.global.nc.L1::no_allocate.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                       : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7])
+                       : "l"(reinterpret_cast<const uint32_t*>(ar) + 8 * q));
+#pragma unroll
+          for (int j = 0; j < 8; ++j) a[8 * q + j] = __half22float2(*reinterpret_cast<__half2*>(&w[j]));
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < R * K; ++k) a[k] = (m0 + k / K < M) ? __half22float2(ar[k]) : make_float2(0.f, 0.f);
+      }
+    } else if constexpr ((R * K) % 4 == 0) {
       if (full) {
 #pragma unroll
         for (int q = 0; q < R * K / 4; ++q) {
