@@ -126,7 +126,8 @@ def test_gemm_chalf_exact_on_integers(env):
     assert np.array_equal(got[..., 0], ref.real) and np.array_equal(got[..., 1], ref.imag)
 
 
-@pytest.mark.parametrize("K,N", [(2, 4), (4, 64), (1, 8), (64, 2), (8, 1), (4, 1), (4, 4), (2, 64), (16, 4), (8, 16), (1, 1), (2, 32)])
+@pytest.mark.parametrize("K,N", [(2, 4), (4, 64), (1, 8), (64, 2), (8, 1), (4, 1), (4, 4), (2, 64), (16, 4), (8, 16), (1, 1), (2, 32),
+                                 (8, 4), (8, 8), (4, 32), (16, 8), (4, 8), (16, 2)])
 def test_gemm_chalf_simt_small_shapes(env, K, N):
     torch, tn = env
     rng = np.random.default_rng(K * 100 + N)
@@ -141,6 +142,25 @@ def test_gemm_chalf_simt_small_shapes(env, K, N):
     got = C.cpu().numpy().astype(np.float64).reshape(M, N, 2)
     ref = a @ b
     assert np.array_equal(got[..., 0] + 1j * got[..., 1], ref)
+
+
+@pytest.mark.parametrize("K,N,M", [(8, 8, 2_500_001), (8, 4, 2_000_003), (16, 4, 1_200_007), (4, 32, 600_001)])
+def test_gemm_chalf_rows_bulk_ring_wrap(env, K, N, M):
+    """Row-streaming steps with K >= 4 run the bulk-copy pipelined kernel: M large enough that every
+    CTA wraps its shared-memory ring several times, with a ragged last tile (and a partial row group
+    where a thread owns 2 rows); exact on small-integer operands."""
+    torch, tn = env
+    rng = np.random.default_rng(K * 1000 + N)
+    a = rng.integers(-3, 4, (M, K)) + 1j * rng.integers(-3, 4, (M, K))
+    b = rng.integers(-2, 3, (K, N)) + 1j * rng.integers(-2, 3, (K, N))
+    bp_km = np.transpose(embed.pad_b(b), (2, 0, 1, 3)).reshape(2 * N, 2 * K).astype(np.float16)
+    C = torch.full((M * 2 * N,), float("nan"), dtype=torch.float16, device="cuda")
+    tn.tn_gemm_chalf(C, torch.from_numpy(_half_pairs(a).reshape(-1)).cuda(),
+                     torch.from_numpy(bp_km.reshape(-1)).cuda(), M, K, N)
+    torch.cuda.synchronize()
+    got = C.cpu().numpy().astype(np.float64).reshape(M, N, 2)
+    ref = a @ b
+    assert np.array_equal(got[..., 0], ref.real) and np.array_equal(got[..., 1], ref.imag)
 
 
 def test_pad_b_and_scaled_gemm(env):
