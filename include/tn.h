@@ -83,7 +83,11 @@ typedef struct {
   int32_t no_gather;         /* 0 (default): a permutation before a tensor-core step whose two
                                 innermost modes are contracted is fused into the GEMM's A load
                                 (gathered cp.async, no permutation pass); 1: always a pass */
-  int32_t reserved[3];
+  int32_t no_fuse_swap_quant; /* 0 (default): a quantised mode swap whose sender permutation keeps
+                                the innermost log2(comm_group/2) modes in place quantises straight
+                                from the unpermuted stem (tn_permute_quant_f16, no permutation
+                                pass); 1: permutation pass, then the codec */
+  int32_t reserved[2];
 } tn_config;
 
 /* Caller-owned device buffers lent to a call (P:18-22 double buffering). */
@@ -220,6 +224,16 @@ TN_API int tn_quant_int8(int8_t* d_codes, float* d_scales, float* d_zeros, const
                   int g, void* stream);
 TN_API int tn_dequant_int8(float* d_y, const int8_t* d_codes, const float* d_scales, const float* d_zeros,
                     uint64_t n, int g, void* stream);
+/* Fused sender side of a quantised mode swap (north_star (5); Alg. 1 P:357-361 + Eq. 1
+ * P:389-406): the codec applied to Y = X.transpose(perm) without materialising Y.  X is a
+ * complex-half tensor of rank n (all dims 2, interleaved fp16 re/im, 2^(n+1) reals), perm follows
+ * tn_permute (output axis j = input axis perm[j], axis 0 outermost).  codec TN_COMM_INT8 writes
+ * 2^(n+1) int8 codes, TN_COMM_INT4 2^n packed bytes (tn_quant_int4_f16 layout); scales/zeros get
+ * 2^(n+1)/g floats.  Codes/scales/zeros are bit-identical to tn_permute then tn_quant_*_f16.
+ * Requires g a power of two >= 2 and perm keeping the innermost log2(g/2) axes in place
+ * (else TN_E_INVALID, nothing launched).  Device pointers; X must not alias the outputs. */
+TN_API int tn_permute_quant_f16(void* d_codes, float* d_scales, float* d_zeros, const void* d_x, int n,
+                                const int* perm, int g, int codec, void* stream);
 /* Same codec on fp16 reals (the complex-half mode-swap payload): the codec's input is the exact
  * float32 value of each fp16; dequantised values are rounded to fp16 (round to nearest even). */
 TN_API int tn_quant_int8_f16(int8_t* d_codes, float* d_scales, float* d_zeros, const void* d_x, uint64_t n,

@@ -97,8 +97,14 @@ void launch_pad_b(__half* bp, const float2* b, int klog, int nlog, const uint32_
 // complex64 -> complex-half with scale from max (entry of the stem)
 void launch_c64_to_chalf(__half2* dst, const float2* src, uint64_t n, const uint32_t* max_bits,
                          int* exp_slot, uint32_t* out_max_bits, cudaStream_t s);
+// fused mode-swap permutation for the codecs (k_quant.cu): nb < 0 = identity (groups in order)
+struct GroupPerm {
+  int nb = -1;      // group-index bits
+  int8_t sbit[48];  // source complex-bit position of group-index bit j
+};
+bool make_group_perm(GroupPerm& gp, int n, const int* perm, int g);
 void launch_quant_int4_half(uint8_t* packed, float* scales, float* zeros, const __half* x, uint64_t n, int g,
-                            cudaStream_t s);
+                            cudaStream_t s, const GroupPerm* gp = nullptr);
 void launch_dequant_int4_half(__half* y, const uint8_t* packed, const float* scales, const float* zeros, uint64_t n,
                               int g, cudaStream_t s);
 void launch_set_u64(uint64_t* p, uint64_t v, cudaStream_t s);
@@ -125,7 +131,7 @@ void launch_quant_int8(int8_t* codes, float* scales, float* zeros, const float* 
 void launch_dequant_int8(float* y, const int8_t* codes, const float* scales, const float* zeros,
                          uint64_t n, int g, cudaStream_t s);
 void launch_quant_int8_half(int8_t* codes, float* scales, float* zeros, const __half* x, uint64_t n, int g,
-                            cudaStream_t s);
+                            cudaStream_t s, const GroupPerm* gp = nullptr);
 void launch_dequant_int8_half(__half* y, const int8_t* codes, const float* scales, const float* zeros, uint64_t n,
                               int g, cudaStream_t s);
 

@@ -4,6 +4,7 @@
 // multiply then an fp32 add (no FMA) so codes are bit-identical to the oracle (oracle/codec.py);
 // constant groups: scale = 0, zero = the constant (C-A11).  One warp per group.
 #include <algorithm>
+#include <vector>
 
 #include "common.cuh"
 
@@ -14,13 +15,32 @@ __device__ __forceinline__ float to_f32(__half v) { return __half2float(v); }
 __device__ __forceinline__ void from_f32(float& d, float v) { d = v; }
 __device__ __forceinline__ void from_f32(__half& d, float v) { d = __float2half_rn(v); }
 
+// Sender-side fusion of the mode-swap permutation (north_star (5): "quantise/
+// dequantise fused into the permutation kernel").  When the permutation keeps the innermost
+// log2(g/2) complex modes in place, every quantisation group of the permuted (send) layout is a
+// contiguous run of g reals in the source, so the codec reads it straight from the unpermuted
+// stem: group gi of the output starts at complex offset sum_j bit_j(gi) 2^sbit[j].  The codes,
+// scales and zeros are bit-identical to permute-then-quantise (same values, same groups); the
+// permutation pass (8 bytes per complex-half element) disappears.  The 32 lanes of the warp that
+// owns a group each evaluate up to two index bits and OR-reduce them (the bits are distinct).
+__device__ __forceinline__ uint64_t group_base(uint64_t gi, int g, const GroupPerm& gp, int lane) {
+  if (gp.nb < 0) return gi * (uint64_t)g;
+  uint64_t c = 0;
+  if (lane < gp.nb && ((gi >> lane) & 1)) c = 1ull << gp.sbit[lane];
+  if (lane + 32 < gp.nb && ((gi >> (lane + 32)) & 1)) c |= 1ull << gp.sbit[lane + 32];
+  const uint32_t lo = __reduce_or_sync(0xffffffffu, (uint32_t)c);
+  const uint32_t hi = __reduce_or_sync(0xffffffffu, (uint32_t)(c >> 32));
+  return ((((uint64_t)hi << 32) | lo)) * 2;  // complex offset -> real offset
+}
+
 template <typename T>
 __global__ void quant_int8_kernel(int8_t* __restrict__ codes, float* __restrict__ scales, float* __restrict__ zeros,
-                                  const T* __restrict__ x, uint64_t n_groups, int g) {
+                                  const T* __restrict__ x, uint64_t n_groups, int g,
+                                  const __grid_constant__ GroupPerm gp) {
   const int lane = threadIdx.x & 31;
   const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
   for (uint64_t gi = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); gi < n_groups; gi += warps) {
-    const T* xs = x + gi * g;
+    const T* xs = x + group_base(gi, g, gp, lane);
     float mx = -INFINITY, mn = INFINITY;
     for (int i = lane; i < g; i += 32) {
       float v = to_f32(xs[i]);
@@ -77,7 +97,7 @@ void launch_quant_int8(int8_t* codes, float* scales, float* zeros, const float* 
   uint64_t blocks = (groups + 7) / 8;
   if (blocks > 148 * 16) blocks = 148 * 16;
   if (blocks == 0) return;
-  quant_int8_kernel<float><<<(unsigned)blocks, 256, 0, s>>>(codes, scales, zeros, x, groups, g);
+  quant_int8_kernel<float><<<(unsigned)blocks, 256, 0, s>>>(codes, scales, zeros, x, groups, g, GroupPerm{});
   TN_CUDA(cudaGetLastError());
 }
 
@@ -94,12 +114,12 @@ void launch_dequant_int8(float* y, const int8_t* codes, const float* scales, con
 // complex-half payload of a mode swap: the interleaved fp16 reals are the codec's input (their exact
 // float32 values), and the dequantised values are rounded back to fp16
 void launch_quant_int8_half(int8_t* codes, float* scales, float* zeros, const __half* x, uint64_t n, int g,
-                            cudaStream_t s) {
+                            cudaStream_t s, const GroupPerm* gp) {
   if (g <= 0 || n % g) throw TnError{TN_E_INVALID, "quant: n must be a multiple of the group size"};
   uint64_t groups = n / g;
   uint64_t blocks = std::min<uint64_t>((groups + 7) / 8, 148ull * 16);
   if (blocks == 0) return;
-  quant_int8_kernel<__half><<<(unsigned)blocks, 256, 0, s>>>(codes, scales, zeros, x, groups, g);
+  quant_int8_kernel<__half><<<(unsigned)blocks, 256, 0, s>>>(codes, scales, zeros, x, groups, g, gp ? *gp : GroupPerm{});
   TN_CUDA(cudaGetLastError());
 }
 
@@ -118,11 +138,11 @@ void launch_dequant_int8_half(__half* y, const int8_t* codes, const float* scale
 // constant, codes 0 (q_min).  One warp per group, each lane packs pairs of reals.
 __global__ void quant_int4_half_kernel(uint8_t* __restrict__ packed, float* __restrict__ scales,
                                        float* __restrict__ zeros, const __half* __restrict__ x, uint64_t n_groups,
-                                       int g) {
+                                       int g, const __grid_constant__ GroupPerm gp) {
   const int lane = threadIdx.x & 31;
   const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
   for (uint64_t gi = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); gi < n_groups; gi += warps) {
-    const __half* xs = x + gi * g;
+    const __half* xs = x + group_base(gi, g, gp, lane);
     float mx = -INFINITY, mn = INFINITY;
     for (int i = lane; i < g; i += 32) {
       float v = __half2float(xs[i]);
@@ -178,12 +198,12 @@ __global__ void dequant_int4_half_kernel(__half* __restrict__ y, const uint8_t* 
 }
 
 void launch_quant_int4_half(uint8_t* packed, float* scales, float* zeros, const __half* x, uint64_t n, int g,
-                            cudaStream_t s) {
+                            cudaStream_t s, const GroupPerm* gp) {
   if (g <= 0 || (g & 1) || n % g) throw TnError{TN_E_INVALID, "int4 quant: n must be a multiple of an even group size"};
   uint64_t groups = n / g;
   uint64_t blocks = std::min<uint64_t>((groups + 7) / 8, 148ull * 16);
   if (blocks == 0) return;
-  quant_int4_half_kernel<<<(unsigned)blocks, 256, 0, s>>>(packed, scales, zeros, x, groups, g);
+  quant_int4_half_kernel<<<(unsigned)blocks, 256, 0, s>>>(packed, scales, zeros, x, groups, g, gp ? *gp : GroupPerm{});
   TN_CUDA(cudaGetLastError());
 }
 
@@ -194,6 +214,24 @@ void launch_dequant_int4_half(__half* y, const uint8_t* packed, const float* sca
   if (blocks == 0) return;
   dequant_int4_half_kernel<<<(unsigned)blocks, 256, 0, s>>>(y, packed, scales, zeros, n, g);
   TN_CUDA(cudaGetLastError());
+}
+
+// Group permutation of a fused permute + quantise (see group_base): the permutation `perm` of a
+// rank-n complex tensor (output axis j = input axis perm[j], axis 0 outermost, the tn_permute
+// convention) fuses when it keeps the innermost log2(g/2) axes in place.  Returns false otherwise.
+bool make_group_perm(GroupPerm& gp, int n, const int* perm, int g) {
+  if (g < 2 || (g & (g - 1)) || n < 0 || n > 46) return false;
+  int b = 0;
+  while ((2 << b) < g) ++b;  // g/2 = 2^b complex elements per group
+  if (b > n) return false;
+  std::vector<int> p_of_q(n);  // destination bit q comes from source bit p_of_q[q]
+  for (int j = 0; j < n; ++j) p_of_q[n - 1 - j] = n - 1 - perm[j];
+  for (int q = 0; q < b; ++q)
+    if (p_of_q[q] != q) return false;
+  gp.nb = n - b;
+  if (gp.nb > 48) return false;
+  for (int j = 0; j < gp.nb; ++j) gp.sbit[j] = (int8_t)p_of_q[j + b];
+  return true;
 }
 
 }  // namespace tn

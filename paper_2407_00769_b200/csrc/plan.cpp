@@ -360,6 +360,14 @@ Plan* load_plan(const char* json, size_t len, const tn_config* cfg_in, int world
           if (snd != L) {
             st.send_perm = true;
             for (int l : snd) st.send_perm_axes.push_back((int)(std::find(L.begin(), L.end(), l) - L.begin()));
+            // the codec can read the unpermuted stem when each group (g/2 complex) stays contiguous
+            int gb = 0;
+            while (cfg.comm_group > 1 && (2 << gb) < cfg.comm_group) ++gb;
+            const int nl = (int)snd.size();
+            bool inner = st.quant && !cfg.no_fuse_swap_quant && gb <= nl &&
+                         (cfg.comm_group & (cfg.comm_group - 1)) == 0;
+            for (int q = 0; inner && q < gb; ++q) inner = st.send_perm_axes[nl - 1 - q] == nl - 1 - q;
+            st.fuse_quant = inner;
           }
           // after the exchange: the swapped-out shard modes become the outermost local modes
           std::vector<int> lay;
@@ -664,6 +672,7 @@ std::string report_json(const Plan& p, const std::vector<float>& ms) {
       << ",\"k\":" << s.klog << ",\"n\":" << s.nlog << ",\"perm\":" << (s.perm ? 1 : 0)
       << ",\"tc\":" << (s.tensor_core ? 1 : 0) << ",\"ga\":" << (s.gather_a ? 1 : 0) << ",\"split\":" << s.split << ",\"swap\":" << (s.swap ? 1 : 0)
       << ",\"quant\":" << (s.quant ? 1 : 0)
+      << ",\"fuse_quant\":" << (s.fuse_quant ? 1 : 0)
       << ",\"in\":";
     jlist(o, s.in_layout);
     o << ",\"R\":";

@@ -60,6 +60,7 @@ struct StemStep {
   std::vector<int> swap_in;       // local labels that become shard modes (same positions)
   bool send_perm = false;         // local permutation putting swap_in outermost before sending
   bool quant = false;             // this swap's payload is group-quantised (else fp16)
+  bool fuse_quant = false;        // quantised + send_perm keeps the innermost log2(g/2) modes: fused codec
   std::vector<int> send_perm_axes;
   std::vector<int> send_layout;   // local layout being sent (swap_in outermost)
 };

@@ -246,7 +246,12 @@ void check_buffers(const Plan& p, const tn_buffers* b) {
 void mode_swap(Plan& p, const StemStep& st, const tn_buffers* b, int& cur, cudaStream_t s) {
   if (!p.comm || !p.comm->nccl_comm) throw TnError{TN_E_NCCL, "sharded plan without an NCCL communicator"};
   const int eb = p.cfg.dtype == TN_CHALF ? 4 : 8;
-  if (st.send_perm) {
+  // quantised swaps read the unpermuted stem group by group when the permutation keeps the
+  // innermost log2(g/2) modes in place (k_quant.cu group_base): no separate permutation pass
+  GroupPerm gp;
+  const bool fused = st.fuse_quant &&
+                     make_group_perm(gp, (int)st.send_layout.size(), st.send_perm_axes.data(), p.cfg.comm_group);
+  if (st.send_perm && !fused) {
     launch_permute(b->d_stem[1 - cur], b->d_stem[cur], eb, (int)st.send_layout.size(), st.send_perm_axes.data(), s);
     ++p.launches;
     cur = 1 - cur;
@@ -285,9 +290,10 @@ void mode_swap(Plan& p, const StemStep& st, const tn_buffers* b, int& cur, cudaS
     auto zeros = [&](unsigned char* base) { return reinterpret_cast<float*>(base + codes_bytes + align_up(4 * ng, 256)); };
     if (int4)
       launch_quant_int4_half(reinterpret_cast<uint8_t*>(codes(Y)), scales(Y), zeros(Y), reinterpret_cast<const __half*>(X),
-                             reals, g, s);
+                             reals, g, s, fused ? &gp : nullptr);
     else
-      launch_quant_int8_half(codes(Y), scales(Y), zeros(Y), reinterpret_cast<const __half*>(X), reals, g, s);
+      launch_quant_int8_half(codes(Y), scales(Y), zeros(Y), reinterpret_cast<const __half*>(X), reals, g, s,
+                             fused ? &gp : nullptr);
     nccl_group(true);
     for (int v = 0; v < (1 << sx); ++v) {
       if (v == me) continue;
@@ -1023,6 +1029,26 @@ int tn_quant_int8_f16(int8_t* d_codes, float* d_scales, float* d_zeros, const vo
                       void* stream) {
   if (!d_codes || !d_scales || !d_zeros || !d_x) return fail(TN_E_INVALID, "NULL argument");
   TN_TRY(launch_quant_int8_half(d_codes, d_scales, d_zeros, (const __half*)d_x, n, g, (cudaStream_t)stream));
+}
+
+int tn_permute_quant_f16(void* d_codes, float* d_scales, float* d_zeros, const void* d_x, int n, const int* perm,
+                         int g, int codec, void* stream) {
+  if (!d_codes || !d_scales || !d_zeros || !d_x || !perm) return fail(TN_E_INVALID, "NULL argument");
+  if (codec != TN_COMM_INT8 && codec != TN_COMM_INT4) return fail(TN_E_INVALID, "codec must be int8 or int4");
+  TN_TRY({
+    GroupPerm gp;
+    if (n < 0 || n > 46) throw TnError{TN_E_INVALID, "permute_quant: rank out of range"};
+    std::vector<int> seen(n, 0);
+    for (int j = 0; j < n; ++j)
+      if (perm[j] < 0 || perm[j] >= n || seen[perm[j]]++) throw TnError{TN_E_INVALID, "permute_quant: not a permutation"};
+    if (!make_group_perm(gp, n, perm, g))
+      throw TnError{TN_E_INVALID, "permute_quant: g must be a power of two whose innermost log2(g/2) axes stay in place"};
+    const uint64_t reals = 2ull << n;
+    if (codec == TN_COMM_INT8)
+      launch_quant_int8_half((int8_t*)d_codes, d_scales, d_zeros, (const __half*)d_x, reals, g, (cudaStream_t)stream, &gp);
+    else
+      launch_quant_int4_half((uint8_t*)d_codes, d_scales, d_zeros, (const __half*)d_x, reals, g, (cudaStream_t)stream, &gp);
+  });
 }
 
 int tn_quant_int4_f16(uint8_t* d_packed, float* d_scales, float* d_zeros, const void* d_x, uint64_t n, int g,

@@ -28,7 +28,7 @@ class tn_config(C.Structure):
     _fields_ = [("dtype", C.c_int32), ("stem_min_log2", C.c_int32), ("comm_codec", C.c_int32),
                 ("comm_group", C.c_int32), ("stem_capacity_bytes", C.c_uint64), ("split_log2", C.c_int32),
                 ("layout_policy", C.c_int32), ("quant_from_pct", C.c_int32), ("virtual_world", C.c_int32),
-                ("no_gather", C.c_int32), ("reserved", C.c_int32 * 3)]
+                ("no_gather", C.c_int32), ("no_fuse_swap_quant", C.c_int32), ("reserved", C.c_int32 * 2)]
 
 
 class tn_buffers(C.Structure):
@@ -78,6 +78,7 @@ def lib():
         L.tn_quant_int8_f16.argtypes = [vp, vp, vp, vp, u64, i32, vp]
         L.tn_dequant_int8_f16.argtypes = [vp, vp, vp, vp, u64, i32, vp]
         L.tn_quant_int4_f16.argtypes = [vp, vp, vp, vp, u64, i32, vp]
+        L.tn_permute_quant_f16.argtypes = [vp, vp, vp, vp, i32, vp, i32, i32, vp]
         L.tn_dequant_int4_f16.argtypes = [vp, vp, vp, vp, u64, i32, vp]
         L.tn_comm_unique_id.argtypes = [vp]
         L.tn_comm_init.argtypes = [vp, i32, i32, i32, C.POINTER(vp)]
@@ -117,9 +118,10 @@ def _stream(stream):
 
 def make_config(dtype=TN_CHALF, stem_min_log2=20, comm_codec=TN_COMM_INT8, comm_group=128,
                 stem_capacity_bytes=0, split_log2=0, layout_policy=0, virtual_world=1, quant_from_pct=-1,
-                no_gather=0):
+                no_gather=0, no_fuse_swap_quant=0):
     c = tn_config()
     c.no_gather = no_gather
+    c.no_fuse_swap_quant = no_fuse_swap_quant
     c.layout_policy = layout_policy
     c.virtual_world = virtual_world  # host-only lowering for several ranks (no communicator)
     c.quant_from_pct = quant_from_pct
@@ -282,6 +284,14 @@ def tn_quant_int8_f16(codes, scales, zeros, x, g, stream=None):
 
 def tn_dequant_int8_f16(y, codes, scales, zeros, g, stream=None):
     _check(lib().tn_dequant_int8_f16(_ptr(y), _ptr(codes), _ptr(scales), _ptr(zeros), y.numel(), g, _stream(stream)))
+
+
+def tn_permute_quant_f16(codes, scales, zeros, x, perm, g, codec=TN_COMM_INT8, stream=None):
+    """x: complex-half stem as a tensor of 2^(n+1) fp16 reals; perm: tn_permute's axes."""
+    n = len(perm)
+    arr = (C.c_int * max(n, 1))(*perm)
+    _check(lib().tn_permute_quant_f16(_ptr(codes), _ptr(scales), _ptr(zeros), _ptr(x), n, arr, g, codec,
+                                      _stream(stream)))
 
 
 def tn_quant_int4_f16(packed, scales, zeros, x, g, stream=None):

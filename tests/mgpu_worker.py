@@ -42,9 +42,12 @@ def main():
         c2 = MP.sub_slice(json.load(f), 20)
     for codec, name, plan, pct, sm in ((tn.TN_COMM_FP16, "fp16", sub, -1, 14), (tn.TN_COMM_INT8, "int8", sub, -1, 14),
                                        (tn.TN_COMM_INT8, "int8_all_c2", c2, 0, 12),
+                                       (tn.TN_COMM_INT8, "int8_all_c3", sub, 0, 14),
+                                       (tn.TN_COMM_INT8, "int8_all_c3_unfused", sub, 0, 14),
                                        (tn.TN_COMM_INT4, "int4", sub, -1, 14),
                                        (tn.TN_COMM_INT4, "int4_late", sub, 30, 14)):
-        p = tn.Plan(plan, tn.make_config(stem_min_log2=sm, comm_codec=codec, quant_from_pct=pct), comm=comm)
+        p = tn.Plan(plan, tn.make_config(stem_min_log2=sm, comm_codec=codec, quant_from_pct=pct,
+                                         no_fuse_swap_quant=int(name.endswith("_unfused"))), comm=comm)
         b = tn.Buffers(p)
         amps = tn.contract(p, b, 0)
         torch.cuda.synchronize()
@@ -60,6 +63,12 @@ def main():
                    "rel_fp16_vs_1gpu_first": metrics.rel_l2(results["fp16"][0], one_first),
                    "rel_int8_all_c2_oracle": metrics.rel_l2(results["int8_all_c2"][0], ref2),
                    "int8_swaps_c2": sum(1 for s in results["int8_all_c2"][1]["steps"] if s.get("quant")),
+                   "fused_swaps_c3": sum(1 for s in results["int8_all_c3"][1]["steps"] if s.get("fuse_quant")),
+                   "fused_swaps_c3_unfused_run": sum(1 for s in results["int8_all_c3_unfused"][1]["steps"]
+                                                     if s.get("fuse_quant")),
+                   "rel_int8_all_c3_oracle": metrics.rel_l2(results["int8_all_c3"][0], ref),
+                   "rel_int8_c3_fused_vs_unfused": metrics.rel_l2(results["int8_all_c3"][0],
+                                                                  results["int8_all_c3_unfused"][0]),
                    "int8_swaps_c3": sum(1 for s in results["int8"][1]["steps"] if s.get("quant")),
                    "rel_fp16_oracle": metrics.rel_l2(results["fp16"][0], ref),
                    "rel_int8_oracle": metrics.rel_l2(results["int8"][0], ref),

@@ -378,3 +378,52 @@ def test_quant_int4_f16_payload_bit_exact(env):
     err = np.abs(y.cpu().numpy().astype(np.float64).reshape(-1, g) - xg)
     span = np.ptp(xg, axis=1)
     assert np.all(err.max(axis=1) <= span / 30 * (1 + 1e-5) + np.abs(xg).max(axis=1) * 2.0 ** -10)
+
+
+def _fusable_perm(rng, n, b):
+    """A random axis permutation of a rank-n tensor that keeps the innermost b axes in place."""
+    outer = [int(a) for a in rng.permutation(n - b)]
+    return outer + list(range(n - b, n))
+
+
+@pytest.mark.parametrize("n,g,codec_id,seed", [(10, 128, 1, 0), (13, 64, 1, 1), (12, 256, 1, 2), (9, 2, 1, 3),
+                                               (16, 128, 1, 4), (11, 128, 2, 5), (14, 32, 2, 6), (7, 128, 1, 7),
+                                               (20, 128, 1, 8), (18, 128, 2, 9)])
+def test_permute_quant_fused_bit_exact(env, n, g, codec_id, seed):
+    """Sender side of a quantised mode swap with the permutation fused into the codec (north_star
+    (5)): codes, scales and zeros of tn_permute_quant_f16 equal the oracle codec applied to the
+    numpy-transposed complex-half payload, bit for bit (int8 and packed int4)."""
+    torch, tn = env
+    rng = np.random.default_rng(seed)
+    b = (g // 2).bit_length() - 1
+    perm = _fusable_perm(rng, n, b)
+    x = (rng.standard_normal((1 << n, 2)) * 10.0 ** rng.uniform(-3, 3)).astype(np.float16)
+    x[: 1 << b] = 0.25                       # a constant group of the source (C-A11)
+    xt = x.reshape([2] * n + [2]).transpose(perm + [n]).reshape(-1)  # the permuted payload
+    X = torch.from_numpy(x.reshape(-1)).cuda()
+    reals = 2 << n
+    ncode = reals if codec_id == 1 else reals // 2
+    codes = torch.empty(ncode, dtype=torch.int8 if codec_id == 1 else torch.uint8, device="cuda")
+    sc = torch.empty(reals // g, dtype=torch.float32, device="cuda")
+    ze = torch.empty_like(sc)
+    tn.tn_permute_quant_f16(codes, sc, ze, X, perm, g, codec_id)
+    torch.cuda.synchronize()
+    lo, hi = (-128, 127) if codec_id == 1 else (0, 15)
+    rc, rs, rz = codec.quantize(xt.astype(np.float32), np.float32(lo), np.float32(hi), 1.0, group=g)
+    want = rc if codec_id == 1 else codec.pack_int4(rc)
+    got = codes.cpu().numpy()
+    assert np.array_equal(got.astype(np.float32) if codec_id == 1 else got, want)
+    assert np.array_equal(sc.cpu().numpy(), rs) and np.array_equal(ze.cpu().numpy(), rz)
+
+
+def test_permute_quant_rejects_unfusable(env):
+    """A permutation that moves one of the innermost log2(g/2) axes is refused (TN_E_INVALID)."""
+    torch, tn = env
+    n = 10
+    perm = list(range(n))
+    perm[-1], perm[0] = perm[0], perm[-1]
+    X = torch.zeros(2 << n, dtype=torch.float16, device="cuda")
+    codes = torch.empty(2 << n, dtype=torch.int8, device="cuda")
+    sc = torch.empty((2 << n) // 128, dtype=torch.float32, device="cuda")
+    with pytest.raises(Exception):
+        tn.tn_permute_quant_f16(codes, sc, sc.clone(), X, perm, 128)

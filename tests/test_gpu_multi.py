@@ -34,6 +34,10 @@ def test_sharded_stem_vs_oracle(world):
     assert v["rel_int8_oracle"] <= 5e-2
     assert v["rel_fp16_vs_1gpu"] == 0.0          # fp16 swaps: bit-identical to one GPU
     assert v["rel_int8_all_c2_oracle"] <= 5e-2
+    # permutation fused into the sender's codec (every swap quantised on the sub-sliced C3, one of
+    # them with a sender permutation at 2 and 4 GPUs): bit-identical to permutation pass + codec
+    assert v["fused_swaps_c3"] >= 1 and v["fused_swaps_c3_unfused_run"] == 0
+    assert v["rel_int8_c3_fused_vs_unfused"] == 0.0
     # int4 preset: late-stage swaps only; bound 0.2 (reading C-A30)
     assert v["rel_int4_oracle"] <= 0.2
     # (the sub-sliced C3's swaps sit at 15-47 % of the path: quant_from_pct = 30 quantises the last
