@@ -388,7 +388,8 @@ def _fusable_perm(rng, n, b):
 
 @pytest.mark.parametrize("n,g,codec_id,seed", [(10, 128, 1, 0), (13, 64, 1, 1), (12, 256, 1, 2), (9, 2, 1, 3),
                                                (16, 128, 1, 4), (11, 128, 2, 5), (14, 32, 2, 6), (7, 128, 1, 7),
-                                               (20, 128, 1, 8), (18, 128, 2, 9)])
+                                               (20, 128, 1, 8), (18, 128, 2, 9), (12, 512, 1, 10),
+                                               (13, 512, 2, 11), (15, 256, 2, 12)])
 def test_permute_quant_fused_bit_exact(env, n, g, codec_id, seed):
     """Sender side of a quantised mode swap with the permutation fused into the codec (north_star
     (5)): codes, scales and zeros of tn_permute_quant_f16 equal the oracle codec applied to the
