@@ -169,9 +169,18 @@ __global__ void __launch_bounds__(256) quant_vec_half_kernel(uint8_t* __restrict
       uint32_t q[16];
 #pragma unroll
       for (int e = 0; e < 16; ++e) {
-        float cc = qmin;
-        if (scale != 0.f) cc = fminf(fmaxf(rintf(__fadd_rn(__fmul_rn(f[e], scale), zero)), qmin), qmax);
-        q[e] = INT4 ? (uint32_t)cc : ((uint32_t)(int)cc & 0xffu);
+        // rint then clamp to [qmin, qmax] == round-to-nearest-even convert with saturation
+        // (cvt.rni.sat) for every finite value; int4 saturates to u8, then to 15
+        const float t = __fadd_rn(__fmul_rn(f[e], scale), zero);
+        uint32_t r;
+        if (INT4) {
+          asm("cvt.rni.sat.u8.f32 %0, %1;" : "=r"(r) : "f"(t));
+          r = min(r, 15u);
+        } else {
+          asm("cvt.rni.sat.s8.f32 %0, %1;" : "=r"(r) : "f"(t));
+          r &= 0xffu;
+        }
+        q[e] = scale != 0.f ? r : (INT4 ? 0u : 0x80u);
       }
       if (INT4) {
         uint2 w;
@@ -219,6 +228,62 @@ static bool launch_quant_vec_half(uint8_t* out, float* scales, float* zeros, con
   return true;
 }
 
+// Vectorised dequantisation for g = 128, 256 or 512: each thread expands 16 codes of one group (one
+// 16-byte int8 / 8-byte int4 load) into 16 fp16 reals (two 16-byte stores); y = (code - zero) /
+// scale per element, the IEEE division of the scalar kernels, so the outputs are identical.
+template <int G, bool INT4>
+__global__ void __launch_bounds__(256) dequant_vec_half_kernel(__half* __restrict__ y, const uint8_t* __restrict__ in,
+                                                               const float* __restrict__ scales,
+                                                               const float* __restrict__ zeros, uint64_t n16) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n16; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t gi = i / (G / 16);
+    const float sc = __ldg(scales + gi), z = __ldg(zeros + gi);
+    float c[16];
+    if (INT4) {
+      const uint2 w = __ldcs(reinterpret_cast<const uint2*>(in + i * 8));
+#pragma unroll
+      for (int e = 0; e < 8; ++e) c[e] = (float)((w.x >> (4 * e)) & 0xF);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) c[8 + e] = (float)((w.y >> (4 * e)) & 0xF);
+    } else {
+      const uint4 w = __ldcs(reinterpret_cast<const uint4*>(in + i * 16));
+      const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+      for (int e = 0; e < 16; ++e) c[e] = (float)(int8_t)((ws[e >> 2] >> (8 * (e & 3))) & 0xFF);
+    }
+    uint32_t o[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const float a = (sc == 0.f) ? z : __fdiv_rn(__fsub_rn(c[2 * e], z), sc);
+      const float b = (sc == 0.f) ? z : __fdiv_rn(__fsub_rn(c[2 * e + 1], z), sc);
+      const __half2 h = __halves2half2(__float2half_rn(a), __float2half_rn(b));
+      o[e] = *reinterpret_cast<const uint32_t*>(&h);
+    }
+    uint4* dst = reinterpret_cast<uint4*>(y + i * 16);
+    __stcs(dst, make_uint4(o[0], o[1], o[2], o[3]));
+    __stcs(dst + 1, make_uint4(o[4], o[5], o[6], o[7]));
+  }
+}
+
+template <bool INT4>
+static bool launch_dequant_vec_half(__half* y, const uint8_t* in, const float* scales, const float* zeros, uint64_t n,
+                                    int g, cudaStream_t s) {
+  if ((g != 128 && g != 256 && g != 512) || quant_scalar_knob() || (reinterpret_cast<uintptr_t>(y) & 15) ||
+      (reinterpret_cast<uintptr_t>(in) & 15))
+    return false;
+  const uint64_t n16 = n / 16;
+  const uint64_t blocks = std::min<uint64_t>((n16 + 255) / 256, 148ull * 8);
+  if (blocks == 0) return true;
+  if (g == 128)
+    dequant_vec_half_kernel<128, INT4><<<(unsigned)blocks, 256, 0, s>>>(y, in, scales, zeros, n16);
+  else if (g == 256)
+    dequant_vec_half_kernel<256, INT4><<<(unsigned)blocks, 256, 0, s>>>(y, in, scales, zeros, n16);
+  else
+    dequant_vec_half_kernel<512, INT4><<<(unsigned)blocks, 256, 0, s>>>(y, in, scales, zeros, n16);
+  TN_CUDA(cudaGetLastError());
+  return true;
+}
+
 void launch_quant_int8(int8_t* codes, float* scales, float* zeros, const float* x, uint64_t n, int g,
                        cudaStream_t s) {
   if (g <= 0 || n % g) throw TnError{TN_E_INVALID, "quant: n must be a multiple of the group size"};
@@ -258,6 +323,7 @@ void launch_quant_int8_half(int8_t* codes, float* scales, float* zeros, const __
 void launch_dequant_int8_half(__half* y, const int8_t* codes, const float* scales, const float* zeros, uint64_t n,
                               int g, cudaStream_t s) {
   if (g <= 0 || n % g) throw TnError{TN_E_INVALID, "dequant: n must be a multiple of the group size"};
+  if (launch_dequant_vec_half<false>(y, reinterpret_cast<const uint8_t*>(codes), scales, zeros, n, g, s)) return;
   uint64_t blocks = std::min<uint64_t>((n + 255) / 256, 148ull * 16);
   if (blocks == 0) return;
   dequant_int8_kernel<__half><<<(unsigned)blocks, 256, 0, s>>>(y, codes, scales, zeros, n, g);
@@ -344,6 +410,7 @@ void launch_quant_int4_half(uint8_t* packed, float* scales, float* zeros, const 
 void launch_dequant_int4_half(__half* y, const uint8_t* packed, const float* scales, const float* zeros, uint64_t n,
                               int g, cudaStream_t s) {
   if (g <= 0 || (g & 1) || n % g) throw TnError{TN_E_INVALID, "int4 dequant: n must be a multiple of an even group size"};
+  if (launch_dequant_vec_half<true>(y, packed, scales, zeros, n, g, s)) return;
   uint64_t blocks = std::min<uint64_t>((n / 2 + 255) / 256, 148ull * 16);
   if (blocks == 0) return;
   dequant_int4_half_kernel<<<(unsigned)blocks, 256, 0, s>>>(y, packed, scales, zeros, n, g);

@@ -43,7 +43,12 @@ def main():
         tn.tn_permute(y.view(torch.complex32), x.view(torch.complex32), perm)
         tn.tn_quant_int8_f16(codes, sc, ze, y, g)
 
-    tf, ts = run(fused), run(separate)
+    def deq():
+        tn.tn_dequant_int8_f16(y, codes, sc, ze, g)
+
+    tf, ts, td = run(fused), run(separate), run(deq)
+    dalg = (2 << n) + 8 * ((2 << n) // g) + (4 << n)
+    print(f"dequant int8 -> complex-half: {td:.3f} ms ({dalg / td / 1e6:.0f} GB/s algorithmic)")
     print(f"n={n} ({(4 << n) / 2**30:.1f} GiB stem): fused {tf:.3f} ms ({alg / tf / 1e6:.0f} GB/s algorithmic), "
           f"permute+quant {ts:.3f} ms, speed-up {ts / tf:.2f}x")
 
