@@ -115,9 +115,10 @@ struct Plan {
   int n_swaps = 0;
   double swap_bytes = 0;          // payload bytes each rank sends per slice (codec applied)
   tn_comm* comm = nullptr;
-  // CUDA graph of the whole tn_stem_contract body (world == 1): captured once per buffer set on a
+  // CUDA graph of the whole tn_stem_contract body (world == 1; sharded: the head, or all with TN_GRAPH_NCCL=1): captured once per buffer set on a
   // library stream, replayed on the caller's stream.  Opaque CUDA handles as void*.
   void* graph_exec = nullptr;
+  bool nccl_warm = false;  // sharded: one eager call done (NCCL connections exist) before capture
   void* cap_stream = nullptr;
   const void* graph_key[4] = {nullptr, nullptr, nullptr, nullptr};
   uint64_t graph_stem_bytes = 0;

@@ -488,6 +488,16 @@ bool graph_wanted(const Plan& p) {
   return !env_off && !p.graph_off;
 }
 
+// Sharded plans keep only the collective-free head in the graph; TN_GRAPH_NCCL=1 (experiment knob)
+// captures the whole subtask, NCCL swaps and max all-reduces included (stream-capturable once
+// NCCL's connections exist, so the first call runs eagerly).  Measured slower on C3 at 2 GPUs
+// (59.2 vs 55.6 ms/subtask), hence off.
+bool graph_whole(const Plan& p) {
+  static const char* e = getenv("TN_GRAPH_NCCL");
+  static const bool on = e != nullptr && atoi(e) != 0;
+  return p.world == 1 || on;
+}
+
 // Capture stem_body on the library stream and instantiate it (once per buffer set).
 void capture_stem(Plan& p, const tn_buffers* b) {
   if (!p.cap_stream) {
@@ -503,7 +513,7 @@ void capture_stem(Plan& p, const tn_buffers* b) {
   p.launches = 0;
   TN_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
   try {
-    stem_body(p, b, cs, true, p.world == 1);  // sharded: the collective-free head only
+    stem_body(p, b, cs, true, graph_whole(p));  // else (sharded): the collective-free head only
   } catch (...) {
     cudaGraph_t junk = nullptr;
     cudaStreamEndCapture(cs, &junk);
@@ -549,10 +559,18 @@ void stem_contract(Plan& p, const tn_buffers* b, uint64_t slice_id, cudaStream_t
   if (graph_wanted(p)) {
     const bool same = p.graph_exec && p.graph_key[0] == b->d_ws && p.graph_key[1] == b->d_stem[0] &&
                       p.graph_key[2] == b->d_stem[1] && p.graph_stem_bytes == b->stem_bytes && p.graph_timing == p.timing;
+    if (!same && p.world > 1 && graph_whole(p) && !p.nccl_warm) {
+      // first sharded call: eager, so NCCL sets up its peer connections outside any capture
+      p.launches = 0;
+      stem_body(p, b, s);
+      p.launches += 1;
+      p.nccl_warm = true;
+      return;
+    }
     if (!same) capture_stem(p, b);
     TN_CUDA(cudaGraphLaunch((cudaGraphExec_t)p.graph_exec, s));
     p.launches = p.graph_launches + 1;
-    if (p.world > 1) {  // the tail (swaps, GEMMs) eagerly on the caller's stream
+    if (p.world > 1 && !graph_whole(p)) {  // the tail (swaps, GEMMs) eagerly on the caller's stream
       stem_body(p, b, s, false, true);
       return;
     }
