@@ -167,3 +167,34 @@ def test_fused_permutation_lowering(tnmod, name):
         assert lay[-1] in R and lay[-2] in R
         kept = [l for l in lay if l not in R]
         assert s["out"][:len(kept)] == kept              # kept modes in stored order, then new modes
+
+
+@pytest.mark.parametrize("world,g", [(8, 128), (4, 32), (2, 8)])
+def test_fused_swap_codec_lowering(tnmod, world, g):
+    """Sender permutation folded into the swap codec (north_star (5)): a swap is marked fuse_quant
+    exactly when it is quantised, needs a sender permutation, and that permutation keeps the
+    innermost log2(g/2) local modes in place (so every codec group is contiguous in the unpermuted
+    stem).  The pre-swap local layout is the previous step's output layout.  no_fuse_swap_quant=1
+    clears every mark and changes nothing else in the lowering."""
+    from workload import make_plans as MP
+    with open(os.path.join(ROOT, "plans", "c3.json")) as f:
+        plan = MP.sub_slice(json.load(f), 22)
+    b = (g // 2).bit_length() - 1
+    kw = dict(stem_min_log2=14, virtual_world=world, quant_from_pct=0, comm_group=g)
+    rf = tnmod.Plan(plan, tnmod.make_config(**kw)).report()["steps"]
+    ru = tnmod.Plan(plan, tnmod.make_config(no_fuse_swap_quant=1, **kw)).report()["steps"]
+    n_fused = 0
+    for i, s in enumerate(rf):
+        if not s["swap"] or i == 0:
+            assert not s["fuse_quant"]
+            continue
+        snd = s["send_layout"]
+        pre = [l for l in rf[i - 1]["out"] if l in snd]          # local modes, stored order
+        assert sorted(pre) == sorted(snd)
+        want = bool(s["quant"]) and pre != snd and pre[len(pre) - b:] == snd[len(snd) - b:]
+        assert bool(s["fuse_quant"]) == want, (i, s["quant"], pre[-b:], snd[-b:])
+        n_fused += want
+    assert n_fused >= 1
+    assert all(not s["fuse_quant"] for s in ru)
+    strip = lambda st: [{k: v for k, v in s.items() if k != "fuse_quant"} for s in st]  # noqa: E731
+    assert strip(rf) == strip(ru)
