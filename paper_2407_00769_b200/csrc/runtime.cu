@@ -490,8 +490,8 @@ bool graph_wanted(const Plan& p) {
 
 // Sharded plans keep only the collective-free head in the graph; TN_GRAPH_NCCL=1 (experiment knob)
 // captures the whole subtask, NCCL swaps and max all-reduces included (stream-capturable once
-// NCCL's connections exist, so the first call runs eagerly).  Measured slower on C3 at 2 GPUs
-// (59.2 vs 55.6 ms/subtask), hence off.
+// NCCL's connections exist, so the first call runs eagerly).  Measured slower on C3 (2 GPUs: 59.2
+// vs 55.6 ms/subtask; 4 GPUs: 41.6 vs 34.0), hence off.
 bool graph_whole(const Plan& p) {
   static const char* e = getenv("TN_GRAPH_NCCL");
   static const bool on = e != nullptr && atoi(e) != 0;
