@@ -68,8 +68,15 @@ typedef struct {
   int32_t comm_codec;        /* TN_COMM_* for sharded mode swaps (ignored at world size 1) */
   int32_t comm_group;        /* quantisation group in reals (int8/int4), e.g. 128 */
   uint64_t stem_capacity_bytes; /* bytes of EACH stem buffer the caller will lend; 0 = no check */
-  int32_t split_log2;        /* split-type tail: 2^split_log2 chunks; -1 = auto
-                                (smallest power of two that fits), 0 = no split */
+  int32_t split_log2;        /* split-type tail: 2^split_log2 chunks, each fixing
+                                split_log2 open legs that stay the outermost local modes of the
+                                tail (never shard modes; a sharded stem chunks every rank's shard,
+                                and a mode swap inside the tail is TN_E_INFEASIBLE).  0 = no split.
+                                -1 = auto, "determined by the current remaining capacity"
+                                (reading C-A19): the smallest power of two whose lowering fits
+                                stem_capacity_bytes (capacity 0: no split); tn_plan_load returns
+                                TN_E_CAPACITY when no chunk count fits.  tn_plan_info.split_chunks
+                                reports the count chosen. */
   int32_t layout_policy;     /* 0 (default): output = kept ++ new (TMA-store epilogue) plus a
                                 permutation pass when the next step's modes are not innermost;
                                 2: each GEMM writes its output with the next step's contracted
@@ -162,7 +169,11 @@ TN_API int tn_split_contract(tn_plan* p, const tn_buffers* b, void* stream);
  * correlated subspace = one value of the j split legs (bit j-1-t of the prefix <-> the t-th entry of
  * "split_modes" in tn_report_json); only those chunks of the tail are contracted.  h_amps receives
  * n_sub blocks of 2^(n_open-j) amplitudes (members = the other open legs in plan order); top_idx
- * receives n_sub*k member indices, k = 1 computed on the device (post-selection). */
+ * receives n_sub*k member indices (post-selection; one rank: k = 1 on the device).
+ * Sharded plans: every rank calls it (collective: the result blocks are gathered in rank order into
+ * the workspace) and every rank receives the whole result.  Ties in top_idx always go to the smaller
+ * member index in member order, whatever the storage layout (C-A23); NaN probabilities rank lowest.
+ * Errors: TN_E_INVALID (k < 0, prefix >= 2^j), TN_E_UNSUPPORTED (prefixes without a split tail). */
 TN_API int tn_sample_amplitudes(tn_plan* p, const tn_buffers* b, const uint64_t* prefixes, size_t n_sub,
                          double* h_amps, int k, uint64_t* top_idx, void* stream);
 
@@ -252,6 +263,16 @@ TN_API int tn_dequant_int4_f16(void* d_y, const uint8_t* d_packed, const float* 
 /* ---- multi-GPU (stem sharded on its log2(world) outermost modes, Alg. 1) ---- */
 TN_API int tn_comm_unique_id(uint8_t out[128]);
 TN_API int tn_comm_init(const uint8_t uid[128], int rank, int world, int device, tn_comm** out);
+/* Loopback transport (testing and schedule validation on one GPU): `world` virtual ranks that all
+ * live on `device`.  out[r] (caller array of `world` pointers) receives rank r's communicator; each
+ * is passed to its own tn_plan_load and freed with tn_comm_free.  Every collective of the sharded
+ * path (mode-swap exchanges, the per-step max all-reduce, the readout all-gather) becomes a host
+ * rendezvous of the virtual ranks plus device-to-device copies ordered by CUDA events, so the same
+ * lowering, codec kernels and swap schedule run as with NCCL.  Each virtual rank's plan must be
+ * driven from its OWN host thread (a rendezvous blocks until every rank arrives; it fails with
+ * TN_E_NCCL after 600 s).  Each rank needs its own buffers; the stem shards are 1/world of the stem,
+ * so world virtual ranks fit wherever one rank holding the whole stem fits. */
+TN_API int tn_comm_init_loopback(int world, int device, tn_comm** out);
 TN_API void tn_comm_free(tn_comm* c);
 
 #ifdef __cplusplus

@@ -48,44 +48,43 @@ def group_params(xp, qmin, qmax):
 
 
 def quantize(x, qmin, qmax, exp=1.0, group=None, round_=True):
-    """x: flat float32 array.  Returns (codes float32 array, scales, zeros) per group."""
+    """x: flat float32 array.  Returns (codes float32 array, scales, zeros) per group.
+    Groups are the rows of x reshaped to [n_groups, g]; every step is elementwise float32 in the
+    order of Eq. 1 (max/min per row, then scale, zero, multiply, add, round, clip)."""
     x = np.asarray(x, dtype=F32).reshape(-1)
     g = x.size if group is None else group
     if x.size % g:
         raise ValueError("group size must divide the tensor")
-    xp = _signed_pow(x, exp)
-    ng = x.size // g
-    codes = np.empty_like(xp)
-    scales = np.empty(ng, dtype=F32)
-    zeros = np.empty(ng, dtype=F32)
-    for i in range(ng):
-        seg = xp[i * g:(i + 1) * g]
-        s, z = group_params(seg, qmin, qmax)
-        if s == 0:                         # degenerate group (C-A11)
-            v = np.full_like(seg, qmin)
-        else:
-            v = (seg * s).astype(F32)      # fp32 multiply (rounded)
-            v = (v + z).astype(F32)        # then fp32 add (rounded); no FMA (C-A13)
-            if round_:
-                v = np.rint(v)             # round half to even
-        codes[i * g:(i + 1) * g] = np.clip(v, qmin, qmax)
-        scales[i] = s
-        zeros[i] = z
+    xp = _signed_pow(x, exp).reshape(-1, g)
+    mx = xp.max(axis=1).astype(F32)
+    mn = xp.min(axis=1).astype(F32)
+    const = mx == mn                                   # degenerate groups (C-A11)
+    den = np.where(const, F32(1.0), (mx - mn).astype(F32)).astype(F32)
+    scales = (F32(qmax - qmin) / den).astype(F32)
+    zeros = ((F32(qmin) * mx).astype(F32) - (F32(qmax) * mn).astype(F32)).astype(F32)
+    zeros = (zeros / den).astype(F32)
+    scales = np.where(const, F32(0.0), scales).astype(F32)
+    zeros = np.where(const, mx, zeros).astype(F32)
+    v = (xp * scales[:, None]).astype(F32)             # fp32 multiply (rounded)
+    v = (v + zeros[:, None]).astype(F32)               # then fp32 add (rounded); no FMA (C-A13)
+    if round_:
+        v = np.rint(v)                                 # round half to even
+    v = np.where(const[:, None], F32(qmin), v)
+    codes = np.clip(v, qmin, qmax).astype(F32).reshape(-1)
     return codes, scales, zeros
 
 
 def dequantize(codes, scales, zeros, exp=1.0, group=None):
     codes = np.asarray(codes, dtype=F32).reshape(-1)
     g = codes.size if group is None else group
-    out = np.empty_like(codes)
-    for i in range(codes.size // g):
-        seg = codes[i * g:(i + 1) * g]
-        if scales[i] == 0:                 # degenerate group (C-A11)
-            y = np.full_like(seg, zeros[i])
-        else:
-            y = ((seg - zeros[i]).astype(F32) / scales[i]).astype(F32)
-        out[i * g:(i + 1) * g] = _signed_pow(y, 1.0 / exp)
-    return out
+    c = codes.reshape(-1, g)
+    scales = np.asarray(scales, dtype=F32)
+    zeros = np.asarray(zeros, dtype=F32)
+    const = scales == 0                                # degenerate group (C-A11)
+    den = np.where(const, F32(1.0), scales).astype(F32)
+    y = ((c - zeros[:, None]).astype(F32) / den[:, None]).astype(F32)
+    y = np.where(const[:, None], zeros[:, None], y).astype(F32)
+    return _signed_pow(y.reshape(-1), 1.0 / exp)
 
 
 def pack_int4(codes):

@@ -41,11 +41,14 @@ def contract_pair(a, b):
     return out, np.tensordot(ta, tb, axes=(ia, ib))
 
 
-def contract(plan, slice_id: int = 0, record=None):
+def contract(plan, slice_id: int = 0, record=None, override=None):
     """Partial amplitudes a_s over the open legs (array with shape (2,)*len(open)).
 
     ``record``: optional dict; if given, record[node_id] = (labels, tensor) for every node id in
-    it on entry (used to compare stem intermediates by label, not by layout)."""
+    it on entry (used to compare stem intermediates by label, not by layout).
+    ``override``: optional dict node_id -> (labels, tensor) replacing that node's value as soon as
+    it is formed (the contraction is linear in every node, so overriding a stem node with a
+    perturbation e yields the perturbation's image at the root; used to propagate swap errors)."""
     if not isinstance(plan, Plan):
         plan = load(plan)
     nodes = slice_leaves(plan, slice_id)
@@ -57,6 +60,11 @@ def contract(plan, slice_id: int = 0, record=None):
         raise ValueError("hyper-edges are not part of the RQC network")
     for u, v in plan.tree:
         nodes.append(contract_pair(nodes[u], nodes[v]))
+        if override is not None and len(nodes) - 1 in override:
+            lab, t = override[len(nodes) - 1]
+            if sorted(lab) != sorted(nodes[-1][0]) or t.shape != nodes[-1][1].shape:
+                raise ValueError("override must carry the node's labels and shape")
+            nodes[-1] = (list(lab), t)
         if record is not None and len(nodes) - 1 in record:
             record[len(nodes) - 1] = nodes[-1]
     labels, t = nodes[-1]

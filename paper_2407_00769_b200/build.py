@@ -24,6 +24,16 @@ def _stale():
     return os.path.getmtime(hdr) > t
 
 
+def _obj_stale(src, obj):
+    """An object is rebuilt when its source or any header (csrc/*.cuh, *.hpp, include/tn.h) is newer."""
+    if not os.path.exists(obj):
+        return True
+    t = os.path.getmtime(obj)
+    hdrs = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".hpp", ".h"))]
+    hdrs.append(os.path.join(os.path.dirname(HERE), "include", "tn.h"))
+    return any(os.path.getmtime(f) > t for f in [src] + hdrs)
+
+
 def build(force=False, verbose=False):
     if not force and not _stale():
         return OUT
@@ -33,11 +43,13 @@ def build(force=False, verbose=False):
     for s in SOURCES:
         src = os.path.join(CSRC, s)
         obj = os.path.join(HERE, "build", s + ".o")
+        objs.append(obj)
+        if not force and not _obj_stale(src, obj):
+            continue
         cmd = [NVCC] + FLAGS + ["-c", src, "-o", obj]
         if s.endswith(".cpp"):
             cmd = [NVCC] + FLAGS + ["-x", "cu", "-c", src, "-o", obj]
         procs.append((s, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
-        objs.append(obj)
     for s, p in procs:
         out, _ = p.communicate()
         if verbose or p.returncode:

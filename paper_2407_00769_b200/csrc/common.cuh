@@ -108,6 +108,11 @@ void launch_quant_int4_half(uint8_t* packed, float* scales, float* zeros, const 
 void launch_dequant_int4_half(__half* y, const uint8_t* packed, const float* scales, const float* zeros, uint64_t n,
                               int g, cudaStream_t s);
 void launch_set_u64(uint64_t* p, uint64_t v, cudaStream_t s);
+struct MaxSlots {
+  int n;
+  const float* p[8];
+};
+void launch_max_slots(float* dst, const MaxSlots& src, cudaStream_t s);
 void launch_copy_c64(float2* dst, const float2* src, uint64_t n, cudaStream_t s);
 void launch_gemm_c64(float2* c, const float2* a, const float2* b, uint64_t M, uint32_t K, uint32_t N,
                      const OutMap* om, cudaStream_t s);
@@ -125,7 +130,14 @@ void launch_gemm_chalf_tc(__half* c, const __half* a, const __half* bp, uint64_t
                           uint32_t N2, const float* in_max, const float* b_bound, uint32_t* out_max,
                           int* exp_slot, const OutMap* om, cudaStream_t s, const AGather* ag = nullptr);
 OutMap identity_map(uint64_t M, uint32_t N);
-void launch_top1_chalf(const __half2* amps, uint64_t n_sub, uint64_t members, uint64_t* top, cudaStream_t s);
+// member (open-leg order) index of a stored amplitude: bit (r-1-t) of the member index is bit
+// src_bit[t] of the layout index
+struct MemberMap {
+  int r;
+  int8_t src_bit[64];
+};
+void launch_top1_chalf(const __half2* amps, uint64_t n_sub, uint64_t members, const MemberMap& mm, uint64_t* top,
+                       cudaStream_t s);
 void launch_quant_int8(int8_t* codes, float* scales, float* zeros, const float* x, uint64_t n, int g,
                        cudaStream_t s);
 void launch_dequant_int8(float* y, const int8_t* codes, const float* scales, const float* zeros,

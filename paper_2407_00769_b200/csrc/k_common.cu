@@ -187,6 +187,20 @@ void launch_set_u64(uint64_t* p, uint64_t v, cudaStream_t s) {
   TN_CUDA(cudaGetLastError());
 }
 
+// Loopback transport (runtime.cu): max over the virtual ranks' 1-float slots, written to `dst`.
+// The slots hold non-negative float bits (atomicMax order); a concurrent reader of `dst` sees its
+// old value or the maximum, both valid bounds for every rank.
+__global__ void max_slots_kernel(float* dst, MaxSlots src) {
+  float m = 0.f;
+  for (int r = 0; r < src.n; ++r) m = fmaxf(m, *src.p[r]);
+  *dst = m;
+}
+
+void launch_max_slots(float* dst, const MaxSlots& src, cudaStream_t s) {
+  max_slots_kernel<<<1, 1, 0, s>>>(dst, src);
+  TN_CUDA(cudaGetLastError());
+}
+
 void launch_copy_c64(float2* dst, const float2* src, uint64_t n, cudaStream_t s) {
   TN_CUDA(cudaMemcpyAsync(dst, src, n * sizeof(float2), cudaMemcpyDeviceToDevice, s));
 }

@@ -39,7 +39,54 @@ static std::vector<int> int_list(const tnjson::Value* v, const char* what) {
   return out;
 }
 
+static Plan* load_plan_fixed(const char* json, size_t len, const tn_config* cfg_in, int world, int split_min = -1);
+
+// A split tail on a sharded stem must start after the last mode swap (each rank chunks its own
+// shard; a swap would need every chunk of every rank).  The swap schedule does not depend on where
+// the tail starts, so a lowering whose tail would contain a swap is redone with the tail starting
+// right after it.
+static Plan* load_plan_split(const char* json, size_t len, const tn_config* cfg, int world) {
+  int split_min = -1;
+  for (int pass = 0; pass < 64; ++pass) {
+    try {
+      return load_plan_fixed(json, len, cfg, world, split_min);
+    } catch (const TnError& e) {
+      const std::string key = "split-retry:";
+      if (e.msg.compare(0, key.size(), key) != 0) throw;
+      const int s = std::stoi(e.msg.substr(key.size()));
+      if (s <= split_min) throw err(TN_E_INFEASIBLE, "split: cannot place the tail after the mode swaps");
+      split_min = s;
+    }
+  }
+  throw err(TN_E_INFEASIBLE, "split: cannot place the tail after the mode swaps");
+}
+
+// cfg.split_log2 = -1 (auto): "the number of chunks is determined by the current remaining
+// capacity of the GPU memory" (reading C-A19: the smallest power of two that fits).  The lowering is
+// tried with j = 0, 1, 2, ... split legs; the first whose buffers fit stem_capacity_bytes wins.
+// Without a capacity (0) there is nothing to fit: no split.
 Plan* load_plan(const char* json, size_t len, const tn_config* cfg_in, int world) {
+  if (!cfg_in || cfg_in->split_log2 >= 0) return load_plan_split(json, len, cfg_in, world);
+  tn_config c = *cfg_in;
+  if (c.stem_capacity_bytes == 0) {
+    c.split_log2 = 0;
+    return load_plan_split(json, len, &c, world);
+  }
+  std::string last = "no split count fits";
+  for (int j = 0; j <= 16; ++j) {
+    c.split_log2 = j;
+    try {
+      return load_plan_split(json, len, &c, world);
+    } catch (const TnError& e) {
+      if (e.code != TN_E_INFEASIBLE) throw;
+      last = e.msg;
+      if (e.msg.find("fewer open legs") != std::string::npos) break;
+    }
+  }
+  throw err(TN_E_CAPACITY, "split auto: no power-of-two chunk count fits stem_capacity_bytes (" + last + ")");
+}
+
+static Plan* load_plan_fixed(const char* json, size_t len, const tn_config* cfg_in, int world, int split_min) {
   tnjson::Value root;
   try {
     root = tnjson::parse(json, len);
@@ -233,7 +280,6 @@ Plan* load_plan(const char* json, size_t len, const tn_config* cfg_in, int world
   // the open legs that enter the stem earliest (longest tail); they sort outermost in every layout.
   std::set<int> split_set;
   if (cfg.split_log2 > 0 && entry_idx >= 0) {
-    if (world > 1) throw err(TN_E_UNSUPPORTED, "split-type tail with a sharded stem");
     std::map<int, int> first_app;  // open leg -> first stem step whose INPUT holds it
     for (int l : p.nodes[p.stem_entry].labels) first_app[l] = 0;
     {
@@ -254,6 +300,7 @@ Plan* load_plan(const char* json, size_t len, const tn_config* cfg_in, int world
       p.split_modes.push_back(cand[t]);
       p.split_from = std::max(p.split_from, first_app[cand[t]]);
     }
+    p.split_from = std::max(p.split_from, split_min);
     p.split_log2 = cfg.split_log2;
     if (p.split_from >= (int)step_nodes.size()) throw err(TN_E_INFEASIBLE, "split: no tail step holds the split modes");
   }
@@ -272,7 +319,7 @@ Plan* load_plan(const char* json, size_t len, const tn_config* cfg_in, int world
   // public numbering: 0 = permutation passes (default, fastest measured), 1 = hybrid, 2 = scatter
   const int policy = cfg.layout_policy == 0 ? 1 : (cfg.layout_policy == 1 ? 0 : cfg.layout_policy);
   const int eb = (cfg.dtype == TN_CHALF) ? 4 : 8;
-  uint64_t smax = 0;
+  uint64_t smax = 0, payload_bytes = 0;
   if (entry_idx >= 0) {
     // branch label sets and contracted sets R_s (stem ∩ branch) along the stem
     std::vector<std::set<int>> Rsets(step_nodes.size());
@@ -308,7 +355,10 @@ Plan* load_plan(const char* json, size_t len, const tn_config* cfg_in, int world
     std::vector<int> shard;
     if (p.shard_log2 > 0) {
       Node& e = p.nodes[p.stem_entry];
-      std::vector<int> cand = e.labels;
+      // split modes must stay local (each rank chunks its own shard of the tail): never shard them
+      std::vector<int> cand;
+      for (int l : e.labels)
+        if (!split_set.count(l)) cand.push_back(l);
       std::stable_sort(cand.begin(), cand.end(), [&](int a, int b) { return nu(a) > nu(b); });
       if ((int)cand.size() <= p.shard_log2) throw err(TN_E_INFEASIBLE, "stem entry has too few modes to shard");
       shard.assign(cand.begin(), cand.begin() + p.shard_log2);
@@ -340,7 +390,7 @@ Plan* load_plan(const char* json, size_t len, const tn_config* cfg_in, int world
           // only the contracted shard modes are swapped)
           std::vector<int> cand;
           for (int l : L)
-            if (!bs.count(l)) cand.push_back(l);
+            if (!bs.count(l) && !split_set.count(l)) cand.push_back(l);
           std::stable_sort(cand.begin(), cand.end(), [&](int a, int b) { return nu(a) > nu(b); });
           if (cand.size() < out_pos.size()) throw err(TN_E_INFEASIBLE, "partition modes run out (swap)");
           st.swap = true;
@@ -376,6 +426,13 @@ Plan* load_plan(const char* json, size_t len, const tn_config* cfg_in, int world
           for (size_t t = 0; t < out_pos.size(); ++t) shard[out_pos[t]] = st.swap_in[t];
           L = lay;
           p.n_swaps++;
+          if (st.quant) {
+            // codes + fp32 scales + zeros of the whole local stem are staged in one stem buffer
+            // (runtime.cu mode_swap): size the buffers for it (matters for small groups / stems)
+            const uint64_t reals = 2ull << L.size(), ng = reals / (uint64_t)cfg.comm_group;
+            const uint64_t cb = align_up(cfg.comm_codec == TN_COMM_INT4 ? reals / 2 : reals, 256);
+            payload_bytes = std::max<uint64_t>(payload_bytes, cb + 2 * align_up(4 * ng, 256));
+          }
           const double n_local = std::ldexp(1.0, (int)L.size());
           const double frac = 1.0 - std::ldexp(1.0, -(int)out_pos.size());
           const double per = !st.quant ? (cfg.dtype == TN_CHALF ? 4.0 : 8.0)
@@ -532,6 +589,12 @@ Plan* load_plan(const char* json, size_t len, const tn_config* cfg_in, int world
         for (int a : st.perm_axes) permuted.push_back(st.in_layout[a]);
         // the first tail step's permutation runs on the whole stem before chunking
         const bool in_ok = ((int)s == p.split_from && st.perm) ? true : prefix_ok(st.in_layout);
+        if (st.swap) {
+          int last = (int)s;  // restart with the tail after the tail's last swap
+          for (size_t q = s; q < p.steps.size(); ++q)
+            if (p.steps[q].swap) last = (int)q + 1;
+          throw err(TN_E_INFEASIBLE, "split-retry:" + std::to_string(last));
+        }
         if (!in_ok || !prefix_ok(st.out_layout) || (st.perm && !prefix_ok(permuted)) || st.mlog < j)
           throw err(TN_E_INFEASIBLE, "split: the split modes do not stay outermost in the tail (step " +
                                          std::to_string(s) + ", from " + std::to_string(p.split_from) + ", in " +
@@ -598,6 +661,7 @@ Plan* load_plan(const char* json, size_t len, const tn_config* cfg_in, int world
       p.perm_bytes += 2.0 * eb * std::ldexp(1.0, (int)L.size());
     }
   }
+  smax = std::max<uint64_t>(smax, (payload_bytes + eb - 1) / eb);
   p.stem_elems_max = smax;
   p.max_stem_log2 = 0;
   while ((1ull << p.max_stem_log2) < smax) p.max_stem_log2++;
@@ -646,6 +710,15 @@ Plan* load_plan(const char* json, size_t len, const tn_config* cfg_in, int world
     const uint64_t T = p.steps.size() - p.split_from, c = 1ull << p.split_log2;
     // + the post-selected member of each subspace (uint64 per chunk)
     off += align_up(4 * c * (2 * T + 1) + 8 * c + 64, 256);
+  }
+  if (world > 1) {
+    // sharded readout: every rank's result block (rank order) and, with a split tail, every rank's
+    // per-chunk exponents are gathered here (the stem buffers may still hold the tail's input)
+    p.ws_gather = off;
+    off += align_up((uint64_t)eb << p.open.size(), 256);
+    p.ws_gather_exp = off;
+    if (!p.split_modes.empty())
+      off += align_up(4ull * world * (1ull << p.split_log2) * (p.steps.size() - p.split_from), 256);
   }
   p.ws_total = off;
   return P.release();

@@ -88,6 +88,8 @@ struct Plan {
   std::vector<uint64_t> tail_slots;  // chunk id held by each result slot of the last tail run
   // workspace layout
   uint64_t ws_leaves = 0, ws_common = 0, ws_b = 0, ws_scratch = 0, ws_total = 0;
+  uint64_t ws_gather = 0;         // world > 1: gathered result (eb << n_open bytes)
+  uint64_t ws_gather_exp = 0;     // world > 1 with a split tail: gathered per-chunk exponents
   uint64_t ws_slice = 0;          // uint64 slice id, read by the kernels (one CUDA graph serves every slice)
   uint64_t stem_elems_max = 0;    // largest stem tensor (elements)
   int max_stem_log2 = 0;

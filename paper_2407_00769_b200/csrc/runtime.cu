@@ -12,7 +12,9 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <condition_variable>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -44,9 +46,50 @@ struct tn_plan {
   Plan* p;
 };
 
+// Loopback transport: `world` virtual ranks on ONE device, each driven by its own host thread
+// (as real ranks are driven by their own processes).  A collective is a host rendezvous of the
+// ranks plus stream-ordered device work: every rank publishes its buffers and an event, waits on its
+// peers' events, moves the data with device-to-device copies (or a tiny max kernel) on its own
+// stream, and waits until its peers have finished reading its buffers before it proceeds.  The
+// same lowering, codec kernels and swap schedule run as with NCCL; only the byte mover differs.
+struct LoopGroup {
+  int world = 0, device = 0, refs = 0;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  uint64_t gen = 0;
+  bool broken = false;
+  std::vector<cudaEvent_t> ready, done;
+  struct Post {
+    int dst;
+    const void* ptr;
+    uint64_t bytes;
+  };
+  std::vector<std::vector<Post>> board;  // board[src]: sends posted by rank src, in order
+  std::vector<const void*> ptr;          // per rank: the buffer of an all-reduce / all-gather
+  void barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    if (broken) throw TnError{TN_E_NCCL, "loopback group broken by an earlier timeout"};
+    const uint64_t g = gen;
+    if (++arrived == world) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+      return;
+    }
+    // a rank that never arrives (error on its thread) must not hang the others forever
+    if (!cv.wait_for(lk, std::chrono::seconds(600), [&] { return gen != g; })) {
+      broken = true;
+      cv.notify_all();
+      throw TnError{TN_E_NCCL, "loopback rendezvous timed out (a virtual rank did not arrive)"};
+    }
+  }
+};
+
 struct tn_comm {
   void* nccl_comm = nullptr;
   int rank = 0, world = 1, device = 0;
+  LoopGroup* loop = nullptr;   // loopback transport (virtual ranks on one device)
 };
 
 // ---- NCCL (dlopen'ed: the process's torch already carries libnccl.so.2) ----
@@ -94,6 +137,112 @@ void nccl_allgather(const void* send, void* recv, size_t count, int type, void* 
 }  // namespace
 
 namespace {
+
+// ---- transport: the byte movers of the sharded stem (NCCL between processes, or loopback) ----
+struct Xfer {
+  int peer;
+  void* ptr;
+  uint64_t bytes;
+};
+
+// Calls on a plan with a communicator run on the communicator's device (a virtual rank's thread,
+// or a process that drives several libraries, need not have selected it).
+void select_device(const Plan& p) {
+  if (p.comm) TN_CUDA(cudaSetDevice(p.comm->device));
+}
+
+void comm_check(const Plan& p) {
+  if (!p.comm || (!p.comm->nccl_comm && !p.comm->loop))
+    throw TnError{TN_E_NCCL, "sharded plan without a communicator"};
+}
+
+// Grouped point-to-point exchange: every (send, recv) pair with the same peer is matched in order.
+void xfer_exchange(Plan& p, const std::vector<Xfer>& sends, const std::vector<Xfer>& recvs, cudaStream_t s) {
+  comm_check(p);
+  tn_comm* c = p.comm;
+  if (!c->loop) {
+    nccl_group(true);
+    for (const Xfer& x : sends) nccl_send(x.ptr, x.bytes, NCCL_INT8, x.peer, c->nccl_comm, s);
+    for (const Xfer& x : recvs) nccl_recv(x.ptr, x.bytes, NCCL_INT8, x.peer, c->nccl_comm, s);
+    nccl_group(false);
+    return;
+  }
+  LoopGroup& g = *c->loop;
+  const int me = c->rank;
+  {
+    std::lock_guard<std::mutex> lk(g.mu);
+    g.board[me].clear();
+    for (const Xfer& x : sends) g.board[me].push_back({x.peer, x.ptr, x.bytes});
+  }
+  TN_CUDA(cudaEventRecord(g.ready[me], s));  // the payload is complete once this event fires
+  g.barrier();
+  std::vector<int> taken(g.world, 0);
+  for (const Xfer& x : recvs) {
+    const LoopGroup::Post* src = nullptr;
+    int k = 0;
+    for (const auto& post : g.board[x.peer])
+      if (post.dst == me && k++ == taken[x.peer]) {
+        src = &post;
+        break;
+      }
+    if (!src || src->bytes != x.bytes) throw TnError{TN_E_NCCL, "loopback exchange: unmatched send/recv"};
+    ++taken[x.peer];
+    TN_CUDA(cudaStreamWaitEvent(s, g.ready[x.peer], 0));
+    TN_CUDA(cudaMemcpyAsync(x.ptr, src->ptr, x.bytes, cudaMemcpyDeviceToDevice, s));
+  }
+  TN_CUDA(cudaEventRecord(g.done[me], s));
+  g.barrier();
+  // the peers' copies out of this rank's send buffers must finish before it writes them again
+  for (const Xfer& x : sends) TN_CUDA(cudaStreamWaitEvent(s, g.done[x.peer], 0));
+}
+
+// 1-float max over ranks (every rank scales the next stem step by the same power of two, C-A28).
+void xfer_allreduce_max(Plan& p, float* slot, cudaStream_t s) {
+  comm_check(p);
+  tn_comm* c = p.comm;
+  if (!c->loop) {
+    nccl_allreduce_max(slot, 1, c->nccl_comm, s);
+    return;
+  }
+  LoopGroup& g = *c->loop;
+  g.ptr[c->rank] = slot;
+  TN_CUDA(cudaEventRecord(g.ready[c->rank], s));
+  g.barrier();
+  MaxSlots ms;
+  ms.n = g.world;
+  for (int r = 0; r < g.world; ++r) {
+    ms.p[r] = static_cast<const float*>(g.ptr[r]);
+    if (r != c->rank) TN_CUDA(cudaStreamWaitEvent(s, g.ready[r], 0));
+  }
+  launch_max_slots(slot, ms, s);
+  TN_CUDA(cudaEventRecord(g.done[c->rank], s));
+  g.barrier();
+  for (int r = 0; r < g.world; ++r)
+    if (r != c->rank) TN_CUDA(cudaStreamWaitEvent(s, g.done[r], 0));
+}
+
+// recv[r * bytes ..] = rank r's `send` (rank order).
+void xfer_allgather(Plan& p, const void* send, void* recv, uint64_t bytes, cudaStream_t s) {
+  comm_check(p);
+  tn_comm* c = p.comm;
+  if (!c->loop) {
+    nccl_allgather(send, recv, bytes, NCCL_INT8, c->nccl_comm, s);
+    return;
+  }
+  LoopGroup& g = *c->loop;
+  g.ptr[c->rank] = send;
+  TN_CUDA(cudaEventRecord(g.ready[c->rank], s));
+  g.barrier();
+  for (int r = 0; r < g.world; ++r) {
+    if (r != c->rank) TN_CUDA(cudaStreamWaitEvent(s, g.ready[r], 0));
+    TN_CUDA(cudaMemcpyAsync(static_cast<unsigned char*>(recv) + (uint64_t)r * bytes, g.ptr[r], bytes,
+                            cudaMemcpyDeviceToDevice, s));
+  }
+  TN_CUDA(cudaEventRecord(g.done[c->rank], s));
+  g.barrier();
+  for (int r = 0; r < g.world; ++r)
+    if (r != c->rank) TN_CUDA(cudaStreamWaitEvent(s, g.done[r], 0));
+}
 
 struct Scratch {
   float* max_slot;    // [S+2]   max |real| of the stem entering step i (float bits via atomicMax)
@@ -244,7 +393,7 @@ void check_buffers(const Plan& p, const tn_buffers* b) {
 // swap, reading C-A17).  int8: each chunk is quantised in groups of comm_group reals (groups never
 // straddle chunks), sent as codes + fp32 scale/zero, and dequantised straight into complex-half.
 void mode_swap(Plan& p, const StemStep& st, const tn_buffers* b, int& cur, cudaStream_t s) {
-  if (!p.comm || !p.comm->nccl_comm) throw TnError{TN_E_NCCL, "sharded plan without an NCCL communicator"};
+  comm_check(p);
   const int eb = p.cfg.dtype == TN_CHALF ? 4 : 8;
   // quantised swaps read the unpermuted stem group by group when the permutation keeps the
   // innermost log2(g/2) modes in place (k_quant.cu group_base): no separate permutation pass
@@ -273,9 +422,9 @@ void mode_swap(Plan& p, const StemStep& st, const tn_buffers* b, int& cur, cudaS
     }
     return r;
   };
-  void* comm = p.comm->nccl_comm;
   unsigned char* X = static_cast<unsigned char*>(b->d_stem[cur]);
   unsigned char* Y = static_cast<unsigned char*>(b->d_stem[1 - cur]);
+  std::vector<Xfer> sends, recvs;
   const bool quant = st.quant;  // lowering: int8/int4 codec, complex-half, late enough in the path
   if (quant) {
     const int g = p.cfg.comm_group;
@@ -285,6 +434,9 @@ void mode_swap(Plan& p, const StemStep& st, const tn_buffers* b, int& cur, cudaS
     const uint64_t ng = reals / g, cng = creals / g;
     const uint64_t cbytes = int4 ? creals / 2 : creals;  // code bytes per chunk
     const uint64_t codes_bytes = align_up(int4 ? reals / 2 : reals, 256);
+    // codes + scales + zeros live in one stem buffer (the lowering sizes the buffers for it)
+    if (codes_bytes + 2 * align_up(4 * ng, 256) > b->stem_bytes)
+      throw TnError{TN_E_CAPACITY, "quantised swap payload exceeds the stem buffer"};
     auto codes = [&](unsigned char* base) { return reinterpret_cast<int8_t*>(base); };
     auto scales = [&](unsigned char* base) { return reinterpret_cast<float*>(base + codes_bytes); };
     auto zeros = [&](unsigned char* base) { return reinterpret_cast<float*>(base + codes_bytes + align_up(4 * ng, 256)); };
@@ -294,18 +446,17 @@ void mode_swap(Plan& p, const StemStep& st, const tn_buffers* b, int& cur, cudaS
     else
       launch_quant_int8_half(codes(Y), scales(Y), zeros(Y), reinterpret_cast<const __half*>(X), reals, g, s,
                              fused ? &gp : nullptr);
-    nccl_group(true);
     for (int v = 0; v < (1 << sx); ++v) {
       if (v == me) continue;
       int peer = peer_of(v);
-      nccl_send(codes(Y) + v * cbytes, cbytes, NCCL_INT8, peer, comm, s);
-      nccl_send(scales(Y) + v * cng, cng, NCCL_FLOAT32, peer, comm, s);
-      nccl_send(zeros(Y) + v * cng, cng, NCCL_FLOAT32, peer, comm, s);
-      nccl_recv(codes(X) + v * cbytes, cbytes, NCCL_INT8, peer, comm, s);
-      nccl_recv(scales(X) + v * cng, cng, NCCL_FLOAT32, peer, comm, s);
-      nccl_recv(zeros(X) + v * cng, cng, NCCL_FLOAT32, peer, comm, s);
+      sends.push_back({peer, codes(Y) + v * cbytes, cbytes});
+      sends.push_back({peer, scales(Y) + v * cng, 4 * cng});
+      sends.push_back({peer, zeros(Y) + v * cng, 4 * cng});
+      recvs.push_back({peer, codes(X) + v * cbytes, cbytes});
+      recvs.push_back({peer, scales(X) + v * cng, 4 * cng});
+      recvs.push_back({peer, zeros(X) + v * cng, 4 * cng});
     }
-    nccl_group(false);
+    xfer_exchange(p, sends, recvs, s);
     TN_CUDA(cudaMemcpyAsync(codes(X) + me * cbytes, codes(Y) + me * cbytes, cbytes, cudaMemcpyDeviceToDevice, s));
     TN_CUDA(cudaMemcpyAsync(scales(X) + me * cng, scales(Y) + me * cng, 4 * cng, cudaMemcpyDeviceToDevice, s));
     TN_CUDA(cudaMemcpyAsync(zeros(X) + me * cng, zeros(Y) + me * cng, 4 * cng, cudaMemcpyDeviceToDevice, s));
@@ -316,18 +467,15 @@ void mode_swap(Plan& p, const StemStep& st, const tn_buffers* b, int& cur, cudaS
       launch_dequant_int8_half(reinterpret_cast<__half*>(Y), codes(X), scales(X), zeros(X), reals, g, s);
     p.launches += 2;
   } else {
-    const int type = eb == 4 ? NCCL_FLOAT16 : NCCL_FLOAT32;
-    const size_t cnt = 2 * chunk;  // reals per chunk
-    nccl_group(true);
+    const uint64_t cb = chunk * eb;  // bytes per chunk
     for (int v = 0; v < (1 << sx); ++v) {
       if (v == me) continue;
       int peer = peer_of(v);
-      nccl_send(X + (uint64_t)v * chunk * eb, cnt, type, peer, comm, s);
-      nccl_recv(Y + (uint64_t)v * chunk * eb, cnt, type, peer, comm, s);
+      sends.push_back({peer, X + (uint64_t)v * cb, cb});
+      recvs.push_back({peer, Y + (uint64_t)v * cb, cb});
     }
-    nccl_group(false);
-    TN_CUDA(cudaMemcpyAsync(Y + (uint64_t)me * chunk * eb, X + (uint64_t)me * chunk * eb, chunk * eb,
-                            cudaMemcpyDeviceToDevice, s));
+    xfer_exchange(p, sends, recvs, s);
+    TN_CUDA(cudaMemcpyAsync(Y + (uint64_t)me * cb, X + (uint64_t)me * cb, cb, cudaMemcpyDeviceToDevice, s));
   }
   cur = 1 - cur;
 }
@@ -438,7 +586,7 @@ void stem_body(Plan& p, const tn_buffers* b, cudaStream_t s, bool head = true, b
   }
   if (!tail) return;
   // every rank scales the first step by the same power of two
-  if (p.world > 1 && p.cfg.dtype == TN_CHALF) nccl_allreduce_max(&sc.max_slot[0], 1, p.comm->nccl_comm, s);
+  if (p.world > 1 && p.cfg.dtype == TN_CHALF) xfer_allreduce_max(p, &sc.max_slot[0], s);
   int cur = 0;
   rec_event(p, 1, s);
   const size_t n_main = p.split_modes.empty() ? p.steps.size() : (size_t)p.split_from;
@@ -456,7 +604,7 @@ void stem_body(Plan& p, const tn_buffers* b, cudaStream_t s, bool head = true, b
     run_gemm(p, st, i, b->d_stem[cur], b->d_stem[1 - cur], 0, &sc.max_slot[i],
              reinterpret_cast<uint32_t*>(&sc.max_slot[i + 1]), &sc.exps[2 + 2 * i], W, sc, s);
     // every rank must scale the next step by the same power of two
-    if (p.world > 1 && p.cfg.dtype == TN_CHALF) nccl_allreduce_max(&sc.max_slot[i + 1], 1, p.comm->nccl_comm, s);
+    if (p.world > 1 && p.cfg.dtype == TN_CHALF) xfer_allreduce_max(p, &sc.max_slot[i + 1], s);
     cur = 1 - cur;
     rec_event(p, 3 + 2 * i, s);
   }
@@ -541,7 +689,9 @@ void capture_stem(Plan& p, const tn_buffers* b) {
 // (one tiny kernel), then the body runs eagerly or as a replay of its CUDA graph: the common phase
 // alone is hundreds of small launches whose CPU cost would otherwise not shrink with more GPUs.
 void stem_contract(Plan& p, const tn_buffers* b, uint64_t slice_id, cudaStream_t s) {
+  select_device(p);
   check_buffers(p, b);
+  p.tail_slots.clear();  // a new stem: any earlier tail result is stale
   if (p.world > 1 && !p.comm) throw TnError{TN_E_INVALID, "plan lowered for several ranks without a communicator"};
   if (p.sliced.size() < 64 && slice_id >= (1ull << p.sliced.size()))
     throw TnError{TN_E_INVALID, "slice_id >= 2^|sliced|"};
@@ -596,6 +746,7 @@ void stem_contract(Plan& p, const tn_buffers* b, uint64_t slice_id, cudaStream_t
 // sparse-state batch of P:525-537: only the requested prefixes are contracted), slot i = ids[i].
 void split_contract(Plan& p, const tn_buffers* b, cudaStream_t s, const std::vector<uint64_t>* ids = nullptr) {
   if (p.split_modes.empty()) return;
+  select_device(p);
   check_buffers(p, b);
   unsigned char* W = static_cast<unsigned char*>(b->d_ws);
   Scratch sc = scratch_of(p, W);
@@ -654,86 +805,131 @@ void split_contract(Plan& p, const tn_buffers* b, cudaStream_t s, const std::vec
   p.result_off = 2 * cmax;
 }
 
-// Sparse-state batch (Fig. 5): the requested correlated subspaces are the prefix values
-// of the split legs; only those chunks of the tail are contracted (a gather on the stem operand,
-// the branches do not depend on the prefix).  Writes n_sub blocks of 2^(n_open - j) amplitudes
-// (members in `open` order without the split legs), unscaled exactly (a.9), and the post-selected
-// member of each subspace (device top-1, ties -> smaller index, C-A23).
-void sample_sparse(Plan& p, const tn_buffers* b, const uint64_t* prefixes, size_t n_sub, double* h_amps, int k,
-                   uint64_t* top_idx, cudaStream_t s) {
-  if (p.split_modes.empty())
-    throw TnError{TN_E_UNSUPPORTED, "sparse-state batch needs a split plan (cfg.split_log2 = prefix legs)"};
-  if (p.world > 1) throw TnError{TN_E_UNSUPPORTED, "sparse-state batch with a sharded stem"};
-  std::vector<uint64_t> ids(prefixes, prefixes + n_sub);
-  split_contract(p, b, s, &ids);
+// Result readout (a.8 + a.9), synchronous.  The result block of every rank (sharded: gathered in
+// rank order into the workspace) is read to the host, each amplitude is unscaled exactly by its
+// accumulated power-of-two exponent (global steps + its split chunk's own chain, C-A8), and the
+// amplitudes are reordered from the storage layout into member order.
+//   ids == nullptr (dense): all 2^n_open amplitudes in `open` order (every chunk of a split tail).
+//   ids (sparse-state batch, Fig. 5): the requested correlated subspaces are prefix values
+//   of the split legs; only those chunks of the tail are contracted; n_sub blocks of 2^(n_open - j)
+//   members (open legs without the split legs, `open` order).
+// top_idx: k most probable members per block, ties -> the smaller member index (C-A23): k = 1 on
+// the device for a single-rank complex-half batch, else on the host.
+void read_result(Plan& p, const tn_buffers* b, cudaStream_t s, const std::vector<uint64_t>* ids, double* h_amps,
+                 int k, uint64_t* top_idx) {
   unsigned char* W = static_cast<unsigned char*>(b->d_ws);
-  Scratch sc = scratch_of(p, W);
   const int eb = p.cfg.dtype == TN_CHALF ? 4 : 8;
-  const int j = (int)p.split_modes.size();
-  const uint64_t chunks = 1ull << j, T = p.steps.size() - p.split_from;
-  const std::vector<int> lay(p.final_layout.begin() + j, p.final_layout.end());
-  const uint64_t members = 1ull << lay.size();
+  const bool split = !p.split_modes.empty();
+  if (ids && !split)
+    throw TnError{TN_E_UNSUPPORTED, "sparse-state batch needs a split plan (cfg.split_log2 = prefix legs)"};
+  if (split) {
+    if (ids) {
+      split_contract(p, b, s, ids);
+    } else {  // dense readout needs every chunk in its own slot (a sparse batch may have run last)
+      bool all = p.tail_slots.size() == (1ull << p.split_modes.size());
+      for (size_t i = 0; all && i < p.tail_slots.size(); ++i) all = p.tail_slots[i] == i;
+      if (!all) split_contract(p, b, s);
+    }
+  }
+  const int j = (int)p.split_modes.size(), R = (int)p.world;
+  const uint64_t chunks = 1ull << j, T = split ? p.steps.size() - p.split_from : 0;
+  const uint64_t nsel = ids ? ids->size() : 1;  // result blocks (slots) per rank
+  // storage layout of one block: split tail -> the final layout without the split legs
+  std::vector<int> lay(p.final_layout.begin() + (ids ? j : 0), p.final_layout.end());
+  if (p.final_perm) lay = p.open;  // (one rank, no split) the last pass wrote `open` order
+  if (!ids && split) {  // slot v = chunk v: split legs (chunk order) outermost
+    lay.assign(p.split_modes.begin(), p.split_modes.end());
+    lay.insert(lay.end(), p.final_layout.begin() + j, p.final_layout.end());
+  }
+  const uint64_t local = 1ull << lay.size();  // elements per block and rank
   const unsigned char* res = static_cast<const unsigned char*>(b->d_stem[p.result_buf]) + p.result_off * eb;
+  Scratch sc = scratch_of(p, W);
+  const int* cexp = reinterpret_cast<const int*>(reinterpret_cast<const float*>(sc.entry_max + 1) + chunks * (T + 1));
+  const uint64_t ncexp = ids ? nsel * T : chunks * T;  // per-slot exponents (slot-major)
+  // members: global layout = rank bits (final_shard) ++ lay; member order = `open` minus split legs
+  std::vector<int> glay = p.final_shard;
+  glay.insert(glay.end(), lay.begin(), lay.end());
+  std::vector<int> mord;
+  for (int l : p.open)
+    if (!ids || std::find(p.split_modes.begin(), p.split_modes.end(), l) == p.split_modes.end()) mord.push_back(l);
+  const int r = (int)glay.size();
+  if ((int)mord.size() != r) throw TnError{TN_E_INVALID, "internal: result layout does not cover the output legs"};
+  std::vector<int> bitpos(r);  // member bit (r-1-t) <- layout bit bitpos[t]
+  for (int t = 0; t < r; ++t)
+    bitpos[t] = r - 1 - (int)(std::find(glay.begin(), glay.end(), mord[t]) - glay.begin());
   std::vector<uint64_t> top_dev;
-  if (top_idx && k == 1 && p.cfg.dtype == TN_CHALF) {
+  const bool dev_top = ids && top_idx && k == 1 && p.cfg.dtype == TN_CHALF && R == 1;
+  if (dev_top) {
     // behind the per-chunk scale chains in the split scratch (the stem must stay intact: a later
     // dense readout re-runs the tail from it)
-    const float* cm = reinterpret_cast<const float*>(sc.entry_max + 1);
-    uintptr_t top_addr = reinterpret_cast<uintptr_t>(cm + chunks * (2 * T + 1));
+    uintptr_t top_addr = reinterpret_cast<uintptr_t>(reinterpret_cast<const float*>(sc.entry_max + 1) +
+                                                     chunks * (2 * T + 1));
     uint64_t* d_top = reinterpret_cast<uint64_t*>((top_addr + 7) & ~(uintptr_t)7);
-    launch_top1_chalf(reinterpret_cast<const __half2*>(res), n_sub, members, d_top, s);
-    top_dev.resize(n_sub);
-    TN_CUDA(cudaMemcpyAsync(top_dev.data(), d_top, 8 * n_sub, cudaMemcpyDeviceToHost, s));
+    MemberMap mm;
+    mm.r = r;
+    for (int t = 0; t < r; ++t) mm.src_bit[t] = (int8_t)bitpos[t];
+    launch_top1_chalf(reinterpret_cast<const __half2*>(res), nsel, local, mm, d_top, s);
+    top_dev.resize(nsel);
+    TN_CUDA(cudaMemcpyAsync(top_dev.data(), d_top, 8 * nsel, cudaMemcpyDeviceToHost, s));
   }
-  std::vector<int> ex(p.n_exp_slots), ce(chunks * T);
+  if (R > 1) {
+    if (nsel * local * R * eb > (uint64_t)eb << p.open.size()) throw TnError{TN_E_CAPACITY, "gather region too small"};
+    xfer_allgather(p, res, W + p.ws_gather, nsel * local * eb, s);
+    res = W + p.ws_gather;
+    if (split) {
+      xfer_allgather(p, cexp, W + p.ws_gather_exp, 4 * ncexp, s);
+      cexp = reinterpret_cast<const int*>(W + p.ws_gather_exp);
+    }
+  }
+  std::vector<int> ex(p.n_exp_slots), ce(R * ncexp);
   TN_CUDA(cudaMemcpyAsync(ex.data(), sc.exps, 4 * ex.size(), cudaMemcpyDeviceToHost, s));
-  const float* cmaxs = reinterpret_cast<const float*>(sc.entry_max + 1);
-  TN_CUDA(cudaMemcpyAsync(ce.data(), cmaxs + chunks * (T + 1), 4 * ce.size(), cudaMemcpyDeviceToHost, s));
-  std::vector<double> vals(2 * n_sub * members);
+  if (split) TN_CUDA(cudaMemcpyAsync(ce.data(), cexp, 4 * ce.size(), cudaMemcpyDeviceToHost, s));
+  const uint64_t total = R * nsel * local;
+  std::vector<double> vals(2 * total);
   if (p.cfg.dtype == TN_CHALF) {
-    std::vector<__half> buf(2 * n_sub * members);
-    TN_CUDA(cudaMemcpyAsync(buf.data(), res, 4 * n_sub * members, cudaMemcpyDeviceToHost, s));
+    std::vector<__half> buf(2 * total);
+    TN_CUDA(cudaMemcpyAsync(buf.data(), res, 4 * total, cudaMemcpyDeviceToHost, s));
     TN_CUDA(cudaStreamSynchronize(s));
     for (size_t i = 0; i < buf.size(); ++i) vals[i] = (double)__half2float(buf[i]);
   } else {
-    std::vector<float> buf(2 * n_sub * members);
-    TN_CUDA(cudaMemcpyAsync(buf.data(), res, 8 * n_sub * members, cudaMemcpyDeviceToHost, s));
+    std::vector<float> buf(2 * total);
+    TN_CUDA(cudaMemcpyAsync(buf.data(), res, 8 * total, cudaMemcpyDeviceToHost, s));
     TN_CUDA(cudaStreamSynchronize(s));
     for (size_t i = 0; i < buf.size(); ++i) vals[i] = buf[i];
   }
   int E = 0;
   for (int e : ex) E += e;
-  // member order: the open legs without the split legs, in `open` order
-  std::vector<int> mord;
-  for (int l : p.open)
-    if (std::find(p.split_modes.begin(), p.split_modes.end(), l) == p.split_modes.end()) mord.push_back(l);
-  const int r = (int)lay.size();
-  std::vector<int> pos(r);
-  for (int i = 0; i < r; ++i) pos[i] = (int)(std::find(lay.begin(), lay.end(), mord[i]) - lay.begin());
-  auto lay_index = [&](uint64_t o) {  // member index in `mord` order -> index in layout order
-    uint64_t src = 0;
-    for (int i = 0; i < r; ++i)
-      if ((o >> (r - 1 - i)) & 1) src |= 1ull << (r - 1 - pos[i]);
-    return src;
+  // exponent of (rank q, slot sl): dense split -> slot = chunk = top j bits of `lay`
+  auto chain = [&](int q, uint64_t sl) {
+    int e = E;
+    for (uint64_t t = 0; t < T; ++t) e += ce[(uint64_t)q * ncexp + sl * T + t];
+    return e;
   };
-  std::vector<uint64_t> inv(members);
-  for (uint64_t o = 0; o < members; ++o) inv[lay_index(o)] = o;
-  for (size_t sl = 0; sl < n_sub; ++sl) {
-    int Ev = E;
-    for (uint64_t t = 0; t < T; ++t) Ev += ce[sl * T + t];
+  const uint64_t members = 1ull << r;
+  const int lbits = (int)lay.size();
+  for (uint64_t sl = 0; sl < nsel; ++sl) {
+    double* out = h_amps + 2 * sl * members;
     for (uint64_t o = 0; o < members; ++o) {
-      const uint64_t src = sl * members + lay_index(o);
-      h_amps[2 * (sl * members + o)] = std::ldexp(vals[2 * src], -Ev);
-      h_amps[2 * (sl * members + o) + 1] = std::ldexp(vals[2 * src + 1], -Ev);
+      uint64_t g = 0;  // index in the global layout (rank bits, then the block layout)
+      for (int t = 0; t < r; ++t)
+        if ((o >> (r - 1 - t)) & 1) g |= 1ull << bitpos[t];
+      const int q = (int)(g >> lbits);
+      const uint64_t li = g & (local - 1);
+      const int e = !split ? E : chain(q, ids ? sl : (li >> (lbits - j)));
+      const uint64_t src = ((uint64_t)q * nsel + sl) * local + li;
+      out[2 * o] = std::ldexp(vals[2 * src], -e);
+      out[2 * o + 1] = std::ldexp(vals[2 * src + 1], -e);
     }
     if (top_idx && k > 0) {
       if (!top_dev.empty()) {
-        top_idx[sl] = inv[top_dev[sl]];
+        top_idx[sl] = top_dev[sl];
       } else {
         std::vector<uint64_t> idx(members);
         for (uint64_t i = 0; i < members; ++i) idx[i] = i;
-        const double* a = h_amps + 2 * sl * members;
-        auto prob = [&](uint64_t i) { return a[2 * i] * a[2 * i] + a[2 * i + 1] * a[2 * i + 1]; };
+        auto prob = [&](uint64_t i) {
+          const double pr = out[2 * i] * out[2 * i] + out[2 * i + 1] * out[2 * i + 1];
+          return pr == pr ? pr : -1.0;
+        };
         std::stable_sort(idx.begin(), idx.end(), [&](uint64_t x, uint64_t y) { return prob(x) > prob(y); });
         for (int q = 0; q < k && (uint64_t)q < members; ++q) top_idx[sl * k + q] = idx[q];
       }
@@ -804,6 +1000,7 @@ int tn_plan_upload(tn_plan* h, const tn_buffers* b, void* stream) {
   if (!h || !b || !b->d_ws) return fail(TN_E_INVALID, "NULL argument");
   TN_TRY({
     Plan& p = *h->p;
+    select_device(p);
     if (b->ws_bytes < p.ws_total) throw TnError{TN_E_CAPACITY, "workspace too small"};
     if (!p.pinned) {
       TN_CUDA(cudaMallocHost(&p.pinned, p.ws_leaves));
@@ -831,90 +1028,30 @@ int tn_sample_amplitudes(tn_plan* h, const tn_buffers* b, const uint64_t* prefix
                          int k, uint64_t* top_idx, void* stream) {
   if (!h || !b || !h_amps) return fail(TN_E_INVALID, "NULL argument");
   if ((prefixes == nullptr) != (n_sub == 0)) return fail(TN_E_INVALID, "prefixes and n_sub must come together");
-  if (prefixes) {
-    TN_TRY(sample_sparse(*h->p, b, prefixes, n_sub, h_amps, k, top_idx, (cudaStream_t)stream));
-  }
+  if (k < 0) return fail(TN_E_INVALID, "k < 0");
   TN_TRY({
     Plan& p = *h->p;
+    select_device(p);
     cudaStream_t s = (cudaStream_t)stream;
-    const uint64_t n = 1ull << p.open.size();
-    std::vector<int> layout;
-    std::vector<double> vals(2 * n);
-    unsigned char* W = static_cast<unsigned char*>(b->d_ws);
-    int E = 0;
-    if (p.result_in_ws) {
-      int id = p.root;
-      const Node& r = p.nodes[id];
-      std::vector<float> buf(2 * n);
-      if (r.kind == NODE_LEAF) throw TnError{TN_E_UNSUPPORTED, "single-tensor network"};
-      TN_CUDA(cudaMemcpyAsync(buf.data(), W + r.ws_off, 8 * n, cudaMemcpyDeviceToHost, s));
-      TN_CUDA(cudaStreamSynchronize(s));
-      for (uint64_t i = 0; i < 2 * n; ++i) vals[i] = buf[i];
-      layout = r.labels;
-    } else {
-      Scratch sc = scratch_of(p, W);
-      std::vector<int> ex(p.n_exp_slots);
-      TN_CUDA(cudaMemcpyAsync(ex.data(), sc.exps, 4 * ex.size(), cudaMemcpyDeviceToHost, s));
-      const int ebr = p.cfg.dtype == TN_CHALF ? 4 : 8;
-      if (!p.split_modes.empty()) {
-        // dense readout needs every chunk in its own slot (a sparse batch may have run last)
-        bool all = p.tail_slots.size() == (1ull << p.split_modes.size());
-        for (size_t i = 0; all && i < p.tail_slots.size(); ++i) all = p.tail_slots[i] == i;
-        if (!all) split_contract(p, b, s);
-      }
-      const void* res = static_cast<const unsigned char*>(b->d_stem[p.result_buf]) + p.result_off * ebr;
-      std::vector<int> chunk_e;  // split tail: each chunk's own exponent sum
-      if (!p.split_modes.empty()) {
-        const uint64_t chunks = 1ull << p.split_modes.size(), T = p.steps.size() - p.split_from;
-        std::vector<int> ce(chunks * T);
-        const float* cmaxs = reinterpret_cast<const float*>(sc.entry_max + 1);
-        TN_CUDA(cudaMemcpyAsync(ce.data(), cmaxs + chunks * (T + 1), 4 * ce.size(), cudaMemcpyDeviceToHost, s));
-        TN_CUDA(cudaStreamSynchronize(s));
-        chunk_e.assign(chunks, 0);
-        for (uint64_t v = 0; v < chunks; ++v)
-          for (uint64_t t = 0; t < T; ++t) chunk_e[v] += ce[v * T + t];
-      }
-      if (p.world > 1) {
-        // the result is sharded on final_shard: gather every rank's block (rank order)
-        const int eb = p.cfg.dtype == TN_CHALF ? 4 : 8;
-        const uint64_t n_local = n >> p.shard_log2;
-        nccl_allgather(res, b->d_stem[1 - p.result_buf], n_local * eb, NCCL_INT8, p.comm->nccl_comm, s);
-        res = b->d_stem[1 - p.result_buf];
-      }
-      if (p.cfg.dtype == TN_CHALF) {
-        std::vector<__half> buf(2 * n);
-        TN_CUDA(cudaMemcpyAsync(buf.data(), res, 4 * n, cudaMemcpyDeviceToHost, s));
-        TN_CUDA(cudaStreamSynchronize(s));
-        for (uint64_t i = 0; i < 2 * n; ++i) vals[i] = (double)__half2float(buf[i]);
-      } else {
-        std::vector<float> buf(2 * n);
-        TN_CUDA(cudaMemcpyAsync(buf.data(), res, 8 * n, cudaMemcpyDeviceToHost, s));
-        TN_CUDA(cudaStreamSynchronize(s));
-        for (uint64_t i = 0; i < 2 * n; ++i) vals[i] = buf[i];
-      }
-      for (int e : ex) E += e;
-      if (p.final_perm) {
-        layout = p.open;
-      } else {
-        layout = p.final_shard;
-        if (!p.split_modes.empty()) {  // slot v = chunk v: split legs in chunk order, then the rest
-          layout.insert(layout.end(), p.split_modes.begin(), p.split_modes.end());
-          layout.insert(layout.end(), p.final_layout.begin() + p.split_modes.size(), p.final_layout.end());
-        } else {
-          layout.insert(layout.end(), p.final_layout.begin(), p.final_layout.end());
-        }
-      }
-      if (!chunk_e.empty()) {
-        // chunk v = top j bits of the result index (split modes outermost): apply its exponent
-        const int j = (int)p.split_modes.size(), r = (int)layout.size();
-        for (uint64_t i = 0; i < n; ++i) {
-          const int sh = -chunk_e[i >> (r - j)];
-          vals[2 * i] = std::ldexp(vals[2 * i], sh);
-          vals[2 * i + 1] = std::ldexp(vals[2 * i + 1], sh);
-        }
-      }
+    if (prefixes) {
+      std::vector<uint64_t> ids(prefixes, prefixes + n_sub);
+      read_result(p, b, s, &ids, h_amps, k, top_idx);
+      return TN_OK;
     }
-    // reorder into `open` order and unscale exactly by 2^-E (a.9)
+    if (!p.result_in_ws) {
+      check_buffers(p, b);
+      read_result(p, b, s, nullptr, h_amps, k, top_idx);
+      return TN_OK;
+    }
+    // no stem steps: the root is a common-type node in the workspace (complex64, one rank)
+    const uint64_t n = 1ull << p.open.size();
+    unsigned char* W = static_cast<unsigned char*>(b->d_ws);
+    const Node& rt = p.nodes[p.root];
+    if (rt.kind == NODE_LEAF) throw TnError{TN_E_UNSUPPORTED, "single-tensor network"};
+    std::vector<float> buf(2 * n);
+    TN_CUDA(cudaMemcpyAsync(buf.data(), W + rt.ws_off, 8 * n, cudaMemcpyDeviceToHost, s));
+    TN_CUDA(cudaStreamSynchronize(s));
+    const std::vector<int>& layout = rt.labels;
     const int r = (int)p.open.size();
     std::vector<int> pos(r);
     for (int i = 0; i < r; ++i) pos[i] = (int)(std::find(layout.begin(), layout.end(), p.open[i]) - layout.begin());
@@ -922,15 +1059,15 @@ int tn_sample_amplitudes(tn_plan* h, const tn_buffers* b, const uint64_t* prefix
       uint64_t src = 0;
       for (int i = 0; i < r; ++i)
         if ((o >> (r - 1 - i)) & 1) src |= 1ull << (r - 1 - pos[i]);
-      h_amps[2 * o] = std::ldexp(vals[2 * src], -E);
-      h_amps[2 * o + 1] = std::ldexp(vals[2 * src + 1], -E);
+      h_amps[2 * o] = buf[2 * src];
+      h_amps[2 * o + 1] = buf[2 * src + 1];
     }
     if (top_idx && k > 0) {
       std::vector<uint64_t> idx(n);
       for (uint64_t i = 0; i < n; ++i) idx[i] = i;
       auto prob = [&](uint64_t i) { return h_amps[2 * i] * h_amps[2 * i] + h_amps[2 * i + 1] * h_amps[2 * i + 1]; };
       std::stable_sort(idx.begin(), idx.end(), [&](uint64_t a, uint64_t c) { return prob(a) > prob(c); });
-      for (int j = 0; j < k && (uint64_t)j < n; ++j) top_idx[j] = idx[j];
+      for (int q = 0; q < k && (uint64_t)q < n; ++q) top_idx[q] = idx[q];
     }
   });
 }
@@ -1134,8 +1271,51 @@ int tn_comm_init(const uint8_t uid[128], int rank, int world, int device, tn_com
   });
 }
 
+int tn_comm_init_loopback(int world, int device, tn_comm** out) {
+  if (!out) return fail(TN_E_INVALID, "NULL argument");
+  if (world != 1 && world != 2 && world != 4 && world != 8) return fail(TN_E_UNSUPPORTED, "world must be 1,2,4,8");
+  TN_TRY({
+    TN_CUDA(cudaSetDevice(device));
+    LoopGroup* g = new LoopGroup();
+    g->world = world;
+    g->device = device;
+    g->board.resize(world);
+    g->ptr.assign(world, nullptr);
+    g->ready.assign(world, nullptr);
+    g->done.assign(world, nullptr);
+    for (int r = 0; r < world; ++r) {
+      TN_CUDA(cudaEventCreateWithFlags(&g->ready[r], cudaEventDisableTiming));
+      TN_CUDA(cudaEventCreateWithFlags(&g->done[r], cudaEventDisableTiming));
+    }
+    for (int r = 0; r < world; ++r) {
+      tn_comm* c = new tn_comm();
+      c->rank = r;
+      c->world = world;
+      c->device = device;
+      c->loop = g;
+      g->refs++;
+      out[r] = c;
+    }
+  });
+}
+
 void tn_comm_free(tn_comm* c) {
   if (!c) return;
+  if (c->loop) {
+    LoopGroup* g = c->loop;
+    bool last = false;
+    {
+      std::lock_guard<std::mutex> lk(g->mu);
+      last = --g->refs == 0;
+    }
+    if (last) {
+      for (cudaEvent_t e : g->ready) cudaEventDestroy(e);
+      for (cudaEvent_t e : g->done) cudaEventDestroy(e);
+      delete g;
+    }
+    delete c;
+    return;
+  }
   if (c->nccl_comm) {
     try {
       auto fn = (nccl_destroy_fn)nccl_sym("ncclCommDestroy");

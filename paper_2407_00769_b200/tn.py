@@ -82,6 +82,7 @@ def lib():
         L.tn_dequant_int4_f16.argtypes = [vp, vp, vp, vp, u64, i32, vp]
         L.tn_comm_unique_id.argtypes = [vp]
         L.tn_comm_init.argtypes = [vp, i32, i32, i32, C.POINTER(vp)]
+        L.tn_comm_init_loopback.argtypes = [i32, i32, vp]
         L.tn_comm_free.argtypes = [vp]
         L.tn_comm_free.restype = None
         _lib = L
@@ -333,3 +334,57 @@ class Comm:
         if getattr(self, "_h", None) and _lib is not None:
             _lib.tn_comm_free(self._h)
             self._h = None
+
+
+class LoopbackComm:
+    """tn_comm_init_loopback: `world` virtual ranks on one device (include/tn.h).  Drive each
+    rank's plan from its own thread (see run_ranks)."""
+
+    def __init__(self, world, device=0):
+        arr = (C.c_void_p * world)()
+        _check(lib().tn_comm_init_loopback(world, device, arr))
+        self._h = [C.c_void_p(arr[r]) for r in range(world)]
+        self.world = world
+        self.ranks = [_Rank(self, r) for r in range(world)]
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            for h in self._h:
+                _lib.tn_comm_free(h)
+            self._h = None
+
+
+class _Rank:
+    def __init__(self, group, rank):
+        self.group, self.rank, self.world = group, rank, group.world
+
+    @property
+    def handle(self):
+        return self.group._h[self.rank]
+
+
+def run_ranks(world, fn):
+    """Run fn(rank) on `world` threads, one per virtual rank, each with its own CUDA stream;
+    returns the per-rank results (re-raises the first exception)."""
+    import threading
+    import torch
+    dev = torch.cuda.current_device()
+    out, errs = [None] * world, [None] * world
+
+    def body(r):
+        try:
+            torch.cuda.set_device(dev)
+            with torch.cuda.stream(torch.cuda.Stream()):
+                out[r] = fn(r)
+                torch.cuda.current_stream().synchronize()
+        except BaseException as e:  # noqa: BLE001
+            errs[r] = e
+    ts = [threading.Thread(target=body, args=(r,)) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for e in errs:
+        if e is not None:
+            raise e
+    return out

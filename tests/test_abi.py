@@ -198,3 +198,45 @@ def test_fused_swap_codec_lowering(tnmod, world, g):
     assert all(not s["fuse_quant"] for s in ru)
     strip = lambda st: [{k: v for k, v in s.items() if k != "fuse_quant"} for s in st]  # noqa: E731
     assert strip(rf) == strip(ru)
+
+
+def test_split_auto_chunk_count(tnmod):
+    """split_log2 = -1 (reading C-A19): the smallest power-of-two chunk count whose lowering
+    fits stem_capacity_bytes; no capacity -> no split; nothing fits -> TN_E_CAPACITY."""
+    with open(os.path.join(ROOT, "plans", "c3.json")) as f:
+        c3 = json.load(f)
+    need = {}
+    for j in range(4):
+        need[j] = _load(tnmod, c3, stem_min_log2=20, split_log2=j).info()["stem_bytes"]
+    assert need[0] > need[3]
+    assert _load(tnmod, c3, stem_min_log2=20, split_log2=-1).info()["split_chunks"] == 1
+    for cap in (need[0], need[0] - 1, need[3]):
+        p = _load(tnmod, c3, stem_min_log2=20, split_log2=-1, stem_capacity_bytes=cap)
+        c = p.info()["split_chunks"]
+        j = c.bit_length() - 1
+        assert need[j] <= cap and all(need[i] > cap for i in range(j))
+    with pytest.raises(tnmod.TnError) as e:
+        _load(tnmod, c3, stem_min_log2=20, split_log2=-1, stem_capacity_bytes=1 << 30)
+    assert e.value.code == -4
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_split_tail_with_sharded_stem_lowering(tnmod, world):
+    """Split tail on a sharded stem: split legs are never shard or swap-in modes, and the tail starts
+    after the last mode swap (host lowering for `world` virtual ranks)."""
+    from workload import make_plans as MP
+    with open(os.path.join(ROOT, "plans", "c2.json")) as f:
+        sub = MP.sub_slice(json.load(f), 20)
+    for j in (1, 2, 3):
+        p = _load(tnmod, sub, stem_min_log2=12, split_log2=j, virtual_world=world)
+        rep = p.report()
+        assert p.info()["split_chunks"] == 2 ** j
+        sm = set(rep["split_modes"])
+        assert not sm & set(rep["shard0"])
+        tail = [s for s in rep["steps"] if s["split"]]
+        assert tail and all(not s["swap"] for s in tail)
+        for s in rep["steps"]:
+            if s["swap"]:
+                assert not sm & set(s["swap_in"])
+            if s["split"]:
+                assert set(s["in"][:j]) == sm or s is tail[0]

@@ -166,3 +166,75 @@ def test_fused_permutation_matches_permute_pass(tn, dtype):
     assert out[0][1] >= 1 and out[1][1] == 0 and out[0][2] < out[1][2]
     assert np.array_equal(out[0][0], out[1][0])
     assert metrics.rel_l2(out[0][0], contract.contract(load(sub), 0)) <= TOL[dtype]
+
+
+def _free():
+    import gc
+    import torch
+    gc.collect()
+    torch.cuda.empty_cache()
+
+
+def test_c3_split_auto_capacity(tn):
+    """SURVEY a.7 protocol at full C3 size: buffers sized below the unsplit stem force the automatic
+    chunk count (split_log2 = -1, C-A19) to c >= 2; same amplitudes as the unsplit run (chunk
+    scales are powers of two, so only fp16 subnormals could differ)."""
+    c3 = _plan("c3")
+    p0 = tn.Plan(c3, tn.make_config(stem_min_log2=20))
+    one = tn.contract(p0, tn.Buffers(p0), 0)
+    need0 = p0.info()["stem_bytes"]
+    del p0
+    _free()
+    cap = tn.Plan(c3, tn.make_config(stem_min_log2=20, split_log2=3)).info()["stem_bytes"]
+    assert cap < need0
+    p = tn.Plan(c3, tn.make_config(stem_min_log2=20, split_log2=-1, stem_capacity_bytes=cap))
+    assert p.info()["split_chunks"] >= 2 and p.info()["stem_bytes"] <= cap
+    got = tn.contract(p, tn.Buffers(p, stem_bytes=cap), 0)
+    del p
+    _free()
+    assert metrics.rel_l2(got, one) <= 1e-6
+
+
+def test_c3_sub_split_auto_vs_oracle(tn):
+    sub = MP.sub_slice(_plan("c3"), 22)
+    ref = contract.contract(load(sub), 0)
+    cap = tn.Plan(sub, tn.make_config(stem_min_log2=14, split_log2=2)).info()["stem_bytes"]
+    p = tn.Plan(sub, tn.make_config(stem_min_log2=14, split_log2=-1, stem_capacity_bytes=cap))
+    assert p.info()["split_chunks"] >= 2
+    assert metrics.rel_l2(tn.contract(p, tn.Buffers(p, stem_bytes=cap), 0), ref) <= 2e-2
+
+
+def test_c3_full_equals_sum_of_gpu_subslices(tn):
+    """SURVEY c.6 step 2 at full size: the full C3 subtask (stem 2^33) = the sum of its 4 GPU
+    sub-slices over 2 extra sliced edges (slicing identity P:318), within the fp16 bound."""
+    c3 = _plan("c3")
+    p = tn.Plan(c3, tn.make_config(stem_min_log2=20))
+    full = tn.contract(p, tn.Buffers(p), 0)
+    assert p.info()["max_stem_log2"] == 33
+    del p
+    _free()
+    sub = MP.sub_slice(c3, 31)
+    extra = sub["sliced"][len(c3["sliced"]):]
+    assert len(extra) >= 2
+    sub["sliced"] = extra + c3["sliced"]  # extra edges first: slice e sets them, the rest stay 0
+    p = tn.Plan(sub, tn.make_config(stem_min_log2=20))
+    b = tn.Buffers(p)
+    tot = 0
+    for e in range(1 << len(extra)):
+        tot = tot + tn.contract(p, b, e)
+    del p, b
+    _free()
+    assert metrics.rel_l2(tot, full) <= 2e-2
+
+
+def test_c3_subslice_fp16_vs_complex64(tn):
+    """SURVEY c.6 step 3: C3 sub-sliced by one edge (stem 2^32): complex-half vs the complex64 path."""
+    sub = MP.sub_slice(_plan("c3"), 32)
+    a32, p = run_gpu(tn, sub, 1, 0, stem_min_log2=20)
+    assert p.info()["max_stem_log2"] >= 31
+    del p
+    _free()
+    a16, p = run_gpu(tn, sub, 0, 0, stem_min_log2=20)
+    del p
+    _free()
+    assert metrics.rel_l2(a16, a32) <= 2e-2

@@ -1,0 +1,219 @@
+"""Sharded stem on ONE GPU through the loopback transport (include/tn.h tn_comm_init_loopback):
+G virtual ranks, each on its own host thread and CUDA stream, run the identical lowering, swap
+schedule and codec kernels as the NCCL path (Alg. 1, Eq. 1
+P:389-406); only the byte mover is a device-to-device copy.  This is what makes the sharded path
+parity-testable on the driver's 1-GPU box.
+
+Bounds (BASELINE.json north_star): rel-L2 <= 2e-2 (fp16 storage), <= 5e-2 with int8 swaps.
+fp16 swaps are bit-identical to one GPU (a swap moves bits; every rank's per-element sums are the
+single-GPU ones and the all-reduced max keeps the exponents identical).
+int8-on-every-swap and int4 bounds: the oracle's own prediction of the error of exactly those swaps
+(reading C-A32)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle import contract, metrics
+from oracle.plan import load
+from workload import make_plans as MP
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def tn():
+    import torch
+    from paper_2407_00769_b200 import build as B
+    B.build()
+    from paper_2407_00769_b200 import tn as T
+    assert torch.cuda.is_available()
+    return T
+
+
+def _plan(name):
+    with open(os.path.join(ROOT, "plans", f"{name}.json")) as f:
+        return json.load(f)
+
+
+@pytest.fixture(scope="module")
+def c3sub():
+    sub = MP.sub_slice(_plan("c3"), 22)
+    return sub, contract.contract(load(sub), 0)
+
+
+def run_loopback(tn, plan, world, cfg_kw, slice_id=0, sparse=None):
+    """Every virtual rank contracts the slice; returns (rank-0 amplitudes, rank-0 report, all amps)."""
+    group = tn.LoopbackComm(world)
+
+    def rank_fn(r):
+        p = tn.Plan(plan, tn.make_config(**cfg_kw), comm=group.ranks[r])
+        b = tn.Buffers(p)
+        if sparse is None:
+            a = tn.contract(p, b, slice_id)
+        else:
+            tn.tn_plan_upload(p, b)
+            tn.tn_stem_contract(p, b, slice_id)
+            a = tn.tn_sample_sparse(p, b, sparse, k=1)
+        return a, p.report(), p.info()
+
+    out = tn.run_ranks(world, rank_fn)
+    return out
+
+
+def run_one(tn, plan, cfg_kw, slice_id=0):
+    p = tn.Plan(plan, tn.make_config(**cfg_kw))
+    return tn.contract(p, tn.Buffers(p), slice_id), p
+
+
+def n_swaps(rep, quant=None):
+    return sum(1 for s in rep["steps"] if s.get("swap") and (quant is None or s.get("quant") == quant))
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_loopback_fp16_bit_identical_and_oracle(tn, c3sub, world):
+    sub, ref = c3sub
+    one, _ = run_one(tn, sub, dict(stem_min_log2=14))
+    out = run_loopback(tn, sub, world, dict(stem_min_log2=14, comm_codec=tn.TN_COMM_FP16))
+    assert n_swaps(out[0][1]) >= 1
+    for a, rep, _ in out:  # every rank reads the whole result
+        assert np.array_equal(a, one)
+    assert metrics.rel_l2(out[0][0], ref) <= 2e-2
+
+
+def predicted_swap_error(plan, rep, ref, preset):
+    """Reading C-A32: the codec error of each quantised swap, propagated to the result by the
+    oracle.  For swap i the oracle's stem tensor entering step i is laid out as the sender sees it
+    (rank bits = shard_before, then send_layout), quantised and dequantised by the ORACLE codec
+    (Eq. 1, groups of g reals along the innermost modes, preset `preset`), and the error e_i is
+    pushed through the rest of the network (contract(..., override) — the contraction is linear
+    in every node, so the root receives L_i(e_i)).  Independent swap errors add in quadrature:
+    pred^2 = sum_i |L_i(e_i)|^2 / |ref|^2."""
+    from oracle import codec
+    P = load(plan)
+    nl = len(P.tensors)
+    qmin, qmax, ex, g, rnd = codec.PRESETS[preset]
+    sw = [i for i, st in enumerate(rep["steps"]) if st.get("quant")]
+    if not sw:
+        return 0.0
+    stem_in = {}
+    for i in sw:
+        st = rep["steps"][i]
+        u, v = P.tree[st["node"] - nl]
+        stem_in[i] = v if u == st["branch"] else u
+    rec = {stem_in[i]: None for i in sw}
+    contract.contract(P, 0, record=rec)
+    tot = 0.0
+    for i in sw:
+        st = rep["steps"][i]
+        lab, t = rec[stem_in[i]]
+        glay = list(st["shard_before"]) + list(st["send_layout"])
+        x = np.transpose(t, [lab.index(l) for l in glay])
+        re = np.stack([x.real, x.imag], axis=-1).astype(np.float32).reshape(-1)
+        c, sc, ze = codec.quantize(re, qmin, qmax, ex, g, rnd)
+        y = codec.dequantize(c, sc, ze, ex, g).astype(np.float64).reshape(x.shape + (2,))
+        e = (y[..., 0] + 1j * y[..., 1]) - x
+        e = np.transpose(e, [glay.index(l) for l in lab])
+        le = contract.contract(P, 0, override={stem_in[i]: (lab, e)})
+        tot += float(np.sum(np.abs(le) ** 2))
+    return float(np.sqrt(tot) / np.linalg.norm(ref))
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+@pytest.mark.parametrize("codec", ["int8", "int4"])
+def test_loopback_quantised_swaps_vs_oracle(tn, c3sub, world, codec):
+    """Default late-stage policy (C-A26) and every swap quantised, against the error the
+    oracle predicts for exactly these swaps (C-A32): the GPU error may exceed the prediction only
+    by fp16 storage and the randomness of the codec's rounding (factor 2)."""
+    sub, ref = c3sub
+    cc = {"int8": tn.TN_COMM_INT8, "int4": tn.TN_COMM_INT4}[codec]
+    preset = {"int8": "int8_g128", "int4": "int4"}[codec]
+    fp16 = run_loopback(tn, sub, world, dict(stem_min_log2=14, comm_codec=tn.TN_COMM_FP16))
+    e16 = metrics.rel_l2(fp16[0][0], ref)
+    for pct in (-1, 0):
+        out = run_loopback(tn, sub, world, dict(stem_min_log2=14, comm_codec=cc, quant_from_pct=pct))
+        rep = out[0][1]
+        nq = n_swaps(rep, quant=1)
+        assert nq >= 1 or pct < 0
+        if pct == 0:
+            assert nq == n_swaps(rep)
+        err = metrics.rel_l2(out[0][0], ref)
+        pred = predicted_swap_error(sub, rep, ref, preset)
+        bound = 2.0 * float(np.hypot(pred, e16)) + 1e-3
+        print(f"world={world} {codec} pct={pct}: swaps={nq} err={err:.3e} predicted={pred:.3e} fp16={e16:.3e}")
+        assert err <= bound, (err, pred, e16)
+        if codec == "int8" and pct < 0:
+            assert err <= 5e-2   # BASELINE north_star bound with int8 communication
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_loopback_fused_codec_bit_identical(tn, c3sub, world):
+    """Sender permutation fused into the codec == permutation pass + codec, bit for bit."""
+    sub, _ = c3sub
+    kw = dict(stem_min_log2=14, comm_codec=tn.TN_COMM_INT8, quant_from_pct=0)
+    fused = run_loopback(tn, sub, world, kw)
+    unf = run_loopback(tn, sub, world, dict(kw, no_fuse_swap_quant=1))
+    assert sum(s["fuse_quant"] for s in unf[0][1]["steps"]) == 0
+    assert np.array_equal(fused[0][0], unf[0][0])
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_loopback_c1_all_legs_open(tn, world):
+    """C1: 12 open legs, result gathered from 1/G shards into the workspace (ADVICE: the gather
+    must not write past a shard-sized stem buffer)."""
+    plan = _plan("c1")
+    ref = contract.contract(load(plan), 0)
+    for dtype, tol in ((0, 2e-2), (1, 1e-5)):
+        out = run_loopback(tn, plan, world, dict(dtype=dtype, stem_min_log2=8, comm_codec=tn.TN_COMM_FP16))
+        for a, _, _ in out:
+            assert metrics.rel_l2(a, ref) <= tol
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("split", [1, 2])
+def test_loopback_split_tail_sharded(tn, world, split):
+    """Split-type tail on a sharded stem: each rank chunks its own shard; per-rank
+    chunk exponents are gathered with the result."""
+    sub = MP.sub_slice(_plan("c2"), 20)
+    ref = contract.contract(load(sub), 0)
+    for dtype, tol in ((0, 2e-2), (1, 1e-5)):
+        kw = dict(dtype=dtype, stem_min_log2=12, split_log2=split, comm_codec=tn.TN_COMM_FP16)
+        out = run_loopback(tn, sub, world, kw)
+        assert out[0][2]["split_chunks"] == 2 ** split
+        assert sum(s["split"] for s in out[0][1]["steps"]) >= 1
+        assert all(not s["swap"] for s in out[0][1]["steps"] if s["split"])
+        for a, _, _ in out:
+            assert metrics.rel_l2(a, ref) <= tol
+        one, _ = run_one(tn, sub, dict(dtype=dtype, stem_min_log2=12, split_log2=split))
+        assert metrics.rel_l2(out[0][0], one) <= (1e-6 if dtype == 0 else 1e-7)
+
+
+def test_loopback_sparse_batch_sharded(tn):
+    """Sparse-state batch with a sharded stem: same subspaces and picks as one GPU."""
+    plan = MP.build_plan(3, 4, False, 8, 12, None, trials=2, seed=0)
+    kw = dict(dtype=0, stem_min_log2=6, split_log2=4, comm_codec=tn.TN_COMM_FP16)
+    pre = np.array([3, 0, 15, 7, 9], dtype=np.uint64)
+    p1 = tn.Plan(plan, tn.make_config(**kw))
+    b1 = tn.Buffers(p1)
+    tn.tn_plan_upload(p1, b1)
+    tn.tn_stem_contract(p1, b1, 0)
+    a1, t1 = tn.tn_sample_sparse(p1, b1, pre, k=1)
+    out = run_loopback(tn, plan, 2, kw, sparse=pre)
+    a2, t2 = out[0][0]
+    assert metrics.rel_l2(a2, a1) <= 1e-6
+    pr = np.abs(a1) ** 2
+    for i in range(len(pre)):
+        assert pr[i, int(t2[i, 0])] >= (1 - 4e-2) * pr[i].max()
+
+
+def test_c3_sub26_vs_oracle(tn):
+    """C3 sub-sliced to 2^26 (SURVEY §8(c) c.6 step 1 at 2^26): one GPU and 4 virtual ranks."""
+    sub = MP.sub_slice(_plan("c3"), 26)
+    ref = contract.contract(load(sub), 0)
+    one, p = run_one(tn, sub, dict(stem_min_log2=18))
+    assert p.info()["max_stem_log2"] >= 25
+    assert metrics.rel_l2(one, ref) <= 2e-2
+    out = run_loopback(tn, sub, 4, dict(stem_min_log2=18, comm_codec=tn.TN_COMM_FP16))
+    assert np.array_equal(out[0][0], one)

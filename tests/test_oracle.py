@@ -240,3 +240,25 @@ def test_flops_convention():
     plan = {"tensors": [{"labels": [0, 1], "data": [0.0] * 8}, {"labels": [1, 2], "data": [0.0] * 8}],
             "open": [0, 2], "tree": [[0, 1]], "sliced": []}
     assert contract.flops(plan) == 64
+
+
+def test_override_is_linear_and_consistent():
+    """contract(override=...) (used to propagate swap errors): overriding a node with its own value
+    changes nothing; overriding with zeros gives zero; the root is linear in the overridden node."""
+    from oracle.plan import load as _load
+    plan = MP.build_plan(3, 3, False, 5, 3, None, trials=2, seed=3)
+    P = _load(plan)
+    nl = len(P.tensors)
+    node = nl + len(P.tree) // 2
+    rec = {node: None}
+    ref = contract.contract(P, 0, record=rec)
+    lab, t = rec[node]
+    assert np.array_equal(contract.contract(P, 0, override={node: (lab, t)}), ref)
+    assert np.all(contract.contract(P, 0, override={node: (lab, np.zeros_like(t))}) == 0)
+    rng = np.random.default_rng(0)
+    a = rng.standard_normal(t.shape) + 1j * rng.standard_normal(t.shape)
+    b = rng.standard_normal(t.shape) + 1j * rng.standard_normal(t.shape)
+    la = contract.contract(P, 0, override={node: (lab, a)})
+    lb = contract.contract(P, 0, override={node: (lab, b)})
+    lab_ = contract.contract(P, 0, override={node: (lab, 2 * a - 3j * b)})
+    assert np.allclose(lab_, 2 * la - 3j * lb, rtol=1e-12, atol=1e-14 * np.abs(lab_).max())
