@@ -53,8 +53,11 @@ enum {
 enum { TN_CHALF = 0,   /* complex-half: interleaved fp16 (re,im), fp32 accumulation */
        TN_CFLOAT = 1   /* complex64: interleaved fp32, fp32 SIMT FMA (reference-precision path) */ };
 
-/* mode-swap payload codec (Eq. 1, Table 1) */
-enum { TN_COMM_FP16 = 0, TN_COMM_INT8 = 1, TN_COMM_INT4 = 2 };
+/* mode-swap payload codec (Eq. 1, Table 1):
+ *   TN_COMM_INT8 / TN_COMM_INT4: per-block groups of cfg.comm_group reals (power of two >= 16), exp 1
+ *   TN_COMM_INT8_TENSOR: the paper's Table 1 int8 preset: one group per destination chunk
+ *     (the "entire tensor" a peer receives; groups never straddle destinations), exp 0.2 (C-A10) */
+enum { TN_COMM_FP16 = 0, TN_COMM_INT8 = 1, TN_COMM_INT4 = 2, TN_COMM_INT8_TENSOR = 3 };
 
 typedef struct tn_plan tn_plan;
 typedef struct tn_comm tn_comm;
@@ -251,6 +254,16 @@ TN_API int tn_quant_int8_f16(int8_t* d_codes, float* d_scales, float* d_zeros, c
                              int g, void* stream);
 TN_API int tn_dequant_int8_f16(void* d_y, const int8_t* d_codes, const float* d_scales, const float* d_zeros,
                                uint64_t n, int g, void* stream);
+/* Table 1 int8 preset codec with exponent (Eq. 1 with exp, reading C-A10) on fp16 reals, groups of g
+ * reals (g a power of two dividing n; the mode swap uses g = one destination chunk, e = 0.2):
+ * x' = sign(x)|x|^e (double pow, rounded to fp32), scale/zero of Eq. 1 from max/min of x' per group,
+ * code = rint(x' scale + zero) clamped to [-128, 127] (fp32 multiply then add); dequantised
+ * y = sign(y')|y'|^(1/e), y' = (code - zero)/scale, rounded to fp16.  Constant groups: scale 0, zero =
+ * the transformed constant.  d_tmp: device scratch of 8 * n/g bytes.  Two/one kernels. */
+TN_API int tn_quant_int8_exp_f16(int8_t* d_codes, float* d_scales, float* d_zeros, const void* d_x, uint64_t n,
+                                 uint64_t g, double e, void* d_tmp, void* stream);
+TN_API int tn_dequant_int8_exp_f16(void* d_y, const int8_t* d_codes, const float* d_scales, const float* d_zeros,
+                                   uint64_t n, uint64_t g, double e, void* stream);
 /* int4 preset (Table 1: q in [0, 15], exp 1, groups of g reals) on fp16
  * reals: n/2 packed bytes, two codes per byte with the low nibble = even index (reading C-A14);
  * scale = 15/(max-min), zero = -15*min/(max-min) per group (fp32, multiply then add, no FMA;

@@ -146,6 +146,11 @@ void launch_quant_int8_half(int8_t* codes, float* scales, float* zeros, const __
                             cudaStream_t s, const GroupPerm* gp = nullptr);
 void launch_dequant_int8_half(__half* y, const int8_t* codes, const float* scales, const float* zeros, uint64_t n,
                               int g, cudaStream_t s);
+// Table 1 int8 preset (exp != 1, large power-of-two groups); d_tmp holds 2 * n/g uint32
+void launch_quant_int8_exp_half(int8_t* codes, float* scales, float* zeros, const __half* x, uint64_t n, uint64_t g,
+                                double e, uint32_t* d_tmp, cudaStream_t s);
+void launch_dequant_int8_exp_half(__half* y, const int8_t* codes, const float* scales, const float* zeros, uint64_t n,
+                                  uint64_t g, double e, cudaStream_t s);
 
 // ---- device helpers ----
 __host__ __device__ inline int64_t outmap_m(const OutMap& o, uint64_t m) {

@@ -435,4 +435,136 @@ bool make_group_perm(GroupPerm& gp, int n, const int* perm, int g) {
   return true;
 }
 
+// ---- Table 1 int8 preset (int8, group = the entire tensor, exp 0.2), readings C-A10/C-A13 ----
+// x' = sign(x)|x|^exp (evaluated in double, rounded to fp32, as the oracle's _signed_pow); scale and
+// zero of Eq. 1 from max/min of x' over the group; code = rint(x' scale + zero) (fp32 multiply then
+// add); dequant y' = (code - zero)/scale, y = sign(y')|y'|^(1/exp), rounded to fp16.  In a mode swap
+// the "entire tensor" is each destination chunk (groups never straddle destinations).
+// x -> x' is monotone, so max/min of x' over a group are the transforms of max/min of x: pass 1
+// reduces max/min of the fp16 values per group (order-preserving integer atomics), pass 2 encodes.
+__device__ __forceinline__ float spow(float x, double e) {
+  const float r = (float)pow((double)fabsf(x), e);
+  return x < 0.f ? -r : (x > 0.f ? r : 0.f);
+}
+__device__ __forceinline__ uint32_t f2ord(float f) {
+  const uint32_t u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float ord2f(uint32_t u) {
+  return __uint_as_float((u & 0x80000000u) ? (u & 0x7fffffffu) : ~u);
+}
+
+// tiles of T reals (T = min(2048, g), g a power of two): every tile lies in one group
+__global__ void __launch_bounds__(256) minmax_groups_half_kernel(const __half* __restrict__ x, uint64_t n, int tile_log2,
+                                                                 int g_log2, uint32_t* __restrict__ mx_ord,
+                                                                 uint32_t* __restrict__ mn_ord) {
+  const uint64_t T = 1ull << tile_log2, tiles = n >> tile_log2;
+  for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+    float mx = -INFINITY, mn = INFINITY;
+    for (uint64_t i = threadIdx.x; i < T; i += blockDim.x) {
+      const float v = __half2float(x[(t << tile_log2) + i]);
+      mx = fmaxf(mx, v);
+      mn = fminf(mn, v);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+      const uint64_t gi = (t << tile_log2) >> g_log2;
+      atomicMax(mx_ord + gi, f2ord(mx));
+      atomicMin(mn_ord + gi, f2ord(mn));
+    }
+  }
+}
+
+__global__ void init_minmax_kernel(uint32_t* mx_ord, uint32_t* mn_ord, uint64_t ng) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < ng; i += (uint64_t)gridDim.x * blockDim.x) {
+    mx_ord[i] = 0u;           // below every ordered float
+    mn_ord[i] = 0xffffffffu;  // above every ordered float
+  }
+}
+
+__device__ __forceinline__ void group_scale_zero(uint32_t mxo, uint32_t mno, double e, float& scale, float& zero) {
+  const float mx = spow(ord2f(mxo), e), mn = spow(ord2f(mno), e);
+  if (mx == mn) {
+    scale = 0.f;
+    zero = mx;
+  } else {
+    const float den = __fsub_rn(mx, mn);
+    scale = __fdiv_rn(255.f, den);
+    zero = __fdiv_rn(__fsub_rn(__fmul_rn(-128.f, mx), __fmul_rn(127.f, mn)), den);
+  }
+}
+
+__global__ void __launch_bounds__(256) quant_exp_half_kernel(int8_t* __restrict__ codes, float* __restrict__ scales,
+                                                             float* __restrict__ zeros, const __half* __restrict__ x,
+                                                             uint64_t n, int g_log2, double e,
+                                                             const uint32_t* __restrict__ mx_ord,
+                                                             const uint32_t* __restrict__ mn_ord) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t gi = i >> g_log2;
+    float scale, zero;
+    group_scale_zero(mx_ord[gi], mn_ord[gi], e, scale, zero);
+    if ((i & ((1ull << g_log2) - 1)) == 0) {
+      scales[gi] = scale;
+      zeros[gi] = zero;
+    }
+    float c = -128.f;
+    if (scale != 0.f) {
+      c = rintf(__fadd_rn(__fmul_rn(spow(__half2float(x[i]), e), scale), zero));
+      c = fminf(fmaxf(c, -128.f), 127.f);
+    }
+    codes[i] = (int8_t)(int)c;
+  }
+}
+
+__global__ void __launch_bounds__(256) dequant_exp_half_kernel(__half* __restrict__ y, const int8_t* __restrict__ codes,
+                                                               const float* __restrict__ scales,
+                                                               const float* __restrict__ zeros, uint64_t n, int g_log2,
+                                                               double inv_e) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t gi = i >> g_log2;
+    const float s = scales[gi], z = zeros[gi];
+    const float yp = (s == 0.f) ? z : __fdiv_rn(__fsub_rn((float)codes[i], z), s);
+    y[i] = __float2half_rn(spow(yp, inv_e));
+  }
+}
+
+static int log2_exact(uint64_t g) {
+  if (g == 0 || (g & (g - 1))) return -1;
+  int b = 0;
+  while ((1ull << b) < g) ++b;
+  return b;
+}
+
+void launch_quant_int8_exp_half(int8_t* codes, float* scales, float* zeros, const __half* x, uint64_t n, uint64_t g,
+                                double e, uint32_t* d_tmp, cudaStream_t s) {
+  const int gl = log2_exact(g);
+  if (gl < 0 || n % g || !(e > 0.0)) throw TnError{TN_E_INVALID, "int8 exp codec: g must be a power of two dividing n, exp > 0"};
+  if (n == 0) return;
+  const uint64_t ng = n / g;
+  uint32_t* mx = d_tmp;
+  uint32_t* mn = d_tmp + ng;
+  const unsigned gb = (unsigned)std::min<uint64_t>((ng + 255) / 256, 148ull * 8);
+  init_minmax_kernel<<<gb, 256, 0, s>>>(mx, mn, ng);
+  const int tl = std::min(gl, 11);
+  const uint64_t tiles = n >> tl;
+  minmax_groups_half_kernel<<<(unsigned)std::min<uint64_t>(tiles, 148ull * 16), 256, 0, s>>>(x, n, tl, gl, mx, mn);
+  quant_exp_half_kernel<<<(unsigned)std::min<uint64_t>((n + 255) / 256, 148ull * 16), 256, 0, s>>>(codes, scales, zeros, x,
+                                                                                                  n, gl, e, mx, mn);
+  TN_CUDA(cudaGetLastError());
+}
+
+void launch_dequant_int8_exp_half(__half* y, const int8_t* codes, const float* scales, const float* zeros, uint64_t n,
+                                  uint64_t g, double e, cudaStream_t s) {
+  const int gl = log2_exact(g);
+  if (gl < 0 || n % g || !(e > 0.0)) throw TnError{TN_E_INVALID, "int8 exp codec: g must be a power of two dividing n, exp > 0"};
+  if (n == 0) return;
+  dequant_exp_half_kernel<<<(unsigned)std::min<uint64_t>((n + 255) / 256, 148ull * 16), 256, 0, s>>>(y, codes, scales,
+                                                                                                    zeros, n, gl, 1.0 / e);
+  TN_CUDA(cudaGetLastError());
+}
+
 }  // namespace tn

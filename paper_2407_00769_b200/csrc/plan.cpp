@@ -106,6 +106,10 @@ static Plan* load_plan_fixed(const char* json, size_t len, const tn_config* cfg_
   if (cfg.stem_min_log2 < 0) cfg.stem_min_log2 = 20;
   if (cfg.dtype != TN_CHALF && cfg.dtype != TN_CFLOAT) throw err(TN_E_INVALID, "cfg.dtype");
   if (cfg.comm_group <= 0) cfg.comm_group = 128;
+  if (cfg.comm_codec < TN_COMM_FP16 || cfg.comm_codec > TN_COMM_INT8_TENSOR) throw err(TN_E_INVALID, "cfg.comm_codec");
+  if (cfg.comm_codec != TN_COMM_FP16 && cfg.comm_codec != TN_COMM_INT8_TENSOR &&
+      (cfg.comm_group < 16 || (cfg.comm_group & (cfg.comm_group - 1))))
+    throw err(TN_E_INVALID, "cfg.comm_group must be a power of two >= 16 for the group codecs");
   p.cfg = cfg;
   if (world != 1 && world != 2 && world != 4 && world != 8) throw err(TN_E_UNSUPPORTED, "world must be 1, 2, 4 or 8");
   p.world = world;
@@ -397,7 +401,9 @@ static Plan* load_plan_fixed(const char* json, size_t len, const tn_config* cfg_
           // quantise only in the later stages of the path (earlier errors accumulate)
           {
             const int pct = cfg.quant_from_pct < 0 ? 50 : cfg.quant_from_pct;
-            st.quant = cfg.dtype == TN_CHALF && (cfg.comm_codec == TN_COMM_INT8 || cfg.comm_codec == TN_COMM_INT4) &&
+            st.quant = cfg.dtype == TN_CHALF &&
+                       (cfg.comm_codec == TN_COMM_INT8 || cfg.comm_codec == TN_COMM_INT4 ||
+                        cfg.comm_codec == TN_COMM_INT8_TENSOR) &&
                        100.0 * (double)s >= pct * (double)step_nodes.size();
           }
           st.swap_out_pos = out_pos;
@@ -414,7 +420,7 @@ static Plan* load_plan_fixed(const char* json, size_t len, const tn_config* cfg_
             int gb = 0;
             while (cfg.comm_group > 1 && (2 << gb) < cfg.comm_group) ++gb;
             const int nl = (int)snd.size();
-            bool inner = st.quant && !cfg.no_fuse_swap_quant && gb <= nl &&
+            bool inner = st.quant && cfg.comm_codec != TN_COMM_INT8_TENSOR && !cfg.no_fuse_swap_quant && gb <= nl &&
                          (cfg.comm_group & (cfg.comm_group - 1)) == 0;
             for (int q = 0; inner && q < gb; ++q) inner = st.send_perm_axes[nl - 1 - q] == nl - 1 - q;
             st.fuse_quant = inner;
@@ -429,14 +435,18 @@ static Plan* load_plan_fixed(const char* json, size_t len, const tn_config* cfg_
           if (st.quant) {
             // codes + fp32 scales + zeros of the whole local stem are staged in one stem buffer
             // (runtime.cu mode_swap): size the buffers for it (matters for small groups / stems)
-            const uint64_t reals = 2ull << L.size(), ng = reals / (uint64_t)cfg.comm_group;
+            const uint64_t reals = 2ull << L.size();
+            const uint64_t ng = cfg.comm_codec == TN_COMM_INT8_TENSOR ? (1ull << out_pos.size())
+                                                                      : reals / (uint64_t)cfg.comm_group;
             const uint64_t cb = align_up(cfg.comm_codec == TN_COMM_INT4 ? reals / 2 : reals, 256);
-            payload_bytes = std::max<uint64_t>(payload_bytes, cb + 2 * align_up(4 * ng, 256));
+            payload_bytes = std::max<uint64_t>(payload_bytes, cb + 3 * align_up(8 * ng, 256));
           }
           const double n_local = std::ldexp(1.0, (int)L.size());
           const double frac = 1.0 - std::ldexp(1.0, -(int)out_pos.size());
           const double per = !st.quant ? (cfg.dtype == TN_CHALF ? 4.0 : 8.0)
-                                        : ((cfg.comm_codec == TN_COMM_INT4 ? 1.0 : 2.0) + 16.0 / cfg.comm_group);
+                             : cfg.comm_codec == TN_COMM_INT8_TENSOR ? 2.0
+                                                                     : ((cfg.comm_codec == TN_COMM_INT4 ? 1.0 : 2.0) +
+                                                                        16.0 / cfg.comm_group);
           p.swap_bytes += frac * n_local * per;
         }
         st.shard_after = shard;

@@ -427,24 +427,28 @@ void mode_swap(Plan& p, const StemStep& st, const tn_buffers* b, int& cur, cudaS
   std::vector<Xfer> sends, recvs;
   const bool quant = st.quant;  // lowering: int8/int4 codec, complex-half, late enough in the path
   if (quant) {
-    const int g = p.cfg.comm_group;
-    const bool int4 = p.cfg.comm_codec == TN_COMM_INT4;
+    const bool tensor = p.cfg.comm_codec == TN_COMM_INT8_TENSOR;  // Table 1 preset: one group per chunk
     const uint64_t reals = 2 * n_local, creals = 2 * chunk;
+    const uint64_t g = tensor ? creals : (uint64_t)p.cfg.comm_group;
+    const bool int4 = p.cfg.comm_codec == TN_COMM_INT4;
     if (creals % g) throw TnError{TN_E_INFEASIBLE, "swap chunk is not a multiple of the quantisation group"};
     const uint64_t ng = reals / g, cng = creals / g;
     const uint64_t cbytes = int4 ? creals / 2 : creals;  // code bytes per chunk
     const uint64_t codes_bytes = align_up(int4 ? reals / 2 : reals, 256);
     // codes + scales + zeros live in one stem buffer (the lowering sizes the buffers for it)
-    if (codes_bytes + 2 * align_up(4 * ng, 256) > b->stem_bytes)
+    if (codes_bytes + 3 * align_up(8 * ng, 256) > b->stem_bytes)
       throw TnError{TN_E_CAPACITY, "quantised swap payload exceeds the stem buffer"};
     auto codes = [&](unsigned char* base) { return reinterpret_cast<int8_t*>(base); };
     auto scales = [&](unsigned char* base) { return reinterpret_cast<float*>(base + codes_bytes); };
     auto zeros = [&](unsigned char* base) { return reinterpret_cast<float*>(base + codes_bytes + align_up(4 * ng, 256)); };
-    if (int4)
+    if (tensor)
+      launch_quant_int8_exp_half(codes(Y), scales(Y), zeros(Y), reinterpret_cast<const __half*>(X), reals, g, 0.2,
+                                 reinterpret_cast<uint32_t*>(Y + codes_bytes + 2 * align_up(4 * ng, 256)), s);
+    else if (int4)
       launch_quant_int4_half(reinterpret_cast<uint8_t*>(codes(Y)), scales(Y), zeros(Y), reinterpret_cast<const __half*>(X),
-                             reals, g, s, fused ? &gp : nullptr);
+                             reals, (int)g, s, fused ? &gp : nullptr);
     else
-      launch_quant_int8_half(codes(Y), scales(Y), zeros(Y), reinterpret_cast<const __half*>(X), reals, g, s,
+      launch_quant_int8_half(codes(Y), scales(Y), zeros(Y), reinterpret_cast<const __half*>(X), reals, (int)g, s,
                              fused ? &gp : nullptr);
     for (int v = 0; v < (1 << sx); ++v) {
       if (v == me) continue;
@@ -460,11 +464,13 @@ void mode_swap(Plan& p, const StemStep& st, const tn_buffers* b, int& cur, cudaS
     TN_CUDA(cudaMemcpyAsync(codes(X) + me * cbytes, codes(Y) + me * cbytes, cbytes, cudaMemcpyDeviceToDevice, s));
     TN_CUDA(cudaMemcpyAsync(scales(X) + me * cng, scales(Y) + me * cng, 4 * cng, cudaMemcpyDeviceToDevice, s));
     TN_CUDA(cudaMemcpyAsync(zeros(X) + me * cng, zeros(Y) + me * cng, 4 * cng, cudaMemcpyDeviceToDevice, s));
-    if (int4)
+    if (tensor)
+      launch_dequant_int8_exp_half(reinterpret_cast<__half*>(Y), codes(X), scales(X), zeros(X), reals, g, 0.2, s);
+    else if (int4)
       launch_dequant_int4_half(reinterpret_cast<__half*>(Y), reinterpret_cast<const uint8_t*>(codes(X)), scales(X),
-                               zeros(X), reals, g, s);
+                               zeros(X), reals, (int)g, s);
     else
-      launch_dequant_int8_half(reinterpret_cast<__half*>(Y), codes(X), scales(X), zeros(X), reals, g, s);
+      launch_dequant_int8_half(reinterpret_cast<__half*>(Y), codes(X), scales(X), zeros(X), reals, (int)g, s);
     p.launches += 2;
   } else {
     const uint64_t cb = chunk * eb;  // bytes per chunk
@@ -1204,6 +1210,19 @@ int tn_permute_quant_f16(void* d_codes, float* d_scales, float* d_zeros, const v
     else
       launch_quant_int4_half((uint8_t*)d_codes, d_scales, d_zeros, (const __half*)d_x, reals, g, (cudaStream_t)stream, &gp);
   });
+}
+
+int tn_quant_int8_exp_f16(int8_t* d_codes, float* d_scales, float* d_zeros, const void* d_x, uint64_t n, uint64_t g,
+                          double e, void* d_tmp, void* stream) {
+  if (!d_codes || !d_scales || !d_zeros || !d_x || !d_tmp) return fail(TN_E_INVALID, "NULL argument");
+  TN_TRY(launch_quant_int8_exp_half(d_codes, d_scales, d_zeros, (const __half*)d_x, n, g, e, (uint32_t*)d_tmp,
+                                    (cudaStream_t)stream));
+}
+
+int tn_dequant_int8_exp_f16(void* d_y, const int8_t* d_codes, const float* d_scales, const float* d_zeros, uint64_t n,
+                            uint64_t g, double e, void* stream) {
+  if (!d_y || !d_codes || !d_scales || !d_zeros) return fail(TN_E_INVALID, "NULL argument");
+  TN_TRY(launch_dequant_int8_exp_half((__half*)d_y, d_codes, d_scales, d_zeros, n, g, e, (cudaStream_t)stream));
 }
 
 int tn_quant_int4_f16(uint8_t* d_packed, float* d_scales, float* d_zeros, const void* d_x, uint64_t n, int g,

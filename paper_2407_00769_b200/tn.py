@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libtn.so")
 
 TN_CHALF, TN_CFLOAT = 0, 1
-TN_COMM_FP16, TN_COMM_INT8, TN_COMM_INT4 = 0, 1, 2
+TN_COMM_FP16, TN_COMM_INT8, TN_COMM_INT4, TN_COMM_INT8_TENSOR = 0, 1, 2, 3
 ERRORS = {0: "TN_OK", -1: "TN_E_INVALID", -2: "TN_E_PARSE", -3: "TN_E_INFEASIBLE", -4: "TN_E_CAPACITY",
           -5: "TN_E_CUDA", -6: "TN_E_NCCL", -7: "TN_E_UNSUPPORTED"}
 
@@ -80,6 +80,8 @@ def lib():
         L.tn_quant_int4_f16.argtypes = [vp, vp, vp, vp, u64, i32, vp]
         L.tn_permute_quant_f16.argtypes = [vp, vp, vp, vp, i32, vp, i32, i32, vp]
         L.tn_dequant_int4_f16.argtypes = [vp, vp, vp, vp, u64, i32, vp]
+        L.tn_quant_int8_exp_f16.argtypes = [vp, vp, vp, vp, u64, u64, C.c_double, vp, vp]
+        L.tn_dequant_int8_exp_f16.argtypes = [vp, vp, vp, vp, u64, u64, C.c_double, vp]
         L.tn_comm_unique_id.argtypes = [vp]
         L.tn_comm_init.argtypes = [vp, i32, i32, i32, C.POINTER(vp)]
         L.tn_comm_init_loopback.argtypes = [i32, i32, vp]
@@ -293,6 +295,16 @@ def tn_permute_quant_f16(codes, scales, zeros, x, perm, g, codec=TN_COMM_INT8, s
     arr = (C.c_int * max(n, 1))(*perm)
     _check(lib().tn_permute_quant_f16(_ptr(codes), _ptr(scales), _ptr(zeros), _ptr(x), n, arr, g, codec,
                                       _stream(stream)))
+
+
+def tn_quant_int8_exp_f16(codes, scales, zeros, x, g, e, tmp, stream=None):
+    _check(lib().tn_quant_int8_exp_f16(_ptr(codes), _ptr(scales), _ptr(zeros), _ptr(x), x.numel(), g, e, _ptr(tmp),
+                                       _stream(stream)))
+
+
+def tn_dequant_int8_exp_f16(y, codes, scales, zeros, g, e, stream=None):
+    _check(lib().tn_dequant_int8_exp_f16(_ptr(y), _ptr(codes), _ptr(scales), _ptr(zeros), y.numel(), g, e,
+                                         _stream(stream)))
 
 
 def tn_quant_int4_f16(packed, scales, zeros, x, g, stream=None):

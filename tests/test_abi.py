@@ -169,7 +169,7 @@ def test_fused_permutation_lowering(tnmod, name):
         assert s["out"][:len(kept)] == kept              # kept modes in stored order, then new modes
 
 
-@pytest.mark.parametrize("world,g", [(8, 128), (4, 32), (2, 8)])
+@pytest.mark.parametrize("world,g", [(8, 128), (4, 32), (2, 16)])
 def test_fused_swap_codec_lowering(tnmod, world, g):
     """Sender permutation folded into the swap codec (north_star (5)): a swap is marked fuse_quant
     exactly when it is quantised, needs a sender permutation, and that permutation keeps the
@@ -240,3 +240,16 @@ def test_split_tail_with_sharded_stem_lowering(tnmod, world):
                 assert not sm & set(s["swap_in"])
             if s["split"]:
                 assert set(s["in"][:j]) == sm or s is tail[0]
+
+
+def test_codec_group_validation(tnmod, c1_plan):
+    """ADVICE (round 1): the group codecs stage codes + scales + zeros in one stem buffer, which only
+    fits for groups of >= 16 reals; other groups are refused at load time."""
+    for g in (8, 24, 0x7fff):
+        with pytest.raises(tnmod.TnError) as e:
+            _load(tnmod, c1_plan, stem_min_log2=6, comm_codec=tnmod.TN_COMM_INT8, comm_group=g)
+        assert e.value.code == -1
+    _load(tnmod, c1_plan, stem_min_log2=6, comm_codec=tnmod.TN_COMM_INT8, comm_group=16)
+    _load(tnmod, c1_plan, stem_min_log2=6, comm_codec=tnmod.TN_COMM_INT8_TENSOR, comm_group=8)
+    with pytest.raises(tnmod.TnError):
+        _load(tnmod, c1_plan, stem_min_log2=6, comm_codec=7)

