@@ -7,7 +7,7 @@ A step = one subtask: tn_stem_contract (common phase + Eq. 6 padding + all stem 
 tn_split_contract, inputs (leaves) resident in HBM.  value = effective TFLOPS of the job (8 flops
 per complex MAC of the stem GEMMs, reading C-A21) / max-over-ranks device time.
 Multi-GPU (C4): ONE subtask sharded across the N GPUs on its log2 N outermost modes, with
-int8-quantised (late-stage, P:612-618) or fp16 NCCL mode swaps (Alg. 1) — strong scaling.
+int8-quantised (late-stage, P:620-621) or fp16 NCCL mode swaps (Alg. 1) — strong scaling.
 --replicas runs independent slices per GPU instead (weak scaling, no collective).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--plan c3]

@@ -86,7 +86,7 @@ typedef struct {
                                 modes innermost (scatter epilogue, no permutation passes);
                                 1: scatter when its stores are >= 64 B contiguous, else as 0 */
   int32_t quant_from_pct;    /* int8/int4 swaps only at stem steps >= this percentage of the path
-                                (P:612-618 "quantify in the later stages"); earlier swaps send
+                                (P:620-621 "quantify in the later stages"); earlier swaps send
                                 fp16.  Negative: 50 */
   int32_t virtual_world;     /* > 1 with comm == NULL: lower the plan for that many ranks
                                 (host-only inspection of the shard/swap schedule) */

@@ -386,7 +386,7 @@ __global__ void __launch_bounds__(kAMode == 1 ? kThreadsGather : kThreads, 1)
           b_resident = pn == n0;
         }
         for (int kb = 0; kb < num_k; ++kb, ++qa) {
-          if (kAMode == 3) {
+          if constexpr (kAMode == 3) {
             // A: the raw box (source order) into raw slot qa % kRaw, for warps 2-3 to reshuffle
             const int r = (int)(qa % C::kRaw);
             mbar_wait(&raw_empty[r], ((qa / C::kRaw) & 1) ^ 1);
@@ -455,6 +455,7 @@ __global__ void __launch_bounds__(kAMode == 1 ? kThreadsGather : kThreads, 1)
       }
     }
   } else if (kAMode == 3 && (warp == 2 || warp == 3)) {
+    if constexpr (kAMode == 3) {
     // ===== A reshuffle (warps 2 and 3, alternate iterations): raw slot (source order) ->
     // interleaved K-major stage, 16-byte pieces, bank-conflict-free enumeration (NdArgs)
     const int h = warp - 2;
@@ -516,6 +517,7 @@ __global__ void __launch_bounds__(kAMode == 1 ? kThreadsGather : kThreads, 1)
           mbar_arrive(&raw_empty[r]);
         }
       }
+    }
     }
   } else if (kGather && warp >= 12) {
     // ===== A gather (fused stem permutation): warp g fills the ring slots s = g mod 4 with
@@ -818,12 +820,9 @@ static CUtensorMap make_map_2d(const void* base, uint64_t inner, uint64_t outer,
 }
 
 static int num_sms() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    TN_CUDA(cudaGetDevice(&dev));
-    TN_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
-  }
+  int dev = 0, n = 0;
+  TN_CUDA(cudaGetDevice(&dev));
+  TN_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
   return n;
 }
 
@@ -867,11 +866,19 @@ static void launch_bn(__half* c, const __half* a, const __half* bp, uint64_t M, 
                       cudaStream_t s, const AGather* ag, const NdPlan* np) {
   const uint32_t N2 = std::max<uint32_t>(N2_real, 16);  // B_P has at least 16 (zero-padded) rows
   using C = tc::Cfg<BN, KB, G == 3 ? 1 : 0>;
-  static bool attr = false;
-  if (!attr) {
-    TN_CUDA(cudaFuncSetAttribute(tc::gemm_chalf_tc_kernel<BN, KB, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 C::kSmem));
-    attr = true;
+  {
+    // the dynamic shared-memory opt-in is per device: remember it per device ordinal (a process may
+    // drive several devices, e.g. one thread per GPU)
+    static std::mutex mu;
+    static uint64_t done = 0;
+    int dev = 0;
+    TN_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    if (dev >= 64 || !((done >> dev) & 1)) {
+      TN_CUDA(cudaFuncSetAttribute(tc::gemm_chalf_tc_kernel<BN, KB, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   C::kSmem));
+      if (dev < 64) done |= 1ull << dev;
+    }
   }
   AGatherArgs gargs;
   memset(&gargs, 0, sizeof(gargs));

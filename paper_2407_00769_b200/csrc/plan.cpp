@@ -315,12 +315,13 @@ static Plan* load_plan_fixed(const char* json, size_t len, const tn_config* cfg_
   };
 
   // ---- steps
-  // Layout policy.  layout_policy 0 (default): every GEMM writes its output with
-  // the modes the NEXT step contracts as the innermost block (scatter epilogue), so each stem
-  // operand is read as stored (K-major) and no standalone permutation pass is needed; the other
-  // modes are ordered by next use, furthest first.  layout_policy 1: output = kept ++ new and a
-  // permutation pass whenever R_i is not innermost (the classic "reorder then GEMM").
-  // public numbering: 0 = permutation passes (default, fastest measured), 1 = hybrid, 2 = scatter
+  // Layout policy (tn.h tn_config.layout_policy).  Public 0 (default): every GEMM writes
+  // kept ++ new (identity output, TMA-store epilogue); a step whose contracted modes are not the
+  // innermost block gets its permutation fused into the GEMM's A load (gathered A) or, when that is
+  // impossible, a standalone permutation pass ("reorder then GEMM").  Public 2: every GEMM
+  // writes the NEXT step's contracted modes innermost (scatter epilogue), so no permutation is ever
+  // needed.  Public 1: scatter only when a thread's stores are >= 64 B contiguous, else as 0.
+  // Internal numbering (below): 1 = public 0, 0 = public 1, 2 = public 2.
   const int policy = cfg.layout_policy == 0 ? 1 : (cfg.layout_policy == 1 ? 0 : cfg.layout_policy);
   const int eb = (cfg.dtype == TN_CHALF) ? 4 : 8;
   uint64_t smax = 0, payload_bytes = 0;
@@ -398,7 +399,7 @@ static Plan* load_plan_fixed(const char* json, size_t len, const tn_config* cfg_
           std::stable_sort(cand.begin(), cand.end(), [&](int a, int b) { return nu(a) > nu(b); });
           if (cand.size() < out_pos.size()) throw err(TN_E_INFEASIBLE, "partition modes run out (swap)");
           st.swap = true;
-          // quantise only in the later stages of the path (earlier errors accumulate)
+          // quantise only in the later stages of the path (earlier errors accumulate), C-A26
           {
             const int pct = cfg.quant_from_pct < 0 ? 50 : cfg.quant_from_pct;
             st.quant = cfg.dtype == TN_CHALF &&
@@ -488,7 +489,6 @@ static Plan* load_plan_fixed(const char* json, size_t len, const tn_config* cfg_
       for (int l : B)
         if (std::find(R.begin(), R.end(), l) == R.end()) newl.push_back(l);
       std::vector<int> out;
-      bool scatter = false;
       if (policy == 0 || policy == 2) {
         if (s + 1 == step_nodes.size()) {
           // the last step writes the result directly in output order (local modes only)
@@ -496,7 +496,6 @@ static Plan* load_plan_fixed(const char* json, size_t len, const tn_config* cfg_
             if (split_set.count(l)) out.push_back(l);
           for (int l : p.open)
             if (std::find(shard.begin(), shard.end(), l) == shard.end() && !split_set.count(l)) out.push_back(l);
-          scatter = true;
         } else {
           // [rest by next use] ++ [kept ∩ R_next] ++ [new ∩ R_next]  (new innermost)
           const std::set<int>& Rn = Rsets[s + 1];
@@ -512,7 +511,6 @@ static Plan* load_plan_fixed(const char* json, size_t len, const tn_config* cfg_
             out = rest;
             out.insert(out.end(), kl.begin(), kl.end());
             out.insert(out.end(), nlo.begin(), nlo.end());
-            scatter = true;
           } else {
             // identity output (TMA store): kept ++ [new by next use, new ∩ R_next innermost]
             by_next_use(nhi);
@@ -521,7 +519,6 @@ static Plan* load_plan_fixed(const char* json, size_t len, const tn_config* cfg_
             out.insert(out.end(), nlo.begin(), nlo.end());
           }
         }
-        (void)scatter;
         // B's N order follows the output order of the new labels (outer -> inner)
         std::vector<int> nord;
         for (int l : out)

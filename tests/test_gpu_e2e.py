@@ -43,7 +43,8 @@ def run_gpu(tn, plan, dtype, slice_id=0, stem_min_log2=6, policy=0):
 @pytest.mark.parametrize("dtype", [0, 1])
 @pytest.mark.parametrize("stem_min", [6, 8, 10])
 def test_c1_full_state_vs_oracle(tn, dtype, stem_min, policy):
-    """policy 0: scatter-epilogue layouts (no permutation passes); 1: permutation passes."""
+    """public layout policies (tn.h): 0 = identity outputs + fused/standalone permutations, 1 = hybrid,
+    2 = scatter-epilogue layouts (no permutation passes)."""
     plan = _plan("c1")
     ref = contract.contract(load(plan), 0)
     got, p = run_gpu(tn, plan, dtype, 0, stem_min, policy)

@@ -112,8 +112,11 @@ def predicted_swap_error(plan, rep, ref, preset):
         glay = list(st["shard_before"]) + list(st["send_layout"])
         x = np.transpose(t, [lab.index(l) for l in glay])
         re = np.stack([x.real, x.imag], axis=-1).astype(np.float32).reshape(-1)
-        c, sc, ze = codec.quantize(re, qmin, qmax, ex, g, rnd)
-        y = codec.dequantize(c, sc, ze, ex, g).astype(np.float64).reshape(x.shape + (2,))
+        # Table 1 int8 preset: one group per destination chunk (the reals after the rank bits and the
+        # swapped-in modes)
+        gi = g if g is not None else 2 << (len(st["send_layout"]) - len(st["swap_out_pos"]))
+        c, sc, ze = codec.quantize(re, qmin, qmax, ex, gi, rnd)
+        y = codec.dequantize(c, sc, ze, ex, gi).astype(np.float64).reshape(x.shape + (2,))
         e = (y[..., 0] + 1j * y[..., 1]) - x
         e = np.transpose(e, [glay.index(l) for l in lab])
         le = contract.contract(P, 0, override={stem_in[i]: (lab, e)})
@@ -122,14 +125,14 @@ def predicted_swap_error(plan, rep, ref, preset):
 
 
 @pytest.mark.parametrize("world", [2, 4, 8])
-@pytest.mark.parametrize("codec", ["int8", "int4"])
+@pytest.mark.parametrize("codec", ["int8", "int4", "int8_tensor"])
 def test_loopback_quantised_swaps_vs_oracle(tn, c3sub, world, codec):
     """Default late-stage policy (C-A26) and every swap quantised, against the error the
     oracle predicts for exactly these swaps (C-A32): the GPU error may exceed the prediction only
     by fp16 storage and the randomness of the codec's rounding (factor 2)."""
     sub, ref = c3sub
-    cc = {"int8": tn.TN_COMM_INT8, "int4": tn.TN_COMM_INT4}[codec]
-    preset = {"int8": "int8_g128", "int4": "int4"}[codec]
+    cc = {"int8": tn.TN_COMM_INT8, "int4": tn.TN_COMM_INT4, "int8_tensor": tn.TN_COMM_INT8_TENSOR}[codec]
+    preset = {"int8": "int8_g128", "int4": "int4", "int8_tensor": "int8"}[codec]
     fp16 = run_loopback(tn, sub, world, dict(stem_min_log2=14, comm_codec=tn.TN_COMM_FP16))
     e16 = metrics.rel_l2(fp16[0][0], ref)
     for pct in (-1, 0):
@@ -192,9 +195,9 @@ def test_loopback_split_tail_sharded(tn, world, split):
 
 def test_loopback_sparse_batch_sharded(tn):
     """Sparse-state batch with a sharded stem: same subspaces and picks as one GPU."""
-    plan = MP.build_plan(3, 4, False, 8, 12, None, trials=2, seed=0)
-    kw = dict(dtype=0, stem_min_log2=6, split_log2=4, comm_codec=tn.TN_COMM_FP16)
-    pre = np.array([3, 0, 15, 7, 9], dtype=np.uint64)
+    plan = MP.sub_slice(_plan("c2"), 20)
+    kw = dict(dtype=0, stem_min_log2=12, split_log2=3, comm_codec=tn.TN_COMM_FP16)
+    pre = np.array([3, 0, 7, 5], dtype=np.uint64)
     p1 = tn.Plan(plan, tn.make_config(**kw))
     b1 = tn.Buffers(p1)
     tn.tn_plan_upload(p1, b1)
