@@ -31,10 +31,18 @@ sys.path.insert(0, ROOT)
 
 METRIC = "stem-contraction effective TFLOPS/GPU and subtask time-to-solution at 1/2/4/8 B200"
 WORKLOADS = {
-    "c3": "C3: 53-qubit (6x9 grid minus a corner) 20-cycle Sycamore-style RQC network, one sliced subtask, "
-          "6 open legs, largest stem 2^33 complex-half, stem buffers 2 x 32 GiB",
+    "c3": "C3: 53-qubit (6x9 grid minus a corner) 20-cycle Sycamore-style RQC network, one sliced subtask "
+          "(158 sliced edges, branch-grouped stem: MB-scale non-stem tensors), 6 open legs, largest stem 2^32 "
+          "complex-half, stem buffers 2 x 16 GiB",
+    "c3_sweep": "C3 (round-1 plan, memory-bound variant): same network, 188 sliced edges, 12-branch groups, "
+                "largest stem 2^33 complex-half, stem buffers 2 x 32 GiB",
     "c2": "C2: 30-qubit (5x6) 14-cycle RQC, one sliced subtask, 10 open legs",
 }
+
+
+# layout policy per plan (tn.h tn_config.layout_policy): the grouped C3 steps are mostly compute-bound,
+# so writing every output in the next step's order (scatter epilogue, no permutation passes) wins
+DEFAULT_POLICY = {"c3": 2}
 
 
 def peaks():
@@ -144,7 +152,20 @@ def cpu_baseline(plan, target_log2, steps=1, warmup=0):
     return {"value": fl / t / 1e12, "unit": "TFLOPS", "cores": _CORES, "kind": "oracle",
             "seconds": t, "sample": f"oracle (numpy complex128, np.tensordot) on slice 0 of the same plan "
                                    f"sub-sliced by {len(sub['sliced']) - len(plan['sliced'])} extra edges "
-                                   f"(every intermediate <= 2^{target_log2}); {fl:.3e} flops in {t:.2f} s"}
+                                   f"(every intermediate <= 2^{target_log2}); {fl:.3e} flops in {t:.2f} s"}, sub
+
+
+def parity(tn, sub, cfg_kw):
+    """The GPU path on the oracle's sub-slice (same plan, same kernels, fewer modes; SURVEY §8(c) c.6
+    step 1) against the oracle's complex128 amplitudes: rel-L2, bound 2e-2 (north_star)."""
+    from oracle import contract, metrics
+    from oracle.plan import load
+    ref = contract.contract(load(sub), 0)
+    p = tn.Plan(sub, tn.make_config(**cfg_kw))
+    got = tn.contract(p, tn.Buffers(p), 0)
+    return {"rel_l2_vs_oracle": metrics.rel_l2(got, ref), "bound": 2e-2,
+            "sample": f"slice 0 of the plan sub-sliced to max 2^{p.info()['max_stem_log2']} "
+                      f"({len(sub['sliced'])} sliced edges), complex-half GPU path vs oracle complex128"}
 
 
 def main():
@@ -157,7 +178,8 @@ def main():
     ap.add_argument("--oracle-log2", type=int, default=24)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--replicas", action="store_true", help="N>1: independent slices per GPU (weak scaling)")
-    ap.add_argument("--comm", default="int8", choices=["int8", "int4", "fp16"])
+    ap.add_argument("--comm", default="int8", choices=["int8", "int4", "fp16", "int8_tensor"])
+    ap.add_argument("--policy", type=int, default=-1, help="layout policy (tn.h); -1: the plan's default")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -196,8 +218,11 @@ def main():
 
     sharded = world > 1 and not args.replicas
     comm = tn.Comm(rank, world, local) if sharded else None
-    codec = {"int8": tn.TN_COMM_INT8, "int4": tn.TN_COMM_INT4}.get(args.comm, tn.TN_COMM_FP16)
-    p = tn.Plan(plan_json, tn.make_config(dtype=tn.TN_CHALF, stem_min_log2=20, comm_codec=codec), comm=comm)
+    codec = {"int8": tn.TN_COMM_INT8, "int4": tn.TN_COMM_INT4, "int8_tensor": tn.TN_COMM_INT8_TENSOR}.get(
+        args.comm, tn.TN_COMM_FP16)
+    policy = args.policy if args.policy >= 0 else DEFAULT_POLICY.get(args.plan, 0)
+    p = tn.Plan(plan_json, tn.make_config(dtype=tn.TN_CHALF, stem_min_log2=20, comm_codec=codec,
+                                          layout_policy=policy), comm=comm)
     info = p.info()
     bufs = tn.Buffers(p)
     n_sl = min(info["n_slices_log2"], 63)
@@ -294,7 +319,8 @@ def main():
         else:
             ach = gemm_flops / (gemm_ms * 1e-3) / 1e12
             roof = {"kernel": "gemm_chalf_tc", "bound": "tensor", "achieved": ach, "peak": tc_burst,
-                    "unit": "TFLOP/s", "frac": ach / tc_burst}
+                    "unit": "TFLOP/s", "frac": ach / tc_burst, "peak_sustained": tc_sus,
+                    "frac_sustained": ach / tc_sus, "peak_spec": 2250.0, "frac_spec": ach / 2250.0}
         roof["roofline_time_frac"] = t_roof_gemm / gemm_ms if gemm_ms else None
         roof["launches_per_step"] = len(steps)
     else:
@@ -324,7 +350,9 @@ def main():
                            "mode_swaps": rep.get("n_swaps", 0), "swap_bytes_per_rank": rep.get("swap_bytes", 0),
                            "stem_steps": info["n_stem_steps"], "permutes": info["n_permutes"],
                            "max_stem_log2": info["max_stem_log2"], "stem_flops": flops,
-                           "l2": "inputs larger than L2 (stem tensors up to 32 GiB >> 126 MB)"},
+                           "layout_policy": policy,
+                           "l2": f"inputs larger than L2 (stem tensors up to {info['stem_bytes'] / 2**30:.0f} GiB "
+                                 f">> 126 MB)"},
                 "tflops_per_gpu": value / world, "subtask_ms": t_ms,
                 "breakdown_ms": {"common+prep": common_ms, "permute": perm_ms, "gemm": gemm_ms},
                 "roofline": roof,
@@ -340,9 +368,12 @@ def main():
                  "note": "context only (SURVEY 8(f) #4); a step = one subtask (sharded) or one per rank"}}
         if world == 1 and not args.no_cpu:
             try:
-                line["cpu_baseline"] = cpu_baseline(plan_json, args.oracle_log2)
+                line["cpu_baseline"], sub = cpu_baseline(plan_json, args.oracle_log2)
+                line["parity"] = parity(tn, sub, dict(dtype=tn.TN_CHALF, stem_min_log2=min(20, args.oracle_log2 - 4),
+                                                      layout_policy=policy))
             except Exception as e:  # the oracle must not take the GPU number down with it
-                line["cpu_baseline"] = {"error": str(e)}
+                line.setdefault("cpu_baseline", {"error": str(e)})
+                line["parity"] = {"error": str(e)}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -222,6 +222,30 @@ TN_API int tn_gemm_chalf_gather(void* d_c, const void* d_a, const void* d_bp, in
                                 const int64_t* m_stride, const int64_t* k_stride, const float* d_in_max,
                                 const float* d_b_bound, uint32_t* d_out_max, int* d_exp, void* stream);
 
+/* Gather-batched complex-half GEMM (sparse-state contraction, P:533-537 and Fig. 5 bottom:
+ * "obtain multiple tensors at specified positions through the indices Index_A and Index_B to form
+ * A_I and B_I before performing matrix multiplication"):
+ *   C[b] = 2^e A[index_a[b]] B[index_b[b]],  b < n_out,
+ * one tcgen05 launch for the whole batch (A_I / B_I are never materialised: the TMA loads read the
+ * indexed entries in place).  A: n_a entries of [M][K] complex-half (interleaved fp16, row-major,
+ * entry a at element a*M*K); B_P: n_b blocks of fp16 [2N][2K] (tn_gemm_chalf's B_P layout, block j at
+ * element j*4*N*K); C: n_out entries of [M][N] complex-half.  index_a / index_b: DEVICE int32 arrays
+ * of n_out entries (< n_a / < n_b; not checked on the device).  M a multiple of 128, K >= 4 and N >= 8
+ * powers of two; the scale pointers as tn_gemm_chalf (one exponent for the whole batch). */
+TN_API int tn_gemm_chalf_batched(void* d_c, const void* d_a, const void* d_bp, uint64_t M, uint32_t K, uint32_t N,
+                                 uint64_t n_out, const int32_t* d_index_a, const int32_t* d_index_b, uint64_t n_a,
+                                 uint64_t n_b, const float* d_in_max, const float* d_b_bound, uint32_t* d_out_max,
+                                 int* d_exp, void* stream);
+/* Padded 2-d index variant (Fig. 5 top: "we use the input tensor A directly ... padding
+ * Index_B to a new 2d-index whose size is m_a*m_r ... excess positions are replaced with -1 ...
+ * C_P = A x B_P"): C_P[a] = A[a] [B[t(a,0)] | B[t(a,1)] | ... | B[t(a,m_r-1)]] for a < n_a, with
+ * t(a,r) = table[a*m_r + r] (DEVICE int32, row-major [n_a][m_r]); t < 0 gives a zero block (its MMA
+ * is skipped).  C_P: n_a entries of [M][m_r*N] complex-half; the valid products are the blocks
+ * with t >= 0 (C is C_P "flattened ... then extract valid tensors in it").  Shapes as above. */
+TN_API int tn_gemm_chalf_padded(void* d_c, const void* d_a, const void* d_bp, uint64_t M, uint32_t K, uint32_t N,
+                                uint64_t n_a, const int32_t* d_table, int m_r, uint64_t n_b, const float* d_in_max,
+                                const float* d_b_bound, uint32_t* d_out_max, int* d_exp, void* stream);
+
 /* Complex64 stem GEMM (fp32 SIMT): C[M,N] = A[M,K] B[K,N], all interleaved complex64 row-major. */
 TN_API int tn_gemm_cfloat(void* d_c, const void* d_a, const void* d_b, uint64_t M, uint32_t K, uint32_t N,
                    void* stream);

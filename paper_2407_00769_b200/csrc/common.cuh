@@ -129,6 +129,20 @@ struct AGather {
 void launch_gemm_chalf_tc(__half* c, const __half* a, const __half* bp, uint64_t M, uint32_t K2,
                           uint32_t N2, const float* in_max, const float* b_bound, uint32_t* out_max,
                           int* exp_slot, const OutMap* om, cudaStream_t s, const AGather* ag = nullptr);
+// Gather-batched tcgen05 GEMM (Fig. 5; see BatchArgs in gemm_tc.cuh): n_out
+// entries of M rows (M % 128 == 0).  Index variant (pad_r == 0): C[b] = A[ia[b]] x B_P[ib[b]].
+// Padded 2-d index (pad_r > 0, n_out = n_a): C_P[a] = A[a] x [B_P[table[a pad_r + r]]]_r, rows of
+// C_P are pad_r blocks of 2N reals, table < 0 -> zero block.  ia/ib/table are device int32 arrays.
+struct BatchSpec {
+  int pad_r = 0;
+  const int* ia = nullptr;
+  const int* ib = nullptr;
+  const int* table = nullptr;
+  uint64_t n_out = 0, n_a = 0, n_b = 0;
+};
+void launch_gemm_chalf_tc_batched(__half* c, const __half* a, const __half* bp, uint64_t M, uint32_t K2, uint32_t N2,
+                                  const float* in_max, const float* b_bound, uint32_t* out_max, int* exp_slot,
+                                  const BatchSpec& bs, cudaStream_t s);
 OutMap identity_map(uint64_t M, uint32_t N);
 // member (open-leg order) index of a stored amplitude: bit (r-1-t) of the member index is bit
 // src_bit[t] of the layout index

@@ -280,7 +280,47 @@ struct NdArgs {
   uint32_t lane_dst[5], it_dst[8];
 };
 
+// Gather-batched operands (§3.4.2 Fig. 5): the launch computes several
+// independent products of identical shape.  Entry b of the output (M rows of C, M a multiple of 128):
+//   index variant (pad_r == 0):  C[b] = A[ia[b]] x B_P[ib[b]]            (Fig. 5 bottom, A_I x B_I)
+//   padded 2-d index (pad_r > 0): C_P[b] = A[b] x [B_P[t_0] | ... | B_P[t_{pad_r-1}]],
+//                                 t_r = table[b * pad_r + r], t_r < 0 -> a zero block (Fig. 5 top)
+// A entry a = rows [a M, (a+1) M) of the A map, B_P block j = rows [j b_rows, (j+1) b_rows) of the B
+// map (b_rows = max(2N, 16)), C entry b = rows [b M, (b+1) M) of the C map (padded: pad_r b_rows
+// columns).  Indices are read on the device, so one launch (or one captured graph) serves any
+// batch; A is never materialised as A_I (a repeated A entry is re-read from L2 by neighbouring tiles).
+struct BatchArgs {
+  int on;
+  int pad_r;
+  const int* ia;
+  const int* ib;
+  const int* table;
+  uint32_t m_tiles;   // 128-row tiles per entry
+  uint64_t rows;      // M
+  uint32_t b_rows;    // rows of one B_P block
+};
+
 namespace tc {
+
+// Tile t -> C tile (m0 row, n0 column), A row and B row of its operands, skip = zero tile.
+__device__ __forceinline__ void batch_tile(const BatchArgs& ba, uint32_t t, uint32_t num_n, int BNv, int& m0, int& n0,
+                                           int& a_row, int& b_row, bool& skip) {
+  const uint32_t per = ba.m_tiles * num_n;
+  const uint32_t b = t / per, rem = t % per, mt = rem / num_n, nt = rem % num_n;
+  m0 = (int)(b * ba.rows + (uint64_t)mt * BM);
+  n0 = (int)(nt * BNv);
+  skip = false;
+  if (ba.pad_r > 0) {
+    const uint32_t per_r = ba.b_rows / BNv, r = nt / per_r, w = nt % per_r;
+    const int j = __ldg(ba.table + (uint64_t)b * ba.pad_r + r);
+    skip = j < 0;
+    a_row = m0;
+    b_row = (int)((skip ? 0 : j) * ba.b_rows + w * BNv);
+  } else {
+    a_row = (int)((uint64_t)__ldg(ba.ia + b) * ba.rows + (uint64_t)mt * BM);
+    b_row = (int)((uint64_t)__ldg(ba.ib + b) * ba.b_rows + nt * BNv);
+  }
+}
 
 __device__ __forceinline__ void cp_async16(uint32_t smem_addr, const void* gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr), "l"(gmem) : "memory");
@@ -308,7 +348,7 @@ __global__ void __launch_bounds__(kAMode == 1 ? kThreadsGather : kThreads, 1)
                          const float* in_max, const float* b_bound, uint32_t* out_max, int* exp_slot,
                          const __grid_constant__ ScatterArgs sc_args, uint32_t* out_scatter, uint64_t rows,
                          uint32_t n_cols, const __grid_constant__ AGatherArgs ga,
-                         const __grid_constant__ NdArgs nda, int epi_stg) {
+                         const __grid_constant__ NdArgs nda, int epi_stg, const __grid_constant__ BatchArgs ba) {
   constexpr bool kGather = kAMode == 1;
   constexpr bool kInter = kAMode == 2 || kAMode == 3;
   using C = Cfg<BN, KB, kAMode == 3 ? 1 : 0>;
@@ -373,14 +413,21 @@ __global__ void __launch_bounds__(kAMode == 1 ? kThreadsGather : kThreads, 1)
       const uint32_t reuse_dist = (uint32_t)C::kStages * gridDim.x;  // tile that last filled this slot
       uint32_t qa = 0;  // stage counter (raw A slots)
       for (uint32_t t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-        int m0, n0;
-        tile_coords(sc_args, t, num_n, BM, BN, m0, n0);
+        int m0, n0, a_row, b_row;
+        bool skip = false;
+        if (ba.on) {
+          batch_tile(ba, t, num_n, BN, m0, n0, a_row, b_row, skip);
+        } else {
+          tile_coords(sc_args, t, num_n, BM, BN, m0, n0);
+          a_row = m0;
+          b_row = n0;
+        }
         int cm[5] = {0, 0, 0, 0, 0};  // row part of the N-d box coordinates (once per tile)
         if (nda.nd > 0) nd_coords_rows(nda, ga.m_base + (uint64_t)m0, cm);
         // single k-block: the slot still holds B of the tile kStages iterations ago; skip the B
         // load when that tile had the same n-block (always when N fits one tile)
         bool b_resident = false;
-        if (num_k == 1 && t >= blockIdx.x + reuse_dist) {
+        if (!ba.on && num_k == 1 && t >= blockIdx.x + reuse_dist) {
           int pm, pn;
           tile_coords(sc_args, t - reuse_dist, num_n, BM, BN, pm, pn);
           b_resident = pn == n0;
@@ -396,7 +443,9 @@ __global__ void __launch_bounds__(kAMode == 1 ? kThreadsGather : kThreads, 1)
             tma_load_nd(sRaw + r * C::kABytes, &tmA, &raw_full[r], nda.nd, cc);
           }
           mbar_wait(&empty[s], ph ^ 1);
-          if (kGather || kAMode == 3) {  // A comes from the gather / reshuffle warps
+          if (skip) {  // zero tile of the padded 2-d index: nothing to load, the MMA is skipped
+            mbar_arrive(&full[s]);
+          } else if (kGather || kAMode == 3) {  // A comes from the gather / reshuffle warps
             if (b_resident) {
               mbar_arrive(&full[s]);
             } else {
@@ -410,9 +459,9 @@ __global__ void __launch_bounds__(kAMode == 1 ? kThreadsGather : kThreads, 1)
               nd_coords_k(nda, (uint32_t)kb * (KB / 2), cm, cc);
               tma_load_nd(sA + s * C::kABytes, &tmA, &full[s], nda.nd, cc);
             } else {
-              tma_load_2d(sA + s * C::kABytes, &tmA, &full[s], kb * KB, m0);
+              tma_load_2d(sA + s * C::kABytes, &tmA, &full[s], kb * KB, a_row);
             }
-            if (!b_resident) tma_load_2d(sB + s * C::kBBytes, &tmB, &full[s], kb * KB, n0);
+            if (!b_resident) tma_load_2d(sB + s * C::kBBytes, &tmB, &full[s], kb * KB, b_row);
           }
           if (++s == C::kStages) {
             s = 0;
@@ -429,12 +478,25 @@ __global__ void __launch_bounds__(kAMode == 1 ? kThreadsGather : kThreads, 1)
       uint32_t i = 0;
       for (uint32_t t = blockIdx.x; t < num_tiles; t += gridDim.x, ++i) {
         const uint32_t acc = i % C::kNAcc, aph = (i / C::kNAcc) & 1;
+        bool skip = false;
+        if (ba.on && ba.pad_r > 0) {
+          int m0, n0, ar, br;
+          batch_tile(ba, t, num_n, BN, m0, n0, ar, br, skip);
+        }
         mbar_wait(&tempty[acc], aph ^ 1);
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + acc * C::kAccStride;
         for (int kb = 0; kb < num_k; ++kb) {
           mbar_wait(&full[s], ph);
           tc_fence_after();
+          if (skip) {  // zero tile: release the stage, no MMA
+            mma_commit(&empty[s]);
+            if (++s == C::kStages) {
+              s = 0;
+              ph ^= 1;
+            }
+            continue;
+          }
           if (kGather && ga.fence) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // experiment knob
           const int nkk = (kb == num_k - 1) ? last_kk : KB / 16;
           const uint64_t ad = kInter ? smem_desc_interleaved(sA + s * C::kABytes)
@@ -637,7 +699,13 @@ __global__ void __launch_bounds__(kAMode == 1 ? kThreadsGather : kThreads, 1)
     for (uint32_t t = blockIdx.x + grp * gridDim.x, i = grp; t < num_tiles; t += 2 * gridDim.x, i += 2) {
       const uint32_t acc = i % C::kNAcc, aph = (i / C::kNAcc) & 1;
       int m0, n0;
-      tile_coords(sc_args, t, num_n, BM, BN, m0, n0);
+      bool skip = false;
+      if (ba.on) {
+        int ar, br;
+        batch_tile(ba, t, num_n, BN, m0, n0, ar, br, skip);
+      } else {
+        tile_coords(sc_args, t, num_n, BM, BN, m0, n0);
+      }
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
       const uint32_t taddr = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * C::kAccStride;
@@ -681,6 +749,7 @@ __global__ void __launch_bounds__(kAMode == 1 ? kThreadsGather : kThreads, 1)
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
             float x0 = __uint_as_float(r[h][2 * j]) * sc, x1 = __uint_as_float(r[h][2 * j + 1]) * sc;
+            if (skip) x0 = x1 = 0.f;  // zero block of the padded 2-d index (TMEM was not written)
             __half2 hv = __floats2half2_rn(x0, x1);
             float2 hf = __half22float2(hv);
             if (j < nvalid) mx = fmaxf(mx, fmaxf(fabsf(hf.x), fabsf(hf.y)));
@@ -863,7 +932,7 @@ static CUtensorMap make_map_nd(const void* base, const NdPlan& np) {
 template <int BN, int KB, int G>
 static void launch_bn(__half* c, const __half* a, const __half* bp, uint64_t M, uint32_t K2, uint32_t N2_real,
                       const float* in_max, const float* b_bound, uint32_t* out_max, int* exp_slot, const OutMap* om,
-                      cudaStream_t s, const AGather* ag, const NdPlan* np) {
+                      cudaStream_t s, const AGather* ag, const NdPlan* np, const BatchSpec* bs) {
   const uint32_t N2 = std::max<uint32_t>(N2_real, 16);  // B_P has at least 16 (zero-padded) rows
   using C = tc::Cfg<BN, KB, G == 3 ? 1 : 0>;
   {
@@ -950,6 +1019,46 @@ static void launch_bn(__half* c, const __half* a, const __half* bp, uint64_t M, 
     for (int j = 0; j < kMaxModes; ++j) sa.ms[j] = om->ms[j];
     for (int j = 0; j < 24; ++j) sa.ns[j] = om->ns[j];
   }
+  if (bs) {
+    // gather-batched launch (Fig. 5): one launch over every entry, plain 2-D maps over all entries
+    if (G != 0 || np || (om && !om->identity) || N2_real < 16 || M % tc::BM)
+      throw TnError{TN_E_INVALID, "batched GEMM: needs M % 128 == 0, 2N >= 16, identity output, plain A"};
+    BatchArgs ba;
+    memset(&ba, 0, sizeof(ba));
+    ba.on = 1;
+    ba.pad_r = bs->pad_r;
+    ba.ia = bs->ia;
+    ba.ib = bs->ib;
+    ba.table = bs->table;
+    ba.m_tiles = (uint32_t)(M / tc::BM);
+    ba.rows = M;
+    ba.b_rows = N2;
+    const uint32_t cols = bs->pad_r > 0 ? (uint32_t)bs->pad_r * N2 : N2;  // C columns per row
+    if (N2 % BN) throw TnError{TN_E_INVALID, "batched GEMM: B block rows must be a multiple of the tile"};
+    const uint64_t a_rows = (uint64_t)bs->n_a * M, c_rows = (uint64_t)bs->n_out * M;
+    const uint64_t b_rows_all = (uint64_t)bs->n_b * N2;
+    if (a_rows >= (1ull << 31) || c_rows >= (1ull << 31) || b_rows_all >= (1ull << 31))
+      throw TnError{TN_E_UNSUPPORTED, "batched GEMM: more than 2^31 rows"};
+    CUtensorMap ma = make_map_2d(a, K2, a_rows, KB, tc::BM);
+    CUtensorMap mbm = make_map_2d(bp, K2, b_rows_all, KB, BN);
+    CUtensorMap mc = make_map_2d(c, cols, c_rows, 64, tc::BM);
+    const uint32_t num_n = cols / BN;
+    const uint64_t tiles = (uint64_t)bs->n_out * ba.m_tiles * num_n;
+    if (tiles == 0) return;
+    if (tiles >= (1ull << 32)) throw TnError{TN_E_UNSUPPORTED, "batched GEMM: too many tiles"};
+    const int grid = (int)std::min<uint64_t>(tiles, (uint64_t)num_sms());
+    ScatterArgs sa0;
+    memset(&sa0, 0, sizeof(sa0));
+    AGatherArgs g0;
+    memset(&g0, 0, sizeof(g0));
+    NdArgs n0;
+    memset(&n0, 0, sizeof(n0));
+    tc::gemm_chalf_tc_kernel<BN, KB, G><<<grid, tc::kThreads, C::kSmem, s>>>(
+        ma, mbm, mc, (uint32_t)(tiles / num_n), num_n, (int)K2, in_max, b_bound, out_max, exp_slot, sa0,
+        reinterpret_cast<uint32_t*>(c), c_rows, cols / 2, g0, n0, 0, ba);
+    TN_CUDA(cudaGetLastError());
+    return;
+  }
   CUtensorMap mb = make_map_2d(bp, K2, N2_real, KB, BN);  // rows >= 2N: TMA zero fill
   // output store mode: 0 = one 128-row TMA store per subtile after a group barrier.  Experiments
   // (TN_STG_EPI): 1 = LSU stores from the staged subtile (slower); 2 = evict-first L2 hint (mixed);
@@ -974,7 +1083,7 @@ static void launch_bn(__half* c, const __half* a, const __half* bp, uint64_t M, 
     // the exponent is recorded once (first chunk); later chunks reuse the same inputs
     tc::gemm_chalf_tc_kernel<BN, KB, G><<<grid, G == 1 ? tc::kThreadsGather : tc::kThreads, C::kSmem, s>>>(
         ma, mb, mc, num_m, num_n, (int)K2, in_max, b_bound, out_max, m_off ? nullptr : exp_slot, sa, out_sc, mm,
-        n_cols, gargs, nda, epi_stg);
+        n_cols, gargs, nda, epi_stg, BatchArgs{});
     TN_CUDA(cudaGetLastError());
   }
 }
@@ -982,26 +1091,26 @@ static void launch_bn(__half* c, const __half* a, const __half* bp, uint64_t M, 
 template <int KB, int G>
 static void launch_k(__half* c, const __half* a, const __half* bp, uint64_t M, uint32_t K2, uint32_t N2,
                      const float* in_max, const float* b_bound, uint32_t* out_max, int* exp_slot, const OutMap* om,
-                     cudaStream_t s, const AGather* ag, const NdPlan* np) {
+                     cudaStream_t s, const AGather* ag, const NdPlan* np, const BatchSpec* bs) {
   static const uint32_t bn_cap = getenv("TN_MAX_BN") ? (uint32_t)atoi(getenv("TN_MAX_BN")) : 256;  // tuning knob
   const uint32_t nsel = std::min<uint32_t>(N2 < 16 ? 16 : N2, bn_cap);
   switch (nsel) {
-    case 16: launch_bn<16, KB, G>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, ag, np); break;
-    case 32: launch_bn<32, KB, G>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, ag, np); break;
-    case 64: launch_bn<64, KB, G>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, ag, np); break;
-    case 128: launch_bn<128, KB, G>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, ag, np); break;
-    default: launch_bn<256, KB, G>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, ag, np); break;
+    case 16: launch_bn<16, KB, G>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, ag, np, bs); break;
+    case 32: launch_bn<32, KB, G>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, ag, np, bs); break;
+    case 64: launch_bn<64, KB, G>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, ag, np, bs); break;
+    case 128: launch_bn<128, KB, G>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, ag, np, bs); break;
+    default: launch_bn<256, KB, G>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, ag, np, bs); break;
   }
 }
 
 template <int G>
 void launch_kb(int KB, __half* c, const __half* a, const __half* bp, uint64_t M, uint32_t K2, uint32_t N2,
                       const float* in_max, const float* b_bound, uint32_t* out_max, int* exp_slot, const OutMap* om,
-                      cudaStream_t s, const AGather* ag, const NdPlan* np) {
+                      cudaStream_t s, const AGather* ag, const NdPlan* np, const BatchSpec* bs) {
   switch (KB) {
-    case 64: launch_k<64, G>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, ag, np); break;
-    case 32: launch_k<32, G>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, ag, np); break;
-    default: launch_k<16, G>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, ag, np); break;
+    case 64: launch_k<64, G>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, ag, np, bs); break;
+    case 32: launch_k<32, G>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, ag, np, bs); break;
+    default: launch_k<16, G>(c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, ag, np, bs); break;
   }
 }
 

@@ -9,16 +9,16 @@ namespace tn {
 
 extern template void launch_kb<0>(int, __half*, const __half*, const __half*, uint64_t, uint32_t, uint32_t,
                                   const float*, const float*, uint32_t*, int*, const OutMap*, cudaStream_t,
-                                  const AGather*, const NdPlan*);
+                                  const AGather*, const NdPlan*, const BatchSpec*);
 extern template void launch_kb<1>(int, __half*, const __half*, const __half*, uint64_t, uint32_t, uint32_t,
                                   const float*, const float*, uint32_t*, int*, const OutMap*, cudaStream_t,
-                                  const AGather*, const NdPlan*);
+                                  const AGather*, const NdPlan*, const BatchSpec*);
 extern template void launch_kb<2>(int, __half*, const __half*, const __half*, uint64_t, uint32_t, uint32_t,
                                   const float*, const float*, uint32_t*, int*, const OutMap*, cudaStream_t,
-                                  const AGather*, const NdPlan*);
+                                  const AGather*, const NdPlan*, const BatchSpec*);
 extern template void launch_kb<3>(int, __half*, const __half*, const __half*, uint64_t, uint32_t, uint32_t,
                                   const float*, const float*, uint32_t*, int*, const OutMap*, cudaStream_t,
-                                  const AGather*, const NdPlan*);
+                                  const AGather*, const NdPlan*, const BatchSpec*);
 
 static bool build_nd(const AGather& ag, NdPlan& out) {
   int pm[kMaxModes], pk[24];
@@ -315,19 +315,30 @@ void launch_gemm_chalf_tc(__half* c, const __half* a, const __half* bp, uint64_t
     if (direct && (direct_wide || !raw)) {
       // one N-d TMA box per stage (coordinates per dim from the global row)
       if (np.interleaved)
-        launch_kb<2>(np.KB, c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, ag, &np);
+        launch_kb<2>(np.KB, c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, ag, &np, nullptr);
       else
-        launch_kb<0>(np.KB, c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, ag, &np);
+        launch_kb<0>(np.KB, c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, ag, &np, nullptr);
       return;
     }
     if (raw) {
-      launch_kb<3>(rp.KB, c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, ag, &rp);
+      launch_kb<3>(rp.KB, c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, ag, &rp, nullptr);
       return;
     }
-    launch_kb<1>(kb_plain, c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, ag, nullptr);
+    launch_kb<1>(kb_plain, c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, ag, nullptr, nullptr);
     return;
   }
-  launch_kb<0>(kb_plain, c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, nullptr, nullptr);
+  launch_kb<0>(kb_plain, c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, nullptr, nullptr, nullptr);
+}
+
+void launch_gemm_chalf_tc_batched(__half* c, const __half* a, const __half* bp, uint64_t M, uint32_t K2, uint32_t N2,
+                                  const float* in_max, const float* b_bound, uint32_t* out_max, int* exp_slot,
+                                  const BatchSpec& bs, cudaStream_t s) {
+  if (K2 < 8 || (K2 & (K2 - 1)) || N2 < 16 || (N2 & (N2 - 1)))
+    throw TnError{TN_E_INVALID, "batched GEMM: K >= 4 and N >= 8 powers of two"};
+  if (bs.pad_r > 0 ? (!bs.table || bs.n_out != bs.n_a) : (!bs.ia || !bs.ib))
+    throw TnError{TN_E_INVALID, "batched GEMM: index arrays missing"};
+  const int kb = K2 >= 64 ? 64 : (K2 >= 32 ? 32 : 16);
+  launch_kb<0>(kb, c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, nullptr, s, nullptr, nullptr, &bs);
 }
 
 }  // namespace tn

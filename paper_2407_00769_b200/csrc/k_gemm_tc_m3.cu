@@ -4,5 +4,5 @@
 namespace tn {
 template void launch_kb<3>(int, __half*, const __half*, const __half*, uint64_t, uint32_t, uint32_t, const float*,
                             const float*, uint32_t*, int*, const OutMap*, cudaStream_t, const AGather*,
-                            const NdPlan*);
+                            const NdPlan*, const BatchSpec*);
 }  // namespace tn

@@ -1153,6 +1153,44 @@ int tn_gemm_chalf_gather(void* d_c, const void* d_a, const void* d_bp, int mlog,
   });
 }
 
+int tn_gemm_chalf_batched(void* d_c, const void* d_a, const void* d_bp, uint64_t M, uint32_t K, uint32_t N,
+                          uint64_t n_out, const int32_t* d_index_a, const int32_t* d_index_b, uint64_t n_a,
+                          uint64_t n_b, const float* d_in_max, const float* d_b_bound, uint32_t* d_out_max,
+                          int* d_exp, void* stream) {
+  if (!d_c || !d_a || !d_bp || !d_index_a || !d_index_b) return fail(TN_E_INVALID, "NULL argument");
+  TN_TRY({
+    BatchSpec bs;
+    bs.ia = d_index_a;
+    bs.ib = d_index_b;
+    bs.n_out = n_out;
+    bs.n_a = n_a;
+    bs.n_b = n_b;
+    const float* im = (d_in_max && d_b_bound) ? d_in_max : nullptr;
+    const float* bb = (d_in_max && d_b_bound) ? d_b_bound : nullptr;
+    launch_gemm_chalf_tc_batched((__half*)d_c, (const __half*)d_a, (const __half*)d_bp, M, 2 * K, 2 * N, im, bb,
+                                 d_out_max, d_exp, bs, (cudaStream_t)stream);
+  });
+}
+
+int tn_gemm_chalf_padded(void* d_c, const void* d_a, const void* d_bp, uint64_t M, uint32_t K, uint32_t N,
+                         uint64_t n_a, const int32_t* d_table, int m_r, uint64_t n_b, const float* d_in_max,
+                         const float* d_b_bound, uint32_t* d_out_max, int* d_exp, void* stream) {
+  if (!d_c || !d_a || !d_bp || !d_table) return fail(TN_E_INVALID, "NULL argument");
+  if (m_r <= 0) return fail(TN_E_INVALID, "m_r must be positive");
+  TN_TRY({
+    BatchSpec bs;
+    bs.pad_r = m_r;
+    bs.table = d_table;
+    bs.n_out = n_a;
+    bs.n_a = n_a;
+    bs.n_b = n_b;
+    const float* im = (d_in_max && d_b_bound) ? d_in_max : nullptr;
+    const float* bb = (d_in_max && d_b_bound) ? d_b_bound : nullptr;
+    launch_gemm_chalf_tc_batched((__half*)d_c, (const __half*)d_a, (const __half*)d_bp, M, 2 * K, 2 * N, im, bb,
+                                 d_out_max, d_exp, bs, (cudaStream_t)stream);
+  });
+}
+
 int tn_gemm_cfloat(void* d_c, const void* d_a, const void* d_b, uint64_t M, uint32_t K, uint32_t N, void* stream) {
   if (!d_c || !d_a || !d_b) return fail(TN_E_INVALID, "NULL argument");
   TN_TRY(launch_gemm_c64((float2*)d_c, (const float2*)d_a, (const float2*)d_b, M, K, N, nullptr, (cudaStream_t)stream));

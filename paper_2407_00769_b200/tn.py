@@ -72,6 +72,10 @@ def lib():
         L.tn_gemm_chalf_gather.argtypes = [vp, vp, vp, i32, i32, C.c_uint32, C.POINTER(C.c_int64),
                                            C.POINTER(C.c_int64), vp, vp, vp, vp, vp]
         L.tn_gemm_cfloat.argtypes = [vp, vp, vp, u64, C.c_uint32, C.c_uint32, vp]
+        L.tn_gemm_chalf_batched.argtypes = [vp, vp, vp, u64, C.c_uint32, C.c_uint32, u64, vp, vp, u64, u64,
+                                            vp, vp, vp, vp, vp]
+        L.tn_gemm_chalf_padded.argtypes = [vp, vp, vp, u64, C.c_uint32, C.c_uint32, u64, vp, i32, u64,
+                                           vp, vp, vp, vp, vp]
         L.tn_pad_b.argtypes = [vp, vp, C.c_uint32, C.c_uint32, vp, vp, vp, vp]
         L.tn_quant_int8.argtypes = [vp, vp, vp, vp, u64, i32, vp]
         L.tn_dequant_int8.argtypes = [vp, vp, vp, vp, u64, i32, vp]
@@ -267,6 +271,22 @@ def tn_gemm_chalf_gather(c, a, bp, mlog, klog, N, m_stride, k_stride, in_max=Non
     ks = (C.c_int64 * max(len(k_stride), 1))(*k_stride)
     _check(lib().tn_gemm_chalf_gather(_ptr(c), _ptr(a), _ptr(bp), mlog, klog, N, ms, ks, _ptr(in_max),
                                       _ptr(b_bound), _ptr(out_max), _ptr(exp), _stream(stream)))
+
+
+def tn_gemm_chalf_batched(c, a, bp, M, K, N, index_a, index_b, n_a, n_b, in_max=None, b_bound=None, out_max=None,
+                          exp=None, stream=None):
+    """index_a / index_b: int32 CUDA tensors of n_out entries."""
+    _check(lib().tn_gemm_chalf_batched(_ptr(c), _ptr(a), _ptr(bp), M, K, N, index_a.numel(), _ptr(index_a),
+                                       _ptr(index_b), n_a, n_b, _ptr(in_max), _ptr(b_bound), _ptr(out_max),
+                                       _ptr(exp), _stream(stream)))
+
+
+def tn_gemm_chalf_padded(c, a, bp, M, K, N, table, n_b, in_max=None, b_bound=None, out_max=None, exp=None,
+                         stream=None):
+    """table: int32 CUDA tensor [n_a, m_r] (-1 = zero block)."""
+    n_a, m_r = table.shape
+    _check(lib().tn_gemm_chalf_padded(_ptr(c), _ptr(a), _ptr(bp), M, K, N, n_a, _ptr(table), m_r, n_b,
+                                      _ptr(in_max), _ptr(b_bound), _ptr(out_max), _ptr(exp), _stream(stream)))
 
 
 def tn_gemm_cfloat(c, a, b, M, K, N, stream=None):

@@ -203,7 +203,7 @@ def test_fused_swap_codec_lowering(tnmod, world, g):
 def test_split_auto_chunk_count(tnmod):
     """split_log2 = -1 (reading C-A19): the smallest power-of-two chunk count whose lowering
     fits stem_capacity_bytes; no capacity -> no split; nothing fits -> TN_E_CAPACITY."""
-    with open(os.path.join(ROOT, "plans", "c3.json")) as f:
+    with open(os.path.join(ROOT, "plans", "c3_sweep.json")) as f:
         c3 = json.load(f)
     need = {}
     for j in range(4):

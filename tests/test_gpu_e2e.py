@@ -180,7 +180,7 @@ def test_c3_split_auto_capacity(tn):
     """SURVEY a.7 protocol at full C3 size: buffers sized below the unsplit stem force the automatic
     chunk count (split_log2 = -1, C-A19) to c >= 2; same amplitudes as the unsplit run (chunk
     scales are powers of two, so only fp16 subnormals could differ)."""
-    c3 = _plan("c3")
+    c3 = _plan("c3_sweep")  # the round-1 C3 plan: its largest stem is in the tail
     p0 = tn.Plan(c3, tn.make_config(stem_min_log2=20))
     one = tn.contract(p0, tn.Buffers(p0), 0)
     need0 = p0.info()["stem_bytes"]

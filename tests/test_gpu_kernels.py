@@ -460,3 +460,74 @@ def test_quant_int8_exp02_tensor_preset_vs_oracle(env, g):
     close = (got == want) | (np.abs(got.astype(np.float64) - want) <= 2.0 ** -10 * np.abs(want.astype(np.float64)))
     assert close.all()
     assert np.array_equal(got[g:2 * g], x[g:2 * g])       # constant group round-trips exactly
+
+
+def _sparse_operands(rng, m_a, n_b, M, K, N):
+    a = (rng.standard_normal((m_a, M, K)) + 1j * rng.standard_normal((m_a, M, K))) / np.sqrt(2)
+    b = (rng.standard_normal((n_b, K, N)) + 1j * rng.standard_normal((n_b, K, N))) / np.sqrt(2 * K)
+    a16 = a.real.astype(np.float16) + 1j * a.imag.astype(np.float16)
+    b16 = b.real.astype(np.float16) + 1j * b.imag.astype(np.float16)
+    A = np.stack([a16.real, a16.imag], axis=-1).astype(np.float16).reshape(-1)
+    bp = np.stack([np.transpose(embed.pad_b(b16[j]), (2, 0, 1, 3)).reshape(2 * N, 2 * K) for j in range(n_b)])
+    return a16, b16, A, bp.astype(np.float16).reshape(-1)
+
+
+def _close(got, ref):
+    tol = 2.0 ** -10 * np.abs(ref) + 1e-3 * np.sqrt(np.mean(np.abs(ref) ** 2)) + 1e-7
+    return np.all(np.abs(got - ref) <= tol)
+
+
+@pytest.mark.parametrize("M,K,N", [(128, 8, 8), (256, 64, 16), (512, 32, 128), (128, 256, 64)])
+def test_gemm_chalf_batched_vs_oracle_gather(env, M, K, N):
+    """Fig. 5 bottom: C[n] = A[Index_A[n]] x B[Index_B[n]] in one tcgen05 launch vs the
+    oracle's gather_contract (oracle/sparse.py) on the same fp16 operands; Index_A with the paper's
+    repeat pattern [0, 0, 1, 1, 1, 3, 4, ...]."""
+    from oracle import sparse
+    torch, tn = env
+    rng = np.random.default_rng(M + K + N)
+    m_a, n_b = 6, 5
+    ia = np.array([0, 0, 1, 1, 1, 3, 4, 5, 5, 2], dtype=np.int32)
+    ib = rng.integers(0, n_b, size=ia.size).astype(np.int32)
+    a16, b16, A, BP = _sparse_operands(rng, m_a, n_b, M, K, N)
+    ref = sparse.gather_contract(a16, b16, ia, ib)                       # [n, M, N] complex128
+    C = torch.full((ia.size * M * N * 2,), float("nan"), dtype=torch.float16, device="cuda")
+    tn.tn_gemm_chalf_batched(C, torch.from_numpy(A).cuda(), torch.from_numpy(BP).cuda(), M, K, N,
+                             torch.from_numpy(ia).cuda(), torch.from_numpy(ib).cuda(), m_a, n_b)
+    torch.cuda.synchronize()
+    g = C.cpu().numpy().astype(np.float64).reshape(ia.size, M, N, 2)
+    assert _close(g[..., 0] + 1j * g[..., 1], ref)
+
+
+@pytest.mark.parametrize("M,K,N", [(128, 16, 8), (256, 64, 32), (128, 32, 256)])
+def test_gemm_chalf_padded_index_vs_oracle(env, M, K, N):
+    """Fig. 5 top: the padded 2-d index of Index_B (m_r = max repeat of Index_A, -1 padding,
+    built by the oracle's build_padded_index) drives C_P = A x B_P on the GPU; the extracted valid
+    blocks equal the oracle's padded_contract and gather_contract (same fp16 operands); the padding
+    blocks are exact zeros."""
+    from oracle import sparse
+    torch, tn = env
+    rng = np.random.default_rng(7 * M + K + N)
+    m_a, n_b = 5, 4
+    ia = np.array([0, 0, 1, 1, 1, 3, 4], dtype=np.int64)                 # the paper's example: m_r = 3
+    ib = rng.integers(0, n_b, size=ia.size)
+    table, m_r = sparse.build_padded_index(ia, ib, m_a)
+    assert m_r == 3
+    a16, b16, A, BP = _sparse_operands(rng, m_a, n_b, M, K, N)
+    ref = sparse.padded_contract(a16, b16, ia, ib)
+    assert np.allclose(ref, sparse.gather_contract(a16, b16, ia, ib))
+    C = torch.full((m_a * M * m_r * N * 2,), float("nan"), dtype=torch.float16, device="cuda")
+    tn.tn_gemm_chalf_padded(C, torch.from_numpy(A).cuda(), torch.from_numpy(BP).cuda(), M, K, N,
+                            torch.from_numpy(table.astype(np.int32)).cuda(), n_b)
+    torch.cuda.synchronize()
+    g = C.cpu().numpy().astype(np.float64).reshape(m_a, M, m_r, N, 2)
+    cp = g[..., 0] + 1j * g[..., 1]                                       # C_P[a, m, r, n]
+    occ = np.zeros(m_a, dtype=np.int64)
+    got = []
+    for i in ia:                                                          # extract valid blocks (P:537)
+        got.append(cp[i, :, occ[i], :])
+        occ[i] += 1
+    assert _close(np.stack(got), ref)
+    for a in range(m_a):
+        for r in range(m_r):
+            if table[a, r] < 0:
+                assert np.all(cp[a, :, r, :] == 0)

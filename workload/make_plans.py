@@ -31,8 +31,12 @@ CONFIGS = {
     "c1": dict(rows=3, cols=4, drop=False, cycles=8, n_open=12, max_log2=None, trials=8),
     # C2: 30-qubit 14-cycle, stem <= 2^28, 10 open legs (BJ configs[1])
     "c2": dict(rows=5, cols=6, drop=False, cycles=14, n_open=10, max_log2=30, trials=0),
-    # C3: 53-qubit (6x9 minus a corner) 20-cycle, stem <= 2^32, 6 open legs (BJ configs[2])
-    "c3": dict(rows=6, cols=9, drop=True, cycles=20, n_open=6, max_log2=35, trials=0),
+    # C3: 53-qubit (6x9 minus a corner) 20-cycle, 6 open legs (BJ configs[2]).  Branch grouping over
+    # up to 24 consecutive stem branches (MB-scale non-stem tensors), then as few sliced edges
+    # as keep the largest stem at 2^32 ("~2^32 complex-half in double buffers")
+    "c3": dict(rows=6, cols=9, drop=True, cycles=20, n_open=6, max_log2=35, trials=0, max_group=24, stem_log2=32),
+    # round-1 C3 plan (kept as the memory-bound variant): 12-branch groups, 188 sliced edges, stem 2^33
+    "c3_sweep": dict(rows=6, cols=9, drop=True, cycles=20, n_open=6, max_log2=35, trials=0),
 }
 
 
@@ -64,7 +68,7 @@ def sweep_orders(circ, net):
 
 
 def build_plan(rows, cols, drop, cycles, n_open, max_log2, trials, seed=0, group=True,
-               max_branch_log2=20):
+               max_branch_log2=20, max_group=12, stem_log2=None):
     circ = C.make_circuit(rows, cols, cycles, seed=seed, drop_corner=drop)
     n = circ["n_qubits"]
     bits = C.random_bits(n, seed + 1000)
@@ -82,7 +86,8 @@ def build_plan(rows, cols, drop, cycles, n_open, max_log2, trials, seed=0, group
     if max_log2 is None:
         max_log2 = 10 ** 6
     res = PL.plan_network(leaf_masks, open_mask, max_log2, trials=trials, seed=seed, group=group,
-                          max_branch_log2=max_branch_log2, sweeps=sweep_orders(circ, net))
+                          max_branch_log2=max_branch_log2, sweeps=sweep_orders(circ, net), max_group=max_group,
+                          stem_log2=stem_log2)
     tree, sliced, stem = res["tree"], res["sliced"], res["stem"]
     tensors = []
     for ls, d in net.tensors:
@@ -129,7 +134,8 @@ def main(argv):
         cfg = CONFIGS[name]
         t0 = time.time()
         plan = build_plan(cfg["rows"], cfg["cols"], cfg["drop"], cfg["cycles"], cfg["n_open"],
-                          cfg["max_log2"], cfg["trials"])
+                          cfg["max_log2"], cfg["trials"], max_group=cfg.get("max_group", 12),
+                          stem_log2=cfg.get("stem_log2"))
         p = write_plan(name, plan)
         m = plan["meta"]
         print(f"{name}: {p} tensors={m['n_tensors']} sliced={m['n_sliced']} "

@@ -264,6 +264,25 @@ def group_branches(tree, sliced, stem, max_branch_log2=20, max_group=12):
     return Tree(tree.leaf_masks, new_pairs), new_stem, best[L]
 
 
+def unslice_to_target(tree, sliced, target_log2):
+    """Greedily un-slice edges (fewest subtasks) while every intermediate of ``tree`` stays
+    <= 2^target_log2 elements: each pass removes the sliced label whose removal keeps the bound and
+    adds the least per-slice cost.  Branch grouping shrinks the stem, so a grouped tree needs far
+    fewer sliced edges than the ungrouped tree it came from."""
+    while True:
+        best = None
+        for l in bits_of(sliced):
+            s2 = sliced & ~(1 << l)
+            if tree.max_log2(s2) > target_log2:
+                continue
+            c = tree.total_cost(s2)
+            if best is None or c < best[0]:
+                best = (c, l)
+        if best is None:
+            return sliced
+        sliced &= ~(1 << best[1])
+
+
 def left_deep_pairs(order):
     """SSA pairs of the left-deep tree absorbing leaves in ``order`` (a sweep)."""
     n = len(order)
@@ -276,7 +295,7 @@ def left_deep_pairs(order):
 
 
 def plan_network(leaf_masks, open_mask, max_log2, trials=32, seed=0, group=True,
-                 max_branch_log2=20, sweeps=()):
+                 max_branch_log2=20, sweeps=(), max_group=12, stem_log2=None):
     """Search seeded random-greedy trees and the given sweep orders (left-deep trees); slice each
     to ``max_log2``; keep the cheapest by total (all-slices) cost.  Returns dict with tree,
     sliced mask, stem."""
@@ -304,7 +323,10 @@ def plan_network(leaf_masks, open_mask, max_log2, trials=32, seed=0, group=True,
     stem = find_stem(tree, sliced)
     est = None
     if group:
-        tree, stem, est = group_branches(tree, sliced, stem, max_branch_log2=max_branch_log2)
+        tree, stem, est = group_branches(tree, sliced, stem, max_branch_log2=max_branch_log2, max_group=max_group)
+    if stem_log2 is not None:
+        # fewer sliced edges: bigger (paper-like) subtasks with the largest stem at 2^stem_log2
+        sliced = unslice_to_target(tree, sliced, stem_log2)
     return {"tree": tree, "sliced": sliced, "stem": stem, "est_time": est}
 
 
