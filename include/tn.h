@@ -241,7 +241,8 @@ TN_API int tn_gemm_chalf_batched(void* d_c, const void* d_a, const void* d_bp, u
  * C_P = A x B_P"): C_P[a] = A[a] [B[t(a,0)] | B[t(a,1)] | ... | B[t(a,m_r-1)]] for a < n_a, with
  * t(a,r) = table[a*m_r + r] (DEVICE int32, row-major [n_a][m_r]); t < 0 gives a zero block (its MMA
  * is skipped).  C_P: n_a entries of [M][m_r*N] complex-half; the valid products are the blocks
- * with t >= 0 (C is C_P "flattened ... then extract valid tensors in it").  Shapes as above. */
+ * with t >= 0 (C is C_P "flattened ... then extract valid tensors in it").  Shapes as above, and
+ * N >= 32 when m_r > 1. */
 TN_API int tn_gemm_chalf_padded(void* d_c, const void* d_a, const void* d_bp, uint64_t M, uint32_t K, uint32_t N,
                                 uint64_t n_a, const int32_t* d_table, int m_r, uint64_t n_b, const float* d_in_max,
                                 const float* d_b_bound, uint32_t* d_out_max, int* d_exp, void* stream);

@@ -1035,6 +1035,9 @@ static void launch_bn(__half* c, const __half* a, const __half* bp, uint64_t M, 
     ba.b_rows = N2;
     const uint32_t cols = bs->pad_r > 0 ? (uint32_t)bs->pad_r * N2 : N2;  // C columns per row
     if (N2 % BN) throw TnError{TN_E_INVALID, "batched GEMM: B block rows must be a multiple of the tile"};
+    // the epilogue stages 64-column subtiles and stores them with a 64-wide TMA box: a C row narrower
+    // than one tile is clipped by the map, a padded row of several narrow blocks would be overwritten
+    if (bs->pad_r > 1 && N2 < 64) throw TnError{TN_E_INVALID, "padded 2-d index: needs N >= 32"};
     const uint64_t a_rows = (uint64_t)bs->n_a * M, c_rows = (uint64_t)bs->n_out * M;
     const uint64_t b_rows_all = (uint64_t)bs->n_b * N2;
     if (a_rows >= (1ull << 31) || c_rows >= (1ull << 31) || b_rows_all >= (1ull << 31))

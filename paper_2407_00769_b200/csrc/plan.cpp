@@ -149,6 +149,7 @@ static Plan* load_plan_fixed(const char* json, size_t len, const tn_config* cfg_
     }
   }
   std::vector<int> stem_in = int_list(root.get("stem"), "stem");
+  p.sparse_legs = int_list(root.get("sparse_legs"), "sparse_legs");
 
   // ---- label validation: no hyper-edges; open legs appear once; closed labels twice
   std::map<int, int> count;
@@ -169,6 +170,12 @@ static Plan* load_plan_fixed(const char* json, size_t len, const tn_config* cfg_
     if (!count.count(l) || open_set.count(l)) throw err(TN_E_INVALID, "sliced label must be a closed edge");
     if (!sl_set.insert(l).second) throw err(TN_E_INVALID, "duplicate sliced label");
   }
+  // sparse-state legs: open legs whose values are given per correlated subspace
+  std::set<int> sparse_set;
+  for (int l : p.sparse_legs)
+    if (!open_set.count(l) || !sparse_set.insert(l).second)
+      throw err(TN_E_INVALID, "sparse_legs must be distinct open legs");
+  if (p.sparse_legs.size() > 63) throw err(TN_E_UNSUPPORTED, "more than 63 sparse legs");
 
   // ---- nodes
   const int nl = (int)p.leaves.size();
@@ -280,6 +287,29 @@ static Plan* load_plan_fixed(const char* json, size_t len, const tn_config* cfg_
     }
   }
   for (int l : p.open) next_use.erase(l);  // open legs are never contracted
+  // ---- sparse-state tail ("sparse state occurs in the final stage"): from the first stem step
+  // whose branch holds a sparse leg, every stem tensor is a batch over the distinct values its sparse
+  // legs take among the requested subspaces (a slice per batch entry: fixing the legs like slicing
+  // fixes an edge), contracted with gather-batched GEMMs (Fig. 5).  The dense lowering below
+  // therefore ignores sparse legs; the branches keep them as batch modes of their B_P blocks.
+  if (!sparse_set.empty()) {
+    if (entry_idx < 0) throw err(TN_E_UNSUPPORTED, "sparse legs need stem steps");
+    for (int l : p.nodes[p.stem_entry].labels)
+      if (sparse_set.count(l)) throw err(TN_E_UNSUPPORTED, "sparse legs must enter the stem through branches (the stem entry holds one)");
+    if (cfg.split_log2 != 0) throw err(TN_E_UNSUPPORTED, "split tail together with sparse legs (the sparse batch is chunked instead)");
+    if (world > 1) throw err(TN_E_UNSUPPORTED, "sparse-state batch on a sharded stem (run replicas)");
+    int prev = p.stem_entry;
+    for (size_t s = 0; s < step_nodes.size() && p.sparse_from < 0; ++s) {
+      const Node& n = p.nodes[step_nodes[s]];
+      int br = (n.u == prev) ? n.v : n.u;
+      for (int l : p.nodes[br].labels)
+        if (sparse_set.count(l)) p.sparse_from = (int)s;
+      prev = step_nodes[s];
+    }
+    if (p.sparse_from < 0) throw err(TN_E_INVALID, "no stem step holds a sparse leg");
+    // common-type nodes that hold a sparse leg may only feed the tail as branches: the stem before
+    // the tail must be free of them (checked per step below)
+  }
   // ---- split-type tail: 2^j chunks fix j open legs.  The chosen legs are
   // the open legs that enter the stem earliest (longest tail); they sort outermost in every layout.
   std::set<int> split_set;
@@ -334,7 +364,8 @@ static Plan* load_plan_fixed(const char* json, size_t len, const tn_config* cfg_
       for (size_t s = 0; s < step_nodes.size(); ++s) {
         const Node& n = p.nodes[step_nodes[s]];
         int br = (n.u == prev) ? n.v : n.u;
-        for (int l : p.nodes[br].labels) (cur.count(l) ? Rsets[s] : cur).insert(l);
+        for (int l : p.nodes[br].labels)
+          if (!sparse_set.count(l)) (cur.count(l) ? Rsets[s] : cur).insert(l);
         for (int l : Rsets[s]) cur.erase(l);
         prev = step_nodes[s];
       }
@@ -382,7 +413,10 @@ static Plan* load_plan_fixed(const char* json, size_t len, const tn_config* cfg_
       st.node = step_nodes[s];
       const Node& n = p.nodes[st.node];
       st.branch = (n.u == prev) ? n.v : n.u;
-      const auto& B = p.nodes[st.branch].labels;
+      st.sparse = (p.sparse_from >= 0 && (int)s >= p.sparse_from) ? 1 : 0;
+      std::vector<int> B;  // dense branch labels (sparse legs are the B_P block index)
+      for (int l : p.nodes[st.branch].labels) (sparse_set.count(l) ? st.b_sparse : B).push_back(l);
+      if (!st.sparse && !st.b_sparse.empty()) throw err(TN_E_INVALID, "sparse leg in a stem branch before the sparse tail");
       std::set<int> bs(B.begin(), B.end());
       if (!shard.empty()) {
         // Alg. 1: a contracted shard mode forces an all-to-all mode swap first.
@@ -473,7 +507,7 @@ static Plan* load_plan_fixed(const char* json, size_t len, const tn_config* cfg_
         const bool rows_k = kl <= 4 && nl <= 5 && kl + nl <= 7;
         const bool tc_k = cfg.dtype == TN_CHALF && kl >= 2 && !rows_k &&
                           ((kl >= 3 && nl >= 3) || kl >= 4 || kl + nl > 11);
-        const bool fusable = !cfg.no_gather && tc_k && kl >= 3 && kept.size() >= 7 && L.size() >= 2 &&
+        const bool fusable = !cfg.no_gather && !st.sparse && tc_k && kl >= 3 && kept.size() >= 7 && L.size() >= 2 &&
                              bs.count(L[L.size() - 1]) && bs.count(L[L.size() - 2]) &&
                              (split_set.empty() || (int)s < p.split_from);
         if (!fusable) by_next_use(kept);
@@ -489,7 +523,7 @@ static Plan* load_plan_fixed(const char* json, size_t len, const tn_config* cfg_
       for (int l : B)
         if (std::find(R.begin(), R.end(), l) == R.end()) newl.push_back(l);
       std::vector<int> out;
-      if (policy == 0 || policy == 2) {
+      if ((policy == 0 || policy == 2) && !st.sparse) {
         if (s + 1 == step_nodes.size()) {
           // the last step writes the result directly in output order (local modes only)
           for (int l : L)  // split tail: the split modes stay the outermost block
@@ -545,7 +579,9 @@ static Plan* load_plan_fixed(const char* json, size_t len, const tn_config* cfg_
       {
         std::set<int> chk(st.out_layout.begin(), st.out_layout.end());
         chk.insert(shard.begin(), shard.end());
-        std::set<int> want(n.labels.begin(), n.labels.end());
+        std::set<int> want;
+        for (int l : n.labels)
+          if (!sparse_set.count(l)) want.insert(l);
         if (chk != want || chk.size() != st.out_layout.size() + shard.size())
           throw err(TN_E_INVALID, "internal: step output labels mismatch");
       }
@@ -642,7 +678,7 @@ static Plan* load_plan_fixed(const char* json, size_t len, const tn_config* cfg_
     // layout are unchanged.
     if (!cfg.no_gather && cfg.dtype == TN_CHALF) {
       for (auto& st : p.steps) {
-        if (!st.perm || !st.tensor_core || st.split || st.mlog < 7 || st.klog < 3) continue;
+        if (!st.perm || !st.tensor_core || st.split || st.sparse || st.mlog < 7 || st.klog < 3) continue;
         const std::vector<int>& IL = st.in_layout;
         const int r = (int)IL.size();
         std::set<int> Rs(st.R.begin(), st.R.end());
@@ -662,7 +698,7 @@ static Plan* load_plan_fixed(const char* json, size_t len, const tn_config* cfg_
         p.n_permutes--;
       }
     }
-    if (shard.empty() && p.split_modes.empty() && L != p.open) {
+    if (shard.empty() && p.split_modes.empty() && p.sparse_from < 0 && L != p.open) {
       p.final_perm = true;
       for (int l : p.open) p.final_perm_axes.push_back((int)(std::find(L.begin(), L.end(), l) - L.begin()));
       p.perm_bytes += 2.0 * eb * std::ldexp(1.0, (int)L.size());
@@ -694,14 +730,19 @@ static Plan* load_plan_fixed(const char* json, size_t len, const tn_config* cfg_
   p.ws_common = off;
   for (auto& st : p.steps) {
     uint64_t kn = 1ull << (st.klog + st.nlog);
+    const uint64_t nb = 1ull << st.b_sparse.size();  // sparse tail: one block per sparse-leg value
     st.b_tmp_off = off;
-    off += align_up(8 * kn, 1024);
+    off += align_up(8 * kn, 1024) * nb;
     if (cfg.dtype == TN_CHALF) {
       st.b_off = off;
       // fp16 [max(2N, 16)][2K]: rows beyond 2N are zero (tcgen05 N >= 16)
-      off += align_up(std::max<uint64_t>(8 * kn, 64ull << st.klog), 1024);
+      // sparse tail: blocks back to back (the batched GEMM's B map steps by exactly one block)
+      st.b_blk = st.sparse ? std::max<uint64_t>(8 * kn, 64ull << st.klog)
+                           : align_up(std::max<uint64_t>(8 * kn, 64ull << st.klog), 1024);
+      off += align_up(st.b_blk * nb, 1024);
     } else {
       st.b_off = st.b_tmp_off;
+      st.b_blk = align_up(8 * kn, 1024);
     }
   }
   p.ws_b = off;
@@ -751,7 +792,7 @@ std::string report_json(const Plan& p, const std::vector<float>& ms) {
     o << (i ? "," : "") << "{\"node\":" << s.node << ",\"branch\":" << s.branch << ",\"m\":" << s.mlog
       << ",\"k\":" << s.klog << ",\"n\":" << s.nlog << ",\"perm\":" << (s.perm ? 1 : 0)
       << ",\"tc\":" << (s.tensor_core ? 1 : 0) << ",\"ga\":" << (s.gather_a ? 1 : 0) << ",\"split\":" << s.split << ",\"swap\":" << (s.swap ? 1 : 0)
-      << ",\"quant\":" << (s.quant ? 1 : 0)
+      << ",\"quant\":" << (s.quant ? 1 : 0) << ",\"sparse\":" << s.sparse
       << ",\"fuse_quant\":" << (s.fuse_quant ? 1 : 0)
       << ",\"in\":";
     jlist(o, s.in_layout);
@@ -759,6 +800,10 @@ std::string report_json(const Plan& p, const std::vector<float>& ms) {
     jlist(o, s.R);
     o << ",\"out\":";
     jlist(o, s.out_layout);
+    if (s.sparse) {
+      o << ",\"b_sparse\":";
+      jlist(o, s.b_sparse);
+    }
     if (s.swap) {
       o << ",\"shard_before\":";
       jlist(o, s.shard_before);
@@ -789,7 +834,9 @@ std::string report_json(const Plan& p, const std::vector<float>& ms) {
   jlist(o, p.stem_entry >= 0 ? p.nodes[p.stem_entry].labels : std::vector<int>());
   o << ",\"split_modes\":";
   jlist(o, p.split_modes);
-  o << ",\"split_from\":" << p.split_from;
+  o << ",\"split_from\":" << p.split_from << ",\"sparse_from\":" << p.sparse_from
+    << ",\"sparse_chunks\":" << p.sparse_chunks << ",\"sparse_legs\":";
+  jlist(o, p.sparse_legs);
   o << ",\"shard0\":";
   jlist(o, p.shard0);
   o << ",\"final_layout\":";

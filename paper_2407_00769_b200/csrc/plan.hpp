@@ -53,6 +53,9 @@ struct StemStep {
   std::vector<int64_t> m_stride, n_stride;
   bool out_identity = true;       // out_layout == kept ++ newl (plain row-major [M][N])
   int split = 0;                  // 1 = split-type (chunked tail) step
+  int sparse = 0;                 // 1 = sparse-state tail step (gather-batched GEMM, Fig. 5)
+  std::vector<int> b_sparse;      // sparse legs of the branch (B_P block index bits, MSB first)
+  uint64_t b_blk = 0;             // bytes of one B_P block
   // sharded stem (world > 1), Alg. 1: mode swap before this step when R ∩ shard != ∅
   bool swap = false;
   std::vector<int> shard_before, shard_after;  // shard labels, rank bit order (MSB first)
@@ -80,6 +83,9 @@ struct Plan {
   bool final_perm = false;        // final permutation into `open` order
   std::vector<int> final_perm_axes;
   int split_from = -1;            // first split-type step index (-1: none)
+  std::vector<int> sparse_legs;   // open legs given per correlated subspace (sparse-state batch)
+  int sparse_from = -1;           // first sparse-tail step (-1: none)
+  uint64_t sparse_chunks = 0;     // subspace chunks of the last sparse-tail run
   int split_log2 = 0;             // chunks = 2^split_log2
   std::vector<int> split_modes;   // open legs fixed per chunk (outermost in every tail layout)
   uint64_t split_chunk_max = 0;   // largest per-chunk stem tensor of the tail (elements)

@@ -349,9 +349,56 @@ void run_common(const Plan& p, unsigned char* W, cudaStream_t s) {
   }
 }
 
+// Sparse-tail step: the branch is dense over its sparse legs; block b of its operand is
+// the branch with those legs fixed to the bits of b (MSB = first leg), i.e. a slice of it.  All
+// blocks share one power-of-two scale (the max over every block), so the batched GEMM has one
+// exponent per step.
+void prepare_b_sparse(const Plan& p, const StemStep& st, size_t i, unsigned char* W, const Scratch& sc, cudaStream_t s) {
+  View v = view_of(p, st.branch, W);
+  const int nsp = (int)st.b_sparse.size();
+  const uint64_t nb = 1ull << nsp, kn = 1ull << (st.klog + st.nlog);
+  const uint64_t tmp_blk = align_up(8 * kn, 1024);
+  for (uint64_t bv = 0; bv < nb; ++bv) {
+    GatherArgs g;
+    memset(&g, 0, sizeof(g));
+    int64_t off = 0;
+    for (int t = 0; t < nsp; ++t)
+      if ((bv >> (nsp - 1 - t)) & 1) off += v.stride_of(st.b_sparse[t]);
+    g.src = v.base + off;
+    g.ss = v.so;
+    g.dst = reinterpret_cast<float2*>(W + st.b_tmp_off + bv * tmp_blk);
+    g.klog = st.klog;
+    g.nlog = st.nlog;
+    for (int j = 0; j < st.klog; ++j) g.sk[j] = v.stride_of(st.R[st.klog - 1 - j]);
+    for (int j = 0; j < st.nlog; ++j) g.sn[j] = v.stride_of(st.newl[st.nlog - 1 - j]);
+    launch_gather_kn(g, s);
+    const_cast<Plan&>(p).launches++;
+    if (p.cfg.dtype == TN_CHALF) launch_max_abs_f32(reinterpret_cast<const float*>(g.dst), 2 * kn, &sc.b_max[i], s);
+  }
+  if (p.cfg.dtype != TN_CHALF) {
+    // complex64 path: the blocks are consumed as [K][N] complex64 at b_off + bv * b_blk
+    for (uint64_t bv = 0; bv < nb; ++bv)
+      if (st.b_off + bv * st.b_blk != st.b_tmp_off + bv * tmp_blk)
+        TN_CUDA(cudaMemcpyAsync(W + st.b_off + bv * st.b_blk, W + st.b_tmp_off + bv * tmp_blk, 8 * kn,
+                                cudaMemcpyDeviceToDevice, s));
+    return;
+  }
+  for (uint64_t bv = 0; bv < nb; ++bv) {
+    unsigned char* bp = W + st.b_off + bv * st.b_blk;
+    if (st.nlog < 3) TN_CUDA(cudaMemsetAsync(bp, 0, 64ull << st.klog, s));
+    launch_pad_b(reinterpret_cast<__half*>(bp), reinterpret_cast<const float2*>(W + st.b_tmp_off + bv * tmp_blk),
+                 st.klog, st.nlog, &sc.b_max[i], &sc.b_bound[i], &sc.exps[1 + 2 * i], s);
+    const_cast<Plan&>(p).launches++;
+  }
+}
+
 void prepare_b(const Plan& p, unsigned char* W, const Scratch& sc, cudaStream_t s) {
   for (size_t i = 0; i < p.steps.size(); ++i) {
     const StemStep& st = p.steps[i];
+    if (st.sparse) {
+      prepare_b_sparse(p, st, i, W, sc, s);
+      continue;
+    }
     View v = view_of(p, st.branch, W);
     GatherArgs g;
     memset(&g, 0, sizeof(g));
@@ -595,7 +642,8 @@ void stem_body(Plan& p, const tn_buffers* b, cudaStream_t s, bool head = true, b
   if (p.world > 1 && p.cfg.dtype == TN_CHALF) xfer_allreduce_max(p, &sc.max_slot[0], s);
   int cur = 0;
   rec_event(p, 1, s);
-  const size_t n_main = p.split_modes.empty() ? p.steps.size() : (size_t)p.split_from;
+  const size_t n_main = !p.split_modes.empty() ? (size_t)p.split_from
+                                               : (p.sparse_from >= 0 ? (size_t)p.sparse_from : p.steps.size());
   for (size_t i = 0; i < n_main; ++i) {
     const StemStep& st = p.steps[i];
     if (st.swap) {
@@ -626,6 +674,7 @@ void stem_body(Plan& p, const tn_buffers* b, cudaStream_t s, bool head = true, b
     return;  // the chunked tail runs in tn_split_contract
   }
   p.stem_cur = cur;
+  if (p.sparse_from >= 0) return;  // the sparse-state tail runs in tn_sample_amplitudes (needs the prefixes)
   if (p.final_perm) {
     launch_permute(b->d_stem[1 - cur], b->d_stem[cur], eb, (int)p.final_layout.size(), p.final_perm_axes.data(), s);
     ++p.launches;
@@ -734,7 +783,7 @@ void stem_contract(Plan& p, const tn_buffers* b, uint64_t slice_id, cudaStream_t
     p.result_buf = p.graph_result_buf;
     p.result_off = 0;
     p.result_in_ws = p.steps.empty();
-    p.ev_valid = p.timing != 0 && p.split_modes.empty();  // the graph records the same events
+    p.ev_valid = p.timing != 0 && p.split_modes.empty() && p.sparse_from < 0;  // the graph records the same events
     return;
   }
   p.launches = 0;
@@ -809,6 +858,264 @@ void split_contract(Plan& p, const tn_buffers* b, cudaStream_t s, const std::vec
   p.ev_valid = p.timing != 0;
   p.result_buf = 1 - p.stem_cur;
   p.result_off = 2 * cmax;
+}
+
+// ---- sparse-state tail (Fig. 5) ----
+// Per tail step t: the distinct values (keys) that the sparse legs held after the step take among
+// the requested subspaces; output entry c = key c; A entry index_a[c] = c's key restricted to the legs
+// held before the step; B block index_b[c] = c's bits on the branch's sparse legs.
+struct SparseStep {
+  std::vector<uint64_t> keys;     // sorted prefix values masked to the legs held after the step
+  std::vector<int32_t> ia, ib;
+  uint64_t n_in = 1;              // entries of the step's input
+};
+
+std::vector<SparseStep> sparse_schedule(const Plan& p, const std::vector<uint64_t>& pre) {
+  const int L = (int)p.sparse_legs.size();
+  auto leg_bit = [&](int label) {
+    const int t = (int)(std::find(p.sparse_legs.begin(), p.sparse_legs.end(), label) - p.sparse_legs.begin());
+    return L - 1 - t;  // prefix bit of sparse leg t (MSB first)
+  };
+  std::vector<SparseStep> out;
+  uint64_t mask = 0;
+  std::vector<uint64_t> prev_keys{0};
+  for (size_t i = p.sparse_from; i < p.steps.size(); ++i) {
+    const StemStep& st = p.steps[i];
+    for (int l : st.b_sparse) mask |= 1ull << leg_bit(l);
+    SparseStep ss;
+    ss.n_in = prev_keys.size();
+    for (uint64_t v : pre) ss.keys.push_back(v & mask);
+    std::sort(ss.keys.begin(), ss.keys.end());
+    ss.keys.erase(std::unique(ss.keys.begin(), ss.keys.end()), ss.keys.end());
+    const uint64_t prev_mask = mask & ~[&] {
+      uint64_t m = 0;
+      for (int l : st.b_sparse) m |= 1ull << leg_bit(l);
+      return m;
+    }();
+    for (uint64_t c : ss.keys) {
+      const uint64_t a = c & prev_mask;
+      ss.ia.push_back((int32_t)(std::lower_bound(prev_keys.begin(), prev_keys.end(), a) - prev_keys.begin()));
+      int32_t bidx = 0;
+      for (int l : st.b_sparse) bidx = (bidx << 1) | (int32_t)((c >> leg_bit(l)) & 1);
+      ss.ib.push_back(bidx);
+    }
+    prev_keys = ss.keys;
+    out.push_back(std::move(ss));
+  }
+  return out;
+}
+
+uint64_t pow2_at_least(uint64_t n) {
+  uint64_t r = 1;
+  while (r < n) r <<= 1;
+  return r;
+}
+
+// Bytes of the free stem buffer one chunk of subspaces needs: two ping-pong regions (each the largest
+// tail tensor, permutation passes run on a power-of-two batch) + the index arrays + the top-1 slots.
+uint64_t sparse_need(const Plan& p, const std::vector<SparseStep>& sch, uint64_t& region, uint64_t& idx_off) {
+  const int eb = p.cfg.dtype == TN_CHALF ? 4 : 8;
+  uint64_t r = 0, nidx = 0;
+  for (size_t t = 0; t < sch.size(); ++t) {
+    const StemStep& st = p.steps[p.sparse_from + t];
+    const uint64_t n_in = st.perm ? pow2_at_least(sch[t].n_in) : sch[t].n_in;
+    r = std::max(r, n_in << st.in_layout.size());
+    r = std::max(r, (uint64_t)sch[t].keys.size() << st.out_layout.size());
+    nidx += 2 * sch[t].keys.size();
+  }
+  region = align_up(r * eb, 1024);
+  idx_off = 2 * region;
+  return idx_off + align_up(4 * nidx, 256) + 8 * (sch.empty() ? 1 : sch.back().keys.size()) + 256;
+}
+
+// Runs the sparse-state tail for the subspaces `pre` (in chunks of subspaces when the free stem
+// buffer cannot hold the whole batch: "the number of chunks is determined by the current
+// remaining capacity") and reads their amplitudes + post-selected members.
+void sparse_tail(Plan& p, const tn_buffers* b, const uint64_t* prefixes, size_t n_sub, double* h_amps, int k,
+                 uint64_t* top_idx, cudaStream_t s) {
+  select_device(p);
+  check_buffers(p, b);
+  const int L = (int)p.sparse_legs.size();
+  for (size_t i = 0; i < n_sub; ++i)
+    if (L < 64 && (prefixes[i] >> L) != 0) throw TnError{TN_E_INVALID, "prefix has bits beyond the sparse legs"};
+  unsigned char* W = static_cast<unsigned char*>(b->d_ws);
+  Scratch sc = scratch_of(p, W);
+  const int eb = p.cfg.dtype == TN_CHALF ? 4 : 8;
+  const size_t t0 = (size_t)p.sparse_from, T = p.steps.size() - t0;
+  unsigned char* X = static_cast<unsigned char*>(b->d_stem[p.stem_cur]);
+  unsigned char* Y = static_cast<unsigned char*>(b->d_stem[1 - p.stem_cur]);
+  // distinct subspaces, sorted: the chunks cut this list
+  std::vector<uint64_t> uniq(prefixes, prefixes + n_sub);
+  std::sort(uniq.begin(), uniq.end());
+  uniq.erase(std::unique(uniq.begin(), uniq.end()), uniq.end());
+  int jc = 0;
+  for (;; ++jc) {
+    const uint64_t c = 1ull << jc, per = (uniq.size() + c - 1) / c;
+    bool fits = true;
+    for (uint64_t q = 0; q < c && fits; ++q) {
+      const uint64_t lo = q * per, hi = std::min<uint64_t>(uniq.size(), lo + per);
+      if (lo >= hi) continue;
+      uint64_t region, idx;
+      std::vector<uint64_t> part(uniq.begin() + lo, uniq.begin() + hi);
+      fits = sparse_need(p, sparse_schedule(p, part), region, idx) <= b->stem_bytes;
+    }
+    if (fits) break;
+    if (c >= uniq.size()) throw TnError{TN_E_CAPACITY, "sparse tail: one subspace does not fit the free stem buffer"};
+  }
+  p.sparse_chunks = 1ull << jc;
+  // members: the open legs without the sparse legs, `open` order; stored in the final dense layout
+  std::vector<int> mord;
+  for (int l : p.open)
+    if (std::find(p.sparse_legs.begin(), p.sparse_legs.end(), l) == p.sparse_legs.end()) mord.push_back(l);
+  const std::vector<int>& lay = p.final_layout;
+  const int r = (int)lay.size();
+  if ((int)mord.size() != r) throw TnError{TN_E_INVALID, "internal: sparse result layout does not cover the members"};
+  const uint64_t members = 1ull << r;
+  std::vector<int> bitpos(r);
+  for (int t = 0; t < r; ++t) bitpos[t] = r - 1 - (int)(std::find(lay.begin(), lay.end(), mord[t]) - lay.begin());
+  MemberMap mm;
+  mm.r = r;
+  for (int t = 0; t < r; ++t) mm.src_bit[t] = (int8_t)bitpos[t];
+  const uint64_t c = 1ull << jc, per = (uniq.size() + c - 1) / c;
+  std::vector<double> amp_of(2 * members * uniq.size());
+  std::vector<uint64_t> top_of(uniq.size());
+  for (uint64_t q = 0; q < c; ++q) {
+    const uint64_t lo = q * per, hi = std::min<uint64_t>(uniq.size(), lo + per);
+    if (lo >= hi) continue;
+    std::vector<uint64_t> part(uniq.begin() + lo, uniq.begin() + hi);
+    const std::vector<SparseStep> sch = sparse_schedule(p, part);
+    uint64_t region, idx_off;
+    sparse_need(p, sch, region, idx_off);
+    unsigned char* RA = Y;
+    unsigned char* RB = Y + region;
+    // index arrays: staged on the host, one copy (the stream orders it before the GEMMs)
+    std::vector<int32_t> hidx;
+    std::vector<uint64_t> ia_off(T), ib_off(T);
+    for (size_t t = 0; t < T; ++t) {
+      ia_off[t] = hidx.size();
+      hidx.insert(hidx.end(), sch[t].ia.begin(), sch[t].ia.end());
+      ib_off[t] = hidx.size();
+      hidx.insert(hidx.end(), sch[t].ib.begin(), sch[t].ib.end());
+    }
+    int32_t* didx = reinterpret_cast<int32_t*>(Y + idx_off);
+    TN_CUDA(cudaMemcpyAsync(didx, hidx.data(), 4 * hidx.size(), cudaMemcpyHostToDevice, s));
+    // fresh tail scale chain for this chunk (the stem entering the tail keeps its max slot)
+    TN_CUDA(cudaMemsetAsync(&sc.max_slot[t0 + 1], 0, 4 * T, s));
+    TN_CUDA(cudaMemsetAsync(&sc.exps[2 + 2 * t0], 0, 4 * (2 * T - 1), s));
+    const unsigned char* cur = X;
+    for (size_t t = 0; t < T; ++t) {
+      const size_t i = t0 + t;
+      const StemStep& st = p.steps[i];
+      const uint64_t n_in = sch[t].n_in, n_out = sch[t].keys.size();
+      unsigned char* other = (cur == RA) ? RB : RA;
+      if (st.perm) {  // the same permutation of every entry: batch bits outermost, untouched
+        const int nb = (int)std::log2((double)pow2_at_least(n_in));
+        std::vector<int> axes;
+        for (int a = 0; a < nb; ++a) axes.push_back(a);
+        for (int a : st.perm_axes) axes.push_back(a + nb);
+        launch_permute(other, cur, eb, nb + (int)st.in_layout.size(), axes.data(), s);
+        ++p.launches;
+        cur = other;
+        other = (cur == RA) ? RB : RA;
+      }
+      const uint64_t M = 1ull << st.mlog;
+      const uint32_t K = 1u << st.klog, N = 1u << st.nlog;
+      const float* in_max = &sc.max_slot[i];
+      uint32_t* out_max = reinterpret_cast<uint32_t*>(&sc.max_slot[i + 1]);
+      int* exp_slot = &sc.exps[2 + 2 * i];
+      const bool batched = p.cfg.dtype == TN_CHALF && st.tensor_core && M % 128 == 0 && N >= 8 && K >= 4;
+      if (batched) {
+        BatchSpec bs;
+        bs.ia = didx + ia_off[t];
+        bs.ib = didx + ib_off[t];
+        bs.n_out = n_out;
+        bs.n_a = n_in;
+        bs.n_b = 1ull << st.b_sparse.size();
+        launch_gemm_chalf_tc_batched(reinterpret_cast<__half*>(other), reinterpret_cast<const __half*>(cur),
+                                     reinterpret_cast<const __half*>(W + st.b_off), M, 2 * K, 2 * N, in_max,
+                                     &sc.b_bound[i], out_max, exp_slot, bs, s);
+        ++p.launches;
+      } else {
+        // small steps: one GEMM per entry (identical scale inputs, so every entry writes the same exponent)
+        OutMap om = identity_map(M, N);
+        for (uint64_t e = 0; e < n_out; ++e) {
+          const unsigned char* a = cur + (uint64_t)sch[t].ia[e] * (M * K) * eb;
+          const unsigned char* bb = W + st.b_off + (uint64_t)sch[t].ib[e] * st.b_blk;
+          unsigned char* cc = other + e * (M * N) * eb;
+          if (p.cfg.dtype == TN_CHALF) {
+            if (st.tensor_core)
+              launch_gemm_chalf_tc(reinterpret_cast<__half*>(cc), reinterpret_cast<const __half*>(a),
+                                   reinterpret_cast<const __half*>(bb), M, 2 * K, 2 * N, in_max, &sc.b_bound[i], out_max,
+                                   exp_slot, &om, s);
+            else
+              launch_gemm_chalf_simt(reinterpret_cast<__half2*>(cc), reinterpret_cast<const __half2*>(a),
+                                     reinterpret_cast<const __half*>(bb), M, K, N, in_max, &sc.b_bound[i], out_max,
+                                     exp_slot, &om, s);
+          } else {
+            launch_gemm_c64(reinterpret_cast<float2*>(cc), reinterpret_cast<const float2*>(a),
+                            reinterpret_cast<const float2*>(bb), M, K, N, &om, s);
+          }
+          ++p.launches;
+        }
+      }
+      cur = other;
+    }
+    // read this chunk: amplitudes, exponents, post-selection
+    const uint64_t n_last = sch.back().keys.size();
+    uint64_t* d_top = reinterpret_cast<uint64_t*>(Y + align_up(idx_off + 4 * hidx.size(), 256));
+    const bool dev_top = p.cfg.dtype == TN_CHALF && top_idx && k == 1;
+    if (dev_top) launch_top1_chalf(reinterpret_cast<const __half2*>(cur), n_last, members, mm, d_top, s);
+    std::vector<int> ex(p.n_exp_slots);
+    TN_CUDA(cudaMemcpyAsync(ex.data(), sc.exps, 4 * ex.size(), cudaMemcpyDeviceToHost, s));
+    std::vector<uint64_t> top(n_last);
+    if (dev_top) TN_CUDA(cudaMemcpyAsync(top.data(), d_top, 8 * n_last, cudaMemcpyDeviceToHost, s));
+    std::vector<double> vals(2 * n_last * members);
+    if (p.cfg.dtype == TN_CHALF) {
+      std::vector<__half> buf(vals.size());
+      TN_CUDA(cudaMemcpyAsync(buf.data(), cur, 2 * buf.size(), cudaMemcpyDeviceToHost, s));
+      TN_CUDA(cudaStreamSynchronize(s));
+      for (size_t e = 0; e < buf.size(); ++e) vals[e] = (double)__half2float(buf[e]);
+    } else {
+      std::vector<float> buf(vals.size());
+      TN_CUDA(cudaMemcpyAsync(buf.data(), cur, 4 * buf.size(), cudaMemcpyDeviceToHost, s));
+      TN_CUDA(cudaStreamSynchronize(s));
+      for (size_t e = 0; e < buf.size(); ++e) vals[e] = buf[e];
+    }
+    int E = 0;
+    for (int e : ex) E += e;
+    for (uint64_t u = lo; u < hi; ++u) {
+      const uint64_t e = (uint64_t)(std::lower_bound(sch.back().keys.begin(), sch.back().keys.end(), uniq[u]) -
+                                    sch.back().keys.begin());
+      double* out = &amp_of[2 * members * u];
+      for (uint64_t o = 0; o < members; ++o) {
+        uint64_t g = 0;
+        for (int t = 0; t < r; ++t)
+          if ((o >> (r - 1 - t)) & 1) g |= 1ull << bitpos[t];
+        out[2 * o] = std::ldexp(vals[2 * (e * members + g)], -E);
+        out[2 * o + 1] = std::ldexp(vals[2 * (e * members + g) + 1], -E);
+      }
+      top_of[u] = dev_top ? top[e] : 0;
+    }
+  }
+  for (size_t i = 0; i < n_sub; ++i) {
+    const uint64_t u = (uint64_t)(std::lower_bound(uniq.begin(), uniq.end(), prefixes[i]) - uniq.begin());
+    memcpy(h_amps + 2 * members * i, &amp_of[2 * members * u], 16 * members);
+    if (top_idx && k > 0) {
+      if (k == 1 && p.cfg.dtype == TN_CHALF) {
+        top_idx[i] = top_of[u];
+      } else {
+        const double* a = h_amps + 2 * members * i;
+        std::vector<uint64_t> idx(members);
+        for (uint64_t m = 0; m < members; ++m) idx[m] = m;
+        auto prob = [&](uint64_t m) {
+          const double pr = a[2 * m] * a[2 * m] + a[2 * m + 1] * a[2 * m + 1];
+          return pr == pr ? pr : -1.0;
+        };
+        std::stable_sort(idx.begin(), idx.end(), [&](uint64_t x, uint64_t y) { return prob(x) > prob(y); });
+        for (int q = 0; q < k && (uint64_t)q < members; ++q) top_idx[i * k + q] = idx[q];
+      }
+    }
+  }
 }
 
 // Result readout (a.8 + a.9), synchronous.  The result block of every rank (sharded: gathered in
@@ -1039,6 +1346,11 @@ int tn_sample_amplitudes(tn_plan* h, const tn_buffers* b, const uint64_t* prefix
     Plan& p = *h->p;
     select_device(p);
     cudaStream_t s = (cudaStream_t)stream;
+    if (p.sparse_from >= 0) {
+      if (!prefixes) throw TnError{TN_E_INVALID, "a sparse-state plan needs the subspace prefixes"};
+      sparse_tail(p, b, prefixes, n_sub, h_amps, k, top_idx, s);
+      return TN_OK;
+    }
     if (prefixes) {
       std::vector<uint64_t> ids(prefixes, prefixes + n_sub);
       read_result(p, b, s, &ids, h_amps, k, top_idx);

@@ -474,7 +474,10 @@ def _sparse_operands(rng, m_a, n_b, M, K, N):
 
 def _close(got, ref):
     tol = 2.0 ** -10 * np.abs(ref) + 1e-3 * np.sqrt(np.mean(np.abs(ref) ** 2)) + 1e-7
-    return np.all(np.abs(got - ref) <= tol)
+    bad = np.abs(got - ref) > tol
+    if bad.any():
+        print("mismatches", int(bad.sum()), "of", bad.size, "first at", np.argwhere(bad)[:4].tolist())
+    return not bad.any()
 
 
 @pytest.mark.parametrize("M,K,N", [(128, 8, 8), (256, 64, 16), (512, 32, 128), (128, 256, 64)])
@@ -498,7 +501,7 @@ def test_gemm_chalf_batched_vs_oracle_gather(env, M, K, N):
     assert _close(g[..., 0] + 1j * g[..., 1], ref)
 
 
-@pytest.mark.parametrize("M,K,N", [(128, 16, 8), (256, 64, 32), (128, 32, 256)])
+@pytest.mark.parametrize("M,K,N", [(128, 16, 32), (256, 64, 32), (128, 32, 256), (256, 128, 64)])
 def test_gemm_chalf_padded_index_vs_oracle(env, M, K, N):
     """Fig. 5 top: the padded 2-d index of Index_B (m_r = max repeat of Index_A, -1 padding,
     built by the oracle's build_padded_index) drives C_P = A x B_P on the GPU; the extracted valid
