@@ -113,6 +113,7 @@ struct MaxSlots {
   const float* p[8];
 };
 void launch_max_slots(float* dst, const MaxSlots& src, cudaStream_t s);
+void launch_redo_check(const uint32_t* out_max, const float* in_max, float* redo_in, int bits, cudaStream_t s);
 void launch_copy_c64(float2* dst, const float2* src, uint64_t n, cudaStream_t s);
 void launch_gemm_c64(float2* c, const float2* a, const float2* b, uint64_t M, uint32_t K, uint32_t N,
                      const OutMap* om, cudaStream_t s);

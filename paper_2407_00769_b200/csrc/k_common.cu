@@ -201,6 +201,23 @@ void launch_max_slots(float* dst, const MaxSlots& src, cudaStream_t s) {
   TN_CUDA(cudaGetLastError());
 }
 
+// Scale re-run decision (reading C-A28, revised): a GEMM's output exponent comes from a bound
+// (max|A| x max column 1-norm of B_P) so |C| <= 2^14 is guaranteed, but heavy cancellation can leave
+// the actual max |C| far below it and push the fp16 output into subnormals / zero.  When the realised
+// max (out_max, already scaled) is below 2^(14 - bits), the GEMM is run again from the same input
+// with an input max smaller by exactly 2^delta (delta = the exponent that brings out_max near 2^14),
+// i.e. an output exponent larger by delta; otherwise the re-run launch exits at once (-1).
+__global__ void redo_check_kernel(const uint32_t* out_max, const float* in_max, float* redo_in, int bits) {
+  const float m = __uint_as_float(*out_max);
+  const int d = scale_exp_for(m);
+  *redo_in = (m > 0.f && d >= bits) ? ldexpf(*in_max, -d) : -1.f;
+}
+
+void launch_redo_check(const uint32_t* out_max, const float* in_max, float* redo_in, int bits, cudaStream_t s) {
+  redo_check_kernel<<<1, 1, 0, s>>>(out_max, in_max, redo_in, bits);
+  TN_CUDA(cudaGetLastError());
+}
+
 void launch_copy_c64(float2* dst, const float2* src, uint64_t n, cudaStream_t s) {
   TN_CUDA(cudaMemcpyAsync(dst, src, n * sizeof(float2), cudaMemcpyDeviceToDevice, s));
 }

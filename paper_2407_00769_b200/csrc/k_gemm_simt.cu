@@ -124,6 +124,7 @@ __global__ void __launch_bounds__(256) gemm_chalf_simt_kernel(__half2* __restric
   __shared__ float2 sB[2048];
   const bool smem_b = K * N <= 2048;
   int e = 0;
+  if (in_max && in_max[0] < 0.f) return;  // scale re-run not needed (runtime.cu redo)
   if (in_max && b_bound) e = scale_exp_for(in_max[0] * b_bound[0]);
   if (exp_slot && blockIdx.x == 0 && threadIdx.x == 0) *exp_slot = e;
   const float sc = ldexpf(1.f, e);
@@ -224,6 +225,7 @@ __global__ void __launch_bounds__(256) gemm_chalf_rows_kernel(uint32_t* __restri
   constexpr int R = RowsCfg<K, N>::kRpt;
   __shared__ float2 sB[K * N];
   int e = 0;
+  if (in_max && in_max[0] < 0.f) return;  // scale re-run not needed (runtime.cu redo)
   if (in_max && b_bound) e = scale_exp_for(in_max[0] * b_bound[0]);
   if (exp_slot && blockIdx.x == 0 && threadIdx.x == 0) *exp_slot = e;
   const float sc = ldexpf(1.f, e);

@@ -705,6 +705,17 @@ static Plan* load_plan_fixed(const char* json, size_t len, const tn_config* cfg_
     }
   }
   smax = std::max<uint64_t>(smax, (payload_bytes + eb - 1) / eb);
+  if (p.sparse_from >= 0) {
+    // sparse tail: the stem entering it stays in one buffer (every chunk of subspaces re-reads it),
+    // the tail ping-pongs between two regions of the other: size the buffers so that at least one
+    // subspace at a time fits (runtime.cu sparse_need; larger batches are chunked)
+    uint64_t tmax = 0;
+    for (size_t s = p.sparse_from; s < p.steps.size(); ++s)
+      tmax = std::max<uint64_t>(tmax, std::max<uint64_t>(1ull << p.steps[s].in_layout.size(),
+                                                         1ull << p.steps[s].out_layout.size()));
+    const uint64_t need = 2 * align_up(tmax * eb, 1024) + 8 * (p.steps.size() - p.sparse_from) + 4096;
+    smax = std::max<uint64_t>(smax, (need + eb - 1) / eb);
+  }
   p.stem_elems_max = smax;
   p.max_stem_log2 = 0;
   while ((1ull << p.max_stem_log2) < smax) p.max_stem_log2++;
@@ -752,7 +763,7 @@ static Plan* load_plan_fixed(const char* json, size_t len, const tn_config* cfg_
   size_t S = p.steps.size();
   p.n_exp_slots = (int)(2 * S + 4);
   // max_slot[S+2], b_bound[S+2], b_max[S+2], exps[n_exp_slots], entry_max (runtime.cu scratch_of)
-  off += align_up(4 * 3 * (S + 2) + 4 * p.n_exp_slots + 4 + 64, 256);
+  off += align_up(4 * 4 * (S + 2) + 4 * p.n_exp_slots + 4 + 64, 256);
   if (!p.split_modes.empty()) {
     // per chunk: max slots [T+1] and step exponents [T] of the tail (each chunk has its own scale)
     const uint64_t T = p.steps.size() - p.split_from, c = 1ull << p.split_log2;

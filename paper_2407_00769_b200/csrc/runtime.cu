@@ -248,6 +248,7 @@ struct Scratch {
   float* max_slot;    // [S+2]   max |real| of the stem entering step i (float bits via atomicMax)
   float* b_bound;     // [S+2]
   uint32_t* b_max;    // [S+2]
+  float* redo_in;     // [S+2]   input max of the scale re-run of step i (-1: not needed)
   int* exps;          // [n_exp_slots]
   uint32_t* entry_max;
   uint64_t bytes;
@@ -260,7 +261,8 @@ Scratch scratch_of(const Plan& p, unsigned char* W) {
   s.max_slot = reinterpret_cast<float*>(base);
   s.b_bound = s.max_slot + (S + 2);
   s.b_max = reinterpret_cast<uint32_t*>(s.b_bound + (S + 2));
-  s.exps = reinterpret_cast<int*>(s.b_max + (S + 2));
+  s.redo_in = reinterpret_cast<float*>(s.b_max + (S + 2));
+  s.exps = reinterpret_cast<int*>(s.redo_in + (S + 2));
   s.entry_max = reinterpret_cast<uint32_t*>(s.exps + p.n_exp_slots);
   s.bytes = p.ws_total - p.ws_scratch;
   return s;
@@ -546,8 +548,27 @@ void rec_event(Plan& p, size_t k, cudaStream_t s) {
 
 // One stem GEMM (Eq. 6 on tcgen05, SIMT for small K*N, complex64 SIMT for the fp32 path) from
 // `src` to `dst`; mshift > 0 runs it on one chunk of the split tail (the top mshift m bits fixed).
+int redo_bits() {
+  static const int b = getenv("TN_REDO_BITS") ? atoi(getenv("TN_REDO_BITS")) : 10;
+  return b;
+}
+
+void run_gemm_once(Plan& p, const StemStep& st, size_t i, const void* src, void* dst, int mshift, const float* in_max,
+                   uint32_t* out_max, int* exp_slot, unsigned char* W, const Scratch& sc, cudaStream_t s);
+
+// One stem GEMM plus its scale re-run (complex-half: redo_check + the same launch, which exits at once
+// unless the realised output max lost more than TN_REDO_BITS (default 10) bits of fp16 headroom).
 void run_gemm(Plan& p, const StemStep& st, size_t i, const void* src, void* dst, int mshift, const float* in_max,
               uint32_t* out_max, int* exp_slot, unsigned char* W, const Scratch& sc, cudaStream_t s) {
+  run_gemm_once(p, st, i, src, dst, mshift, in_max, out_max, exp_slot, W, sc, s);
+  if (p.cfg.dtype != TN_CHALF || !in_max || redo_bits() <= 0) return;
+  launch_redo_check(out_max, in_max, &sc.redo_in[i], redo_bits(), s);
+  run_gemm_once(p, st, i, src, dst, mshift, &sc.redo_in[i], out_max, exp_slot, W, sc, s);
+  ++p.launches;
+}
+
+void run_gemm_once(Plan& p, const StemStep& st, size_t i, const void* src, void* dst, int mshift, const float* in_max,
+                   uint32_t* out_max, int* exp_slot, unsigned char* W, const Scratch& sc, cudaStream_t s) {
   const int mlog = st.mlog - mshift;
   const uint64_t M = 1ull << mlog;
   const uint32_t K = 1u << st.klog, N = 1u << st.nlog;
@@ -1024,6 +1045,12 @@ void sparse_tail(Plan& p, const tn_buffers* b, const uint64_t* prefixes, size_t 
       uint32_t* out_max = reinterpret_cast<uint32_t*>(&sc.max_slot[i + 1]);
       int* exp_slot = &sc.exps[2 + 2 * i];
       const bool batched = p.cfg.dtype == TN_CHALF && st.tensor_core && M % 128 == 0 && N >= 8 && K >= 4;
+      // scale re-run (run_gemm): the whole batched step again when the realised max lost too many bits
+      for (int pass = 0; pass < (p.cfg.dtype == TN_CHALF && redo_bits() > 0 ? 2 : 1); ++pass) {
+      if (pass == 1) {
+        launch_redo_check(out_max, &sc.max_slot[i], &sc.redo_in[i], redo_bits(), s);
+        in_max = &sc.redo_in[i];
+      }
       if (batched) {
         BatchSpec bs;
         bs.ia = didx + ia_off[t];
@@ -1057,6 +1084,7 @@ void sparse_tail(Plan& p, const tn_buffers* b, const uint64_t* prefixes, size_t 
           }
           ++p.launches;
         }
+      }
       }
       cur = other;
     }
