@@ -97,7 +97,16 @@ typedef struct {
                                 the innermost log2(comm_group/2) modes in place quantises straight
                                 from the unpermuted stem (tn_permute_quant_f16, no permutation
                                 pass); 1: permutation pass, then the codec */
-  int32_t reserved[2];
+  int32_t recompute;         /* 1: recomputation on halves: the stem
+                                is halved along one open leg (a free mode of the largest stem
+                                tensor) right before the step that produces that tensor; the rest
+                                of the path runs twice, once per half, inside the two stem buffers,
+                                and the halves are concatenated (split machinery with 2 chunks, so
+                                tn_split_contract runs the halves).  Peak stem bytes halve when the
+                                largest tensor lies in the recomputed region.  Needs split_log2 = 0;
+                                no mode swap may fall into the recomputed region ("there is no data
+                                communication").  0: off */
+  int32_t reserved;
 } tn_config;
 
 /* Caller-owned device buffers lent to a call (P:18-22 double buffering). */
@@ -124,6 +133,8 @@ typedef struct {
   uint64_t h2d_bytes;        /* bytes tn_plan_upload copies host->device */
   uint64_t split_chunks;     /* chunk count of the split-type tail (1 = none) */
   uint64_t n_launches;       /* kernels the last tn_stem_contract launched (0 before the first) */
+  uint64_t n_sparse_legs;    /* sparse-state legs (plan "sparse_legs"): a subspace block holds
+                                2^(n_open - n_sparse_legs) members */
 } tn_plan_info;
 
 TN_API const char* tn_last_error(void);

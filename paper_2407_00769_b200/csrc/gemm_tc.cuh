@@ -753,8 +753,9 @@ __global__ void __launch_bounds__(kAMode == 1 ? kThreadsGather : kThreads, 1)
             float x0 = __uint_as_float(r[h][2 * j]) * sc, x1 = __uint_as_float(r[h][2 * j + 1]) * sc;
             if (skip) x0 = x1 = 0.f;  // zero block of the padded 2-d index (TMEM was not written)
             __half2 hv = __floats2half2_rn(x0, x1);
-            float2 hf = __half22float2(hv);
-            if (j < nvalid) mx = fmaxf(mx, fmaxf(fabsf(hf.x), fabsf(hf.y)));
+            // the max of the scaled fp32 values (not of their fp16 roundings): it stays meaningful when
+            // cancellation pushes the stored values into fp16 subnormals or zero (scale re-run, redo_check)
+            if (j < nvalid) mx = fmaxf(mx, fmaxf(fabsf(x0), fabsf(x1)));
             pk[j] = *reinterpret_cast<uint32_t*>(&hv);
           }
           if (scat) {

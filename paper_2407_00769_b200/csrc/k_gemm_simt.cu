@@ -169,8 +169,7 @@ __global__ void __launch_bounds__(256) gemm_chalf_simt_kernel(__half2* __restric
           ci = fmaf(a.x, b.y, fmaf(a.y, b.x, ci));
         }
         __half2 h = __floats2half2_rn(cr * sc, ci * sc);
-        float2 hf = __half22float2(h);
-        mx = fmaxf(mx, fmaxf(fabsf(hf.x), fabsf(hf.y)));
+        mx = fmaxf(mx, fmaxf(fabsf(cr * sc), fabsf(ci * sc)));  // fp32 max (see gemm_tc.cuh epilogue)
         pk[v] = *reinterpret_cast<uint32_t*>(&h);
       }
       const uint64_t m = m0 + r;
@@ -288,8 +287,7 @@ __global__ void __launch_bounds__(256) gemm_chalf_rows_kernel(uint32_t* __restri
           ci = fmaf(a[r * K + k].x, b.y, fmaf(a[r * K + k].y, b.x, ci));
         }
         __half2 h = __floats2half2_rn(cr * sc, ci * sc);
-        float2 hf = __half22float2(h);
-        if (r == 0 || m0 + r < M) mx = fmaxf(mx, fmaxf(fabsf(hf.x), fabsf(hf.y)));
+        if (r == 0 || m0 + r < M) mx = fmaxf(mx, fmaxf(fabsf(cr * sc), fabsf(ci * sc)));  // fp32 max
         out[r * N + n] = *reinterpret_cast<uint32_t*>(&h);
       }
     if (om.identity && full) {

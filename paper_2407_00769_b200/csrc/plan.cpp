@@ -313,7 +313,9 @@ static Plan* load_plan_fixed(const char* json, size_t len, const tn_config* cfg_
   // ---- split-type tail: 2^j chunks fix j open legs.  The chosen legs are
   // the open legs that enter the stem earliest (longest tail); they sort outermost in every layout.
   std::set<int> split_set;
-  if (cfg.split_log2 > 0 && entry_idx >= 0) {
+  if (cfg.recompute && cfg.split_log2 != 0) throw err(TN_E_INVALID, "recompute needs split_log2 = 0");
+  if (cfg.recompute && !sparse_set.empty()) throw err(TN_E_UNSUPPORTED, "recompute together with sparse legs");
+  if ((cfg.split_log2 > 0 || cfg.recompute) && entry_idx >= 0) {
     std::map<int, int> first_app;  // open leg -> first stem step whose INPUT holds it
     for (int l : p.nodes[p.stem_entry].labels) first_app[l] = 0;
     {
@@ -328,14 +330,30 @@ static Plan* load_plan_fixed(const char* json, size_t len, const tn_config* cfg_
     }
     std::vector<int> cand(p.open.begin(), p.open.end());
     std::stable_sort(cand.begin(), cand.end(), [&](int a, int b) { return first_app[a] < first_app[b]; });
-    if ((int)cand.size() < cfg.split_log2) throw err(TN_E_INFEASIBLE, "split: fewer open legs than split modes");
-    for (int t = 0; t < cfg.split_log2; ++t) {
+    int nsplit = cfg.split_log2;
+    int from_min = split_min;
+    if (cfg.recompute) {
+      // recomputation on halves: halve right before the step producing the largest stem
+      // tensor, along an open leg (a free mode that survives to the end, so the halves concatenate)
+      // already held by the stem there
+      nsplit = 1;
+      std::vector<int> sz(step_nodes.size());
+      for (size_t s = 0; s < step_nodes.size(); ++s) sz[s] = (int)p.nodes[step_nodes[s]].labels.size();
+      const int peak = (int)(std::max_element(sz.begin(), sz.end()) - sz.begin());
+      cand.erase(std::remove_if(cand.begin(), cand.end(), [&](int l) { return first_app[l] > peak; }), cand.end());
+      if (cand.empty()) throw err(TN_E_INFEASIBLE, "recompute: no open leg in the stem before its largest tensor");
+      std::stable_sort(cand.begin(), cand.end(), [&](int a, int b) { return first_app[a] > first_app[b]; });
+      from_min = std::max(from_min, peak);
+      p.recompute_from = peak;
+    }
+    if ((int)cand.size() < nsplit) throw err(TN_E_INFEASIBLE, "split: fewer open legs than split modes");
+    for (int t = 0; t < nsplit; ++t) {
       split_set.insert(cand[t]);
       p.split_modes.push_back(cand[t]);
       p.split_from = std::max(p.split_from, first_app[cand[t]]);
     }
-    p.split_from = std::max(p.split_from, split_min);
-    p.split_log2 = cfg.split_log2;
+    p.split_from = std::max(p.split_from, from_min);
+    p.split_log2 = nsplit;
     if (p.split_from >= (int)step_nodes.size()) throw err(TN_E_INFEASIBLE, "split: no tail step holds the split modes");
   }
   auto nu = [&](int l) {
@@ -660,10 +678,11 @@ static Plan* load_plan_fixed(const char* json, size_t len, const tn_config* cfg_
       }
       p.final_perm = false;  // the host reorders the chunked result (each chunk has its own scale)
       // the free buffer holds two chunk regions plus the assembled result
-      smax = std::max<uint64_t>(smax, 2 * cmax + (1ull << L.size()));
-      // the full-size tensors of the tail are never materialised: the stem buffers only need the
-      // tail's input (the stem entering the split point)
-      uint64_t need = 2 * cmax + (1ull << L.size());
+      // the full-size tensors of the tail are never materialised: one buffer holds the tail's input
+      // (the stem entering the split point) + one chunk region, the other one chunk region + the
+      // result slots (runtime.cu split_contract)
+      const uint64_t in_full = 1ull << p.steps[p.split_from].in_layout.size();
+      uint64_t need = std::max<uint64_t>(cmax + (1ull << L.size()), align_up(in_full * eb, 1024) / eb + cmax);
       for (int s = 0; s <= p.split_from && s < (int)p.steps.size(); ++s) {
         const StemStep& st = p.steps[s];
         need = std::max<uint64_t>(need, 1ull << st.in_layout.size());
@@ -845,7 +864,8 @@ std::string report_json(const Plan& p, const std::vector<float>& ms) {
   jlist(o, p.stem_entry >= 0 ? p.nodes[p.stem_entry].labels : std::vector<int>());
   o << ",\"split_modes\":";
   jlist(o, p.split_modes);
-  o << ",\"split_from\":" << p.split_from << ",\"sparse_from\":" << p.sparse_from
+  o << ",\"split_from\":" << p.split_from << ",\"recompute_from\":" << p.recompute_from
+    << ",\"sparse_from\":" << p.sparse_from
     << ",\"sparse_chunks\":" << p.sparse_chunks << ",\"sparse_legs\":";
   jlist(o, p.sparse_legs);
   o << ",\"shard0\":";

@@ -85,6 +85,7 @@ struct Plan {
   int split_from = -1;            // first split-type step index (-1: none)
   std::vector<int> sparse_legs;   // open legs given per correlated subspace (sparse-state batch)
   int sparse_from = -1;           // first sparse-tail step (-1: none)
+  int recompute_from = -1;        // recomputation on halves: the step producing the largest tensor
   uint64_t sparse_chunks = 0;     // subspace chunks of the last sparse-tail run
   int split_log2 = 0;             // chunks = 2^split_log2
   std::vector<int> split_modes;   // open legs fixed per chunk (outermost in every tail layout)

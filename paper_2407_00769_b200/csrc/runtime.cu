@@ -838,13 +838,18 @@ void split_contract(Plan& p, const tn_buffers* b, cudaStream_t s, const std::vec
   for (uint64_t i = 0; i < nsel; ++i) p.tail_slots[i] = ids ? (*ids)[i] : i;
   const uint64_t chunk_in = 1ull << (p.steps[p.split_from].in_layout.size() - j);
   const uint64_t chunk_out = 1ull << (p.final_layout.size() - j);
-  if ((2 * cmax + chunks * chunk_out) * eb > b->stem_bytes)
-    throw TnError{TN_E_CAPACITY, "split tail: chunk regions do not fit the free stem buffer"};
+  // the chunk intermediates ping-pong between region RA at the start of the free buffer and region RB
+  // behind the tail's input in the stem buffer (which every chunk reads in place); the result slots
+  // follow RA.  Each buffer then holds at most one chunk-sized intermediate, so halving the tail
+  // (recomputation) halves the peak bytes per buffer.
+  const uint64_t in_bytes = align_up(chunks * chunk_in * eb, 1024);
+  if ((cmax + chunks * chunk_out) * eb > b->stem_bytes || in_bytes + cmax * eb > b->stem_bytes)
+    throw TnError{TN_E_CAPACITY, "split tail: chunk regions do not fit the stem buffers"};
   unsigned char* X = static_cast<unsigned char*>(b->d_stem[p.stem_cur]);
   unsigned char* Y = static_cast<unsigned char*>(b->d_stem[1 - p.stem_cur]);
   unsigned char* RA = Y;
-  unsigned char* RB = Y + cmax * eb;
-  unsigned char* RES = Y + 2 * cmax * eb;
+  unsigned char* RB = X + in_bytes;
+  unsigned char* RES = Y + cmax * eb;
   float* cmaxs = reinterpret_cast<float*>(sc.entry_max + 1);   // [chunks][T+1]
   int* cexps = reinterpret_cast<int*>(cmaxs + chunks * (T + 1));  // [chunks][T]
   // timing: the whole chunked tail is attributed to the final interval of the report
@@ -878,7 +883,7 @@ void split_contract(Plan& p, const tn_buffers* b, cudaStream_t s, const std::vec
   rec_event(p, 2 + 2 * p.steps.size(), s);
   p.ev_valid = p.timing != 0;
   p.result_buf = 1 - p.stem_cur;
-  p.result_off = 2 * cmax;
+  p.result_off = cmax;
 }
 
 // ---- sparse-state tail (Fig. 5) ----
@@ -1324,6 +1329,7 @@ int tn_plan_info_get(const tn_plan* h, tn_plan_info* info) {
   info->h2d_bytes = p.h2d_bytes;
   info->split_chunks = 1ull << p.split_log2;
   info->n_launches = p.launches;
+  info->n_sparse_legs = p.sparse_legs.size();
   return TN_OK;
 }
 

@@ -28,7 +28,8 @@ class tn_config(C.Structure):
     _fields_ = [("dtype", C.c_int32), ("stem_min_log2", C.c_int32), ("comm_codec", C.c_int32),
                 ("comm_group", C.c_int32), ("stem_capacity_bytes", C.c_uint64), ("split_log2", C.c_int32),
                 ("layout_policy", C.c_int32), ("quant_from_pct", C.c_int32), ("virtual_world", C.c_int32),
-                ("no_gather", C.c_int32), ("no_fuse_swap_quant", C.c_int32), ("reserved", C.c_int32 * 2)]
+                ("no_gather", C.c_int32), ("no_fuse_swap_quant", C.c_int32), ("recompute", C.c_int32),
+                ("reserved", C.c_int32)]
 
 
 class tn_buffers(C.Structure):
@@ -41,7 +42,8 @@ class tn_plan_info(C.Structure):
                 ("n_stem_steps", C.c_uint64), ("n_permutes", C.c_uint64), ("n_common", C.c_uint64),
                 ("stem_flops", C.c_double), ("total_flops", C.c_double), ("stem_bytes_alg", C.c_double),
                 ("perm_bytes", C.c_double), ("n_open", C.c_uint64), ("max_stem_log2", C.c_uint64),
-                ("h2d_bytes", C.c_uint64), ("split_chunks", C.c_uint64), ("n_launches", C.c_uint64)]
+                ("h2d_bytes", C.c_uint64), ("split_chunks", C.c_uint64), ("n_launches", C.c_uint64),
+                ("n_sparse_legs", C.c_uint64)]
 
 
 _lib = None
@@ -125,8 +127,9 @@ def _stream(stream):
 
 def make_config(dtype=TN_CHALF, stem_min_log2=20, comm_codec=TN_COMM_INT8, comm_group=128,
                 stem_capacity_bytes=0, split_log2=0, layout_policy=0, virtual_world=1, quant_from_pct=-1,
-                no_gather=0, no_fuse_swap_quant=0):
+                no_gather=0, no_fuse_swap_quant=0, recompute=0):
     c = tn_config()
+    c.recompute = recompute
     c.no_gather = no_gather
     c.no_fuse_swap_quant = no_fuse_swap_quant
     c.layout_policy = layout_policy
@@ -224,7 +227,8 @@ def tn_sample_sparse(plan, bufs, prefixes, k=1, stream=None):
     legs) and the post-selected member of each.  Returns (complex128 [n_sub, members], top [n_sub, k])."""
     import numpy as np
     info = plan.info()
-    j = int(np.log2(info["split_chunks"]))
+    # sparse-state plan: subspaces are values of the sparse legs; split plan: values of the split legs
+    j = info["n_sparse_legs"] or int(np.log2(info["split_chunks"]))
     members = 1 << (info["n_open"] - j)
     pre = np.ascontiguousarray(np.asarray(prefixes, dtype=np.uint64))
     out = np.empty(2 * len(pre) * members, dtype=np.float64)

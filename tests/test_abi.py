@@ -253,3 +253,23 @@ def test_codec_group_validation(tnmod, c1_plan):
     _load(tnmod, c1_plan, stem_min_log2=6, comm_codec=tnmod.TN_COMM_INT8_TENSOR, comm_group=8)
     with pytest.raises(tnmod.TnError):
         _load(tnmod, c1_plan, stem_min_log2=6, comm_codec=7)
+
+
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
+def test_recompute_on_halves_halves_peak(tnmod, world):
+    """Recomputation on halves: the stem is halved along an open leg
+    right before the step that produces its largest tensor; per-buffer stem bytes halve (+ the
+    tail input), no mode swap falls into the recomputed region, two chunks."""
+    with open(os.path.join(ROOT, "plans", "c3_sweep.json")) as f:
+        plan = json.load(f)
+    base = _load(tnmod, plan, stem_min_log2=20, virtual_world=world).info()["stem_bytes"]
+    p = _load(tnmod, plan, stem_min_log2=20, virtual_world=world, recompute=1)
+    rep = p.report()
+    assert p.info()["split_chunks"] == 2 and rep["recompute_from"] >= 0
+    assert rep["split_from"] >= rep["recompute_from"]
+    sizes = [s["m"] + s["n"] for s in rep["steps"]]
+    assert p.info()["stem_bytes"] <= 0.52 * base
+    assert all(not s["swap"] for s in rep["steps"] if s["split"])
+    with pytest.raises(tnmod.TnError):
+        _load(tnmod, plan, stem_min_log2=20, recompute=1, split_log2=2)
+    assert max(sizes) + (world.bit_length() - 1) >= 32    # the recomputed region holds the 2^33 tensor

@@ -250,3 +250,35 @@ def test_c3_subslice_fp16_vs_complex64(tn):
     del p
     _free()
     assert metrics.rel_l2(a16, a32) <= 2e-2
+
+
+def test_recompute_on_halves_full_c3(tn):
+    """Recomputation on halves at full size (round-1 C3 plan, stem 2^33): the two halves, each run
+    through the rest of the path inside the stem buffers and concatenated, give the same amplitudes
+    as the unhalved run with half the stem-buffer bytes."""
+    c3 = _plan("c3_sweep")
+    p0 = tn.Plan(c3, tn.make_config(stem_min_log2=20))
+    one = tn.contract(p0, tn.Buffers(p0), 0)
+    need0 = p0.info()["stem_bytes"]
+    del p0
+    _free()
+    p = tn.Plan(c3, tn.make_config(stem_min_log2=20, recompute=1))
+    assert p.info()["stem_bytes"] <= 0.52 * need0
+    got = tn.contract(p, tn.Buffers(p), 0)
+    del p
+    _free()
+    assert metrics.rel_l2(got, one) <= 1e-2
+
+
+@pytest.mark.parametrize("dtype", [0, 1])
+def test_recompute_on_halves_vs_oracle(tn, dtype):
+    """C2 sub-slice: recomputed halves vs the oracle, and complex64 bit-identical to no recompute."""
+    sub = MP.sub_slice(_plan("c2"), 22)
+    ref = contract.contract(load(sub), 0)
+    p = tn.Plan(sub, tn.make_config(dtype=dtype, stem_min_log2=12, recompute=1))
+    assert p.info()["split_chunks"] == 2
+    got = tn.contract(p, tn.Buffers(p), 0)
+    assert metrics.rel_l2(got, ref) <= TOL[dtype]
+    if dtype == 1:
+        p0 = tn.Plan(sub, tn.make_config(dtype=1, stem_min_log2=12))
+        assert np.array_equal(tn.contract(p0, tn.Buffers(p0), 0), got)
