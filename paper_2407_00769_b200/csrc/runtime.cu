@@ -1026,8 +1026,8 @@ void sparse_tail(Plan& p, const tn_buffers* b, const uint64_t* prefixes, size_t 
     int32_t* didx = reinterpret_cast<int32_t*>(Y + idx_off);
     TN_CUDA(cudaMemcpyAsync(didx, hidx.data(), 4 * hidx.size(), cudaMemcpyHostToDevice, s));
     // fresh tail scale chain for this chunk (the stem entering the tail keeps its max slot)
+    // (every tail GEMM rewrites its exponent slot 2 + 2i; the B_P slots 1 + 2i stay from the head)
     TN_CUDA(cudaMemsetAsync(&sc.max_slot[t0 + 1], 0, 4 * T, s));
-    TN_CUDA(cudaMemsetAsync(&sc.exps[2 + 2 * t0], 0, 4 * (2 * T - 1), s));
     const unsigned char* cur = X;
     for (size_t t = 0; t < T; ++t) {
       const size_t i = t0 + t;

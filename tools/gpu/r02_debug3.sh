@@ -1,0 +1,5 @@
+set -x
+python -m pytest tests/test_gpu_sparse_state.py tests/test_gpu_e2e.py -m gpu -q --timeout 900 -k "sparse or recompute or split" -rA > gpurun_out/t7.log 2>&1
+timeout 900 python tools/debug_parity.py c3 20,24 > gpurun_out/dbg3_c3.log 2>&1
+timeout 600 python tools/debug_parity.py c3_sweep 22 > gpurun_out/dbg3_c3sweep.log 2>&1
+tail -3 gpurun_out/t7.log

@@ -34,9 +34,12 @@ CONFIGS = {
     # C3: 53-qubit (6x9 minus a corner) 20-cycle, 6 open legs (BJ configs[2]).  Branch grouping over
     # up to 24 consecutive stem branches (MB-scale non-stem tensors), then as few sliced edges
     # as keep the largest stem at 2^32 ("~2^32 complex-half in double buffers")
-    "c3": dict(rows=6, cols=9, drop=True, cycles=20, n_open=6, max_log2=35, trials=0, max_group=24, stem_log2=32),
+    # fSim angles jittered per coupler (reading C-A2, revised): at theta = pi/2 exactly fSim is a phased
+    # SWAP whose zero pattern makes most slices of a heavily sliced 53-qubit network structurally zero
+    "c3": dict(rows=6, cols=9, drop=True, cycles=20, n_open=6, max_log2=35, trials=0, max_group=24, stem_log2=32,
+               jitter=0.2),
     # round-1 C3 plan (kept as the memory-bound variant): 12-branch groups, 188 sliced edges, stem 2^33
-    "c3_sweep": dict(rows=6, cols=9, drop=True, cycles=20, n_open=6, max_log2=35, trials=0),
+    "c3_sweep": dict(rows=6, cols=9, drop=True, cycles=20, n_open=6, max_log2=35, trials=0, jitter=0.2),
 }
 
 
@@ -68,8 +71,8 @@ def sweep_orders(circ, net):
 
 
 def build_plan(rows, cols, drop, cycles, n_open, max_log2, trials, seed=0, group=True,
-               max_branch_log2=20, max_group=12, stem_log2=None):
-    circ = C.make_circuit(rows, cols, cycles, seed=seed, drop_corner=drop)
+               max_branch_log2=20, max_group=12, stem_log2=None, jitter=0.0):
+    circ = C.make_circuit(rows, cols, cycles, seed=seed, drop_corner=drop, jitter=jitter)
     n = circ["n_qubits"]
     bits = C.random_bits(n, seed + 1000)
     oq = open_qubit_choice(n, n_open)
@@ -135,7 +138,7 @@ def main(argv):
         t0 = time.time()
         plan = build_plan(cfg["rows"], cfg["cols"], cfg["drop"], cfg["cycles"], cfg["n_open"],
                           cfg["max_log2"], cfg["trials"], max_group=cfg.get("max_group", 12),
-                          stem_log2=cfg.get("stem_log2"))
+                          stem_log2=cfg.get("stem_log2"), jitter=cfg.get("jitter", 0.0))
         p = write_plan(name, plan)
         m = plan["meta"]
         print(f"{name}: {p} tensors={m['n_tensors']} sliced={m['n_sliced']} "
