@@ -116,7 +116,13 @@ void launch_max_slots(float* dst, const MaxSlots& src, cudaStream_t s);
 void launch_redo_check(const uint32_t* out_max, const float* in_max, float* redo_in, int bits, cudaStream_t s);
 void launch_copy_c64(float2* dst, const float2* src, uint64_t n, cudaStream_t s);
 void launch_gemm_c64(float2* c, const float2* a, const float2* b, uint64_t M, uint32_t K, uint32_t N,
-                     const OutMap* om, cudaStream_t s);
+                     const OutMap* om, cudaStream_t s, const float* in_max = nullptr, const float* b_bound = nullptr,
+                     uint32_t* out_max = nullptr, int* exp_slot = nullptr);
+// complex64 operand B [K][N]: *b_bound = max over n of sum_k (|Re B| + |Im B|) (float bits, atomicMax)
+void launch_colnorm_c64(const float2* b, int klog, int nlog, float* b_bound, cudaStream_t s);
+// complex64 stem entry: dst = src * 2^e, e from *max_bits (as launch_c64_to_chalf); out max recorded
+void launch_c64_scale(float2* dst, const float2* src, uint64_t n, const uint32_t* max_bits, int* exp_slot,
+                      uint32_t* out_max_bits, cudaStream_t s);
 void launch_gemm_chalf_simt(__half2* c, const __half2* a, const __half* bp, uint64_t M, uint32_t K,
                             uint32_t N, const float* in_max, const float* b_bound,
                             uint32_t* out_max, int* exp_slot, const OutMap* om, cudaStream_t s);

@@ -180,6 +180,54 @@ void launch_c64_to_chalf(__half2* dst, const float2* src, uint64_t n, const uint
   TN_CUDA(cudaGetLastError());
 }
 
+// complex64 path (C-A8 for fp32): column bound of B and the scaled stem entry
+__global__ void colnorm_c64_kernel(const float2* __restrict__ b, int klog, int nlog, float* b_bound) {
+  const int K = 1 << klog, N = 1 << nlog;
+  const int warps = blockDim.x >> 5, lane = threadIdx.x & 31;
+  for (int n = blockIdx.x * warps + (threadIdx.x >> 5); n < N; n += gridDim.x * warps) {
+    float l1 = 0.f;
+    for (int k = lane; k < K; k += 32) {
+      const float2 v = b[(size_t)k * N + n];
+      l1 += fabsf(v.x) + fabsf(v.y);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) l1 += __shfl_xor_sync(0xffffffffu, l1, o);
+    if (lane == 0) atomic_max_pos(reinterpret_cast<uint32_t*>(b_bound), l1);
+  }
+}
+
+void launch_colnorm_c64(const float2* b, int klog, int nlog, float* b_bound, cudaStream_t s) {
+  const int N = 1 << nlog;
+  int blocks = (N + 7) / 8;
+  if (blocks > 148 * 4) blocks = 148 * 4;
+  colnorm_c64_kernel<<<blocks, 256, 0, s>>>(b, klog, nlog, b_bound);
+  TN_CUDA(cudaGetLastError());
+}
+
+__global__ void c64_scale_kernel(float2* __restrict__ dst, const float2* __restrict__ src, uint64_t n,
+                                 const uint32_t* max_bits, int* exp_slot, uint32_t* out_max) {
+  const int e = max_bits ? scale_exp_for(__uint_as_float(*max_bits)) : 0;
+  if (exp_slot && blockIdx.x == 0 && threadIdx.x == 0) *exp_slot = e;
+  const float sc = ldexpf(1.f, e);
+  float m = 0.f;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const float2 v = make_float2(src[i].x * sc, src[i].y * sc);
+    dst[i] = v;
+    m = fmaxf(m, fmaxf(fabsf(v.x), fabsf(v.y)));
+  }
+  m = warp_max(m);
+  if (out_max && (threadIdx.x & 31) == 0) atomic_max_pos(out_max, m);
+}
+
+void launch_c64_scale(float2* dst, const float2* src, uint64_t n, const uint32_t* max_bits, int* exp_slot,
+                      uint32_t* out_max_bits, cudaStream_t s) {
+  uint64_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  if (blocks == 0) blocks = 1;
+  c64_scale_kernel<<<(unsigned)blocks, 256, 0, s>>>(dst, src, n, max_bits, exp_slot, out_max_bits);
+  TN_CUDA(cudaGetLastError());
+}
+
 __global__ void set_u64_kernel(uint64_t* p, uint64_t v) { *p = v; }
 
 void launch_set_u64(uint64_t* p, uint64_t v, cudaStream_t s) {

@@ -15,7 +15,15 @@ constexpr int TM = 64, TN_ = 64, TK = 8;
 
 __global__ void __launch_bounds__(256) gemm_c64_kernel(float2* __restrict__ C, const float2* __restrict__ A,
                                                        const float2* __restrict__ B, uint64_t M, int K, int N,
-                                                       const OutMap om, uint64_t m_base) {
+                                                       const OutMap om, uint64_t m_base, const float* in_max,
+                                                       const float* b_bound, uint32_t* out_max, int* exp_slot) {
+  // power-of-two output scale (reading C-A8, also for complex64: one-slice partial amplitudes of a
+  // 53-qubit network fall below fp32's normal range, 1e-38, long before the root)
+  int e = 0;
+  if (in_max && b_bound) e = scale_exp_for(in_max[0] * b_bound[0]);
+  if (exp_slot && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0 && m_base == 0) *exp_slot = e;
+  const float sc = ldexpf(1.f, e);
+  float mx = 0.f;
   __shared__ float2 As[TK][TM + 1];
   __shared__ float2 Bs[TK][TN_];
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
@@ -65,17 +73,25 @@ __global__ void __launch_bounds__(256) gemm_c64_kernel(float2* __restrict__ C, c
     for (int j = 0; j < 4; ++j) {
       int gn = n0 + tx + 16 * j;
       if (gn < N) {
+        const float2 v = make_float2(acc[i][j].x * sc, acc[i][j].y * sc);
+        mx = fmaxf(mx, fmaxf(fabsf(v.x), fabsf(v.y)));
         if (om.identity)
-          C[gm * N + gn] = acc[i][j];
+          C[gm * N + gn] = v;
         else
-          C[mo + outmap_n(om, gn)] = acc[i][j];
+          C[mo + outmap_n(om, gn)] = v;
       }
     }
+  }
+  if (out_max) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(out_max, __float_as_uint(mx));
   }
 }
 
 void launch_gemm_c64(float2* c, const float2* a, const float2* b, uint64_t M, uint32_t K, uint32_t N,
-                     const OutMap* om_in, cudaStream_t s) {
+                     const OutMap* om_in, cudaStream_t s, const float* in_max, const float* b_bound, uint32_t* out_max,
+                     int* exp_slot) {
   OutMap om = om_in ? *om_in : identity_map(M, N);
   uint64_t gy = (M + TM - 1) / TM;
   if (gy > 65535ull * 1024) throw TnError{TN_E_UNSUPPORTED, "gemm_c64: M too large"};
@@ -87,7 +103,7 @@ void launch_gemm_c64(float2* c, const float2* a, const float2* b, uint64_t M, ui
     grid.y = (unsigned)ny;
     uint64_t moff = y0 * TM;
     gemm_c64_kernel<<<grid, 256, 0, s>>>(om.identity ? c + moff * N : c, a + moff * K, b, M - moff, (int)K, (int)N, om,
-                                         moff);
+                                         moff, in_max, b_bound, out_max, exp_slot);
   }
   TN_CUDA(cudaGetLastError());
 }

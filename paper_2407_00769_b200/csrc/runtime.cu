@@ -379,10 +379,13 @@ void prepare_b_sparse(const Plan& p, const StemStep& st, size_t i, unsigned char
   }
   if (p.cfg.dtype != TN_CHALF) {
     // complex64 path: the blocks are consumed as [K][N] complex64 at b_off + bv * b_blk
-    for (uint64_t bv = 0; bv < nb; ++bv)
+    for (uint64_t bv = 0; bv < nb; ++bv) {
       if (st.b_off + bv * st.b_blk != st.b_tmp_off + bv * tmp_blk)
         TN_CUDA(cudaMemcpyAsync(W + st.b_off + bv * st.b_blk, W + st.b_tmp_off + bv * tmp_blk, 8 * kn,
                                 cudaMemcpyDeviceToDevice, s));
+      launch_colnorm_c64(reinterpret_cast<const float2*>(W + st.b_tmp_off + bv * tmp_blk), st.klog, st.nlog,
+                         &sc.b_bound[i], s);
+    }
     return;
   }
   for (uint64_t bv = 0; bv < nb; ++bv) {
@@ -412,6 +415,10 @@ void prepare_b(const Plan& p, unsigned char* W, const Scratch& sc, cudaStream_t 
     for (int j = 0; j < st.klog; ++j) g.sk[j] = v.stride_of(st.R[st.klog - 1 - j]);
     for (int j = 0; j < st.nlog; ++j) g.sn[j] = v.stride_of(st.newl[st.nlog - 1 - j]);
     launch_gather_kn(g, s);
+    if (p.cfg.dtype != TN_CHALF) {
+      launch_colnorm_c64(g.dst, st.klog, st.nlog, &sc.b_bound[i], s);
+      const_cast<Plan&>(p).launches++;
+    }
     if (p.cfg.dtype == TN_CHALF) {
       const_cast<Plan&>(p).launches += 2;
       uint64_t kn = 1ull << (st.klog + st.nlog);
@@ -598,7 +605,8 @@ void run_gemm_once(Plan& p, const StemStep& st, size_t i, const void* src, void*
                              exp_slot, &om, s);
   } else {
     launch_gemm_c64(reinterpret_cast<float2*>(dst), reinterpret_cast<const float2*>(src),
-                    reinterpret_cast<const float2*>(W + st.b_off), M, K, N, &om, s);
+                    reinterpret_cast<const float2*>(W + st.b_off), M, K, N, &om, s, in_max, &sc.b_bound[i], out_max,
+                    exp_slot);
   }
   ++p.launches;
 }
@@ -654,7 +662,9 @@ void stem_body(Plan& p, const tn_buffers* b, cudaStream_t s, bool head = true, b
       launch_c64_to_chalf(reinterpret_cast<__half2*>(b->d_stem[0]), src + (uint64_t)p.rank * n_local, n_local,
                           sc.entry_max, &sc.exps[0], reinterpret_cast<uint32_t*>(&sc.max_slot[0]), s);
     } else {
-      launch_copy_c64(reinterpret_cast<float2*>(b->d_stem[0]), src + (uint64_t)p.rank * n_local, n_local, s);
+      launch_max_abs_f32(reinterpret_cast<const float*>(src), 2 * n, sc.entry_max, s);
+      launch_c64_scale(reinterpret_cast<float2*>(b->d_stem[0]), src + (uint64_t)p.rank * n_local, n_local,
+                       sc.entry_max, &sc.exps[0], reinterpret_cast<uint32_t*>(&sc.max_slot[0]), s);
     }
   }
   }
@@ -1085,7 +1095,8 @@ void sparse_tail(Plan& p, const tn_buffers* b, const uint64_t* prefixes, size_t 
                                      exp_slot, &om, s);
           } else {
             launch_gemm_c64(reinterpret_cast<float2*>(cc), reinterpret_cast<const float2*>(a),
-                            reinterpret_cast<const float2*>(bb), M, K, N, &om, s);
+                            reinterpret_cast<const float2*>(bb), M, K, N, &om, s, in_max, &sc.b_bound[i], out_max,
+                            exp_slot);
           }
           ++p.launches;
         }
