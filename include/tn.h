@@ -215,9 +215,11 @@ TN_API int tn_permute(void* d_dst, const void* d_src, int elem_bytes, int n, con
  * d_bp: padded real B_P, fp16 [2N][2K] row-major (K-major): row (n,c), column (k,a) holds
  * c=0: (Re b, -Im b)[a], c=1: (Im b, Re b)[a] (reading C-A6).  The scale 2^e is chosen on the
  * device from *d_in_max (max |real component| of A) and *d_b_bound (max column 1-norm of B_P)
- * so that |C| <= 2^14; e is added to *d_exp.  *d_out_max receives max |real component| of C as
- * float bits (atomicMax; caller zeroes it).  Any of the four scale pointers may be NULL: then
- * e = 0 and no max is recorded.  K, N powers of two, M any.  K >= 4 runs on tcgen05 (for N < 8,
+ * so that |C| <= 2^14; e is written to *d_exp.  *d_out_max receives max |real component| of the
+ * scaled fp32 results before their fp16 rounding, as float bits (atomicMax; caller zeroes it; it
+ * stays meaningful when cancellation makes the stored fp16 values underflow).  A negative *d_in_max
+ * makes the launch return at once (the library's scale re-run uses that as "not needed").  Any of
+ * the four scale pointers may be NULL: then e = 0 and no max is recorded.  K, N powers of two, M any.  K >= 4 runs on tcgen05 (for N < 8,
  * d_bp must hold 16 rows with rows 2N..15 zero); K < 4 runs on the SIMT kernel. */
 TN_API int tn_gemm_chalf(void* d_c, const void* d_a, const void* d_bp, uint64_t M, uint32_t K, uint32_t N,
                   const float* d_in_max, const float* d_b_bound, uint32_t* d_out_max, int* d_exp,

@@ -565,13 +565,19 @@ void run_gemm_once(Plan& p, const StemStep& st, size_t i, const void* src, void*
 
 // One stem GEMM plus its scale re-run (complex-half: redo_check + the same launch, which exits at once
 // unless the realised output max lost more than TN_REDO_BITS (default 10) bits of fp16 headroom).
+// collective (sharded main path): every rank must scale by the same power of two, so the realised max is
+// all-reduced before the re-run decision and again after it (per-rank split-tail chains pass false).
 void run_gemm(Plan& p, const StemStep& st, size_t i, const void* src, void* dst, int mshift, const float* in_max,
-              uint32_t* out_max, int* exp_slot, unsigned char* W, const Scratch& sc, cudaStream_t s) {
+              uint32_t* out_max, int* exp_slot, unsigned char* W, const Scratch& sc, cudaStream_t s,
+              bool collective = false) {
   run_gemm_once(p, st, i, src, dst, mshift, in_max, out_max, exp_slot, W, sc, s);
+  const bool coll = collective && p.world > 1 && p.cfg.dtype == TN_CHALF;
+  if (coll) xfer_allreduce_max(p, reinterpret_cast<float*>(out_max), s);
   if (p.cfg.dtype != TN_CHALF || !in_max || redo_bits() <= 0) return;
   launch_redo_check(out_max, in_max, &sc.redo_in[i], redo_bits(), s);
   run_gemm_once(p, st, i, src, dst, mshift, &sc.redo_in[i], out_max, exp_slot, W, sc, s);
   ++p.launches;
+  if (coll) xfer_allreduce_max(p, reinterpret_cast<float*>(out_max), s);
 }
 
 void run_gemm_once(Plan& p, const StemStep& st, size_t i, const void* src, void* dst, int mshift, const float* in_max,
@@ -686,10 +692,9 @@ void stem_body(Plan& p, const tn_buffers* b, cudaStream_t s, bool head = true, b
       cur = 1 - cur;
     }
     rec_event(p, 2 + 2 * i, s);
+    // (sharded: the max all-reduces inside make every rank scale the next step identically)
     run_gemm(p, st, i, b->d_stem[cur], b->d_stem[1 - cur], 0, &sc.max_slot[i],
-             reinterpret_cast<uint32_t*>(&sc.max_slot[i + 1]), &sc.exps[2 + 2 * i], W, sc, s);
-    // every rank must scale the next step by the same power of two
-    if (p.world > 1 && p.cfg.dtype == TN_CHALF) xfer_allreduce_max(p, &sc.max_slot[i + 1], s);
+             reinterpret_cast<uint32_t*>(&sc.max_slot[i + 1]), &sc.exps[2 + 2 * i], W, sc, s, true);
     cur = 1 - cur;
     rec_event(p, 3 + 2 * i, s);
   }

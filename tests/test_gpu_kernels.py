@@ -203,8 +203,10 @@ def test_pad_b_and_scaled_gemm(env):
     got = C.cpu().numpy().astype(np.float64).reshape(M, 2 * N)
     assert np.abs(got).max() <= 2 ** 14
     assert np.all(np.abs(got - ref) <= 2.0 ** -10 * np.abs(ref) + 1e-3 * np.sqrt(np.mean(ref ** 2)))
+    # out_max: max of the scaled fp32 values before the fp16 rounding (so it stays meaningful when the
+    # stored values underflow, reading C-A28): within half an fp16 ulp of the stored max
     mx = np.frombuffer(np.int32(out_max.item()).tobytes(), dtype=np.float32)[0]
-    assert mx == np.abs(got).max()
+    assert abs(mx - np.abs(got).max()) <= 2.0 ** -11 * np.abs(got).max()
 
 
 @pytest.mark.parametrize("M,K,N", [(1, 1, 1), (100, 3, 5), (1000, 64, 64), (4097, 128, 33)])

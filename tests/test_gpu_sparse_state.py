@@ -114,3 +114,23 @@ def test_sparse_tail_chunked_by_capacity(tn):
     ref = oracle_blocks(plan, contract.contract(load(plan), 0))
     for i in range(32):
         assert metrics.rel_l2(a_all[i], ref[i]) <= 2e-2
+
+
+def test_c5_sparse_state_subslice_vs_oracle(tn):
+    """C5 (BJ configs[4]): 53-qubit 20-cycle network, 10 member legs, 12 sparse legs entering the stem
+    in its final stage; sub-sliced so the oracle's dense root (2^22 amplitudes) is cheap; 64 seeded
+    prefixes.  Complex-half amplitudes per subspace vs the oracle, valid post-selected members."""
+    with open(os.path.join(ROOT, "plans", "c5.json")) as f:
+        c5 = json.load(f)
+    sub = MP.sub_slice(c5, 24)
+    assert sub["sparse_legs"] == c5["sparse_legs"]
+    ref = oracle_blocks(sub, contract.contract(load(sub), 0))
+    rng = np.random.default_rng(5)
+    pre = rng.choice(2 ** 12, size=64, replace=False).astype(np.uint64)
+    amps, top, p = run(tn, sub, 0, 16, pre)
+    assert p.info()["n_sparse_legs"] == 12
+    errs = [metrics.rel_l2(amps[i], ref[v]) for i, v in enumerate(pre)]
+    assert max(errs) <= 2e-2, max(errs)
+    for i, v in enumerate(pre):
+        pr = np.abs(ref[v]) ** 2
+        assert pr[int(top[i, 0])] >= (1 - 4e-2) * pr.max()

@@ -40,7 +40,37 @@ CONFIGS = {
                jitter=0.2),
     # round-1 C3 plan (kept as the memory-bound variant): 12-branch groups, 188 sliced edges, stem 2^33
     "c3_sweep": dict(rows=6, cols=9, drop=True, cycles=20, n_open=6, max_log2=35, trials=0, jitter=0.2),
+    # C5 (BJ configs[4]): the C3 circuit with 22 output legs open: the 12 that enter the stem last are
+    # the sparse-state legs (a correlated subspace = one value of them, "sparse state occurs in
+    # the final stage"), the other 10 the members of each subspace (q_open = 10)
+    "c5": dict(rows=6, cols=9, drop=True, cycles=20, n_open=22, max_log2=35, trials=0, max_group=24, stem_log2=32,
+               jitter=0.2, sparse=12),
 }
+
+
+def choose_sparse_legs(plan, n_sparse):
+    """The n_sparse open legs whose first appearance along the stem (in a stem branch) is latest;
+    legs already in the first stem tensors are never chosen (they would have to be batch modes of
+    the whole stem)."""
+    masks = []
+    for t in plan["tensors"]:
+        m = 0
+        for l in t["labels"]:
+            m |= 1 << l
+        masks.append(m)
+    tree = PL.Tree(masks, [tuple(p) for p in plan["tree"]])
+    stem = plan["stem"]
+    first = {}
+    for s, (a, b) in enumerate(zip(stem[:-1], stem[1:])):
+        u, v = tree.children[b]
+        br = v if u == a else u
+        for l in PL.bits_of(tree.masks[br]):
+            first.setdefault(l, s + 1)
+    cand = [l for l in plan["open"] if l in first]
+    cand.sort(key=lambda l: -first[l])
+    if len(cand) < n_sparse:
+        raise RuntimeError("not enough late-entering open legs for the sparse state")
+    return sorted(cand[:n_sparse], key=plan["open"].index)
 
 
 def open_qubit_choice(n, n_open):
@@ -139,6 +169,8 @@ def main(argv):
         plan = build_plan(cfg["rows"], cfg["cols"], cfg["drop"], cfg["cycles"], cfg["n_open"],
                           cfg["max_log2"], cfg["trials"], max_group=cfg.get("max_group", 12),
                           stem_log2=cfg.get("stem_log2"), jitter=cfg.get("jitter", 0.0))
+        if cfg.get("sparse"):
+            plan["sparse_legs"] = choose_sparse_legs(plan, cfg["sparse"])
         p = write_plan(name, plan)
         m = plan["meta"]
         print(f"{name}: {p} tensors={m['n_tensors']} sliced={m['n_sliced']} "
