@@ -87,7 +87,8 @@ typedef struct {
                                 1: scatter when its stores are >= 64 B contiguous, else as 0 */
   int32_t quant_from_pct;    /* int8/int4 swaps only at stem steps >= this percentage of the path
                                 ("quantify in the later stages"); earlier swaps send
-                                fp16.  Negative: 50 */
+                                fp16.  Negative: 65 (the sub-sliced C3 at 8 ranks keeps the
+                                north_star 5e-2 bound with int8 swaps from 65 %, not from 50 %) */
   int32_t virtual_world;     /* > 1 with comm == NULL: lower the plan for that many ranks
                                 (host-only inspection of the shard/swap schedule) */
   int32_t no_gather;         /* 0 (default): a permutation before a tensor-core step whose two

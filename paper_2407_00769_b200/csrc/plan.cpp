@@ -453,7 +453,7 @@ static Plan* load_plan_fixed(const char* json, size_t len, const tn_config* cfg_
           st.swap = true;
           // quantise only in the later stages of the path (earlier errors accumulate), C-A26
           {
-            const int pct = cfg.quant_from_pct < 0 ? 50 : cfg.quant_from_pct;
+            const int pct = cfg.quant_from_pct < 0 ? 65 : cfg.quant_from_pct;
             st.quant = cfg.dtype == TN_CHALF &&
                        (cfg.comm_codec == TN_COMM_INT8 || cfg.comm_codec == TN_COMM_INT4 ||
                         cfg.comm_codec == TN_COMM_INT8_TENSOR) &&
@@ -866,7 +866,7 @@ std::string report_json(const Plan& p, const std::vector<float>& ms) {
   jlist(o, p.split_modes);
   o << ",\"split_from\":" << p.split_from << ",\"recompute_from\":" << p.recompute_from
     << ",\"sparse_from\":" << p.sparse_from
-    << ",\"sparse_chunks\":" << p.sparse_chunks << ",\"sparse_legs\":";
+    << ",\"sparse_chunks\":" << p.sparse_chunks << ",\"sparse_flops\":" << p.sparse_flops << ",\"sparse_legs\":";
   jlist(o, p.sparse_legs);
   o << ",\"shard0\":";
   jlist(o, p.shard0);

@@ -87,6 +87,7 @@ struct Plan {
   int sparse_from = -1;           // first sparse-tail step (-1: none)
   int recompute_from = -1;        // recomputation on halves: the step producing the largest tensor
   uint64_t sparse_chunks = 0;     // subspace chunks of the last sparse-tail run
+  double sparse_flops = 0;        // 8 x complex MACs of the last sparse-tail run (every chunk)
   int split_log2 = 0;             // chunks = 2^split_log2
   std::vector<int> split_modes;   // open legs fixed per chunk (outermost in every tail layout)
   uint64_t split_chunk_max = 0;   // largest per-chunk stem tensor of the tail (elements)

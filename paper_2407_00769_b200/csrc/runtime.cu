@@ -571,7 +571,7 @@ void run_gemm(Plan& p, const StemStep& st, size_t i, const void* src, void* dst,
               uint32_t* out_max, int* exp_slot, unsigned char* W, const Scratch& sc, cudaStream_t s,
               bool collective = false) {
   run_gemm_once(p, st, i, src, dst, mshift, in_max, out_max, exp_slot, W, sc, s);
-  const bool coll = collective && p.world > 1 && p.cfg.dtype == TN_CHALF;
+  const bool coll = collective && p.world > 1;  // both dtypes scale by powers of two (C-A8)
   if (coll) xfer_allreduce_max(p, reinterpret_cast<float*>(out_max), s);
   if (p.cfg.dtype != TN_CHALF || !in_max || redo_bits() <= 0) return;
   launch_redo_check(out_max, in_max, &sc.redo_in[i], redo_bits(), s);
@@ -676,7 +676,7 @@ void stem_body(Plan& p, const tn_buffers* b, cudaStream_t s, bool head = true, b
   }
   if (!tail) return;
   // every rank scales the first step by the same power of two
-  if (p.world > 1 && p.cfg.dtype == TN_CHALF) xfer_allreduce_max(p, &sc.max_slot[0], s);
+  if (p.world > 1) xfer_allreduce_max(p, &sc.max_slot[0], s);
   int cur = 0;
   rec_event(p, 1, s);
   const size_t n_main = !p.split_modes.empty() ? (size_t)p.split_from
@@ -1004,6 +1004,7 @@ void sparse_tail(Plan& p, const tn_buffers* b, const uint64_t* prefixes, size_t 
     if (c >= uniq.size()) throw TnError{TN_E_CAPACITY, "sparse tail: one subspace does not fit the free stem buffer"};
   }
   p.sparse_chunks = 1ull << jc;
+  p.sparse_flops = 0;
   // members: the open legs without the sparse legs, `open` order; stored in the final dense layout
   std::vector<int> mord;
   for (int l : p.open)
@@ -1061,6 +1062,7 @@ void sparse_tail(Plan& p, const tn_buffers* b, const uint64_t* prefixes, size_t 
       }
       const uint64_t M = 1ull << st.mlog;
       const uint32_t K = 1u << st.klog, N = 1u << st.nlog;
+      p.sparse_flops += 8.0 * (double)n_out * (double)M * K * N;
       const float* in_max = &sc.max_slot[i];
       uint32_t* out_max = reinterpret_cast<uint32_t*>(&sc.max_slot[i + 1]);
       int* exp_slot = &sc.exps[2 + 2 * i];
