@@ -37,6 +37,8 @@ WORKLOADS = {
     "c3_sweep": "C3 (round-1 plan, memory-bound variant): same network, 188 sliced edges, 12-branch groups, "
                 "largest stem 2^33 complex-half, stem buffers 2 x 32 GiB",
     "c2": "C2: 30-qubit (5x6) 14-cycle RQC, one sliced subtask, 10 open legs",
+    "c5": "C5: the C3 network with 22 output legs open: sparse-state batch of 1024 seeded correlated subspaces "
+          "(values of the 12 legs entering the stem last) x 1024 members, top-1 post-selection per subspace",
 }
 
 
@@ -168,6 +170,98 @@ def parity(tn, sub, cfg_kw):
                       f"({len(sub['sliced'])} sliced edges), complex-half GPU path vs oracle complex128"}
 
 
+def bench_sparse(args, plan_json, tn, torch, dist, world, rank, local):
+    """C5 (BJ configs[4]): one subtask = the dense stem + the sparse-state tail for S seeded correlated
+    subspaces (values of the plan's sparse legs) + top-1 post-selection on the device.
+    Replicas over GPUs: rank r runs slice r (weak scaling).  Reported beside the metric:
+    the linear XEB of the S post-selected samples of THIS slice (a partial sum, reading C-A25: context,
+    not a fidelity estimate) and the parity of the same path on the oracle's sub-slice."""
+    import numpy as np
+    from paper_2407_00769_b200 import postselect
+    dev_stream = torch.cuda.current_stream()
+    L = len(plan_json["sparse_legs"])
+    rng = np.random.default_rng(args.seed)
+    pre = np.sort(rng.choice(2 ** L, size=min(args.subspaces, 2 ** L), replace=False)).astype(np.uint64)
+    p = tn.Plan(plan_json, tn.make_config(dtype=tn.TN_CHALF, stem_min_log2=20))
+    info = p.info()
+    free = torch.cuda.mem_get_info()[0]
+    stem_bytes = max(info["stem_bytes"], int(min(free * 0.42, 80 << 30)) // 4096 * 4096)
+    bufs = tn.Buffers(p, stem_bytes=stem_bytes)
+    n_sl = min(info["n_slices_log2"], 63)
+    slice_id = rank % (1 << n_sl) if n_sl else 0
+    tn.tn_plan_upload(p, bufs)
+
+    def step():
+        tn.tn_stem_contract(p, bufs, slice_id)
+        return tn.tn_sample_sparse(p, bufs, pre, k=1)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    clk = Clocks(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(dev_stream)
+    for _ in range(args.steps):
+        amps, top = step()
+    e1.record(dev_stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = clk.stop()
+    t_ms = e0.elapsed_time(e1) / args.steps
+    rep = p.report()
+    flops_rank = info["stem_flops"] + rep["sparse_flops"]
+    if world > 1:
+        tt = torch.tensor([t_ms], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_ms = float(tt.item())
+    value = flops_rank * world / (t_ms * 1e-3) / 1e12
+    chosen = np.abs(amps[np.arange(len(pre)), top[:, 0].astype(np.int64)]) ** 2
+    n_qubits = plan_json["circuit"]["n_qubits"]
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "TFLOPS", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": t_ms, "higher_is_better": True,
+                "scaling": "weak" if world > 1 else "strong", "vs_baseline": None, "dtype": "f16",
+                "data": "synthetic",
+                "config": {"workload": WORKLOADS.get(args.plan, args.plan), "plan": f"plans/{args.plan}.json",
+                           "slice": "rank r runs slice r (replicas over independent subtasks)",
+                           "subspaces": int(len(pre)), "members": int(amps.shape[1]), "sparse_legs": L,
+                           "sparse_from_step": rep["sparse_from"], "stem_steps": info["n_stem_steps"],
+                           "sparse_chunks": rep["sparse_chunks"], "stem_flops": info["stem_flops"],
+                           "sparse_tail_flops": rep["sparse_flops"], "stem_buffers_gib": 2 * stem_bytes / 2 ** 30,
+                           "l2": "tail tensors larger than L2"},
+                "tflops_per_gpu": value / world, "subtask_ms": t_ms,
+                "samples": {"n": int(len(pre)), "xeb_one_slice": postselect.linear_xeb(chosen, n_qubits),
+                            "note": "top-1 per subspace of ONE slice's partial amplitudes (C-A25): context only"},
+                "gpu_launches": p.info()["n_launches"] * args.steps, "clocks": clocks}
+        if world == 1 and not args.no_cpu:
+            try:
+                from oracle import contract, metrics
+                from oracle.plan import load
+                from workload import make_plans as MP
+                sub = MP.sub_slice(plan_json, args.oracle_log2)
+                ref = contract.contract(load(sub), 0)
+                sp = sub["sparse_legs"]
+                rest = [l for l in sub["open"] if l not in sp]
+                blocks = np.transpose(ref, [sub["open"].index(l) for l in sp + rest]).reshape(2 ** len(sp), -1)
+                q = tn.Plan(sub, tn.make_config(dtype=tn.TN_CHALF, stem_min_log2=min(20, args.oracle_log2 - 4)))
+                qb = tn.Buffers(q)
+                tn.tn_plan_upload(q, qb)
+                tn.tn_stem_contract(q, qb, 0)
+                few = pre[:64]
+                got, _ = tn.tn_sample_sparse(q, qb, few, k=1)
+                line["parity"] = {"rel_l2_vs_oracle": metrics.rel_l2(got, blocks[few.astype(np.int64)]), "bound": 2e-2,
+                                  "sample": f"64 subspaces of slice 0 of the plan sub-sliced to 2^{args.oracle_log2}"}
+            except Exception as e:
+                line["parity"] = {"error": str(e)}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -180,6 +274,8 @@ def main():
     ap.add_argument("--replicas", action="store_true", help="N>1: independent slices per GPU (weak scaling)")
     ap.add_argument("--comm", default="int8", choices=["int8", "int4", "fp16", "int8_tensor"])
     ap.add_argument("--policy", type=int, default=-1, help="layout policy (tn.h); -1: the plan's default")
+    ap.add_argument("--subspaces", type=int, default=1024, help="sparse-state plans: correlated subspaces")
+    ap.add_argument("--seed", type=int, default=0)
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -216,6 +312,8 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev_stream = torch.cuda.current_stream()
 
+    if plan_json.get("sparse_legs"):
+        return bench_sparse(args, plan_json, tn, torch, dist, world, rank, local)
     sharded = world > 1 and not args.replicas
     comm = tn.Comm(rank, world, local) if sharded else None
     codec = {"int8": tn.TN_COMM_INT8, "int4": tn.TN_COMM_INT4, "int8_tensor": tn.TN_COMM_INT8_TENSOR}.get(

@@ -229,9 +229,11 @@ TN_API int tn_gemm_chalf(void* d_c, const void* d_a, const void* d_bp, uint64_t 
 /* tn_gemm_chalf with a strided (gathered) A: A[m, k] is the complex-half element at
  * d_a + sum_j bit_j(m) m_stride[j] + sum_j bit_j(k) k_stride[j] (complex elements; j = 0 is the
  * lowest bit).  This is the stem permutation fused into the GEMM load ("dimension
- * reordering").  M = 2^mlog >= 128, K = 2^klog >= 8 with k_stride[0] = 1, k_stride[1] = 2 (every
- * 16-byte piece of a row contiguous), N a power of two; C row-major [M][N].  Scale pointers as
- * tn_gemm_chalf.  TN_E_INVALID otherwise. */
+ * reordering").  M = 2^mlog >= 128, K = 2^klog >= 8, N a power of two; C row-major [M][N].  Any
+ * strides: with k_stride[0] = 1, k_stride[1] = 2 the load moves 16-byte pieces (N-d TMA boxes or
+ * cp.async), otherwise 4-byte cp.async pieces (coalesced when the 5 smallest strides among m bits
+ * 0..6 and k bits 0..4 are 1, 2, 4, 8, 16).  Scale pointers as tn_gemm_chalf.  TN_E_INVALID
+ * otherwise. */
 TN_API int tn_gemm_chalf_gather(void* d_c, const void* d_a, const void* d_bp, int mlog, int klog, uint32_t N,
                                 const int64_t* m_stride, const int64_t* k_stride, const float* d_in_max,
                                 const float* d_b_bound, uint32_t* d_out_max, int* d_exp, void* stream);

@@ -197,7 +197,7 @@ struct Cfg {
   // the TMA-store staging (128B swizzle) must start 1024-aligned: pad the stage area
   static constexpr int kStageArea = (kStages * kStageBytes + 1023) / 1024 * 1024;
   static constexpr int kSmem =
-      kStageArea + kCBytes + kRawBytes + 1024 /*align*/ + 2048 /*barriers, gather table*/;
+      kStageArea + kCBytes + kRawBytes + 1024 /*align*/ + 4096 /*barriers, gather table (<= 192 x 16 B)*/;
   // TMEM accumulators: as many as fit in 512 columns (<= 16), so the MMA runs ahead of the
   // epilogue by several tiles when a tile is small (small K, small N)
   static constexpr int kAccStride = BN < 32 ? 32 : BN;
@@ -325,6 +325,9 @@ __device__ __forceinline__ void batch_tile(const BatchArgs& ba, uint32_t t, uint
 __device__ __forceinline__ void cp_async16(uint32_t smem_addr, const void* gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr), "l"(gmem) : "memory");
 }
+__device__ __forceinline__ void cp_async4(uint32_t smem_addr, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_addr), "l"(gmem) : "memory");
+}
 
 // Row / k parts of the N-d box coordinates: the TMA thread evaluates the row part once per tile
 // and the k part once per stage (a handful of shifts, so the single issuing thread keeps up).
@@ -342,14 +345,18 @@ __device__ __forceinline__ void nd_coords_k(const NdArgs& nda, uint32_t k, const
 // 3 = A by an N-d TMA box in source order into a raw slot, reshuffled by warp 3 (16-byte pieces)
 // into the interleaved layout
 template <int BN, int KB, int kAMode>
-__global__ void __launch_bounds__(kAMode == 1 ? kThreadsGather : kThreads, 1)
+__global__ void __launch_bounds__((kAMode == 1 || kAMode == 4) ? kThreadsGather : kThreads, 1)
     gemm_chalf_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                          const __grid_constant__ CUtensorMap tmC, uint32_t num_m, uint32_t num_n, int K2,
                          const float* in_max, const float* b_bound, uint32_t* out_max, int* exp_slot,
                          const __grid_constant__ ScatterArgs sc_args, uint32_t* out_scatter, uint64_t rows,
                          uint32_t n_cols, const __grid_constant__ AGatherArgs ga,
                          const __grid_constant__ NdArgs nda, int epi_stg, const __grid_constant__ BatchArgs ba) {
-  constexpr bool kGather = kAMode == 1;
+  // 1: cp.async gather of 16-byte pieces (4 consecutive complex k); 4: of 4-byte pieces (single
+  // complex elements, any layout: the stem permutation of a step whose contracted modes sit in the
+  // middle of the stored order, fused into the load)
+  constexpr bool kGather = kAMode == 1 || kAMode == 4;
+  constexpr bool kWord = kAMode == 4;
   constexpr bool kInter = kAMode == 2 || kAMode == 3;
   using C = Cfg<BN, KB, kAMode == 3 ? 1 : 0>;
   // a negative input max is the "no re-run needed" signal of the scale re-run (runtime.cu redo)
@@ -590,7 +597,8 @@ __global__ void __launch_bounds__(kAMode == 1 ? kThreadsGather : kThreads, 1)
     const int g = warp - 12;
     constexpr int kCB = KB / 8;                 // 16-byte chunks per row
     constexpr int kLogCB = kCB == 8 ? 3 : (kCB == 4 ? 2 : 1);
-    constexpr int kIters = BM * kCB / 32;       // pieces per lane per stage (32, 16 or 8)
+    constexpr int kPieces = kWord ? KB / 2 : kCB;  // pieces per row (complex elements or 16-byte chunks)
+    constexpr int kIters = BM * kPieces / 32;   // pieces per lane per stage
     // piece v = it * 32 + lane; vector bits 0..4 come from the lane, 5.. from it.  Offsets and
     // (row, chunk) of both parts are tile-independent: lane part in registers, it part in a
     // 32-entry smem table (one broadcast load per piece)
@@ -598,25 +606,23 @@ __global__ void __launch_bounds__(kAMode == 1 ? kThreadsGather : kThreads, 1)
     int r_lane = 0, c_lane = 0;
     int64_t off_it = 0;
     int r_it = 0, c_it = 0;
-    for (int b = 0; b < ga.nvb; ++b) {
-      const bool on = b < 5 ? ((lane >> b) & 1) : ((lane >> (b - 5)) & 1);
-      if (!on) continue;
-      const int64_t st = ga.vb_is_k[b] ? ga.ks[2 + ga.vb_idx[b]] : ga.ms[ga.vb_idx[b]];
-      const int rb = ga.vb_is_k[b] ? 0 : (1 << ga.vb_idx[b]);
-      const int cb = ga.vb_is_k[b] ? (1 << ga.vb_idx[b]) : 0;
-      if (b < 5) {
-        off_lane += st;
-        r_lane |= rb;
-        c_lane |= cb;
-      } else {
-        off_it += st;
-        r_it |= rb;
-        c_it |= cb;
-      }
+    for (int b = 0; b < 5 && b < ga.nvb; ++b) {
+      if (!((lane >> b) & 1)) continue;
+      off_lane += ga.vb_is_k[b] ? ga.ks[(kWord ? 0 : 2) + ga.vb_idx[b]] : ga.ms[ga.vb_idx[b]];
+      r_lane |= ga.vb_is_k[b] ? 0 : (1 << ga.vb_idx[b]);
+      c_lane |= ga.vb_is_k[b] ? (1 << ga.vb_idx[b]) : 0;
     }
-    if (lane < kIters) {
-      gtab[lane].off = off_it;
-      gtab[lane].rc = (r_it << 8) | c_it;
+    for (int it = lane; it < kIters; it += 32) {  // iteration part of the piece index (bits >= 5)
+      off_it = 0;
+      r_it = c_it = 0;
+      for (int b = 5; b < ga.nvb; ++b) {
+        if (!((it >> (b - 5)) & 1)) continue;
+        off_it += ga.vb_is_k[b] ? ga.ks[(kWord ? 0 : 2) + ga.vb_idx[b]] : ga.ms[ga.vb_idx[b]];
+        r_it |= ga.vb_is_k[b] ? 0 : (1 << ga.vb_idx[b]);
+        c_it |= ga.vb_is_k[b] ? (1 << ga.vb_idx[b]) : 0;
+      }
+      gtab[it].off = off_it;
+      gtab[it].rc = (r_it << 8) | c_it;
     }
     __syncwarp();
     const uint32_t sA_u32 = smem_u32(sA);
@@ -665,13 +671,16 @@ __global__ void __launch_bounds__(kAMode == 1 ? kThreadsGather : kThreads, 1)
         mbar_wait(&empty[s], ph ^ 1);
         const uint32_t stage = sA_u32 + s * C::kABytes;
         const uint32_t* src = ga.a + base;
-#pragma unroll
+#pragma unroll 8
         for (int it = 0; it < kIters; ++it) {
           const GTab e = gtab[it];
           const int r = r_lane | (e.rc >> 8), c = c_lane | (e.rc & 0xff);
           // swizzled K-major row (SW128 / SW64 / SW32 as the TMA box would have written it)
           const int sw = KB == 64 ? (r & 7) : (KB == 32 ? ((r >> 1) & 3) : ((r >> 2) & 1));
-          cp_async16(stage + r * (2 * KB) + ((c ^ sw) << 4), src + e.off);
+          if constexpr (kWord)
+            cp_async4(stage + r * (2 * KB) + ((((c >> 2) ^ sw)) << 4) + ((c & 3) << 2), src + e.off);
+          else
+            cp_async16(stage + r * (2 * KB) + ((c ^ sw) << 4), src + e.off);
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
         pend |= (uint32_t)s << (8 * npend);
@@ -957,9 +966,9 @@ static void launch_bn(__half* c, const __half* a, const __half* bp, uint64_t M, 
   NdArgs nda;
   memset(&nda, 0, sizeof(nda));
   if (np) nda = np->args;
-  if (G == 1) {
-    // vector bits of a stage: 7 row bits + log2(KB/8) chunk bits, by source stride (lanes take the
-    // 5 smallest: the most contiguous reads)
+  if (G == 1 || G == 4) {
+    // vector bits of a stage: 7 row bits + log2(KB/8) chunk bits (G = 4: log2(KB/2) complex k bits),
+    // by source stride (lanes take the 5 smallest: the most contiguous reads)
     gargs.a = reinterpret_cast<const uint32_t*>(a);
     static const bool fence_env = getenv("TN_GATHER_FENCE") != nullptr;
     gargs.fence = fence_env ? 1 : 0;
@@ -973,8 +982,8 @@ static void launch_bn(__half* c, const __half* a, const __half* bp, uint64_t M, 
     };
     std::vector<VB> vb;
     for (int j = 0; j < 7; ++j) vb.push_back({ag->ms[j], 0, j});
-    const int cb = KB == 64 ? 3 : (KB == 32 ? 2 : 1);
-    for (int j = 0; j < cb; ++j) vb.push_back({ag->ks[2 + j], 1, j});
+    const int cb = G == 4 ? (KB == 64 ? 5 : (KB == 32 ? 4 : 3)) : (KB == 64 ? 3 : (KB == 32 ? 2 : 1));
+    for (int j = 0; j < cb; ++j) vb.push_back({ag->ks[(G == 4 ? 0 : 2) + j], 1, j});
     std::stable_sort(vb.begin(), vb.end(), [](const VB& x, const VB& y) { return x.stride < y.stride; });
     gargs.nvb = (int)vb.size();
     for (int b = 0; b < gargs.nvb; ++b) {
@@ -1087,7 +1096,7 @@ static void launch_bn(__half* c, const __half* a, const __half* bp, uint64_t M, 
     uint64_t tiles = (uint64_t)num_m * num_n;
     int grid = (int)std::min<uint64_t>(tiles, (uint64_t)num_sms());
     // the exponent is recorded once (first chunk); later chunks reuse the same inputs
-    tc::gemm_chalf_tc_kernel<BN, KB, G><<<grid, G == 1 ? tc::kThreadsGather : tc::kThreads, C::kSmem, s>>>(
+    tc::gemm_chalf_tc_kernel<BN, KB, G><<<grid, (G == 1 || G == 4) ? tc::kThreadsGather : tc::kThreads, C::kSmem, s>>>(
         ma, mb, mc, num_m, num_n, (int)K2, in_max, b_bound, out_max, m_off ? nullptr : exp_slot, sa, out_sc, mm,
         n_cols, gargs, nda, epi_stg, BatchArgs{});
     TN_CUDA(cudaGetLastError());

@@ -19,6 +19,9 @@ extern template void launch_kb<2>(int, __half*, const __half*, const __half*, ui
 extern template void launch_kb<3>(int, __half*, const __half*, const __half*, uint64_t, uint32_t, uint32_t,
                                   const float*, const float*, uint32_t*, int*, const OutMap*, cudaStream_t,
                                   const AGather*, const NdPlan*, const BatchSpec*);
+extern template void launch_kb<4>(int, __half*, const __half*, const __half*, uint64_t, uint32_t, uint32_t,
+                                  const float*, const float*, uint32_t*, int*, const OutMap*, cudaStream_t,
+                                  const AGather*, const NdPlan*, const BatchSpec*);
 
 static bool build_nd(const AGather& ag, NdPlan& out) {
   int pm[kMaxModes], pk[24];
@@ -290,11 +293,15 @@ void launch_gemm_chalf_tc(__half* c, const __half* a, const __half* bp, uint64_t
   if (M == 0) return;
   const int kb_plain = K2 >= 64 ? 64 : (K2 >= 32 ? 32 : 16);
   if (ag) {
-    // the gathered load needs whole 128-row tiles, 16-byte pieces (k bits 0, 1 contiguous) and
-    // K-boxes of at least 16 fp16
-    if (M % tc::BM || K2 < 16 || ag->ks[0] != 1 || ag->ks[1] != 2 || (uint64_t)1 << ag->mlog != M ||
-        (2u << ag->klog) != K2)
+    // the gathered load needs whole 128-row tiles and K-boxes of at least 16 fp16
+    if (M % tc::BM || K2 < 16 || (uint64_t)1 << ag->mlog != M || (2u << ag->klog) != K2)
       throw TnError{TN_E_INVALID, "gathered-A GEMM: unsupported operand geometry"};
+    static const int force_word = getenv("TN_GATHER_WORD") ? atoi(getenv("TN_GATHER_WORD")) : 0;  // test knob
+    if (ag->ks[0] != 1 || ag->ks[1] != 2 || force_word) {
+      // contracted modes not innermost (the middle of the stored order): 4-byte cp.async pieces
+      launch_kb<4>(kb_plain, c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, ag, nullptr, nullptr);
+      return;
+    }
     // A/B knobs: TN_GATHER_MODE = 1 (cp.async), 2 (direct N-d box), 3 (raw box + reshuffle)
     static const int force = getenv("TN_GATHER_MODE") ? atoi(getenv("TN_GATHER_MODE")) : 0;
     NdPlan np, rp;

@@ -525,8 +525,20 @@ static Plan* load_plan_fixed(const char* json, size_t len, const tn_config* cfg_
         const bool rows_k = kl <= 4 && nl <= 5 && kl + nl <= 7;
         const bool tc_k = cfg.dtype == TN_CHALF && kl >= 2 && !rows_k &&
                           ((kl >= 3 && nl >= 3) || kl >= 4 || kl + nl > 11);
+        // 16-byte pieces: the two innermost stored modes are contracted.  4-byte pieces (any layout,
+        // e.g. the contracted modes in the middle of the stored order): the warp's lanes still read
+        // 32 contiguous complex when the 5 innermost stored modes are tile bits (the 7 innermost kept
+        // modes = m bits 0..6, or the min(5, K bits) innermost contracted modes of a stage)
+        static const bool no_word = getenv("TN_NO_WORD_GATHER") != nullptr;
+        bool word_ok = !no_word && L.size() >= 5 && kept.size() >= 7;
+        if (word_ok) {
+          std::set<int> tile;
+          for (size_t q = kept.size() - 7; q < kept.size(); ++q) tile.insert(kept[q]);
+          for (int q = kl - std::min(5, kl); q < kl; ++q) tile.insert(R[q]);
+          for (size_t q = L.size() - 5; word_ok && q < L.size(); ++q) word_ok = tile.count(L[q]) > 0;
+        }
         const bool fusable = !cfg.no_gather && !st.sparse && tc_k && kl >= 3 && kept.size() >= 7 && L.size() >= 2 &&
-                             bs.count(L[L.size() - 1]) && bs.count(L[L.size() - 2]) &&
+                             ((bs.count(L[L.size() - 1]) && bs.count(L[L.size() - 2])) || word_ok) &&
                              (split_set.empty() || (int)s < p.split_from);
         if (!fusable) by_next_use(kept);
         std::vector<int> PL = kept;
@@ -701,7 +713,7 @@ static Plan* load_plan_fixed(const char* json, size_t len, const tn_config* cfg_
         const std::vector<int>& IL = st.in_layout;
         const int r = (int)IL.size();
         std::set<int> Rs(st.R.begin(), st.R.end());
-        if (r < 2 || !Rs.count(IL[r - 1]) || !Rs.count(IL[r - 2])) continue;
+        if (r < 5) continue;
         auto src_stride = [&](int l) {
           return (int64_t)1 << (r - 1 - (int)(std::find(IL.begin(), IL.end(), l) - IL.begin()));
         };
@@ -709,7 +721,17 @@ static Plan* load_plan_fixed(const char* json, size_t len, const tn_config* cfg_
         st.a_k_stride.resize(st.klog);
         for (int j = 0; j < st.mlog; ++j) st.a_m_stride[j] = src_stride(st.kept[st.mlog - 1 - j]);
         for (int j = 0; j < st.klog; ++j) st.a_k_stride[j] = src_stride(st.R[st.klog - 1 - j]);
-        if (st.a_k_stride[0] != 1 || st.a_k_stride[1] != 2) continue;
+        if (st.a_k_stride[0] != 1 || st.a_k_stride[1] != 2) {
+          // 4-byte pieces (k_gemm_tc.cu mode 4): fuse only when the lanes read 128 contiguous bytes
+          static const bool no_word = getenv("TN_NO_WORD_GATHER") != nullptr;
+          if (no_word) continue;
+          std::vector<int64_t> bits(st.a_m_stride.begin(), st.a_m_stride.begin() + 7);
+          for (int j = 0; j < std::min(5, st.klog); ++j) bits.push_back(st.a_k_stride[j]);
+          std::sort(bits.begin(), bits.end());
+          bool contig = true;
+          for (int j = 0; j < 5; ++j) contig = contig && bits[j] == ((int64_t)1 << j);
+          if (!contig) continue;
+        }
         st.gather_a = true;
         st.perm = false;
         st.perm_axes.clear();

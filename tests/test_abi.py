@@ -58,8 +58,13 @@ def test_plan_load_info_and_lowering_invariants(tnmod, c1_plan):
         out = st["out"]
         assert len(out) == st["m"] + st["n"]
         if st["ga"]:
-            # permutation fused into the GEMM load: the two innermost stored modes are contracted
-            assert not st["perm"] and st["tc"] and set(lay[-2:]) <= set(R) and st["m"] >= 7
+            # permutation fused into the GEMM load: 16-byte pieces (the two innermost stored modes are
+            # contracted) or 4-byte pieces whose lanes read 32 contiguous complex (the 5 innermost
+            # stored modes are tile bits: the 7 innermost kept or the innermost contracted modes)
+            kept = [l for l in lay if l not in R]
+            tile = set(kept[-7:]) | set(R[-min(5, len(R)):])
+            assert not st["perm"] and st["tc"] and st["m"] >= 7 and st["k"] >= 3
+            assert set(lay[-2:]) <= set(R) or set(lay[-5:]) <= tile
         elif not st["perm"]:
             assert lay[len(lay) - len(R):] == R           # R innermost: GEMM reads A as stored
         assert (set(lay) - set(R)) <= set(out)              # Eq. 4: kept modes remain
@@ -147,7 +152,8 @@ def test_split_tail_lowering(tnmod, j):
 @pytest.mark.parametrize("name", ["c2", "c3"])
 def test_fused_permutation_lowering(tnmod, name):
     """Gathered-A steps (the permutation folded into the GEMM load): only tensor-core steps with
-    M >= 128 and the two innermost stored modes contracted; their kept modes stay in stored order;
+    M >= 128 and either the two innermost stored modes contracted (16-byte pieces) or the 5 innermost
+    stored modes tile bits (4-byte pieces, coalesced); their kept modes stay in stored order;
     the output layout is kept ++ new exactly as after a permutation pass; fusing only removes
     passes (same GEMM geometry and flops)."""
     with open(os.path.join(ROOT, "plans", f"{name}.json")) as f:
@@ -164,8 +170,10 @@ def test_fused_permutation_lowering(tnmod, name):
             continue
         lay, R = s["in"], set(s["R"])
         assert s["tc"] and not s["perm"] and s["m"] >= 7 and s["k"] >= 3
-        assert lay[-1] in R and lay[-2] in R
         kept = [l for l in lay if l not in R]
+        Rl = [l for l in lay if l in R]
+        tile = set(kept[-7:]) | set(Rl[-min(5, len(Rl)):])
+        assert (lay[-1] in R and lay[-2] in R) or set(lay[-5:]) <= tile   # 16-byte or 4-byte pieces
         assert s["out"][:len(kept)] == kept              # kept modes in stored order, then new modes
 
 

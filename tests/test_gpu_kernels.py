@@ -308,10 +308,47 @@ def test_gemm_chalf_gathered_a_exact(env, mlog, klog, N, seed):
 def test_gemm_chalf_gathered_rejects_bad_geometry(env):
     torch, tn = env
     t = torch.zeros(1 << 12, dtype=torch.float16, device="cuda")
-    with pytest.raises(tn.TnError):   # k bit 1 not contiguous
-        tn.tn_gemm_chalf_gather(t, t, t, 7, 3, 8, [1 << j for j in range(3, 10)], [1, 4, 2])
     with pytest.raises(tn.TnError):   # M < 128
         tn.tn_gemm_chalf_gather(t, t, t, 6, 3, 8, [1 << j for j in range(3, 9)], [1, 2, 4])
+    with pytest.raises(tn.TnError):   # K < 8
+        tn.tn_gemm_chalf_gather(t, t, t, 7, 2, 8, [1 << j for j in range(2, 9)], [1, 2])
+
+
+@pytest.mark.parametrize("runs,N", [("m8k5m5", 32), ("m12k6m2", 64), ("m5k7m4", 16), ("m7k3m1k2m2", 128),
+                                    ("m6k9m3", 256), ("m9k4", 8), ("m2k3m5k2m4", 2), ("m10k8", 512)])
+def test_gemm_chalf_gathered_word_pieces_exact(env, runs, N):
+    """Contracted modes NOT innermost (the middle-of-the-order layouts the grouped C3 plan produces):
+    the fused permutation loads single complex elements (4-byte cp.async, mode 4).  Exact integer
+    parity with (transpose, then multiply) as above."""
+    import re
+    torch, tn = env
+    kpos, mpos, b = [], [], 0
+    for kind, cnt in re.findall(r"([km])(\d+)", runs):
+        for _ in range(int(cnt)):
+            (kpos if kind == "k" else mpos).append(b)
+            b += 1
+    mlog, klog, n = len(mpos), len(kpos), b
+    rng = np.random.default_rng(n * 17 + N)
+    ms = [1 << p for p in mpos]
+    ks = [1 << p for p in kpos]
+    x = rng.integers(-1, 2, 1 << n) + 1j * rng.integers(-1, 2, 1 << n)
+    mi = np.arange(1 << mlog)
+    ki = np.arange(1 << klog)
+    moff = sum(((mi >> j) & 1) * ms[j] for j in range(mlog))
+    koff = sum(((ki >> j) & 1) * ks[j] for j in range(klog))
+    a = x[moff[:, None] + koff[None, :]]
+    K = 1 << klog
+    bm = rng.integers(-1, 2, (K, N)) + 1j * rng.integers(-1, 2, (K, N))
+    bp = embed.pad_b(bm)
+    bp_km = np.zeros((max(2 * N, 16), 2 * K), np.float16)
+    bp_km[:2 * N] = np.transpose(bp, (2, 0, 1, 3)).reshape(2 * N, 2 * K)
+    X = torch.from_numpy(_half_pairs(x.reshape(1, -1)).reshape(-1)).cuda()
+    C = torch.full(((1 << mlog) * 2 * N,), float("nan"), dtype=torch.float16, device="cuda")
+    tn.tn_gemm_chalf_gather(C, X, torch.from_numpy(bp_km.reshape(-1)).cuda(), mlog, klog, N, ms, ks)
+    torch.cuda.synchronize()
+    got = C.cpu().numpy().astype(np.float64).reshape(1 << mlog, N, 2)
+    ref = a @ bm
+    assert np.array_equal(got[..., 0], ref.real) and np.array_equal(got[..., 1], ref.imag)
 
 
 @pytest.mark.parametrize("runs,N", [("k2m8k5m5", 32), ("k3m8k2m5", 16), ("k4m4k4m7", 64), ("k5m7k2m3", 8),

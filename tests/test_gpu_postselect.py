@@ -32,7 +32,7 @@ def test_all_slices_post_selection_xeb(tn):
     plan = MP.build_plan(3, 4, False, 14, 12, None, trials=2, seed=11)
     sub = MP.sub_slice(plan, plan["meta"]["max_log2"] - 2)
     n_sl = len(sub["sliced"])
-    assert 1 <= n_sl <= 6
+    assert 1 <= n_sl <= 12
     # the 6 open legs entering the stem last are the sparse legs: 64 subspaces x 64 members
     p0 = tn.Plan(sub, tn.make_config(stem_min_log2=6))
     rep = p0.report()
