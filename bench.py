@@ -42,9 +42,9 @@ WORKLOADS = {
 }
 
 
-# layout policy per plan (tn.h tn_config.layout_policy): the grouped C3 steps are mostly compute-bound,
-# so writing every output in the next step's order (scatter epilogue, no permutation passes) wins
-DEFAULT_POLICY = {"c3": 2}
+# layout policy per plan (tn.h tn_config.layout_policy): identity outputs + permutations fused into the
+# next GEMM's load win everywhere measured (the scatter epilogue, policy 2, was 2.5x slower on C3)
+DEFAULT_POLICY = {}
 
 
 def peaks():
