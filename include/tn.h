@@ -84,7 +84,10 @@ typedef struct {
                                 permutation pass when the next step's modes are not innermost;
                                 2: each GEMM writes its output with the next step's contracted
                                 modes innermost (scatter epilogue, no permutation passes);
-                                1: scatter when its stores are >= 64 B contiguous, else as 0 */
+                                1: scatter when its stores are >= 64 B contiguous, else as 0;
+                                3: as 0, but a GEMM writes C[n][m] (new modes outermost, a
+                                transposed store whose warps write 128 contiguous bytes) when that
+                                puts more of the next step's contracted modes innermost */
   int32_t quant_from_pct;    /* int8/int4 swaps only at stem steps >= this percentage of the path
                                 ("quantify in the later stages"); earlier swaps send
                                 fp16.  Negative: 65 (the sub-sliced C3 at 8 ranks keeps the

@@ -399,7 +399,7 @@ static Plan* load_plan_fixed(const char* json, size_t len, const tn_config* cfg_
       outer.insert(outer.end(), in.begin(), in.end());
       return outer;
     };
-    if ((policy == 0 || policy == 2) && !step_nodes.empty()) {
+    if ((policy == 0 || policy == 2 || policy == 3) && !step_nodes.empty()) {
       // the entry is a common node whose device layout we choose: R_1 innermost
       Node& e = p.nodes[p.stem_entry];
       e.labels = order_with_inner(e.labels, Rsets[0]);
@@ -529,7 +529,9 @@ static Plan* load_plan_fixed(const char* json, size_t len, const tn_config* cfg_
         // e.g. the contracted modes in the middle of the stored order): the warp's lanes still read
         // 32 contiguous complex when the 5 innermost stored modes are tile bits (the 7 innermost kept
         // modes = m bits 0..6, or the min(5, K bits) innermost contracted modes of a stage)
-        static const bool no_word = getenv("TN_NO_WORD_GATHER") != nullptr;
+        // 4-byte gather is opt-in: measured 2-4x slower than pass + TMA GEMM on the C3 steps (per-thread
+        // cp.async.4 requests cap it near 1.2 TB/s aggregate), kept for layouts nothing else can read
+        static const bool no_word = getenv("TN_WORD_GATHER") == nullptr;
         bool word_ok = !no_word && L.size() >= 5 && kept.size() >= 7;
         if (word_ok) {
           std::set<int> tile;
@@ -592,6 +594,23 @@ static Plan* load_plan_fixed(const char* json, size_t len, const tn_config* cfg_
         by_next_use(newl);
         out = kept;
         out.insert(out.end(), newl.begin(), newl.end());
+        if (policy == 3 && !st.sparse && s + 1 < step_nodes.size() &&
+            (split_set.empty() || (int)s + 1 < p.split_from)) {
+          // transposed store C[n][m] (new modes outermost, kept modes innermost in M order) when that
+          // puts more of the next step's contracted modes innermost: the next step then reads its
+          // operand as stored or through a 16-byte fused gather instead of a permutation pass.  The
+          // tcgen05 scatter epilogue writes it with each warp's 32 rows contiguous (128-byte stores).
+          const std::set<int>& Rn = Rsets[s + 1];
+          auto inner_hits = [&](const std::vector<int>& o) {
+            int h = 0;
+            for (auto it = o.rbegin(); it != o.rend() && Rn.count(*it); ++it) ++h;
+            return h;
+          };
+          std::vector<int> tr = newl;
+          tr.insert(tr.end(), kept.begin(), kept.end());
+          const int hid = inner_hits(out), htr = inner_hits(tr);
+          if (htr > hid && (htr == (int)Rn.size() || htr >= 2) && kept.size() >= 5) out = tr;
+        }
       }
       st.R = R;
       st.kept = kept;
@@ -723,7 +742,9 @@ static Plan* load_plan_fixed(const char* json, size_t len, const tn_config* cfg_
         for (int j = 0; j < st.klog; ++j) st.a_k_stride[j] = src_stride(st.R[st.klog - 1 - j]);
         if (st.a_k_stride[0] != 1 || st.a_k_stride[1] != 2) {
           // 4-byte pieces (k_gemm_tc.cu mode 4): fuse only when the lanes read 128 contiguous bytes
-          static const bool no_word = getenv("TN_NO_WORD_GATHER") != nullptr;
+          // 4-byte gather is opt-in: measured 2-4x slower than pass + TMA GEMM on the C3 steps (per-thread
+        // cp.async.4 requests cap it near 1.2 TB/s aggregate), kept for layouts nothing else can read
+        static const bool no_word = getenv("TN_WORD_GATHER") == nullptr;
           if (no_word) continue;
           std::vector<int64_t> bits(st.a_m_stride.begin(), st.a_m_stride.begin() + 7);
           for (int j = 0; j < std::min(5, st.klog); ++j) bits.push_back(st.a_k_stride[j]);

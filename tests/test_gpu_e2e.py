@@ -39,7 +39,7 @@ def run_gpu(tn, plan, dtype, slice_id=0, stem_min_log2=6, policy=0):
     return amps, p
 
 
-@pytest.mark.parametrize("policy", [0, 1, 2])
+@pytest.mark.parametrize("policy", [0, 1, 2, 3])
 @pytest.mark.parametrize("dtype", [0, 1])
 @pytest.mark.parametrize("stem_min", [6, 8, 10])
 def test_c1_full_state_vs_oracle(tn, dtype, stem_min, policy):
@@ -76,7 +76,7 @@ def test_random_small_circuits_sliced(tn, seed, dtype, policy):
 
 
 @pytest.mark.parametrize("dtype", [0, 1])
-@pytest.mark.parametrize("policy", [0, 1, 2])
+@pytest.mark.parametrize("policy", [0, 1, 2, 3])
 def test_c2_reduced_vs_oracle(tn, dtype, policy):
     """C2 (30 qubits, 14 cycles) with extra sub-slicing so the oracle finishes in seconds
     (SURVEY §8(c) c.6): same tree, same kernels, stems up to 2^22."""
@@ -282,3 +282,13 @@ def test_recompute_on_halves_vs_oracle(tn, dtype):
     if dtype == 1:
         p0 = tn.Plan(sub, tn.make_config(dtype=1, stem_min_log2=12))
         assert np.array_equal(tn.contract(p0, tn.Buffers(p0), 0), got)
+
+
+@pytest.mark.parametrize("policy", [0, 3])
+def test_c3_subslice_policies_vs_oracle(tn, policy):
+    """The headline plan sub-sliced to 2^22: identity outputs (policy 0) and transposed C[n][m] stores
+    where they put the next step's contracted modes innermost (policy 3) vs the oracle."""
+    sub = MP.sub_slice(_plan("c3"), 22)
+    ref = contract.contract(load(sub), 0)
+    got, p = run_gpu(tn, sub, 0, 0, stem_min_log2=16, policy=policy)
+    assert metrics.rel_l2(got, ref) <= 2e-2
