@@ -176,28 +176,40 @@ __device__ __forceinline__ void named_bar(int id, int n) {
 
 // KB: fp16 elements of K per stage (the TMA box and swizzle width): 64, or 2K when 2K < 64 so that
 // small-K steps neither stage nor zero-fill 3/4 empty boxes and keep more tiles in flight.
-template <int BN, int KB, int MODE3 = 0>
+// AMODE: the A-operand mode of the kernel (3 = raw landing slots, 4 = 4-byte gather with a bigger table).
+template <int BN, int KB, int AMODE = 0>
 struct Cfg {
   static constexpr int kABytes = BM * KB * 2;
   static constexpr int kBBytes = BN * KB * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kCSub = (BN + 63) / 64;            // 64-column store subtiles
-  // staging ring (64-column subtiles) per epilogue group: 4 deep (more TMA stores in flight) when
-  // that still leaves >= 4 pipeline stages, else 2
-  static constexpr int kNBuf = ((220 * 1024 - 2 * 4 * BM * 128) / kStageBytes >= 4) ? 4 : 2;
+  static constexpr int kMaxSmem = 232448;                 // 227 KB opt-in dynamic shared memory per CTA
+  static constexpr int kTable = AMODE == 4 ? 4096 : 2048; // barriers + gather table
+  // raw TMA landing slots (A mode 3): they are the A bytes in flight from HBM, so as many as fit
+  // (<= 8) next to 2 pipeline stages and 2 staging buffers per epilogue group
+  static constexpr int kRawFit = (220 * 1024 - 2 * 2 * BM * 128 - 2 * kStageBytes) / kABytes;
+  static constexpr int kRaw = AMODE != 3 ? 0 : (kRawFit > TN_RAW_CAP ? TN_RAW_CAP : (kRawFit < 2 ? 2 : kRawFit));
+  static constexpr int kRawBytes = kRaw * kABytes;
+  static constexpr int kFixed = 1024 /*align*/ + kTable + kRawBytes;
+  static constexpr int stages_for(int nbuf) {
+    return (kMaxSmem - kFixed - 2 * nbuf * BM * 128) / kStageBytes;
+  }
+  // output staging ring (64-column subtiles) per epilogue group.  Full K boxes (KB = 64: K-heavy and
+  // compute-bound steps): as few buffers as keep the most pipeline stages — the A operand is the
+  // bytes in flight from HBM, and a tile's epilogue is rare next to its k loop (BN = 256: 4 stages
+  // with one buffer instead of 3 with two).  Short K boxes (output-heavy steps): 4 buffers (more TMA
+  // stores in flight) when that still leaves >= 4 stages, else 2.
+  static constexpr int kNBuf = KB == 64 ? (stages_for(1) > stages_for(2) ? 1 : (stages_for(2) > stages_for(4) ? 2 : 4))
+                                        : (stages_for(4) >= 4 ? 4 : 2);
   static constexpr int kCTma = 2 * kNBuf * BM * 128;      // 128B-swizzled staging for TMA stores, 2 groups
   static constexpr int kCBytes = kCTma;
-  // raw TMA landing slots (A mode 3): they are the A bytes in flight from HBM, so as many as fit
-  // (<= 8) next to 2 pipeline stages
-  static constexpr int kRawFit = (220 * 1024 - kCBytes - 2 * kStageBytes) / kABytes;
-  static constexpr int kRaw = !MODE3 ? 0 : (kRawFit > TN_RAW_CAP ? TN_RAW_CAP : (kRawFit < 2 ? 2 : kRawFit));
-  static constexpr int kRawBytes = kRaw * kABytes;
-  static constexpr int kStagesRaw = (220 * 1024 - kCBytes - kRawBytes) / kStageBytes;
+  static constexpr int kStagesRaw = stages_for(kNBuf);
   static constexpr int kStages = kStagesRaw > 24 ? 24 : kStagesRaw;
   // the TMA-store staging (128B swizzle) must start 1024-aligned: pad the stage area
   static constexpr int kStageArea = (kStages * kStageBytes + 1023) / 1024 * 1024;
-  static constexpr int kSmem =
-      kStageArea + kCBytes + kRawBytes + 1024 /*align*/ + 4096 /*barriers, gather table (<= 192 x 16 B)*/;
+  static constexpr int kSmem = kStageArea + kCBytes + kRawBytes + 1024 /*align*/ + kTable;
+  static_assert(kSmem <= kMaxSmem, "shared memory budget");
+  static_assert(kStages >= 2, "pipeline depth");
   // TMEM accumulators: as many as fit in 512 columns (<= 16), so the MMA runs ahead of the
   // epilogue by several tiles when a tile is small (small K, small N)
   static constexpr int kAccStride = BN < 32 ? 32 : BN;
@@ -358,7 +370,7 @@ __global__ void __launch_bounds__((kAMode == 1 || kAMode == 4) ? kThreadsGather 
   constexpr bool kGather = kAMode == 1 || kAMode == 4;
   constexpr bool kWord = kAMode == 4;
   constexpr bool kInter = kAMode == 2 || kAMode == 3;
-  using C = Cfg<BN, KB, kAMode == 3 ? 1 : 0>;
+  using C = Cfg<BN, KB, kAMode>;
   // a negative input max is the "no re-run needed" signal of the scale re-run (runtime.cu redo)
   if (in_max && in_max[0] < 0.f) return;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -946,7 +958,7 @@ static void launch_bn(__half* c, const __half* a, const __half* bp, uint64_t M, 
                       const float* in_max, const float* b_bound, uint32_t* out_max, int* exp_slot, const OutMap* om,
                       cudaStream_t s, const AGather* ag, const NdPlan* np, const BatchSpec* bs) {
   const uint32_t N2 = std::max<uint32_t>(N2_real, 16);  // B_P has at least 16 (zero-padded) rows
-  using C = tc::Cfg<BN, KB, G == 3 ? 1 : 0>;
+  using C = tc::Cfg<BN, KB, G>;
   {
     // the dynamic shared-memory opt-in is per device: remember it per device ordinal (a process may
     // drive several devices, e.g. one thread per GPU)
