@@ -113,7 +113,7 @@ struct MaxSlots {
   const float* p[8];
 };
 void launch_max_slots(float* dst, const MaxSlots& src, cudaStream_t s);
-void launch_redo_check(const uint32_t* out_max, const float* in_max, float* redo_in, int bits, cudaStream_t s);
+void launch_redo_check(uint32_t* out_max, const float* in_max, float* redo_in, int bits, cudaStream_t s);
 void launch_copy_c64(float2* dst, const float2* src, uint64_t n, cudaStream_t s);
 void launch_gemm_c64(float2* c, const float2* a, const float2* b, uint64_t M, uint32_t K, uint32_t N,
                      const OutMap* om, cudaStream_t s, const float* in_max = nullptr, const float* b_bound = nullptr,
@@ -147,6 +147,10 @@ struct BatchSpec {
   const int* table = nullptr;
   uint64_t n_out = 0, n_a = 0, n_b = 0;
 };
+void launch_gemm_chalf_batched_simt(__half2* c, const __half2* a, const __half* bp, uint64_t M, uint32_t K, uint32_t N,
+                                    uint64_t n_out, const int* ia, const int* ib, uint64_t b_blk_halfs,
+                                    const float* in_max, const float* b_bound, uint32_t* out_max, int* exp_slot,
+                                    cudaStream_t s);
 void launch_gemm_chalf_tc_batched(__half* c, const __half* a, const __half* bp, uint64_t M, uint32_t K2, uint32_t N2,
                                   const float* in_max, const float* b_bound, uint32_t* out_max, int* exp_slot,
                                   const BatchSpec& bs, cudaStream_t s);

@@ -255,13 +255,17 @@ void launch_max_slots(float* dst, const MaxSlots& src, cudaStream_t s) {
 // max (out_max, already scaled) is below 2^(14 - bits), the GEMM is run again from the same input
 // with an input max smaller by exactly 2^delta (delta = the exponent that brings out_max near 2^14),
 // i.e. an output exponent larger by delta; otherwise the re-run launch exits at once (-1).
-__global__ void redo_check_kernel(const uint32_t* out_max, const float* in_max, float* redo_in, int bits) {
+// The re-run's outputs are exactly the first pass's fp32 values times 2^delta, so the realised max is
+// updated here (no second max reduction, and no second all-reduce across ranks).
+__global__ void redo_check_kernel(uint32_t* out_max, const float* in_max, float* redo_in, int bits) {
   const float m = __uint_as_float(*out_max);
   const int d = scale_exp_for(m);
-  *redo_in = (m > 0.f && d >= bits) ? ldexpf(*in_max, -d) : -1.f;
+  const bool redo = m > 0.f && d >= bits;
+  *redo_in = redo ? ldexpf(*in_max, -d) : -1.f;
+  if (redo) *out_max = __float_as_uint(ldexpf(m, d));
 }
 
-void launch_redo_check(const uint32_t* out_max, const float* in_max, float* redo_in, int bits, cudaStream_t s) {
+void launch_redo_check(uint32_t* out_max, const float* in_max, float* redo_in, int bits, cudaStream_t s) {
   redo_check_kernel<<<1, 1, 0, s>>>(out_max, in_max, redo_in, bits);
   TN_CUDA(cudaGetLastError());
 }

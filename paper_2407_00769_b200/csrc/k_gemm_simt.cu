@@ -445,4 +445,55 @@ void launch_gemm_chalf_simt(__half2* c, const __half2* a, const __half* bp, uint
   TN_CUDA(cudaGetLastError());
 }
 
+// Gather-batched complex-half GEMM for the small steps of the sparse-state tail (K < 4, N < 8 or
+// fewer than 128 rows per entry, where the tcgen05 batched launch does not apply): thread per output
+// element, C[b][m][n] = 2^e sum_k A[ia[b]][m][k] B_ib[b][k][n] with B read from its Eq. 6 B_P block
+// (Re b at row 2n, column 2k; Im b at row 2n+1), fp32 accumulation, same scale rule and max record as
+// the other stem GEMMs.  One launch per tail step instead of one per batch entry.
+__global__ void __launch_bounds__(256) gemm_chalf_batched_simt_kernel(
+    __half2* __restrict__ C, const __half2* __restrict__ A, const __half* __restrict__ BP, uint64_t M, int K, int N,
+    uint64_t n_out, const int* __restrict__ ia, const int* __restrict__ ib, uint64_t b_blk_halfs,
+    const float* in_max, const float* b_bound, uint32_t* out_max, int* exp_slot) {
+  if (in_max && in_max[0] < 0.f) return;  // scale re-run not needed (runtime.cu redo)
+  int e = 0;
+  if (in_max && b_bound) e = scale_exp_for(in_max[0] * b_bound[0]);
+  if (exp_slot && blockIdx.x == 0 && threadIdx.x == 0) *exp_slot = e;
+  const float sc = ldexpf(1.f, e);
+  const int K2 = 2 * K;
+  const uint64_t per = M * (uint64_t)N, total = per * n_out;
+  float mx = 0.f;
+  for (uint64_t idx = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t b = idx / per, r = idx % per, m = r / N;
+    const int n = (int)(r % N);
+    const __half2* a = A + ((uint64_t)ia[b] * M + m) * K;
+    const __half* bp = BP + (uint64_t)ib[b] * b_blk_halfs;
+    float cr = 0.f, ci = 0.f;
+    for (int k = 0; k < K; ++k) {
+      const float2 av = __half22float2(a[k]);
+      const float br = __half2float(bp[(size_t)(2 * n) * K2 + 2 * k]);
+      const float bi = __half2float(bp[(size_t)(2 * n + 1) * K2 + 2 * k]);
+      cr = fmaf(av.x, br, fmaf(-av.y, bi, cr));
+      ci = fmaf(av.x, bi, fmaf(av.y, br, ci));
+    }
+    C[idx] = __floats2half2_rn(cr * sc, ci * sc);
+    mx = fmaxf(mx, fmaxf(fabsf(cr * sc), fabsf(ci * sc)));
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if (out_max && (threadIdx.x & 31) == 0) atomic_max_pos2(out_max, mx);
+}
+
+void launch_gemm_chalf_batched_simt(__half2* c, const __half2* a, const __half* bp, uint64_t M, uint32_t K, uint32_t N,
+                                    uint64_t n_out, const int* ia, const int* ib, uint64_t b_blk_halfs,
+                                    const float* in_max, const float* b_bound, uint32_t* out_max, int* exp_slot,
+                                    cudaStream_t s) {
+  const uint64_t total = M * N * n_out;
+  if (total == 0) return;
+  const uint64_t blocks = std::min<uint64_t>((total + 255) / 256, 148ull * 16);
+  gemm_chalf_batched_simt_kernel<<<(unsigned)blocks, 256, 0, s>>>(c, a, bp, M, (int)K, (int)N, n_out, ia, ib, b_blk_halfs,
+                                                                  in_max, b_bound, out_max, exp_slot);
+  TN_CUDA(cudaGetLastError());
+}
+
 }  // namespace tn

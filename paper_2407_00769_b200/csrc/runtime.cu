@@ -566,7 +566,8 @@ void run_gemm_once(Plan& p, const StemStep& st, size_t i, const void* src, void*
 // One stem GEMM plus its scale re-run (complex-half: redo_check + the same launch, which exits at once
 // unless the realised output max lost more than TN_REDO_BITS (default 10) bits of fp16 headroom).
 // collective (sharded main path): every rank must scale by the same power of two, so the realised max is
-// all-reduced before the re-run decision and again after it (per-rank split-tail chains pass false).
+// all-reduced before the re-run decision, which every rank then takes alike (per-rank split-tail
+// chains pass false).
 void run_gemm(Plan& p, const StemStep& st, size_t i, const void* src, void* dst, int mshift, const float* in_max,
               uint32_t* out_max, int* exp_slot, unsigned char* W, const Scratch& sc, cudaStream_t s,
               bool collective = false) {
@@ -574,10 +575,9 @@ void run_gemm(Plan& p, const StemStep& st, size_t i, const void* src, void* dst,
   const bool coll = collective && p.world > 1;  // both dtypes scale by powers of two (C-A8)
   if (coll) xfer_allreduce_max(p, reinterpret_cast<float*>(out_max), s);
   if (p.cfg.dtype != TN_CHALF || !in_max || redo_bits() <= 0) return;
-  launch_redo_check(out_max, in_max, &sc.redo_in[i], redo_bits(), s);
-  run_gemm_once(p, st, i, src, dst, mshift, &sc.redo_in[i], out_max, exp_slot, W, sc, s);
+  launch_redo_check(out_max, in_max, &sc.redo_in[i], redo_bits(), s);  // also sets the re-run's max
+  run_gemm_once(p, st, i, src, dst, mshift, &sc.redo_in[i], nullptr, exp_slot, W, sc, s);
   ++p.launches;
-  if (coll) xfer_allreduce_max(p, reinterpret_cast<float*>(out_max), s);
 }
 
 void run_gemm_once(Plan& p, const StemStep& st, size_t i, const void* src, void* dst, int mshift, const float* in_max,
@@ -1072,6 +1072,7 @@ void sparse_tail(Plan& p, const tn_buffers* b, const uint64_t* prefixes, size_t 
       if (pass == 1) {
         launch_redo_check(out_max, &sc.max_slot[i], &sc.redo_in[i], redo_bits(), s);
         in_max = &sc.redo_in[i];
+        out_max = nullptr;  // redo_check already holds the re-run's max
       }
       if (batched) {
         BatchSpec bs;
@@ -1084,8 +1085,15 @@ void sparse_tail(Plan& p, const tn_buffers* b, const uint64_t* prefixes, size_t 
                                      reinterpret_cast<const __half*>(W + st.b_off), M, 2 * K, 2 * N, in_max,
                                      &sc.b_bound[i], out_max, exp_slot, bs, s);
         ++p.launches;
+      } else if (p.cfg.dtype == TN_CHALF) {
+        // small steps (K < 4, N < 8, < 128 rows per entry): one batched SIMT launch
+        launch_gemm_chalf_batched_simt(reinterpret_cast<__half2*>(other), reinterpret_cast<const __half2*>(cur),
+                                       reinterpret_cast<const __half*>(W + st.b_off), M, K, N, n_out,
+                                       didx + ia_off[t], didx + ib_off[t], st.b_blk / 2, in_max, &sc.b_bound[i],
+                                       out_max, exp_slot, s);
+        ++p.launches;
       } else {
-        // small steps: one GEMM per entry (identical scale inputs, so every entry writes the same exponent)
+        // complex64: one GEMM per entry (identical scale inputs, so every entry writes the same exponent)
         OutMap om = identity_map(M, N);
         for (uint64_t e = 0; e < n_out; ++e) {
           const unsigned char* a = cur + (uint64_t)sch[t].ia[e] * (M * K) * eb;
