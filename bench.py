@@ -149,12 +149,17 @@ def run_oracle(sub, steps, warmup):
 
 
 def cpu_baseline(plan, target_log2, steps=1, warmup=0):
+    from oracle import contract
     sub = oracle_sample(plan, target_log2)
     fl, t = run_oracle(sub, steps, warmup)
+    full = contract.flops(plan)
     return {"value": fl / t / 1e12, "unit": "TFLOPS", "cores": _CORES, "kind": "oracle",
             "seconds": t, "sample": f"oracle (numpy complex128, np.tensordot) on slice 0 of the same plan "
                                    f"sub-sliced by {len(sub['sliced']) - len(plan['sliced'])} extra edges "
-                                   f"(every intermediate <= 2^{target_log2}); {fl:.3e} flops in {t:.2f} s"}, sub
+                                   f"(every intermediate <= 2^{target_log2}); {fl:.3e} flops in {t:.2f} s",
+            "extrapolated_full_subtask_s": t * full / fl,
+            "extrapolation": f"x {full / fl:.1f} = the full subtask's {full:.3e} flops at the sample's rate "
+                             f"(labelled estimate, SURVEY 8(d) d.4)"}, sub
 
 
 def parity(tn, sub, cfg_kw):
@@ -269,7 +274,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--plan", default="c3")
-    ap.add_argument("--oracle-log2", type=int, default=24)
+    ap.add_argument("--oracle-log2", type=int, default=26)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--replicas", action="store_true", help="N>1: independent slices per GPU (weak scaling)")
     ap.add_argument("--comm", default="int8", choices=["int8", "int4", "fp16", "int8_tensor"])
@@ -342,8 +347,13 @@ def main():
     nrg = Energy(local)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(dev_stream)
+    ms_sum = None
     for _ in range(args.steps):
         step()
+        # per-phase CUDA events of this step (recorded by the library inside its graph on this stream);
+        # reading them waits for the step's last event: one short host sync per step
+        msk = p.report().get("ms", [])
+        ms_sum = msk if ms_sum is None else [a + b for a, b in zip(ms_sum, msk)]
     e1.record(dev_stream)
     torch.cuda.synchronize()
     watts = nrg.stop()
@@ -385,8 +395,8 @@ def main():
     value = flops / (t_ms * 1e-3) / 1e12
     hbm, tc_burst, tc_sus, src = peaks()
 
-    # ---- roofline of the dominant kernel (from the timed region's CUDA events)
-    ms = rep.get("ms", [])
+    # ---- roofline of the dominant kernel (from the timed region's CUDA events, mean over the K steps)
+    ms = [x / args.steps for x in ms_sum] if ms_sum else []
     steps = rep["steps"]
     gemm_ms = perm_ms = 0.0
     gemm_bytes = gemm_flops = t_roof_gemm = perm_bytes = 0.0
@@ -429,12 +439,13 @@ def main():
     # subtask, from the committed ncu launch list of this command (profiles/, C3 single GPU only)
     roof["traffic"] = None
     roof["algorithmic_bytes"] = gemm_bytes
-    summ = os.path.join(ROOT, "profiles", "r01_launches_summary.json")
-    if roof["kernel"].startswith("gemm") and args.plan == "c3" and world == 1 and os.path.exists(summ):
+    summ_name = {"c3": "r02_launches_summary.json", "c3_sweep": "r01_launches_summary.json"}.get(args.plan)
+    summ = os.path.join(ROOT, "profiles", summ_name) if summ_name else ""
+    if roof["kernel"].startswith("gemm") and world == 1 and summ and os.path.exists(summ):
         with open(summ) as fh:
             ps = json.load(fh)["per_subtask"]
         roof["traffic"] = sum(ps[f]["dram_bytes"] for f in ("gemm_tc", "gemm_simt") if f in ps)
-        roof["traffic_source"] = "profiles/r01_launches_summary.json (ncu, bytes per subtask, all GEMM launches)"
+        roof["traffic_source"] = f"profiles/{summ_name} (ncu, bytes per subtask, all GEMM launches)"
     roof["share_of_step"] = {"gemm": gemm_ms / t_ms, "permute": perm_ms / t_ms, "common+prep": common_ms / t_ms}
 
     if rank == 0:
