@@ -185,25 +185,28 @@ struct Cfg {
   static constexpr int kCSub = (BN + 63) / 64;            // 64-column store subtiles
   static constexpr int kMaxSmem = 232448;                 // 227 KB opt-in dynamic shared memory per CTA
   static constexpr int kTable = AMODE == 4 ? 4096 : 2048; // barriers + gather table
+  static constexpr bool kDeep = AMODE == 5;               // plain TMA A, deep pipeline (see kNBuf)
   // raw TMA landing slots (A mode 3): they are the A bytes in flight from HBM, so as many as fit
   // (<= 8) next to 2 pipeline stages and 2 staging buffers per epilogue group
-  static constexpr int kRawFit = (220 * 1024 - 2 * 2 * BM * 128 - 2 * kStageBytes) / kABytes;
+  static constexpr int kNBufOld = ((220 * 1024 - 2 * 4 * BM * 128) / kStageBytes >= 4) ? 4 : 2;
+  static constexpr int kRawFit = (220 * 1024 - 2 * kNBufOld * BM * 128 - 2 * kStageBytes) / kABytes;
   static constexpr int kRaw = AMODE != 3 ? 0 : (kRawFit > TN_RAW_CAP ? TN_RAW_CAP : (kRawFit < 2 ? 2 : kRawFit));
   static constexpr int kRawBytes = kRaw * kABytes;
   static constexpr int kFixed = 1024 /*align*/ + kTable + kRawBytes;
   static constexpr int stages_for(int nbuf) {
     return (kMaxSmem - kFixed - 2 * nbuf * BM * 128) / kStageBytes;
   }
-  // output staging ring (64-column subtiles) per epilogue group.  Full K boxes (KB = 64: K-heavy and
-  // compute-bound steps): as few buffers as keep the most pipeline stages — the A operand is the
+  // output staging ring (64-column subtiles) per epilogue group.  Deep variant (AMODE 5, K-heavy
+  // steps, chosen at launch): as few buffers as keep the most pipeline stages — the A operand is the
   // bytes in flight from HBM, and a tile's epilogue is rare next to its k loop (BN = 256: 4 stages
-  // with one buffer instead of 3 with two).  Short K boxes (output-heavy steps): 4 buffers (more TMA
-  // stores in flight) when that still leaves >= 4 stages, else 2.
-  static constexpr int kNBuf = KB == 64 ? (stages_for(1) > stages_for(2) ? 1 : (stages_for(2) > stages_for(4) ? 2 : 4))
-                                        : (stages_for(4) >= 4 ? 4 : 2);
+  // with one buffer instead of 3 with two).  Otherwise: 4 buffers (more TMA stores in flight) when
+  // that still leaves >= 4 stages, else 2.
+  static constexpr int kNBufDeep = stages_for(1) > stages_for(2) ? 1 : (stages_for(2) > stages_for(4) ? 2 : 4);
+  static constexpr int kNBuf = kDeep ? kNBufDeep : kNBufOld;
   static constexpr int kCTma = 2 * kNBuf * BM * 128;      // 128B-swizzled staging for TMA stores, 2 groups
   static constexpr int kCBytes = kCTma;
-  static constexpr int kStagesRaw = stages_for(kNBuf);
+  // round-1 budget (220 KB for stages + staging) unless deep
+  static constexpr int kStagesRaw = kDeep ? stages_for(kNBuf) : (220 * 1024 - kCBytes - kRawBytes) / kStageBytes;
   static constexpr int kStages = kStagesRaw > 24 ? 24 : kStagesRaw;
   // the TMA-store staging (128B swizzle) must start 1024-aligned: pad the stage area
   static constexpr int kStageArea = (kStages * kStageBytes + 1023) / 1024 * 1024;

@@ -22,6 +22,9 @@ extern template void launch_kb<3>(int, __half*, const __half*, const __half*, ui
 extern template void launch_kb<4>(int, __half*, const __half*, const __half*, uint64_t, uint32_t, uint32_t,
                                   const float*, const float*, uint32_t*, int*, const OutMap*, cudaStream_t,
                                   const AGather*, const NdPlan*, const BatchSpec*);
+extern template void launch_kb<5>(int, __half*, const __half*, const __half*, uint64_t, uint32_t, uint32_t,
+                                  const float*, const float*, uint32_t*, int*, const OutMap*, cudaStream_t,
+                                  const AGather*, const NdPlan*, const BatchSpec*);
 
 static bool build_nd(const AGather& ag, NdPlan& out) {
   int pm[kMaxModes], pk[24];
@@ -334,7 +337,14 @@ void launch_gemm_chalf_tc(__half* c, const __half* a, const __half* bp, uint64_t
     launch_kb<1>(kb_plain, c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, ag, nullptr, nullptr);
     return;
   }
-  launch_kb<0>(kb_plain, c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, nullptr, nullptr, nullptr);
+  // plain TMA A: the deep-pipeline variant (one output staging buffer per epilogue group, more stages)
+  // for K-heavy steps; TN_STAGE_DEEP = 0 / 1 forces either (A/B knob)
+  static const int deep_env = getenv("TN_STAGE_DEEP") ? atoi(getenv("TN_STAGE_DEEP")) : -1;
+  const bool deep = deep_env >= 0 ? deep_env != 0 : (K2 >= 512 && K2 >= 4 * N2);
+  if (deep && kb_plain == 64)
+    launch_kb<5>(kb_plain, c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, nullptr, nullptr, nullptr);
+  else
+    launch_kb<0>(kb_plain, c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, nullptr, nullptr, nullptr);
 }
 
 void launch_gemm_chalf_tc_batched(__half* c, const __half* a, const __half* bp, uint64_t M, uint32_t K2, uint32_t N2,
