@@ -784,16 +784,24 @@ __global__ void __launch_bounds__((kAMode == 1 || kAMode == 4) ? kThreadsGather 
           }
           if (scat) {
             if (row_ok) {
-              const uint64_t nb = (uint64_t)((n0 + c) >> 1);
+              const uint64_t nb = (uint64_t)((n0 + c) >> 1);  // a multiple of 16: bits 0..3 are q's
               const int V = 1 << run;
+              // the 16 columns' offsets = this chunk's base (its n bits >= 4, once per chunk) + the
+              // offset of q's bits 0..3 (compile-time q, four strides in registers): a couple of adds
+              // per store instead of a loop over every n bit
+              int64_t nbase = row_off;
+              for (int j = 4; j < sc_args.nbits; ++j)
+                if ((nb >> j) & 1) nbase += sc_args.ns[j];
+              const int64_t ns0 = run <= 0 && sc_args.nbits > 0 ? sc_args.ns[0] : 0;
+              const int64_t ns1 = run <= 1 && sc_args.nbits > 1 ? sc_args.ns[1] : 0;
+              const int64_t ns2 = run <= 2 && sc_args.nbits > 2 ? sc_args.ns[2] : 0;
+              const int64_t ns3 = run <= 3 && sc_args.nbits > 3 ? sc_args.ns[3] : 0;
               // q and v are compile-time (full unroll) so pk stays in registers
 #pragma unroll
               for (int q = 0; q < 16; ++q) {
                 if ((q & (V - 1)) || q >= nvalid) continue;
-                int64_t off = row_off;
-                const uint64_t ng = nb + q;
-                for (int j = run; j < sc_args.nbits; ++j)
-                  if ((ng >> j) & 1) off += sc_args.ns[j];
+                const int64_t off = nbase + ((q & 1) ? ns0 : 0) + ((q & 2) ? ns1 : 0) + ((q & 4) ? ns2 : 0) +
+                                    ((q & 8) ? ns3 : 0);
                 uint32_t* dst = out_scatter + off;
                 if (V >= 8) {
                   // 256-bit stores (STG.256): one full 32-byte sector per instruction and thread
