@@ -280,6 +280,7 @@ def main():
     ap.add_argument("--comm", default="int8", choices=["int8", "int4", "fp16", "int8_tensor"])
     ap.add_argument("--policy", type=int, default=-1, help="layout policy (tn.h); -1: the plan's default")
     ap.add_argument("--subspaces", type=int, default=1024, help="sparse-state plans: correlated subspaces")
+    ap.add_argument("--quant-from-pct", type=int, default=-1, help="sharded: quantise swaps from this %% of the path")
     ap.add_argument("--seed", type=int, default=0)
     args = ap.parse_args()
 
@@ -325,7 +326,7 @@ def main():
         args.comm, tn.TN_COMM_FP16)
     policy = args.policy if args.policy >= 0 else DEFAULT_POLICY.get(args.plan, 0)
     p = tn.Plan(plan_json, tn.make_config(dtype=tn.TN_CHALF, stem_min_log2=20, comm_codec=codec,
-                                          layout_policy=policy), comm=comm)
+                                          layout_policy=policy, quant_from_pct=args.quant_from_pct), comm=comm)
     info = p.info()
     bufs = tn.Buffers(p)
     n_sl = min(info["n_slices_log2"], 63)
@@ -388,6 +389,19 @@ def main():
         tt = torch.tensor([te_ms], device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         te_ms = float(tt.item())
+
+    # ---- sharded with a codec: its error at full size against the same subtask with fp16 swaps
+    comm_err = None
+    if sharded and codec != tn.TN_COMM_FP16 and any(st.get("quant") for st in p.report()["steps"]):
+        a_q = tn.contract(p, bufs, slice_id)
+        p16 = tn.Plan(plan_json, tn.make_config(dtype=tn.TN_CHALF, stem_min_log2=20, comm_codec=tn.TN_COMM_FP16,
+                                                layout_policy=policy), comm=comm)
+        a_16 = tn.contract(p16, tn.Buffers(p16), slice_id)
+        del p16
+        import numpy as np
+        comm_err = {"rel_l2_vs_fp16_swaps": float(np.linalg.norm(a_q - a_16) / np.linalg.norm(a_16)),
+                    "quantised_swaps": sum(1 for st in p.report()["steps"] if st.get("quant")),
+                    "note": "full-size subtask, same slice; fp16 swaps move bits (reading C-A32)"}
 
     # job flops: stem_flops is per rank (a shard does 1/N of the subtask's stem work when sharded;
     # a replica does a whole subtask)
@@ -468,7 +482,7 @@ def main():
                 "e2e": {"value": flops / (te_ms * 1e-3) / 1e12, "unit": "TFLOPS",
                         "ms_per_step": te_ms, "h2d_bytes_per_step": info["h2d_bytes"],
                         "d2h_bytes_per_step": (4 << info["n_open"]) + 4 * (2 * info["n_stem_steps"] + 4)},
-                "gpu_launches": launches, "clocks": clocks,
+                "gpu_launches": launches, "clocks": clocks, "comm_error": comm_err,
                 "energy": None if watts is None else
                 {"joules_per_step": watts * t_ms * 1e-3, "wh_per_step": watts * t_ms * 1e-3 / 3600.0,
                  "mean_board_w_per_gpu": watts / world,

@@ -14,8 +14,10 @@ import torch.distributed as dist
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
 
 from paper_2407_00769_b200 import tn  # noqa: E402
+from swap_error import predicted_swap_error  # noqa: E402
 
 
 def main():
@@ -45,7 +47,8 @@ def main():
                                        (tn.TN_COMM_INT8, "int8_all_c3", sub, 0, 14),
                                        (tn.TN_COMM_INT8, "int8_all_c3_unfused", sub, 0, 14),
                                        (tn.TN_COMM_INT4, "int4", sub, -1, 14),
-                                       (tn.TN_COMM_INT4, "int4_late", sub, 30, 14)):
+                                       (tn.TN_COMM_INT4, "int4_all", sub, 0, 14),
+                                       (tn.TN_COMM_INT8_TENSOR, "int8_tensor_all", sub, 0, 14)):
         p = tn.Plan(plan, tn.make_config(stem_min_log2=sm, comm_codec=codec, quant_from_pct=pct,
                                          no_fuse_swap_quant=int(name.endswith("_unfused"))), comm=comm)
         b = tn.Buffers(p)
@@ -74,8 +77,13 @@ def main():
                    "rel_int8_oracle": metrics.rel_l2(results["int8"][0], ref),
                    "rel_int4_oracle": metrics.rel_l2(results["int4"][0], ref),
                    "int4_swaps_c3": sum(1 for s in results["int4"][1]["steps"] if s.get("quant")),
-                   "rel_int4_late_oracle": metrics.rel_l2(results["int4_late"][0], ref),
-                   "int4_swaps_late": sum(1 for s in results["int4_late"][1]["steps"] if s.get("quant")),
+                   "rel_int4_all_oracle": metrics.rel_l2(results["int4_all"][0], ref),
+                   "rel_int8_tensor_all_oracle": metrics.rel_l2(results["int8_tensor_all"][0], ref),
+                   "fp16_oracle": metrics.rel_l2(results["fp16"][0], ref),
+                   "pred_int8_all": predicted_swap_error(sub, results["int8_all_c3"][1], ref, "int8_g128"),
+                   "pred_int8": predicted_swap_error(sub, results["int8"][1], ref, "int8_g128"),
+                   "pred_int4_all": predicted_swap_error(sub, results["int4_all"][1], ref, "int4"),
+                   "pred_int8_tensor_all": predicted_swap_error(sub, results["int8_tensor_all"][1], ref, "int8"),
                    "rel_fp16_vs_1gpu": metrics.rel_l2(results["fp16"][0], one),
                    "rel_1gpu_oracle": metrics.rel_l2(one, ref),
                    "swaps": sum(1 for s in results["int8"][1]["steps"] if s.get("swap")),
