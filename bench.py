@@ -461,6 +461,20 @@ def main():
         roof["traffic"] = sum(ps[f]["dram_bytes"] for f in ("gemm_tc", "gemm_simt") if f in ps)
         roof["traffic_source"] = f"profiles/{summ_name} (ncu, bytes per subtask, all GEMM launches)"
     roof["share_of_step"] = {"gemm": gemm_ms / t_ms, "permute": perm_ms / t_ms, "common+prep": common_ms / t_ms}
+    # path roofline: sum over stem steps of max(F/P, B_alg/BW) over the measured step
+    # time, and the step-shape histogram (log2 K*N -> steps) of the plan
+    t_roof_path = 0.0
+    shape_hist = {}
+    for st in steps:
+        M, K, N = 2.0 ** st["m"], 2.0 ** st["k"], 2.0 ** st["n"]
+        t_roof_path += max(8 * M * K * N / (tc_burst * 1e12), (4 * (M * K + M * N) + 8 * K * N) / (hbm * 1e9)) * 1e3
+        kn = st["k"] + st["n"]
+        shape_hist[kn] = shape_hist.get(kn, 0) + 1
+    path_roof = {"roofline_ms": t_roof_path, "frac": t_roof_path / t_ms,
+                 "peaks": f"{tc_burst:.0f} TF/s burst, {hbm:.0f} GB/s ({src})",
+                 "log2_KN_histogram": {str(k): shape_hist[k] for k in sorted(shape_hist)},
+                 "tensor_bound_steps": sum(1 for st in steps if 2 * 2.0 ** (st["k"] + st["n"]) /
+                                           (2.0 ** st["k"] + 2.0 ** st["n"]) > tc_burst * 1e3 / hbm)}
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "TFLOPS", "n_gpus": world, "steps": args.steps,
@@ -478,7 +492,7 @@ def main():
                                  f">> 126 MB)"},
                 "tflops_per_gpu": value / world, "subtask_ms": t_ms,
                 "breakdown_ms": {"common+prep": common_ms, "permute": perm_ms, "gemm": gemm_ms},
-                "roofline": roof,
+                "roofline": roof, "path_roofline": path_roof,
                 "e2e": {"value": flops / (te_ms * 1e-3) / 1e12, "unit": "TFLOPS",
                         "ms_per_step": te_ms, "h2d_bytes_per_step": info["h2d_bytes"],
                         "d2h_bytes_per_step": (4 << info["n_open"]) + 4 * (2 * info["n_stem_steps"] + 4)},
