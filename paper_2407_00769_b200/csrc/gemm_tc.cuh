@@ -1110,7 +1110,10 @@ static void launch_bn(__half* c, const __half* a, const __half* bp, uint64_t M, 
   for (uint64_t m_off = 0; m_off < M; m_off += chunk) {
     uint64_t mm = std::min<uint64_t>(chunk, M - m_off);
     // (cp.async gather: the A map is unused; N-d: the whole stem, coordinates from the global row)
-    CUtensorMap ma = np ? make_map_nd(a, *np) : make_map_2d(G ? a : a + m_off * K2, K2, G ? tc::BM : mm, KB, tc::BM);
+    // plain TMA A (modes 0 and 5): a 2-D map over this chunk's rows; the gathers (1, 4) do not use it
+    constexpr bool kPlainA = G == 0 || G == 5;
+    CUtensorMap ma = np ? make_map_nd(a, *np)
+                        : make_map_2d(kPlainA ? a + m_off * K2 : a, K2, kPlainA ? mm : tc::BM, KB, tc::BM);
     gargs.m_base = m_off;
     CUtensorMap mc = make_map_2d(c + m_off * N2, N2, mm, 64, epi_stg == 3 ? 32 : tc::BM);
     // scatter: base of this chunk's rows in the OutMap; row-major: the chunk's first row (STG epilogue)
