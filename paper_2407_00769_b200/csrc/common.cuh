@@ -70,6 +70,7 @@ struct GatherArgs {
 // identity != 0 means plain row-major [M][N] (ms[j] = N << j, ns[j] = 1 << j).
 struct OutMap {
   int mbits, nbits, identity;
+  int transposed;                // C[n][m]: n outermost, m innermost (ns[j] = M << j, ms[j] = 1 << j)
   int64_t ms[kMaxModes];
   int64_t ns[24];
 };

@@ -821,6 +821,13 @@ __global__ void __launch_bounds__((kAMode == 1 || kAMode == 4) ? kThreadsGather 
                 }
               }
             }
+          } else if (epi_stg == 4) {
+            // transposed store C[n][m] (layout policy 3): stage the subtile as [32 complex n][128 m]
+            // (each warp writes 32 consecutive words per column: no bank conflict), then one TMA box
+            uint32_t* st32 = reinterpret_cast<uint32_t*>(sbuf);
+            const int q0 = (c & 63) >> 1;  // first complex column of these 32 real columns
+#pragma unroll
+            for (int j = 0; j < 16; ++j) st32[(q0 + j) * BM + row] = pk[j];
           } else {
             unsigned char* srow = sbuf + row * 128;
             const int cb = (c & 63) >> 3;  // first 16-byte chunk of these 32 columns
@@ -868,6 +875,9 @@ __global__ void __launch_bounds__((kAMode == 1 || kAMode == 4) ? kThreadsGather 
               uint64_t pol;
               asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
               tma_store_2d_hint(&tmC, sbuf, n0 + sub, m0, pol);
+            } else if (epi_stg == 4) {
+              // box {128 m (inner, global row), 32 complex n} of the C^T map
+              tma_store_2d(&tmC, sbuf, (int)(ga.m_base + (uint64_t)m0), (n0 + sub) >> 1);
             } else {
               tma_store_2d(&tmC, sbuf, n0 + sub, m0);
             }
@@ -920,6 +930,20 @@ static CUtensorMap make_map_2d(const void* base, uint64_t inner, uint64_t outer,
                             CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw TnError{TN_E_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")"};
+  return m;
+}
+
+// C^T [N complex][M complex] as 4-byte elements (one complex-half value each), box {128 m, 32 n}
+static CUtensorMap make_map_t(const void* base, uint64_t M, uint64_t N) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {M, N};
+  cuuint64_t strides[1] = {M * 4};
+  cuuint32_t box[2] = {(cuuint32_t)tc::BM, 32};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = get_encode()(&m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<void*>(base), dims, strides, box, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw TnError{TN_E_CUDA, "cuTensorMapEncodeTiled (C^T) failed (" + std::to_string((int)r) + ")"};
   return m;
 }
 
@@ -1017,6 +1041,10 @@ static void launch_bn(__half* c, const __half* a, const __half* bp, uint64_t M, 
   ScatterArgs sa;
   memset(&sa, 0, sizeof(sa));
   const uint32_t n_cols = N2_real / 2;
+  // transposed output C[n][m] (layout policy 3): TMA stores of [32 n][128 m] boxes of a C^T map when
+  // the tile geometry allows (whole 128-row tiles, whole 64-column subtiles), else the scatter path
+  const bool transposed = om && om->transposed && M % tc::BM == 0 && N2_real % 64 == 0 && M < (1ull << 31) &&
+                          !getenv("TN_NO_TSTORE");
   OutMap ident;
   static const bool direct_env = getenv("TN_DIRECT_EPI") != nullptr;  // experiment knob
   if ((N2_real < 16 || direct_env) && (!om || om->identity)) {  // TMA stores need 16-byte rows
@@ -1024,7 +1052,7 @@ static void launch_bn(__half* c, const __half* a, const __half* bp, uint64_t M, 
     om = &ident;
     ident.identity = 0;
   }
-  if (om && !om->identity) {
+  if (om && !om->identity && !transposed) {
     sa.on = 1;
     sa.mbits = om->mbits;
     sa.nbits = om->nbits;
@@ -1115,7 +1143,8 @@ static void launch_bn(__half* c, const __half* a, const __half* bp, uint64_t M, 
     CUtensorMap ma = np ? make_map_nd(a, *np)
                         : make_map_2d(kPlainA ? a + m_off * K2 : a, K2, kPlainA ? mm : tc::BM, KB, tc::BM);
     gargs.m_base = m_off;
-    CUtensorMap mc = make_map_2d(c + m_off * N2, N2, mm, 64, epi_stg == 3 ? 32 : tc::BM);
+    CUtensorMap mc = transposed ? make_map_t(c, M, N2_real / 2)
+                                : make_map_2d(c + m_off * N2, N2, mm, 64, epi_stg == 3 ? 32 : tc::BM);
     // scatter: base of this chunk's rows in the OutMap; row-major: the chunk's first row (STG epilogue)
     uint32_t* out_sc = reinterpret_cast<uint32_t*>(c) + (sa.on ? outmap_m(*om, m_off) : m_off * (N2 / 2));
     uint32_t num_m = (uint32_t)((mm + tc::BM - 1) / tc::BM);
@@ -1124,7 +1153,7 @@ static void launch_bn(__half* c, const __half* a, const __half* bp, uint64_t M, 
     // the exponent is recorded once (first chunk); later chunks reuse the same inputs
     tc::gemm_chalf_tc_kernel<BN, KB, G><<<grid, (G == 1 || G == 4) ? tc::kThreadsGather : tc::kThreads, C::kSmem, s>>>(
         ma, mb, mc, num_m, num_n, (int)K2, in_max, b_bound, out_max, m_off ? nullptr : exp_slot, sa, out_sc, mm,
-        n_cols, gargs, nda, epi_stg, BatchArgs{});
+        n_cols, gargs, nda, transposed ? 4 : epi_stg, BatchArgs{});
     TN_CUDA(cudaGetLastError());
   }
 }

@@ -648,6 +648,9 @@ static Plan* load_plan_fixed(const char* json, size_t len, const tn_config* cfg_
         std::vector<int> ident = kept;
         ident.insert(ident.end(), newl.begin(), newl.end());
         st.out_identity = (ident == out);
+        std::vector<int> trans = newl;
+        trans.insert(trans.end(), kept.begin(), kept.end());
+        st.out_transposed = !st.out_identity && trans == out;
       }
       if (st.klog > 16 || st.nlog > 16) throw err(TN_E_UNSUPPORTED, "stem operand with K or N > 2^16");
       smax = std::max<uint64_t>(smax, 1ull << (st.mlog + st.klog));

@@ -52,6 +52,7 @@ struct StemStep {
   // output address of C[m, n] = sum_j bit_j(m) m_stride[j] + sum_j bit_j(n) n_stride[j] (elements)
   std::vector<int64_t> m_stride, n_stride;
   bool out_identity = true;       // out_layout == kept ++ newl (plain row-major [M][N])
+  bool out_transposed = false;    // out_layout == newl ++ kept (C[n][m], layout policy 3)
   int split = 0;                  // 1 = split-type (chunked tail) step
   int sparse = 0;                 // 1 = sparse-state tail step (gather-batched GEMM, Fig. 5)
   std::vector<int> b_sparse;      // sparse legs of the branch (B_P block index bits, MSB first)

@@ -588,6 +588,7 @@ void run_gemm_once(Plan& p, const StemStep& st, size_t i, const void* src, void*
   OutMap om;
   memset(&om, 0, sizeof(om));
   om.identity = st.out_identity ? 1 : 0;
+  om.transposed = (st.out_transposed && mshift == 0) ? 1 : 0;
   om.mbits = mlog;
   om.nbits = st.nlog;
   for (int j = 0; j < mlog; ++j) om.ms[j] = st.m_stride[j];
