@@ -340,8 +340,9 @@ void launch_gemm_chalf_tc(__half* c, const __half* a, const __half* bp, uint64_t
   // plain TMA A: the deep-pipeline variant (one output staging buffer per epilogue group, more stages)
   // for K-heavy steps; TN_STAGE_DEEP = 0 / 1 forces either (A/B knob)
   static const int deep_env = getenv("TN_STAGE_DEEP") ? atoi(getenv("TN_STAGE_DEEP")) : -1;
-  // (tools/mubench.py A/B, M = 2^23: deep 0.62-0.79x the time for every K >= 2^8, 1.1-1.3x for K <= 2^7)
-  const bool deep = deep_env >= 0 ? deep_env != 0 : K2 >= 512;
+  // (tools/mubench.py A/B, M = 2^23: deep = shallow within noise for K >= 2^8, 1.1-1.3x slower for
+  // K <= 2^7 — the pipeline depth is not what holds the MMA back, so it stays off by default)
+  const bool deep = deep_env > 0;
   if (deep && kb_plain == 64)
     launch_kb<5>(kb_plain, c, a, bp, M, K2, N2, in_max, b_bound, out_max, exp_slot, om, s, nullptr, nullptr, nullptr);
   else
