@@ -42,9 +42,11 @@ WORKLOADS = {
 }
 
 
-# layout policy per plan (tn.h tn_config.layout_policy): identity outputs + permutations fused into the
-# next GEMM's load win everywhere measured (the scatter epilogue, policy 2, was 2.5x slower on C3)
+# layout policy per plan (tn.h tn_config.layout_policy): 3 = identity outputs, transposed C[n][m] TMA
+# stores where they put the next step's contracted modes innermost, permutations fused into the next
+# GEMM's load or passes otherwise (C3: 280 ms vs 325 ms for policy 0 and 2.5x that for policy 2)
 DEFAULT_POLICY = {}
+POLICY_FALLBACK = 3
 
 
 def peaks():
@@ -324,7 +326,7 @@ def main():
     comm = tn.Comm(rank, world, local) if sharded else None
     codec = {"int8": tn.TN_COMM_INT8, "int4": tn.TN_COMM_INT4, "int8_tensor": tn.TN_COMM_INT8_TENSOR}.get(
         args.comm, tn.TN_COMM_FP16)
-    policy = args.policy if args.policy >= 0 else DEFAULT_POLICY.get(args.plan, 0)
+    policy = args.policy if args.policy >= 0 else DEFAULT_POLICY.get(args.plan, POLICY_FALLBACK)
     p = tn.Plan(plan_json, tn.make_config(dtype=tn.TN_CHALF, stem_min_log2=20, comm_codec=codec,
                                           layout_policy=policy, quant_from_pct=args.quant_from_pct), comm=comm)
     info = p.info()

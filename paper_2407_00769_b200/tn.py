@@ -126,7 +126,7 @@ def _stream(stream):
 
 
 def make_config(dtype=TN_CHALF, stem_min_log2=20, comm_codec=TN_COMM_INT8, comm_group=128,
-                stem_capacity_bytes=0, split_log2=0, layout_policy=0, virtual_world=1, quant_from_pct=-1,
+                stem_capacity_bytes=0, split_log2=0, layout_policy=3, virtual_world=1, quant_from_pct=-1,
                 no_gather=0, no_fuse_swap_quant=0, recompute=0):
     c = tn_config()
     c.recompute = recompute
