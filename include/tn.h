@@ -184,8 +184,9 @@ TN_API int tn_split_contract(tn_plan* p, const tn_buffers* b, void* stream);
  * by the accumulated power-of-two exponents (reading C-A8); top_idx (if not NULL) receives the k
  * most probable indices (ties -> smaller index, C-A23).
  * Sparse-state batch (Fig. 5; needs cfg.split_log2 = j > 0): prefixes[i] < 2^j selects a
- * correlated subspace = one value of the j split legs (bit j-1-t of the prefix <-> the t-th entry of
- * "split_modes" in tn_report_json); only those chunks of the tail are contracted.  h_amps receives
+ * correlated subspace = one value of the j split legs (bit j-1-t of the prefix <-> the t-th split leg
+ * in plan order, i.e. in the order the legs appear in `open`; "split_modes" in tn_report_json lists
+ * the legs in chunk order, which depends on the layouts); only those chunks of the tail are contracted.  h_amps receives
  * n_sub blocks of 2^(n_open-j) amplitudes (members = the other open legs in plan order); top_idx
  * receives n_sub*k member indices (post-selection; one rank: k = 1 on the device).
  * Sharded plans: every rank calls it (collective: the result blocks are gathered in rank order into

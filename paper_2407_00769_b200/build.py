@@ -7,7 +7,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libtn.so")
 SOURCES = ["plan.cpp", "k_permute.cu", "k_common.cu", "k_gemm_simt.cu", "k_gemm_tc.cu", "k_gemm_tc_m0.cu",
-           "k_gemm_tc_m1.cu", "k_gemm_tc_m2.cu", "k_gemm_tc_m3.cu", "k_gemm_tc_m4.cu", "k_gemm_tc_m5.cu", "k_quant.cu", "k_select.cu", "runtime.cu"]
+           "k_gemm_tc_m1.cu", "k_gemm_tc_m2.cu", "k_gemm_tc_m3.cu", "k_gemm_tc_m4.cu", "k_gemm_tc_m5.cu", "k_gemm_tc2.cu", "k_quant.cu", "k_select.cu", "runtime.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-gencode", "arch=compute_100a,code=sm_100a",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "--expt-relaxed-constexpr"]

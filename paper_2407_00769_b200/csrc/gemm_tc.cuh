@@ -934,11 +934,12 @@ static CUtensorMap make_map_2d(const void* base, uint64_t inner, uint64_t outer,
 }
 
 // C^T [N complex][M complex] as 4-byte elements (one complex-half value each), box {128 m, 32 n}
+// (N < 32: {128 m, N n}, the tile's single n block)
 static CUtensorMap make_map_t(const void* base, uint64_t M, uint64_t N) {
   CUtensorMap m;
   cuuint64_t dims[2] = {M, N};
   cuuint64_t strides[1] = {M * 4};
-  cuuint32_t box[2] = {(cuuint32_t)tc::BM, 32};
+  cuuint32_t box[2] = {(cuuint32_t)tc::BM, (cuuint32_t)std::min<uint64_t>(N, 32)};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = get_encode()(&m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<void*>(base), dims, strides, box, estr,
                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -987,6 +988,12 @@ static CUtensorMap make_map_nd(const void* base, const NdPlan& np) {
   if (r != CUDA_SUCCESS) throw TnError{TN_E_CUDA, "cuTensorMapEncodeTiled (N-d gather) failed (" + std::to_string((int)r) + ")"};
   return m;
 }
+
+// CTA-pair variant (gemm_tc2.cuh, k_gemm_tc2.cu)
+bool tc2_enabled();
+void launch_tc2(int BN, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, uint32_t num_mp,
+                uint32_t num_n, int K2, const float* in_max, const float* b_bound, uint32_t* out_max, int* exp_slot,
+                int epi, uint64_t m_base, cudaStream_t s);
 
 template <int BN, int KB, int G>
 static void launch_bn(__half* c, const __half* a, const __half* bp, uint64_t M, uint32_t K2, uint32_t N2_real,
@@ -1042,8 +1049,10 @@ static void launch_bn(__half* c, const __half* a, const __half* bp, uint64_t M, 
   memset(&sa, 0, sizeof(sa));
   const uint32_t n_cols = N2_real / 2;
   // transposed output C[n][m] (layout policy 3): TMA stores of [32 n][128 m] boxes of a C^T map when
-  // the tile geometry allows (whole 128-row tiles, whole 64-column subtiles), else the scatter path
-  const bool transposed = om && om->transposed && M % tc::BM == 0 && N2_real % 64 == 0 && M < (1ull << 31) &&
+  // the tile geometry allows (whole 128-row tiles; whole 64-column subtiles, or N = 8 / 16 complex
+  // columns in one tile and one narrower box), else the scatter path
+  const bool transposed = om && om->transposed && M % tc::BM == 0 &&
+                          (N2_real % 64 == 0 || N2_real == 16 || N2_real == 32) && M < (1ull << 31) &&
                           !getenv("TN_NO_TSTORE");
   OutMap ident;
   static const bool direct_env = getenv("TN_DIRECT_EPI") != nullptr;  // experiment knob
@@ -1135,6 +1144,21 @@ static void launch_bn(__half* c, const __half* a, const __half* bp, uint64_t M, 
   // TMA coordinates are int32: process M in chunks of at most 2^30 rows
   const uint32_t num_n = N2 / BN;
   const uint64_t chunk = std::min<uint64_t>(1ull << 30, ((1ull << 31) / num_n) * tc::BM);
+  if constexpr (G == 0 && KB == 64 && BN >= 128) {
+    // plain A, row-major or transposed output, whole 256-row pair tiles: the CTA-pair kernel (half
+    // the B tile staged per SM: fewer shared-memory bytes per MAC on the compute-bound steps)
+    if (!np && !sa.on && epi_stg == 0 && M % 256 == 0 && N2_real % BN == 0 && chunk % 256 == 0 && tc2_enabled()) {
+      CUtensorMap mb2 = make_map_2d(bp, K2, N2_real, KB, BN / 2);
+      for (uint64_t m_off = 0; m_off < M; m_off += chunk) {
+        const uint64_t mm = std::min<uint64_t>(chunk, M - m_off);
+        CUtensorMap ma = make_map_2d(a + m_off * K2, K2, mm, KB, tc::BM);
+        CUtensorMap mc = transposed ? make_map_t(c, M, N2_real / 2) : make_map_2d(c + m_off * N2, N2, mm, 64, tc::BM);
+        launch_tc2(BN, ma, mb2, mc, (uint32_t)(mm / 256), num_n, (int)K2, in_max, b_bound, out_max,
+                   m_off ? nullptr : exp_slot, transposed ? 4 : 0, m_off, s);
+      }
+      return;
+    }
+  }
   for (uint64_t m_off = 0; m_off < M; m_off += chunk) {
     uint64_t mm = std::min<uint64_t>(chunk, M - m_off);
     // (cp.async gather: the A map is unused; N-d: the whole stem, coordinates from the global row)

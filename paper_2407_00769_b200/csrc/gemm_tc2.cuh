@@ -1,0 +1,286 @@
+// CTA-pair (cta_group::2) variant of the complex-half stem GEMM (gemm_tc.cuh), for the steps whose
+// A operand is plain (stored order, no fused gather) and whose output is row-major or transposed.
+//
+// Same operation (Eq. 6: C = A_real x B_P in fp16 with fp32 accumulation and an
+// exact power-of-two output scale, readings C-A7/C-A8); what changes is the tile shape.  A cluster
+// of two CTAs on neighbouring SMs computes one 256 x BN tile with tcgen05.mma.cta_group::2: each CTA
+// stages its own 128 rows of A and HALF of the B tile (BN/2 rows), and the leader's MMA reads both
+// CTAs' shared memory.  Per SM and per k block that is 128 x 64 (A) + BN/2 x 64 (B) staged bytes for
+// 128 x BN x 64 MACs, instead of 128 x 64 + BN x 64 for the single-CTA tile: 1/3 fewer bytes through
+// TMA and shared memory per MAC at BN = 256.  Shared-memory traffic (TMA writes + UMMA reads), not
+// the tensor pipe, is what held the single-CTA kernel near 62 % of the measured fp16 peak on the
+// compute-bound steps.
+//
+// Roles (384 threads per CTA, both CTAs):
+//   warp 0   : TMA producer for this CTA's halves; the loads complete on the LEADER's full barrier
+//              (.cta_group::2 form), whose expected byte count the leader posts for both CTAs
+//   warp 1   : (leader only) MMA issuer; tcgen05.commit multicasts to both CTAs' empty / tfull
+//   warp 2   : TMEM allocator (cta_group::2, both CTAs)
+//   warps 4-11: epilogue, two warpgroups alternating tiles, each CTA drains its own 128 TMEM lanes
+//              (= its 128 rows) and tells the leader through a remote mbarrier arrive
+#pragma once
+#include "gemm_tc.cuh"
+
+namespace tn {
+namespace tc2 {
+
+using namespace tc;
+
+template <int BN>
+struct Cfg2 {
+  static constexpr int KB = 64;
+  static constexpr int kABytes = BM * KB * 2;        // this CTA's 128 rows of A
+  static constexpr int kBBytes = (BN / 2) * KB * 2;  // this CTA's half of the B tile
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kNBuf = 2;                    // 64-column staging buffers per epilogue group
+  static constexpr int kCBytes = 2 * kNBuf * BM * 128;
+  static constexpr int kTable = 1024;                // barriers + TMEM slot
+  static constexpr int kMaxSmem = 232448;
+  static constexpr int kStagesRaw = (kMaxSmem - 1024 - kTable - kCBytes) / kStageBytes;
+  static constexpr int kStages = kStagesRaw > 16 ? 16 : kStagesRaw;
+  static constexpr int kStageArea = (kStages * kStageBytes + 1023) / 1024 * 1024;
+  static constexpr int kSmem = kStageArea + kCBytes + 1024 + kTable;
+  static_assert(kSmem <= kMaxSmem, "shared memory budget");
+  static_assert(kStages >= 3, "pipeline depth");
+  static constexpr int kNAcc = 512 / BN;
+  // M = 256 (the pair), N = BN, fp16 x fp16 -> fp32, both K-major
+  static constexpr uint32_t kIdesc = (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+};
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+// shared::cluster address of the same shared-memory object in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t map_rank(const void* p, uint32_t rank) {
+  uint32_t out;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(out) : "r"(smem_u32(p)), "r"(rank));
+  return out;
+}
+
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// TMA tile load into this CTA's shared memory whose completion is signalled on an mbarrier that may
+// live in the peer CTA (the leader's full barrier)
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, uint32_t bar_cluster, int c0,
+                                                 int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar_cluster)
+      : "memory");
+}
+
+__device__ __forceinline__ void mma_f16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                             uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+// arrive (once) on the mbarrier at this offset in both CTAs of the pair when the leader's
+// previously issued MMAs have completed
+__device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)0x3)
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
+}
+
+// epi: 0 = row-major C tile [128 rows][64-column subtiles] (TMA store box {64, 128}),
+//      4 = transposed C^T (layout policy 3, box {128 m, 32 n} at global row m_base + m0)
+template <int BN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    gemm_chalf_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                          const __grid_constant__ CUtensorMap tmC, uint32_t num_mp, uint32_t num_n, int K2,
+                          const float* in_max, const float* b_bound, uint32_t* out_max, int* exp_slot, int epi,
+                          uint64_t m_base) {
+  using C = Cfg2<BN>;
+  constexpr int KB = C::KB;
+  // "no re-run needed" signal of the scale re-run: both CTAs read the same value and leave together
+  if (in_max && in_max[0] < 0.f) return;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  unsigned char* sA = smem;
+  unsigned char* sB = smem + C::kStages * C::kABytes;
+  unsigned char* sC = smem + C::kStageArea;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sC + C::kCBytes);
+  uint64_t* empty = full + C::kStages;
+  uint64_t* tfull = empty + C::kStages;
+  uint64_t* tempty = tfull + C::kNAcc;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + C::kNAcc);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const uint32_t pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const uint32_t num_tiles = num_mp * num_n;
+  const int num_k = (K2 + KB - 1) / KB;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < C::kStages; ++s) {
+      mbar_init(&full[s], 1);   // leader: its own arrive.expect_tx (bytes of both CTAs)
+      mbar_init(&empty[s], 1);  // one multicast commit per use
+    }
+    for (int a = 0; a < C::kNAcc; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 2);  // leader: one arrive per CTA's epilogue group
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmC)) : "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync();  // barriers initialised and TMEM allocated in both CTAs
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ===== TMA producer (both CTAs): this CTA's A rows and B half, completing on the leader =====
+      int s = 0;
+      uint32_t ph = 0;
+      for (uint32_t t = pair; t < num_tiles; t += npairs) {
+        const int mp = (int)(t / num_n), nb = (int)(t % num_n);
+        const int a_row = mp * 256 + (int)rank * BM;
+        const int b_row = nb * BN + (int)rank * (BN / 2);
+        for (int kb = 0; kb < num_k; ++kb) {
+          mbar_wait(&empty[s], ph ^ 1);
+          if (rank == 0) mbar_expect_tx(&full[s], 2 * C::kStageBytes);
+          const uint32_t fb = map_rank(&full[s], 0);
+          tma_load_2d_pair(sA + s * C::kABytes, &tmA, fb, kb * KB, a_row);
+          tma_load_2d_pair(sB + s * C::kBBytes, &tmB, fb, kb * KB, b_row);
+          if (++s == C::kStages) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      // ===== MMA issuer (leader): M = 256 over both CTAs' A rows, N = BN over both B halves =====
+      int s = 0;
+      uint32_t ph = 0;
+      uint32_t i = 0;
+      for (uint32_t t = pair; t < num_tiles; t += npairs, ++i) {
+        const uint32_t acc = i % C::kNAcc, aph = (i / C::kNAcc) & 1;
+        mbar_wait(&tempty[acc], aph ^ 1);
+        tc_fence_after();
+        const uint32_t tmem_d = tmem_base + acc * BN;
+        for (int kb = 0; kb < num_k; ++kb) {
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          const uint64_t ad = smem_desc_sw<KB>(sA + s * C::kABytes);
+          const uint64_t bd = smem_desc_sw<KB>(sB + s * C::kBBytes);
+#pragma unroll
+          for (int kk = 0; kk < KB / 16; ++kk) mma_f16_pair(tmem_d, ad + 2 * kk, bd + 2 * kk, C::kIdesc, (kb | kk) != 0);
+          mma_commit_pair(&empty[s]);
+          if (++s == C::kStages) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+        mma_commit_pair(&tfull[acc]);
+      }
+    }
+  } else if (warp >= 4) {
+    // ===== epilogue (both CTAs): TMEM lanes = this CTA's 128 rows of the pair tile =====
+    const int grp = (warp - 4) >> 2;
+    const int ew = warp & 3;
+    const int row = ew * 32 + lane;
+    const int etid = threadIdx.x - 128 - 128 * grp;
+    unsigned char* sCg = sC + grp * (C::kNBuf * BM * 128);
+    int e = 0;
+    if (in_max && b_bound) e = scale_exp_for(in_max[0] * b_bound[0]);
+    if (exp_slot && blockIdx.x == 0 && grp == 0 && etid == 0) *exp_slot = e;
+    const float sc = ldexpf(1.f, e);
+    float mx = 0.f;
+    uint32_t gsub = 0;
+    for (uint32_t t = pair + grp * npairs, i = grp; t < num_tiles; t += 2 * npairs, i += 2) {
+      const uint32_t acc = i % C::kNAcc, aph = (i / C::kNAcc) & 1;
+      const int m0 = (int)(t / num_n) * 256 + (int)rank * BM, n0 = (int)(t % num_n) * BN;
+      mbar_wait(&tfull[acc], aph);
+      tc_fence_after();
+      const uint32_t taddr = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN;
+#pragma unroll 1
+      for (int sub = 0; sub < BN; sub += 64, ++gsub) {
+        unsigned char* sbuf = sCg + (gsub % C::kNBuf) * (BM * 128);
+        if (etid == 0) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(C::kNBuf - 1) : "memory");
+        named_bar(1 + grp, 128);
+        uint32_t r[2][32];
+        tmem_ld_32x32b_x32(taddr + sub, r[0]);
+        tmem_ld_32x32b_x32(taddr + sub + 32, r[1]);
+        tmem_ld_wait();
+        if (sub + 64 >= BN) {
+          // this CTA's half of the accumulator drained: tell the leader's MMA (one arrive per group)
+          tc_fence_before();
+          named_bar(1 + grp, 128);
+          if (etid == 0) mbar_arrive_cluster(map_rank(&tempty[acc], 0));
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int c = sub + 32 * h;
+          uint32_t pk[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const float x0 = __uint_as_float(r[h][2 * j]) * sc, x1 = __uint_as_float(r[h][2 * j + 1]) * sc;
+            __half2 hv = __floats2half2_rn(x0, x1);
+            mx = fmaxf(mx, fmaxf(fabsf(x0), fabsf(x1)));
+            pk[j] = *reinterpret_cast<uint32_t*>(&hv);
+          }
+          if (epi == 4) {
+            uint32_t* st32 = reinterpret_cast<uint32_t*>(sbuf);
+            const int q0 = (c & 63) >> 1;
+#pragma unroll
+            for (int j = 0; j < 16; ++j) st32[(q0 + j) * BM + row] = pk[j];
+          } else {
+            unsigned char* srow = sbuf + row * 128;
+            const int cb = (c & 63) >> 3;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const int chunk = (cb + q) ^ (row & 7);
+              *reinterpret_cast<uint4*>(srow + chunk * 16) = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+            }
+          }
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        named_bar(1 + grp, 128);
+        if (etid == 0) {
+          if (epi == 4)
+            tma_store_2d(&tmC, sbuf, (int)(m_base + (uint64_t)m0), (n0 + sub) >> 1);
+          else
+            tma_store_2d(&tmC, sbuf, n0 + sub, m0);
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+      }
+    }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (out_max && lane == 0) atomicMax(out_max, __float_as_uint(mx));
+  }
+  // neither CTA leaves (or frees TMEM) while the pair may still signal its barriers or write its TMEM
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
+}
+
+}  // namespace tc2
+}  // namespace tn

@@ -1413,7 +1413,22 @@ int tn_sample_amplitudes(tn_plan* h, const tn_buffers* b, const uint64_t* prefix
       return TN_OK;
     }
     if (prefixes) {
-      std::vector<uint64_t> ids(prefixes, prefixes + n_sub);
+      // prefix bits follow the split legs in `open` order (plan order), whatever order the lowering
+      // gave the chunks (split_modes: layout-, policy- and world-dependent): prefix -> chunk id
+      const int j = (int)p.split_modes.size();
+      std::vector<int> canon;
+      for (int l : p.open)
+        if (std::find(p.split_modes.begin(), p.split_modes.end(), l) != p.split_modes.end()) canon.push_back(l);
+      std::vector<uint64_t> ids(n_sub);
+      for (size_t i = 0; i < n_sub; ++i) {
+        if (j < 64 && (prefixes[i] >> j) != 0) throw TnError{TN_E_INVALID, "prefix out of range"};
+        uint64_t v = 0;
+        for (int t = 0; t < j; ++t) {
+          const int c = (int)(std::find(canon.begin(), canon.end(), p.split_modes[t]) - canon.begin());
+          v = (v << 1) | ((prefixes[i] >> (j - 1 - c)) & 1);
+        }
+        ids[i] = v;
+      }
       read_result(p, b, s, &ids, h_amps, k, top_idx);
       return TN_OK;
     }

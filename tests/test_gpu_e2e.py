@@ -55,7 +55,7 @@ def test_c1_full_state_vs_oracle(tn, dtype, stem_min, policy):
 
 @pytest.mark.parametrize("seed", range(6))
 @pytest.mark.parametrize("dtype", [0, 1])
-@pytest.mark.parametrize("policy", [0, 1, 2])
+@pytest.mark.parametrize("policy", [0, 1, 2, 3])
 def test_random_small_circuits_sliced(tn, seed, dtype, policy):
     """Seeded small circuits with extra sliced edges: every slice vs the oracle slice, and the
     GPU sum over slices vs the unsliced oracle (slicing identity)."""
@@ -157,11 +157,12 @@ def test_graph_replay_across_slices(tn, dtype):
 def test_fused_permutation_matches_permute_pass(tn, dtype):
     """Gathered-A GEMMs (permutation fused into the load) vs explicit permutation passes on the
     same plan: same operands, same K order, same accumulation -> bit-identical amplitudes; and the
-    oracle within tolerance."""
+    oracle within tolerance.  (Layout policy 0: under policy 3 the output layouts, and so the K
+    orders, depend on which steps can gather.)"""
     sub = MP.sub_slice(_plan("c2"), 22)
     out = {}
     for ng in (0, 1):
-        p = tn.Plan(sub, tn.make_config(dtype=dtype, stem_min_log2=12, no_gather=ng))
+        p = tn.Plan(sub, tn.make_config(dtype=dtype, stem_min_log2=12, no_gather=ng, layout_policy=0))
         rep = p.report()
         out[ng] = (tn.contract(p, tn.Buffers(p), 0), sum(s["ga"] for s in rep["steps"]), p.info()["n_permutes"])
     assert out[0][1] >= 1 and out[1][1] == 0 and out[0][2] < out[1][2]
@@ -272,7 +273,9 @@ def test_recompute_on_halves_full_c3(tn):
 
 @pytest.mark.parametrize("dtype", [0, 1])
 def test_recompute_on_halves_vs_oracle(tn, dtype):
-    """C2 sub-slice: recomputed halves vs the oracle, and complex64 bit-identical to no recompute."""
+    """C2 sub-slice: recomputed halves vs the oracle, and complex64 bit-identical to no recompute
+    (layout policy 0 for that: policy 3 picks transposed outputs only before the tail, which
+    recomputation moves, so the two plans' K orders differ)."""
     sub = MP.sub_slice(_plan("c2"), 22)
     ref = contract.contract(load(sub), 0)
     p = tn.Plan(sub, tn.make_config(dtype=dtype, stem_min_log2=12, recompute=1))
@@ -280,7 +283,9 @@ def test_recompute_on_halves_vs_oracle(tn, dtype):
     got = tn.contract(p, tn.Buffers(p), 0)
     assert metrics.rel_l2(got, ref) <= TOL[dtype]
     if dtype == 1:
-        p0 = tn.Plan(sub, tn.make_config(dtype=1, stem_min_log2=12))
+        p = tn.Plan(sub, tn.make_config(dtype=1, stem_min_log2=12, recompute=1, layout_policy=0))
+        got = tn.contract(p, tn.Buffers(p), 0)
+        p0 = tn.Plan(sub, tn.make_config(dtype=1, stem_min_log2=12, layout_policy=0))
         assert np.array_equal(tn.contract(p0, tn.Buffers(p0), 0), got)
 
 

@@ -82,7 +82,11 @@ def _half_pairs(z):
 @pytest.mark.parametrize("M,K,N", [(1, 8, 8), (128, 8, 8), (300, 16, 8), (1000, 8, 32), (4096 + 37, 32, 64),
                                    (777, 64, 128), (2048, 128, 256), (513, 256, 16), (1024, 512, 512),
                                    (256, 2048, 8), (640, 8, 1024), (1000, 4, 64), (5000, 16, 4),
-                                   (3000, 8, 2), (129, 4, 256), (4100, 16, 256)])
+                                   (3000, 8, 2), (129, 4, 256), (4100, 16, 256),
+                                   # CTA-pair kernel (M % 256 == 0, 2N >= 128, 2K >= 64): single k block,
+                                   # BN = 128 and 256, more pair tiles than resident pairs
+                                   (512, 32, 64), (256, 64, 128), (1536, 32, 512), (65536, 64, 128),
+                                   (16384, 256, 256)])
 def test_gemm_chalf_tensor_core_vs_oracle(env, M, K, N):
     """tcgen05 Eq. 6 GEMM (no scaling) vs the oracle's real-embedding GEMM in fp64 on the same
     fp16 operands.  Error: one fp16 rounding of C (2^-11 relative) + fp32 accumulation."""
@@ -163,12 +167,13 @@ def test_gemm_chalf_rows_bulk_ring_wrap(env, K, N, M):
     assert np.array_equal(got[..., 0], ref.real) and np.array_equal(got[..., 1], ref.imag)
 
 
-def test_pad_b_and_scaled_gemm(env):
+@pytest.mark.parametrize("M", [3000, 4096])
+def test_pad_b_and_scaled_gemm(env, M):
     """Eq. 6 padding on the device (scale 2^t by the C-A8 rule) vs the oracle's pad_b, then the
-    scaled GEMM: exponent recorded, |C| <= 2^14, out_max = max|C|."""
+    scaled GEMM: exponent recorded, |C| <= 2^14, out_max = max|C| (M = 4096: the CTA-pair kernel)."""
     torch, tn = env
     rng = np.random.default_rng(9)
-    K, N, M = 64, 128, 3000
+    K, N = 64, 128
     b = ((rng.standard_normal((K, N)) + 1j * rng.standard_normal((K, N))) * 1e-3).astype(np.complex64)
     B = torch.from_numpy(b.view(np.float32).reshape(-1)).cuda()
     BP = torch.empty(4 * K * N, dtype=torch.float16, device="cuda")

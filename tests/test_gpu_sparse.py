@@ -27,7 +27,9 @@ def tn():
 
 
 def _blocks(ref, open_labels, split_modes):
-    """oracle full-state array [open...] -> [prefix (split_modes order), members (open order)]"""
+    """oracle full-state array [open...] -> [prefix (split legs in open order, include/tn.h), members
+    (open order)]"""
+    split_modes = [l for l in open_labels if l in split_modes]
     rest = [l for l in open_labels if l not in split_modes]
     t = np.transpose(ref, [open_labels.index(l) for l in split_modes + rest])
     return t.reshape(2 ** len(split_modes), -1)
