@@ -413,6 +413,10 @@ def main():
     flops = info["stem_flops"] * world
     value = flops / (t_ms * 1e-3) / 1e12
     hbm, tc_burst, tc_sus, src = peaks()
+    # the GEMMs run inside a step of hundreds of ms under the 1000 W cap: the SUSTAINED tensor peak
+    # (MEASURED_PEAKS bf16_tflops_sustained, cuBLAS back to back for 4 s) is the roofline denominator
+    # (B200_PROFILING: burst for a kernel timed alone, sustained inside a long step); burst reported beside
+    tc_peak = tc_sus
 
     # ---- roofline of the dominant kernel (from the timed region's CUDA events, mean over the K steps)
     ms = [x / args.steps for x in ms_sum] if ms_sum else []
@@ -429,7 +433,7 @@ def main():
         fl = 8 * M * K * N
         gemm_bytes += by
         gemm_flops += fl
-        t_roof_gemm += max(by / (hbm * 1e9), fl / (tc_burst * 1e12)) * 1e3
+        t_roof_gemm += max(by / (hbm * 1e9), fl / (tc_peak * 1e12)) * 1e3
         if st["perm"]:
             perm_bytes += 2 * eb * M * K
     final_ms = ms[-1] if ms else 0.0
@@ -438,16 +442,17 @@ def main():
         perm_bytes += 2 * eb * 2.0 ** len(rep["final_layout"])
     common_ms = ms[0] if ms else 0.0
     if gemm_ms >= perm_ms:
-        bytes_bound = gemm_bytes / (hbm * 1e9) >= gemm_flops / (tc_burst * 1e12)
+        bytes_bound = gemm_bytes / (hbm * 1e9) >= gemm_flops / (tc_peak * 1e12)
         if bytes_bound:
             ach = gemm_bytes / (gemm_ms * 1e-3) / 1e9
             roof = {"kernel": "gemm_chalf_tc (+simt small-K/N steps)", "bound": "hbm", "achieved": ach, "peak": hbm,
                     "unit": "GB/s", "frac": ach / hbm}
         else:
             ach = gemm_flops / (gemm_ms * 1e-3) / 1e12
-            roof = {"kernel": "gemm_chalf_tc", "bound": "tensor", "achieved": ach, "peak": tc_burst,
-                    "unit": "TFLOP/s", "frac": ach / tc_burst, "peak_sustained": tc_sus,
-                    "frac_sustained": ach / tc_sus, "peak_spec": 2250.0, "frac_spec": ach / 2250.0}
+            roof = {"kernel": "gemm_chalf_tc", "bound": "tensor", "achieved": ach, "peak": tc_peak,
+                    "unit": "TFLOP/s", "frac": ach / tc_peak, "peak_kind": "sustained (kernel inside a long step)",
+                    "peak_burst": tc_burst, "frac_burst": ach / tc_burst, "peak_spec": 2250.0,
+                    "frac_spec": ach / 2250.0}
         roof["roofline_time_frac"] = t_roof_gemm / gemm_ms if gemm_ms else None
         roof["launches_per_step"] = len(steps)
     else:
@@ -472,14 +477,14 @@ def main():
     shape_hist = {}
     for st in steps:
         M, K, N = 2.0 ** st["m"], 2.0 ** st["k"], 2.0 ** st["n"]
-        t_roof_path += max(8 * M * K * N / (tc_burst * 1e12), (4 * (M * K + M * N) + 8 * K * N) / (hbm * 1e9)) * 1e3
+        t_roof_path += max(8 * M * K * N / (tc_peak * 1e12), (4 * (M * K + M * N) + 8 * K * N) / (hbm * 1e9)) * 1e3
         kn = st["k"] + st["n"]
         shape_hist[kn] = shape_hist.get(kn, 0) + 1
     path_roof = {"roofline_ms": t_roof_path, "frac": t_roof_path / t_ms,
-                 "peaks": f"{tc_burst:.0f} TF/s burst, {hbm:.0f} GB/s ({src})",
+                 "peaks": f"{tc_peak:.0f} TF/s sustained, {hbm:.0f} GB/s ({src})",
                  "log2_KN_histogram": {str(k): shape_hist[k] for k in sorted(shape_hist)},
                  "tensor_bound_steps": sum(1 for st in steps if 2 * 2.0 ** (st["k"] + st["n"]) /
-                                           (2.0 ** st["k"] + 2.0 ** st["n"]) > tc_burst * 1e3 / hbm)}
+                                           (2.0 ** st["k"] + 2.0 ** st["n"]) > tc_peak * 1e3 / hbm)}
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "TFLOPS", "n_gpus": world, "steps": args.steps,

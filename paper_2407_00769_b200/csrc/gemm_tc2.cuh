@@ -98,6 +98,24 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
 }
 
+// Pair tile i of this cluster -> (m-pair, n-block); false past the end.  order 0: tile t = pair + i *
+// npairs, n fastest (clusters with neighbouring ids share the A rows).  order 1: each cluster runs every
+// n-block of its own m-pairs in turn, so the re-reads of its A rows stay in its own die's L2 (with order 0
+// the clusters sharing an m-pair can sit on both dies: ncu showed 2.3x the A bytes from DRAM at K = N = 2^10).
+__device__ __forceinline__ bool tc2_tile(uint32_t i, uint32_t pair, uint32_t npairs, uint32_t num_mp,
+                                         uint32_t num_n, int order, int& mp, int& nb) {
+  if (order == 1) {
+    const uint32_t m = pair + (i / num_n) * npairs;
+    mp = (int)m;
+    nb = (int)(i % num_n);
+    return m < num_mp;
+  }
+  const uint64_t t = (uint64_t)pair + (uint64_t)i * npairs;
+  mp = (int)(t / num_n);
+  nb = (int)(t % num_n);
+  return t < (uint64_t)num_mp * num_n;
+}
+
 // epi: 0 = row-major C tile [128 rows][64-column subtiles] (TMA store box {64, 128}),
 //      4 = transposed C^T (layout policy 3, box {128 m, 32 n} at global row m_base + m0)
 template <int BN>
@@ -105,7 +123,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     gemm_chalf_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                           const __grid_constant__ CUtensorMap tmC, uint32_t num_mp, uint32_t num_n, int K2,
                           const float* in_max, const float* b_bound, uint32_t* out_max, int* exp_slot, int epi,
-                          uint64_t m_base) {
+                          uint64_t m_base, int order) {
   using C = Cfg2<BN>;
   constexpr int KB = C::KB;
   // "no re-run needed" signal of the scale re-run: both CTAs read the same value and leave together
@@ -124,7 +142,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
   const uint32_t pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
-  const uint32_t num_tiles = num_mp * num_n;
   const int num_k = (K2 + KB - 1) / KB;
 
   if (warp == 0 && lane == 0) {
@@ -155,8 +172,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       // ===== TMA producer (both CTAs): this CTA's A rows and B half, completing on the leader =====
       int s = 0;
       uint32_t ph = 0;
-      for (uint32_t t = pair; t < num_tiles; t += npairs) {
-        const int mp = (int)(t / num_n), nb = (int)(t % num_n);
+      int mp, nb;
+      for (uint32_t i = 0; tc2_tile(i, pair, npairs, num_mp, num_n, order, mp, nb); ++i) {
         const int a_row = mp * 256 + (int)rank * BM;
         const int b_row = nb * BN + (int)rank * (BN / 2);
         for (int kb = 0; kb < num_k; ++kb) {
@@ -177,8 +194,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       // ===== MMA issuer (leader): M = 256 over both CTAs' A rows, N = BN over both B halves =====
       int s = 0;
       uint32_t ph = 0;
-      uint32_t i = 0;
-      for (uint32_t t = pair; t < num_tiles; t += npairs, ++i) {
+      int mp, nb;
+      for (uint32_t i = 0; tc2_tile(i, pair, npairs, num_mp, num_n, order, mp, nb); ++i) {
         const uint32_t acc = i % C::kNAcc, aph = (i / C::kNAcc) & 1;
         mbar_wait(&tempty[acc], aph ^ 1);
         tc_fence_after();
@@ -212,9 +229,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const float sc = ldexpf(1.f, e);
     float mx = 0.f;
     uint32_t gsub = 0;
-    for (uint32_t t = pair + grp * npairs, i = grp; t < num_tiles; t += 2 * npairs, i += 2) {
+    int mp, nb;
+    for (uint32_t i = grp; tc2_tile(i, pair, npairs, num_mp, num_n, order, mp, nb); i += 2) {
       const uint32_t acc = i % C::kNAcc, aph = (i / C::kNAcc) & 1;
-      const int m0 = (int)(t / num_n) * 256 + (int)rank * BM, n0 = (int)(t % num_n) * BN;
+      const int m0 = mp * 256 + (int)rank * BM, n0 = nb * BN;
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
       const uint32_t taddr = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN;

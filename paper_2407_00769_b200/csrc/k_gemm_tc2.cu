@@ -40,9 +40,14 @@ static void launch_tc2_t(const CUtensorMap& ma, const CUtensorMap& mb, const CUt
   }
   const uint64_t tiles = (uint64_t)num_mp * num_n;
   if (tiles == 0) return;
-  const int grid = 2 * (int)std::min<uint64_t>(tiles, (uint64_t)pairs);
+  // tile order (tc2_tile): per-cluster m-pairs when there are enough of them to keep every cluster
+  // busy; TN_TC2_ORDER = 0 / 1 forces either (A/B knob)
+  static const int order_env = getenv("TN_TC2_ORDER") ? atoi(getenv("TN_TC2_ORDER")) : -1;
+  const int order = order_env >= 0 ? order_env : (num_mp >= 8ull * (uint64_t)pairs ? 1 : 0);
+  const uint64_t busy = order == 1 ? std::min<uint64_t>(num_mp, (uint64_t)pairs) : std::min<uint64_t>(tiles, (uint64_t)pairs);
+  const int grid = 2 * (int)busy;
   tc2::gemm_chalf_tc2_kernel<BN><<<grid, tc::kThreads, C::kSmem, s>>>(ma, mb, mc, num_mp, num_n, K2, in_max, b_bound,
-                                                                      out_max, exp_slot, epi, m_base);
+                                                                      out_max, exp_slot, epi, m_base, order);
   TN_CUDA(cudaGetLastError());
 }
 

@@ -160,7 +160,10 @@ def test_loopback_split_tail_sharded(tn, world, split):
 
 
 def test_loopback_sparse_batch_sharded(tn):
-    """Sparse-state batch with a sharded stem: same subspaces and picks as one GPU."""
+    """Sparse-state batch with a sharded stem: same subspaces (prefixes in plan order, include/tn.h)
+    and picks as one GPU.  The two lowerings differ (split point, tail layouts), so the fp32 sums
+    run in different orders before the fp16 roundings: within the fp16 bound of the other
+    sharded-vs-one-GPU tests, not bit-identical."""
     plan = MP.sub_slice(_plan("c2"), 20)
     kw = dict(dtype=0, stem_min_log2=12, split_log2=3, comm_codec=tn.TN_COMM_FP16)
     pre = np.array([3, 0, 7, 5], dtype=np.uint64)
@@ -171,7 +174,7 @@ def test_loopback_sparse_batch_sharded(tn):
     a1, t1 = tn.tn_sample_sparse(p1, b1, pre, k=1)
     out = run_loopback(tn, plan, 2, kw, sparse=pre)
     a2, t2 = out[0][0]
-    assert metrics.rel_l2(a2, a1) <= 1e-6
+    assert metrics.rel_l2(a2, a1) <= 1e-2
     pr = np.abs(a1) ** 2
     for i in range(len(pre)):
         assert pr[i, int(t2[i, 0])] >= (1 - 4e-2) * pr[i].max()
