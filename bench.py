@@ -494,7 +494,7 @@ def main():
                 "config": {"workload": WORKLOADS.get(args.plan, args.plan), "plan": f"plans/{args.plan}.json",
                            "slice": ("slice 0 sharded over all ranks (C4), swaps: " + args.comm) if sharded else
                                     "rank r runs slice r (replicas over independent subtasks)",
-                           "mode_swaps": rep.get("n_swaps", 0), "swap_bytes_per_rank": rep.get("swap_bytes", 0),
+                           "mode_swaps": rep.get("n_swaps", 0), "epilogue_swaps": rep.get("n_fused_swaps", 0), "swap_bytes_per_rank": rep.get("swap_bytes", 0),
                            "stem_steps": info["n_stem_steps"], "permutes": info["n_permutes"],
                            "max_stem_log2": info["max_stem_log2"], "stem_flops": flops,
                            "layout_policy": policy,

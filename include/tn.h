@@ -110,7 +110,13 @@ typedef struct {
                                 largest tensor lies in the recomputed region.  Needs split_log2 = 0;
                                 no mode swap may fall into the recomputed region ("there is no data
                                 communication").  0: off */
-  int32_t reserved;
+  int32_t no_fused_swap;     /* 0 (default): an fp16 mode swap right after a tcgen05 GEMM step is
+                                done by that GEMM's epilogue — each output tile is TMA-stored
+                                straight into the buffer of the rank that owns it after the swap
+                                (NVLink peer memory: CUDA IPC between processes, plain pointers
+                                between loopback ranks), when the swapped modes are tile-constant
+                                (m bits >= 7, n bits >= 5); bit-identical to the exchange.
+                                1: every swap through the transport (NCCL send/recv) */
 } tn_config;
 
 /* Caller-owned device buffers lent to a call (P:18-22 double buffering). */

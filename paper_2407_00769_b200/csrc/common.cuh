@@ -68,11 +68,26 @@ struct GatherArgs {
 // Output address map of a stem GEMM: C[m, n] lives at
 //   sum_j bit_j(m) * ms[j] + sum_j bit_j(n) * ns[j]   (complex elements)
 // identity != 0 means plain row-major [M][N] (ms[j] = N << j, ns[j] = 1 << j).
+// Mode swap done by the epilogue of the GEMM before it (Alg. 1; runtime.cu
+// fused_swap_target): output element C[m, n] belongs to swap member v, formed from nsw of its
+// coordinate bits (is_n[t] ? bit bit[t] of the complex column n : bit bit[t] of the row m, giving
+// bit vbit[t] of v), and is stored at base[v] — member v's rank's receive buffer, at this rank's
+// chunk — at the coordinates with those bits removed.  The launcher honours it only for TMA-store
+// epilogues whose store boxes keep the member bits constant (m bits >= 7, n bits >= 5) and sets
+// honored; otherwise it stores locally and the runtime exchanges through the transport.
+struct PeerTarget {
+  int nsw;
+  int is_n[3], bit[3], vbit[3];
+  void* base[8];
+  int honored;
+};
+
 struct OutMap {
   int mbits, nbits, identity;
   int transposed;                // C[n][m]: n outermost, m innermost (ns[j] = M << j, ms[j] = 1 << j)
   int64_t ms[kMaxModes];
   int64_t ns[24];
+  PeerTarget* peer;              // host only (nullptr: local output)
 };
 
 struct PermArgs {

@@ -315,7 +315,42 @@ struct BatchArgs {
   uint32_t b_rows;    // rows of one B_P block
 };
 
+// Kernel-side form of a PeerTarget (common.cuh): the output store boxes go straight to the swap
+// members' receive buffers.  Entries are sorted so that, per coordinate, bits are removed from the
+// highest down (removing a higher bit leaves the lower bit indices valid).  maps[v]: member v's
+// destination chunk, row-major [M'][2N'] fp16 (box {64, 128}) or transposed C^T [N'][M'] (box
+// {128, 32}), M' / N' = M / N with the member bits removed.
+struct PeerStore {
+  int on, nsw;
+  int8_t is_n[4], bit[4], vbit[4];
+  CUtensorMap maps[8];
+};
+
 namespace tc {
+
+// Member index of a store box at (row m, complex column n) and its coordinates in that member's
+// chunk (the member bits removed).
+__device__ __forceinline__ int peer_coords(const PeerStore& ps, uint64_t& m, uint32_t& n) {
+  int v = 0;
+  for (int t = 0; t < ps.nsw; ++t) {
+    const int b = ps.bit[t];
+    if (ps.is_n[t]) {
+      v |= (int)((n >> b) & 1u) << ps.vbit[t];
+      n = (n & ((1u << b) - 1u)) | ((n >> (b + 1)) << b);
+    } else {
+      v |= (int)((m >> b) & 1ull) << ps.vbit[t];
+      m = (m & ((1ull << b) - 1ull)) | ((m >> (b + 1)) << b);
+    }
+  }
+  return v;
+}
+
+// After the last peer store of a thread: its bulk stores have completed (wait_group 0); make them
+// visible at system scope before the kernel ends (the swap's barrier follows on the stream).
+__device__ __forceinline__ void peer_store_fence() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
+}
 
 // Tile t -> C tile (m0 row, n0 column), A row and B row of its operands, skip = zero tile.
 __device__ __forceinline__ void batch_tile(const BatchArgs& ba, uint32_t t, uint32_t num_n, int BNv, int& m0, int& n0,
@@ -366,7 +401,8 @@ __global__ void __launch_bounds__((kAMode == 1 || kAMode == 4) ? kThreadsGather 
                          const float* in_max, const float* b_bound, uint32_t* out_max, int* exp_slot,
                          const __grid_constant__ ScatterArgs sc_args, uint32_t* out_scatter, uint64_t rows,
                          uint32_t n_cols, const __grid_constant__ AGatherArgs ga,
-                         const __grid_constant__ NdArgs nda, int epi_stg, const __grid_constant__ BatchArgs ba) {
+                         const __grid_constant__ NdArgs nda, int epi_stg, const __grid_constant__ BatchArgs ba,
+                         const __grid_constant__ PeerStore ps) {
   // 1: cp.async gather of 16-byte pieces (4 consecutive complex k); 4: of 4-byte pieces (single
   // complex elements, any layout: the stem permutation of a step whose contracted modes sit in the
   // middle of the stored order, fused into the load)
@@ -875,6 +911,15 @@ __global__ void __launch_bounds__((kAMode == 1 || kAMode == 4) ? kThreadsGather 
               uint64_t pol;
               asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
               tma_store_2d_hint(&tmC, sbuf, n0 + sub, m0, pol);
+            } else if (ps.on) {
+              // fused mode swap: the box goes to the swap member owning it (PeerStore)
+              uint64_t gm = ga.m_base + (uint64_t)m0;
+              uint32_t nc = (uint32_t)(n0 + sub) >> 1;
+              const int v = peer_coords(ps, gm, nc);
+              if (epi_stg == 4)
+                tma_store_2d(&ps.maps[v], sbuf, (int)gm, (int)nc);
+              else
+                tma_store_2d(&ps.maps[v], sbuf, (int)(2 * nc), (int)gm);
             } else if (epi_stg == 4) {
               // box {128 m (inner, global row), 32 complex n} of the C^T map
               tma_store_2d(&tmC, sbuf, (int)(ga.m_base + (uint64_t)m0), (n0 + sub) >> 1);
@@ -886,7 +931,10 @@ __global__ void __launch_bounds__((kAMode == 1 || kAMode == 4) ? kThreadsGather 
         }
       }
     }
-    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    if (lane == 0) {
+      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+      if (ps.on) peer_store_fence();
+    }
 #pragma unroll
     for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     if (out_max && lane == 0) atomicMax(out_max, __float_as_uint(mx));
@@ -948,6 +996,48 @@ static CUtensorMap make_map_t(const void* base, uint64_t M, uint64_t N) {
   return m;
 }
 
+// Fused mode swap (PeerTarget, common.cuh): the store maps of the swap members, or on = 0 when this
+// launch's epilogue cannot do it (scatter or direct stores, batched launches, member bits inside a
+// store box).  pt->honored tells the runtime whether the exchange happened here.
+static PeerStore make_peer_store(PeerTarget* pt, bool tma_epi, bool transposed, uint64_t M, uint32_t N2_real) {
+  PeerStore ps;
+  memset(&ps, 0, sizeof(ps));
+  if (!pt) return ps;
+  pt->honored = 0;
+  if (!tma_epi || pt->nsw <= 0 || pt->nsw > 3) return ps;
+  const uint64_t Nc = N2_real / 2;
+  struct E {
+    int is_n, bit, vbit;
+  };
+  std::vector<E> es;
+  int mrem = 0, nrem = 0;
+  for (int t = 0; t < pt->nsw; ++t) {
+    const int b = pt->bit[t];
+    if (pt->is_n[t]) {
+      if (b < 5 || (1ull << b) >= Nc) return ps;  // a 32-column store box would span two members
+      ++nrem;
+    } else {
+      if (b < 7 || (1ull << b) >= M) return ps;   // a 128-row box would span two members
+      ++mrem;
+    }
+    es.push_back({pt->is_n[t], b, pt->vbit[t]});
+  }
+  std::sort(es.begin(), es.end(), [](const E& x, const E& y) { return x.is_n != y.is_n ? x.is_n < y.is_n : x.bit > y.bit; });
+  const uint64_t Mp = M >> mrem, Np = Nc >> nrem;
+  if (Mp >= (1ull << 31) || 2 * Np >= (1ull << 31)) return ps;
+  for (int v = 0; v < (1 << pt->nsw); ++v)
+    ps.maps[v] = transposed ? make_map_t(pt->base[v], Mp, Np) : make_map_2d(pt->base[v], 2 * Np, Mp, 64, tc::BM);
+  ps.nsw = pt->nsw;
+  for (int t = 0; t < ps.nsw; ++t) {
+    ps.is_n[t] = (int8_t)es[t].is_n;
+    ps.bit[t] = (int8_t)es[t].bit;
+    ps.vbit[t] = (int8_t)es[t].vbit;
+  }
+  ps.on = 1;
+  pt->honored = 1;
+  return ps;
+}
+
 static int num_sms() {
   int dev = 0, n = 0;
   TN_CUDA(cudaGetDevice(&dev));
@@ -993,7 +1083,7 @@ static CUtensorMap make_map_nd(const void* base, const NdPlan& np) {
 bool tc2_enabled();
 void launch_tc2(int BN, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, uint32_t num_mp,
                 uint32_t num_n, int K2, const float* in_max, const float* b_bound, uint32_t* out_max, int* exp_slot,
-                int epi, uint64_t m_base, cudaStream_t s);
+                int epi, uint64_t m_base, const PeerStore& ps, cudaStream_t s);
 
 template <int BN, int KB, int G>
 static void launch_bn(__half* c, const __half* a, const __half* bp, uint64_t M, uint32_t K2, uint32_t N2_real,
@@ -1130,7 +1220,7 @@ static void launch_bn(__half* c, const __half* a, const __half* bp, uint64_t M, 
     memset(&n0, 0, sizeof(n0));
     tc::gemm_chalf_tc_kernel<BN, KB, G><<<grid, tc::kThreads, C::kSmem, s>>>(
         ma, mbm, mc, (uint32_t)(tiles / num_n), num_n, (int)K2, in_max, b_bound, out_max, exp_slot, sa0,
-        reinterpret_cast<uint32_t*>(c), c_rows, cols / 2, g0, n0, 0, ba);
+        reinterpret_cast<uint32_t*>(c), c_rows, cols / 2, g0, n0, 0, ba, PeerStore{});
     TN_CUDA(cudaGetLastError());
     return;
   }
@@ -1144,6 +1234,8 @@ static void launch_bn(__half* c, const __half* a, const __half* bp, uint64_t M, 
   // TMA coordinates are int32: process M in chunks of at most 2^30 rows
   const uint32_t num_n = N2 / BN;
   const uint64_t chunk = std::min<uint64_t>(1ull << 30, ((1ull << 31) / num_n) * tc::BM);
+  const PeerStore ps = make_peer_store(om ? om->peer : nullptr, !sa.on && epi_stg == 0 && (transposed || (om && om->identity)),
+                                       transposed, M, N2_real);
   if constexpr (G == 0 && KB == 64 && BN >= 128) {
     // plain A, row-major or transposed output, whole 256-row pair tiles: the CTA-pair kernel (half
     // the B tile staged per SM: fewer shared-memory bytes per MAC on the compute-bound steps)
@@ -1154,7 +1246,7 @@ static void launch_bn(__half* c, const __half* a, const __half* bp, uint64_t M, 
         CUtensorMap ma = make_map_2d(a + m_off * K2, K2, mm, KB, tc::BM);
         CUtensorMap mc = transposed ? make_map_t(c, M, N2_real / 2) : make_map_2d(c + m_off * N2, N2, mm, 64, tc::BM);
         launch_tc2(BN, ma, mb2, mc, (uint32_t)(mm / 256), num_n, (int)K2, in_max, b_bound, out_max,
-                   m_off ? nullptr : exp_slot, transposed ? 4 : 0, m_off, s);
+                   m_off ? nullptr : exp_slot, transposed ? 4 : 0, m_off, ps, s);
       }
       return;
     }
@@ -1177,7 +1269,7 @@ static void launch_bn(__half* c, const __half* a, const __half* bp, uint64_t M, 
     // the exponent is recorded once (first chunk); later chunks reuse the same inputs
     tc::gemm_chalf_tc_kernel<BN, KB, G><<<grid, (G == 1 || G == 4) ? tc::kThreadsGather : tc::kThreads, C::kSmem, s>>>(
         ma, mb, mc, num_m, num_n, (int)K2, in_max, b_bound, out_max, m_off ? nullptr : exp_slot, sa, out_sc, mm,
-        n_cols, gargs, nda, transposed ? 4 : epi_stg, BatchArgs{});
+        n_cols, gargs, nda, transposed ? 4 : epi_stg, BatchArgs{}, ps);
     TN_CUDA(cudaGetLastError());
   }
 }

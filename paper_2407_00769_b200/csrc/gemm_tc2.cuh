@@ -123,7 +123,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     gemm_chalf_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                           const __grid_constant__ CUtensorMap tmC, uint32_t num_mp, uint32_t num_n, int K2,
                           const float* in_max, const float* b_bound, uint32_t* out_max, int* exp_slot, int epi,
-                          uint64_t m_base, int order) {
+                          uint64_t m_base, int order, const __grid_constant__ PeerStore ps) {
   using C = Cfg2<BN>;
   constexpr int KB = C::KB;
   // "no re-run needed" signal of the scale re-run: both CTAs read the same value and leave together
@@ -280,15 +280,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         named_bar(1 + grp, 128);
         if (etid == 0) {
-          if (epi == 4)
+          if (ps.on) {
+            // fused mode swap: the box goes to the swap member owning it (PeerStore)
+            uint64_t gm = m_base + (uint64_t)m0;
+            uint32_t nc = (uint32_t)(n0 + sub) >> 1;
+            const int v = peer_coords(ps, gm, nc);
+            if (epi == 4)
+              tma_store_2d(&ps.maps[v], sbuf, (int)gm, (int)nc);
+            else
+              tma_store_2d(&ps.maps[v], sbuf, (int)(2 * nc), (int)gm);
+          } else if (epi == 4) {
             tma_store_2d(&tmC, sbuf, (int)(m_base + (uint64_t)m0), (n0 + sub) >> 1);
-          else
+          } else {
             tma_store_2d(&tmC, sbuf, n0 + sub, m0);
+          }
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
       }
     }
-    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    if (lane == 0) {
+      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+      if (ps.on) peer_store_fence();
+    }
 #pragma unroll
     for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     if (out_max && lane == 0) atomicMax(out_max, __float_as_uint(mx));

@@ -12,7 +12,7 @@ bool tc2_enabled() {
 template <int BN>
 static void launch_tc2_t(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, uint32_t num_mp,
                          uint32_t num_n, int K2, const float* in_max, const float* b_bound, uint32_t* out_max,
-                         int* exp_slot, int epi, uint64_t m_base, cudaStream_t s) {
+                         int* exp_slot, int epi, uint64_t m_base, const PeerStore& ps, cudaStream_t s) {
   using C = tc2::Cfg2<BN>;
   // per device: the shared-memory opt-in and how many CTA pairs can be resident at once (an odd SM
   // count per GPC leaves SMs without a partner, so this can be below #SMs / 2)
@@ -47,17 +47,17 @@ static void launch_tc2_t(const CUtensorMap& ma, const CUtensorMap& mb, const CUt
   const uint64_t busy = order == 1 ? std::min<uint64_t>(num_mp, (uint64_t)pairs) : std::min<uint64_t>(tiles, (uint64_t)pairs);
   const int grid = 2 * (int)busy;
   tc2::gemm_chalf_tc2_kernel<BN><<<grid, tc::kThreads, C::kSmem, s>>>(ma, mb, mc, num_mp, num_n, K2, in_max, b_bound,
-                                                                      out_max, exp_slot, epi, m_base, order);
+                                                                      out_max, exp_slot, epi, m_base, order, ps);
   TN_CUDA(cudaGetLastError());
 }
 
 void launch_tc2(int BN, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, uint32_t num_mp,
                 uint32_t num_n, int K2, const float* in_max, const float* b_bound, uint32_t* out_max, int* exp_slot,
-                int epi, uint64_t m_base, cudaStream_t s) {
+                int epi, uint64_t m_base, const PeerStore& ps, cudaStream_t s) {
   if (BN == 256)
-    launch_tc2_t<256>(ma, mb, mc, num_mp, num_n, K2, in_max, b_bound, out_max, exp_slot, epi, m_base, s);
+    launch_tc2_t<256>(ma, mb, mc, num_mp, num_n, K2, in_max, b_bound, out_max, exp_slot, epi, m_base, ps, s);
   else if (BN == 128)
-    launch_tc2_t<128>(ma, mb, mc, num_mp, num_n, K2, in_max, b_bound, out_max, exp_slot, epi, m_base, s);
+    launch_tc2_t<128>(ma, mb, mc, num_mp, num_n, K2, in_max, b_bound, out_max, exp_slot, epi, m_base, ps, s);
   else
     throw TnError{TN_E_INVALID, "CTA-pair GEMM: BN must be 128 or 256"};
 }

@@ -870,6 +870,7 @@ std::string report_json(const Plan& p, const std::vector<float>& ms) {
       << ",\"tc\":" << (s.tensor_core ? 1 : 0) << ",\"ga\":" << (s.gather_a ? 1 : 0) << ",\"split\":" << s.split << ",\"swap\":" << (s.swap ? 1 : 0)
       << ",\"quant\":" << (s.quant ? 1 : 0) << ",\"sparse\":" << s.sparse
       << ",\"fuse_quant\":" << (s.fuse_quant ? 1 : 0)
+      << ",\"out_kind\":" << (s.out_identity ? 0 : (s.out_transposed ? 1 : 2))
       << ",\"in\":";
     jlist(o, s.in_layout);
     o << ",\"R\":";
@@ -919,7 +920,7 @@ std::string report_json(const Plan& p, const std::vector<float>& ms) {
   o << ",\"final_layout\":";
   jlist(o, p.final_layout);
   o << ",\"launches\":" << p.launches << ",\"world\":" << p.world << ",\"n_swaps\":" << p.n_swaps
-    << ",\"swap_bytes\":" << p.swap_bytes << ",\"final_shard\":";
+    << ",\"swap_bytes\":" << p.swap_bytes << ",\"n_fused_swaps\":" << p.n_fused_swaps << ",\"final_shard\":";
   jlist(o, p.final_shard);
   if (!ms.empty()) {  // [common_ms, (perm_ms, gemm_ms) per step..., final_ms]
     o << ",\"ms\":[";

@@ -125,6 +125,10 @@ struct Plan {
   std::vector<int> final_shard;   // shard labels after the last step (the result's rank bits)
   int n_swaps = 0;
   double swap_bytes = 0;          // payload bytes each rank sends per slice (codec applied)
+  int n_fused_swaps = 0;          // swaps of the last run done inside the previous GEMM's epilogue
+  std::vector<void*> peer_stem;   // [2 r + j]: rank r's stem buffer j as this rank addresses it
+  const void* peer_key[2] = {nullptr, nullptr};  // the local buffers peer_stem was set up for
+  std::vector<void*> ipc_open;    // CUDA IPC mappings opened for peer_stem (closed on free)
   tn_comm* comm = nullptr;
   // CUDA graph of the whole tn_stem_contract body (world == 1; sharded: the head, or all with TN_GRAPH_NCCL=1): captured once per buffer set on a
   // library stream, replayed on the caller's stream.  Opaque CUDA handles as void*.

@@ -9,6 +9,7 @@
 //   4. stem loop (Alg. 1 "performer computation of currEin"): per step an optional
 //      permutation buf p -> buf 1-p, then the GEMM buf p -> buf 1-p (static double buffers).
 //   No host synchronisation inside the loop: all scale exponents live on the device.
+#include <cuda.h>
 #include <dlfcn.h>
 
 #include <algorithm>
@@ -67,6 +68,7 @@ struct LoopGroup {
   };
   std::vector<std::vector<Post>> board;  // board[src]: sends posted by rank src, in order
   std::vector<const void*> ptr;          // per rank: the buffer of an all-reduce / all-gather
+  std::vector<void*> stem_ptrs;          // per rank: its two stem buffers (fused mode swaps)
   void barrier() {
     std::unique_lock<std::mutex> lk(mu);
     if (broken) throw TnError{TN_E_NCCL, "loopback group broken by an earlier timeout"};
@@ -242,6 +244,162 @@ void xfer_allgather(Plan& p, const void* send, void* recv, uint64_t bytes, cudaS
   g.barrier();
   for (int r = 0; r < g.world; ++r)
     if (r != c->rank) TN_CUDA(cudaStreamWaitEvent(s, g.done[r], 0));
+}
+
+// ---- peer buffers for mode swaps fused into a GEMM epilogue (PeerTarget, common.cuh) ----
+// Every rank's two stem buffers as device pointers this rank can store to: loopback ranks share
+// the device (plain pointers); NCCL ranks map each other's buffers with CUDA IPC (handles of the
+// allocations holding the caller's buffers, exchanged with an all-gather, opened once per buffer
+// set).  Collective: every rank calls it with its buffers at the same point.
+typedef CUresult (*addr_range_t)(CUdeviceptr*, size_t*, CUdeviceptr);
+
+void close_peers(Plan& p) {
+  for (void* q : p.ipc_open) cudaIpcCloseMemHandle(q);
+  p.ipc_open.clear();
+  p.peer_stem.clear();
+  p.peer_key[0] = p.peer_key[1] = nullptr;
+}
+
+void ensure_peers(Plan& p, const tn_buffers* b, cudaStream_t s) {
+  if (p.world <= 1 || !p.comm) return;
+  if (p.peer_key[0] == b->d_stem[0] && p.peer_key[1] == b->d_stem[1] && p.peer_stem.size() == 2u * p.world) return;
+  close_peers(p);
+  tn_comm* c = p.comm;
+  std::vector<void*> ptrs(2 * p.world, nullptr);
+  if (c->loop) {
+    LoopGroup& g = *c->loop;
+    {
+      std::lock_guard<std::mutex> lk(g.mu);
+      if (g.stem_ptrs.size() != 2u * g.world) g.stem_ptrs.assign(2 * g.world, nullptr);
+      g.stem_ptrs[2 * c->rank] = b->d_stem[0];
+      g.stem_ptrs[2 * c->rank + 1] = b->d_stem[1];
+    }
+    g.barrier();
+    {
+      std::lock_guard<std::mutex> lk(g.mu);
+      ptrs = g.stem_ptrs;
+    }
+    g.barrier();  // nobody republishes before every rank has read
+  } else {
+    static addr_range_t range = nullptr;
+    if (!range) {
+      void* fn = nullptr;
+      cudaDriverEntryPointQueryResult q;
+      if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+          q != cudaDriverEntryPointSuccess)
+        throw TnError{TN_E_CUDA, "cuMemGetAddressRange unavailable"};
+      range = (addr_range_t)fn;
+    }
+    struct Rec {
+      cudaIpcMemHandle_t h[2];
+      uint64_t off[2];
+    };
+    Rec mine;
+    memset(&mine, 0, sizeof(mine));
+    for (int j = 0; j < 2; ++j) {
+      CUdeviceptr base = 0;
+      size_t sz = 0;
+      if (range(&base, &sz, (CUdeviceptr)b->d_stem[j]) != CUDA_SUCCESS)
+        throw TnError{TN_E_CUDA, "cuMemGetAddressRange failed on a stem buffer"};
+      TN_CUDA(cudaIpcGetMemHandle(&mine.h[j], (void*)base));
+      mine.off[j] = (uint64_t)((CUdeviceptr)b->d_stem[j] - base);
+    }
+    unsigned char* d = nullptr;
+    TN_CUDA(cudaMalloc(&d, sizeof(Rec) * (p.world + 1)));
+    std::vector<Rec> all(p.world);
+    try {
+      TN_CUDA(cudaMemcpyAsync(d, &mine, sizeof(Rec), cudaMemcpyHostToDevice, s));
+      xfer_allgather(p, d, d + sizeof(Rec), sizeof(Rec), s);
+      TN_CUDA(cudaMemcpyAsync(all.data(), d + sizeof(Rec), sizeof(Rec) * p.world, cudaMemcpyDeviceToHost, s));
+      TN_CUDA(cudaStreamSynchronize(s));
+    } catch (...) {
+      cudaFree(d);
+      throw;
+    }
+    TN_CUDA(cudaFree(d));
+    std::vector<std::pair<cudaIpcMemHandle_t, void*>> opened;  // one mapping per allocation
+    for (int r = 0; r < p.world; ++r)
+      for (int j = 0; j < 2; ++j) {
+        if (r == p.rank) {
+          ptrs[2 * r + j] = b->d_stem[j];
+          continue;
+        }
+        void* base = nullptr;
+        for (auto& o : opened)
+          if (!memcmp(&o.first, &all[r].h[j], sizeof(cudaIpcMemHandle_t))) base = o.second;
+        if (!base) {
+          TN_CUDA(cudaIpcOpenMemHandle(&base, all[r].h[j], cudaIpcMemLazyEnablePeerAccess));
+          opened.push_back({all[r].h[j], base});
+          p.ipc_open.push_back(base);
+        }
+        ptrs[2 * r + j] = static_cast<unsigned char*>(base) + all[r].off[j];
+      }
+  }
+  p.peer_stem = ptrs;
+  p.peer_key[0] = b->d_stem[0];
+  p.peer_key[1] = b->d_stem[1];
+}
+
+// Members of a mode swap (Alg. 1): this rank's member index (its bits at the swapped shard
+// positions, position 0 = rank MSB) and the rank of member v.
+struct SwapMembers {
+  int S = 0, sx = 0, me = 0, rank = 0;
+  std::vector<int> out_pos;
+  SwapMembers(const Plan& p, const StemStep& st) : S((int)st.shard_before.size()), sx((int)st.swap_out_pos.size()),
+                                                    rank(p.rank), out_pos(st.swap_out_pos) {
+    for (int t = 0; t < sx; ++t) me = (me << 1) | ((rank >> (S - 1 - out_pos[t])) & 1);
+  }
+  int peer_of(int v) const {
+    int r = rank;
+    for (int t = 0; t < sx; ++t) {
+      const int shift = S - 1 - out_pos[t], bit = (v >> (sx - 1 - t)) & 1;
+      r = (r & ~(1 << shift)) | (bit << shift);
+    }
+    return r;
+  }
+};
+
+bool fused_swap_enabled(const Plan& p) {
+  static const char* e = getenv("TN_NO_FUSED_SWAP");  // A/B knob (same as cfg.no_fused_swap = 1)
+  return p.world > 1 && !p.cfg.no_fused_swap && !(e && atoi(e) != 0);
+}
+
+// The mode swap before step i+1 done by step i's GEMM epilogue: each output element goes straight
+// to the rank that owns it after the swap.  Same result as mode_swap (send permutation putting
+// swap_in outermost, chunk v to member v, received at chunk `me`): the receiver's local index is the
+// element's index with the swap_in bits removed, behind the outermost `me` chunk bits.  Only fp16
+// swaps (a quantised one needs the codec) after a tensor-core step; the launcher decides whether
+// its epilogue can (PeerTarget::honored), else the runtime falls back to mode_swap.
+bool fused_swap_target(const Plan& p, size_t i, int cur, PeerTarget& pt) {
+  if (i + 1 >= p.steps.size() || !fused_swap_enabled(p)) return false;
+  const StemStep& st = p.steps[i];
+  const StemStep& nx = p.steps[i + 1];
+  if (!nx.swap || nx.quant || p.cfg.dtype != TN_CHALF || !st.tensor_core || st.split || st.sparse) return false;
+  if (!(st.out_identity || st.out_transposed) || p.peer_stem.size() != 2u * p.world) return false;
+  if (nx.send_layout.size() != st.out_layout.size()) return false;
+  const SwapMembers sm(p, nx);
+  if (sm.sx > 3) return false;
+  memset(&pt, 0, sizeof(pt));
+  pt.nsw = sm.sx;
+  const int L = (int)st.out_layout.size();
+  for (int t = 0; t < sm.sx; ++t) {
+    const auto it = std::find(st.out_layout.begin(), st.out_layout.end(), nx.swap_in[t]);
+    if (it == st.out_layout.end()) return false;
+    const int64_t stride = (int64_t)1 << (L - 1 - (int)(it - st.out_layout.begin()));
+    int is_n = -1, bit = -1;
+    for (int j = 0; j < st.mlog; ++j)
+      if (st.m_stride[j] == stride) is_n = 0, bit = j;
+    for (int j = 0; j < st.nlog; ++j)
+      if (st.n_stride[j] == stride) is_n = 1, bit = j;
+    if (is_n < 0) return false;
+    pt.is_n[t] = is_n;
+    pt.bit[t] = bit;
+    pt.vbit[t] = sm.sx - 1 - t;
+  }
+  const uint64_t chunk_bytes = (4ull << L) >> sm.sx;  // complex-half
+  for (int v = 0; v < (1 << sm.sx); ++v)
+    pt.base[v] = static_cast<unsigned char*>(p.peer_stem[2 * sm.peer_of(v) + (1 - cur)]) + (uint64_t)sm.me * chunk_bytes;
+  return true;
 }
 
 struct Scratch {
@@ -561,7 +719,8 @@ int redo_bits() {
 }
 
 void run_gemm_once(Plan& p, const StemStep& st, size_t i, const void* src, void* dst, int mshift, const float* in_max,
-                   uint32_t* out_max, int* exp_slot, unsigned char* W, const Scratch& sc, cudaStream_t s);
+                   uint32_t* out_max, int* exp_slot, unsigned char* W, const Scratch& sc, cudaStream_t s,
+                   PeerTarget* peer = nullptr);
 
 // One stem GEMM plus its scale re-run (complex-half: redo_check + the same launch, which exits at once
 // unless the realised output max lost more than TN_REDO_BITS (default 10) bits of fp16 headroom).
@@ -570,18 +729,22 @@ void run_gemm_once(Plan& p, const StemStep& st, size_t i, const void* src, void*
 // chains pass false).
 void run_gemm(Plan& p, const StemStep& st, size_t i, const void* src, void* dst, int mshift, const float* in_max,
               uint32_t* out_max, int* exp_slot, unsigned char* W, const Scratch& sc, cudaStream_t s,
-              bool collective = false) {
-  run_gemm_once(p, st, i, src, dst, mshift, in_max, out_max, exp_slot, W, sc, s);
+              bool collective = false, PeerTarget* peer = nullptr) {
+  run_gemm_once(p, st, i, src, dst, mshift, in_max, out_max, exp_slot, W, sc, s, peer);
   const bool coll = collective && p.world > 1;  // both dtypes scale by powers of two (C-A8)
+  // (a fused swap: this all-reduce is also the barrier after which every rank's peer stores are in)
   if (coll) xfer_allreduce_max(p, reinterpret_cast<float*>(out_max), s);
   if (p.cfg.dtype != TN_CHALF || !in_max || redo_bits() <= 0) return;
   launch_redo_check(out_max, in_max, &sc.redo_in[i], redo_bits(), s);  // also sets the re-run's max
-  run_gemm_once(p, st, i, src, dst, mshift, &sc.redo_in[i], nullptr, exp_slot, W, sc, s);
+  run_gemm_once(p, st, i, src, dst, mshift, &sc.redo_in[i], nullptr, exp_slot, W, sc, s, peer);
   ++p.launches;
+  // a re-run rewrites the peers' boxes: barrier again (an all-reduce of the already reduced max)
+  if (coll && peer && peer->honored) xfer_allreduce_max(p, reinterpret_cast<float*>(out_max), s);
 }
 
 void run_gemm_once(Plan& p, const StemStep& st, size_t i, const void* src, void* dst, int mshift, const float* in_max,
-                   uint32_t* out_max, int* exp_slot, unsigned char* W, const Scratch& sc, cudaStream_t s) {
+                   uint32_t* out_max, int* exp_slot, unsigned char* W, const Scratch& sc, cudaStream_t s,
+                   PeerTarget* peer) {
   const int mlog = st.mlog - mshift;
   const uint64_t M = 1ull << mlog;
   const uint32_t K = 1u << st.klog, N = 1u << st.nlog;
@@ -593,6 +756,8 @@ void run_gemm_once(Plan& p, const StemStep& st, size_t i, const void* src, void*
   om.nbits = st.nlog;
   for (int j = 0; j < mlog; ++j) om.ms[j] = st.m_stride[j];
   for (int j = 0; j < st.nlog; ++j) om.ns[j] = st.n_stride[j];
+  if (peer) peer->honored = 0;
+  om.peer = mshift == 0 ? peer : nullptr;
   if (p.cfg.dtype == TN_CHALF) {
     AGather ag;
     if (st.gather_a) {  // the step's permutation, fused into the A load (mshift == 0: not a split step)
@@ -682,21 +847,35 @@ void stem_body(Plan& p, const tn_buffers* b, cudaStream_t s, bool head = true, b
   rec_event(p, 1, s);
   const size_t n_main = !p.split_modes.empty() ? (size_t)p.split_from
                                                : (p.sparse_from >= 0 ? (size_t)p.sparse_from : p.steps.size());
+  bool swapped = false;  // the swap before step i was done by step i-1's epilogue
+  p.n_fused_swaps = 0;
   for (size_t i = 0; i < n_main; ++i) {
     const StemStep& st = p.steps[i];
-    if (st.swap) {
+    if (st.swap && !swapped) {
       mode_swap(p, st, b, cur, s);
     }
+    swapped = false;
     if (st.perm) {
       launch_permute(b->d_stem[1 - cur], b->d_stem[cur], eb, (int)st.in_layout.size(), st.perm_axes.data(), s);
       ++p.launches;
       cur = 1 - cur;
     }
+    // the swap before step i+1 inside this GEMM's epilogue (fp16, NVLink peer stores): first a
+    // barrier (an all-reduce of the already reduced input max) after which no rank still reads the
+    // buffer its peers are about to write
+    PeerTarget pt;
+    const bool fuse = i + 1 < n_main && fused_swap_target(p, i, cur, pt);
+    if (fuse) xfer_allreduce_max(p, &sc.max_slot[i], s);
     rec_event(p, 2 + 2 * i, s);
     // (sharded: the max all-reduces inside make every rank scale the next step identically)
     run_gemm(p, st, i, b->d_stem[cur], b->d_stem[1 - cur], 0, &sc.max_slot[i],
-             reinterpret_cast<uint32_t*>(&sc.max_slot[i + 1]), &sc.exps[2 + 2 * i], W, sc, s, true);
+             reinterpret_cast<uint32_t*>(&sc.max_slot[i + 1]), &sc.exps[2 + 2 * i], W, sc, s, true,
+             fuse ? &pt : nullptr);
     cur = 1 - cur;
+    if (fuse && pt.honored) {
+      swapped = true;
+      ++p.n_fused_swaps;
+    }
     rec_event(p, 3 + 2 * i, s);
   }
   if (!p.split_modes.empty()) {
@@ -798,6 +977,7 @@ void stem_contract(Plan& p, const tn_buffers* b, uint64_t slice_id, cudaStream_t
     }
   }
   launch_set_u64(reinterpret_cast<uint64_t*>(W + p.ws_slice), slice_id, s);
+  if (fused_swap_enabled(p) && p.n_swaps > 0) ensure_peers(p, b, s);  // outside any capture
   if (graph_wanted(p)) {
     const bool same = p.graph_exec && p.graph_key[0] == b->d_ws && p.graph_key[1] == b->d_stem[0] &&
                       p.graph_key[2] == b->d_stem[1] && p.graph_stem_bytes == b->stem_bytes && p.graph_timing == p.timing;
@@ -1363,6 +1543,7 @@ int tn_plan_info_get(const tn_plan* h, tn_plan_info* info) {
 void tn_plan_free(tn_plan* h) {
   if (!h) return;
   if (h->p->pinned) cudaFreeHost(h->p->pinned);
+  close_peers(*h->p);
   if (h->p->graph_exec) cudaGraphExecDestroy((cudaGraphExec_t)h->p->graph_exec);
   if (h->p->cap_stream) cudaStreamDestroy((cudaStream_t)h->p->cap_stream);
   for (void* e : h->p->ev) cudaEventDestroy((cudaEvent_t)e);

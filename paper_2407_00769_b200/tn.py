@@ -29,7 +29,7 @@ class tn_config(C.Structure):
                 ("comm_group", C.c_int32), ("stem_capacity_bytes", C.c_uint64), ("split_log2", C.c_int32),
                 ("layout_policy", C.c_int32), ("quant_from_pct", C.c_int32), ("virtual_world", C.c_int32),
                 ("no_gather", C.c_int32), ("no_fuse_swap_quant", C.c_int32), ("recompute", C.c_int32),
-                ("reserved", C.c_int32)]
+                ("no_fused_swap", C.c_int32)]
 
 
 class tn_buffers(C.Structure):
@@ -127,8 +127,9 @@ def _stream(stream):
 
 def make_config(dtype=TN_CHALF, stem_min_log2=20, comm_codec=TN_COMM_INT8, comm_group=128,
                 stem_capacity_bytes=0, split_log2=0, layout_policy=3, virtual_world=1, quant_from_pct=-1,
-                no_gather=0, no_fuse_swap_quant=0, recompute=0):
+                no_gather=0, no_fuse_swap_quant=0, recompute=0, no_fused_swap=0):
     c = tn_config()
+    c.no_fused_swap = no_fused_swap
     c.recompute = recompute
     c.no_gather = no_gather
     c.no_fuse_swap_quant = no_fuse_swap_quant

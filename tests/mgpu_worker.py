@@ -42,7 +42,9 @@ def main():
     # int8: every swap quantised on C2 (quant_from_pct=0); default late-stage policy on C3
     with open(os.path.join(ROOT, "plans", "c2.json")) as f:
         c2 = MP.sub_slice(json.load(f), 20)
-    for codec, name, plan, pct, sm in ((tn.TN_COMM_FP16, "fp16", sub, -1, 14), (tn.TN_COMM_INT8, "int8", sub, -1, 14),
+    for codec, name, plan, pct, sm in ((tn.TN_COMM_FP16, "fp16", sub, -1, 14),
+                                       (tn.TN_COMM_FP16, "fp16_nofused", sub, -1, 14),
+                                       (tn.TN_COMM_INT8, "int8", sub, -1, 14),
                                        (tn.TN_COMM_INT8, "int8_all_c2", c2, 0, 12),
                                        (tn.TN_COMM_INT8, "int8_all_c3", sub, 0, 14),
                                        (tn.TN_COMM_INT8, "int8_all_c3_unfused", sub, 0, 14),
@@ -50,7 +52,8 @@ def main():
                                        (tn.TN_COMM_INT4, "int4_all", sub, 0, 14),
                                        (tn.TN_COMM_INT8_TENSOR, "int8_tensor_all", sub, 0, 14)):
         p = tn.Plan(plan, tn.make_config(stem_min_log2=sm, comm_codec=codec, quant_from_pct=pct,
-                                         no_fuse_swap_quant=int(name.endswith("_unfused"))), comm=comm)
+                                         no_fuse_swap_quant=int(name.endswith("_unfused")),
+                                         no_fused_swap=int(name.endswith("_nofused"))), comm=comm)
         b = tn.Buffers(p)
         amps = tn.contract(p, b, 0)
         torch.cuda.synchronize()
@@ -85,6 +88,9 @@ def main():
                    "pred_int4_all": predicted_swap_error(sub, results["int4_all"][1], ref, "int4"),
                    "pred_int8_tensor_all": predicted_swap_error(sub, results["int8_tensor_all"][1], ref, "int8"),
                    "rel_fp16_vs_1gpu": metrics.rel_l2(results["fp16"][0], one),
+                   "fp16_epilogue_swaps": results["fp16"][1]["n_fused_swaps"],
+                   "fp16_nofused_epilogue_swaps": results["fp16_nofused"][1]["n_fused_swaps"],
+                   "fp16_fused_equal_transport": bool(np.array_equal(results["fp16"][0], results["fp16_nofused"][0])),
                    "rel_1gpu_oracle": metrics.rel_l2(one, ref),
                    "swaps": sum(1 for s in results["int8"][1]["steps"] if s.get("swap")),
                    "steps": len(results["int8"][1]["steps"])}

@@ -129,6 +129,23 @@ def test_loopback_fused_codec_bit_identical(tn, c3sub, world):
 
 
 @pytest.mark.parametrize("world", [2, 4, 8])
+def test_loopback_fused_swap_bit_identical(tn, c3sub, world):
+    """fp16 mode swaps done by the previous GEMM's epilogue (tn_config.no_fused_swap = 0: output
+    boxes stored straight into the owning rank's buffer) == the exchange through the transport
+    (send permutation + chunk exchange), bit for bit, on every rank."""
+    sub, _ = c3sub
+    kw = dict(stem_min_log2=14, comm_codec=tn.TN_COMM_FP16)
+    fused = run_loopback(tn, sub, world, kw)
+    unf = run_loopback(tn, sub, world, dict(kw, no_fused_swap=1))
+    nf = fused[0][1]["n_fused_swaps"]
+    print(f"world={world}: swaps={n_swaps(fused[0][1])} fused={nf}")
+    assert unf[0][1]["n_fused_swaps"] == 0
+    assert nf >= 1
+    for (a, _, _), (b, _, _) in zip(fused, unf):
+        assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
 def test_loopback_c1_all_legs_open(tn, world):
     """C1: 12 open legs, result gathered from 1/G shards into the workspace (ADVICE: the gather
     must not write past a shard-sized stem buffer)."""

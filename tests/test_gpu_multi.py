@@ -45,6 +45,10 @@ def test_sharded_stem_vs_oracle(world):
     for got, pred in (("rel_int8_all_c3_oracle", "pred_int8_all"), ("rel_int4_all_oracle", "pred_int4_all"),
                       ("rel_int8_tensor_all_oracle", "pred_int8_tensor_all"), ("rel_int8_oracle", "pred_int8")):
         assert v[got] <= 2.0 * float(np.hypot(v[pred], e16)) + 1e-3, (got, v[got], v[pred])
+    # fp16 swaps done by the previous GEMM's epilogue (NVLink peer stores through CUDA IPC):
+    # bit-identical to the NCCL exchange
+    assert v["fp16_epilogue_swaps"] >= 1 and v["fp16_nofused_epilogue_swaps"] == 0
+    assert v["fp16_fused_equal_transport"]
     # permutation fused into the sender's codec: bit-identical to permutation pass + codec
     assert v["fused_swaps_c3_unfused_run"] == 0
     assert v["rel_int8_c3_fused_vs_unfused"] == 0.0
