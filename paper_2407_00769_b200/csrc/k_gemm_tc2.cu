@@ -40,10 +40,15 @@ static void launch_tc2_t(const CUtensorMap& ma, const CUtensorMap& mb, const CUt
   }
   const uint64_t tiles = (uint64_t)num_mp * num_n;
   if (tiles == 0) return;
-  // tile order (tc2_tile): per-cluster m-pairs when there are enough of them to keep every cluster
-  // busy; TN_TC2_ORDER = 0 / 1 forces either (A/B knob)
+  // tile order (tc2_tile): per-cluster m-pairs (order 1) only when every cluster's A rows fit in L2
+  // together (K2 x 256 rows x 2 B x pairs <= 40 MB, i.e. K <= 2^9) and there are enough m-pairs to
+  // keep every cluster busy; otherwise n fastest across clusters (order 0: the clusters sharing an
+  // m-pair read its A rows at the same time).  Measured on C3 step 30 (m21 k11 n11): order 0 49-52
+  // ms vs order 1 55-56 ms; mubench M = 2^21, K = N = 2^10: DRAM reads 19 GB vs 33 GB (A = 8.6 GB).
+  // TN_TC2_ORDER = 0 / 1 forces either (A/B knob)
   static const int order_env = getenv("TN_TC2_ORDER") ? atoi(getenv("TN_TC2_ORDER")) : -1;
-  const int order = order_env >= 0 ? order_env : (num_mp >= 8ull * (uint64_t)pairs ? 1 : 0);
+  const bool a_fits_l2 = (uint64_t)K2 * 256 * 2 * (uint64_t)pairs <= (40ull << 20);
+  const int order = order_env >= 0 ? order_env : (a_fits_l2 && num_mp >= 8ull * (uint64_t)pairs ? 1 : 0);
   const uint64_t busy = order == 1 ? std::min<uint64_t>(num_mp, (uint64_t)pairs) : std::min<uint64_t>(tiles, (uint64_t)pairs);
   const int grid = 2 * (int)busy;
   tc2::gemm_chalf_tc2_kernel<BN><<<grid, tc::kThreads, C::kSmem, s>>>(ma, mb, mc, num_mp, num_n, K2, in_max, b_bound,
