@@ -277,6 +277,23 @@ TN_API int tn_gemm_chalf_padded(void* d_c, const void* d_a, const void* d_bp, ui
 TN_API int tn_gemm_cfloat(void* d_c, const void* d_a, const void* d_b, uint64_t M, uint32_t K, uint32_t N,
                    void* stream);
 
+/* The stem permutation of a step stored as [M >> ma][K][2^ma] (its 2^ma innermost modes are kept
+ * modes, its contracted modes come next: P:534's "dimension reordering" when the contracted modes
+ * sit in the middle of the stored order) folded into the operand layout instead of a pass:
+ *   C[m, n] = 2^e sum_k A[m, k] B[k, n],  A[m, k] at element ((m >> ma) K + k) 2^ma + (m & (2^ma-1)),
+ * computed as the real GEMM over rows (m, c) of an MN-major operand on the CTA-pair tcgen05 kernel
+ * (same 4 M K N real MACs as Eq. 6; the complex combination in the epilogue).
+ * d_bpm = B' fp16 [2N][K] from tn_pad_b_mn.  C row-major [M][N] complex-half.  ma >= 7, M a
+ * multiple of 128 with 2^ma <= M < 2^31, K >= 64 and N >= 64 powers of two; scale pointers as
+ * tn_gemm_chalf.  TN_E_INVALID otherwise (also when the CTA-pair kernel is disabled, TN_TC2=0). */
+TN_API int tn_gemm_chalf_mn(void* d_c, const void* d_a, const void* d_bpm, uint64_t M, uint32_t K, uint32_t N,
+                            int ma, const float* d_in_max, const float* d_b_bound, uint32_t* d_out_max, int* d_exp,
+                            void* stream);
+/* B' for tn_gemm_chalf_mn: rows (n, 0) = Re B[:, n], (n, 1) = Im B[:, n] (fp16, k contiguous), from
+ * complex64 B [K][N]; scale, *d_exp and *d_b_bound exactly as tn_pad_b. */
+TN_API int tn_pad_b_mn(void* d_bpm, const void* d_b, uint32_t K, uint32_t N, float* d_b_bound, int* d_exp,
+                       void* d_scratch /* >= 16 bytes */, void* stream);
+
 /* Build B_P (fp16 [2N][2K]) from complex64 B [K][N] row-major with an exact power-of-two scale
  * 2^t chosen so max|B| maps near 2^14; t is added to *d_exp (may be NULL: t = 0);
  * *d_b_bound receives max column 1-norm of the stored B_P (float).  Two kernels. */

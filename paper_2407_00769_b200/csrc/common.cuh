@@ -107,6 +107,10 @@ void launch_contract_c64(const ContractArgs& a, cudaStream_t s);
 void launch_gather_kn(const GatherArgs& g, cudaStream_t s);
 void launch_max_abs_f32(const float* x, uint64_t n, uint32_t* out_bits, cudaStream_t s);
 void launch_max_abs_f16(const __half* x, uint64_t n, uint32_t* out_bits, cudaStream_t s);
+// B' of the MN-major GEMM: rows (n, c') = c'-part of b[k][n] (k contiguous), fp16, the same scale,
+// exponent slot and column 1-norm bound as launch_pad_b
+void launch_pad_b_mn(__half* bpm, const float2* b, int klog, int nlog, const uint32_t* bmax_bits, float* b_bound,
+                     int* exp_slot, cudaStream_t s);
 // B [K][N] c64 -> B_P fp16 [2N][2K] with scale 2^t (t from *bmax_bits), bound, exp
 void launch_pad_b(__half* bp, const float2* b, int klog, int nlog, const uint32_t* bmax_bits,
                   float* b_bound, int* exp_slot, cudaStream_t s);
@@ -152,6 +156,12 @@ struct AGather {
 void launch_gemm_chalf_tc(__half* c, const __half* a, const __half* bp, uint64_t M, uint32_t K2,
                           uint32_t N2, const float* in_max, const float* b_bound, uint32_t* out_max,
                           int* exp_slot, const OutMap* om, cudaStream_t s, const AGather* ag = nullptr);
+// MN-major A (k_gemm_tc2.cu): A stored [M >> ma][K][2^ma] complex-half (2^ma kept rows innermost),
+// bpm = B' [2N][K] (launch_pad_b_mn); no permutation pass.
+bool mn_gemm_supported(uint64_t M, uint32_t K, uint32_t N, int ma, const OutMap* om);
+void launch_gemm_chalf_mn(__half* c, const __half* a, const __half* bpm, uint64_t M, uint32_t K, uint32_t N, int ma,
+                          const float* in_max, const float* b_bound, uint32_t* out_max, int* exp_slot,
+                          const OutMap* om, cudaStream_t s);
 // Gather-batched tcgen05 GEMM (Fig. 5; see BatchArgs in gemm_tc.cuh): n_out
 // entries of M rows (M % 128 == 0).  Index variant (pad_r == 0): C[b] = A[ia[b]] x B_P[ib[b]].
 // Padded 2-d index (pad_r > 0, n_out = n_a): C_P[a] = A[a] x [B_P[table[a pad_r + r]]]_r, rows of

@@ -983,11 +983,11 @@ static CUtensorMap make_map_2d(const void* base, uint64_t inner, uint64_t outer,
 
 // C^T [N complex][M complex] as 4-byte elements (one complex-half value each), box {128 m, 32 n}
 // (N < 32: {128 m, N n}, the tile's single n block)
-static CUtensorMap make_map_t(const void* base, uint64_t M, uint64_t N) {
+static CUtensorMap make_map_t(const void* base, uint64_t M, uint64_t N, uint32_t box_m = tc::BM) {
   CUtensorMap m;
   cuuint64_t dims[2] = {M, N};
   cuuint64_t strides[1] = {M * 4};
-  cuuint32_t box[2] = {(cuuint32_t)tc::BM, (cuuint32_t)std::min<uint64_t>(N, 32)};
+  cuuint32_t box[2] = {box_m, (cuuint32_t)std::min<uint64_t>(N, 32)};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = get_encode()(&m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<void*>(base), dims, strides, box, estr,
                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -999,7 +999,8 @@ static CUtensorMap make_map_t(const void* base, uint64_t M, uint64_t N) {
 // Fused mode swap (PeerTarget, common.cuh): the store maps of the swap members, or on = 0 when this
 // launch's epilogue cannot do it (scatter or direct stores, batched launches, member bits inside a
 // store box).  pt->honored tells the runtime whether the exchange happened here.
-static PeerStore make_peer_store(PeerTarget* pt, bool tma_epi, bool transposed, uint64_t M, uint32_t N2_real) {
+static PeerStore make_peer_store(PeerTarget* pt, bool tma_epi, bool transposed, uint64_t M, uint32_t N2_real,
+                                 uint32_t box_rows = tc::BM) {
   PeerStore ps;
   memset(&ps, 0, sizeof(ps));
   if (!pt) return ps;
@@ -1017,7 +1018,7 @@ static PeerStore make_peer_store(PeerTarget* pt, bool tma_epi, bool transposed, 
       if (b < 5 || (1ull << b) >= Nc) return ps;  // a 32-column store box would span two members
       ++nrem;
     } else {
-      if (b < 7 || (1ull << b) >= M) return ps;   // a 128-row box would span two members
+      if ((1 << b) < (int)box_rows || (1ull << b) >= M) return ps;   // a row box would span two members
       ++mrem;
     }
     es.push_back({pt->is_n[t], b, pt->vbit[t]});
@@ -1026,7 +1027,7 @@ static PeerStore make_peer_store(PeerTarget* pt, bool tma_epi, bool transposed, 
   const uint64_t Mp = M >> mrem, Np = Nc >> nrem;
   if (Mp >= (1ull << 31) || 2 * Np >= (1ull << 31)) return ps;
   for (int v = 0; v < (1 << pt->nsw); ++v)
-    ps.maps[v] = transposed ? make_map_t(pt->base[v], Mp, Np) : make_map_2d(pt->base[v], 2 * Np, Mp, 64, tc::BM);
+    ps.maps[v] = transposed ? make_map_t(pt->base[v], Mp, Np, box_rows) : make_map_2d(pt->base[v], 2 * Np, Mp, 64, box_rows);
   ps.nsw = pt->nsw;
   for (int t = 0; t < ps.nsw; ++t) {
     ps.is_n[t] = (int8_t)es[t].is_n;
@@ -1083,7 +1084,7 @@ static CUtensorMap make_map_nd(const void* base, const NdPlan& np) {
 bool tc2_enabled();
 void launch_tc2(int BN, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, uint32_t num_mp,
                 uint32_t num_n, int K2, const float* in_max, const float* b_bound, uint32_t* out_max, int* exp_slot,
-                int epi, uint64_t m_base, const PeerStore& ps, cudaStream_t s);
+                int epi, uint64_t m_base, const PeerStore& ps, const NdArgs& nda, cudaStream_t s);
 
 template <int BN, int KB, int G>
 static void launch_bn(__half* c, const __half* a, const __half* bp, uint64_t M, uint32_t K2, uint32_t N2_real,
@@ -1239,14 +1240,17 @@ static void launch_bn(__half* c, const __half* a, const __half* bp, uint64_t M, 
   if constexpr (G == 0 && KB == 64 && BN >= 128) {
     // plain A, row-major or transposed output, whole 256-row pair tiles: the CTA-pair kernel (half
     // the B tile staged per SM: fewer shared-memory bytes per MAC on the compute-bound steps)
-    if (!np && !sa.on && epi_stg == 0 && M % 256 == 0 && N2_real % BN == 0 && chunk % 256 == 0 && tc2_enabled()) {
+    // (also the gathered steps whose permutation is one N-d TMA box of 128-byte swizzled rows: the
+    // producer computes the box coordinates from the global row, the stage image is the same)
+    const bool nd_ok = !np || (np->nd > 0 && !np->interleaved && np->KB == 64);
+    if (nd_ok && !sa.on && epi_stg == 0 && M % 256 == 0 && N2_real % BN == 0 && chunk % 256 == 0 && tc2_enabled()) {
       CUtensorMap mb2 = make_map_2d(bp, K2, N2_real, KB, BN / 2);
       for (uint64_t m_off = 0; m_off < M; m_off += chunk) {
         const uint64_t mm = std::min<uint64_t>(chunk, M - m_off);
-        CUtensorMap ma = make_map_2d(a + m_off * K2, K2, mm, KB, tc::BM);
+        CUtensorMap ma = np ? make_map_nd(a, *np) : make_map_2d(a + m_off * K2, K2, mm, KB, tc::BM);
         CUtensorMap mc = transposed ? make_map_t(c, M, N2_real / 2) : make_map_2d(c + m_off * N2, N2, mm, 64, tc::BM);
         launch_tc2(BN, ma, mb2, mc, (uint32_t)(mm / 256), num_n, (int)K2, in_max, b_bound, out_max,
-                   m_off ? nullptr : exp_slot, transposed ? 4 : 0, m_off, ps, s);
+                   m_off ? nullptr : exp_slot, transposed ? 4 : 0, m_off, ps, nda, s);
       }
       return;
     }

@@ -45,7 +45,22 @@ struct Cfg2 {
   static constexpr int kNAcc = 512 / BN;
   // M = 256 (the pair), N = BN, fp16 x fp16 -> fp32, both K-major
   static constexpr uint32_t kIdesc = (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+  static constexpr uint32_t kIdescMN = kIdesc | (1u << 15);  // A MN-major (bit 15)
 };
+
+// MN-major A (complex rows interleaved, see the kernel comment): SWIZZLE_128B atoms of 64 rows (128 B)
+// x 8 k; the two 64-row atoms of a stage sit LBO = 64 k x 128 B = 8 KB apart, consecutive 8-k groups
+// SBO = 1 KB apart (canonical Major-MN SW128 layout ((8 x 16 B, m), (8, k)) : ((16 B, LBO), (128 B, SBO)))
+__device__ __forceinline__ uint64_t smem_desc_mn_sw128(const void* p) {
+  uint64_t addr = smem_u32(p);
+  uint64_t d = 0;
+  d |= (addr & 0x3FFFFull) >> 4;
+  d |= (uint64_t)(8192 >> 4) << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
 
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
@@ -73,6 +88,26 @@ __device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* m
       "%3}], [%4];" ::"r"(smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar_cluster)
       : "memory");
+}
+
+// N-dimensional form (2..5 dims, coordinates innermost first): the fused stem permutation of a
+// gathered-A step (NdArgs, gemm_tc.cuh) loaded per CTA of the pair
+__device__ __forceinline__ void tma_load_nd_pair(void* dst, const CUtensorMap* map, uint32_t bar_cluster, int nd,
+                                                 const int* c) {
+  const uint32_t d = smem_u32(dst);
+  const uint64_t m = reinterpret_cast<uint64_t>(map);
+  if (nd == 2)
+    asm volatile("cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+                 ::"r"(d), "l"(m), "r"(c[0]), "r"(c[1]), "r"(bar_cluster) : "memory");
+  else if (nd == 3)
+    asm volatile("cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+                 ::"r"(d), "l"(m), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(bar_cluster) : "memory");
+  else if (nd == 4)
+    asm volatile("cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];"
+                 ::"r"(d), "l"(m), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(bar_cluster) : "memory");
+  else
+    asm volatile("cp.async.bulk.tensor.5d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, %6}], [%7];"
+                 ::"r"(d), "l"(m), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(bar_cluster) : "memory");
 }
 
 __device__ __forceinline__ void mma_f16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
@@ -118,12 +153,28 @@ __device__ __forceinline__ bool tc2_tile(uint32_t i, uint32_t pair, uint32_t npa
 
 // epi: 0 = row-major C tile [128 rows][64-column subtiles] (TMA store box {64, 128}),
 //      4 = transposed C^T (layout policy 3, box {128 m, 32 n} at global row m_base + m0)
-template <int BN>
+//
+// kMN: the stem permutation of a step whose stored order is [m_hi | contracted k | m_lo] (m_lo >= 7
+// modes innermost) folded into the operand layout instead of a permutation pass.  With m innermost
+// the real/imaginary parts interleave along m, so the real GEMM is taken over ROWS (m, c):
+//   A'[(m,c)][k] = c-part of A[m,k]  (MN-major: 128 A' rows = 64 complex m are 256 contiguous bytes
+//   per k, loaded as two 3-D TMA boxes {64 halves, 64 k, 1} of the map [m_hi][k][2 m_lo]),
+//   B'[(n,c')][k] = c'-part of b[k,n] (K-major, tn_pad_b_mn),
+//   C'[(m,c)][(n,c')] = sum_k A' B'^T,  Re C = C'[(m,0)][(n,0)] - C'[(m,1)][(n,1)],
+//                                       Im C = C'[(m,0)][(n,1)] + C'[(m,1)][(n,0)]
+// — the same 4 M K N real MACs as Eq. 6, with the complex combination moved
+// from B_P's sign pattern to the epilogue: TMEM lanes 2j / 2j+1 hold the two parts of complex row j,
+// neighbouring threads swap half of their columns (shfl.xor 1) and each writes 8 of every 16
+// complex outputs.  Each CTA's tile is 64 complex rows (the pair: 128), K blocks are 64 complex k.
+template <int BN, bool kMN = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     gemm_chalf_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                           const __grid_constant__ CUtensorMap tmC, uint32_t num_mp, uint32_t num_n, int K2,
                           const float* in_max, const float* b_bound, uint32_t* out_max, int* exp_slot, int epi,
-                          uint64_t m_base, int order, const __grid_constant__ PeerStore ps) {
+                          uint64_t m_base, int order, const __grid_constant__ PeerStore ps,
+                          const __grid_constant__ NdArgs nda, int mn_ma) {
+  // complex rows per CTA tile, per pair tile
+  constexpr int kRows = kMN ? BM / 2 : BM;
   using C = Cfg2<BN>;
   constexpr int KB = C::KB;
   // "no re-run needed" signal of the scale re-run: both CTAs read the same value and leave together
@@ -174,13 +225,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       uint32_t ph = 0;
       int mp, nb;
       for (uint32_t i = 0; tc2_tile(i, pair, npairs, num_mp, num_n, order, mp, nb); ++i) {
-        const int a_row = mp * 256 + (int)rank * BM;
+        const int a_row = mp * 2 * kRows + (int)rank * kRows;
         const int b_row = nb * BN + (int)rank * (BN / 2);
+        int cm[5] = {0, 0, 0, 0, 0};  // N-d A: row part of the box coordinates (global row)
+        if (nda.nd > 0) nd_coords_rows(nda, m_base + (uint64_t)a_row, cm);
         for (int kb = 0; kb < num_k; ++kb) {
           mbar_wait(&empty[s], ph ^ 1);
           if (rank == 0) mbar_expect_tx(&full[s], 2 * C::kStageBytes);
           const uint32_t fb = map_rank(&full[s], 0);
-          tma_load_2d_pair(sA + s * C::kABytes, &tmA, fb, kb * KB, a_row);
+          if constexpr (kMN) {
+            const uint64_t gr = m_base + (uint64_t)a_row;
+            int cc[3] = {(int)(2 * (gr & ((1ull << mn_ma) - 1))), kb * KB, (int)(gr >> mn_ma)};
+            tma_load_nd_pair(sA + s * C::kABytes, &tmA, fb, 3, cc);
+            cc[0] += 64;
+            tma_load_nd_pair(sA + s * C::kABytes + C::kABytes / 2, &tmA, fb, 3, cc);
+          } else if (nda.nd > 0) {
+            int cc[5];
+            nd_coords_k(nda, (uint32_t)kb * (KB / 2), cm, cc);
+            tma_load_nd_pair(sA + s * C::kABytes, &tmA, fb, nda.nd, cc);
+          } else {
+            tma_load_2d_pair(sA + s * C::kABytes, &tmA, fb, kb * KB, a_row);
+          }
           tma_load_2d_pair(sB + s * C::kBBytes, &tmB, fb, kb * KB, b_row);
           if (++s == C::kStages) {
             s = 0;
@@ -203,10 +268,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         for (int kb = 0; kb < num_k; ++kb) {
           mbar_wait(&full[s], ph);
           tc_fence_after();
-          const uint64_t ad = smem_desc_sw<KB>(sA + s * C::kABytes);
           const uint64_t bd = smem_desc_sw<KB>(sB + s * C::kBBytes);
+          if constexpr (kMN) {
+            // 16 k = two 8-k groups = 2 KB further along the MN-major atoms (>>4 => +128)
+            const uint64_t ad = smem_desc_mn_sw128(sA + s * C::kABytes);
 #pragma unroll
-          for (int kk = 0; kk < KB / 16; ++kk) mma_f16_pair(tmem_d, ad + 2 * kk, bd + 2 * kk, C::kIdesc, (kb | kk) != 0);
+            for (int kk = 0; kk < KB / 16; ++kk)
+              mma_f16_pair(tmem_d, ad + 128 * kk, bd + 2 * kk, C::kIdescMN, (kb | kk) != 0);
+          } else {
+            const uint64_t ad = smem_desc_sw<KB>(sA + s * C::kABytes);
+#pragma unroll
+            for (int kk = 0; kk < KB / 16; ++kk)
+              mma_f16_pair(tmem_d, ad + 2 * kk, bd + 2 * kk, C::kIdesc, (kb | kk) != 0);
+          }
           mma_commit_pair(&empty[s]);
           if (++s == C::kStages) {
             s = 0;
@@ -232,7 +306,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     int mp, nb;
     for (uint32_t i = grp; tc2_tile(i, pair, npairs, num_mp, num_n, order, mp, nb); i += 2) {
       const uint32_t acc = i % C::kNAcc, aph = (i / C::kNAcc) & 1;
-      const int m0 = mp * 256 + (int)rank * BM, n0 = nb * BN;
+      const int m0 = mp * 2 * kRows + (int)rank * kRows, n0 = nb * BN;
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
       const uint32_t taddr = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN;
@@ -254,6 +328,44 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int c = sub + 32 * h;
+          if constexpr (kMN) {
+            // lanes 2j (re part of complex row j) and 2j+1 (im part): the even lane finishes columns
+            // 0..7 of these 16 complex columns, the odd lane 8..15, each with its partner's half
+            const int odd = lane & 1, jr = row >> 1;
+            float pv[16];
+#pragma unroll
+            for (int q = 0; q < 16; ++q)
+              pv[q] = __shfl_xor_sync(0xffffffffu, __uint_as_float(odd ? r[h][q] : r[h][16 + q]), 1);  // static indices: no local memory
+            uint32_t pk[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              // x_c'[part]: even: own = part 0 (cols 2q, 2q+1), partner = part 1; odd: own = part 1 at
+              // 16 + 2q, partner = part 0
+              const float a0 = odd ? pv[2 * q] : __uint_as_float(r[h][2 * q]);            // C'[(m,0)][(n,0)]
+              const float a1 = odd ? pv[2 * q + 1] : __uint_as_float(r[h][2 * q + 1]);    // C'[(m,0)][(n,1)]
+              const float b0 = odd ? __uint_as_float(r[h][16 + 2 * q]) : pv[2 * q];        // C'[(m,1)][(n,0)]
+              const float b1 = odd ? __uint_as_float(r[h][17 + 2 * q]) : pv[2 * q + 1];    // C'[(m,1)][(n,1)]
+              const float re = (a0 - b1) * sc, im = (a1 + b0) * sc;
+              __half2 hv = __floats2half2_rn(re, im);
+              mx = fmaxf(mx, fmaxf(fabsf(re), fabsf(im)));
+              pk[q] = *reinterpret_cast<uint32_t*>(&hv);
+            }
+            // complex columns (c & 63) / 2 + 8 odd + q of the 32-column subtile, complex row jr
+            const int q0 = ((c & 63) >> 1) + 8 * odd;
+            if (epi == 4) {
+              uint32_t* st32 = reinterpret_cast<uint32_t*>(sbuf);
+#pragma unroll
+              for (int q = 0; q < 8; ++q) st32[(q0 + q) * kRows + jr] = pk[q];
+            } else {
+              unsigned char* srow = sbuf + jr * 128;
+#pragma unroll
+              for (int q = 0; q < 2; ++q) {
+                const int chunk = ((q0 >> 2) + q) ^ (jr & 7);
+                *reinterpret_cast<uint4*>(srow + chunk * 16) = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+              }
+            }
+            continue;
+          }
           uint32_t pk[16];
 #pragma unroll
           for (int j = 0; j < 16; ++j) {

@@ -153,6 +153,41 @@ void launch_pad_b(__half* bp, const float2* b, int klog, int nlog, const uint32_
   TN_CUDA(cudaGetLastError());
 }
 
+// One warp per column n of B: rows (n,0) = Re b[:, n] and (n,1) = Im b[:, n] of B' [2N][K] (the
+// MN-major GEMM's operand, k_gemm_tc2.cu); the bound is the same column 1-norm as pad_b_kernel's.
+__global__ void pad_b_mn_kernel(__half* __restrict__ bpm, const float2* __restrict__ b, int klog, int nlog,
+                                const uint32_t* bmax_bits, float* b_bound, int* exp_slot) {
+  const int K = 1 << klog, N = 1 << nlog;
+  const int t = bmax_bits ? scale_exp_for(__uint_as_float(*bmax_bits)) : 0;
+  if (exp_slot && blockIdx.x == 0 && threadIdx.x == 0) *exp_slot = t;
+  const float sc = ldexpf(1.f, t);
+  const int warps = blockDim.x >> 5, lane = threadIdx.x & 31;
+  for (int n = blockIdx.x * warps + (threadIdx.x >> 5); n < N; n += gridDim.x * warps) {
+    float l1 = 0.f;
+    __half* r0 = bpm + (size_t)(2 * n) * K;
+    __half* r1 = bpm + (size_t)(2 * n + 1) * K;
+    for (int k = lane; k < K; k += 32) {
+      float2 v = b[(size_t)k * N + n];
+      __half re = __float2half_rn(v.x * sc), im = __float2half_rn(v.y * sc);
+      r0[k] = re;
+      r1[k] = im;
+      l1 += fabsf(__half2float(re)) + fabsf(__half2float(im));
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) l1 += __shfl_xor_sync(0xffffffffu, l1, o);
+    if (lane == 0 && b_bound) atomic_max_pos(reinterpret_cast<uint32_t*>(b_bound), l1);
+  }
+}
+
+void launch_pad_b_mn(__half* bpm, const float2* b, int klog, int nlog, const uint32_t* bmax_bits, float* b_bound,
+                     int* exp_slot, cudaStream_t s) {
+  int N = 1 << nlog;
+  int blocks = (N + 7) / 8;
+  if (blocks > 148 * 4) blocks = 148 * 4;
+  pad_b_mn_kernel<<<blocks, 256, 0, s>>>(bpm, b, klog, nlog, bmax_bits, b_bound, exp_slot);
+  TN_CUDA(cudaGetLastError());
+}
+
 __global__ void c64_to_chalf_kernel(__half2* __restrict__ dst, const float2* __restrict__ src, uint64_t n,
                                     const uint32_t* max_bits, int* exp_slot, uint32_t* out_max) {
   const int e = max_bits ? scale_exp_for(__uint_as_float(*max_bits)) : 0;

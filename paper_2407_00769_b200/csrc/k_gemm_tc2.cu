@@ -9,28 +9,29 @@ bool tc2_enabled() {
   return on;
 }
 
-template <int BN>
+template <int BN, bool kMN>
 static void launch_tc2_t(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, uint32_t num_mp,
                          uint32_t num_n, int K2, const float* in_max, const float* b_bound, uint32_t* out_max,
-                         int* exp_slot, int epi, uint64_t m_base, const PeerStore& ps, cudaStream_t s) {
+                         int* exp_slot, int epi, uint64_t m_base, const PeerStore& ps, const NdArgs& nda,
+                         int mn_ma, cudaStream_t s) {
   using C = tc2::Cfg2<BN>;
   // per device: the shared-memory opt-in and how many CTA pairs can be resident at once (an odd SM
   // count per GPC leaves SMs without a partner, so this can be below #SMs / 2)
   static std::mutex mu;
-  static int max_pairs[64] = {0};
+  static int max_pairs[64] = {0};  // (per instantiation)
   int dev = 0;
   TN_CUDA(cudaGetDevice(&dev));
   int pairs;
   {
     std::lock_guard<std::mutex> lk(mu);
     if (dev >= 64 || max_pairs[dev] == 0) {
-      TN_CUDA(cudaFuncSetAttribute(tc2::gemm_chalf_tc2_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
+      TN_CUDA(cudaFuncSetAttribute(tc2::gemm_chalf_tc2_kernel<BN, kMN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(2 * 128, 1, 1);
       cfg.blockDim = dim3(tc::kThreads, 1, 1);
       cfg.dynamicSmemBytes = C::kSmem;
       int n = 0;
-      TN_CUDA(cudaOccupancyMaxActiveClusters(&n, tc2::gemm_chalf_tc2_kernel<BN>, &cfg));
+      TN_CUDA(cudaOccupancyMaxActiveClusters(&n, tc2::gemm_chalf_tc2_kernel<BN, kMN>, &cfg));
       if (n <= 0) throw TnError{TN_E_CUDA, "CTA-pair GEMM: no resident cluster"};
       if (dev < 64) max_pairs[dev] = n;
       pairs = n;
@@ -51,20 +52,65 @@ static void launch_tc2_t(const CUtensorMap& ma, const CUtensorMap& mb, const CUt
   const int order = order_env >= 0 ? order_env : (a_fits_l2 && num_mp >= 8ull * (uint64_t)pairs ? 1 : 0);
   const uint64_t busy = order == 1 ? std::min<uint64_t>(num_mp, (uint64_t)pairs) : std::min<uint64_t>(tiles, (uint64_t)pairs);
   const int grid = 2 * (int)busy;
-  tc2::gemm_chalf_tc2_kernel<BN><<<grid, tc::kThreads, C::kSmem, s>>>(ma, mb, mc, num_mp, num_n, K2, in_max, b_bound,
-                                                                      out_max, exp_slot, epi, m_base, order, ps);
+  tc2::gemm_chalf_tc2_kernel<BN, kMN><<<grid, tc::kThreads, C::kSmem, s>>>(ma, mb, mc, num_mp, num_n, K2, in_max, b_bound,
+                                                                      out_max, exp_slot, epi, m_base, order, ps, nda, mn_ma);
   TN_CUDA(cudaGetLastError());
 }
 
 void launch_tc2(int BN, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, uint32_t num_mp,
                 uint32_t num_n, int K2, const float* in_max, const float* b_bound, uint32_t* out_max, int* exp_slot,
-                int epi, uint64_t m_base, const PeerStore& ps, cudaStream_t s) {
+                int epi, uint64_t m_base, const PeerStore& ps, const NdArgs& nda, cudaStream_t s) {
   if (BN == 256)
-    launch_tc2_t<256>(ma, mb, mc, num_mp, num_n, K2, in_max, b_bound, out_max, exp_slot, epi, m_base, ps, s);
+    launch_tc2_t<256, false>(ma, mb, mc, num_mp, num_n, K2, in_max, b_bound, out_max, exp_slot, epi, m_base, ps, nda,
+                             0, s);
   else if (BN == 128)
-    launch_tc2_t<128>(ma, mb, mc, num_mp, num_n, K2, in_max, b_bound, out_max, exp_slot, epi, m_base, ps, s);
+    launch_tc2_t<128, false>(ma, mb, mc, num_mp, num_n, K2, in_max, b_bound, out_max, exp_slot, epi, m_base, ps, nda,
+                             0, s);
   else
     throw TnError{TN_E_INVALID, "CTA-pair GEMM: BN must be 128 or 256"};
+}
+
+// MN-major A (gemm_tc2.cuh, kMN): the stem stored as [M >> ma][K][2^ma] complex (the step's kept
+// modes m_lo = 2^ma innermost, then its contracted modes, then the other kept modes) contracted
+// without a permutation pass.  bpm = B' [2N][K] fp16 (tn_pad_b_mn).  K2 (the kernel's k count)
+// is K: one stage = 64 complex k.
+bool mn_gemm_supported(uint64_t M, uint32_t K, uint32_t N, int ma, const OutMap* om) {
+  if (!tc2_enabled() || ma < 7 || K < 64 || (K & (K - 1)) || N < 64 || (N & (N - 1)) || M % 128 || M >= (1ull << 31))
+    return false;
+  if (om && !om->identity && !om->transposed) return false;
+  return (1ull << ma) <= M;
+}
+
+void launch_gemm_chalf_mn(__half* c, const __half* a, const __half* bpm, uint64_t M, uint32_t K, uint32_t N, int ma,
+                          const float* in_max, const float* b_bound, uint32_t* out_max, int* exp_slot,
+                          const OutMap* om, cudaStream_t s) {
+  if (!mn_gemm_supported(M, K, N, ma, om)) throw TnError{TN_E_INVALID, "MN-major GEMM: unsupported geometry"};
+  const bool transposed = om && om->transposed;
+  const uint32_t N2 = 2 * N;
+  const int BN = N2 >= 256 ? 256 : 128;
+  CUtensorMap ma_map;
+  {
+    cuuint64_t dims[3] = {2ull << ma, K, M >> ma};
+    cuuint64_t strides[2] = {4ull << ma, (4ull << ma) * K};
+    cuuint32_t box[3] = {64, 64, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = get_encode()(&ma_map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<__half*>(a), dims, strides, box,
+                              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw TnError{TN_E_CUDA, "cuTensorMapEncodeTiled (MN-major A) failed"};
+  }
+  const CUtensorMap mb = make_map_2d(bpm, K, N2, 64, BN / 2);
+  const CUtensorMap mc = transposed ? make_map_t(c, M, N, 64) : make_map_2d(c, N2, M, 64, 64);
+  const PeerStore ps = make_peer_store(om ? om->peer : nullptr, true, transposed, M, N2, 64);
+  NdArgs nda;
+  memset(&nda, 0, sizeof(nda));
+  const uint32_t num_mp = (uint32_t)(M / 128), num_n = N2 / BN;
+  if (BN == 256)
+    launch_tc2_t<256, true>(ma_map, mb, mc, num_mp, num_n, (int)K, in_max, b_bound, out_max, exp_slot,
+                            transposed ? 4 : 0, 0, ps, nda, ma, s);
+  else
+    launch_tc2_t<128, true>(ma_map, mb, mc, num_mp, num_n, (int)K, in_max, b_bound, out_max, exp_slot,
+                            transposed ? 4 : 0, 0, ps, nda, ma, s);
 }
 
 }  // namespace tn

@@ -542,7 +542,24 @@ static Plan* load_plan_fixed(const char* json, size_t len, const tn_config* cfg_
         const bool fusable = !cfg.no_gather && !st.sparse && tc_k && kl >= 3 && kept.size() >= 7 && L.size() >= 2 &&
                              ((bs.count(L[L.size() - 1]) && bs.count(L[L.size() - 2])) || word_ok) &&
                              (split_set.empty() || (int)s < p.split_from);
-        if (!fusable) by_next_use(kept);
+        // MN-major operand: stored order [kept | R | >= 7 kept], K >= 64, N >= 64 (2N >= 128: the
+        // CTA-pair kernel's B tile), complex-half, not in a split tail or sparse tail
+        {
+          int ma = 0;
+          while (ma < (int)L.size() && !bs.count(L[L.size() - 1 - ma])) ++ma;
+          // only where a pass would be expensive (>= 2^28 elements): the fold keeps the kept modes in
+          // stored order, which forgoes the pass's next-use ordering of them for the later steps
+          static const int mn_min = getenv("TN_MN_MIN_LOG2") ? atoi(getenv("TN_MN_MIN_LOG2")) : 28;  // tuning knob
+          bool block = ma >= 7 && kl >= 6 && nl >= 6 && (int)kept.size() >= 8 && (int)L.size() >= mn_min;
+          for (int q = 0; block && q < kl; ++q) block = bs.count(L[L.size() - 1 - ma - q]) > 0;
+          static const bool mn_off = getenv("TN_NO_MN") != nullptr;  // A/B knob
+          if (block && !mn_off && !fusable && cfg.dtype == TN_CHALF && !st.sparse && tc_k && !cfg.no_gather &&
+              (split_set.empty() || (int)s < p.split_from)) {
+            st.mn = true;
+            st.mn_ma = ma;
+          }
+        }
+        if (!fusable && !st.mn) by_next_use(kept);
         std::vector<int> PL = kept;
         PL.insert(PL.end(), R.begin(), R.end());
         st.perm = true;
@@ -658,7 +675,7 @@ static Plan* load_plan_fixed(const char* json, size_t len, const tn_config* cfg_
       double M = std::ldexp(1.0, st.mlog), K = std::ldexp(1.0, st.klog), N = std::ldexp(1.0, st.nlog);
       p.stem_flops += 8.0 * M * K * N;
       p.stem_bytes_alg += eb * (M * K + M * N) + 8.0 * K * N;
-      if (st.perm) {
+      if (st.perm && !st.mn) {
         p.perm_bytes += 2.0 * eb * M * K;
         p.n_permutes++;
       }
@@ -870,7 +887,7 @@ std::string report_json(const Plan& p, const std::vector<float>& ms) {
       << ",\"tc\":" << (s.tensor_core ? 1 : 0) << ",\"ga\":" << (s.gather_a ? 1 : 0) << ",\"split\":" << s.split << ",\"swap\":" << (s.swap ? 1 : 0)
       << ",\"quant\":" << (s.quant ? 1 : 0) << ",\"sparse\":" << s.sparse
       << ",\"fuse_quant\":" << (s.fuse_quant ? 1 : 0)
-      << ",\"out_kind\":" << (s.out_identity ? 0 : (s.out_transposed ? 1 : 2))
+      << ",\"out_kind\":" << (s.out_identity ? 0 : (s.out_transposed ? 1 : 2)) << ",\"mn\":" << (s.mn ? s.mn_ma : 0)
       << ",\"in\":";
     jlist(o, s.in_layout);
     o << ",\"R\":";

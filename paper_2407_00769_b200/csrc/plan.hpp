@@ -49,6 +49,11 @@ struct StemStep {
   // sum bit_j(k) a_k_stride[j] of the UNPERMUTED in_layout (perm == false then)
   bool gather_a = false;
   std::vector<int64_t> a_m_stride, a_k_stride;
+  // stored order [other kept | R | mn_ma kept modes] (mn_ma >= 7): the permutation is folded into an
+  // MN-major A operand (k_gemm_tc2.cu launch_gemm_chalf_mn, B' via launch_pad_b_mn) when the launch
+  // geometry allows (runtime mn_active); perm / perm_axes stay as the fallback
+  bool mn = false;
+  int mn_ma = 0;
   // output address of C[m, n] = sum_j bit_j(m) m_stride[j] + sum_j bit_j(n) n_stride[j] (elements)
   std::vector<int64_t> m_stride, n_stride;
   bool out_identity = true;       // out_layout == kept ++ newl (plain row-major [M][N])

@@ -513,6 +513,17 @@ void run_common(const Plan& p, unsigned char* W, cudaStream_t s) {
 // the branch with those legs fixed to the bits of b (MSB = first leg), i.e. a slice of it.  All
 // blocks share one power-of-two scale (the max over every block), so the batched GEMM has one
 // exponent per step.
+// The step's permutation folded into an MN-major A operand (StemStep::mn): decided the same way for
+// the operand preparation (B') and the launch (no permutation pass, launch_gemm_chalf_mn).
+bool mn_active(const Plan& p, const StemStep& st) {
+  if (!st.mn || p.cfg.dtype != TN_CHALF || !st.tensor_core || st.split || st.sparse) return false;
+  OutMap om;
+  memset(&om, 0, sizeof(om));
+  om.identity = st.out_identity ? 1 : 0;
+  om.transposed = st.out_transposed ? 1 : 0;
+  return mn_gemm_supported(1ull << st.mlog, 1u << st.klog, 1u << st.nlog, st.mn_ma, &om);
+}
+
 void prepare_b_sparse(const Plan& p, const StemStep& st, size_t i, unsigned char* W, const Scratch& sc, cudaStream_t s) {
   View v = view_of(p, st.branch, W);
   const int nsp = (int)st.b_sparse.size();
@@ -583,8 +594,12 @@ void prepare_b(const Plan& p, unsigned char* W, const Scratch& sc, cudaStream_t 
       if (st.nlog < 3)  // zero the padding rows of B_P (tcgen05 needs N >= 16 real columns)
         TN_CUDA(cudaMemsetAsync(W + st.b_off, 0, 64ull << st.klog, s));
       launch_max_abs_f32(reinterpret_cast<const float*>(g.dst), 2 * kn, &sc.b_max[i], s);
-      launch_pad_b(reinterpret_cast<__half*>(W + st.b_off), g.dst, st.klog, st.nlog, &sc.b_max[i], &sc.b_bound[i],
-                   &sc.exps[1 + 2 * i], s);
+      if (mn_active(p, st))
+        launch_pad_b_mn(reinterpret_cast<__half*>(W + st.b_off), g.dst, st.klog, st.nlog, &sc.b_max[i],
+                        &sc.b_bound[i], &sc.exps[1 + 2 * i], s);
+      else
+        launch_pad_b(reinterpret_cast<__half*>(W + st.b_off), g.dst, st.klog, st.nlog, &sc.b_max[i], &sc.b_bound[i],
+                     &sc.exps[1 + 2 * i], s);
     }
   }
 }
@@ -774,7 +789,11 @@ void run_gemm_once(Plan& p, const StemStep& st, size_t i, const void* src, void*
       for (int j = 0; j < st.mlog; ++j) ag.ms[j] = st.a_m_stride[j];
       for (int j = 0; j < st.klog; ++j) ag.ks[j] = st.a_k_stride[j];
     }
-    if (st.tensor_core)
+    if (mshift == 0 && mn_active(p, st))
+      launch_gemm_chalf_mn(reinterpret_cast<__half*>(dst), reinterpret_cast<const __half*>(src),
+                           reinterpret_cast<const __half*>(W + st.b_off), M, K, N, st.mn_ma, in_max, &sc.b_bound[i],
+                           out_max, exp_slot, &om, s);
+    else if (st.tensor_core)
       launch_gemm_chalf_tc(reinterpret_cast<__half*>(dst), reinterpret_cast<const __half*>(src),
                            reinterpret_cast<const __half*>(W + st.b_off), M, 2 * K, 2 * N, in_max, &sc.b_bound[i],
                            out_max, exp_slot, &om, s, st.gather_a ? &ag : nullptr);
@@ -862,7 +881,7 @@ void stem_body(Plan& p, const tn_buffers* b, cudaStream_t s, bool head = true, b
       mode_swap(p, st, b, cur, s);
     }
     swapped = false;
-    if (st.perm) {
+    if (st.perm && !mn_active(p, st)) {
       launch_permute(b->d_stem[1 - cur], b->d_stem[cur], eb, (int)st.in_layout.size(), st.perm_axes.data(), s);
       ++p.launches;
       cur = 1 - cur;
@@ -1770,6 +1789,35 @@ int tn_gemm_chalf_padded(void* d_c, const void* d_a, const void* d_bp, uint64_t 
 int tn_gemm_cfloat(void* d_c, const void* d_a, const void* d_b, uint64_t M, uint32_t K, uint32_t N, void* stream) {
   if (!d_c || !d_a || !d_b) return fail(TN_E_INVALID, "NULL argument");
   TN_TRY(launch_gemm_c64((float2*)d_c, (const float2*)d_a, (const float2*)d_b, M, K, N, nullptr, (cudaStream_t)stream));
+}
+
+int tn_gemm_chalf_mn(void* d_c, const void* d_a, const void* d_bpm, uint64_t M, uint32_t K, uint32_t N, int ma,
+                     const float* d_in_max, const float* d_b_bound, uint32_t* d_out_max, int* d_exp, void* stream) {
+  if (!d_c || !d_a || !d_bpm) return fail(TN_E_INVALID, "NULL argument");
+  if (!mn_gemm_supported(M, K, N, ma, nullptr)) return fail(TN_E_INVALID, "MN-major GEMM: unsupported geometry");
+  TN_TRY({
+    const float* im = (d_in_max && d_b_bound) ? d_in_max : nullptr;
+    const float* bb = (d_in_max && d_b_bound) ? d_b_bound : nullptr;
+    launch_gemm_chalf_mn((__half*)d_c, (const __half*)d_a, (const __half*)d_bpm, M, K, N, ma, im, bb, d_out_max,
+                         d_exp, nullptr, (cudaStream_t)stream);
+  });
+}
+
+int tn_pad_b_mn(void* d_bpm, const void* d_b, uint32_t K, uint32_t N, float* d_b_bound, int* d_exp, void* d_scratch,
+                void* stream) {
+  if (!d_bpm || !d_b || !d_scratch) return fail(TN_E_INVALID, "NULL argument");
+  if (!K || !N || (K & (K - 1)) || (N & (N - 1))) return fail(TN_E_INVALID, "K and N must be powers of two");
+  TN_TRY({
+    cudaStream_t s = (cudaStream_t)stream;
+    int klog = 0, nlog = 0;
+    while ((1u << klog) < K) ++klog;
+    while ((1u << nlog) < N) ++nlog;
+    uint32_t* mx = static_cast<uint32_t*>(d_scratch);
+    TN_CUDA(cudaMemsetAsync(mx, 0, 4, s));
+    if (d_b_bound) TN_CUDA(cudaMemsetAsync(d_b_bound, 0, 4, s));
+    launch_max_abs_f32((const float*)d_b, 2ull * K * N, mx, s);
+    launch_pad_b_mn((__half*)d_bpm, (const float2*)d_b, klog, nlog, d_exp ? mx : nullptr, d_b_bound, d_exp, s);
+  });
 }
 
 int tn_pad_b(void* d_bp, const void* d_b, uint32_t K, uint32_t N, float* d_b_bound, int* d_exp, void* d_scratch,

@@ -79,6 +79,8 @@ def lib():
         L.tn_gemm_chalf_padded.argtypes = [vp, vp, vp, u64, C.c_uint32, C.c_uint32, u64, vp, i32, u64,
                                            vp, vp, vp, vp, vp]
         L.tn_pad_b.argtypes = [vp, vp, C.c_uint32, C.c_uint32, vp, vp, vp, vp]
+        L.tn_pad_b_mn.argtypes = [vp, vp, C.c_uint32, C.c_uint32, vp, vp, vp, vp]
+        L.tn_gemm_chalf_mn.argtypes = [vp, vp, vp, u64, C.c_uint32, C.c_uint32, i32, vp, vp, vp, vp, vp]
         L.tn_quant_int8.argtypes = [vp, vp, vp, vp, u64, i32, vp]
         L.tn_dequant_int8.argtypes = [vp, vp, vp, vp, u64, i32, vp]
         L.tn_quant_int8_f16.argtypes = [vp, vp, vp, vp, u64, i32, vp]
@@ -296,6 +298,15 @@ def tn_gemm_chalf_padded(c, a, bp, M, K, N, table, n_b, in_max=None, b_bound=Non
 
 def tn_gemm_cfloat(c, a, b, M, K, N, stream=None):
     _check(lib().tn_gemm_cfloat(_ptr(c), _ptr(a), _ptr(b), M, K, N, _stream(stream)))
+
+
+def tn_gemm_chalf_mn(c, a, bpm, M, K, N, ma, in_max=None, b_bound=None, out_max=None, exp=None, stream=None):
+    _check(lib().tn_gemm_chalf_mn(_ptr(c), _ptr(a), _ptr(bpm), M, K, N, ma, _ptr(in_max), _ptr(b_bound),
+                                  _ptr(out_max), _ptr(exp), _stream(stream)))
+
+
+def tn_pad_b_mn(bpm, b, K, N, b_bound=None, exp=None, scratch=None, stream=None):
+    _check(lib().tn_pad_b_mn(_ptr(bpm), _ptr(b), K, N, _ptr(b_bound), _ptr(exp), _ptr(scratch), _stream(stream)))
 
 
 def tn_pad_b(bp, b, K, N, b_bound=None, exp=None, scratch=None, stream=None):

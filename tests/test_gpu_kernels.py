@@ -214,6 +214,61 @@ def test_pad_b_and_scaled_gemm(env, M):
     assert abs(mx - np.abs(got).max()) <= 2.0 ** -11 * np.abs(got).max()
 
 
+@pytest.mark.parametrize("M,K,N,ma", [(128, 64, 64, 7), (1024, 64, 128, 7), (4096, 128, 256, 9),
+                                      (2048, 512, 512, 8), (1 << 14, 64, 64, 14)])
+def test_gemm_chalf_mn_exact(env, M, K, N, ma):
+    """The permutation folded into an MN-major operand (tn_gemm_chalf_mn): A stored [M >> ma][K][2^ma]
+    (kept modes innermost, the contracted ones next).  Integer operands in [-1, 1]: every product and
+    sum is exact, so C equals a @ b bit for bit, and the scaled launch equals the Eq. 6 path
+    (tn_gemm_chalf on the explicitly permuted A with B_P) bit for bit, exponent and max included."""
+    torch, tn = env
+    rng = np.random.default_rng(M + K + N)
+    x = rng.integers(-1, 2, (M >> ma, K, 1 << ma)) + 1j * rng.integers(-1, 2, (M >> ma, K, 1 << ma))
+    a = np.transpose(x, (0, 2, 1)).reshape(M, K)                     # a[m, k], m = (hi, lo)
+    b = rng.integers(-1, 2, (K, N)) + 1j * rng.integers(-1, 2, (K, N))
+    B = torch.from_numpy(b.astype(np.complex64).view(np.float32).reshape(-1)).cuda()
+    BPM = torch.empty(2 * N * K, dtype=torch.float16, device="cuda")
+    scratch = torch.zeros(4, dtype=torch.int32, device="cuda")
+    tn.tn_pad_b_mn(BPM, B, K, N, None, None, scratch)
+    torch.cuda.synchronize()
+    exp_bpm = np.stack([b.real.T, b.imag.T], axis=1).reshape(2 * N, K).astype(np.float16)
+    assert np.array_equal(BPM.cpu().numpy().reshape(2 * N, K), exp_bpm)
+    X = torch.from_numpy(_half_pairs(x.reshape(1, -1)).reshape(-1)).cuda()
+    C = torch.full((M * 2 * N,), float("nan"), dtype=torch.float16, device="cuda")
+    tn.tn_gemm_chalf_mn(C, X, BPM, M, K, N, ma)
+    torch.cuda.synchronize()
+    got = C.cpu().numpy().astype(np.float64).reshape(M, N, 2)
+    ref = a @ b
+    assert np.array_equal(got[..., 0], ref.real) and np.array_equal(got[..., 1], ref.imag)
+    # scaled: the same exponent, values and realised max as the Eq. 6 GEMM on the permuted operand
+    bound = torch.zeros(1, dtype=torch.float32, device="cuda")
+    ex = torch.zeros(4, dtype=torch.int32, device="cuda")
+    tn.tn_pad_b_mn(BPM, B, K, N, bound, ex[0:], scratch)
+    BP = torch.empty(4 * K * N, dtype=torch.float16, device="cuda")
+    bound2 = torch.zeros(1, dtype=torch.float32, device="cuda")
+    tn.tn_pad_b(BP, B, K, N, bound2, ex[1:], scratch)
+    in_max = torch.tensor([1.0], device="cuda")
+    om1 = torch.zeros(1, dtype=torch.int32, device="cuda")
+    om2 = torch.zeros(1, dtype=torch.int32, device="cuda")
+    C2 = torch.empty_like(C)
+    tn.tn_gemm_chalf_mn(C, X, BPM, M, K, N, ma, in_max, bound, om1, ex[2:])
+    tn.tn_gemm_chalf(C2, torch.from_numpy(_half_pairs(a).reshape(-1)).cuda(), BP, M, K, N, in_max, bound2, om2,
+                     ex[3:])
+    torch.cuda.synchronize()
+    assert float(bound.item()) == float(bound2.item())
+    assert int(ex[2].item()) == int(ex[3].item())
+    assert torch.equal(C, C2)
+    assert int(om1.item()) == int(om2.item())
+
+
+def test_gemm_chalf_mn_rejects_bad_geometry(env):
+    torch, tn = env
+    t = torch.zeros(16, dtype=torch.float16, device="cuda")
+    for M, K, N, ma in ((1024, 32, 64, 7), (1024, 64, 32, 7), (1024, 64, 64, 6), (1000, 64, 64, 7), (64, 64, 64, 7)):
+        with pytest.raises(tn.TnError):
+            tn.tn_gemm_chalf_mn(t, t, t, M, K, N, ma)
+
+
 @pytest.mark.parametrize("M,K,N", [(1, 1, 1), (100, 3, 5), (1000, 64, 64), (4097, 128, 33)])
 def test_gemm_cfloat(env, M, K, N):
     torch, tn = env
@@ -358,7 +413,9 @@ def test_gemm_chalf_gathered_word_pieces_exact(env, runs, N):
 
 @pytest.mark.parametrize("runs,N", [("k2m8k5m5", 32), ("k3m8k2m5", 16), ("k4m4k4m7", 64), ("k5m7k2m3", 8),
                                     ("k7m9", 256), ("k2m3k3m9", 4), ("k2m7k1m1k3m2", 64), ("k4m2k3m8", 2),
-                                    ("k3m1k4m9", 128), ("k2m12k4", 16)])
+                                    ("k3m1k4m9", 128), ("k2m12k4", 16),
+                                    # 128-byte rows, N >= 128, M % 256 == 0: the CTA-pair kernel's N-d box
+                                    ("k5m9k2m4", 128), ("k6m8k3m5", 256)])
 def test_gemm_chalf_gathered_runs_exact(env, runs, N):
     """Stem layouts as they occur on the C3 path (runs of contracted k / kept m modes, innermost
     first, kept modes in stored order): these go through the N-dimensional TMA box (swizzled rows
