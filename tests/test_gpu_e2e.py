@@ -297,3 +297,29 @@ def test_c3_subslice_policies_vs_oracle(tn, policy):
     ref = contract.contract(load(sub), 0)
     got, p = run_gpu(tn, sub, 0, 0, stem_min_log2=16, policy=policy)
     assert metrics.rel_l2(got, ref) <= 2e-2
+
+
+def test_mn_major_steps_vs_oracle(tn):
+    """Steps stored [kept | contracted | >= 7 kept] run on the MN-major operand (no permutation pass,
+    k_gemm_tc2.cu): C3 sub-sliced to 2^24 with the fold enabled down to 2^18-element steps, one GPU
+    and 4 loopback ranks, against the oracle (fp16 bound) and against the same lowering with the
+    fold off (the same sums in another fp32 order)."""
+    import subprocess
+    import sys
+    import tempfile
+    sub = MP.sub_slice(_plan("c3"), 24)
+    ref = contract.contract(load(sub), 0)
+    got = {}
+    for mode, env in (("mn", {"TN_MN_MIN_LOG2": "18"}), ("pass", {"TN_NO_MN": "1"})):
+        with tempfile.NamedTemporaryFile(suffix=".npz", delete=False) as f:
+            path = f.name
+        r = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "mn_worker.py"), path],
+                           env=dict(os.environ, **env), capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+        got[mode] = np.load(path)
+    assert len(got["mn"]["mn_one"]) >= 1 and len(got["mn"]["mn_four"]) >= 1
+    assert len(got["pass"]["mn_one"]) == 0
+    for key in ("one", "four"):
+        assert metrics.rel_l2(got["mn"][key], ref) <= 2e-2
+        assert metrics.rel_l2(got["pass"][key], ref) <= 2e-2
+
