@@ -166,13 +166,26 @@ __device__ __forceinline__ bool tc2_tile(uint32_t i, uint32_t pair, uint32_t npa
 // from B_P's sign pattern to the epilogue: TMEM lanes 2j / 2j+1 hold the two parts of complex row j,
 // neighbouring threads swap half of their columns (shfl.xor 1) and each writes 8 of every 16
 // complex outputs.  Each CTA's tile is 64 complex rows (the pair: 128), K blocks are 64 complex k.
+// Output row permutation of an MN-major step (the kept modes above its 64-row tile written in
+// next-use order, plan.cpp): store row = sum_j bit_j(m) << p[j] (p[j] = j for j < 6)
+struct RowPerm {
+  int on, nb;
+  int8_t p[64];
+};
+
+__device__ __forceinline__ uint64_t row_perm(const RowPerm& rp, uint64_t m) {
+  uint64_t r = m & 63;
+  for (int j = 6; j < rp.nb; ++j) r |= ((m >> j) & 1ull) << rp.p[j];
+  return r;
+}
+
 template <int BN, bool kMN = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     gemm_chalf_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                           const __grid_constant__ CUtensorMap tmC, uint32_t num_mp, uint32_t num_n, int K2,
                           const float* in_max, const float* b_bound, uint32_t* out_max, int* exp_slot, int epi,
                           uint64_t m_base, int order, const __grid_constant__ PeerStore ps,
-                          const __grid_constant__ NdArgs nda, int mn_ma) {
+                          const __grid_constant__ NdArgs nda, int mn_ma, const __grid_constant__ RowPerm rp) {
   // complex rows per CTA tile, per pair tile
   constexpr int kRows = kMN ? BM / 2 : BM;
   using C = Cfg2<BN>;
@@ -401,6 +414,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               tma_store_2d(&ps.maps[v], sbuf, (int)gm, (int)nc);
             else
               tma_store_2d(&ps.maps[v], sbuf, (int)(2 * nc), (int)gm);
+          } else if (kMN && rp.on) {
+            const uint64_t gm = row_perm(rp, m_base + (uint64_t)m0);
+            if (epi == 4)
+              tma_store_2d(&tmC, sbuf, (int)gm, (n0 + sub) >> 1);
+            else
+              tma_store_2d(&tmC, sbuf, n0 + sub, (int)gm);
           } else if (epi == 4) {
             tma_store_2d(&tmC, sbuf, (int)(m_base + (uint64_t)m0), (n0 + sub) >> 1);
           } else {

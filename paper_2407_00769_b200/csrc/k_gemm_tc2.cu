@@ -13,7 +13,7 @@ template <int BN, bool kMN>
 static void launch_tc2_t(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, uint32_t num_mp,
                          uint32_t num_n, int K2, const float* in_max, const float* b_bound, uint32_t* out_max,
                          int* exp_slot, int epi, uint64_t m_base, const PeerStore& ps, const NdArgs& nda,
-                         int mn_ma, cudaStream_t s) {
+                         int mn_ma, const tc2::RowPerm& rp, cudaStream_t s) {
   using C = tc2::Cfg2<BN>;
   // per device: the shared-memory opt-in and how many CTA pairs can be resident at once (an odd SM
   // count per GPC leaves SMs without a partner, so this can be below #SMs / 2)
@@ -53,7 +53,7 @@ static void launch_tc2_t(const CUtensorMap& ma, const CUtensorMap& mb, const CUt
   const uint64_t busy = order == 1 ? std::min<uint64_t>(num_mp, (uint64_t)pairs) : std::min<uint64_t>(tiles, (uint64_t)pairs);
   const int grid = 2 * (int)busy;
   tc2::gemm_chalf_tc2_kernel<BN, kMN><<<grid, tc::kThreads, C::kSmem, s>>>(ma, mb, mc, num_mp, num_n, K2, in_max, b_bound,
-                                                                      out_max, exp_slot, epi, m_base, order, ps, nda, mn_ma);
+                                                                      out_max, exp_slot, epi, m_base, order, ps, nda, mn_ma, rp);
   TN_CUDA(cudaGetLastError());
 }
 
@@ -62,10 +62,10 @@ void launch_tc2(int BN, const CUtensorMap& ma, const CUtensorMap& mb, const CUte
                 int epi, uint64_t m_base, const PeerStore& ps, const NdArgs& nda, cudaStream_t s) {
   if (BN == 256)
     launch_tc2_t<256, false>(ma, mb, mc, num_mp, num_n, K2, in_max, b_bound, out_max, exp_slot, epi, m_base, ps, nda,
-                             0, s);
+                             0, tc2::RowPerm{}, s);
   else if (BN == 128)
     launch_tc2_t<128, false>(ma, mb, mc, num_mp, num_n, K2, in_max, b_bound, out_max, exp_slot, epi, m_base, ps, nda,
-                             0, s);
+                             0, tc2::RowPerm{}, s);
   else
     throw TnError{TN_E_INVALID, "CTA-pair GEMM: BN must be 128 or 256"};
 }
@@ -74,10 +74,50 @@ void launch_tc2(int BN, const CUtensorMap& ma, const CUtensorMap& mb, const CUte
 // modes m_lo = 2^ma innermost, then its contracted modes, then the other kept modes) contracted
 // without a permutation pass.  bpm = B' [2N][K] fp16 (tn_pad_b_mn).  K2 (the kernel's k count)
 // is K: one stage = 64 complex k.
+// Output of an MN-major step: 0 = row-major C[m][n], 1 = transposed C[n][m], each optionally with
+// its m bits >= 6 permuted (rp: the kept modes above the 64-row tile in next-use order); -1 = other.
+static int mn_out_kind(const OutMap* om, uint64_t M, uint32_t N, tc2::RowPerm* rp) {
+  tc2::RowPerm r;
+  memset(&r, 0, sizeof(r));
+  int kind = 0;
+  if (om && !om->identity) {
+    if (om->transposed) {
+      kind = 1;
+    } else {
+      // row-permuted identity (ns = 1 << j, ms = N << p_j) or transposed (ns = M << j, ms = 1 << p_j)
+      bool ident = true, trans = true;
+      for (int j = 0; j < om->nbits; ++j) {
+        ident = ident && om->ns[j] == ((int64_t)1 << j);
+        trans = trans && om->ns[j] == ((int64_t)M << j);
+      }
+      if (!ident && !trans) return -1;
+      kind = ident ? 0 : 1;
+      const int64_t unit = ident ? (int64_t)N : 1;
+      uint64_t seen = 0;
+      r.nb = om->mbits;
+      if (r.nb > 64) return -1;
+      for (int j = 0; j < om->mbits; ++j) {
+        const int64_t st = om->ms[j];
+        if (st <= 0 || st % unit) return -1;
+        const int64_t q = st / unit;
+        if (q & (q - 1)) return -1;
+        int p = 0;
+        while (((int64_t)1 << p) < q) ++p;
+        if (p >= om->mbits || ((seen >> p) & 1) || (j < 6 && p != j)) return -1;
+        seen |= 1ull << p;
+        r.p[j] = (int8_t)p;
+      }
+      r.on = 1;
+    }
+  }
+  if (rp) *rp = r;
+  return kind;
+}
+
 bool mn_gemm_supported(uint64_t M, uint32_t K, uint32_t N, int ma, const OutMap* om) {
   if (!tc2_enabled() || ma < 7 || K < 64 || (K & (K - 1)) || N < 64 || (N & (N - 1)) || M % 128 || M >= (1ull << 31))
     return false;
-  if (om && !om->identity && !om->transposed) return false;
+  if (mn_out_kind(om, M, N, nullptr) < 0) return false;
   return (1ull << ma) <= M;
 }
 
@@ -85,7 +125,8 @@ void launch_gemm_chalf_mn(__half* c, const __half* a, const __half* bpm, uint64_
                           const float* in_max, const float* b_bound, uint32_t* out_max, int* exp_slot,
                           const OutMap* om, cudaStream_t s) {
   if (!mn_gemm_supported(M, K, N, ma, om)) throw TnError{TN_E_INVALID, "MN-major GEMM: unsupported geometry"};
-  const bool transposed = om && om->transposed;
+  tc2::RowPerm rp;
+  const bool transposed = mn_out_kind(om, M, N, &rp) == 1;
   const uint32_t N2 = 2 * N;
   const int BN = N2 >= 256 ? 256 : 128;
   CUtensorMap ma_map;
@@ -101,16 +142,17 @@ void launch_gemm_chalf_mn(__half* c, const __half* a, const __half* bpm, uint64_
   }
   const CUtensorMap mb = make_map_2d(bpm, K, N2, 64, BN / 2);
   const CUtensorMap mc = transposed ? make_map_t(c, M, N, 64) : make_map_2d(c, N2, M, 64, 64);
-  const PeerStore ps = make_peer_store(om ? om->peer : nullptr, true, transposed, M, N2, 64);
+  // (peer stores only for an unpermuted output: a fused swap's member bits are output-row bits)
+  const PeerStore ps = make_peer_store(om ? om->peer : nullptr, !rp.on, transposed, M, N2, 64);
   NdArgs nda;
   memset(&nda, 0, sizeof(nda));
   const uint32_t num_mp = (uint32_t)(M / 128), num_n = N2 / BN;
   if (BN == 256)
     launch_tc2_t<256, true>(ma_map, mb, mc, num_mp, num_n, (int)K, in_max, b_bound, out_max, exp_slot,
-                            transposed ? 4 : 0, 0, ps, nda, ma, s);
+                            transposed ? 4 : 0, 0, ps, nda, ma, rp, s);
   else
     launch_tc2_t<128, true>(ma_map, mb, mc, num_mp, num_n, (int)K, in_max, b_bound, out_max, exp_slot,
-                            transposed ? 4 : 0, 0, ps, nda, ma, s);
+                            transposed ? 4 : 0, 0, ps, nda, ma, rp, s);
 }
 
 }  // namespace tn

@@ -609,7 +609,20 @@ static Plan* load_plan_fixed(const char* json, size_t len, const tn_config* cfg_
         newl = nord;
       } else {
         by_next_use(newl);
-        out = kept;
+        // kept modes in the output: M order.  TN_MN_ROWPERM=1 (opt-in): after an MN-major step (M order
+        // = stored order) every kept mode above the 64-row tile goes by next use, as a pass would have
+        // ordered them, and the epilogue places each tile at its permuted row (RowPerm).  Measured on
+        // C3 (3 interleaved reps): 277 ms with it vs 270 ms without (the 6 tile modes stay in stored
+        // order either way, so the later layouts still differ from the pass path's), hence off.
+        std::vector<int> kout = kept;
+        static const bool rowperm_on = getenv("TN_MN_ROWPERM") && atoi(getenv("TN_MN_ROWPERM")) == 1;
+        if (st.mn && rowperm_on) {
+          std::vector<int> hi(kept.begin(), kept.end() - 6);
+          by_next_use(hi);
+          kout = hi;
+          kout.insert(kout.end(), kept.end() - 6, kept.end());
+        }
+        out = kout;
         out.insert(out.end(), newl.begin(), newl.end());
         if (policy == 3 && !st.sparse && s + 1 < step_nodes.size() &&
             (split_set.empty() || (int)s + 1 < p.split_from)) {
@@ -624,7 +637,7 @@ static Plan* load_plan_fixed(const char* json, size_t len, const tn_config* cfg_
             return h;
           };
           std::vector<int> tr = newl;
-          tr.insert(tr.end(), kept.begin(), kept.end());
+          tr.insert(tr.end(), kout.begin(), kout.end());
           const int hid = inner_hits(out), htr = inner_hits(tr);
           if (htr > hid && (htr == (int)Rn.size() || htr >= 2) && kept.size() >= 5) out = tr;
         }

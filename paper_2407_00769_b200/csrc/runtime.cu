@@ -515,12 +515,23 @@ void run_common(const Plan& p, unsigned char* W, cudaStream_t s) {
 // exponent per step.
 // The step's permutation folded into an MN-major A operand (StemStep::mn): decided the same way for
 // the operand preparation (B') and the launch (no permutation pass, launch_gemm_chalf_mn).
-bool mn_active(const Plan& p, const StemStep& st) {
-  if (!st.mn || p.cfg.dtype != TN_CHALF || !st.tensor_core || st.split || st.sparse) return false;
+// Output address map of a stem step (the whole step, or one chunk of a split tail: mshift > 0)
+OutMap step_outmap(const StemStep& st, int mshift) {
+  const int mlog = st.mlog - mshift;
   OutMap om;
   memset(&om, 0, sizeof(om));
   om.identity = st.out_identity ? 1 : 0;
-  om.transposed = st.out_transposed ? 1 : 0;
+  om.transposed = (st.out_transposed && mshift == 0) ? 1 : 0;
+  om.mbits = mlog;
+  om.nbits = st.nlog;
+  for (int j = 0; j < mlog; ++j) om.ms[j] = st.m_stride[j];
+  for (int j = 0; j < st.nlog; ++j) om.ns[j] = st.n_stride[j];
+  return om;
+}
+
+bool mn_active(const Plan& p, const StemStep& st) {
+  if (!st.mn || p.cfg.dtype != TN_CHALF || !st.tensor_core || st.split || st.sparse) return false;
+  const OutMap om = step_outmap(st, 0);
   return mn_gemm_supported(1ull << st.mlog, 1u << st.klog, 1u << st.nlog, st.mn_ma, &om);
 }
 
@@ -770,14 +781,7 @@ void run_gemm_once(Plan& p, const StemStep& st, size_t i, const void* src, void*
   const int mlog = st.mlog - mshift;
   const uint64_t M = 1ull << mlog;
   const uint32_t K = 1u << st.klog, N = 1u << st.nlog;
-  OutMap om;
-  memset(&om, 0, sizeof(om));
-  om.identity = st.out_identity ? 1 : 0;
-  om.transposed = (st.out_transposed && mshift == 0) ? 1 : 0;
-  om.mbits = mlog;
-  om.nbits = st.nlog;
-  for (int j = 0; j < mlog; ++j) om.ms[j] = st.m_stride[j];
-  for (int j = 0; j < st.nlog; ++j) om.ns[j] = st.n_stride[j];
+  OutMap om = step_outmap(st, mshift);
   if (peer) peer->honored = 0;
   om.peer = mshift == 0 ? peer : nullptr;
   if (p.cfg.dtype == TN_CHALF) {
