@@ -450,6 +450,28 @@ static Plan* load_plan_fixed(const char* json, size_t len, const tn_config* cfg_
             if (!bs.count(l) && !split_set.count(l)) cand.push_back(l);
           std::stable_sort(cand.begin(), cand.end(), [&](int a, int b) { return nu(a) > nu(b); });
           if (cand.size() < out_pos.size()) throw err(TN_E_INFEASIBLE, "partition modes run out (swap)");
+          // prefer modes the previous GEMM's epilogue can route (runtime.cu fused_swap_target: whole
+          // store boxes per member, m bits >= 7 / n bits >= 5 of its output) among the modes whose next
+          // use ties with the last of the sx C-A17 picks (TN_SWAP_PICK=0: plain C-A17 order).  (Among
+          // the 2 sx furthest, ignoring ties, C3 at 2 ranks got 4 swaps / 15.0 GB per rank instead of
+          // 3 / 10.7 GB.)
+          static const bool pick_env = !getenv("TN_SWAP_PICK") || atoi(getenv("TN_SWAP_PICK")) != 0;
+          if (pick_env && !p.steps.empty() && p.steps.back().tensor_core && cfg.dtype == TN_CHALF) {
+            const StemStep& pv = p.steps.back();
+            auto routable = [&](int l) {
+              const auto it = std::find(L.begin(), L.end(), l);
+              if (it == L.end()) return false;
+              const int pos = (int)(L.end() - it) - 1;  // bit position from the innermost
+              const bool ident = pv.out_identity, tr = pv.out_transposed;
+              if (ident) return pos >= pv.nlog + 7 || (pos >= 5 && pos < pv.nlog);
+              if (tr) return (pos >= 7 && pos < pv.mlog) || pos >= pv.mlog + 5;
+              return false;
+            };
+            const int last = nu(cand[out_pos.size() - 1]);
+            size_t top = 0;
+            while (top < cand.size() && nu(cand[top]) >= last) ++top;
+            std::stable_partition(cand.begin(), cand.begin() + top, routable);
+          }
           st.swap = true;
           // quantise only in the later stages of the path (earlier errors accumulate), C-A26
           {
