@@ -646,7 +646,11 @@ static Plan* load_plan_fixed(const char* json, size_t len, const tn_config* cfg_
         }
         out = kout;
         out.insert(out.end(), newl.begin(), newl.end());
-        if (policy == 3 && !st.sparse && s + 1 < step_nodes.size() &&
+        // (not for a SIMT row-streaming step, K <= 16, N <= 32, K*N <= 128: its transposed stores are
+        // 4-byte scatters; C3 step 14 at 4 ranks took 6.9 ms instead of ~1.7 ms)
+        static const bool rows_tr = getenv("TN_ROWS_TRANSPOSE") != nullptr;  // A/B knob
+        const bool rows_step = !rows_tr && R.size() <= 4 && newl.size() <= 5 && R.size() + newl.size() <= 7;
+        if (policy == 3 && !st.sparse && s + 1 < step_nodes.size() && !rows_step &&
             (split_set.empty() || (int)s + 1 < p.split_from)) {
           // transposed store C[n][m] (new modes outermost, kept modes innermost in M order) when that
           // puts more of the next step's contracted modes innermost: the next step then reads its
