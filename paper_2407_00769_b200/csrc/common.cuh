@@ -102,7 +102,14 @@ struct PermArgs {
 };
 
 // ---- launchers (all asynchronous on `s`) ----
-void launch_permute(void* dst, const void* src, int elem_bytes, int n, const int* perm, cudaStream_t s);
+// Member chunks of a mode swap through peer memory: output bytes [v chunk_bytes, (v+1) chunk_bytes)
+// of a permutation go to base[v] (member v's receive buffer at this rank's chunk) instead of dst.
+struct PeerChunks {
+  uint64_t chunk_bytes;
+  void* base[8];
+};
+void launch_permute(void* dst, const void* src, int elem_bytes, int n, const int* perm, cudaStream_t s,
+                    const PeerChunks* pc = nullptr);
 void launch_contract_c64(const ContractArgs& a, cudaStream_t s);
 void launch_gather_kn(const GatherArgs& g, cudaStream_t s);
 void launch_max_abs_f32(const float* x, uint64_t n, uint32_t* out_bits, cudaStream_t s);

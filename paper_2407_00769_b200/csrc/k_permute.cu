@@ -33,9 +33,23 @@ struct PermArgs2 {
   int64_t outer_out[64];
 };
 
+// Output routed to the swap members (mode swap through NVLink peer memory, runtime.cu mode_swap):
+// output element O (in T units) goes to base[O >> shift] + (O & (2^shift - 1)).
+struct PeerRoute {
+  int on, shift;
+  unsigned char* base[8];
+};
+
+template <typename T>
+__device__ __forceinline__ T* route_out(T* dst, const PeerRoute& pr, int64_t o) {
+  if (!pr.on) return dst + o;
+  return reinterpret_cast<T*>(pr.base[o >> pr.shift]) + (o & ((1ll << pr.shift) - 1));
+}
+
 template <typename T>
 __global__ void __launch_bounds__(256) permute_kernel(T* __restrict__ dst, const T* __restrict__ src,
-                                                      const PermArgs2 args, uint64_t n_tiles) {
+                                                      const PermArgs2 args, uint64_t n_tiles,
+                                                      const __grid_constant__ PeerRoute pr) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int u = args.u, vb = args.vb;
   const int tsz = 1 << u, nvec = tsz >> vb, V = 1 << vb;
@@ -70,7 +84,6 @@ __global__ void __launch_bounds__(256) permute_kernel(T* __restrict__ dst, const
         bo += args.outer_out[j];
       }
     const T* s = src + bi;
-    T* d = dst + bo;
     if (V == 1) {
 #pragma unroll 4
       for (int v = threadIdx.x; v < nvec; v += blockDim.x) tile[v] = __ldg(s + in_tbl[v]);
@@ -82,7 +95,7 @@ __global__ void __launch_bounds__(256) permute_kernel(T* __restrict__ dst, const
     __syncthreads();
     if (V == 1) {
 #pragma unroll 4
-      for (int v = threadIdx.x; v < nvec; v += blockDim.x) d[out_tbl[v]] = tile[wr_tbl[v]];
+      for (int v = threadIdx.x; v < nvec; v += blockDim.x) *route_out(dst, pr, bo + out_tbl[v]) = tile[wr_tbl[v]];
     } else {
 #pragma unroll 2
       for (int v = threadIdx.x; v < nvec; v += blockDim.x) {
@@ -90,7 +103,7 @@ __global__ void __launch_bounds__(256) permute_kernel(T* __restrict__ dst, const
         uint4 x;
         T* xp = reinterpret_cast<T*>(&x);
         for (int j = 0; j < V; ++j) xp[j] = tile[wt[j]];
-        *reinterpret_cast<uint4*>(d + out_tbl[v]) = x;
+        *reinterpret_cast<uint4*>(route_out(dst, pr, bo + out_tbl[v])) = x;
       }
     }
     __syncthreads();
@@ -116,7 +129,8 @@ __device__ __forceinline__ int perm_swz(int v) { return v ^ (((v >> 3) ^ (v >> 6
 
 template <typename T, int NV>
 __global__ void __launch_bounds__(256) permute_pipe_kernel(T* __restrict__ dst, const T* __restrict__ src,
-                                                           const PermArgs2 args, uint64_t n_tiles) {
+                                                           const PermArgs2 args, uint64_t n_tiles,
+                                                           const __grid_constant__ PeerRoute pr) {
   extern __shared__ __align__(16) uint4 ring[];
   constexpr int V = 16 / sizeof(T);
   const int u = args.u, vb = args.vb;
@@ -188,7 +202,7 @@ __global__ void __launch_bounds__(256) permute_pipe_kernel(T* __restrict__ dst, 
         T* xp = reinterpret_cast<T*>(&x);
 #pragma unroll
         for (int q = 0; q < V; ++q) xp[q] = tile[gi[i][q]];
-        *reinterpret_cast<uint4*>(dst + bo + out_off[i]) = x;
+        *reinterpret_cast<uint4*>(route_out(dst, pr, bo + out_off[i])) = x;
       }
     }
     __syncthreads();
@@ -198,7 +212,8 @@ __global__ void __launch_bounds__(256) permute_pipe_kernel(T* __restrict__ dst, 
 }
 
 template <typename T>
-static void launch_pipe(void* dst, const void* src, const PermArgs2& args, uint64_t n_tiles, int nvec, cudaStream_t s) {
+static void launch_pipe(void* dst, const void* src, const PermArgs2& args, uint64_t n_tiles, int nvec, cudaStream_t s,
+                        const PeerRoute& pr) {
   const size_t smem = (size_t)kPermStages * nvec * 16;
   static bool attr = false;
   if (!attr) {
@@ -212,18 +227,33 @@ static void launch_pipe(void* dst, const void* src, const PermArgs2& args, uint6
   static const int ctas = getenv("TN_PERM_CTAS") ? atoi(getenv("TN_PERM_CTAS")) : 2;  // tuning knob
   const int blocks = (int)std::min<uint64_t>(n_tiles, 148ull * ctas);
   if (nvec > 2048)
-    permute_pipe_kernel<T, 16><<<blocks, 256, smem, s>>>((T*)dst, (const T*)src, args, n_tiles);
+    permute_pipe_kernel<T, 16><<<blocks, 256, smem, s>>>((T*)dst, (const T*)src, args, n_tiles, pr);
   else if (nvec > 1024)
-    permute_pipe_kernel<T, 8><<<blocks, 256, smem, s>>>((T*)dst, (const T*)src, args, n_tiles);
+    permute_pipe_kernel<T, 8><<<blocks, 256, smem, s>>>((T*)dst, (const T*)src, args, n_tiles, pr);
   else if (nvec > 512)
-    permute_pipe_kernel<T, 4><<<blocks, 256, smem, s>>>((T*)dst, (const T*)src, args, n_tiles);
+    permute_pipe_kernel<T, 4><<<blocks, 256, smem, s>>>((T*)dst, (const T*)src, args, n_tiles, pr);
   else if (nvec > 256)
-    permute_pipe_kernel<T, 2><<<blocks, 256, smem, s>>>((T*)dst, (const T*)src, args, n_tiles);
+    permute_pipe_kernel<T, 2><<<blocks, 256, smem, s>>>((T*)dst, (const T*)src, args, n_tiles, pr);
   else
-    permute_pipe_kernel<T, 1><<<blocks, 256, smem, s>>>((T*)dst, (const T*)src, args, n_tiles);
+    permute_pipe_kernel<T, 1><<<blocks, 256, smem, s>>>((T*)dst, (const T*)src, args, n_tiles, pr);
 }
 
-void launch_permute(void* dst, const void* src, int elem_bytes, int n, const int* perm, cudaStream_t s) {
+// PeerRoute for element type T from the byte-level routing (chunk_bytes per member, base[v] already
+// at this rank's chunk in member v's buffer)
+template <typename T>
+static PeerRoute route_for(const PeerChunks* pc) {
+  PeerRoute r;
+  memset(&r, 0, sizeof(r));
+  if (!pc) return r;
+  r.on = 1;
+  uint64_t c = pc->chunk_bytes / sizeof(T);
+  while ((1ull << r.shift) < c) ++r.shift;
+  for (int v = 0; v < 8; ++v) r.base[v] = static_cast<unsigned char*>(pc->base[v]);
+  return r;
+}
+
+void launch_permute(void* dst, const void* src, int elem_bytes, int n, const int* perm, cudaStream_t s,
+                    const PeerChunks* pc) {
   if (n < 0 || n > 46) throw TnError{TN_E_INVALID, "permute: rank out of range"};
   if (elem_bytes != 4 && elem_bytes != 8 && elem_bytes != 16)
     throw TnError{TN_E_INVALID, "permute: elem_bytes must be 4, 8 or 16"};
@@ -237,8 +267,17 @@ void launch_permute(void* dst, const void* src, int elem_bytes, int n, const int
     p_of_q[n - 1 - j] = n - 1 - perm[j];
   }
   const uint64_t total = 1ull << n;
+  if (pc && (pc->chunk_bytes & (pc->chunk_bytes - 1)))
+    throw TnError{TN_E_INVALID, "permute: member chunks must be powers of two"};
   if (ident) {
-    TN_CUDA(cudaMemcpyAsync(dst, src, total * elem_bytes, cudaMemcpyDeviceToDevice, s));
+    if (!pc) {
+      TN_CUDA(cudaMemcpyAsync(dst, src, total * elem_bytes, cudaMemcpyDeviceToDevice, s));
+    } else {
+      const uint64_t nc = total * elem_bytes / pc->chunk_bytes;
+      for (uint64_t v = 0; v < nc; ++v)
+        TN_CUDA(cudaMemcpyAsync(pc->base[v], static_cast<const unsigned char*>(src) + v * pc->chunk_bytes,
+                                pc->chunk_bytes, cudaMemcpyDeviceToDevice, s));
+    }
     return;
   }
   // fold leading bits that stay in place into a wider element (up to 16 bytes)
@@ -319,9 +358,9 @@ void launch_permute(void* dst, const void* src, int elem_bytes, int n, const int
   static const bool legacy = getenv("TN_PERM_LEGACY") != nullptr;  // A/B knob for the old kernel
   if (vb == vb_full && nvec <= 4096 && !legacy) {
     switch (eb) {
-      case 4: launch_pipe<uint32_t>(dst, src, args, n_tiles, nvec, s); break;
-      case 8: launch_pipe<uint2>(dst, src, args, n_tiles, nvec, s); break;
-      default: launch_pipe<uint4>(dst, src, args, n_tiles, nvec, s); break;
+      case 4: launch_pipe<uint32_t>(dst, src, args, n_tiles, nvec, s, route_for<uint32_t>(pc)); break;
+      case 8: launch_pipe<uint2>(dst, src, args, n_tiles, nvec, s, route_for<uint2>(pc)); break;
+      default: launch_pipe<uint4>(dst, src, args, n_tiles, nvec, s, route_for<uint4>(pc)); break;
     }
     TN_CUDA(cudaGetLastError());
     return;
@@ -335,21 +374,24 @@ void launch_permute(void* dst, const void* src, int elem_bytes, int n, const int
         TN_CUDA(cudaFuncSetAttribute(permute_kernel<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
         attr_set[0] = true;
       }
-      permute_kernel<uint32_t><<<blocks, 256, smem, s>>>((uint32_t*)dst, (const uint32_t*)src, args, n_tiles);
+      permute_kernel<uint32_t><<<blocks, 256, smem, s>>>((uint32_t*)dst, (const uint32_t*)src, args, n_tiles,
+                                                         route_for<uint32_t>(pc));
       break;
     case 8:
       if (!attr_set[1]) {
         TN_CUDA(cudaFuncSetAttribute(permute_kernel<uint2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
         attr_set[1] = true;
       }
-      permute_kernel<uint2><<<blocks, 256, smem, s>>>((uint2*)dst, (const uint2*)src, args, n_tiles);
+      permute_kernel<uint2><<<blocks, 256, smem, s>>>((uint2*)dst, (const uint2*)src, args, n_tiles,
+                                                      route_for<uint2>(pc));
       break;
     default:
       if (!attr_set[2]) {
         TN_CUDA(cudaFuncSetAttribute(permute_kernel<uint4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
         attr_set[2] = true;
       }
-      permute_kernel<uint4><<<blocks, 256, smem, s>>>((uint4*)dst, (const uint4*)src, args, n_tiles);
+      permute_kernel<uint4><<<blocks, 256, smem, s>>>((uint4*)dst, (const uint4*)src, args, n_tiles,
+                                                      route_for<uint4>(pc));
       break;
   }
   TN_CUDA(cudaGetLastError());

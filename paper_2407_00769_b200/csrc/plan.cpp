@@ -976,7 +976,7 @@ std::string report_json(const Plan& p, const std::vector<float>& ms) {
   o << ",\"final_layout\":";
   jlist(o, p.final_layout);
   o << ",\"launches\":" << p.launches << ",\"world\":" << p.world << ",\"n_swaps\":" << p.n_swaps
-    << ",\"swap_bytes\":" << p.swap_bytes << ",\"n_fused_swaps\":" << p.n_fused_swaps << ",\"final_shard\":";
+    << ",\"swap_bytes\":" << p.swap_bytes << ",\"n_fused_swaps\":" << p.n_fused_swaps << ",\"n_peer_swaps\":" << p.n_peer_swaps << ",\"final_shard\":";
   jlist(o, p.final_shard);
   if (!ms.empty()) {  // [common_ms, (perm_ms, gemm_ms) per step..., final_ms]
     o << ",\"ms\":[";

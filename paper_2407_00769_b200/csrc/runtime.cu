@@ -372,6 +372,7 @@ bool fused_swap_enabled(const Plan& p) {
 // its epilogue can (PeerTarget::honored), else the runtime falls back to mode_swap.
 bool fused_swap_target(const Plan& p, size_t i, int cur, PeerTarget& pt) {
   if (i + 1 >= p.steps.size() || !fused_swap_enabled(p)) return false;
+  if (getenv("TN_NO_EPILOGUE_SWAP")) return false;  // test knob (read per call): the peer-pass swap only
   const StemStep& st = p.steps[i];
   const StemStep& nx = p.steps[i + 1];
   if (!nx.swap || nx.quant || p.cfg.dtype != TN_CHALF || !st.tensor_core || st.split || st.sparse) return false;
@@ -632,9 +633,41 @@ void check_buffers(const Plan& p, const tn_buffers* b) {
 // modes are the outermost local modes.  Only members that differ in the swapped bits talk (partial
 // swap, reading C-A17).  int8: each chunk is quantised in groups of comm_group reals (groups never
 // straddle chunks), sent as codes + fp32 scale/zero, and dequantised straight into complex-half.
-void mode_swap(Plan& p, const StemStep& st, const tn_buffers* b, int& cur, cudaStream_t s) {
+// An fp16 / complex64 mode swap without the transport: the send permutation (or a plain chunk copy)
+// writes every member's chunk straight into that member's receive buffer over NVLink peer memory
+// (one pass, no NCCL payload); bar_slot = an already reduced max slot whose re-reduction is the
+// barrier before (no rank still reads the buffer its peers write) and after (every chunk is in).
+// TN_SWAP_NCCL=1 keeps the transport (A/B knob); quantised swaps always use it (the codec).
+bool peer_swap_enabled(const Plan& p) {
+  const char* e = getenv("TN_SWAP_NCCL");  // A/B and test knob (read per call)
+  return fused_swap_enabled(p) && !(e && atoi(e) != 0) && p.peer_stem.size() == 2u * p.world;
+}
+
+void mode_swap(Plan& p, const StemStep& st, const tn_buffers* b, int& cur, cudaStream_t s, float* bar_slot) {
   comm_check(p);
   const int eb = p.cfg.dtype == TN_CHALF ? 4 : 8;
+  if (!st.quant && bar_slot && peer_swap_enabled(p)) {
+    const SwapMembers sm(p, st);
+    const uint64_t n_local = 1ull << st.send_layout.size();
+    PeerChunks pc;
+    memset(&pc, 0, sizeof(pc));
+    pc.chunk_bytes = (n_local >> sm.sx) * eb;
+    for (int v = 0; v < (1 << sm.sx); ++v)
+      pc.base[v] = static_cast<unsigned char*>(p.peer_stem[2 * sm.peer_of(v) + (1 - cur)]) + (uint64_t)sm.me * pc.chunk_bytes;
+    std::vector<int> axes;
+    if (st.send_perm) {
+      axes = st.send_perm_axes;
+    } else {
+      for (size_t j = 0; j < st.send_layout.size(); ++j) axes.push_back((int)j);
+    }
+    xfer_allreduce_max(p, bar_slot, s);
+    launch_permute(nullptr, b->d_stem[cur], eb, (int)st.send_layout.size(), axes.data(), s, &pc);
+    ++p.launches;
+    xfer_allreduce_max(p, bar_slot, s);
+    cur = 1 - cur;
+    ++p.n_peer_swaps;
+    return;
+  }
   // quantised swaps read the unpermuted stem group by group when the permutation keeps the
   // innermost log2(g/2) modes in place (k_quant.cu group_base): no separate permutation pass
   GroupPerm gp;
@@ -879,10 +912,11 @@ void stem_body(Plan& p, const tn_buffers* b, cudaStream_t s, bool head = true, b
                                                : (p.sparse_from >= 0 ? (size_t)p.sparse_from : p.steps.size());
   bool swapped = false;  // the swap before step i was done by step i-1's epilogue
   p.n_fused_swaps = 0;
+  p.n_peer_swaps = 0;
   for (size_t i = 0; i < n_main; ++i) {
     const StemStep& st = p.steps[i];
     if (st.swap && !swapped) {
-      mode_swap(p, st, b, cur, s);
+      mode_swap(p, st, b, cur, s, &sc.max_slot[i]);
     }
     swapped = false;
     if (st.perm && !mn_active(p, st)) {

@@ -91,6 +91,7 @@ def main():
                    "fp16_epilogue_swaps": results["fp16"][1]["n_fused_swaps"],
                    "fp16_nofused_epilogue_swaps": results["fp16_nofused"][1]["n_fused_swaps"],
                    "fp16_fused_equal_transport": bool(np.array_equal(results["fp16"][0], results["fp16_nofused"][0])),
+                   "fp16_peer_pass_swaps": results["fp16"][1]["n_peer_swaps"],
                    "rel_1gpu_oracle": metrics.rel_l2(one, ref),
                    "swaps": sum(1 for s in results["int8"][1]["steps"] if s.get("swap")),
                    "steps": len(results["int8"][1]["steps"])}

@@ -131,18 +131,27 @@ def test_loopback_fused_codec_bit_identical(tn, c3sub, world):
 @pytest.mark.parametrize("world", [2, 4, 8])
 def test_loopback_fused_swap_bit_identical(tn, c3sub, world):
     """fp16 mode swaps done by the previous GEMM's epilogue (tn_config.no_fused_swap = 0: output
-    boxes stored straight into the owning rank's buffer) == the exchange through the transport
-    (send permutation + chunk exchange), bit for bit, on every rank."""
+    boxes stored straight into the owning rank's buffer), and the others by one peer-memory pass
+    (the send permutation writing each member's chunk into its buffer) == the exchange through the
+    transport (send permutation + chunk exchange), bit for bit, on every rank; likewise with every
+    swap done by the peer pass."""
     sub, _ = c3sub
     kw = dict(stem_min_log2=14, comm_codec=tn.TN_COMM_FP16)
     fused = run_loopback(tn, sub, world, kw)
     unf = run_loopback(tn, sub, world, dict(kw, no_fused_swap=1))
+    # every swap as a peer-memory pass (the send permutation writing the members' chunks directly)
+    os.environ["TN_NO_EPILOGUE_SWAP"] = "1"
+    try:
+        pas = run_loopback(tn, sub, world, kw)
+    finally:
+        del os.environ["TN_NO_EPILOGUE_SWAP"]
     nf = fused[0][1]["n_fused_swaps"]
-    print(f"world={world}: swaps={n_swaps(fused[0][1])} fused={nf}")
-    assert unf[0][1]["n_fused_swaps"] == 0
-    assert nf >= 1
-    for (a, _, _), (b, _, _) in zip(fused, unf):
-        assert np.array_equal(a, b)
+    print(f"world={world}: swaps={n_swaps(fused[0][1])} fused={nf} peer-pass={fused[0][1]['n_peer_swaps']}")
+    assert unf[0][1]["n_fused_swaps"] == 0 and unf[0][1]["n_peer_swaps"] == 0
+    assert nf >= 1 and nf + fused[0][1]["n_peer_swaps"] == n_swaps(fused[0][1])
+    assert pas[0][1]["n_fused_swaps"] == 0 and pas[0][1]["n_peer_swaps"] == n_swaps(pas[0][1])
+    for (a, _, _), (b, _, _), (c, _, _) in zip(fused, unf, pas):
+        assert np.array_equal(a, b) and np.array_equal(a, c)
 
 
 @pytest.mark.parametrize("world", [2, 4, 8])

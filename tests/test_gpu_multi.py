@@ -48,6 +48,7 @@ def test_sharded_stem_vs_oracle(world):
     # fp16 swaps done by the previous GEMM's epilogue (NVLink peer stores through CUDA IPC):
     # bit-identical to the NCCL exchange
     assert v["fp16_epilogue_swaps"] >= 1 and v["fp16_nofused_epilogue_swaps"] == 0
+    assert v["fp16_epilogue_swaps"] + v["fp16_peer_pass_swaps"] == v["swaps"]
     assert v["fp16_fused_equal_transport"]
     # permutation fused into the sender's codec: bit-identical to permutation pass + codec
     assert v["fused_swaps_c3_unfused_run"] == 0
