@@ -118,6 +118,8 @@ void launch_max_abs_f16(const __half* x, uint64_t n, uint32_t* out_bits, cudaStr
 // exponent slot and column 1-norm bound as launch_pad_b
 void launch_pad_b_mn(__half* bpm, const float2* b, int klog, int nlog, const uint32_t* bmax_bits, float* b_bound,
                      int* exp_slot, cudaStream_t s);
+// B' = blockdiag(B_P x f) fp16 [max(f 2N, 16)][f 2K] (row folding, StemStep::fold)
+void launch_fold_b(__half* bf, const __half* bp, int klog, int nlog, int f, cudaStream_t s);
 // B [K][N] c64 -> B_P fp16 [2N][2K] with scale 2^t (t from *bmax_bits), bound, exp
 void launch_pad_b(__half* bp, const float2* b, int klog, int nlog, const uint32_t* bmax_bits,
                   float* b_bound, int* exp_slot, cudaStream_t s);

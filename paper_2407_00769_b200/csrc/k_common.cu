@@ -188,6 +188,26 @@ void launch_pad_b_mn(__half* bpm, const float2* b, int klog, int nlog, const uin
   TN_CUDA(cudaGetLastError());
 }
 
+// B' = blockdiag(B_P, ..., B_P) (fold copies): B' [max(f 2N, 16)][f 2K] fp16 from B_P [2N][2K]
+__global__ void fold_b_kernel(__half* __restrict__ bf, const __half* __restrict__ bp, int k2, int n2, int f,
+                              uint64_t rows) {
+  const uint64_t cols = (uint64_t)f * k2, total = rows * cols;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t r = i / cols, c = i % cols;
+    const uint64_t bi = r / n2, bj = c / k2;
+    bf[i] = (r < (uint64_t)f * n2 && bi == bj) ? bp[(r % n2) * k2 + (c % k2)] : __float2half_rn(0.f);
+  }
+}
+
+void launch_fold_b(__half* bf, const __half* bp, int klog, int nlog, int f, cudaStream_t s) {
+  const int k2 = 2 << klog, n2 = 2 << nlog;
+  const uint64_t rows = std::max<uint64_t>((uint64_t)f * n2, 16);
+  const uint64_t total = rows * (uint64_t)f * k2;
+  const int blocks = (int)std::min<uint64_t>((total + 255) / 256, 148 * 4);
+  fold_b_kernel<<<blocks, 256, 0, s>>>(bf, bp, k2, n2, f, rows);
+  TN_CUDA(cudaGetLastError());
+}
+
 __global__ void c64_to_chalf_kernel(__half2* __restrict__ dst, const float2* __restrict__ src, uint64_t n,
                                     const uint32_t* max_bits, int* exp_slot, uint32_t* out_max) {
   const int e = max_bits ? scale_exp_for(__uint_as_float(*max_bits)) : 0;

@@ -860,12 +860,30 @@ static Plan* load_plan_fixed(const char* json, size_t len, const tn_config* cfg_
     off += align_up(8ull << p.nodes[id].labels.size(), 256);
   }
   p.ws_common = off;
+  static const bool fold_off = getenv("TN_NO_FOLD") != nullptr;  // A/B knob
   for (auto& st : p.steps) {
     uint64_t kn = 1ull << (st.klog + st.nlog);
     const uint64_t nb = 1ull << st.b_sparse.size();  // sparse tail: one block per sparse-leg value
     st.b_tmp_off = off;
     off += align_up(8 * kn, 1024) * nb;
-    if (cfg.dtype == TN_CHALF) {
+    st.fold = 1;
+    if (cfg.dtype == TN_CHALF && !fold_off && !st.gather_a && !st.mn && st.out_identity && !st.split && !st.sparse &&
+        st.klog >= 1 && st.klog <= 4) {
+      int fl = 0;
+      while ((4 << (st.klog + fl)) < 128) ++fl;  // rows of 2K fp16 -> 128 bytes
+      if (st.mlog - fl >= 8) {
+        st.fold = 1 << fl;
+        st.tensor_core = true;
+        const uint64_t rows = std::max<uint64_t>((uint64_t)st.fold * 2 << st.nlog, 16);
+        st.b_fold_bytes = align_up(rows * ((uint64_t)st.fold * 2 << st.klog) * 2, 1024);
+      }
+    }
+    if (cfg.dtype == TN_CHALF && st.fold > 1) {
+      // B' = blockdiag(B_P x fold), then the B_P scratch it is built from
+      st.b_off = off;
+      st.b_blk = st.b_fold_bytes;
+      off += st.b_fold_bytes + align_up(std::max<uint64_t>(8 * kn, 64ull << st.klog), 1024);
+    } else if (cfg.dtype == TN_CHALF) {
       st.b_off = off;
       // fp16 [max(2N, 16)][2K]: rows beyond 2N are zero (tcgen05 N >= 16)
       // sparse tail: blocks back to back (the batched GEMM's B map steps by exactly one block)
@@ -927,6 +945,7 @@ std::string report_json(const Plan& p, const std::vector<float>& ms) {
       << ",\"quant\":" << (s.quant ? 1 : 0) << ",\"sparse\":" << s.sparse
       << ",\"fuse_quant\":" << (s.fuse_quant ? 1 : 0)
       << ",\"out_kind\":" << (s.out_identity ? 0 : (s.out_transposed ? 1 : 2)) << ",\"mn\":" << (s.mn ? s.mn_ma : 0)
+      << ",\"fold\":" << s.fold
       << ",\"in\":";
     jlist(o, s.in_layout);
     o << ",\"R\":";

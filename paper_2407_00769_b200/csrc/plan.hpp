@@ -54,6 +54,11 @@ struct StemStep {
   // geometry allows (runtime mn_active); perm / perm_axes stay as the fallback
   bool mn = false;
   int mn_ma = 0;
+  // row folding (plain A, row-major output, 2K x 2 B < 128 B): the tcgen05 GEMM runs on [M/f][f 2K] x
+  // blockdiag(B_P x f) -> [M/f][f 2N], the same bytes read as rows of 128 B (the TMA engine's
+  // per-row cost made 64-byte rows its limit); B' at b_off, B_P scratch at b_off + b_fold_bytes
+  int fold = 1;
+  uint64_t b_fold_bytes = 0;
   // output address of C[m, n] = sum_j bit_j(m) m_stride[j] + sum_j bit_j(n) n_stride[j] (elements)
   std::vector<int64_t> m_stride, n_stride;
   bool out_identity = true;       // out_layout == kept ++ newl (plain row-major [M][N])

@@ -375,7 +375,8 @@ bool fused_swap_target(const Plan& p, size_t i, int cur, PeerTarget& pt) {
   if (getenv("TN_NO_EPILOGUE_SWAP")) return false;  // test knob (read per call): the peer-pass swap only
   const StemStep& st = p.steps[i];
   const StemStep& nx = p.steps[i + 1];
-  if (!nx.swap || nx.quant || p.cfg.dtype != TN_CHALF || !st.tensor_core || st.split || st.sparse) return false;
+  if (!nx.swap || nx.quant || p.cfg.dtype != TN_CHALF || !st.tensor_core || st.split || st.sparse || st.fold > 1)
+    return false;
   if (!(st.out_identity || st.out_transposed) || p.peer_stem.size() != 2u * p.world) return false;
   if (nx.send_layout.size() != st.out_layout.size()) return false;
   const SwapMembers sm(p, nx);
@@ -606,7 +607,13 @@ void prepare_b(const Plan& p, unsigned char* W, const Scratch& sc, cudaStream_t 
       if (st.nlog < 3)  // zero the padding rows of B_P (tcgen05 needs N >= 16 real columns)
         TN_CUDA(cudaMemsetAsync(W + st.b_off, 0, 64ull << st.klog, s));
       launch_max_abs_f32(reinterpret_cast<const float*>(g.dst), 2 * kn, &sc.b_max[i], s);
-      if (mn_active(p, st))
+      if (st.fold > 1) {
+        __half* scratch = reinterpret_cast<__half*>(W + st.b_off + st.b_fold_bytes);
+        if (st.nlog < 3) TN_CUDA(cudaMemsetAsync(scratch, 0, 64ull << st.klog, s));
+        launch_pad_b(scratch, g.dst, st.klog, st.nlog, &sc.b_max[i], &sc.b_bound[i], &sc.exps[1 + 2 * i], s);
+        launch_fold_b(reinterpret_cast<__half*>(W + st.b_off), scratch, st.klog, st.nlog, st.fold, s);
+        const_cast<Plan&>(p).launches++;
+      } else if (mn_active(p, st))
         launch_pad_b_mn(reinterpret_cast<__half*>(W + st.b_off), g.dst, st.klog, st.nlog, &sc.b_max[i],
                         &sc.b_bound[i], &sc.exps[1 + 2 * i], s);
       else
@@ -826,7 +833,14 @@ void run_gemm_once(Plan& p, const StemStep& st, size_t i, const void* src, void*
       for (int j = 0; j < st.mlog; ++j) ag.ms[j] = st.a_m_stride[j];
       for (int j = 0; j < st.klog; ++j) ag.ks[j] = st.a_k_stride[j];
     }
-    if (mshift == 0 && mn_active(p, st))
+    if (mshift == 0 && st.fold > 1) {
+      // row folding: [M/f][f 2K] x blockdiag(B_P) -> [M/f][f 2N], the same row-major bytes
+      OutMap fo = identity_map(M / st.fold, (uint32_t)st.fold * N);
+      fo.peer = nullptr;
+      launch_gemm_chalf_tc(reinterpret_cast<__half*>(dst), reinterpret_cast<const __half*>(src),
+                           reinterpret_cast<const __half*>(W + st.b_off), M / st.fold, st.fold * 2 * K,
+                           st.fold * 2 * N, in_max, &sc.b_bound[i], out_max, exp_slot, &fo, s, nullptr);
+    } else if (mshift == 0 && mn_active(p, st))
       launch_gemm_chalf_mn(reinterpret_cast<__half*>(dst), reinterpret_cast<const __half*>(src),
                            reinterpret_cast<const __half*>(W + st.b_off), M, K, N, st.mn_ma, in_max, &sc.b_bound[i],
                            out_max, exp_slot, &om, s);
