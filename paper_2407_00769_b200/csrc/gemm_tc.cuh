@@ -864,6 +864,17 @@ __global__ void __launch_bounds__((kAMode == 1 || kAMode == 4) ? kThreadsGather 
             const int q0 = (c & 63) >> 1;  // first complex column of these 32 real columns
 #pragma unroll
             for (int j = 0; j < 16; ++j) st32[(q0 + j) * BM + row] = pk[j];
+          } else if (BN < 64 && epi_stg == 5) {
+            // packed narrow rows: 64 / BN output rows (BN fp16 each) share one 128-byte staging row,
+            // stored as rows of 128 B (the TMA engine's per-row cost made 32/64-byte rows its limit)
+            constexpr int kFo = BN < 64 ? 64 / BN : 1;
+            const int prow = row / kFo, part = row % kFo;
+            unsigned char* srow = sbuf + prow * 128;
+#pragma unroll
+            for (int q = 0; q < BN / 8; ++q) {
+              const int chunk = (part * (BN / 8) + q) ^ (prow & 7);
+              *reinterpret_cast<uint4*>(srow + chunk * 16) = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+            }
           } else {
             unsigned char* srow = sbuf + row * 128;
             const int cb = (c & 63) >> 3;  // first 16-byte chunk of these 32 columns
@@ -918,8 +929,12 @@ __global__ void __launch_bounds__((kAMode == 1 || kAMode == 4) ? kThreadsGather 
               const int v = peer_coords(ps, gm, nc);
               if (epi_stg == 4)
                 tma_store_2d(&ps.maps[v], sbuf, (int)gm, (int)nc);
+              else if (BN < 64 && epi_stg == 5)
+                tma_store_2d(&ps.maps[v], sbuf, 0, (int)(gm / (64 / BN)));
               else
                 tma_store_2d(&ps.maps[v], sbuf, (int)(2 * nc), (int)gm);
+            } else if (BN < 64 && epi_stg == 5) {
+              tma_store_2d(&tmC, sbuf, 0, m0 / (64 / BN));  // [rows / (64 / BN)][64 fp16] map
             } else if (epi_stg == 4) {
               // box {128 m (inner, global row), 32 complex n} of the C^T map
               tma_store_2d(&tmC, sbuf, (int)(ga.m_base + (uint64_t)m0), (n0 + sub) >> 1);
@@ -1000,7 +1015,7 @@ static CUtensorMap make_map_t(const void* base, uint64_t M, uint64_t N, uint32_t
 // launch's epilogue cannot do it (scatter or direct stores, batched launches, member bits inside a
 // store box).  pt->honored tells the runtime whether the exchange happened here.
 static PeerStore make_peer_store(PeerTarget* pt, bool tma_epi, bool transposed, uint64_t M, uint32_t N2_real,
-                                 uint32_t box_rows = tc::BM) {
+                                 uint32_t box_rows = tc::BM, int pack = 1) {
   PeerStore ps;
   memset(&ps, 0, sizeof(ps));
   if (!pt) return ps;
@@ -1015,7 +1030,7 @@ static PeerStore make_peer_store(PeerTarget* pt, bool tma_epi, bool transposed, 
   for (int t = 0; t < pt->nsw; ++t) {
     const int b = pt->bit[t];
     if (pt->is_n[t]) {
-      if (b < 5 || (1ull << b) >= Nc) return ps;  // a 32-column store box would span two members
+      if (b < 5 || (1ull << b) >= Nc || pack > 1) return ps;  // a 32-column store box would span two members
       ++nrem;
     } else {
       if ((1 << b) < (int)box_rows || (1ull << b) >= M) return ps;   // a row box would span two members
@@ -1027,7 +1042,9 @@ static PeerStore make_peer_store(PeerTarget* pt, bool tma_epi, bool transposed, 
   const uint64_t Mp = M >> mrem, Np = Nc >> nrem;
   if (Mp >= (1ull << 31) || 2 * Np >= (1ull << 31)) return ps;
   for (int v = 0; v < (1 << pt->nsw); ++v)
-    ps.maps[v] = transposed ? make_map_t(pt->base[v], Mp, Np, box_rows) : make_map_2d(pt->base[v], 2 * Np, Mp, 64, box_rows);
+    ps.maps[v] = transposed ? make_map_t(pt->base[v], Mp, Np, box_rows)
+                 : pack > 1 ? make_map_2d(pt->base[v], 64, Mp / pack, 64, box_rows / pack)
+                            : make_map_2d(pt->base[v], 2 * Np, Mp, 64, box_rows);
   ps.nsw = pt->nsw;
   for (int t = 0; t < ps.nsw; ++t) {
     ps.is_n[t] = (int8_t)es[t].is_n;
@@ -1235,8 +1252,13 @@ static void launch_bn(__half* c, const __half* a, const __half* bp, uint64_t M, 
   // TMA coordinates are int32: process M in chunks of at most 2^30 rows
   const uint32_t num_n = N2 / BN;
   const uint64_t chunk = std::min<uint64_t>(1ull << 30, ((1ull << 31) / num_n) * tc::BM);
+  // packed narrow rows (epilogue mode 5): a row-major output whose rows are 32 or 64 bytes is staged
+  // and TMA-stored as rows of 128 B (64 / BN output rows each)
+  static const bool no_pack = getenv("TN_NO_PACK") != nullptr;  // A/B knob
+  const bool packed = BN < 64 && !no_pack && !sa.on && !bs && epi_stg == 0 && !transposed && (!om || om->identity) &&
+                      N2_real == (uint32_t)BN && M % tc::BM == 0;
   const PeerStore ps = make_peer_store(om ? om->peer : nullptr, !sa.on && epi_stg == 0 && (transposed || (om && om->identity)),
-                                       transposed, M, N2_real);
+                                       transposed, M, N2_real, tc::BM, packed ? 64 / BN : 1);
   if constexpr (G == 0 && KB == 64 && BN >= 128) {
     // plain A, row-major or transposed output, whole 256-row pair tiles: the CTA-pair kernel (half
     // the B tile staged per SM: fewer shared-memory bytes per MAC on the compute-bound steps)
@@ -1264,6 +1286,7 @@ static void launch_bn(__half* c, const __half* a, const __half* bp, uint64_t M, 
                         : make_map_2d(kPlainA ? a + m_off * K2 : a, K2, kPlainA ? mm : tc::BM, KB, tc::BM);
     gargs.m_base = m_off;
     CUtensorMap mc = transposed ? make_map_t(c, M, N2_real / 2)
+                     : packed   ? make_map_2d(c + m_off * N2, 64, mm * N2 / 64, 64, tc::BM * BN / 64)
                                 : make_map_2d(c + m_off * N2, N2, mm, 64, epi_stg == 3 ? 32 : tc::BM);
     // scatter: base of this chunk's rows in the OutMap; row-major: the chunk's first row (STG epilogue)
     uint32_t* out_sc = reinterpret_cast<uint32_t*>(c) + (sa.on ? outmap_m(*om, m_off) : m_off * (N2 / 2));
@@ -1273,7 +1296,7 @@ static void launch_bn(__half* c, const __half* a, const __half* bp, uint64_t M, 
     // the exponent is recorded once (first chunk); later chunks reuse the same inputs
     tc::gemm_chalf_tc_kernel<BN, KB, G><<<grid, (G == 1 || G == 4) ? tc::kThreadsGather : tc::kThreads, C::kSmem, s>>>(
         ma, mb, mc, num_m, num_n, (int)K2, in_max, b_bound, out_max, m_off ? nullptr : exp_slot, sa, out_sc, mm,
-        n_cols, gargs, nda, transposed ? 4 : epi_stg, BatchArgs{}, ps);
+        n_cols, gargs, nda, transposed ? 4 : (packed ? 5 : epi_stg), BatchArgs{}, ps);
     TN_CUDA(cudaGetLastError());
   }
 }

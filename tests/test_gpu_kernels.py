@@ -86,7 +86,9 @@ def _half_pairs(z):
                                    # CTA-pair kernel (M % 256 == 0, 2N >= 128, 2K >= 64): single k block,
                                    # BN = 128 and 256, more pair tiles than resident pairs
                                    (512, 32, 64), (256, 64, 128), (1536, 32, 512), (65536, 64, 128),
-                                   (16384, 256, 256)])
+                                   (16384, 256, 256),
+                                   # packed narrow rows (2N = 16 / 32 fp16 per row stored as 128-byte rows)
+                                   (4096, 16, 16), (1024, 32, 8), (128, 4, 16)])
 def test_gemm_chalf_tensor_core_vs_oracle(env, M, K, N):
     """tcgen05 Eq. 6 GEMM (no scaling) vs the oracle's real-embedding GEMM in fp64 on the same
     fp16 operands.  Error: one fp16 rounding of C (2^-11 relative) + fp32 accumulation."""
