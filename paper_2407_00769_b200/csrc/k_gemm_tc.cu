@@ -310,11 +310,15 @@ void launch_gemm_chalf_tc(__half* c, const __half* a, const __half* bp, uint64_t
     NdPlan np, rp;
     const bool direct = force != 1 && force != 3 && build_nd(*ag, np);
     const bool raw = force != 1 && force != 2 && build_raw(*ag, rp);
-    // A direct box unless its TMA rows are only 32 B: there the raw box (rows as long as the source
-    // runs allow) plus the smem reshuffle wins (C3 step 50, m28 k5 n5: 22.5 -> 13.5 ms; m21 k9 n6:
-    // 1.63 -> 1.18 ms); at 64-byte rows the two tie, at 128 B the direct box is faster.
+    // A direct box unless its TMA rows are shorter than 128 B: there the raw box (rows as long as the
+    // source runs allow) plus the smem reshuffle wins (round-1 C3 step 50, m28 k5 n5, 32-byte rows:
+    // 22.5 -> 13.5 ms; m21 k9 n6: 1.63 -> 1.18 ms; 64-byte rows: see raw_below); at 128 B the direct
+    // box is faster.
     // Raw box when no direct one exists (<= 5 dims); else cp.async.
-    static const int raw_below = getenv("TN_RAW_BELOW") ? atoi(getenv("TN_RAW_BELOW")) : 64;  // tuning knob
+    // 128: 64-byte rows also take the raw box.  In isolation at full clock the two tie at 64 B, but
+    // inside the power-capped subtask (SM clock ~1.2-1.4 GHz) the direct box's per-row TMA cost
+    // dominates: C3 step 4 (m24 k8 n7, 64-byte rows) 8.0-10.8 ms raw vs 12.9-13.0 ms direct.
+    static const int raw_below = getenv("TN_RAW_BELOW") ? atoi(getenv("TN_RAW_BELOW")) : 128;  // tuning knob
     const bool direct_wide = direct && (int)(np.box[0] * 4) >= raw_below;
     static const bool dbg = getenv("TN_GATHER_DEBUG") != nullptr;
     if (dbg) {
