@@ -111,6 +111,10 @@ struct PeerChunks {
 void launch_permute(void* dst, const void* src, int elem_bytes, int n, const int* perm, cudaStream_t s,
                     const PeerChunks* pc = nullptr);
 void launch_contract_c64(const ContractArgs& a, cudaStream_t s);
+// one launch for the contractions of one tree level (device arrays: args[nnodes], start[nnodes + 1]
+// = first block of each node, start[nnodes] = blocks)
+void launch_contract_c64_level(const ContractArgs* d_args, const uint32_t* d_start, int nnodes, uint32_t blocks,
+                               cudaStream_t s);
 void launch_gather_kn(const GatherArgs& g, cudaStream_t s);
 void launch_max_abs_f32(const float* x, uint64_t n, uint32_t* out_bits, cudaStream_t s);
 void launch_max_abs_f16(const __half* x, uint64_t n, uint32_t* out_bits, cudaStream_t s);

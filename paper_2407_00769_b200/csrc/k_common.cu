@@ -59,6 +59,57 @@ __global__ void contract_c64_kernel(const ContractArgs args, uint64_t n_out_elem
   }
 }
 
+// Level-batched common phase: every contraction of one tree level (independent of each other) in
+// one launch.  Block b of the launch belongs to node i with start[i] <= b < start[i+1] and works on
+// that node's outputs [(b - start[i]) * 256, ...) with a grid stride of the node's block count.
+__global__ void contract_c64_level_kernel(const ContractArgs* __restrict__ args, const uint32_t* __restrict__ start,
+                                          int nnodes) {
+  int lo = 0, hi = nnodes - 1;
+  while (lo < hi) {  // last node whose start <= blockIdx.x
+    const int mid = (lo + hi + 1) >> 1;
+    if (start[mid] <= blockIdx.x) lo = mid; else hi = mid - 1;
+  }
+  const ContractArgs& a = args[lo];
+  const uint32_t nb = start[lo + 1] - start[lo], b = blockIdx.x - start[lo];
+  const uint64_t n_out = 1ull << a.n_out, nred = 1ull << a.n_red;
+  const float2* A = a.a + slice_offset(a.sa);
+  const float2* B = a.b + slice_offset(a.sb);
+  for (uint64_t o = b * (uint64_t)blockDim.x + threadIdx.x; o < n_out; o += (uint64_t)nb * blockDim.x) {
+    int64_t oa = 0, ob = 0;
+    for (int j = 0; j < a.n_out; ++j)
+      if (o >> j & 1) {
+        oa += a.out_sa[j];
+        ob += a.out_sb[j];
+      }
+    float2 acc = make_float2(0.f, 0.f);
+    uint64_t g = 0;
+    for (uint64_t r = 0; r < nred; ++r) {
+      if (r) {
+        int j = __ffsll((long long)r) - 1;  // Gray code: bit j flips
+        g ^= 1ull << j;
+        if (g >> j & 1) {
+          oa += a.red_sa[j];
+          ob += a.red_sb[j];
+        } else {
+          oa -= a.red_sa[j];
+          ob -= a.red_sb[j];
+        }
+      }
+      float2 x = A[oa], y = B[ob];
+      acc.x = fmaf(x.x, y.x, fmaf(-x.y, y.y, acc.x));
+      acc.y = fmaf(x.x, y.y, fmaf(x.y, y.x, acc.y));
+    }
+    a.c[o] = acc;
+  }
+}
+
+void launch_contract_c64_level(const ContractArgs* d_args, const uint32_t* d_start, int nnodes, uint32_t blocks,
+                               cudaStream_t s) {
+  if (nnodes <= 0 || blocks == 0) return;
+  contract_c64_level_kernel<<<blocks, 256, 0, s>>>(d_args, d_start, nnodes);
+  TN_CUDA(cudaGetLastError());
+}
+
 void launch_contract_c64(const ContractArgs& a, cudaStream_t s) {
   uint64_t n = 1ull << a.n_out;
   int threads = 256;

@@ -140,6 +140,13 @@ struct Plan {
   std::vector<void*> peer_stem;   // [2 r + j]: rank r's stem buffer j as this rank addresses it
   const void* peer_key[2] = {nullptr, nullptr};  // the local buffers peer_stem was set up for
   std::vector<void*> ipc_open;    // CUDA IPC mappings opened for peer_stem (closed on free)
+  // level-batched common phase (runtime.cu run_common): device copies of every common contraction's
+  // arguments, grouped by tree level, built for one workspace (key)
+  void* common_dev = nullptr;
+  const void* common_key = nullptr;
+  std::vector<int> common_level_nodes;     // per level: node count
+  std::vector<uint32_t> common_level_blocks;  // per level: blocks of the launch
+  std::vector<uint64_t> common_level_args, common_level_start;  // byte offsets into common_dev
   tn_comm* comm = nullptr;
   // CUDA graph of the whole tn_stem_contract body (world == 1; sharded: the head, or all with TN_GRAPH_NCCL=1): captured once per buffer set on a
   // library stream, replayed on the caller's stream.  Opaque CUDA handles as void*.

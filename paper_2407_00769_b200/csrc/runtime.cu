@@ -477,8 +477,73 @@ View view_of(const Plan& p, int id, unsigned char* W) {
   return v;
 }
 
+ContractArgs common_args(const Plan& p, int id, unsigned char* W);
+
+// The common phase level by level (one launch per tree level; TN_COMMON_SERIAL=1: one launch per
+// contraction, the round-1 form).  The argument tables live in a library-owned device buffer built
+// once per workspace, before any capture (prepare_common).
+void prepare_common(Plan& p, unsigned char* W) {
+  if (p.common_dev && p.common_key == W) return;
+  if (p.common_dev) cudaFree(p.common_dev);
+  p.common_dev = nullptr;
+  p.common_level_nodes.clear();
+  p.common_level_blocks.clear();
+  p.common_level_args.clear();
+  p.common_level_start.clear();
+  std::vector<int> level(p.nodes.size(), 0);
+  int maxl = -1;
+  for (int id : p.common_order) {  // children before parents
+    const Node& n = p.nodes[id];
+    int l = 0;
+    for (int c : {n.u, n.v})
+      if (c >= 0 && p.nodes[c].kind == NODE_COMMON) l = std::max(l, level[c] + 1);
+    level[id] = l;
+    maxl = std::max(maxl, l);
+  }
+  std::vector<unsigned char> host;
+  for (int l = 0; l <= maxl; ++l) {
+    std::vector<ContractArgs> args;
+    std::vector<uint32_t> start(1, 0);
+    for (int id : p.common_order)
+      if (level[id] == l) {
+        args.push_back(common_args(p, id, W));
+        const uint64_t n = 1ull << args.back().n_out;
+        const uint64_t nb = std::min<uint64_t>((n + 255) / 256, 148 * 16);
+        start.push_back(start.back() + (uint32_t)nb);
+      }
+    auto put = [&](const void* src, size_t bytes) {
+      const uint64_t off = (host.size() + 255) / 256 * 256;
+      host.resize(off + bytes);
+      memcpy(host.data() + off, src, bytes);
+      return off;
+    };
+    p.common_level_nodes.push_back((int)args.size());
+    p.common_level_blocks.push_back(start.back());
+    p.common_level_args.push_back(put(args.data(), args.size() * sizeof(ContractArgs)));
+    p.common_level_start.push_back(put(start.data(), start.size() * sizeof(uint32_t)));
+  }
+  if (!host.empty()) {
+    TN_CUDA(cudaMalloc(&p.common_dev, host.size()));
+    TN_CUDA(cudaMemcpy(p.common_dev, host.data(), host.size(), cudaMemcpyHostToDevice));
+  }
+  p.common_key = W;
+}
+
 void run_common(const Plan& p, unsigned char* W, cudaStream_t s) {
-  for (int id : p.common_order) {
+  static const bool serial = getenv("TN_COMMON_SERIAL") != nullptr;  // A/B knob
+  if (!serial && p.common_dev && p.common_key == W) {
+    const unsigned char* d = static_cast<const unsigned char*>(p.common_dev);
+    for (size_t l = 0; l < p.common_level_nodes.size(); ++l)
+      launch_contract_c64_level(reinterpret_cast<const ContractArgs*>(d + p.common_level_args[l]),
+                                reinterpret_cast<const uint32_t*>(d + p.common_level_start[l]),
+                                p.common_level_nodes[l], p.common_level_blocks[l], s);
+    return;
+  }
+  for (int id : p.common_order) launch_contract_c64(common_args(p, id, W), s);
+}
+
+ContractArgs common_args(const Plan& p, int id, unsigned char* W) {
+  {
     const Node& n = p.nodes[id];
     View a = view_of(p, n.u, W), b = view_of(p, n.v, W);
     ContractArgs args;
@@ -507,7 +572,7 @@ void run_common(const Plan& p, unsigned char* W, cudaStream_t s) {
       }
     }
     args.n_red = nr;
-    launch_contract_c64(args, s);
+    return args;
   }
 }
 
@@ -871,7 +936,8 @@ void stem_body(Plan& p, const tn_buffers* b, cudaStream_t s, bool head = true, b
     rec_event(p, 0, s);
     TN_CUDA(cudaMemsetAsync(W + p.ws_scratch, 0, sc.bytes, s));
     run_common(p, W, s);
-    p.launches += p.common_order.size();
+    static const bool serial = getenv("TN_COMMON_SERIAL") != nullptr;
+    p.launches += (!serial && p.common_dev && p.common_key == W) ? p.common_level_nodes.size() : p.common_order.size();
   }
   p.result_in_ws = p.steps.empty();
   if (p.steps.empty()) return;
@@ -1056,6 +1122,7 @@ void stem_contract(Plan& p, const tn_buffers* b, uint64_t slice_id, cudaStream_t
   }
   launch_set_u64(reinterpret_cast<uint64_t*>(W + p.ws_slice), slice_id, s);
   if (fused_swap_enabled(p) && p.n_swaps > 0) ensure_peers(p, b, s);  // outside any capture
+  prepare_common(p, W);
   if (graph_wanted(p)) {
     const bool same = p.graph_exec && p.graph_key[0] == b->d_ws && p.graph_key[1] == b->d_stem[0] &&
                       p.graph_key[2] == b->d_stem[1] && p.graph_stem_bytes == b->stem_bytes && p.graph_timing == p.timing;
@@ -1622,6 +1689,7 @@ void tn_plan_free(tn_plan* h) {
   if (!h) return;
   if (h->p->pinned) cudaFreeHost(h->p->pinned);
   close_peers(*h->p);
+  if (h->p->common_dev) cudaFree(h->p->common_dev);
   if (h->p->graph_exec) cudaGraphExecDestroy((cudaGraphExec_t)h->p->graph_exec);
   if (h->p->cap_stream) cudaStreamDestroy((cudaStream_t)h->p->cap_stream);
   for (void* e : h->p->ev) cudaEventDestroy((cudaEvent_t)e);
