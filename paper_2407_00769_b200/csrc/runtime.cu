@@ -262,7 +262,7 @@ void close_peers(Plan& p) {
 
 void ensure_peers(Plan& p, const tn_buffers* b, cudaStream_t s) {
   if (p.world <= 1 || !p.comm) return;
-  if (p.peer_key[0] == b->d_stem[0] && p.peer_key[1] == b->d_stem[1] && p.peer_stem.size() == 2u * p.world) return;
+  if (p.peer_key[0] == b->d_stem[0] && p.peer_key[1] == b->d_stem[1]) return;  // set up (or refused) already
   close_peers(p);
   tn_comm* c = p.comm;
   std::vector<void*> ptrs(2 * p.world, nullptr);
@@ -290,50 +290,84 @@ void ensure_peers(Plan& p, const tn_buffers* b, cudaStream_t s) {
         throw TnError{TN_E_CUDA, "cuMemGetAddressRange unavailable"};
       range = (addr_range_t)fn;
     }
+    // Every rank takes part in both collectives whatever fails locally, and all ranks agree on the
+    // outcome: if any rank cannot export or map a buffer, nobody uses peer memory (the swaps then go
+    // through the transport), instead of some ranks storing into peers that never mapped them.
     struct Rec {
       cudaIpcMemHandle_t h[2];
       uint64_t off[2];
+      int ok;
+      int pad;
     };
     Rec mine;
     memset(&mine, 0, sizeof(mine));
-    for (int j = 0; j < 2; ++j) {
+    mine.ok = 1;
+    for (int j = 0; j < 2 && mine.ok; ++j) {
       CUdeviceptr base = 0;
       size_t sz = 0;
-      if (range(&base, &sz, (CUdeviceptr)b->d_stem[j]) != CUDA_SUCCESS)
-        throw TnError{TN_E_CUDA, "cuMemGetAddressRange failed on a stem buffer"};
-      TN_CUDA(cudaIpcGetMemHandle(&mine.h[j], (void*)base));
+      if (range(&base, &sz, (CUdeviceptr)b->d_stem[j]) != CUDA_SUCCESS ||
+          cudaIpcGetMemHandle(&mine.h[j], (void*)base) != cudaSuccess) {
+        cudaGetLastError();
+        mine.ok = 0;
+        break;
+      }
       mine.off[j] = (uint64_t)((CUdeviceptr)b->d_stem[j] - base);
     }
     unsigned char* d = nullptr;
-    TN_CUDA(cudaMalloc(&d, sizeof(Rec) * (p.world + 1)));
+    TN_CUDA(cudaMalloc(&d, sizeof(Rec) * (p.world + 1) + 256));
     std::vector<Rec> all(p.world);
+    bool ok = true;
     try {
       TN_CUDA(cudaMemcpyAsync(d, &mine, sizeof(Rec), cudaMemcpyHostToDevice, s));
       xfer_allgather(p, d, d + sizeof(Rec), sizeof(Rec), s);
       TN_CUDA(cudaMemcpyAsync(all.data(), d + sizeof(Rec), sizeof(Rec) * p.world, cudaMemcpyDeviceToHost, s));
       TN_CUDA(cudaStreamSynchronize(s));
+      for (const Rec& r : all) ok = ok && r.ok;
+      std::vector<std::pair<cudaIpcMemHandle_t, void*>> opened;  // one mapping per allocation
+      bool mapped = true;
+      for (int r = 0; ok && mapped && r < p.world; ++r)
+        for (int j = 0; mapped && j < 2; ++j) {
+          if (r == p.rank) {
+            ptrs[2 * r + j] = b->d_stem[j];
+            continue;
+          }
+          void* base = nullptr;
+          for (auto& o : opened)
+            if (!memcmp(&o.first, &all[r].h[j], sizeof(cudaIpcMemHandle_t))) base = o.second;
+          if (!base) {
+            if (cudaIpcOpenMemHandle(&base, all[r].h[j], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+              cudaGetLastError();
+              mapped = false;
+              break;
+            }
+            opened.push_back({all[r].h[j], base});
+            p.ipc_open.push_back(base);
+          }
+          ptrs[2 * r + j] = static_cast<unsigned char*>(base) + all[r].off[j];
+        }
+      if (ok) {
+        // second agreement: every rank mapped every peer (max over ranks of "failed")
+        float* flag = reinterpret_cast<float*>(d + sizeof(Rec) * (p.world + 1));
+        const float failed = mapped ? 0.f : 1.f;
+        TN_CUDA(cudaMemcpyAsync(flag, &failed, 4, cudaMemcpyHostToDevice, s));
+        xfer_allreduce_max(p, flag, s);
+        float any = 0.f;
+        TN_CUDA(cudaMemcpyAsync(&any, flag, 4, cudaMemcpyDeviceToHost, s));
+        TN_CUDA(cudaStreamSynchronize(s));
+        ok = any == 0.f;
+      }
     } catch (...) {
       cudaFree(d);
       throw;
     }
     TN_CUDA(cudaFree(d));
-    std::vector<std::pair<cudaIpcMemHandle_t, void*>> opened;  // one mapping per allocation
-    for (int r = 0; r < p.world; ++r)
-      for (int j = 0; j < 2; ++j) {
-        if (r == p.rank) {
-          ptrs[2 * r + j] = b->d_stem[j];
-          continue;
-        }
-        void* base = nullptr;
-        for (auto& o : opened)
-          if (!memcmp(&o.first, &all[r].h[j], sizeof(cudaIpcMemHandle_t))) base = o.second;
-        if (!base) {
-          TN_CUDA(cudaIpcOpenMemHandle(&base, all[r].h[j], cudaIpcMemLazyEnablePeerAccess));
-          opened.push_back({all[r].h[j], base});
-          p.ipc_open.push_back(base);
-        }
-        ptrs[2 * r + j] = static_cast<unsigned char*>(base) + all[r].off[j];
-      }
+    if (!ok) {
+      fprintf(stderr, "tn: peer-memory mode swaps unavailable (CUDA IPC); using the transport\n");
+      close_peers(p);
+      p.peer_key[0] = b->d_stem[0];  // do not retry for this buffer set
+      p.peer_key[1] = b->d_stem[1];
+      return;
+    }
   }
   p.peer_stem = ptrs;
   p.peer_key[0] = b->d_stem[0];
