@@ -377,28 +377,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 *reinterpret_cast<uint4*>(srow + chunk * 16) = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
               }
             }
-            continue;
-          }
-          uint32_t pk[16];
-#pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const float x0 = __uint_as_float(r[h][2 * j]) * sc, x1 = __uint_as_float(r[h][2 * j + 1]) * sc;
-            __half2 hv = __floats2half2_rn(x0, x1);
-            mx = fmaxf(mx, fmaxf(fabsf(x0), fabsf(x1)));
-            pk[j] = *reinterpret_cast<uint32_t*>(&hv);
-          }
-          if (epi == 4) {
-            uint32_t* st32 = reinterpret_cast<uint32_t*>(sbuf);
-            const int q0 = (c & 63) >> 1;
-#pragma unroll
-            for (int j = 0; j < 16; ++j) st32[(q0 + j) * BM + row] = pk[j];
           } else {
-            unsigned char* srow = sbuf + row * 128;
-            const int cb = (c & 63) >> 3;
+            uint32_t pk[16];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const int chunk = (cb + q) ^ (row & 7);
-              *reinterpret_cast<uint4*>(srow + chunk * 16) = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+            for (int j = 0; j < 16; ++j) {
+              const float x0 = __uint_as_float(r[h][2 * j]) * sc, x1 = __uint_as_float(r[h][2 * j + 1]) * sc;
+              __half2 hv = __floats2half2_rn(x0, x1);
+              mx = fmaxf(mx, fmaxf(fabsf(x0), fabsf(x1)));
+              pk[j] = *reinterpret_cast<uint32_t*>(&hv);
+            }
+            if (epi == 4) {
+              uint32_t* st32 = reinterpret_cast<uint32_t*>(sbuf);
+              const int q0 = (c & 63) >> 1;
+#pragma unroll
+              for (int j = 0; j < 16; ++j) st32[(q0 + j) * BM + row] = pk[j];
+            } else {
+              unsigned char* srow = sbuf + row * 128;
+              const int cb = (c & 63) >> 3;
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const int chunk = (cb + q) ^ (row & 7);
+                *reinterpret_cast<uint4*>(srow + chunk * 16) = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+              }
             }
           }
         }
