@@ -283,3 +283,80 @@ def test_recompute_on_halves_halves_peak(tnmod, world):
     with pytest.raises(tnmod.TnError):
         _load(tnmod, plan, stem_min_log2=20, recompute=1, split_log2=2)
     assert max(sizes) + (world.bit_length() - 1) >= 32    # the recomputed region holds the 2^33 tensor
+
+
+def _runs(step):
+    """Stored order of a step's input, innermost first, as 'k'/'m' per mode."""
+    R = set(step["R"])
+    return ["k" if x in R else "m" for x in reversed(step["in"])]
+
+
+@pytest.mark.parametrize("world", [1, 4])
+def test_mn_major_lowering(tnmod, world):
+    """Steps folded into the MN-major operand (plan.cpp, StemStep::mn): stored order
+    [kept | contracted | >= 7 kept], K >= 64, N >= 64, >= 2^28 elements; the permutation stays as the
+    fallback (perm = 1) but is not counted in n_permutes / perm_bytes."""
+    with open(os.path.join(ROOT, "plans", "c3.json")) as f:
+        plan = json.load(f)
+    p = _load(tnmod, plan, virtual_world=world)
+    rep, info = p.report(), p.info()
+    mn = [s for s in rep["steps"] if s["mn"]]
+    assert len(mn) >= 1
+    for s in mn:
+        runs = _runs(s)
+        ma = s["mn"]
+        assert ma >= 7 and runs[:ma] == ["m"] * ma and runs[ma:ma + s["k"]] == ["k"] * s["k"]
+        assert set(runs[ma + s["k"]:]) <= {"m"}
+        assert s["k"] >= 6 and s["n"] >= 6 and len(s["in"]) >= 28 and s["perm"] == 1 and s["ga"] == 0
+    # (+1: the final permutation into output order, one GPU)
+    assert info["n_permutes"] - sum(1 for s in rep["steps"] if s["perm"] and not s["mn"]) in (0, 1)
+
+
+@pytest.mark.parametrize("name", ["c2", "c3"])
+def test_row_folding_lowering(tnmod, name):
+    """Row folding (StemStep::fold): only plain A (as stored or after a pass; no gather), row-major outputs with rows of
+    2K fp16 < 128 B, f = 128 B / row bytes, at least 2^8 folded rows; such steps run on tcgen05."""
+    with open(os.path.join(ROOT, "plans", f"{name}.json")) as f:
+        plan = json.load(f)
+    for world in (1, 4):
+        rep = _load(tnmod, plan, virtual_world=world).report()
+        for s in rep["steps"]:
+            if s["fold"] > 1:
+                assert s["ga"] == 0 and s["mn"] == 0 and s["out_kind"] == 0 and s["k"] <= 4 and s["tc"] == 1
+                assert s["fold"] * (4 << s["k"]) == 128 and s["m"] - (s["fold"].bit_length() - 1) >= 8
+
+
+def test_no_transposed_output_for_row_streaming_steps(tnmod):
+    """Layout policy 3 never gives a SIMT row-streaming step (K <= 16, N <= 32, K N <= 128) a
+    transposed output: its stores would be 4-byte scatters."""
+    with open(os.path.join(ROOT, "plans", "c3.json")) as f:
+        plan = json.load(f)
+    for world in (1, 2, 4, 8):
+        rep = _load(tnmod, plan, virtual_world=world).report()
+        for s in rep["steps"]:
+            if s["k"] <= 4 and s["n"] <= 5 and s["k"] + s["n"] <= 7:
+                assert s["out_kind"] != 1
+
+
+@pytest.mark.parametrize("world,routable", [(4, 5), (8, 10)])
+def test_swaps_routable_by_the_epilogue(tnmod, world, routable):
+    """The C3 swap schedule at 4 / 8 ranks: every swapped-in mode is a bit of the previous tcgen05
+    step's output that a store box keeps constant (m bit >= 7 or n bit >= 5 of its M / N index), so
+    every swap can be done by that GEMM's epilogue (runtime.cu fused_swap_target)."""
+    with open(os.path.join(ROOT, "plans", "c3.json")) as f:
+        plan = json.load(f)
+    rep = _load(tnmod, plan, virtual_world=world).report()
+    ok = 0
+    for i, s in enumerate(rep["steps"]):
+        if not s["swap"]:
+            continue
+        pv = rep["steps"][i - 1]
+        pos = [len(pv["out"]) - 1 - pv["out"].index(x) for x in s["swap_in"]]
+        if pv["out_kind"] == 0:
+            good = all(q >= pv["n"] + 7 or 5 <= q < pv["n"] for q in pos)
+        elif pv["out_kind"] == 1:
+            good = all(7 <= q < pv["m"] or q >= pv["m"] + 5 for q in pos)
+        else:
+            good = False
+        ok += bool(good and pv["tc"] and pv["fold"] == 1)
+    assert rep["n_swaps"] == routable and ok == routable
