@@ -434,27 +434,46 @@ def main():
         gemm_bytes += by
         gemm_flops += fl
         t_roof_gemm += max(by / (hbm * 1e9), fl / (tc_peak * 1e12)) * 1e3
-        if st["perm"]:
+        if st.get("pass", st["perm"]):  # (an MN-major step has perm = 1 but runs no pass)
             perm_bytes += 2 * eb * M * K
     final_ms = ms[-1] if ms else 0.0
     if rep.get("final_layout") and final_ms > 0:
         perm_ms += final_ms
         perm_bytes += 2 * eb * 2.0 ** len(rep["final_layout"])
     common_ms = ms[0] if ms else 0.0
+    # per GEMM kernel (the library reports which kernel each step ran: "tc2" CTA-pair tcgen05,
+    # "tc2_mn" its MN-major form, "tc1" single-CTA tcgen05, "simt", "c64"); the dominant one is the
+    # kernel with the most step time.  The GEMM family as a whole is kept beside it.
+    fam = {}
+    for i, st in enumerate(steps):
+        k = st.get("kern") or "gemm"
+        k = "gemm_chalf_tc2" if k.startswith("tc2") else {"tc1": "gemm_chalf_tc", "simt": "gemm_chalf_rows",
+                                                          "c64": "gemm_c64"}.get(k, k)
+        M, K, N = 2.0 ** st["m"], 2.0 ** st["k"], 2.0 ** st["n"]
+        f = fam.setdefault(k, {"ms": 0.0, "flops": 0.0, "bytes": 0.0, "launches": 0})
+        f["ms"] += ms[2 + 2 * i]
+        f["flops"] += 8 * M * K * N
+        f["bytes"] += eb * (M * K + M * N) + 8 * K * N
+        f["launches"] += 1
+
+    def roof_of(name, ms_, flops_, bytes_):
+        if bytes_ / (hbm * 1e9) >= flops_ / (tc_peak * 1e12):
+            ach = bytes_ / (ms_ * 1e-3) / 1e9
+            return {"kernel": name, "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm}
+        ach = flops_ / (ms_ * 1e-3) / 1e12
+        return {"kernel": name, "bound": "tensor", "achieved": ach, "peak": tc_peak, "unit": "TFLOP/s",
+                "frac": ach / tc_peak, "peak_kind": "sustained (kernel inside a long step)", "peak_burst": tc_burst,
+                "frac_burst": ach / tc_burst, "peak_spec": 2250.0, "frac_spec": ach / 2250.0}
+
     if gemm_ms >= perm_ms:
-        bytes_bound = gemm_bytes / (hbm * 1e9) >= gemm_flops / (tc_peak * 1e12)
-        if bytes_bound:
-            ach = gemm_bytes / (gemm_ms * 1e-3) / 1e9
-            roof = {"kernel": "gemm_chalf_tc (+simt small-K/N steps)", "bound": "hbm", "achieved": ach, "peak": hbm,
-                    "unit": "GB/s", "frac": ach / hbm}
-        else:
-            ach = gemm_flops / (gemm_ms * 1e-3) / 1e12
-            roof = {"kernel": "gemm_chalf_tc", "bound": "tensor", "achieved": ach, "peak": tc_peak,
-                    "unit": "TFLOP/s", "frac": ach / tc_peak, "peak_kind": "sustained (kernel inside a long step)",
-                    "peak_burst": tc_burst, "frac_burst": ach / tc_burst, "peak_spec": 2250.0,
-                    "frac_spec": ach / 2250.0}
-        roof["roofline_time_frac"] = t_roof_gemm / gemm_ms if gemm_ms else None
-        roof["launches_per_step"] = len(steps)
+        dom = max(fam, key=lambda k: fam[k]["ms"])
+        d = fam[dom]
+        roof = roof_of(dom, d["ms"], d["flops"], d["bytes"])
+        roof["launches_per_step"] = d["launches"]
+        roof["share_of_gemm_time"] = d["ms"] / gemm_ms if gemm_ms else None
+        roof["gemm_family"] = roof_of("all stem GEMMs", gemm_ms, gemm_flops, gemm_bytes)
+        roof["gemm_family"]["roofline_time_frac"] = t_roof_gemm / gemm_ms if gemm_ms else None
+        roof["per_kernel_ms"] = {k: round(v["ms"], 3) for k, v in sorted(fam.items(), key=lambda x: -x[1]["ms"])}
     else:
         ach = perm_bytes / (perm_ms * 1e-3) / 1e9
         roof = {"kernel": "permute", "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm}
@@ -462,14 +481,17 @@ def main():
     # traffic: DRAM bytes (dram__bytes_read + dram__bytes_write) of the same kernel family per
     # subtask, from the committed ncu launch list of this command (profiles/, C3 single GPU only)
     roof["traffic"] = None
-    roof["algorithmic_bytes"] = gemm_bytes
+    roof["algorithmic_bytes"] = fam[roof["kernel"]]["bytes"] if roof["kernel"] in fam else gemm_bytes
     summ_name = {"c3": "r02_launches_summary.json", "c3_sweep": "r01_launches_summary.json"}.get(args.plan)
     summ = os.path.join(ROOT, "profiles", summ_name) if summ_name else ""
     if roof["kernel"].startswith("gemm") and world == 1 and summ and os.path.exists(summ):
         with open(summ) as fh:
             ps = json.load(fh)["per_subtask"]
-        roof["traffic"] = sum(ps[f]["dram_bytes"] for f in ("gemm_tc", "gemm_simt") if f in ps)
-        roof["traffic_source"] = f"profiles/{summ_name} (ncu, bytes per subtask, all GEMM launches)"
+        # ncu families (tools/ncu_summary.py): gemm_tc2 = the CTA-pair kernel (both forms)
+        key = {"gemm_chalf_tc2": "gemm_tc2", "gemm_chalf_tc": "gemm_tc", "gemm_chalf_rows": "gemm_simt"}.get(roof["kernel"])
+        if key in ps:
+            roof["traffic"] = ps[key]["dram_bytes"]
+            roof["traffic_source"] = f"profiles/{summ_name} (ncu, DRAM bytes per subtask of this kernel's launches)"
     roof["share_of_step"] = {"gemm": gemm_ms / t_ms, "permute": perm_ms / t_ms, "common+prep": common_ms / t_ms}
     # path roofline: sum over stem steps of max(F/P, B_alg/BW) over the measured step
     # time, and the step-shape histogram (log2 K*N -> steps) of the plan

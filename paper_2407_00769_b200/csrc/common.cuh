@@ -101,6 +101,10 @@ struct PermArgs {
   int64_t outer_out[64];
 };
 
+// Which GEMM kernel family the last stem-GEMM launch on this host thread used ("tc2", "tc2_mn",
+// "tc1", "simt", "c64"; reporting only: tn_report_json's per-step "kern")
+extern thread_local const char* g_last_kern;
+
 // ---- launchers (all asynchronous on `s`) ----
 // Member chunks of a mode swap through peer memory: output bytes [v chunk_bytes, (v+1) chunk_bytes)
 // of a permutation go to base[v] (member v's receive buffer at this rank's chunk) instead of dst.

@@ -1236,6 +1236,7 @@ static void launch_bn(__half* c, const __half* a, const __half* bp, uint64_t M, 
     memset(&g0, 0, sizeof(g0));
     NdArgs n0;
     memset(&n0, 0, sizeof(n0));
+    g_last_kern = "tc1";
     tc::gemm_chalf_tc_kernel<BN, KB, G><<<grid, tc::kThreads, C::kSmem, s>>>(
         ma, mbm, mc, (uint32_t)(tiles / num_n), num_n, (int)K2, in_max, b_bound, out_max, exp_slot, sa0,
         reinterpret_cast<uint32_t*>(c), c_rows, cols / 2, g0, n0, 0, ba, PeerStore{});
@@ -1294,6 +1295,7 @@ static void launch_bn(__half* c, const __half* a, const __half* bp, uint64_t M, 
     uint64_t tiles = (uint64_t)num_m * num_n;
     int grid = (int)std::min<uint64_t>(tiles, (uint64_t)num_sms());
     // the exponent is recorded once (first chunk); later chunks reuse the same inputs
+    g_last_kern = "tc1";
     tc::gemm_chalf_tc_kernel<BN, KB, G><<<grid, (G == 1 || G == 4) ? tc::kThreadsGather : tc::kThreads, C::kSmem, s>>>(
         ma, mb, mc, num_m, num_n, (int)K2, in_max, b_bound, out_max, m_off ? nullptr : exp_slot, sa, out_sc, mm,
         n_cols, gargs, nda, transposed ? 4 : (packed ? 5 : epi_stg), BatchArgs{}, ps);

@@ -92,6 +92,7 @@ __global__ void __launch_bounds__(256) gemm_c64_kernel(float2* __restrict__ C, c
 void launch_gemm_c64(float2* c, const float2* a, const float2* b, uint64_t M, uint32_t K, uint32_t N,
                      const OutMap* om_in, cudaStream_t s, const float* in_max, const float* b_bound, uint32_t* out_max,
                      int* exp_slot) {
+  g_last_kern = "c64";
   OutMap om = om_in ? *om_in : identity_map(M, N);
   uint64_t gy = (M + TM - 1) / TM;
   if (gy > 65535ull * 1024) throw TnError{TN_E_UNSUPPORTED, "gemm_c64: M too large"};
@@ -410,6 +411,7 @@ static bool rows_ok(uint32_t K, uint32_t N) { return K <= 16 && N <= 32 && K * N
 void launch_gemm_chalf_simt(__half2* c, const __half2* a, const __half* bp, uint64_t M, uint32_t K, uint32_t N,
                             const float* in_max, const float* b_bound, uint32_t* out_max, int* exp_slot,
                             const OutMap* om_in, cudaStream_t s) {
+  g_last_kern = "simt";
   if (K > (uint32_t)kTileCplx) throw TnError{TN_E_UNSUPPORTED, "SIMT complex-half GEMM: K > 4096"};
   OutMap om = om_in ? *om_in : identity_map(M, N);
   int nlog = 0;

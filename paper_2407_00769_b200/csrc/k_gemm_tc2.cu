@@ -52,6 +52,7 @@ static void launch_tc2_t(const CUtensorMap& ma, const CUtensorMap& mb, const CUt
   const int order = order_env >= 0 ? order_env : (a_fits_l2 && num_mp >= 8ull * (uint64_t)pairs ? 1 : 0);
   const uint64_t busy = order == 1 ? std::min<uint64_t>(num_mp, (uint64_t)pairs) : std::min<uint64_t>(tiles, (uint64_t)pairs);
   const int grid = 2 * (int)busy;
+  g_last_kern = kMN ? "tc2_mn" : "tc2";
   tc2::gemm_chalf_tc2_kernel<BN, kMN><<<grid, tc::kThreads, C::kSmem, s>>>(ma, mb, mc, num_mp, num_n, K2, in_max, b_bound,
                                                                       out_max, exp_slot, epi, m_base, order, ps, nda, mn_ma, rp);
   TN_CUDA(cudaGetLastError());

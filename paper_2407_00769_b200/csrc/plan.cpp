@@ -946,6 +946,8 @@ std::string report_json(const Plan& p, const std::vector<float>& ms) {
       << ",\"fuse_quant\":" << (s.fuse_quant ? 1 : 0)
       << ",\"out_kind\":" << (s.out_identity ? 0 : (s.out_transposed ? 1 : 2)) << ",\"mn\":" << (s.mn ? s.mn_ma : 0)
       << ",\"fold\":" << s.fold
+      << ",\"kern\":\"" << (i < p.step_kern.size() ? p.step_kern[i] : std::string()) << "\""
+      << ",\"pass\":" << (i < p.step_pass.size() ? p.step_pass[i] : (s.perm ? 1 : 0))
       << ",\"in\":";
     jlist(o, s.in_layout);
     o << ",\"R\":";

@@ -23,6 +23,9 @@
 #include "common.cuh"
 
 using namespace tn;
+namespace tn {
+thread_local const char* g_last_kern = "";
+}
 
 static thread_local std::string g_err;
 
@@ -1033,6 +1036,11 @@ void stem_body(Plan& p, const tn_buffers* b, cudaStream_t s, bool head = true, b
       mode_swap(p, st, b, cur, s, &sc.max_slot[i]);
     }
     swapped = false;
+    if (p.step_kern.size() != p.steps.size()) {
+      p.step_kern.assign(p.steps.size(), "");
+      p.step_pass.assign(p.steps.size(), 0);
+    }
+    p.step_pass[i] = st.perm && !mn_active(p, st);
     if (st.perm && !mn_active(p, st)) {
       launch_permute(b->d_stem[1 - cur], b->d_stem[cur], eb, (int)st.in_layout.size(), st.perm_axes.data(), s);
       ++p.launches;
@@ -1046,9 +1054,11 @@ void stem_body(Plan& p, const tn_buffers* b, cudaStream_t s, bool head = true, b
     if (fuse) xfer_allreduce_max(p, &sc.max_slot[i], s);
     rec_event(p, 2 + 2 * i, s);
     // (sharded: the max all-reduces inside make every rank scale the next step identically)
+    g_last_kern = "";
     run_gemm(p, st, i, b->d_stem[cur], b->d_stem[1 - cur], 0, &sc.max_slot[i],
              reinterpret_cast<uint32_t*>(&sc.max_slot[i + 1]), &sc.exps[2 + 2 * i], W, sc, s, true,
              fuse ? &pt : nullptr);
+    p.step_kern[i] = g_last_kern;
     cur = 1 - cur;
     if (fuse && pt.honored) {
       swapped = true;

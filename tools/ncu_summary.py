@@ -13,6 +13,8 @@ import sys
 
 
 def family(name):
+    if "gemm_chalf_tc2" in name:
+        return "gemm_tc2"  # the CTA-pair kernel (plain, N-d box and MN-major forms)
     if "gemm_chalf_tc" in name:
         return "gemm_tc"
     if "gemm_chalf_rows" in name or "gemm_chalf_simt" in name:
