@@ -90,6 +90,28 @@ __device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* m
       : "memory");
 }
 
+// The same with an L2 eviction-priority hint (createpolicy): the streamed A operand evict_first, the
+// B_P tile every m pair re-reads evict_last, so the A stream does not push B out of L2
+__device__ __forceinline__ void tma_load_2d_pair_hint(void* dst, const CUtensorMap* map, uint32_t bar_cluster, int c0,
+                                                      int c1, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar_cluster), "l"(pol)
+      : "memory");
+}
+
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
 // N-dimensional form (2..5 dims, coordinates innermost first): the fused stem permutation of a
 // gathered-A step (NdArgs, gemm_tc.cuh) loaded per CTA of the pair
 __device__ __forceinline__ void tma_load_nd_pair(void* dst, const CUtensorMap* map, uint32_t bar_cluster, int nd,
@@ -185,7 +207,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                           const __grid_constant__ CUtensorMap tmC, uint32_t num_mp, uint32_t num_n, int K2,
                           const float* in_max, const float* b_bound, uint32_t* out_max, int* exp_slot, int epi,
                           uint64_t m_base, int order, const __grid_constant__ PeerStore ps,
-                          const __grid_constant__ NdArgs nda, int mn_ma, const __grid_constant__ RowPerm rp) {
+                          const __grid_constant__ NdArgs nda, int mn_ma, const __grid_constant__ RowPerm rp,
+                          int l2_hints) {
   // complex rows per CTA tile, per pair tile
   constexpr int kRows = kMN ? BM / 2 : BM;
   using C = Cfg2<BN>;
@@ -236,6 +259,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       // ===== TMA producer (both CTAs): this CTA's A rows and B half, completing on the leader =====
       int s = 0;
       uint32_t ph = 0;
+      const bool hints = l2_hints != 0;
+      const uint64_t pol_a = hints ? l2_policy_evict_first() : 0, pol_b = hints ? l2_policy_evict_last() : 0;
       int mp, nb;
       for (uint32_t i = 0; tc2_tile(i, pair, npairs, num_mp, num_n, order, mp, nb); ++i) {
         const int a_row = mp * 2 * kRows + (int)rank * kRows;
@@ -256,10 +281,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             int cc[5];
             nd_coords_k(nda, (uint32_t)kb * (KB / 2), cm, cc);
             tma_load_nd_pair(sA + s * C::kABytes, &tmA, fb, nda.nd, cc);
+          } else if (hints) {
+            tma_load_2d_pair_hint(sA + s * C::kABytes, &tmA, fb, kb * KB, a_row, pol_a);
           } else {
             tma_load_2d_pair(sA + s * C::kABytes, &tmA, fb, kb * KB, a_row);
           }
-          tma_load_2d_pair(sB + s * C::kBBytes, &tmB, fb, kb * KB, b_row);
+          if (hints)
+            tma_load_2d_pair_hint(sB + s * C::kBBytes, &tmB, fb, kb * KB, b_row, pol_b);
+          else
+            tma_load_2d_pair(sB + s * C::kBBytes, &tmB, fb, kb * KB, b_row);
           if (++s == C::kStages) {
             s = 0;
             ph ^= 1;

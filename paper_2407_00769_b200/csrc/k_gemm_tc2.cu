@@ -53,8 +53,12 @@ static void launch_tc2_t(const CUtensorMap& ma, const CUtensorMap& mb, const CUt
   const uint64_t busy = order == 1 ? std::min<uint64_t>(num_mp, (uint64_t)pairs) : std::min<uint64_t>(tiles, (uint64_t)pairs);
   const int grid = 2 * (int)busy;
   g_last_kern = kMN ? "tc2_mn" : "tc2";
+  // L2 eviction hints on the A / B loads (A evict_first, B evict_last; TN_L2_HINTS=1, A/B knob): measured
+  // worse — C3 step 30's shape read 158.8 GB from DRAM with them vs 141.3 GB without (the clusters that
+  // share an m pair re-read its A rows from L2), M = 2^21 K = 2^9 N = 2^10 8.5 vs 6.3 ms — so off
+  static const int hints_env = getenv("TN_L2_HINTS") ? atoi(getenv("TN_L2_HINTS")) : 0;
   tc2::gemm_chalf_tc2_kernel<BN, kMN><<<grid, tc::kThreads, C::kSmem, s>>>(ma, mb, mc, num_mp, num_n, K2, in_max, b_bound,
-                                                                      out_max, exp_slot, epi, m_base, order, ps, nda, mn_ma, rp);
+                                                                      out_max, exp_slot, epi, m_base, order, ps, nda, mn_ma, rp, hints_env);
   TN_CUDA(cudaGetLastError());
 }
 
