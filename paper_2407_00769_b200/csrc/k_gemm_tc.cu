@@ -92,6 +92,37 @@ static bool build_nd(const AGather& ag, NdPlan& out) {
     if (!used_m[j]) grow(0, j);
   for (int j = 0; j < ag.klog; ++j)
     if (!used_k[j]) grow(1, j);
+  // Outside the box, two runs that are adjacent in the source (one m run, one k run, in either
+  // order) share one tensor dim: its coordinate is the m part | the k part shifted past it (NdArgs
+  // keeps one m and one k part per dim).  E.g. [k5 | m11 | k8 | m2 | k3 | m3] (6 runs) becomes
+  // 4 dims {k5}{m11}{k8 m2}{k3 m3}.
+  auto all_out = [&](const std::vector<std::pair<int, int>>& d) {
+    for (auto& b : d)
+      if (inbox(b.first, b.second)) return false;
+    return true;
+  };
+  auto one_kind = [&](const std::vector<std::pair<int, int>>& d) {
+    for (auto& b : d)
+      if (b.first != d[0].first) return false;
+    return true;
+  };
+  for (bool merged = true; merged && dims.size() > 5;) {
+    merged = false;
+    for (size_t a = 0; a < dims.size() && !merged; ++a)
+      for (size_t b = 0; b < dims.size() && !merged; ++b) {
+        if (a == b || !all_out(dims[a]) || !all_out(dims[b]) || !one_kind(dims[a]) || !one_kind(dims[b]) ||
+            dims[a][0].first == dims[b][0].first)
+          continue;
+        const auto& lo = dims[a];
+        const auto& hi = dims[b];
+        if (src(hi[0].first, hi[0].second) != src(lo.back().first, lo.back().second) + 1) continue;
+        std::vector<std::pair<int, int>> m = lo;
+        m.insert(m.end(), hi.begin(), hi.end());
+        dims[a] = m;
+        dims.erase(dims.begin() + b);
+        merged = true;
+      }
+  }
   if (dims.size() > 5) return false;
   // box dims must tile the box sequence in order (each a contiguous segment)
   size_t pos = 0;
@@ -118,8 +149,31 @@ static bool build_nd(const AGather& ag, NdPlan& out) {
     out.dim[d] = 1ull << v.size();
     out.stride[d] = 4ull << src(v[0].first, v[0].second);
     out.box[d] = 1u << nbox;
-    if (mixed && nbox != (int)v.size()) return false;  // a mixed dim must lie inside the box
-    if (nbox != (int)v.size()) {  // the dim's bits are consecutive j of one kind
+    if (mixed && nbox != 0 && nbox != (int)v.size()) return false;  // a mixed dim lies inside or outside the box
+    if (nbox == 0) {
+      // outside the box: one run of consecutive j per kind (two when merged above), each the
+      // coordinate bits [offset, offset + length) of the dim
+      int off = 0;
+      for (size_t q = 0; q < v.size();) {
+        size_t e = q + 1;
+        while (e < v.size() && v[e].first == v[q].first && v[e].second == v[e - 1].second + 1) ++e;
+        const int len = (int)(e - q);
+        const uint32_t mask = len >= 32 ? 0xffffffffu : ((1u << len) - 1);
+        if (v[q].first == 0) {
+          if (out.args.mmask[d]) return false;
+          out.args.mj0[d] = (int8_t)v[q].second;
+          out.args.mmask[d] = mask;
+          out.args.msh[d] = (int8_t)off;
+        } else {
+          if (out.args.kmask[d]) return false;
+          out.args.kj0[d] = (int8_t)v[q].second;
+          out.args.kmask[d] = mask;
+          out.args.ksh[d] = (int8_t)off;
+        }
+        off += len;
+        q = e;
+      }
+    } else if (nbox != (int)v.size()) {  // the dim's bits are consecutive j of one kind
       const uint32_t mask = v.size() >= 32 ? 0xffffffffu : ((1u << v.size()) - 1);
       if (v[0].first == 0) {
         out.args.mj0[d] = (int8_t)v[0].second;

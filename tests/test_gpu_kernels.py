@@ -417,7 +417,9 @@ def test_gemm_chalf_gathered_word_pieces_exact(env, runs, N):
                                     ("k7m9", 256), ("k2m3k3m9", 4), ("k2m7k1m1k3m2", 64), ("k4m2k3m8", 2),
                                     ("k3m1k4m9", 128), ("k2m12k4", 16),
                                     # 128-byte rows, N >= 128, M % 256 == 0: the CTA-pair kernel's N-d box
-                                    ("k5m9k2m4", 128), ("k6m8k3m5", 256)])
+                                    ("k5m9k2m4", 128), ("k6m8k3m5", 256),
+                                    # 6 source runs: adjacent m / k runs outside the box share a TMA dim
+                                    ("k5m8k3m2k2m3", 32), ("k5m9k2m1k3m2", 128)])
 def test_gemm_chalf_gathered_runs_exact(env, runs, N):
     """Stem layouts as they occur on the C3 path (runs of contracted k / kept m modes, innermost
     first, kept modes in stored order): these go through the N-dimensional TMA box (swizzled rows
