@@ -88,6 +88,7 @@ struct OutMap {
   int64_t ms[kMaxModes];
   int64_t ns[24];
   PeerTarget* peer;              // host only (nullptr: local output)
+  int fold_t;                    // 2: a row-folded GEMM (f = 2, N = 16) writing the unfolded C^T [16][2 M]
 };
 
 struct PermArgs {

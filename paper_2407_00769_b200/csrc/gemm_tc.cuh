@@ -857,6 +857,13 @@ __global__ void __launch_bounds__((kAMode == 1 || kAMode == 4) ? kThreadsGather 
                 }
               }
             }
+          } else if (BN == 64 && epi_stg == 6) {
+            // row-folded GEMM (f = 2) with a transposed output: tile row p holds output rows 2p + h
+            // (h = this 32-column half) for 16 complex columns; staged as C^T [16 n][256 m], one
+            // TMA box of 1 KB rows
+            uint32_t* st32 = reinterpret_cast<uint32_t*>(sbuf);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) st32[j * (2 * BM) + 2 * row + h] = pk[j];
           } else if (epi_stg == 4) {
             // transposed store C[n][m] (layout policy 3): stage the subtile as [32 complex n][128 m]
             // (each warp writes 32 consecutive words per column: no bank conflict), then one TMA box
@@ -935,6 +942,8 @@ __global__ void __launch_bounds__((kAMode == 1 || kAMode == 4) ? kThreadsGather 
                 tma_store_2d(&ps.maps[v], sbuf, (int)(2 * nc), (int)gm);
             } else if (BN < 64 && epi_stg == 5) {
               tma_store_2d(&tmC, sbuf, 0, m0 / (64 / BN));  // [rows / (64 / BN)][64 fp16] map
+            } else if (BN == 64 && epi_stg == 6) {
+              tma_store_2d(&tmC, sbuf, (int)(2 * (ga.m_base + (uint64_t)m0)), 0);  // C^T map, box {256 m, 16 n}
             } else if (epi_stg == 4) {
               // box {128 m (inner, global row), 32 complex n} of the C^T map
               tma_store_2d(&tmC, sbuf, (int)(ga.m_base + (uint64_t)m0), (n0 + sub) >> 1);
@@ -1255,6 +1264,10 @@ static void launch_bn(__half* c, const __half* a, const __half* bp, uint64_t M, 
   const uint64_t chunk = std::min<uint64_t>(1ull << 30, ((1ull << 31) / num_n) * tc::BM);
   // packed narrow rows (epilogue mode 5): a row-major output whose rows are 32 or 64 bytes is staged
   // and TMA-stored as rows of 128 B (64 / BN output rows each)
+  // row-folded GEMM (f = 2, 16 complex columns per output row) whose output is transposed C^T
+  // (epilogue mode 6): the caller marks it with OutMap::fold_t = 2; M, N2_real are the folded shape
+  const bool fold_t = om && om->fold_t == 2 && BN == 64 && N2_real == 64 && !bs && M % tc::BM == 0;
+  if (om && om->fold_t && !fold_t) throw TnError{TN_E_INVALID, "folded transposed output: unsupported geometry"};
   static const bool no_pack = getenv("TN_NO_PACK") != nullptr;  // A/B knob
   const bool packed = BN < 64 && !no_pack && !sa.on && !bs && epi_stg == 0 && !transposed && (!om || om->identity) &&
                       N2_real == (uint32_t)BN && M % tc::BM == 0;
@@ -1286,7 +1299,8 @@ static void launch_bn(__half* c, const __half* a, const __half* bp, uint64_t M, 
     CUtensorMap ma = np ? make_map_nd(a, *np)
                         : make_map_2d(kPlainA ? a + m_off * K2 : a, K2, kPlainA ? mm : tc::BM, KB, tc::BM);
     gargs.m_base = m_off;
-    CUtensorMap mc = transposed ? make_map_t(c, M, N2_real / 2)
+    CUtensorMap mc = fold_t     ? make_map_t(c, 2 * M, 16, 2 * tc::BM)
+                     : transposed ? make_map_t(c, M, N2_real / 2)
                      : packed   ? make_map_2d(c + m_off * N2, 64, mm * N2 / 64, 64, tc::BM * BN / 64)
                                 : make_map_2d(c + m_off * N2, N2, mm, 64, epi_stg == 3 ? 32 : tc::BM);
     // scatter: base of this chunk's rows in the OutMap; row-major: the chunk's first row (STG epilogue)
@@ -1298,7 +1312,7 @@ static void launch_bn(__half* c, const __half* a, const __half* bp, uint64_t M, 
     g_last_kern = "tc1";
     tc::gemm_chalf_tc_kernel<BN, KB, G><<<grid, (G == 1 || G == 4) ? tc::kThreadsGather : tc::kThreads, C::kSmem, s>>>(
         ma, mb, mc, num_m, num_n, (int)K2, in_max, b_bound, out_max, m_off ? nullptr : exp_slot, sa, out_sc, mm,
-        n_cols, gargs, nda, transposed ? 4 : (packed ? 5 : epi_stg), BatchArgs{}, ps);
+        n_cols, gargs, nda, fold_t ? 6 : (transposed ? 4 : (packed ? 5 : epi_stg)), BatchArgs{}, ps);
     TN_CUDA(cudaGetLastError());
   }
 }

@@ -867,8 +867,9 @@ static Plan* load_plan_fixed(const char* json, size_t len, const tn_config* cfg_
     st.b_tmp_off = off;
     off += align_up(8 * kn, 1024) * nb;
     st.fold = 1;
-    if (cfg.dtype == TN_CHALF && !fold_off && !st.gather_a && !st.mn && st.out_identity && !st.split && !st.sparse &&
-        st.klog >= 1 && st.klog <= 4) {
+    // (a transposed output only for f = 2 and N = 16: the folded tile is then one C^T box {256 m, 16 n})
+    if (cfg.dtype == TN_CHALF && !fold_off && !st.gather_a && !st.mn && !st.split && !st.sparse &&
+        st.klog >= 1 && st.klog <= 4 && (st.out_identity || (st.out_transposed && st.klog == 4 && st.nlog == 4))) {
       int fl = 0;
       while ((4 << (st.klog + fl)) < 128) ++fl;  // rows of 2K fp16 -> 128 bytes
       if (st.mlog - fl >= 8) {

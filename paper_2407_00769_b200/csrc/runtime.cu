@@ -939,6 +939,7 @@ void run_gemm_once(Plan& p, const StemStep& st, size_t i, const void* src, void*
       // row folding: [M/f][f 2K] x blockdiag(B_P) -> [M/f][f 2N], the same row-major bytes
       OutMap fo = identity_map(M / st.fold, (uint32_t)st.fold * N);
       fo.peer = nullptr;
+      fo.fold_t = st.out_transposed ? st.fold : 0;  // (f = 2, N = 16: epilogue mode 6)
       launch_gemm_chalf_tc(reinterpret_cast<__half*>(dst), reinterpret_cast<const __half*>(src),
                            reinterpret_cast<const __half*>(W + st.b_off), M / st.fold, st.fold * 2 * K,
                            st.fold * 2 * N, in_max, &sc.b_bound[i], out_max, exp_slot, &fo, s, nullptr);
