@@ -1110,7 +1110,7 @@ static CUtensorMap make_map_nd(const void* base, const NdPlan& np) {
 bool tc2_enabled();
 void launch_tc2(int BN, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, uint32_t num_mp,
                 uint32_t num_n, int K2, const float* in_max, const float* b_bound, uint32_t* out_max, int* exp_slot,
-                int epi, uint64_t m_base, const PeerStore& ps, const NdArgs& nda, cudaStream_t s);
+                int epi, uint64_t m_base, const PeerStore& ps, const NdArgs& nda, cudaStream_t s, int a_inter = 0);
 
 template <int BN, int KB, int G>
 static void launch_bn(__half* c, const __half* a, const __half* bp, uint64_t M, uint32_t K2, uint32_t N2_real,
@@ -1273,12 +1273,15 @@ static void launch_bn(__half* c, const __half* a, const __half* bp, uint64_t M, 
                       N2_real == (uint32_t)BN && M % tc::BM == 0;
   const PeerStore ps = make_peer_store(om ? om->peer : nullptr, !sa.on && epi_stg == 0 && (transposed || (om && om->identity)),
                                        transposed, M, N2_real, tc::BM, packed ? 64 / BN : 1);
-  if constexpr (G == 0 && KB == 64 && BN >= 128) {
+  if constexpr ((G == 0 || G == 2) && KB == 64 && BN >= 128) {
     // plain A, row-major or transposed output, whole 256-row pair tiles: the CTA-pair kernel (half
     // the B tile staged per SM: fewer shared-memory bytes per MAC on the compute-bound steps)
     // (also the gathered steps whose permutation is one N-d TMA box of 128-byte swizzled rows: the
     // producer computes the box coordinates from the global row, the stage image is the same)
-    const bool nd_ok = !np || (np->nd > 0 && !np->interleaved && np->KB == 64);
+    // (G = 2: the N-d box lands in the no-swizzle core-matrix layout; TN_TC2_INTER=0 keeps it on tc1)
+    static const bool inter_ok = !getenv("TN_TC2_INTER") || atoi(getenv("TN_TC2_INTER")) != 0;
+    const bool nd_ok = G == 2 ? (inter_ok && np && np->nd > 0 && np->interleaved && np->KB == 64)
+                              : (!np || (np->nd > 0 && !np->interleaved && np->KB == 64));
     if (nd_ok && !sa.on && epi_stg == 0 && M % 256 == 0 && N2_real % BN == 0 && chunk % 256 == 0 && tc2_enabled()) {
       CUtensorMap mb2 = make_map_2d(bp, K2, N2_real, KB, BN / 2);
       for (uint64_t m_off = 0; m_off < M; m_off += chunk) {
@@ -1286,7 +1289,7 @@ static void launch_bn(__half* c, const __half* a, const __half* bp, uint64_t M, 
         CUtensorMap ma = np ? make_map_nd(a, *np) : make_map_2d(a + m_off * K2, K2, mm, KB, tc::BM);
         CUtensorMap mc = transposed ? make_map_t(c, M, N2_real / 2) : make_map_2d(c + m_off * N2, N2, mm, 64, tc::BM);
         launch_tc2(BN, ma, mb2, mc, (uint32_t)(mm / 256), num_n, (int)K2, in_max, b_bound, out_max,
-                   m_off ? nullptr : exp_slot, transposed ? 4 : 0, m_off, ps, nda, s);
+                   m_off ? nullptr : exp_slot, transposed ? 4 : 0, m_off, ps, nda, s, G == 2 ? 1 : 0);
       }
       return;
     }

@@ -208,7 +208,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                           const float* in_max, const float* b_bound, uint32_t* out_max, int* exp_slot, int epi,
                           uint64_t m_base, int order, const __grid_constant__ PeerStore ps,
                           const __grid_constant__ NdArgs nda, int mn_ma, const __grid_constant__ RowPerm rp,
-                          int l2_hints) {
+                          int l2_hints, int a_inter) {
   // complex rows per CTA tile, per pair tile
   constexpr int kRows = kMN ? BM / 2 : BM;
   using C = Cfg2<BN>;
@@ -318,6 +318,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int kk = 0; kk < KB / 16; ++kk)
               mma_f16_pair(tmem_d, ad + 128 * kk, bd + 2 * kk, C::kIdescMN, (kb | kk) != 0);
+          } else if (a_inter) {
+            // A landed by the N-d box in the no-swizzle core-matrix layout (gathered steps whose two
+            // innermost stored modes are the only contracted modes there): 16 k = two 2048-byte
+            // columns of core matrices (>>4 => +256)
+            const uint64_t ad = smem_desc_interleaved(sA + s * C::kABytes);
+#pragma unroll
+            for (int kk = 0; kk < KB / 16; ++kk)
+              mma_f16_pair(tmem_d, ad + 256 * kk, bd + 2 * kk, C::kIdesc, (kb | kk) != 0);
           } else {
             const uint64_t ad = smem_desc_sw<KB>(sA + s * C::kABytes);
 #pragma unroll

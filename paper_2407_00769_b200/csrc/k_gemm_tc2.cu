@@ -13,7 +13,7 @@ template <int BN, bool kMN>
 static void launch_tc2_t(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, uint32_t num_mp,
                          uint32_t num_n, int K2, const float* in_max, const float* b_bound, uint32_t* out_max,
                          int* exp_slot, int epi, uint64_t m_base, const PeerStore& ps, const NdArgs& nda,
-                         int mn_ma, const tc2::RowPerm& rp, cudaStream_t s) {
+                         int mn_ma, const tc2::RowPerm& rp, cudaStream_t s, int a_inter = 0) {
   using C = tc2::Cfg2<BN>;
   // per device: the shared-memory opt-in and how many CTA pairs can be resident at once (an odd SM
   // count per GPC leaves SMs without a partner, so this can be below #SMs / 2)
@@ -58,19 +58,19 @@ static void launch_tc2_t(const CUtensorMap& ma, const CUtensorMap& mb, const CUt
   // share an m pair re-read its A rows from L2), M = 2^21 K = 2^9 N = 2^10 8.5 vs 6.3 ms — so off
   static const int hints_env = getenv("TN_L2_HINTS") ? atoi(getenv("TN_L2_HINTS")) : 0;
   tc2::gemm_chalf_tc2_kernel<BN, kMN><<<grid, tc::kThreads, C::kSmem, s>>>(ma, mb, mc, num_mp, num_n, K2, in_max, b_bound,
-                                                                      out_max, exp_slot, epi, m_base, order, ps, nda, mn_ma, rp, hints_env);
+                                                                      out_max, exp_slot, epi, m_base, order, ps, nda, mn_ma, rp, hints_env, a_inter);
   TN_CUDA(cudaGetLastError());
 }
 
 void launch_tc2(int BN, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, uint32_t num_mp,
                 uint32_t num_n, int K2, const float* in_max, const float* b_bound, uint32_t* out_max, int* exp_slot,
-                int epi, uint64_t m_base, const PeerStore& ps, const NdArgs& nda, cudaStream_t s) {
+                int epi, uint64_t m_base, const PeerStore& ps, const NdArgs& nda, cudaStream_t s, int a_inter) {
   if (BN == 256)
     launch_tc2_t<256, false>(ma, mb, mc, num_mp, num_n, K2, in_max, b_bound, out_max, exp_slot, epi, m_base, ps, nda,
-                             0, tc2::RowPerm{}, s);
+                             0, tc2::RowPerm{}, s, a_inter);
   else if (BN == 128)
     launch_tc2_t<128, false>(ma, mb, mc, num_mp, num_n, K2, in_max, b_bound, out_max, exp_slot, epi, m_base, ps, nda,
-                             0, tc2::RowPerm{}, s);
+                             0, tc2::RowPerm{}, s, a_inter);
   else
     throw TnError{TN_E_INVALID, "CTA-pair GEMM: BN must be 128 or 256"};
 }
