@@ -1282,7 +1282,12 @@ static void launch_bn(__half* c, const __half* a, const __half* bp, uint64_t M, 
     static const bool inter_ok = !getenv("TN_TC2_INTER") || atoi(getenv("TN_TC2_INTER")) != 0;
     const bool nd_ok = G == 2 ? (inter_ok && np && np->nd > 0 && np->interleaved && np->KB == 64)
                               : (!np || (np->nd > 0 && !np->interleaved && np->KB == 64));
-    if (nd_ok && !sa.on && epi_stg == 0 && M % 256 == 0 && N2_real % BN == 0 && chunk % 256 == 0 && tc2_enabled()) {
+    // (a row-major output with BN = 128 and K <= 64 complex stays single-CTA: mubench M = 2^25, k5 n6
+    // 2.16 vs 2.95 ms, k6 n6 2.60 vs 3.38 ms; from BN = 256 or K >= 128 the pair kernel is equal or
+    // faster; transposed outputs: C3 step 29, m26 k5 n6, no better on the single-CTA kernel)
+    const bool pair_wins = BN >= 256 || K2 >= 256 || transposed;
+    if (nd_ok && pair_wins && !sa.on && epi_stg == 0 && M % 256 == 0 && N2_real % BN == 0 && chunk % 256 == 0 &&
+        tc2_enabled()) {
       CUtensorMap mb2 = make_map_2d(bp, K2, N2_real, KB, BN / 2);
       for (uint64_t m_off = 0; m_off < M; m_off += chunk) {
         const uint64_t mm = std::min<uint64_t>(chunk, M - m_off);

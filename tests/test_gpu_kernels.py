@@ -85,7 +85,7 @@ def _half_pairs(z):
                                    (3000, 8, 2), (129, 4, 256), (4100, 16, 256),
                                    # CTA-pair kernel (M % 256 == 0, 2N >= 128, 2K >= 64): single k block,
                                    # BN = 128 and 256, more pair tiles than resident pairs
-                                   (512, 32, 64), (256, 64, 128), (1536, 32, 512), (65536, 64, 128),
+                                   (512, 32, 64), (256, 64, 128), (1536, 32, 512), (65536, 64, 128), (2048, 128, 64),
                                    (16384, 256, 256),
                                    # packed narrow rows (2N = 16 / 32 fp16 per row stored as 128-byte rows)
                                    (4096, 16, 16), (1024, 32, 8), (128, 4, 16)])
