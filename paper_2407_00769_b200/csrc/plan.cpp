@@ -41,6 +41,50 @@ static std::vector<int> int_list(const tnjson::Value* v, const char* what) {
 
 static Plan* load_plan_fixed(const char* json, size_t len, const tn_config* cfg_in, int world, int split_min = -1);
 
+// Steps the MN-major fold may not take in this lowering (load_plan_mn's search)
+static thread_local const std::set<int>* g_mn_forbid = nullptr;
+
+// The MN-major fold keeps a step's kept modes in stored order, which changes every later layout: a
+// fold can cost more passes downstream than it saves.  The lowering is repeated with folds
+// forbidden (each folded step of an explored lowering, depth first, <= 24 lowerings of ~10 ms) and
+// the one with the fewest permutation-pass bytes is kept (first found on ties).  On C3 the ranking
+// of four variants by pass bytes (73.6 / 86.4 / 90.7 / 103 GB) matched their measured subtask times
+// (257.5 / 263.7 / 267.8 / 275.3 ms, 3 interleaved reps).  TN_MN_SEARCH=0: the greedy lowering.
+static Plan* load_plan_mn(const char* json, size_t len, const tn_config* cfg, int world, int split_min) {
+  std::set<int> forbid;
+  g_mn_forbid = &forbid;
+  struct Reset {
+    ~Reset() { g_mn_forbid = nullptr; }
+  } reset;
+  std::unique_ptr<Plan> best(load_plan_fixed(json, len, cfg, world, split_min));
+  static const bool off = getenv("TN_MN_SEARCH") && atoi(getenv("TN_MN_SEARCH")) == 0;
+  auto taken = [](const Plan& p) {
+    std::set<int> t;
+    for (size_t i = 0; i < p.steps.size(); ++i)
+      if (p.steps[i].mn) t.insert((int)i);
+    return t;
+  };
+  if (off) return best.release();
+  std::vector<std::pair<std::set<int>, std::set<int>>> stack{{forbid, taken(*best)}};
+  std::set<std::set<int>> seen{forbid};
+  int evals = 1;
+  while (!stack.empty() && evals < 24) {
+    const auto top = stack.back();
+    stack.pop_back();
+    for (int t : top.second) {
+      std::set<int> f2 = top.first;
+      f2.insert(t);
+      if (!seen.insert(f2).second || evals >= 24) continue;
+      forbid = f2;
+      std::unique_ptr<Plan> q(load_plan_fixed(json, len, cfg, world, split_min));
+      ++evals;
+      stack.push_back({f2, taken(*q)});
+      if (q->perm_bytes < best->perm_bytes) best = std::move(q);
+    }
+  }
+  return best.release();
+}
+
 // A split tail on a sharded stem must start after the last mode swap (each rank chunks its own
 // shard; a swap would need every chunk of every rank).  The swap schedule does not depend on where
 // the tail starts, so a lowering whose tail would contain a swap is redone with the tail starting
@@ -49,7 +93,7 @@ static Plan* load_plan_split(const char* json, size_t len, const tn_config* cfg,
   int split_min = -1;
   for (int pass = 0; pass < 64; ++pass) {
     try {
-      return load_plan_fixed(json, len, cfg, world, split_min);
+      return load_plan_mn(json, len, cfg, world, split_min);
     } catch (const TnError& e) {
       const std::string key = "split-retry:";
       if (e.msg.compare(0, key.size(), key) != 0) throw;
@@ -575,6 +619,13 @@ static Plan* load_plan_fixed(const char* json, size_t len, const tn_config* cfg_
           bool block = ma >= 7 && kl >= 6 && nl >= 6 && (int)kept.size() >= 8 && (int)L.size() >= mn_min;
           for (int q = 0; block && q < kl; ++q) block = bs.count(L[L.size() - 1 - ma - q]) > 0;
           static const bool mn_off = getenv("TN_NO_MN") != nullptr;  // A/B knob
+          // TN_MN_STEPS="i,j,..." (experiment knob): only these step indices may take the fold
+          static const char* mn_steps = getenv("TN_MN_STEPS");
+          if (mn_steps) {
+            const std::string lst = std::string(",") + mn_steps + ",";
+            block = block && lst.find("," + std::to_string(s) + ",") != std::string::npos;
+          }
+          if (g_mn_forbid && g_mn_forbid->count((int)s)) block = false;
           if (block && !mn_off && !fusable && cfg.dtype == TN_CHALF && !st.sparse && tc_k && !cfg.no_gather &&
               (split_set.empty() || (int)s < p.split_from)) {
             st.mn = true;
