@@ -174,6 +174,7 @@ struct AGather {
 void launch_gemm_chalf_tc(__half* c, const __half* a, const __half* bp, uint64_t M, uint32_t K2,
                           uint32_t N2, const float* in_max, const float* b_bound, uint32_t* out_max,
                           int* exp_slot, const OutMap* om, cudaStream_t s, const AGather* ag = nullptr);
+int gather_mode_of(const AGather& ag);  // k_gemm_tc.cu: the gathered-A path (plan.cpp cost model)
 // MN-major A (k_gemm_tc2.cu): A stored [M >> ma][K][2^ma] complex-half (2^ma kept rows innermost),
 // bpm = B' [2N][K] (launch_pad_b_mn); no permutation pass.
 bool mn_gemm_supported(uint64_t M, uint32_t K, uint32_t N, int ma, const OutMap* om);

@@ -342,6 +342,28 @@ static bool build_raw(const AGather& ag, NdPlan& out) {
 }
 
 
+// The A-operand path a gathered step will take (the same choice as launch_gemm_chalf_tc, without the
+// A/B knobs): 0 direct N-d box (rows >= 128 B), 2 core-matrix box, 3 raw box + reshuffle, 1 cp.async
+// 16-byte pieces, 4 cp.async 4-byte pieces.  For the lowering's cost model (plan.cpp).
+int gather_mode_of(const AGather& ag) {
+  if (ag.ks[0] != 1 || ag.ks[1] != 2) return 4;
+  NdPlan np, rp;
+  const bool direct = build_nd(ag, np), raw = build_raw(ag, rp);
+  const bool wide = direct && (int)(np.box[0] * 4) >= 128;
+  if (direct && (wide || !raw)) return np.interleaved ? 2 : 0;
+  return raw ? 3 : 1;
+}
+
+int gather_mode_of_strides(int mlog, int klog, const int64_t* ms, const int64_t* ks) {
+  AGather ag;
+  memset(&ag, 0, sizeof(ag));
+  ag.mlog = mlog;
+  ag.klog = klog;
+  for (int j = 0; j < mlog && j < kMaxModes; ++j) ag.ms[j] = ms[j];
+  for (int j = 0; j < klog && j < 24; ++j) ag.ks[j] = ks[j];
+  return gather_mode_of(ag);
+}
+
 void launch_gemm_chalf_tc(__half* c, const __half* a, const __half* bp, uint64_t M, uint32_t K2, uint32_t N2,
                           const float* in_max, const float* b_bound, uint32_t* out_max, int* exp_slot,
                           const OutMap* om, cudaStream_t s, const AGather* ag) {

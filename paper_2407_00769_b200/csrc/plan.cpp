@@ -41,8 +41,24 @@ static std::vector<int> int_list(const tnjson::Value* v, const char* what) {
 
 static Plan* load_plan_fixed(const char* json, size_t len, const tn_config* cfg_in, int world, int split_min = -1);
 
-// Steps the MN-major fold may not take in this lowering (load_plan_mn's search)
+// Steps the MN-major fold may not take in this lowering (load_plan_mn's search), and steps whose
+// layout-policy-3 output choice (row-major vs transposed) is inverted (its hill climb)
 static thread_local const std::set<int>* g_mn_forbid = nullptr;
+static thread_local const std::set<int>* g_tr_flip = nullptr;
+
+// Lowering cost for the searches: bytes of permutation passes plus the extra cost of the gathered A
+// loads, as A bytes times a per-path factor measured against a plain read (raw box + reshuffle
+// ~0.3, cp.async 16-byte pieces ~1, 4-byte pieces ~3: tools/gather_bench.py)
+static double plan_cost(const Plan& p) {
+  double c = p.perm_bytes;
+  for (const StemStep& st : p.steps) {
+    if (!st.gather_a || st.a_m_stride.empty()) continue;
+    const int mode = gather_mode_of_strides(st.mlog, st.klog, st.a_m_stride.data(), st.a_k_stride.data());
+    const double f = mode == 3 ? 0.3 : mode == 1 ? 1.0 : mode == 4 ? 3.0 : 0.0;
+    c += f * 4.0 * std::ldexp(1.0, st.mlog + st.klog);
+  }
+  return c;
+}
 
 // The MN-major fold keeps a step's kept modes in stored order, which changes every later layout: a
 // fold can cost more passes downstream than it saves.  The lowering is repeated with folds
@@ -79,8 +95,45 @@ static Plan* load_plan_mn(const char* json, size_t len, const tn_config* cfg, in
       std::unique_ptr<Plan> q(load_plan_fixed(json, len, cfg, world, split_min));
       ++evals;
       stack.push_back({f2, taken(*q)});
-      if (q->perm_bytes < best->perm_bytes) best = std::move(q);
+      if (plan_cost(*q) < plan_cost(*best)) best = std::move(q);
     }
+  }
+  // then (TN_TR_SEARCH=1, opt-in) a hill climb over the transposed-output choices with the chosen folds
+  // fixed: invert one choice at a time, keep it when the cost drops.  It lowers the modelled cost
+  // (C3: 4 GPUs 24.7 vs 28.1 GB of passes) but measured no faster (1 GPU 248.8 vs 244.6 ms, 4 GPUs
+  // 80.6 vs 80.6 ms, 3 interleaved reps each) for ~0.5 s more per plan load, hence off
+  static const bool tr_off = !getenv("TN_TR_SEARCH") || atoi(getenv("TN_TR_SEARCH")) == 0;
+  if (tr_off) return best.release();
+  std::set<int> mn_taken = taken(*best), f_best;
+  forbid.clear();
+  for (size_t i = 0; i < best->steps.size(); ++i)
+    if (!mn_taken.count((int)i)) forbid.insert((int)i);  // the same folds as the best plan
+  std::set<int> flips;
+  g_tr_flip = &flips;
+  struct ResetTr {
+    ~ResetTr() { g_tr_flip = nullptr; }
+  } reset_tr;
+  double c_best = plan_cost(*best);
+  for (int pass = 0; pass < 2; ++pass) {
+    bool improved = false;
+    std::vector<int> pts;
+    for (size_t i = 0; i < best->steps.size(); ++i)
+      if (best->steps[i].tr_choice) pts.push_back((int)i);
+    for (int s : pts) {
+      std::set<int> f2 = flips;
+      if (!f2.insert(s).second) f2.erase(s);
+      flips = f2;
+      std::unique_ptr<Plan> q(load_plan_fixed(json, len, cfg, world, split_min));
+      const double c = plan_cost(*q);
+      if (c < c_best && taken(*q) == mn_taken) {
+        best = std::move(q);
+        c_best = c;
+        improved = true;
+      } else {
+        if (!f2.count(s)) flips.insert(s); else flips.erase(s);  // undo
+      }
+    }
+    if (!improved) break;
   }
   return best.release();
 }
@@ -716,7 +769,12 @@ static Plan* load_plan_fixed(const char* json, size_t len, const tn_config* cfg_
           std::vector<int> tr = newl;
           tr.insert(tr.end(), kout.begin(), kout.end());
           const int hid = inner_hits(out), htr = inner_hits(tr);
-          if (htr > hid && (htr == (int)Rn.size() || htr >= 2) && kept.size() >= 5) out = tr;
+          bool want = htr > hid && (htr == (int)Rn.size() || htr >= 2) && kept.size() >= 5;
+          if (kept.size() >= 5) {
+            st.tr_choice = true;
+            if (g_tr_flip && g_tr_flip->count((int)s)) want = !want;
+          }
+          if (want) out = tr;
         }
       }
       st.R = R;

@@ -33,6 +33,10 @@ struct Node {
 };
 
 // One stem step: [optional permutation] + GEMM  C[kept, new] = A[kept, R] * B[R, new].
+// k_gemm_tc.cu: the A-operand path of a gathered step (0 direct box, 2 core-matrix box, 3 raw box,
+// 1 cp.async 16 B, 4 cp.async 4 B), for the lowering's cost model
+int gather_mode_of_strides(int mlog, int klog, const int64_t* ms, const int64_t* ks);
+
 struct StemStep {
   int node = -1;                  // tree node produced by this step
   int branch = -1;                // the non-stem operand (common node or leaf)
@@ -57,6 +61,7 @@ struct StemStep {
   // row folding (plain A, row-major output, 2K x 2 B < 128 B): the tcgen05 GEMM runs on [M/f][f 2K] x
   // blockdiag(B_P x f) -> [M/f][f 2N], the same bytes read as rows of 128 B (the TMA engine's
   // per-row cost made 64-byte rows its limit); B' at b_off, B_P scratch at b_off + b_fold_bytes
+  bool tr_choice = false;         // layout policy 3 weighed a transposed output here (search point)
   int fold = 1;
   uint64_t b_fold_bytes = 0;
   // output address of C[m, n] = sum_j bit_j(m) m_stride[j] + sum_j bit_j(n) n_stride[j] (elements)
