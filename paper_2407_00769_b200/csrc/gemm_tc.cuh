@@ -1273,7 +1273,7 @@ static void launch_bn(__half* c, const __half* a, const __half* bp, uint64_t M, 
                       N2_real == (uint32_t)BN && M % tc::BM == 0;
   const PeerStore ps = make_peer_store(om ? om->peer : nullptr, !sa.on && epi_stg == 0 && (transposed || (om && om->identity)),
                                        transposed, M, N2_real, tc::BM, packed ? 64 / BN : 1);
-  if constexpr ((G == 0 || G == 2) && KB == 64 && BN >= 128) {
+  if constexpr ((G == 0 || G == 2) && KB == 64 && BN >= 64) {
     // plain A, row-major or transposed output, whole 256-row pair tiles: the CTA-pair kernel (half
     // the B tile staged per SM: fewer shared-memory bytes per MAC on the compute-bound steps)
     // (also the gathered steps whose permutation is one N-d TMA box of 128-byte swizzled rows: the
@@ -1285,7 +1285,8 @@ static void launch_bn(__half* c, const __half* a, const __half* bp, uint64_t M, 
     // (a row-major output with BN = 128 and K <= 64 complex stays single-CTA: mubench M = 2^25, k5 n6
     // 2.16 vs 2.95 ms, k6 n6 2.60 vs 3.38 ms; from BN = 256 or K >= 128 the pair kernel is equal or
     // faster; transposed outputs: C3 step 29, m26 k5 n6, no better on the single-CTA kernel)
-    const bool pair_wins = BN >= 256 || K2 >= 256 || transposed;
+    // (BN = 64: only K-heavy steps, K >= 128 complex, e.g. C3 step 31 m16 k16 n5)
+    const bool pair_wins = BN >= 128 ? (BN >= 256 || K2 >= 256 || transposed) : K2 >= 256;
     if (nd_ok && pair_wins && !sa.on && epi_stg == 0 && M % 256 == 0 && N2_real % BN == 0 && chunk % 256 == 0 &&
         tc2_enabled()) {
       CUtensorMap mb2 = make_map_2d(bp, K2, N2_real, KB, BN / 2);

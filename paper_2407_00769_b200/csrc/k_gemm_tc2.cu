@@ -71,8 +71,11 @@ void launch_tc2(int BN, const CUtensorMap& ma, const CUtensorMap& mb, const CUte
   else if (BN == 128)
     launch_tc2_t<128, false>(ma, mb, mc, num_mp, num_n, K2, in_max, b_bound, out_max, exp_slot, epi, m_base, ps, nda,
                              0, tc2::RowPerm{}, s, a_inter);
+  else if (BN == 64)
+    launch_tc2_t<64, false>(ma, mb, mc, num_mp, num_n, K2, in_max, b_bound, out_max, exp_slot, epi, m_base, ps, nda,
+                            0, tc2::RowPerm{}, s, a_inter);
   else
-    throw TnError{TN_E_INVALID, "CTA-pair GEMM: BN must be 128 or 256"};
+    throw TnError{TN_E_INVALID, "CTA-pair GEMM: BN must be 64, 128 or 256"};
 }
 
 // MN-major A (gemm_tc2.cuh, kMN): the stem stored as [M >> ma][K][2^ma] complex (the step's kept

@@ -86,6 +86,7 @@ def _half_pairs(z):
                                    # CTA-pair kernel (M % 256 == 0, 2N >= 128, 2K >= 64): single k block,
                                    # BN = 128 and 256, more pair tiles than resident pairs
                                    (512, 32, 64), (256, 64, 128), (1536, 32, 512), (65536, 64, 128), (2048, 128, 64),
+                                   (1024, 128, 32), (4096, 512, 32),
                                    (16384, 256, 256),
                                    # packed narrow rows (2N = 16 / 32 fp16 per row stored as 128-byte rows)
                                    (4096, 16, 16), (1024, 32, 8), (128, 4, 16)])
@@ -421,7 +422,7 @@ def test_gemm_chalf_gathered_word_pieces_exact(env, runs, N):
                                     # 6 source runs: adjacent m / k runs outside the box share a TMA dim
                                     ("k5m8k3m2k2m3", 32), ("k5m9k2m1k3m2", 128),
                                     # two contracted modes innermost (core-matrix box) on the CTA-pair kernel
-                                    ("k2m8k5m5", 128), ("k2m9k4m3", 256)])
+                                    ("k2m8k5m5", 128), ("k2m9k4m3", 256), ("k5m9k2m1k3m2", 32)])
 def test_gemm_chalf_gathered_runs_exact(env, runs, N):
     """Stem layouts as they occur on the C3 path (runs of contracted k / kept m modes, innermost
     first, kept modes in stored order): these go through the N-dimensional TMA box (swizzled rows
