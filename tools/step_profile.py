@@ -42,9 +42,9 @@ def main():
         pms = [x["ms"][1 + 2 * i] for x in runs]
         gms = [x["ms"][2 + 2 * i] for x in runs]
         pm, gm = statistics.median(pms), statistics.median(gms)
-        key = ("tc" if s["tc"] else "simt")
+        key = s.get("kern") or ("tc" if s["tc"] else "simt")
         tot[key] = tot.get(key, 0) + gm
-        print(f"{i:3d} m{s['m']:2d} k{s['k']:2d} n{s['n']:2d} {key:4s} ga{s['ga']} perm {pm:7.3f} gemm {gm:7.3f} ms "
+        print(f"{i:3d} m{s['m']:2d} k{s['k']:2d} n{s['n']:2d} {key:6s} ga{s['ga']} perm {pm:7.3f} gemm {gm:7.3f} ms "
               f"[{min(gms):7.3f} {max(gms):7.3f}] {by / gm / 1e6 if gm > 0 else 0:5.0f} GB/s "
               f"{fl / gm / 1e9 if gm > 0 else 0:6.0f} TF/s  in {4*M*K/2**30:.2f} GiB out {4*M*N/2**30:.2f} GiB")
     perm_tot = sum(statistics.median(x["ms"][1 + 2 * i] for x in runs) for i in range(len(r["steps"])))
