@@ -422,7 +422,9 @@ def test_gemm_chalf_gathered_word_pieces_exact(env, runs, N):
                                     # 6 source runs: adjacent m / k runs outside the box share a TMA dim
                                     ("k5m8k3m2k2m3", 32), ("k5m9k2m1k3m2", 128),
                                     # two contracted modes innermost (core-matrix box) on the CTA-pair kernel
-                                    ("k2m8k5m5", 128), ("k2m9k4m3", 256), ("k5m9k2m1k3m2", 32)])
+                                    ("k2m8k5m5", 128), ("k2m9k4m3", 256), ("k5m9k2m1k3m2", 32),
+                                    # short direct rows: raw box + reshuffle on the CTA-pair kernel
+                                    ("k4m8k4m4", 128), ("k3m1k6m9", 128), ("k3m1k3m10", 64)])
 def test_gemm_chalf_gathered_runs_exact(env, runs, N):
     """Stem layouts as they occur on the C3 path (runs of contracted k / kept m modes, innermost
     first, kept modes in stored order): these go through the N-dimensional TMA box (swizzled rows
