@@ -112,6 +112,11 @@ extern thread_local const char* g_last_kern;
 struct PeerChunks {
   uint64_t chunk_bytes;
   void* base[8];
+  // bit routing (nsw > 0, replaces the chunk routing): output element O goes to member v whose bit
+  // vbit[t] is O's bit pos[t] (bit positions in elem_bytes units, from the innermost); that bit is
+  // replaced by mebit[t] and the element lands at base[v] + O' (base = the start of the buffer)
+  int nsw;
+  int pos[3], vbit[3], mebit[3];
 };
 void launch_permute(void* dst, const void* src, int elem_bytes, int n, const int* perm, cudaStream_t s,
                     const PeerChunks* pc = nullptr);

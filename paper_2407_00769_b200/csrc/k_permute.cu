@@ -35,14 +35,25 @@ struct PermArgs2 {
 
 // Output routed to the swap members (mode swap through NVLink peer memory, runtime.cu mode_swap):
 // output element O (in T units) goes to base[O >> shift] + (O & (2^shift - 1)).
+// Bit routing (nsw > 0, the swap pass composed with the next step's permutation): member v's bit
+// vbit[t] is O's bit pos[t], which is replaced by mebit[t] (this rank's own member bit).
 struct PeerRoute {
-  int on, shift;
+  int on, shift, nsw;
+  int pos[3], vbit[3], mebit[3];
   unsigned char* base[8];
 };
 
 template <typename T>
 __device__ __forceinline__ T* route_out(T* dst, const PeerRoute& pr, int64_t o) {
   if (!pr.on) return dst + o;
+  if (pr.nsw) {
+    int v = 0;
+    for (int t = 0; t < pr.nsw; ++t) {
+      v |= (int)((o >> pr.pos[t]) & 1) << pr.vbit[t];
+      o = (o & ~(1ll << pr.pos[t])) | ((int64_t)pr.mebit[t] << pr.pos[t]);
+    }
+    return reinterpret_cast<T*>(pr.base[v]) + o;
+  }
   return reinterpret_cast<T*>(pr.base[o >> pr.shift]) + (o & ((1ll << pr.shift) - 1));
 }
 
@@ -241,11 +252,24 @@ static void launch_pipe(void* dst, const void* src, const PermArgs2& args, uint6
 // PeerRoute for element type T from the byte-level routing (chunk_bytes per member, base[v] already
 // at this rank's chunk in member v's buffer)
 template <typename T>
-static PeerRoute route_for(const PeerChunks* pc) {
+static PeerRoute route_for(const PeerChunks* pc, int elem_bytes, int vb) {
   PeerRoute r;
   memset(&r, 0, sizeof(r));
   if (!pc) return r;
   r.on = 1;
+  if (pc->nsw > 0) {
+    int f = 0;  // element bits folded into T
+    while ((elem_bytes << f) < (int)sizeof(T)) ++f;
+    r.nsw = pc->nsw;
+    for (int t = 0; t < pc->nsw; ++t) {
+      r.pos[t] = pc->pos[t] - f;
+      if (r.pos[t] < vb) throw TnError{TN_E_INVALID, "permute: a routing bit lies inside a 16-byte vector"};
+      r.vbit[t] = pc->vbit[t];
+      r.mebit[t] = pc->mebit[t];
+    }
+    for (int v = 0; v < 8; ++v) r.base[v] = static_cast<unsigned char*>(pc->base[v]);
+    return r;
+  }
   uint64_t c = pc->chunk_bytes / sizeof(T);
   while ((1ull << r.shift) < c) ++r.shift;
   for (int v = 0; v < 8; ++v) r.base[v] = static_cast<unsigned char*>(pc->base[v]);
@@ -269,7 +293,7 @@ void launch_permute(void* dst, const void* src, int elem_bytes, int n, const int
   const uint64_t total = 1ull << n;
   if (pc && (pc->chunk_bytes & (pc->chunk_bytes - 1)))
     throw TnError{TN_E_INVALID, "permute: member chunks must be powers of two"};
-  if (ident) {
+  if (ident && !(pc && pc->nsw > 0)) {
     if (!pc) {
       TN_CUDA(cudaMemcpyAsync(dst, src, total * elem_bytes, cudaMemcpyDeviceToDevice, s));
     } else {
@@ -358,9 +382,9 @@ void launch_permute(void* dst, const void* src, int elem_bytes, int n, const int
   static const bool legacy = getenv("TN_PERM_LEGACY") != nullptr;  // A/B knob for the old kernel
   if (vb == vb_full && nvec <= 4096 && !legacy) {
     switch (eb) {
-      case 4: launch_pipe<uint32_t>(dst, src, args, n_tiles, nvec, s, route_for<uint32_t>(pc)); break;
-      case 8: launch_pipe<uint2>(dst, src, args, n_tiles, nvec, s, route_for<uint2>(pc)); break;
-      default: launch_pipe<uint4>(dst, src, args, n_tiles, nvec, s, route_for<uint4>(pc)); break;
+      case 4: launch_pipe<uint32_t>(dst, src, args, n_tiles, nvec, s, route_for<uint32_t>(pc, elem_bytes, vb)); break;
+      case 8: launch_pipe<uint2>(dst, src, args, n_tiles, nvec, s, route_for<uint2>(pc, elem_bytes, vb)); break;
+      default: launch_pipe<uint4>(dst, src, args, n_tiles, nvec, s, route_for<uint4>(pc, elem_bytes, vb)); break;
     }
     TN_CUDA(cudaGetLastError());
     return;
@@ -375,7 +399,7 @@ void launch_permute(void* dst, const void* src, int elem_bytes, int n, const int
         attr_set[0] = true;
       }
       permute_kernel<uint32_t><<<blocks, 256, smem, s>>>((uint32_t*)dst, (const uint32_t*)src, args, n_tiles,
-                                                         route_for<uint32_t>(pc));
+                                                         route_for<uint32_t>(pc, elem_bytes, vb));
       break;
     case 8:
       if (!attr_set[1]) {
@@ -383,7 +407,7 @@ void launch_permute(void* dst, const void* src, int elem_bytes, int n, const int
         attr_set[1] = true;
       }
       permute_kernel<uint2><<<blocks, 256, smem, s>>>((uint2*)dst, (const uint2*)src, args, n_tiles,
-                                                      route_for<uint2>(pc));
+                                                      route_for<uint2>(pc, elem_bytes, vb));
       break;
     default:
       if (!attr_set[2]) {
@@ -391,7 +415,7 @@ void launch_permute(void* dst, const void* src, int elem_bytes, int n, const int
         attr_set[2] = true;
       }
       permute_kernel<uint4><<<blocks, 256, smem, s>>>((uint4*)dst, (const uint4*)src, args, n_tiles,
-                                                      route_for<uint4>(pc));
+                                                      route_for<uint4>(pc, elem_bytes, vb));
       break;
   }
   TN_CUDA(cudaGetLastError());

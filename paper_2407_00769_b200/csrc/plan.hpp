@@ -142,6 +142,7 @@ struct Plan {
   double swap_bytes = 0;          // payload bytes each rank sends per slice (codec applied)
   int n_fused_swaps = 0;          // swaps of the last run done inside the previous GEMM's epilogue
   int n_peer_swaps = 0;           // other swaps of the last run moved by a peer-memory pass (no NCCL)
+  int n_composed_swaps = 0;       // of those, passes that also did the next step's permutation
   std::vector<std::string> step_kern;  // per step: GEMM kernel family of the last (eager / captured) run
   std::vector<int> step_pass;          // per step: 1 when a permutation pass ran before its GEMM
   std::vector<void*> peer_stem;   // [2 r + j]: rank r's stem buffer j as this rank addresses it

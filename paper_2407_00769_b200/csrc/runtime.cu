@@ -752,6 +752,59 @@ bool peer_swap_enabled(const Plan& p) {
   return fused_swap_enabled(p) && !(e && atoi(e) != 0) && p.peer_stem.size() == 2u * p.world;
 }
 
+// The peer-memory swap pass composed with step st's own permutation (st.perm, no MN-major read):
+// ONE pass from the sender's layout straight into the receiver's permuted layout.  The sender sees
+// the permuted layout with each swapped-out shard mode replaced by the swap_in mode at the same
+// position t (V[j] = send_layout[perm_axes[j]]); that bit picks the member (bit sx-1-t of v) and is
+// replaced by this rank's own member bit (bit sx-1-t of me), which is where the receiver keeps it.
+// Saves the receiver's separate permutation pass (a full local read + write).  Returns false (no
+// work done) when the routing bits would fall inside a 16-byte vector or TN_NO_SWAP_COMPOSE is set.
+bool mode_swap_composed(Plan& p, const StemStep& st, const tn_buffers* b, int& cur, cudaStream_t s,
+                        float* bar_slot) {
+  const char* e = getenv("TN_NO_SWAP_COMPOSE");  // A/B knob (read per call)
+  if ((e && atoi(e) != 0) || st.quant || !bar_slot || !peer_swap_enabled(p) || !st.perm || mn_active(p, st))
+    return false;
+  const int eb = p.cfg.dtype == TN_CHALF ? 4 : 8;
+  const SwapMembers sm(p, st);
+  const int n = (int)st.send_layout.size();
+  if (sm.sx < 1 || sm.sx > 3 || (int)st.perm_axes.size() != n) return false;
+  // the member bit splits the output into runs of 2^pos elements alternating between destinations:
+  // short runs make NVLink stores inefficient (C3 at 2 GPUs: pos = 2, 16-byte runs, the composed
+  // pass took 16.5 ms against 11.4 ms for swap pass + permutation pass), so compose only when runs
+  // are >= 16 KB (TN_SWAP_COMPOSE_MIN_POS overrides, for tests; >= the 16-byte vector)
+  const char* mp = getenv("TN_SWAP_COMPOSE_MIN_POS");
+  const int min_pos = std::max(eb == 4 ? 2 : 1, mp ? atoi(mp) : (eb == 4 ? 12 : 11));
+  PeerChunks pc;
+  memset(&pc, 0, sizeof(pc));
+  pc.nsw = sm.sx;
+  std::vector<int> axes(n);
+  for (int j = 0; j < n; ++j) {
+    const int q = st.perm_axes[j];
+    axes[j] = st.send_perm ? st.send_perm_axes[q] : q;
+    if (q < sm.sx) {
+      const int pos = n - 1 - j;
+      if (pos < min_pos) return false;
+      pc.pos[q] = pos;
+      pc.vbit[q] = sm.sx - 1 - q;
+      pc.mebit[q] = (sm.me >> (sm.sx - 1 - q)) & 1;
+    }
+  }
+  for (int v = 0; v < (1 << sm.sx); ++v) pc.base[v] = p.peer_stem[2 * sm.peer_of(v) + (1 - cur)];
+  if (getenv("TN_DEBUG_COMPOSE")) {
+    fprintf(stderr, "compose n=%d sx=%d pos=%d axes(outermost first):", n, sm.sx, pc.pos[0]);
+    for (int j = 0; j < n; ++j) fprintf(stderr, " %d", axes[j]);
+    fprintf(stderr, "\n");
+  }
+  xfer_allreduce_max(p, bar_slot, s);
+  launch_permute(nullptr, b->d_stem[cur], eb, n, axes.data(), s, &pc);
+  ++p.launches;
+  xfer_allreduce_max(p, bar_slot, s);
+  cur = 1 - cur;
+  ++p.n_peer_swaps;
+  ++p.n_composed_swaps;
+  return true;
+}
+
 void mode_swap(Plan& p, const StemStep& st, const tn_buffers* b, int& cur, cudaStream_t s, float* bar_slot) {
   comm_check(p);
   const int eb = p.cfg.dtype == TN_CHALF ? 4 : 8;
@@ -1031,10 +1084,13 @@ void stem_body(Plan& p, const tn_buffers* b, cudaStream_t s, bool head = true, b
   bool swapped = false;  // the swap before step i was done by step i-1's epilogue
   p.n_fused_swaps = 0;
   p.n_peer_swaps = 0;
+  p.n_composed_swaps = 0;
   for (size_t i = 0; i < n_main; ++i) {
     const StemStep& st = p.steps[i];
+    bool composed = false;  // the swap pass also did this step's permutation
     if (st.swap && !swapped) {
-      mode_swap(p, st, b, cur, s, &sc.max_slot[i]);
+      composed = mode_swap_composed(p, st, b, cur, s, &sc.max_slot[i]);
+      if (!composed) mode_swap(p, st, b, cur, s, &sc.max_slot[i]);
     }
     swapped = false;
     if (p.step_kern.size() != p.steps.size()) {
@@ -1042,7 +1098,7 @@ void stem_body(Plan& p, const tn_buffers* b, cudaStream_t s, bool head = true, b
       p.step_pass.assign(p.steps.size(), 0);
     }
     p.step_pass[i] = st.perm && !mn_active(p, st);
-    if (st.perm && !mn_active(p, st)) {
+    if (st.perm && !mn_active(p, st) && !composed) {
       launch_permute(b->d_stem[1 - cur], b->d_stem[cur], eb, (int)st.in_layout.size(), st.perm_axes.data(), s);
       ++p.launches;
       cur = 1 - cur;

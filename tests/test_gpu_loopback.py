@@ -141,12 +141,31 @@ def test_loopback_fused_swap_bit_identical(tn, c3sub, world):
     unf = run_loopback(tn, sub, world, dict(kw, no_fused_swap=1))
     # every swap as a peer-memory pass (the send permutation writing the members' chunks directly)
     os.environ["TN_NO_EPILOGUE_SWAP"] = "1"
+    os.environ["TN_SWAP_COMPOSE_MIN_POS"] = "0"  # compose whatever the run length (16-byte vectors)
     try:
         pas = run_loopback(tn, sub, world, kw)
     finally:
         del os.environ["TN_NO_EPILOGUE_SWAP"]
+        del os.environ["TN_SWAP_COMPOSE_MIN_POS"]
+    # ... and with the peer pass kept apart from the next step's own permutation pass
+    os.environ["TN_NO_EPILOGUE_SWAP"] = "1"
+    os.environ["TN_NO_SWAP_COMPOSE"] = "1"
+    try:
+        sep = run_loopback(tn, sub, world, kw)
+    finally:
+        del os.environ["TN_NO_EPILOGUE_SWAP"]
+        del os.environ["TN_NO_SWAP_COMPOSE"]
     nf = fused[0][1]["n_fused_swaps"]
-    print(f"world={world}: swaps={n_swaps(fused[0][1])} fused={nf} peer-pass={fused[0][1]['n_peer_swaps']}")
+    print(f"world={world}: swaps={n_swaps(fused[0][1])} fused={nf} peer-pass={fused[0][1]['n_peer_swaps']} "
+          f"composed={pas[0][1]['n_composed_swaps']}")
+    assert sep[0][1]["n_composed_swaps"] == 0 and sep[0][1]["n_peer_swaps"] == n_swaps(sep[0][1])
+    # a swap before a step with its own permutation pass is composed with it (unless a routing bit
+    # falls inside a 16-byte vector)
+    assert pas[0][1]["n_composed_swaps"] <= sum(1 for x in pas[0][1]["steps"] if x["swap"] and x["pass"])
+    if world == 8:
+        assert pas[0][1]["n_composed_swaps"] >= 1
+    for (a, _, _), (d, _, _) in zip(pas, sep):
+        assert np.array_equal(a, d)
     assert unf[0][1]["n_fused_swaps"] == 0 and unf[0][1]["n_peer_swaps"] == 0
     assert nf >= 1 and nf + fused[0][1]["n_peer_swaps"] == n_swaps(fused[0][1])
     assert pas[0][1]["n_fused_swaps"] == 0 and pas[0][1]["n_peer_swaps"] == n_swaps(pas[0][1])
