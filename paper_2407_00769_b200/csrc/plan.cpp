@@ -1056,6 +1056,10 @@ std::string report_json(const Plan& p, const std::vector<float>& ms) {
       << ",\"fuse_quant\":" << (s.fuse_quant ? 1 : 0)
       << ",\"out_kind\":" << (s.out_identity ? 0 : (s.out_transposed ? 1 : 2)) << ",\"mn\":" << (s.mn ? s.mn_ma : 0)
       << ",\"fold\":" << s.fold
+      << ",\"gmode\":"
+      << (s.gather_a && !s.a_m_stride.empty()
+              ? gather_mode_of_strides(s.mlog, s.klog, s.a_m_stride.data(), s.a_k_stride.data())
+              : -1)
       << ",\"kern\":\"" << (i < p.step_kern.size() ? p.step_kern[i] : std::string()) << "\""
       << ",\"pass\":" << (i < p.step_pass.size() ? p.step_pass[i] : (s.perm ? 1 : 0))
       << ",\"in\":";
@@ -1107,7 +1111,7 @@ std::string report_json(const Plan& p, const std::vector<float>& ms) {
   o << ",\"final_layout\":";
   jlist(o, p.final_layout);
   o << ",\"launches\":" << p.launches << ",\"world\":" << p.world << ",\"n_swaps\":" << p.n_swaps
-    << ",\"swap_bytes\":" << p.swap_bytes << ",\"n_fused_swaps\":" << p.n_fused_swaps << ",\"n_peer_swaps\":" << p.n_peer_swaps << ",\"final_shard\":";
+    << ",\"swap_bytes\":" << p.swap_bytes << ",\"n_fused_swaps\":" << p.n_fused_swaps << ",\"n_peer_swaps\":" << p.n_peer_swaps << ",\"n_composed_swaps\":" << p.n_composed_swaps << ",\"final_shard\":";
   jlist(o, p.final_shard);
   if (!ms.empty()) {  // [common_ms, (perm_ms, gemm_ms) per step..., final_ms]
     o << ",\"ms\":[";
