@@ -27,6 +27,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <mutex>
+#include <type_traits>
 
 #include "common.cuh"
 
@@ -808,16 +809,26 @@ __global__ void __launch_bounds__((kAMode == 1 || kAMode == 4) ? kThreadsGather 
           // complex values of this 32-column chunk that exist (N < 8 pads B_P with zero rows)
           const int nleft = (int)n_cols - ((n0 + c) >> 1);
           const int nvalid = nleft < 16 ? (nleft > 0 ? nleft : 0) : 16;
+          // (two copies of the loop: the common case — all 16 columns real, no zero block — without
+          // the per-value selects, which cost ~25 % of the epilogue's issue slots on output-heavy steps)
+          auto convert = [&](auto all_valid) {
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            float x0 = __uint_as_float(r[h][2 * j]) * sc, x1 = __uint_as_float(r[h][2 * j + 1]) * sc;
-            if (skip) x0 = x1 = 0.f;  // zero block of the padded 2-d index (TMEM was not written)
-            __half2 hv = __floats2half2_rn(x0, x1);
-            // the max of the scaled fp32 values (not of their fp16 roundings): it stays meaningful when
-            // cancellation pushes the stored values into fp16 subnormals or zero (scale re-run, redo_check)
-            if (j < nvalid) mx = fmaxf(mx, fmaxf(fabsf(x0), fabsf(x1)));
-            pk[j] = *reinterpret_cast<uint32_t*>(&hv);
-          }
+            for (int j = 0; j < 16; ++j) {
+              float x0 = __uint_as_float(r[h][2 * j]) * sc, x1 = __uint_as_float(r[h][2 * j + 1]) * sc;
+              if constexpr (!decltype(all_valid)::value) {
+                if (skip) x0 = x1 = 0.f;  // zero block of the padded 2-d index (TMEM was not written)
+              }
+              __half2 hv = __floats2half2_rn(x0, x1);
+              // the max of the scaled fp32 values (not of their fp16 roundings): it stays meaningful when
+              // cancellation pushes the stored values into fp16 subnormals or zero (scale re-run, redo_check)
+              if (decltype(all_valid)::value || j < nvalid) mx = fmaxf(mx, fmaxf(fabsf(x0), fabsf(x1)));
+              pk[j] = *reinterpret_cast<uint32_t*>(&hv);
+            }
+          };
+          if (nvalid == 16 && !skip)
+            convert(std::true_type{});
+          else
+            convert(std::false_type{});
           if (scat) {
             if (row_ok) {
               const uint64_t nb = (uint64_t)((n0 + c) >> 1);  // a multiple of 16: bits 0..3 are q's
