@@ -47,6 +47,15 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// epilogue staging stores with 32-bit shared addresses (the generic 64-bit stores cost address
+// arithmetic per store)
+__device__ __forceinline__ void sts32(uint32_t addr, uint32_t v) {
+  asm volatile("st.shared.b32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
+
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
 }
@@ -872,36 +881,35 @@ __global__ void __launch_bounds__((kAMode == 1 || kAMode == 4) ? kThreadsGather 
             // row-folded GEMM (f = 2) with a transposed output: tile row p holds output rows 2p + h
             // (h = this 32-column half) for 16 complex columns; staged as C^T [16 n][256 m], one
             // TMA box of 1 KB rows
-            uint32_t* st32 = reinterpret_cast<uint32_t*>(sbuf);
+            const uint32_t sb = smem_u32(sbuf);
 #pragma unroll
-            for (int j = 0; j < 16; ++j) st32[j * (2 * BM) + 2 * row + h] = pk[j];
+            for (int j = 0; j < 16; ++j) sts32(sb + 4u * (j * (2 * BM) + 2 * row + h), pk[j]);
           } else if (epi_stg == 4) {
             // transposed store C[n][m] (layout policy 3): stage the subtile as [32 complex n][128 m]
             // (each warp writes 32 consecutive words per column: no bank conflict), then one TMA box
-            uint32_t* st32 = reinterpret_cast<uint32_t*>(sbuf);
+            const uint32_t sb = smem_u32(sbuf);
             const int q0 = (c & 63) >> 1;  // first complex column of these 32 real columns
 #pragma unroll
-            for (int j = 0; j < 16; ++j) st32[(q0 + j) * BM + row] = pk[j];
+            for (int j = 0; j < 16; ++j) sts32(sb + 4u * ((q0 + j) * BM + row), pk[j]);
           } else if (BN < 64 && epi_stg == 5) {
             // packed narrow rows: 64 / BN output rows (BN fp16 each) share one 128-byte staging row,
             // stored as rows of 128 B (the TMA engine's per-row cost made 32/64-byte rows its limit)
             constexpr int kFo = BN < 64 ? 64 / BN : 1;
             const int prow = row / kFo, part = row % kFo;
-            unsigned char* srow = sbuf + prow * 128;
+            const uint32_t srow = smem_u32(sbuf) + prow * 128;
 #pragma unroll
             for (int q = 0; q < BN / 8; ++q) {
               const int chunk = (part * (BN / 8) + q) ^ (prow & 7);
-              *reinterpret_cast<uint4*>(srow + chunk * 16) = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+              sts128(srow + chunk * 16, pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
             }
           } else {
-            unsigned char* srow = sbuf + row * 128;
+            const uint32_t srow = smem_u32(sbuf) + row * 128;
             const int cb = (c & 63) >> 3;  // first 16-byte chunk of these 32 columns
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
               if ((c & 63) + q * 8 < BN || BN >= 64) {
                 const int chunk = (cb + q) ^ (row & 7);
-                uint4 v = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
-                *reinterpret_cast<uint4*>(srow + chunk * 16) = v;
+                sts128(srow + chunk * 16, pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
               }
             }
           }

@@ -404,15 +404,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             // complex columns (c & 63) / 2 + 8 odd + q of the 32-column subtile, complex row jr
             const int q0 = ((c & 63) >> 1) + 8 * odd;
             if (epi == 4) {
-              uint32_t* st32 = reinterpret_cast<uint32_t*>(sbuf);
+              const uint32_t sb = smem_u32(sbuf);
 #pragma unroll
-              for (int q = 0; q < 8; ++q) st32[(q0 + q) * kRows + jr] = pk[q];
+              for (int q = 0; q < 8; ++q) sts32(sb + 4u * ((q0 + q) * kRows + jr), pk[q]);
             } else {
-              unsigned char* srow = sbuf + jr * 128;
+              const uint32_t srow = smem_u32(sbuf) + jr * 128;
 #pragma unroll
               for (int q = 0; q < 2; ++q) {
                 const int chunk = ((q0 >> 2) + q) ^ (jr & 7);
-                *reinterpret_cast<uint4*>(srow + chunk * 16) = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+                sts128(srow + chunk * 16, pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
               }
             }
           } else {
@@ -425,17 +425,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               pk[j] = *reinterpret_cast<uint32_t*>(&hv);
             }
             if (epi == 4) {
-              uint32_t* st32 = reinterpret_cast<uint32_t*>(sbuf);
+              const uint32_t sb = smem_u32(sbuf);
               const int q0 = (c & 63) >> 1;
 #pragma unroll
-              for (int j = 0; j < 16; ++j) st32[(q0 + j) * BM + row] = pk[j];
+              for (int j = 0; j < 16; ++j) sts32(sb + 4u * ((q0 + j) * BM + row), pk[j]);
             } else {
-              unsigned char* srow = sbuf + row * 128;
+              const uint32_t srow = smem_u32(sbuf) + row * 128;
               const int cb = (c & 63) >> 3;
 #pragma unroll
               for (int q = 0; q < 4; ++q) {
                 const int chunk = (cb + q) ^ (row & 7);
-                *reinterpret_cast<uint4*>(srow + chunk * 16) = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+                sts128(srow + chunk * 16, pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
               }
             }
           }
