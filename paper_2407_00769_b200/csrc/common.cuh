@@ -182,10 +182,12 @@ void launch_gemm_chalf_tc(__half* c, const __half* a, const __half* bp, uint64_t
 int gather_mode_of(const AGather& ag);  // k_gemm_tc.cu: the gathered-A path (plan.cpp cost model)
 // MN-major A (k_gemm_tc2.cu): A stored [M >> ma][K][2^ma] complex-half (2^ma kept rows innermost),
 // bpm = B' [2N][K] (launch_pad_b_mn); no permutation pass.
-bool mn_gemm_supported(uint64_t M, uint32_t K, uint32_t N, int ma, const OutMap* om);
+// Split form (kl, mm > 0): A stored [M >> (ma + mm)][K >> kl][2^mm][2^kl][2^ma] (a run of mm kept
+// modes between the contracted ones; output rows in stored order m_hi, m_mid, m_lo).
+bool mn_gemm_supported(uint64_t M, uint32_t K, uint32_t N, int ma, const OutMap* om, int kl = 0, int mm = 0);
 void launch_gemm_chalf_mn(__half* c, const __half* a, const __half* bpm, uint64_t M, uint32_t K, uint32_t N, int ma,
                           const float* in_max, const float* b_bound, uint32_t* out_max, int* exp_slot,
-                          const OutMap* om, cudaStream_t s);
+                          const OutMap* om, cudaStream_t s, int kl = 0, int mm = 0);
 // Gather-batched tcgen05 GEMM (Fig. 5; see BatchArgs in gemm_tc.cuh): n_out
 // entries of M rows (M % 128 == 0).  Index variant (pad_r == 0): C[b] = A[ia[b]] x B_P[ib[b]].
 // Padded 2-d index (pad_r > 0, n_out = n_a): C_P[a] = A[a] x [B_P[table[a pad_r + r]]]_r, rows of

@@ -266,17 +266,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const int a_row = mp * 2 * kRows + (int)rank * kRows;
         const int b_row = nb * BN + (int)rank * (BN / 2);
         int cm[5] = {0, 0, 0, 0, 0};  // N-d A: row part of the box coordinates (global row)
-        if (nda.nd > 0) nd_coords_rows(nda, m_base + (uint64_t)a_row, cm);
+        if (!kMN && nda.nd > 0) nd_coords_rows(nda, m_base + (uint64_t)a_row, cm);
         for (int kb = 0; kb < num_k; ++kb) {
           mbar_wait(&empty[s], ph ^ 1);
           if (rank == 0) mbar_expect_tx(&full[s], 2 * C::kStageBytes);
           const uint32_t fb = map_rank(&full[s], 0);
           if constexpr (kMN) {
             const uint64_t gr = m_base + (uint64_t)a_row;
-            int cc[3] = {(int)(2 * (gr & ((1ull << mn_ma) - 1))), kb * KB, (int)(gr >> mn_ma)};
-            tma_load_nd_pair(sA + s * C::kABytes, &tmA, fb, 3, cc);
-            cc[0] += 64;
-            tma_load_nd_pair(sA + s * C::kABytes + C::kABytes / 2, &tmA, fb, 3, cc);
+            if (nda.nd == 5) {
+              // split block: (m_lo halves, k_lo, m_mid, k_hi, m_hi)
+              const int kl = nda.kj0[0], mm = nda.mj0[0];
+              const uint64_t r = gr >> mn_ma;
+              const int k0 = kb * KB;
+              int cc[5] = {(int)(2 * (gr & ((1ull << mn_ma) - 1))), k0 & ((1 << kl) - 1), (int)(r & ((1ull << mm) - 1)),
+                           k0 >> kl, (int)(r >> mm)};
+              tma_load_nd_pair(sA + s * C::kABytes, &tmA, fb, 5, cc);
+              cc[0] += 64;
+              tma_load_nd_pair(sA + s * C::kABytes + C::kABytes / 2, &tmA, fb, 5, cc);
+            } else {
+              int cc[3] = {(int)(2 * (gr & ((1ull << mn_ma) - 1))), kb * KB, (int)(gr >> mn_ma)};
+              tma_load_nd_pair(sA + s * C::kABytes, &tmA, fb, 3, cc);
+              cc[0] += 64;
+              tma_load_nd_pair(sA + s * C::kABytes + C::kABytes / 2, &tmA, fb, 3, cc);
+            }
           } else if (nda.nd > 0) {
             int cc[5];
             nd_coords_k(nda, (uint32_t)kb * (KB / 2), cm, cc);

@@ -122,23 +122,42 @@ static int mn_out_kind(const OutMap* om, uint64_t M, uint32_t N, tc2::RowPerm* r
   return kind;
 }
 
-bool mn_gemm_supported(uint64_t M, uint32_t K, uint32_t N, int ma, const OutMap* om) {
+bool mn_gemm_supported(uint64_t M, uint32_t K, uint32_t N, int ma, const OutMap* om, int kl, int mm) {
   if (!tc2_enabled() || ma < 7 || K < 64 || (K & (K - 1)) || N < 64 || (N & (N - 1)) || M % 128 || M >= (1ull << 31))
     return false;
   if (mn_out_kind(om, M, N, nullptr) < 0) return false;
-  return (1ull << ma) <= M;
+  if ((kl > 0) != (mm > 0) || kl < 0 || mm < 0 || (1ull << kl) >= K) return false;
+  return (1ull << (ma + mm)) <= M;
 }
 
 void launch_gemm_chalf_mn(__half* c, const __half* a, const __half* bpm, uint64_t M, uint32_t K, uint32_t N, int ma,
                           const float* in_max, const float* b_bound, uint32_t* out_max, int* exp_slot,
-                          const OutMap* om, cudaStream_t s) {
-  if (!mn_gemm_supported(M, K, N, ma, om)) throw TnError{TN_E_INVALID, "MN-major GEMM: unsupported geometry"};
+                          const OutMap* om, cudaStream_t s, int kl, int mm) {
+  if (!mn_gemm_supported(M, K, N, ma, om, kl, mm)) throw TnError{TN_E_INVALID, "MN-major GEMM: unsupported geometry"};
   tc2::RowPerm rp;
   const bool transposed = mn_out_kind(om, M, N, &rp) == 1;
   const uint32_t N2 = 2 * N;
   const int BN = N2 >= 256 ? 256 : 128;
   CUtensorMap ma_map;
-  {
+  NdArgs nda;
+  memset(&nda, 0, sizeof(nda));
+  if (kl > 0) {
+    // split block: 5-d map (m_lo halves, k_lo, m_mid, k_hi, m_hi), box {64, min(64, 2^kl), 1,
+    // 64 / that, 1}: the same 64 rows of 128 B (local k = k_lo + 2^kl k_hi) as the 3-d box
+    const uint64_t klo = 1ull << kl, khi = K >> kl, mmid = 1ull << mm;
+    cuuint64_t dims[5] = {2ull << ma, klo, mmid, khi, M >> (ma + mm)};
+    cuuint64_t strides[4] = {4ull << ma, (4ull << ma) * klo, (4ull << ma) * klo * mmid, (4ull << ma) * klo * mmid * khi};
+    const cuuint32_t bk = (cuuint32_t)std::min<uint64_t>(64, klo);
+    cuuint32_t box[5] = {64, bk, 1, 64 / bk, 1};
+    cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+    CUresult r = get_encode()(&ma_map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 5, const_cast<__half*>(a), dims, strides, box,
+                              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw TnError{TN_E_CUDA, "cuTensorMapEncodeTiled (split MN-major A) failed"};
+    nda.nd = 5;
+    nda.kj0[0] = (int8_t)kl;
+    nda.mj0[0] = (int8_t)mm;
+  } else {
     cuuint64_t dims[3] = {2ull << ma, K, M >> ma};
     cuuint64_t strides[2] = {4ull << ma, (4ull << ma) * K};
     cuuint32_t box[3] = {64, 64, 1};
@@ -152,8 +171,6 @@ void launch_gemm_chalf_mn(__half* c, const __half* a, const __half* bpm, uint64_
   const CUtensorMap mc = transposed ? make_map_t(c, M, N, 64) : make_map_2d(c, N2, M, 64, 64);
   // (peer stores only for an unpermuted output: a fused swap's member bits are output-row bits)
   const PeerStore ps = make_peer_store(om ? om->peer : nullptr, !rp.on, transposed, M, N2, 64);
-  NdArgs nda;
-  memset(&nda, 0, sizeof(nda));
   const uint32_t num_mp = (uint32_t)(M / 128), num_n = N2 / BN;
   if (BN == 256)
     launch_tc2_t<256, true>(ma_map, mb, mc, num_mp, num_n, (int)K, in_max, b_bound, out_max, exp_slot,

@@ -669,8 +669,28 @@ static Plan* load_plan_fixed(const char* json, size_t len, const tn_config* cfg_
           // only where a pass would be expensive (>= 2^28 elements): the fold keeps the kept modes in
           // stored order, which forgoes the pass's next-use ordering of them for the later steps
           static const int mn_min = getenv("TN_MN_MIN_LOG2") ? atoi(getenv("TN_MN_MIN_LOG2")) : 28;  // tuning knob
-          bool block = ma >= 7 && kl >= 6 && nl >= 6 && (int)kept.size() >= 8 && (int)L.size() >= mn_min;
+          const bool geo = ma >= 7 && kl >= 6 && nl >= 6 && (int)kept.size() >= 8 && (int)L.size() >= mn_min;
+          bool block = geo;
           for (int q = 0; block && q < kl; ++q) block = bs.count(L[L.size() - 1 - ma - q]) > 0;
+          // split block: [.. | R_hi | m_mid | R_lo | m_lo], one kept run inside the contracted modes
+          // (5-d A map).  Opt-in (TN_MN_SPLIT=1): exact, and it cuts C3's modelled pass bytes from
+          // 73.6 to 47.8 GB on one GPU, but the MN-major kernel is slower than pass + plain GEMM on
+          // several of the steps it then takes (C3 steps 20 / 21 / 24: 10.0 / 10.9 / 11.0 vs 7.6 /
+          // 7.3 / 6.0 ms), so the subtask measured 260.9-263.7 vs 249.1-261.6 ms (3 interleaved reps);
+          // the search's cost counts pass bytes only
+          int split_kl = 0, split_mm = 0;
+          static const bool split_on = getenv("TN_MN_SPLIT") && atoi(getenv("TN_MN_SPLIT")) != 0;
+          if (geo && !block && split_on) {
+            int pos = (int)L.size() - 1 - ma, q1 = 0, mm = 0, q2 = 0;
+            while (pos >= 0 && bs.count(L[pos])) ++q1, --pos;
+            while (pos >= 0 && !bs.count(L[pos])) ++mm, --pos;
+            while (pos >= 0 && bs.count(L[pos])) ++q2, --pos;
+            if (q1 >= 1 && mm >= 1 && q1 + q2 == kl) {
+              block = true;
+              split_kl = q1;
+              split_mm = mm;
+            }
+          }
           static const bool mn_off = getenv("TN_NO_MN") != nullptr;  // A/B knob
           // TN_MN_STEPS="i,j,..." (experiment knob): only these step indices may take the fold
           static const char* mn_steps = getenv("TN_MN_STEPS");
@@ -683,6 +703,8 @@ static Plan* load_plan_fixed(const char* json, size_t len, const tn_config* cfg_
               (split_set.empty() || (int)s < p.split_from)) {
             st.mn = true;
             st.mn_ma = ma;
+            st.mn_kl = split_kl;
+            st.mn_mm = split_mm;
           }
         }
         if (!fusable && !st.mn) by_next_use(kept);
@@ -1054,7 +1076,7 @@ std::string report_json(const Plan& p, const std::vector<float>& ms) {
       << ",\"tc\":" << (s.tensor_core ? 1 : 0) << ",\"ga\":" << (s.gather_a ? 1 : 0) << ",\"split\":" << s.split << ",\"swap\":" << (s.swap ? 1 : 0)
       << ",\"quant\":" << (s.quant ? 1 : 0) << ",\"sparse\":" << s.sparse
       << ",\"fuse_quant\":" << (s.fuse_quant ? 1 : 0)
-      << ",\"out_kind\":" << (s.out_identity ? 0 : (s.out_transposed ? 1 : 2)) << ",\"mn\":" << (s.mn ? s.mn_ma : 0)
+      << ",\"out_kind\":" << (s.out_identity ? 0 : (s.out_transposed ? 1 : 2)) << ",\"mn\":" << (s.mn ? s.mn_ma : 0) << ",\"mn_split\":[" << s.mn_kl << "," << s.mn_mm << "]"
       << ",\"fold\":" << s.fold
       << ",\"gmode\":"
       << (s.gather_a && !s.a_m_stride.empty()

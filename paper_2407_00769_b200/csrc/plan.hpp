@@ -58,6 +58,9 @@ struct StemStep {
   // geometry allows (runtime mn_active); perm / perm_axes stay as the fallback
   bool mn = false;
   int mn_ma = 0;
+  // split contraction block [other kept | R_hi | mn_mm kept | R_lo (mn_kl modes) | mn_ma kept]: one
+  // kept run inside the contracted modes (a 5-d A map); 0 = one contiguous block
+  int mn_kl = 0, mn_mm = 0;
   // row folding (plain A, row-major output, 2K x 2 B < 128 B): the tcgen05 GEMM runs on [M/f][f 2K] x
   // blockdiag(B_P x f) -> [M/f][f 2N], the same bytes read as rows of 128 B (the TMA engine's
   // per-row cost made 64-byte rows its limit); B' at b_off, B_P scratch at b_off + b_fold_bytes

@@ -636,7 +636,7 @@ OutMap step_outmap(const StemStep& st, int mshift) {
 bool mn_active(const Plan& p, const StemStep& st) {
   if (!st.mn || p.cfg.dtype != TN_CHALF || !st.tensor_core || st.split || st.sparse) return false;
   const OutMap om = step_outmap(st, 0);
-  return mn_gemm_supported(1ull << st.mlog, 1u << st.klog, 1u << st.nlog, st.mn_ma, &om);
+  return mn_gemm_supported(1ull << st.mlog, 1u << st.klog, 1u << st.nlog, st.mn_ma, &om, st.mn_kl, st.mn_mm);
 }
 
 void prepare_b_sparse(const Plan& p, const StemStep& st, size_t i, unsigned char* W, const Scratch& sc, cudaStream_t s) {
@@ -999,7 +999,7 @@ void run_gemm_once(Plan& p, const StemStep& st, size_t i, const void* src, void*
     } else if (mshift == 0 && mn_active(p, st))
       launch_gemm_chalf_mn(reinterpret_cast<__half*>(dst), reinterpret_cast<const __half*>(src),
                            reinterpret_cast<const __half*>(W + st.b_off), M, K, N, st.mn_ma, in_max, &sc.b_bound[i],
-                           out_max, exp_slot, &om, s);
+                           out_max, exp_slot, &om, s, st.mn_kl, st.mn_mm);
     else if (st.tensor_core)
       launch_gemm_chalf_tc(reinterpret_cast<__half*>(dst), reinterpret_cast<const __half*>(src),
                            reinterpret_cast<const __half*>(W + st.b_off), M, 2 * K, 2 * N, in_max, &sc.b_bound[i],

@@ -294,7 +294,7 @@ def _runs(step):
 @pytest.mark.parametrize("world", [1, 4])
 def test_mn_major_lowering(tnmod, world):
     """Steps folded into the MN-major operand (plan.cpp, StemStep::mn): stored order
-    [kept | contracted | >= 7 kept], K >= 64, N >= 64, >= 2^28 elements; the permutation stays as the
+    [kept | contracted | >= 7 kept] (or the contracted block split by one kept run), K >= 64, N >= 64, >= 2^28 elements; the permutation stays as the
     fallback (perm = 1) but is not counted in n_permutes / perm_bytes."""
     with open(os.path.join(ROOT, "plans", "c3.json")) as f:
         plan = json.load(f)
@@ -305,8 +305,18 @@ def test_mn_major_lowering(tnmod, world):
     for s in mn:
         runs = _runs(s)
         ma = s["mn"]
-        assert ma >= 7 and runs[:ma] == ["m"] * ma and runs[ma:ma + s["k"]] == ["k"] * s["k"]
-        assert set(runs[ma + s["k"]:]) <= {"m"}
+        kl, mm = s["mn_split"]
+        if kl == 0:
+            assert mm == 0
+            assert ma >= 7 and runs[:ma] == ["m"] * ma and runs[ma:ma + s["k"]] == ["k"] * s["k"]
+            assert set(runs[ma + s["k"]:]) <= {"m"}
+        else:
+            # split block [.. | k_hi | m_mid | k_lo | m_lo]: one kept run inside the contracted modes
+            assert ma >= 7 and mm >= 1 and 1 <= kl < s["k"]
+            assert runs[:ma] == ["m"] * ma and runs[ma:ma + kl] == ["k"] * kl
+            assert runs[ma + kl:ma + kl + mm] == ["m"] * mm
+            assert runs[ma + kl + mm:ma + mm + s["k"]] == ["k"] * (s["k"] - kl)
+            assert set(runs[ma + mm + s["k"]:]) <= {"m"}
         assert s["k"] >= 6 and s["n"] >= 6 and len(s["in"]) >= 28 and s["perm"] == 1 and s["ga"] == 0
     # (+1: the final permutation into output order, one GPU)
     assert info["n_permutes"] - sum(1 for s in rep["steps"] if s["perm"] and not s["mn"]) in (0, 1)

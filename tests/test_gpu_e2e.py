@@ -301,17 +301,18 @@ def test_c3_subslice_policies_vs_oracle(tn, policy):
 
 def test_mn_major_steps_vs_oracle(tn):
     """Steps stored [kept | contracted | >= 7 kept] run on the MN-major operand (no permutation pass,
-    k_gemm_tc2.cu): C3 sub-sliced to 2^24 with the fold enabled down to 2^18-element steps, one GPU
+    k_gemm_tc2.cu): C3 sub-sliced to 2^25 with the fold enabled down to 2^18-element steps, one GPU
     and 4 loopback ranks, against the oracle (fp16 bound); also with the row-permuted output
-    (TN_MN_ROWPERM=1) and with the fold off."""
+    (TN_MN_ROWPERM=1), with the split block (TN_MN_SPLIT=1: [.. | k_hi | m_mid | k_lo | m_lo]
+    stored steps on a 5-d A map instead of a pass) and with the fold off."""
     import subprocess
     import sys
     import tempfile
-    sub = MP.sub_slice(_plan("c3"), 24)
+    sub = MP.sub_slice(_plan("c3"), 25)
     ref = contract.contract(load(sub), 0)
     got = {}
     for mode, env in (("mn", {"TN_MN_MIN_LOG2": "18"}), ("mn_rowperm", {"TN_MN_MIN_LOG2": "18", "TN_MN_ROWPERM": "1"}),
-                      ("pass", {"TN_NO_MN": "1"})):
+                      ("mn_split", {"TN_MN_MIN_LOG2": "18", "TN_MN_SPLIT": "1"}), ("pass", {"TN_NO_MN": "1"})):
         with tempfile.NamedTemporaryFile(suffix=".npz", delete=False) as f:
             path = f.name
         r = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "mn_worker.py"), path],
@@ -321,6 +322,7 @@ def test_mn_major_steps_vs_oracle(tn):
     assert len(got["mn"]["mn_one"]) >= 1 and len(got["mn"]["mn_four"]) >= 1
     assert len(got["mn_rowperm"]["mn_one"]) >= 1
     assert len(got["pass"]["mn_one"]) == 0
+    assert len(got["mn_split"]["split_one"]) >= 1 and len(got["mn"]["split_one"]) == 0
     for mode in got:
         for key in ("one", "four"):
             assert metrics.rel_l2(got[mode][key], ref) <= 2e-2, (mode, key)
